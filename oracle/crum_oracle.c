@@ -1,0 +1,636 @@
+/*
+ * crum_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU model of CRUM's shadow-page
+ * synchronisation (arXiv 1808.00117, Alg. 1 at PAPER.md:403-431, sec. 3.2 at
+ * PAPER.md:433-444, sec. 3.4 drain/restart at PAPER.md:543-565), written to
+ * the readings listed in DESIGN.md sec. "Readings".
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this code.  It shares no source, header,
+ * table or constant with the CUDA path under paper_1808_00117_b200/.
+ *
+ * Everything is scalar C11: byte loops, memcmp/memcpy, a bit-at-a-time CRC-32
+ * and XXH3-64 computed stripe by stripe in the library's documented order.
+ * No blocking, fusion or reordering beyond what the definitions state.
+ *
+ * Pins (tests/test_oracle_*.py):
+ *   orc_xxh3_64      -- python-xxhash xxh3_64_intdigest (library routine)
+ *   orc_crc32        -- zlib.crc32 (library routine)
+ *   orc_detect       -- brute-force Python bytes comparison, exhaustive flips
+ *   sync / gather / restore -- invariants restore(ckpt(x)) == x, sync;sync==0,
+ *                        dirty set == written set, numpy-assembled image bytes.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* Status codes: the values are the ABI contract of include/crum.h (restated
+ * here, not included, so the oracle stays independent of the product). */
+enum {
+    ORC_OK = 0,
+    ORC_E_INVAL = -1,
+    ORC_E_OVERLAP = -2,
+    ORC_E_NOREGION = -3,
+    ORC_E_RANGE = -4,
+    ORC_E_NOMEM = -5,
+    ORC_E_CAPACITY = -6,
+    ORC_E_CORRUPT = -7,
+    ORC_E_MISMATCH = -8,
+};
+
+enum { ORC_MODE_COMPARE = 0, ORC_MODE_HASH = 1 };
+enum { ORC_FULL = 1u, ORC_VERIFY = 2u };
+enum { ORC_IMG_FULL = 1u, ORC_IMG_HAS_HASHES = 2u };
+
+#define ORC_MIN_PAGE 4096ull
+#define ORC_MAX_PAGE (2ull << 20)
+#define ORC_MAX_TOTAL_PAGES 0x7fffffffull
+
+typedef struct {
+    uint64_t scanned_pages, scanned_bytes;
+    uint64_t dirty_pages, dirty_bytes, dirty_runs;
+    uint64_t image_bytes;
+} orc_report;
+
+typedef struct {
+    uint32_t id;
+    uint32_t mode;
+    uint8_t *cur;        /* the registered bytes ("real" pages, Q5) */
+    uint64_t bytes;      /* B_r */
+    uint64_t page_size;  /* P_r */
+    uint64_t n_pages;    /* n_r = ceil(B_r / P_r) */
+    uint8_t *mirror;     /* compare mode: last committed bytes (B_r) */
+    uint64_t *table;     /* hash mode: last committed XXH3 per page */
+    uint8_t *force;      /* per-page force-dirty bit (Q3) */
+} orc_region;
+
+typedef struct {
+    orc_region *r;       /* ascending id order */
+    uint32_t n;
+    uint32_t next_id;
+} orc_ctx;
+
+/* ------------------------------------------------------------------ */
+/* Little-endian helpers (byte by byte, host-endianness independent).  */
+/* ------------------------------------------------------------------ */
+static uint64_t rd64(const uint8_t *p)
+{
+    uint64_t v = 0;
+    for (int i = 7; i >= 0; --i) v = (v << 8) | p[i];
+    return v;
+}
+static uint32_t rd32(const uint8_t *p)
+{
+    return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+static void wr64(uint8_t *p, uint64_t v)
+{
+    for (int i = 0; i < 8; ++i) p[i] = (uint8_t)(v >> (8 * i));
+}
+static void wr32(uint8_t *p, uint32_t v)
+{
+    for (int i = 0; i < 4; ++i) p[i] = (uint8_t)(v >> (8 * i));
+}
+
+/* ------------------------------------------------------------------ */
+/* CRC-32 (zlib polynomial, reflected 0xEDB88320, init/final ~0),      */
+/* one bit at a time -- the textbook definition.                       */
+/* ------------------------------------------------------------------ */
+uint32_t orc_crc32(const uint8_t *p, uint64_t n)
+{
+    uint32_t c = 0xffffffffu;
+    for (uint64_t i = 0; i < n; ++i) {
+        c ^= p[i];
+        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xedb88320u & (0u - (c & 1u)));
+    }
+    return c ^ 0xffffffffu;
+}
+
+/* ------------------------------------------------------------------ */
+/* XXH3-64, seed 0, default secret, long-input path (len > 240).       */
+/* Reading Q8: the per-page hash is XXH3_64bits of the     */
+/* zero-padded P-byte slot.  Steps follow xxhash 0.8's documented long */
+/* loop: stripes of 64 B, blocks of 16 stripes, scramble after each    */
+/* full block, a partial last block, the last stripe at secret offset  */
+/* 121, merge at secret offset 11, avalanche.                          */
+/* ------------------------------------------------------------------ */
+static const uint8_t orc_secret[192] = {
+    0xb8, 0xfe, 0x6c, 0x39, 0x23, 0xa4, 0x4b, 0xbe, 0x7c, 0x01, 0x81, 0x2c, 0xf7, 0x21, 0xad, 0x1c,
+    0xde, 0xd4, 0x6d, 0xe9, 0x83, 0x90, 0x97, 0xdb, 0x72, 0x40, 0xa4, 0xa4, 0xb7, 0xb3, 0x67, 0x1f,
+    0xcb, 0x79, 0xe6, 0x4e, 0xcc, 0xc0, 0xe5, 0x78, 0x82, 0x5a, 0xd0, 0x7d, 0xcc, 0xff, 0x72, 0x21,
+    0xb8, 0x08, 0x46, 0x74, 0xf7, 0x43, 0x24, 0x8e, 0xe0, 0x35, 0x90, 0xe6, 0x81, 0x3a, 0x26, 0x4c,
+    0x3c, 0x28, 0x52, 0xbb, 0x91, 0xc3, 0x00, 0xcb, 0x88, 0xd0, 0x65, 0x8b, 0x1b, 0x53, 0x2e, 0xa3,
+    0x71, 0x64, 0x48, 0x97, 0xa2, 0x0d, 0xf9, 0x4e, 0x38, 0x19, 0xef, 0x46, 0xa9, 0xde, 0xac, 0xd8,
+    0xa8, 0xfa, 0x76, 0x3f, 0xe3, 0x9c, 0x34, 0x3f, 0xf9, 0xdc, 0xbb, 0xc7, 0xc7, 0x0b, 0x4f, 0x1d,
+    0x8a, 0x51, 0xe0, 0x4b, 0xcd, 0xb4, 0x59, 0x31, 0xc8, 0x9f, 0x7e, 0xc9, 0xd9, 0x78, 0x73, 0x64,
+    0xea, 0xc5, 0xac, 0x83, 0x34, 0xd3, 0xeb, 0xc3, 0xc5, 0x81, 0xa0, 0xff, 0xfa, 0x13, 0x63, 0xeb,
+    0x17, 0x0d, 0xdd, 0x51, 0xb7, 0xf0, 0xda, 0x49, 0xd3, 0x16, 0x55, 0x26, 0x29, 0xd4, 0x68, 0x9e,
+    0x2b, 0x16, 0xbe, 0x58, 0x7d, 0x47, 0xa1, 0xfc, 0x8f, 0xf8, 0xb8, 0xd1, 0x7a, 0xd0, 0x31, 0xce,
+    0x45, 0xcb, 0x3a, 0x8f, 0x95, 0x16, 0x04, 0x28, 0xaf, 0xd7, 0xfb, 0xca, 0xbb, 0x4b, 0x40, 0x7e,
+};
+
+#define ORC_P32_1 0x9E3779B1ull
+#define ORC_P32_2 0x85EBCA77ull
+#define ORC_P32_3 0xC2B2AE3Dull
+#define ORC_P64_1 0x9E3779B185EBCA87ull
+#define ORC_P64_2 0xC2B2AE3D27D4EB4Full
+#define ORC_P64_3 0x165667B19E3779F9ull
+#define ORC_P64_4 0x85EBCA77C2B2AE63ull
+#define ORC_P64_5 0x27D4EB2F165667C5ull
+#define ORC_PMX1 0x165667919E3779F9ull
+
+/* One 64-byte stripe into the 8 accumulators, secret at byte offset `so`. */
+static void orc_accumulate_stripe(uint64_t acc[8], const uint8_t *in, uint64_t so)
+{
+    for (int l = 0; l < 8; ++l) {
+        uint64_t v = rd64(in + 8 * l);
+        uint64_t k = v ^ rd64(orc_secret + so + 8 * l);
+        acc[l ^ 1] += v;
+        acc[l] += (k & 0xffffffffull) * (k >> 32);
+    }
+}
+
+static void orc_scramble(uint64_t acc[8])
+{
+    for (int l = 0; l < 8; ++l) {
+        uint64_t a = acc[l];
+        a ^= a >> 47;
+        a ^= rd64(orc_secret + 128 + 8 * l);
+        a *= ORC_P32_1;
+        acc[l] = a;
+    }
+}
+
+/* 64x64 -> 128 multiply folded (lo ^ hi), from 32-bit halves. */
+static uint64_t orc_mul128_fold64(uint64_t a, uint64_t b)
+{
+    uint64_t a0 = a & 0xffffffffull, a1 = a >> 32;
+    uint64_t b0 = b & 0xffffffffull, b1 = b >> 32;
+    uint64_t p00 = a0 * b0, p01 = a0 * b1, p10 = a1 * b0, p11 = a1 * b1;
+    uint64_t mid = (p00 >> 32) + (p10 & 0xffffffffull) + p01;
+    uint64_t lo = (mid << 32) | (p00 & 0xffffffffull);
+    uint64_t hi = p11 + (p10 >> 32) + (mid >> 32);
+    return lo ^ hi;
+}
+
+/* Returns 0 for len <= 240 (outside the oracle's contract; all slots are
+ * >= 4096 bytes). */
+uint64_t orc_xxh3_64(const uint8_t *in, uint64_t len)
+{
+    if (len <= 240) return 0;
+    uint64_t acc[8] = {ORC_P32_3, ORC_P64_1, ORC_P64_2, ORC_P64_3,
+                       ORC_P64_4, ORC_P32_2, ORC_P64_5, ORC_P32_1};
+    const uint64_t stripes_per_block = (192 - 64) / 8; /* 16 */
+    const uint64_t block_len = 64 * stripes_per_block; /* 1024 */
+    const uint64_t nb = (len - 1) / block_len;
+    for (uint64_t b = 0; b < nb; ++b) {
+        for (uint64_t s = 0; s < stripes_per_block; ++s)
+            orc_accumulate_stripe(acc, in + b * block_len + 64 * s, 8 * s);
+        orc_scramble(acc);
+    }
+    const uint64_t last_stripes = ((len - 1) - block_len * nb) / 64;
+    for (uint64_t s = 0; s < last_stripes; ++s)
+        orc_accumulate_stripe(acc, in + nb * block_len + 64 * s, 8 * s);
+    orc_accumulate_stripe(acc, in + len - 64, 192 - 64 - 7);
+    uint64_t r = len * ORC_P64_1;
+    for (int i = 0; i < 4; ++i)
+        r += orc_mul128_fold64(acc[2 * i] ^ rd64(orc_secret + 11 + 16 * i),
+                               acc[2 * i + 1] ^ rd64(orc_secret + 11 + 16 * i + 8));
+    r ^= r >> 37;
+    r *= ORC_PMX1;
+    r ^= r >> 32;
+    return r;
+}
+
+/* ------------------------------------------------------------------ */
+/* Region bookkeeping.                                                 */
+/* ------------------------------------------------------------------ */
+static uint64_t page_len(const orc_region *g, uint64_t i)
+{
+    uint64_t off = i * g->page_size;
+    uint64_t rest = g->bytes - off;
+    return rest < g->page_size ? rest : g->page_size;
+}
+
+/* H(r,i): XXH3 of the page's logical bytes followed by zero padding to P. */
+static uint64_t page_hash(const orc_region *g, uint64_t i)
+{
+    uint64_t len = page_len(g, i);
+    if (len == g->page_size) return orc_xxh3_64(g->cur + i * g->page_size, len);
+    uint8_t *slot = (uint8_t *)calloc(1, g->page_size);
+    memcpy(slot, g->cur + i * g->page_size, len);
+    uint64_t h = orc_xxh3_64(slot, g->page_size);
+    free(slot);
+    return h;
+}
+
+static orc_region *find(orc_ctx *c, uint32_t id)
+{
+    for (uint32_t k = 0; k < c->n; ++k)
+        if (c->r[k].id == id) return &c->r[k];
+    return NULL;
+}
+
+static uint64_t total_pages(const orc_ctx *c)
+{
+    uint64_t n = 0;
+    for (uint32_t k = 0; k < c->n; ++k) n += c->r[k].n_pages;
+    return n;
+}
+
+orc_ctx *orc_create(void)
+{
+    orc_ctx *c = (orc_ctx *)calloc(1, sizeof(orc_ctx));
+    if (c) c->next_id = 1;
+    return c;
+}
+
+static void free_region(orc_region *g)
+{
+    free(g->mirror);
+    free(g->table);
+    free(g->force);
+}
+
+void orc_destroy(orc_ctx *c)
+{
+    if (!c) return;
+    for (uint32_t k = 0; k < c->n; ++k) free_region(&c->r[k]);
+    free(c->r);
+    free(c);
+}
+
+/* Alg. 1 "CUDA Create UVM region" + "all the pages in
+ * the regions are marked as dirty": force[] = 1. */
+int orc_register_region(orc_ctx *c, uint8_t *ptr, uint64_t bytes, uint64_t page_size,
+                        uint32_t mode, uint32_t *id_out)
+{
+    if (!c || !ptr || !id_out || bytes == 0) return ORC_E_INVAL;
+    if (page_size < ORC_MIN_PAGE || page_size > ORC_MAX_PAGE || (page_size & (page_size - 1)))
+        return ORC_E_INVAL;
+    if (((uintptr_t)ptr) % 16 != 0) return ORC_E_INVAL;
+    if (mode != ORC_MODE_COMPARE && mode != ORC_MODE_HASH) return ORC_E_INVAL;
+    uint64_t n = bytes / page_size + (bytes % page_size != 0);
+    if (n > 0xffffffffull) return ORC_E_INVAL;
+    if (total_pages(c) + n > ORC_MAX_TOTAL_PAGES) return ORC_E_INVAL;
+    uintptr_t lo = (uintptr_t)ptr, hi = lo + bytes;
+    for (uint32_t k = 0; k < c->n; ++k) {
+        uintptr_t a = (uintptr_t)c->r[k].cur, b = a + c->r[k].bytes;
+        if (lo < b && a < hi) return ORC_E_OVERLAP;
+    }
+    orc_region g;
+    memset(&g, 0, sizeof g);
+    g.mode = mode;
+    g.cur = ptr;
+    g.bytes = bytes;
+    g.page_size = page_size;
+    g.n_pages = n;
+    g.force = (uint8_t *)malloc(n);
+    if (mode == ORC_MODE_COMPARE) g.mirror = (uint8_t *)calloc(1, bytes);
+    else g.table = (uint64_t *)calloc(n, sizeof(uint64_t));
+    orc_region *nr = (orc_region *)realloc(c->r, (c->n + 1) * sizeof(orc_region));
+    if (!g.force || (!g.mirror && !g.table) || !nr) {
+        free_region(&g);
+        if (nr) c->r = nr;
+        return ORC_E_NOMEM;
+    }
+    c->r = nr;
+    memset(g.force, 1, n);
+    g.id = c->next_id++;
+    c->r[c->n++] = g;
+    *id_out = g.id;
+    return ORC_OK;
+}
+
+int orc_unregister_region(orc_ctx *c, uint32_t id)
+{
+    if (!c) return ORC_E_INVAL;
+    for (uint32_t k = 0; k < c->n; ++k) {
+        if (c->r[k].id != id) continue;
+        free_region(&c->r[k]);
+        memmove(&c->r[k], &c->r[k + 1], (c->n - k - 1) * sizeof(orc_region));
+        c->n--;
+        return ORC_OK;
+    }
+    return ORC_E_NOREGION;
+}
+
+/* MarkPageAsDirty (Alg. 1) as an explicit call: every page
+ * overlapping [off, off+len) gets its force bit. */
+int orc_mark_dirty(orc_ctx *c, uint32_t id, uint64_t off, uint64_t len)
+{
+    if (!c) return ORC_E_INVAL;
+    orc_region *g = find(c, id);
+    if (!g) return ORC_E_NOREGION;
+    if (off > g->bytes || len > g->bytes - off) return ORC_E_RANGE;
+    if (len == 0) return ORC_OK;
+    for (uint64_t i = off / g->page_size; i <= (off + len - 1) / g->page_size; ++i) g->force[i] = 1;
+    return ORC_OK;
+}
+
+/* Detect (pure): D_r = { i : force[i] or content changed since commit }.
+ * Reading Q1: "dirty" = bytes differ from the last committed snapshot
+ * (compare: memcmp over the logical length; hash: H(r,i) != table[i]). */
+static int page_dirty(const orc_region *g, uint64_t i)
+{
+    if (g->force[i]) return 1;
+    if (g->mode == ORC_MODE_COMPARE) {
+        uint64_t off = i * g->page_size;
+        return memcmp(g->cur + off, g->mirror + off, page_len(g, i)) != 0;
+    }
+    return page_hash(g, i) != g->table[i];
+}
+
+int orc_detect(orc_ctx *c, uint32_t id, uint8_t *flags_out)
+{
+    if (!c || !flags_out) return ORC_E_INVAL;
+    orc_region *g = find(c, id);
+    if (!g) return ORC_E_NOREGION;
+    for (uint64_t i = 0; i < g->n_pages; ++i) flags_out[i] = (uint8_t)page_dirty(g, i);
+    return ORC_OK;
+}
+
+/* Commit (ClearDirtyPages): snapshot <- current, force <- 0. */
+static void commit_page(orc_region *g, uint64_t i)
+{
+    if (g->mode == ORC_MODE_COMPARE) {
+        uint64_t off = i * g->page_size;
+        memcpy(g->mirror + off, g->cur + off, page_len(g, i));
+    } else {
+        g->table[i] = page_hash(g, i);
+    }
+    g->force[i] = 0;
+}
+
+/* Alg. 1 "CUDA call": for r ascending, detect D_r and
+ * commit all of it; return sum |D_r|. */
+int orc_sync_shadow(orc_ctx *c, uint64_t *n_out)
+{
+    if (!c) return ORC_E_INVAL;
+    uint64_t total = 0;
+    for (uint32_t k = 0; k < c->n; ++k) {
+        orc_region *g = &c->r[k];
+        for (uint64_t i = 0; i < g->n_pages; ++i) {
+            if (page_dirty(g, i)) {
+                commit_page(g, i);
+                total++;
+            }
+        }
+    }
+    if (n_out) *n_out = total;
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Image format v1 (reading Q10).            */
+/* ------------------------------------------------------------------ */
+static uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+static uint64_t meta_bytes_for(uint64_t R, uint64_t K, int has_hashes)
+{
+    return 64 + 48 * R + round_up(4 * K, 8) + (has_hashes ? 8 * K : 0);
+}
+
+static int any_hash_region(const orc_ctx *c)
+{
+    for (uint32_t k = 0; k < c->n; ++k)
+        if (c->r[k].mode == ORC_MODE_HASH) return 1;
+    return 0;
+}
+
+/* Worst-case image size when at most max_dirty pages are listed. */
+int orc_image_required_bytes(orc_ctx *c, uint64_t max_dirty, uint64_t *out)
+{
+    if (!c || !out) return ORC_E_INVAL;
+    uint64_t N = total_pages(c), K = max_dirty < N ? max_dirty : N;
+    uint64_t payload = 0, maxp = 0;
+    for (uint32_t k = 0; k < c->n; ++k) {
+        payload += c->r[k].n_pages * c->r[k].page_size;
+        if (c->r[k].page_size > maxp) maxp = c->r[k].page_size;
+    }
+    if (K < N && K * maxp < payload) payload = K * maxp;
+    *out = round_up(meta_bytes_for(c->n, K, any_hash_region(c)), 4096) + payload;
+    return ORC_OK;
+}
+
+/* Checkpoint drain as an incremental gather (sec. 3.4, PAPER.md:547-551;
+ * readings Q5, Q12): list D_r (or every page under FULL) for r ascending,
+ * assemble the v1 image, then commit every listed page.  On CAPACITY nothing
+ * changes and report->image_bytes holds the required size. */
+int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap,
+                          orc_report *rep)
+{
+    if (!c || !img || (flags & ~ORC_FULL)) return ORC_E_INVAL;
+    const uint32_t R = c->n;
+    uint64_t N = total_pages(c);
+    /* Step 1: the listed pages (global order: region table order, page index). */
+    uint8_t **listed = (uint8_t **)calloc(R ? R : 1, sizeof(uint8_t *));
+    uint64_t K = 0, payload = 0, dirty_bytes = 0, runs = 0, scanned_bytes = 0;
+    for (uint32_t k = 0; k < R; ++k) {
+        orc_region *g = &c->r[k];
+        listed[k] = (uint8_t *)calloc(g->n_pages, 1);
+        scanned_bytes += g->bytes;
+        for (uint64_t i = 0; i < g->n_pages; ++i) {
+            listed[k][i] = (flags & ORC_FULL) ? 1 : (uint8_t)page_dirty(g, i);
+            if (!listed[k][i]) continue;
+            K++;
+            payload += g->page_size;
+            dirty_bytes += page_len(g, i);
+            if (i == 0 || !listed[k][i - 1]) runs++;
+        }
+    }
+    const int has_hashes = any_hash_region(c);
+    const uint64_t meta = meta_bytes_for(R, K, has_hashes);
+    const uint64_t poff = round_up(meta, 4096);
+    const uint64_t total = poff + payload;
+    if (rep) {
+        rep->scanned_pages = N;
+        rep->scanned_bytes = scanned_bytes;
+        rep->dirty_pages = K;
+        rep->dirty_bytes = dirty_bytes;
+        rep->dirty_runs = runs;
+        rep->image_bytes = total;
+    }
+    if (cap < total) {
+        for (uint32_t k = 0; k < R; ++k) free(listed[k]);
+        free(listed);
+        return ORC_E_CAPACITY;
+    }
+    /* Step 2: assemble. */
+    memset(img, 0, total);
+    memcpy(img, "CRUM", 4);
+    wr32(img + 4, 1);
+    wr32(img + 8, ((flags & ORC_FULL) ? ORC_IMG_FULL : 0) | (has_hashes ? ORC_IMG_HAS_HASHES : 0));
+    wr32(img + 12, R);
+    wr64(img + 16, K);
+    wr64(img + 24, meta);
+    wr64(img + 32, poff);
+    wr64(img + 40, payload);
+    uint8_t *tab = img + 64;
+    uint8_t *ids = tab + 48 * (uint64_t)R;
+    uint8_t *hashes = ids + round_up(4 * K, 8);
+    uint64_t slot = 0, pbyte = 0;
+    for (uint32_t k = 0; k < R; ++k) {
+        orc_region *g = &c->r[k];
+        uint64_t nd = 0, first = slot;
+        for (uint64_t i = 0; i < g->n_pages; ++i) {
+            if (!listed[k][i]) continue;
+            wr32(ids + 4 * slot, (uint32_t)i);
+            if (has_hashes) wr64(hashes + 8 * slot, g->mode == ORC_MODE_HASH ? page_hash(g, i) : 0);
+            memcpy(img + poff + pbyte, g->cur + i * g->page_size, page_len(g, i));
+            pbyte += g->page_size;
+            slot++;
+            nd++;
+        }
+        uint8_t *e = tab + 48 * (uint64_t)k;
+        wr32(e + 0, g->id);
+        wr32(e + 4, g->mode);
+        wr64(e + 8, g->bytes);
+        wr64(e + 16, g->page_size);
+        wr64(e + 24, g->n_pages);
+        wr64(e + 32, nd);
+        wr64(e + 40, first);
+    }
+    wr32(img + 48, orc_crc32(img + 64, meta - 64));
+    wr32(img + 60, orc_crc32(img, 60));
+    /* Step 3: commit every listed page. */
+    for (uint32_t k = 0; k < R; ++k) {
+        for (uint64_t i = 0; i < c->r[k].n_pages; ++i)
+            if (listed[k][i]) commit_page(&c->r[k], i);
+        free(listed[k]);
+    }
+    free(listed);
+    return ORC_OK;
+}
+
+/* Restart data movement (sec. 3.4; reading Q11): validate
+ * everything first, then write each listed page's logical bytes back and
+ * commit it (mirror <- slot / table <- listed hash, force <- 0). */
+int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t flags,
+                        orc_report *rep)
+{
+    if (!c || !img || (flags & ~ORC_VERIFY)) return ORC_E_INVAL;
+    if (len < 64 || memcmp(img, "CRUM", 4) != 0) return ORC_E_CORRUPT;
+    if (orc_crc32(img, 60) != rd32(img + 60)) return ORC_E_CORRUPT;
+    const uint32_t version = rd32(img + 4), iflags = rd32(img + 8), R = rd32(img + 12);
+    const uint64_t K = rd64(img + 16), meta = rd64(img + 24), poff = rd64(img + 32),
+                   payload = rd64(img + 40);
+    if (version != 1 || (iflags & ~3u) != 0 || rd64(img + 52) != 0) return ORC_E_CORRUPT;
+    const int has_hashes = (iflags & ORC_IMG_HAS_HASHES) != 0;
+    if (K > ORC_MAX_TOTAL_PAGES || R > 0x7fffffffu) return ORC_E_CORRUPT;
+    if (meta != meta_bytes_for(R, K, has_hashes) || poff != round_up(meta, 4096)) return ORC_E_CORRUPT;
+    if (len < poff || len - poff < payload) return ORC_E_CORRUPT;
+    if (orc_crc32(img + 64, meta - 64) != rd32(img + 48)) return ORC_E_CORRUPT;
+    const uint8_t *tab = img + 64;
+    const uint8_t *ids = tab + 48 * (uint64_t)R;
+    const uint8_t *hashes = ids + round_up(4 * K, 8);
+    /* Structural consistency of the table, ids and hash list. */
+    uint64_t sum = 0, pay = 0;
+    int any_hash = 0;
+    for (uint32_t k = 0; k < R; ++k) {
+        const uint8_t *e = tab + 48 * (uint64_t)k;
+        uint32_t mode = rd32(e + 4);
+        uint64_t bytes = rd64(e + 8), ps = rd64(e + 16), np = rd64(e + 24), nd = rd64(e + 32),
+                 first = rd64(e + 40);
+        if (mode > 1 || ps < ORC_MIN_PAGE || ps > ORC_MAX_PAGE || (ps & (ps - 1)) || bytes == 0)
+            return ORC_E_CORRUPT;
+        if (np != bytes / ps + (bytes % ps != 0) || nd > np || first != sum) return ORC_E_CORRUPT;
+        if ((iflags & ORC_IMG_FULL) && nd != np) return ORC_E_CORRUPT;
+        if (mode == ORC_MODE_HASH) any_hash = 1;
+        for (uint64_t j = 0; j < nd; ++j) {
+            if (first + j >= K) return ORC_E_CORRUPT;
+            uint32_t id = rd32(ids + 4 * (first + j));
+            if (id >= np) return ORC_E_CORRUPT;
+            if (j > 0 && id <= rd32(ids + 4 * (first + j - 1))) return ORC_E_CORRUPT;
+            if (has_hashes && mode == ORC_MODE_COMPARE && rd64(hashes + 8 * (first + j)) != 0)
+                return ORC_E_CORRUPT;
+        }
+        sum += nd;
+        pay += nd * ps;
+    }
+    if (sum != K || pay != payload || any_hash != has_hashes) return ORC_E_CORRUPT;
+    /* The table must describe the live registered set (reading Q11). */
+    if (R != c->n) return ORC_E_MISMATCH;
+    for (uint32_t k = 0; k < R; ++k) {
+        const uint8_t *e = tab + 48 * (uint64_t)k;
+        const orc_region *g = &c->r[k];
+        if (rd32(e) != g->id || rd32(e + 4) != g->mode || rd64(e + 8) != g->bytes ||
+            rd64(e + 16) != g->page_size || rd64(e + 24) != g->n_pages)
+            return ORC_E_MISMATCH;
+    }
+    /* CRUM_VERIFY: recompute the hash of every hash-mode slot. */
+    if (flags & ORC_VERIFY) {
+        uint64_t pbyte = 0;
+        for (uint32_t k = 0; k < R; ++k) {
+            const orc_region *g = &c->r[k];
+            uint64_t first = rd64(tab + 48 * (uint64_t)k + 40), nd = rd64(tab + 48 * (uint64_t)k + 32);
+            for (uint64_t j = 0; j < nd; ++j) {
+                if (g->mode == ORC_MODE_HASH &&
+                    orc_xxh3_64(img + poff + pbyte, g->page_size) != rd64(hashes + 8 * (first + j)))
+                    return ORC_E_CORRUPT;
+                pbyte += g->page_size;
+            }
+        }
+    }
+    /* Apply. */
+    uint64_t pbyte = 0, dirty_bytes = 0, runs = 0, scanned = 0;
+    for (uint32_t k = 0; k < R; ++k) {
+        orc_region *g = &c->r[k];
+        uint64_t first = rd64(tab + 48 * (uint64_t)k + 40), nd = rd64(tab + 48 * (uint64_t)k + 32);
+        scanned += g->bytes;
+        for (uint64_t j = 0; j < nd; ++j) {
+            uint64_t i = rd32(ids + 4 * (first + j));
+            uint64_t l = page_len(g, i);
+            memcpy(g->cur + i * g->page_size, img + poff + pbyte, l);
+            if (g->mode == ORC_MODE_COMPARE) memcpy(g->mirror + i * g->page_size, img + poff + pbyte, l);
+            else g->table[i] = rd64(hashes + 8 * (first + j));
+            g->force[i] = 0;
+            dirty_bytes += l;
+            if (j == 0 || rd32(ids + 4 * (first + j - 1)) + 1 != i) runs++;
+            pbyte += g->page_size;
+        }
+    }
+    if (rep) {
+        rep->scanned_pages = total_pages(c);
+        rep->scanned_bytes = scanned;
+        rep->dirty_pages = K;
+        rep->dirty_bytes = dirty_bytes;
+        rep->dirty_runs = runs;
+        rep->image_bytes = poff + payload;
+    }
+    return ORC_OK;
+}
+
+/* Introspection for tests: copies of the force bits, hash table, mirror. */
+int orc_get_force(orc_ctx *c, uint32_t id, uint8_t *out)
+{
+    orc_region *g = c ? find(c, id) : NULL;
+    if (!g) return ORC_E_NOREGION;
+    memcpy(out, g->force, g->n_pages);
+    return ORC_OK;
+}
+int orc_get_hashes(orc_ctx *c, uint32_t id, uint64_t *out)
+{
+    orc_region *g = c ? find(c, id) : NULL;
+    if (!g) return ORC_E_NOREGION;
+    if (g->mode != ORC_MODE_HASH) return ORC_E_INVAL;
+    memcpy(out, g->table, g->n_pages * sizeof(uint64_t));
+    return ORC_OK;
+}
+int orc_get_mirror(orc_ctx *c, uint32_t id, uint8_t *out)
+{
+    orc_region *g = c ? find(c, id) : NULL;
+    if (!g) return ORC_E_NOREGION;
+    if (g->mode != ORC_MODE_COMPARE) return ORC_E_INVAL;
+    memcpy(out, g->mirror, g->bytes);
+    return ORC_OK;
+}
+int orc_page_hash(orc_ctx *c, uint32_t id, uint64_t i, uint64_t *out)
+{
+    orc_region *g = c ? find(c, id) : NULL;
+    if (!g) return ORC_E_NOREGION;
+    if (i >= g->n_pages) return ORC_E_RANGE;
+    *out = page_hash(g, i);
+    return ORC_OK;
+}

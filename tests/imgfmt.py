@@ -1,0 +1,72 @@
+"""Independent image-format v1 builder/parser for tests (DESIGN.md "Image
+format"), written with library routines only: struct, zlib.crc32 and
+xxhash.xxh3_64_intdigest.  It pins the oracle's image assembly and is reused by
+the GPU parity tests to decode images.  Imports neither oracle/ nor the
+product package.
+"""
+from __future__ import annotations
+
+import struct
+import zlib
+
+import numpy as np
+import xxhash
+
+HDR = struct.Struct("<4sIIIQQQQI8sI")  # 64 bytes
+ENTRY = struct.Struct("<IIQQQQQ")      # 48 bytes
+assert HDR.size == 64 and ENTRY.size == 48
+
+
+def round_up(x, a):
+    return (x + a - 1) // a * a
+
+
+def slot_bytes(cur: np.ndarray, page_size: int, i: int) -> bytes:
+    seg = cur[i * page_size:(i + 1) * page_size].tobytes()
+    return seg + b"\0" * (page_size - len(seg))
+
+
+def build_image(regions, listed, full=False) -> bytes:
+    """regions: list of dicts {id, mode, cur (np.uint8 array), page_size};
+    listed: list (same order) of ascending page-index lists."""
+    R = len(regions)
+    K = sum(len(l) for l in listed)
+    has_hashes = any(r["mode"] == 1 for r in regions)
+    meta = 64 + 48 * R + round_up(4 * K, 8) + (8 * K if has_hashes else 0)
+    poff = round_up(meta, 4096)
+    table, ids, hashes, payload = b"", b"", b"", []
+    first = 0
+    for r, l in zip(regions, listed):
+        cur, P = r["cur"], r["page_size"]
+        n = -(-cur.nbytes // P)
+        table += ENTRY.pack(r["id"], r["mode"], cur.nbytes, P, n, len(l), first)
+        first += len(l)
+        for i in l:
+            s = slot_bytes(cur, P, i)
+            ids += struct.pack("<I", i)
+            if has_hashes:
+                hashes += struct.pack("<Q", xxhash.xxh3_64_intdigest(s) if r["mode"] == 1 else 0)
+            payload.append(s)
+    ids += b"\0" * (round_up(4 * K, 8) - 4 * K)
+    body = table + ids + hashes
+    assert 64 + len(body) == meta
+    flags = (1 if full else 0) | (2 if has_hashes else 0)
+    pay = b"".join(payload)
+    hdr0 = struct.pack("<4sIIIQQQQI8s", b"CRUM", 1, flags, R, K, meta, poff, len(pay),
+                       zlib.crc32(body), b"\0" * 8)
+    hdr = hdr0 + struct.pack("<I", zlib.crc32(hdr0))
+    return hdr + body + b"\0" * (poff - meta) + pay
+
+
+def parse_image(img: bytes):
+    img = bytes(img)
+    magic, ver, flags, R, K, meta, poff, paylen, mcrc, _res, hcrc = HDR.unpack_from(img, 0)
+    table = [ENTRY.unpack_from(img, 64 + 48 * k) for k in range(R)]
+    ids_off = 64 + 48 * R
+    ids = list(struct.unpack_from(f"<{K}I", img, ids_off)) if K else []
+    hashes = []
+    if flags & 2 and K:
+        hashes = list(struct.unpack_from(f"<{K}Q", img, ids_off + round_up(4 * K, 8)))
+    return dict(magic=magic, version=ver, flags=flags, R=R, K=K, meta=meta, poff=poff,
+                payload_bytes=paylen, meta_crc=mcrc, header_crc=hcrc, table=table, ids=ids,
+                hashes=hashes)
