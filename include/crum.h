@@ -1,0 +1,227 @@
+/*
+ * crum.h -- C ABI of the B200-native shadow-page synchronisation library
+ * (libcrum.so), the data-parallel hot path of CRUM (arXiv 1808.00117).
+ *
+ * The calls follow the paper's statement of the problem:
+ *   Alg. 1 "Shadow page synchronization algorithm":
+ *     - "CUDA Create UVM region": CreateShadowPage, all pages dirty
+ *                           -> crum_register_region
+ *     - "Page Fault ... MarkPageAsDirty()"
+ *                                                       -> crum_mark_dirty and
+ *       content-based detection inside every sync/gather (reading Q1)
+ *     - "CUDA call: if hasDirtyPages: SendDataToRealPages(); ClearDirtyPages()"
+ *                           -> crum_sync_shadow
+ *   sec. 3.4 checkpoint drain: "for all the active CUDA-MALLOC and CUDA-UVM
+ *     memory regions, data is read in from the GPU to the host"
+ *                                                       -> crum_checkpoint_gather
+ *   sec. 3.4 restart: "transfers the data into the actual CUDA and CUDA-UVM
+ *     regions"                       -> crum_restore_scatter
+ *
+ * Conventions (all functions):
+ *   - Return int: CRUM_OK (0) or a negative crum_status.  No exceptions cross
+ *     the ABI, nothing calls exit().  On any error other than CRUM_E_CUDA no
+ *     state changes: registry, snapshots, hash tables and force bits are
+ *     untouched; a failed gather commits nothing; a rejected restore writes
+ *     nothing.  CRUM_E_CUDA is sticky: it poisons the context (every later
+ *     call on it returns CRUM_E_CUDA); crum_last_error_detail() says why.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Work is enqueued after all prior work on `stream`: that is the
+ *     quiescence point, the analog of the paper's cudaDeviceSynchronize drain
+ *     (PAPER.md:545).  Writers on other streams during a call are undefined
+ *     behaviour.  The library keeps no stream handle after a call returns.
+ *   - Device pointers are plain CUDA device (or managed) addresses on the
+ *     context's device; host pointers are ordinary process addresses.
+ *   - A context is single-threaded (one thread at a time per context).
+ */
+#ifndef CRUM_H
+#define CRUM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifndef CRUM_API
+#if defined(__GNUC__)
+#define CRUM_API __attribute__((visibility("default")))
+#else
+#define CRUM_API
+#endif
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CRUM_ABI_VERSION 1
+
+/* Status codes. */
+enum crum_status {
+    CRUM_OK = 0,
+    CRUM_E_INVAL = -1,     /* null pointer, bytes == 0, bad page size / mode / flags, misaligned ptr */
+    CRUM_E_OVERLAP = -2,   /* new range overlaps a live region ("Overlap") */
+    CRUM_E_NOREGION = -3,  /* unknown region id */
+    CRUM_E_RANGE = -4,     /* crum_mark_dirty range outside the region */
+    CRUM_E_NOMEM = -5,     /* device or pinned host allocation failed */
+    CRUM_E_CAPACITY = -6,  /* image buffer too small; report->image_bytes = required size */
+    CRUM_E_CORRUPT = -7,   /* bad magic/version/CRC/sizes/ids, or a hash mismatch under CRUM_VERIFY */
+    CRUM_E_MISMATCH = -8,  /* image region table != live registered set */
+    CRUM_E_BUSY = -9,      /* reserved */
+    CRUM_E_DEVICE = -10,   /* ptr not accessible from the context's device; no such device */
+    CRUM_E_CUDA = -11      /* underlying CUDA error (sticky) */
+};
+
+/* Per-region dirty-detection mode (reading Q1/Q8). */
+typedef enum {
+    CRUM_MODE_COMPARE = 0,   /* device byte mirror of the region, per-page compare */
+    CRUM_MODE_HASH_XXH3 = 1  /* 8 B per page: XXH3-64 (seed 0) of the zero-padded page slot */
+} crum_mode;
+
+/* Call flags. */
+enum {
+    CRUM_FULL = 1u << 0,   /* gather: list every page (the paper's full drain) */
+    CRUM_VERIFY = 1u << 1  /* restore: recompute and check every hash-mode slot before writing */
+};
+
+typedef struct crum_ctx crum_ctx;     /* one per (process, CUDA device) */
+typedef struct crum_image crum_image; /* library-owned pinned host buffer holding one image */
+
+typedef struct {
+    uint64_t chunk_bytes; /* host-link pipeline chunk (0 = 64 MiB); multiple of 4096 */
+    uint32_t flags;       /* reserved, must be 0 */
+    uint32_t reserved;    /* must be 0 */
+} crum_config;
+
+/* Outcome of a sync / gather / restore.  Times are CUDA-event milliseconds
+ * on the call's stream (0 when not measured). */
+typedef struct {
+    uint64_t scanned_pages;  /* N = sum of n_r over live regions */
+    uint64_t scanned_bytes;  /* F = sum of B_r */
+    uint64_t dirty_pages;    /* K (pages listed / committed / restored) */
+    uint64_t dirty_bytes;    /* sum of logical lengths of those pages */
+    uint64_t dirty_runs;     /* maximal runs of consecutive page indices, summed over regions */
+    uint64_t image_bytes;    /* image length (gather, restore); required size on CRUM_E_CAPACITY */
+    double t_detect_ms;      /* A1: detect */
+    double t_compact_ms;     /* A2: compact + image metadata */
+    double t_gather_ms;      /* A3: gather + commit (restore: scatter + commit) */
+    double t_copy_ms;        /* A4: host-link copy (D2H for gather, H2D for restore) */
+    double t_total_ms;       /* whole call, first enqueue to completion */
+} crum_report;
+
+/* ---------------------------------------------------------------------------
+ * Context.  crum_create binds to CUDA device `device` (cudaSetDevice is
+ * called by every entry point).  cfg may be NULL (defaults).  Errors:
+ * INVAL (null out / bad cfg), DEVICE (no such device), NOMEM, CUDA.
+ * crum_destroy frees everything the library owns for this context (snapshots,
+ * hash tables, scratch); images must be destroyed before their context.
+ * ------------------------------------------------------------------------- */
+CRUM_API int crum_create(int device, const crum_config *cfg, crum_ctx **out);
+CRUM_API int crum_destroy(crum_ctx *ctx);
+
+/* ---------------------------------------------------------------------------
+ * Alg. 1 "CUDA Create UVM region".  Registers the caller's
+ * device/managed range [ptr, ptr+bytes) split into pages of page_size bytes
+ * (the last page may be partial: logical length B - i*P, Q7) and
+ * creates its shadow: a device byte mirror (COMPARE) or an 8 B/page hash
+ * table (HASH_XXH3).  Every page starts force-dirty ("all the pages in the
+ * regions are marked as dirty"), so the first sync/gather
+ * lists all n = ceil(bytes/page_size) pages.
+ * Preconditions: ptr 16-byte aligned, accessible from the context's device;
+ * bytes > 0; page_size a power of two in [4096, 2 MiB]; n < 2^32 and the
+ * context's total page count < 2^31; no overlap with a live region.
+ * Ownership: the caller owns ptr and must keep it valid until unregister; the
+ * library never frees or moves it.  Region ids start at 1, increase
+ * monotonically and are never reused; id order is image order.
+ * Errors: INVAL, DEVICE, OVERLAP, NOMEM, CUDA.
+ * ------------------------------------------------------------------------- */
+CRUM_API int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page_size,
+                         uint32_t mode, uint32_t *region_id_out);
+CRUM_API int crum_unregister_region(crum_ctx *ctx, uint32_t region_id);
+
+/* Alg. 1 MarkPageAsDirty as an explicit call: sets the force
+ * bit of every page overlapping [offset, offset+len).  len == 0 is a no-op.
+ * Errors: NOREGION, RANGE (offset+len > bytes). */
+CRUM_API int crum_mark_dirty(crum_ctx *ctx, uint32_t region_id, uint64_t offset, uint64_t len);
+
+/* ---------------------------------------------------------------------------
+ * Alg. 1 "CUDA call" event: detect the dirty pages of every
+ * live region (force bit, or bytes differ from the snapshot / XXH3 differs
+ * from the stored hash), then commit them (snapshot <- current, force <- 0).
+ * If dirty_pages_out is non-NULL the call waits and stores K; if NULL the call
+ * is fully stream-asynchronous.  An immediate second sync returns 0.
+ * ------------------------------------------------------------------------- */
+CRUM_API int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_pages_out);
+
+/* Upper bound on the image size when at most max_dirty_pages are listed
+ * (pass UINT64_MAX for "every page"). */
+CRUM_API int crum_image_required_bytes(crum_ctx *ctx, uint64_t max_dirty_pages, uint64_t *bytes_out);
+
+/* Pinned host images (cudaHostAlloc).  crum_image_import copies `len` bytes
+ * into a new image (for restart from a file).  crum_image_data exposes the
+ * buffer: *data_out (host pointer, owned by the image), *len_out (valid image
+ * length; 0 before the first gather), *capacity_out (may be NULL). */
+CRUM_API int crum_image_create(crum_ctx *ctx, uint64_t capacity_bytes, crum_image **out);
+CRUM_API int crum_image_import(crum_ctx *ctx, const void *bytes, uint64_t len, crum_image **out);
+CRUM_API int crum_image_data(const crum_image *img, void **data_out, uint64_t *len_out, uint64_t *capacity_out);
+CRUM_API int crum_image_destroy(crum_image *img);
+
+/* ---------------------------------------------------------------------------
+ * sec. 3.4 checkpoint drain as an incremental gather (DESIGN
+ * readings Q5/Q12): detect (A1), compact the dirty ids in (region id, page
+ * index) order (A2), gather those pages into the v1 image (A3; DESIGN.md
+ * "Image format") and commit them, copying the image into `img` in pinned host
+ * memory over the host link (A4).  flags: 0 or CRUM_FULL.  Returns when the
+ * image is complete in host memory and the commit is done.
+ * Errors: INVAL; CAPACITY (nothing committed; report->image_bytes = needed);
+ * CUDA.  report may be NULL.
+ * ------------------------------------------------------------------------- */
+CRUM_API int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_t flags,
+                           crum_report *report_out);
+
+/* Same, but the image is written into a caller-owned DEVICE buffer
+ * [dev_image, dev_image+capacity) and never crosses the host link.
+ * If report_out is NULL the call is stream-asynchronous and capacity must be
+ * >= crum_image_required_bytes(ctx, UINT64_MAX) (else CAPACITY, checked on the
+ * host before anything is enqueued); with a report the call waits, and an
+ * image larger than capacity returns CAPACITY with nothing committed.
+ * The image length is report_out->image_bytes (also header bytes 32..47). */
+CRUM_API int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capacity, void *stream,
+                                  uint32_t flags, crum_report *report_out);
+
+/* ---------------------------------------------------------------------------
+ * sec. 3.4 restart (reading Q11): validate the image
+ * (magic, version, both CRC-32s, sizes, ids strictly ascending and in range,
+ * table == live registered set), then write each listed page's logical bytes
+ * back into its region and commit it (snapshot <- slot / table <- listed
+ * hash, force <- 0).  flags: 0 or CRUM_VERIFY.  Pages not listed are left
+ * alone, so image k restores state k onto state k-1.
+ * Errors: INVAL, CORRUPT, MISMATCH (nothing written), CUDA.
+ * ------------------------------------------------------------------------- */
+CRUM_API int crum_restore_scatter(crum_ctx *ctx, const crum_image *img, void *stream, uint32_t flags,
+                         crum_report *report_out);
+CRUM_API int crum_restore_scatter_device(crum_ctx *ctx, const void *dev_image, uint64_t len, void *stream,
+                                uint32_t flags, crum_report *report_out);
+
+/* Status text; thread-local detail of the last error on this thread. */
+CRUM_API const char *crum_status_string(int status);
+CRUM_API const char *crum_last_error_detail(void);
+
+/* ---------------------------------------------------------------------------
+ * Test/parity hooks (not on the hot path).
+ * crum_debug_detect: run A1 over every live region WITHOUT committing and copy
+ *   (force | changed) per page, in global page order (regions ascending), into
+ *   host_flags[0..n) (n must equal the total page count).
+ * crum_debug_export: copy a region's FORCE bits (u8 per page), HASHES (u64 per
+ *   page, hash mode) or MIRROR (B bytes, compare mode) into host_buf (len must
+ *   match exactly).
+ * ------------------------------------------------------------------------- */
+enum { CRUM_EXPORT_FORCE = 0, CRUM_EXPORT_HASHES = 1, CRUM_EXPORT_MIRROR = 2 };
+CRUM_API int crum_debug_detect(crum_ctx *ctx, void *stream, uint8_t *host_flags, uint64_t n);
+CRUM_API int crum_debug_export(crum_ctx *ctx, uint32_t region_id, int what, void *host_buf, uint64_t len);
+
+/* Number of kernel launches this context has enqueued so far (bench evidence). */
+CRUM_API uint64_t crum_launch_count(const crum_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CRUM_H */

@@ -1,0 +1,45 @@
+/*
+ * crum_synth.h -- seeded synthetic-input kernels exported by libcrum.so for
+ * tests and bench.py (NOT part of the shadow-page method).  They implement
+ * the counter-based recipe of synth/__init__.py
+ * on the device, so multi-GiB footprints need not cross the host link:
+ *
+ *   content: u64 word j of region r = splitmix64(S ^ (r << 40) ^ (word_offset + j))
+ *   writer : each listed page's logical words ^= splitmix64((S+2) ^ (epoch << 56)
+ *            ^ (r << 40) ^ page) | 1   (touch != 0: only the page's last word)
+ *
+ * All pointers are device pointers; work is enqueued on `stream` (void* =
+ * cudaStream_t).  Returns CRUM_OK or CRUM_E_INVAL / CRUM_E_CUDA.
+ */
+#ifndef CRUM_SYNTH_H
+#define CRUM_SYNTH_H
+
+#include <stdint.h>
+
+#ifndef CRUM_API
+#if defined(__GNUC__)
+#define CRUM_API __attribute__((visibility("default")))
+#else
+#define CRUM_API
+#endif
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+CRUM_API int crum_synth_fill(void *dev_ptr, uint64_t bytes, uint64_t seed, uint64_t region_index,
+                    uint64_t word_offset, void *stream);
+
+CRUM_API int crum_synth_write_pages(void *dev_ptr, uint64_t bytes, uint64_t page_size,
+                           const uint32_t *dev_pages, uint64_t n_pages, uint64_t seed,
+                           uint64_t epoch, uint64_t region_index, int touch, void *stream);
+
+/* Streaming write of `bytes` to scrub L2 between timed repetitions. */
+CRUM_API int crum_synth_scrub(void *dev_ptr, uint64_t bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CRUM_SYNTH_H */

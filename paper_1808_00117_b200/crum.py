@@ -1,0 +1,316 @@
+"""Thin ctypes binding over libcrum.so (include/crum.h, include/crum_synth.h).
+
+Argument marshalling only: every step of the shadow-page path runs in the
+library's sm_100a kernels.  There is no CPU fallback -- if libcrum.so is
+missing this module raises ImportError (build it with
+``python -m paper_1808_00117_b200.build``).
+
+Region memory, streams and images are passed as raw addresses; helpers accept
+torch tensors / streams (``.data_ptr()``, ``.cuda_stream``) without importing
+torch themselves.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcrum.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libcrum.so not built at {LIB_PATH}; run `python -m paper_1808_00117_b200.build`")
+
+_L = C.CDLL(LIB_PATH)
+
+OK = 0
+E_INVAL, E_OVERLAP, E_NOREGION, E_RANGE, E_NOMEM = -1, -2, -3, -4, -5
+E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY, E_DEVICE, E_CUDA = -6, -7, -8, -9, -10, -11
+MODE_COMPARE, MODE_HASH = 0, 1
+FULL, VERIFY = 1, 2
+EXPORT_FORCE, EXPORT_HASHES, EXPORT_MIRROR = 0, 1, 2
+ALL_PAGES = (1 << 64) - 1
+
+# Every symbol include/*.h declares (checked by tests/test_abi_cpu.py).
+EXPORTED = (
+    "crum_create", "crum_destroy", "crum_register_region", "crum_unregister_region", "crum_mark_dirty",
+    "crum_sync_shadow", "crum_image_required_bytes", "crum_image_create", "crum_image_import",
+    "crum_image_data", "crum_image_destroy", "crum_checkpoint_gather", "crum_checkpoint_gather_device",
+    "crum_restore_scatter", "crum_restore_scatter_device", "crum_status_string", "crum_last_error_detail",
+    "crum_debug_detect", "crum_debug_export", "crum_launch_count",
+    "crum_synth_fill", "crum_synth_write_pages", "crum_synth_scrub",
+)
+
+
+class Config(C.Structure):
+    _fields_ = [("chunk_bytes", C.c_uint64), ("flags", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+class Report(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("scanned_pages", "scanned_bytes", "dirty_pages", "dirty_bytes",
+                                          "dirty_runs", "image_bytes")] + \
+               [(n, C.c_double) for n in ("t_detect_ms", "t_compact_ms", "t_gather_ms", "t_copy_ms",
+                                          "t_total_ms")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_vp, _u64, _u32, _i = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int
+_sig = {
+    "crum_create": (_i, [_i, C.POINTER(Config), C.POINTER(_vp)]),
+    "crum_destroy": (_i, [_vp]),
+    "crum_register_region": (_i, [_vp, _vp, _u64, _u64, _u32, C.POINTER(_u32)]),
+    "crum_unregister_region": (_i, [_vp, _u32]),
+    "crum_mark_dirty": (_i, [_vp, _u32, _u64, _u64]),
+    "crum_sync_shadow": (_i, [_vp, _vp, C.POINTER(_u64)]),
+    "crum_image_required_bytes": (_i, [_vp, _u64, C.POINTER(_u64)]),
+    "crum_image_create": (_i, [_vp, _u64, C.POINTER(_vp)]),
+    "crum_image_import": (_i, [_vp, _vp, _u64, C.POINTER(_vp)]),
+    "crum_image_data": (_i, [_vp, C.POINTER(_vp), C.POINTER(_u64), C.POINTER(_u64)]),
+    "crum_image_destroy": (_i, [_vp]),
+    "crum_checkpoint_gather": (_i, [_vp, _vp, _vp, _u32, C.POINTER(Report)]),
+    "crum_checkpoint_gather_device": (_i, [_vp, _vp, _u64, _vp, _u32, C.POINTER(Report)]),
+    "crum_restore_scatter": (_i, [_vp, _vp, _vp, _u32, C.POINTER(Report)]),
+    "crum_restore_scatter_device": (_i, [_vp, _vp, _u64, _vp, _u32, C.POINTER(Report)]),
+    "crum_status_string": (C.c_char_p, [_i]),
+    "crum_last_error_detail": (C.c_char_p, []),
+    "crum_debug_detect": (_i, [_vp, _vp, _vp, _u64]),
+    "crum_debug_export": (_i, [_vp, _u32, _i, _vp, _u64]),
+    "crum_launch_count": (_u64, [_vp]),
+    "crum_synth_fill": (_i, [_vp, _u64, _u64, _u64, _u64, _vp]),
+    "crum_synth_write_pages": (_i, [_vp, _u64, _u64, _vp, _u64, _u64, _u64, _u64, _i, _vp]),
+    "crum_synth_scrub": (_i, [_vp, _u64, _vp]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_L, _name)
+    _f.restype, _f.argtypes = _res, _args
+
+
+def lib():
+    return _L
+
+
+class CrumError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        detail = (_L.crum_last_error_detail() or b"").decode(errors="replace")
+        msg = (_L.crum_status_string(status) or b"?").decode()
+        super().__init__(f"{what}: {msg} ({status}) {detail}")
+        self.status = status
+        self.detail = detail
+
+
+def _check(st: int, what: str):
+    if st != OK:
+        raise CrumError(st, what)
+
+
+def _stream(s) -> int | None:
+    if s is None:
+        return None
+    if hasattr(s, "cuda_stream"):
+        return int(s.cuda_stream)
+    return int(s)
+
+
+def _addr(x) -> int:
+    if hasattr(x, "data_ptr"):
+        return int(x.data_ptr())
+    return int(x)
+
+
+class Image:
+    """A library-owned pinned host image (crum_image)."""
+
+    def __init__(self, ctx: "Context", capacity: int | None = None, data: bytes | np.ndarray | None = None):
+        self._h = _vp()
+        self._ctx = ctx
+        if data is not None:
+            buf = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray)
+                                       else data.view(np.uint8).reshape(-1))
+            _check(_L.crum_image_import(ctx._h, buf.ctypes.data if buf.nbytes else None, buf.nbytes,
+                                        C.byref(self._h)), "crum_image_import")
+        else:
+            if capacity is None:
+                capacity = ctx.image_required_bytes()
+            _check(_L.crum_image_create(ctx._h, capacity, C.byref(self._h)), "crum_image_create")
+
+    def _info(self):
+        p, n, cap = _vp(), _u64(), _u64()
+        _check(_L.crum_image_data(self._h, C.byref(p), C.byref(n), C.byref(cap)), "crum_image_data")
+        return p.value or 0, n.value, cap.value
+
+    @property
+    def length(self) -> int:
+        return self._info()[1]
+
+    @property
+    def capacity(self) -> int:
+        return self._info()[2]
+
+    @property
+    def address(self) -> int:
+        return self._info()[0]
+
+    def view(self, full_capacity: bool = False) -> np.ndarray:
+        """Zero-copy numpy view of the pinned buffer (valid until destroy)."""
+        p, n, cap = self._info()
+        m = cap if full_capacity else n
+        if m == 0:
+            return np.zeros(0, dtype=np.uint8)
+        return np.ctypeslib.as_array((C.c_uint8 * m).from_address(p))
+
+    def tobytes(self) -> bytes:
+        return self.view().tobytes()
+
+    def destroy(self):
+        if self._h and self._h.value:
+            _L.crum_image_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+class Context:
+    """crum_ctx: one per (process, CUDA device)."""
+
+    def __init__(self, device: int = 0, chunk_bytes: int = 0):
+        self._h = _vp()
+        cfg = Config(chunk_bytes, 0, 0)
+        _check(_L.crum_create(device, C.byref(cfg), C.byref(self._h)), "crum_create")
+        self.device = device
+        self._keep = {}
+
+    def close(self):
+        if self._h and self._h.value:
+            _L.crum_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- Alg. 1 "CUDA Create UVM region"
+    def register_region(self, ptr, nbytes: int | None = None, page_size: int = 65536, mode: int = MODE_COMPARE,
+                        keep=None) -> int:
+        if nbytes is None:
+            nbytes = int(ptr.numel() * ptr.element_size())
+        rid = _u32()
+        _check(_L.crum_register_region(self._h, _addr(ptr), nbytes, page_size, mode, C.byref(rid)),
+               "crum_register_region")
+        self._keep[rid.value] = keep if keep is not None else (ptr if hasattr(ptr, "data_ptr") else None)
+        return rid.value
+
+    def try_register(self, ptr: int, nbytes: int, page_size: int, mode: int = MODE_COMPARE) -> int:
+        """Raw status of crum_register_region (tests of the error paths)."""
+        rid = _u32()
+        return _L.crum_register_region(self._h, ptr, nbytes, page_size, mode, C.byref(rid))
+
+    def unregister_region(self, rid: int):
+        _check(_L.crum_unregister_region(self._h, rid), "crum_unregister_region")
+        self._keep.pop(rid, None)
+
+    def mark_dirty(self, rid: int, offset: int, length: int) -> int:
+        return _L.crum_mark_dirty(self._h, rid, offset, length)
+
+    # -- Alg. 1 "CUDA call"
+    def sync_shadow(self, stream=None, wait: bool = True):
+        n = _u64()
+        _check(_L.crum_sync_shadow(self._h, _stream(stream), C.byref(n) if wait else None), "crum_sync_shadow")
+        return n.value if wait else None
+
+    def image_required_bytes(self, max_dirty: int = ALL_PAGES) -> int:
+        n = _u64()
+        _check(_L.crum_image_required_bytes(self._h, max_dirty, C.byref(n)), "crum_image_required_bytes")
+        return n.value
+
+    def new_image(self, capacity: int | None = None) -> Image:
+        return Image(self, capacity)
+
+    def import_image(self, data) -> Image:
+        return Image(self, data=data)
+
+    # -- sec. 3.4 drain
+    def checkpoint_gather(self, image: Image, stream=None, flags: int = 0, raise_on_error: bool = True):
+        rep = Report()
+        st = _L.crum_checkpoint_gather(self._h, image._h, _stream(stream), flags, C.byref(rep))
+        if raise_on_error:
+            _check(st, "crum_checkpoint_gather")
+            return rep.as_dict()
+        return st, rep.as_dict()
+
+    def checkpoint_gather_device(self, dev_ptr, capacity: int, stream=None, flags: int = 0, report: bool = True,
+                                 raise_on_error: bool = True):
+        rep = Report()
+        st = _L.crum_checkpoint_gather_device(self._h, _addr(dev_ptr), capacity, _stream(stream), flags,
+                                              C.byref(rep) if report else None)
+        if raise_on_error:
+            _check(st, "crum_checkpoint_gather_device")
+            return rep.as_dict() if report else None
+        return st, (rep.as_dict() if report else None)
+
+    # -- sec. 3.4 restart
+    def restore_scatter(self, image: Image, stream=None, flags: int = 0, raise_on_error: bool = True):
+        rep = Report()
+        st = _L.crum_restore_scatter(self._h, image._h, _stream(stream), flags, C.byref(rep))
+        if raise_on_error:
+            _check(st, "crum_restore_scatter")
+            return rep.as_dict()
+        return st, rep.as_dict()
+
+    def restore_scatter_device(self, dev_ptr, length: int, stream=None, flags: int = 0, report: bool = True,
+                               raise_on_error: bool = True):
+        rep = Report()
+        st = _L.crum_restore_scatter_device(self._h, _addr(dev_ptr), length, _stream(stream), flags,
+                                            C.byref(rep) if report else None)
+        if raise_on_error:
+            _check(st, "crum_restore_scatter_device")
+            return rep.as_dict() if report else None
+        return st, (rep.as_dict() if report else None)
+
+    # -- test hooks
+    def debug_detect(self, n_pages: int, stream=None) -> np.ndarray:
+        out = np.zeros(n_pages, dtype=np.uint8)
+        _check(_L.crum_debug_detect(self._h, _stream(stream), out.ctypes.data if n_pages else None, n_pages),
+               "crum_debug_detect")
+        return out
+
+    def debug_export(self, rid: int, what: int, n: int) -> np.ndarray:
+        dtype = np.uint64 if what == EXPORT_HASHES else np.uint8
+        out = np.zeros(n, dtype=dtype)
+        _check(_L.crum_debug_export(self._h, rid, what, out.ctypes.data, out.nbytes), "crum_debug_export")
+        return out
+
+    @property
+    def launch_count(self) -> int:
+        return int(_L.crum_launch_count(self._h))
+
+
+# -- synthetic inputs (include/crum_synth.h) --------------------------------
+def synth_fill(dev_ptr, nbytes: int, seed: int, region_index: int, word_offset: int = 0, stream=None):
+    _check(_L.crum_synth_fill(_addr(dev_ptr), nbytes, seed, region_index, word_offset, _stream(stream)),
+           "crum_synth_fill")
+
+
+def synth_write_pages(dev_ptr, nbytes: int, page_size: int, dev_pages, n_pages: int, seed: int, epoch: int,
+                      region_index: int, touch: bool = False, stream=None):
+    _check(_L.crum_synth_write_pages(_addr(dev_ptr), nbytes, page_size, _addr(dev_pages) if n_pages else None,
+                                     n_pages, seed, epoch, region_index, int(touch), _stream(stream)),
+           "crum_synth_write_pages")
+
+
+def synth_scrub(dev_ptr, nbytes: int, stream=None):
+    _check(_L.crum_synth_scrub(_addr(dev_ptr), nbytes, _stream(stream)), "crum_synth_scrub")

@@ -1,0 +1,133 @@
+// crum_internal.cuh -- device-side data layout and kernel launchers of
+// libcrum.so (private to the library; the ABI is include/crum.h).
+//
+// HBM layout:
+//   * registered regions: the caller's bytes, untouched except by restore.
+//   * per region: COMPARE -> byte mirror (B_r bytes, 256-B aligned);
+//                 HASH    -> u64 table[n_r] (last committed XXH3 per page).
+//   * per context, indexed by the global page id g (regions ascending, pages
+//     ascending; page i of region r is g = page_base_r + i):
+//       force[g]   u8  force-dirty bit (register sets all; commit clears)
+//       flags[g]   u8  "content changed" bit written by detect (scratch)
+//       newhash[g] u64 XXH3 of the page computed by detect (scratch)
+//       gids[K]    u32 compacted dirty page ids, ascending (scratch)
+//     per-page arrays are padded to a multiple of kPagesPerCompactBlock with
+//     zeros so compaction can use 16-byte vector loads without bounds checks.
+//   * image (device buffer): v1 format, header | table | ids | hashes | pad |
+//     payload (slots of P_r bytes, 4096-aligned).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace crum {
+
+constexpr uint32_t kSegLog2 = 12;              // 4 KiB work segment (min page size)
+constexpr uint32_t kSegBytes = 1u << kSegLog2;
+constexpr uint32_t kPagesPerThread = 16;       // compaction: one uint4 of flags per thread
+constexpr uint32_t kCompactThreads = 256;
+constexpr uint32_t kPagesPerCompactBlock = kPagesPerThread * kCompactThreads;  // 4096
+
+enum : uint32_t { kModeCompare = 0, kModeHash = 1 };
+enum : uint32_t { kStOk = 0, kStCapacity = 6, kStCorrupt = 7 };
+
+struct DevRegion {
+    uint8_t *base;      // registered bytes
+    uint8_t *mirror;    // compare mode snapshot (nullptr in hash mode)
+    uint64_t *table;    // hash mode snapshot (nullptr in compare mode)
+    uint64_t bytes;     // B_r
+    uint64_t page_base; // global id of page 0
+    uint64_t n_pages;   // n_r
+    uint32_t log2p;     // log2(P_r)
+    uint32_t mode;
+    uint32_t id;
+    uint32_t aligned32; // base is 32-byte aligned (256-bit vector path allowed)
+};
+
+// Per-region results of compaction (gather) or of the image table (restore).
+struct RegStat {
+    uint64_t first;        // index of the region's first listed slot
+    uint64_t n_dirty;      // slots listed for the region
+    uint64_t payload_base; // byte offset of the region's first slot inside the payload
+    uint64_t unit_base;    // 4 KiB payload units before the region (prefix)
+};
+
+// Device-resident bookkeeping of one gather / restore call.
+struct DevStats {
+    uint64_t K;
+    uint64_t meta_bytes;
+    uint64_t poff;
+    uint64_t payload_bytes;
+    uint64_t image_bytes;
+    uint64_t dirty_bytes;
+    uint64_t dirty_runs;
+    uint64_t total_units;
+    uint32_t status;        // kStOk / kStCapacity / kStCorrupt
+    uint32_t crc_acc;       // XOR of per-chunk raw CRC terms (meta CRC)
+    uint32_t img_flags;     // header flags (bit0 FULL, bit1 HAS_HASHES)
+    uint32_t n_regions;
+    uint64_t capacity;      // device image capacity (gather)
+    uint32_t meta_crc;      // final zlib CRC-32 of [64, meta_bytes)
+    uint32_t pad0;
+};
+
+struct Launch {
+    cudaStream_t stream;
+    int sms;
+    uint64_t *counter;  // incremented per kernel launch
+};
+
+// ---- detect (kernels_detect.cu) ----
+void launch_detect_compare(const Launch &L, const DevRegion *regs, const uint32_t *cmp_idx,
+                           const uint64_t *cmp_seg, uint32_t n_cmp, uint64_t n_seg,
+                           const uint8_t *force, uint8_t *flags);
+void launch_detect_hash(const Launch &L, const DevRegion *regs, const uint32_t *hash_idx,
+                        const uint64_t *hash_grp, uint32_t n_hash, uint64_t n_grp,
+                        uint8_t *flags, uint64_t *newhash);
+void launch_verify_hash(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
+                        const uint8_t *meta, const uint8_t *payload_base, int add_poff, DevStats *st);
+
+// ---- compaction, metadata, gather, scatter, CRC (kernels_image.cu) ----
+void launch_compact(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N,
+                    int full, uint32_t *blk_counts, uint32_t *gids, DevStats *st);
+void launch_region_stats(const Launch &L, const DevRegion *regs, uint32_t R, const uint32_t *gids,
+                         RegStat *rs, DevStats *st, int full, int has_hashes, uint64_t capacity);
+void launch_meta(const Launch &L, const DevRegion *regs, uint32_t R, const uint32_t *gids,
+                 const uint64_t *newhash, const RegStat *rs, DevStats *st, uint8_t *img);
+// dst_base == nullptr: commit only.  Else unit u is written at
+// dst_base + (add_poff ? st->poff : 0) + (u - dst_unit0) * 4096.
+void launch_gather(const Launch &L, const DevRegion *regs, uint32_t R, const uint32_t *gids,
+                   const uint64_t *newhash, const RegStat *rs, const DevStats *st, uint8_t *dst_base,
+                   uint64_t dst_unit0, int add_poff, uint8_t *force, uint64_t unit_lo, uint64_t unit_hi);
+void launch_crc_meta(const Launch &L, const uint8_t *img, DevStats *st, const uint32_t *x2n);
+void launch_header(const Launch &L, uint8_t *img, DevStats *st, const uint32_t *x2n);
+void launch_restore_validate(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
+                             const uint8_t *img, DevStats *st);
+void launch_scatter(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
+                    const uint8_t *meta, const DevStats *st, const uint8_t *src_base, uint64_t src_unit0,
+                    int add_poff, uint8_t *force, uint64_t unit_lo, uint64_t unit_hi);
+void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N,
+                         uint8_t *out);
+
+// ---- synthetic inputs (synth.cu) ----
+void launch_synth_fill(cudaStream_t s, uint8_t *p, uint64_t bytes, uint64_t seed, uint64_t r,
+                       uint64_t word_offset);
+void launch_synth_write(cudaStream_t s, uint8_t *p, uint64_t bytes, uint64_t page_size,
+                        const uint32_t *pages, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t r,
+                        int touch);
+void launch_synth_scrub(cudaStream_t s, uint8_t *p, uint64_t bytes);
+
+// ---- small device helpers shared by the kernel files ----
+__host__ __device__ inline uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// Largest r in [0, n) with prefix[r] <= key (prefix is ascending, prefix[0] == 0).
+__device__ __forceinline__ uint32_t upper_region(const uint64_t *prefix, uint32_t n, uint64_t key) {
+    uint32_t lo = 0, hi = n;  // answer in [lo, hi)
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(prefix + mid) <= key) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+}  // namespace crum

@@ -1,0 +1,374 @@
+// kernels_detect.cu -- A1 "detect": which pages changed
+// since the last commit.  Reading Q1: the paper's write-fault
+// MarkPageAsDirty (Alg. 1) becomes a content test, because
+// GPU stores cannot be trapped:
+//   COMPARE: any byte of page i differs from the device mirror  (HBM: 2 reads)
+//   HASH   : XXH3-64 of the zero-padded slot differs from table  (HBM: 1 read)
+//
+// Both kernels are persistent grid-stride loops sized to the SM count.
+//  * compare: one warp per 4 KiB segment; 256-bit (LDG.256) streaming loads,
+//    4 per lane per operand = 8 x 32 B in flight per lane; warp vote.
+//  * hash: one warp per page (two 4 KiB pages per warp), lane = 4*b + p owns
+//    block b (1 KiB) and u64 lanes {2p, 2p+1} of every stripe, so the
+//    per-block "accumulate" sums stay in registers (no shuffles); the serial
+//    scramble chain across blocks runs on 4 lanes per page fed by 8 shuffles
+//    per 8 KiB.  XXH3 structure: xxhash 0.8 long-input loop (see
+//    DESIGN.md "XXH3 on the GPU"), written here independently of oracle/.
+#include "crum_internal.cuh"
+
+namespace crum {
+
+// ---------------------------------------------------------------------------
+// Streaming vector loads (read-only path, no L1 allocation).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ld256(const void *p, uint32_t (&r)[8]) {
+    asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "l"(p));
+}
+__device__ __forceinline__ uint4 ld128(const void *p) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p));
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// COMPARE detect.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_detect_compare(
+    const DevRegion *__restrict__ regs, const uint32_t *__restrict__ cmp_idx,
+    const uint64_t *__restrict__ cmp_seg, uint32_t n_cmp, uint64_t n_seg,
+    const uint8_t *__restrict__ force, uint8_t *__restrict__ flags) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t wpb = blockDim.x >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
+    uint64_t r_lo = 1, r_hi = 0;  // cached segment range of the current region
+    DevRegion R{};
+    for (uint64_t s = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); s < n_seg; s += nwarps) {
+        if (s < r_lo || s >= r_hi) {
+            uint32_t r = upper_region(cmp_seg, n_cmp, s);
+            R = regs[__ldg(cmp_idx + r)];
+            r_lo = __ldg(cmp_seg + r);
+            r_hi = __ldg(cmp_seg + r + 1);
+        }
+        const uint64_t si = s - r_lo;
+        const uint64_t off = si << kSegLog2;
+        const uint64_t g = R.page_base + (si >> (R.log2p - kSegLog2));
+        if (__ldg(force + g)) continue;  // already dirty: no need to read the bytes
+        const uint64_t len = R.bytes - off;
+        const uint8_t *a = R.base + off;
+        const uint8_t *b = R.mirror + off;
+        uint32_t x = 0;
+        if (len >= kSegBytes) {
+            if (R.aligned32) {
+                uint32_t va[4][8], vb[4][8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    ld256(a + i * 1024 + lane * 32, va[i]);
+                    ld256(b + i * 1024 + lane * 32, vb[i]);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) x |= va[i][j] ^ vb[i][j];
+            } else {
+                uint4 va[8], vb[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    va[i] = ld128(a + i * 512 + lane * 16);
+                    vb[i] = ld128(b + i * 512 + lane * 16);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    x |= (va[i].x ^ vb[i].x) | (va[i].y ^ vb[i].y) | (va[i].z ^ vb[i].z) |
+                         (va[i].w ^ vb[i].w);
+            }
+        } else {  // logical tail of a partial last page (reading Q7): bytewise
+            for (uint32_t o = lane; o < len; o += 32) x |= (uint32_t)(a[o] ^ b[o]);
+        }
+        if (__any_sync(0xffffffffu, x != 0) && lane == 0) flags[g] = 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// XXH3-64 (seed 0, default 192-byte secret), long-input path, per page slot.
+// ---------------------------------------------------------------------------
+constexpr uint8_t kSecretBytes[192] = {
+    0xb8, 0xfe, 0x6c, 0x39, 0x23, 0xa4, 0x4b, 0xbe, 0x7c, 0x01, 0x81, 0x2c, 0xf7, 0x21, 0xad, 0x1c,
+    0xde, 0xd4, 0x6d, 0xe9, 0x83, 0x90, 0x97, 0xdb, 0x72, 0x40, 0xa4, 0xa4, 0xb7, 0xb3, 0x67, 0x1f,
+    0xcb, 0x79, 0xe6, 0x4e, 0xcc, 0xc0, 0xe5, 0x78, 0x82, 0x5a, 0xd0, 0x7d, 0xcc, 0xff, 0x72, 0x21,
+    0xb8, 0x08, 0x46, 0x74, 0xf7, 0x43, 0x24, 0x8e, 0xe0, 0x35, 0x90, 0xe6, 0x81, 0x3a, 0x26, 0x4c,
+    0x3c, 0x28, 0x52, 0xbb, 0x91, 0xc3, 0x00, 0xcb, 0x88, 0xd0, 0x65, 0x8b, 0x1b, 0x53, 0x2e, 0xa3,
+    0x71, 0x64, 0x48, 0x97, 0xa2, 0x0d, 0xf9, 0x4e, 0x38, 0x19, 0xef, 0x46, 0xa9, 0xde, 0xac, 0xd8,
+    0xa8, 0xfa, 0x76, 0x3f, 0xe3, 0x9c, 0x34, 0x3f, 0xf9, 0xdc, 0xbb, 0xc7, 0xc7, 0x0b, 0x4f, 0x1d,
+    0x8a, 0x51, 0xe0, 0x4b, 0xcd, 0xb4, 0x59, 0x31, 0xc8, 0x9f, 0x7e, 0xc9, 0xd9, 0x78, 0x73, 0x64,
+    0xea, 0xc5, 0xac, 0x83, 0x34, 0xd3, 0xeb, 0xc3, 0xc5, 0x81, 0xa0, 0xff, 0xfa, 0x13, 0x63, 0xeb,
+    0x17, 0x0d, 0xdd, 0x51, 0xb7, 0xf0, 0xda, 0x49, 0xd3, 0x16, 0x55, 0x26, 0x29, 0xd4, 0x68, 0x9e,
+    0x2b, 0x16, 0xbe, 0x58, 0x7d, 0x47, 0xa1, 0xfc, 0x8f, 0xf8, 0xb8, 0xd1, 0x7a, 0xd0, 0x31, 0xce,
+    0x45, 0xcb, 0x3a, 0x8f, 0x95, 0x16, 0x04, 0x28, 0xaf, 0xd7, 0xfb, 0xca, 0xbb, 0x4b, 0x40, 0x7e,
+};
+
+struct XxhConsts {
+    uint64_t w[24];      // secret as 24 aligned little-endian words (stripe keys, scramble keys 16..23)
+    uint64_t last[8];    // words at byte offset 121 + 8l (the last stripe)
+    uint64_t merge[8];   // words at byte offset 11 + 8l (merge)
+    uint64_t init[8];    // initial accumulators
+};
+
+constexpr uint64_t le64_at(int off) {
+    uint64_t v = 0;
+    for (int i = 7; i >= 0; --i) v = (v << 8) | kSecretBytes[off + i];
+    return v;
+}
+
+constexpr XxhConsts make_consts() {
+    XxhConsts c{};
+    for (int i = 0; i < 24; ++i) c.w[i] = le64_at(8 * i);
+    for (int l = 0; l < 8; ++l) c.last[l] = le64_at(121 + 8 * l);
+    for (int l = 0; l < 8; ++l) c.merge[l] = le64_at(11 + 8 * l);
+    c.init[0] = 0xC2B2AE3Dull;            // PRIME32_3
+    c.init[1] = 0x9E3779B185EBCA87ull;    // PRIME64_1
+    c.init[2] = 0xC2B2AE3D27D4EB4Full;    // PRIME64_2
+    c.init[3] = 0x165667B19E3779F9ull;    // PRIME64_3
+    c.init[4] = 0x85EBCA77C2B2AE63ull;    // PRIME64_4
+    c.init[5] = 0x85EBCA77ull;            // PRIME32_2
+    c.init[6] = 0x27D4EB2F165667C5ull;    // PRIME64_5
+    c.init[7] = 0x9E3779B1ull;            // PRIME32_1
+    return c;
+}
+
+__constant__ XxhConsts c_xxh = make_consts();
+
+constexpr uint64_t kP32_1 = 0x9E3779B1ull;
+constexpr uint64_t kP64_1 = 0x9E3779B185EBCA87ull;
+constexpr uint64_t kMx1 = 0x165667919E3779F9ull;
+
+// Per-lane constants: lane p (= lane & 3) owns accumulator lanes 2p, 2p+1.
+struct LaneKeys {
+    uint64_t sw[17];           // stripe keys: word (s + 2p), s = 0..16
+    uint64_t last0, last1;     // last-stripe keys for lanes 2p, 2p+1
+    uint64_t scr0, scr1;       // scramble keys
+    uint64_t mrg0, mrg1;       // merge keys
+    uint64_t init0, init1;     // initial accumulators
+};
+
+__device__ __forceinline__ void load_lane_keys(LaneKeys &k, uint32_t p) {
+#pragma unroll
+    for (int j = 0; j < 17; ++j) k.sw[j] = c_xxh.w[2 * p + j];
+    k.last0 = c_xxh.last[2 * p];
+    k.last1 = c_xxh.last[2 * p + 1];
+    k.scr0 = c_xxh.w[16 + 2 * p];
+    k.scr1 = c_xxh.w[17 + 2 * p];
+    k.mrg0 = c_xxh.merge[2 * p];
+    k.mrg1 = c_xxh.merge[2 * p + 1];
+    k.init0 = c_xxh.init[2 * p];
+    k.init1 = c_xxh.init[2 * p + 1];
+}
+
+// One stripe's contribution to accumulator lanes (2p, 2p+1):
+//   acc[l]   += lo32(v_l ^ key_l) * hi32(v_l ^ key_l)
+//   acc[l^1] += v_l
+__device__ __forceinline__ void accum16(uint64_t &a0, uint64_t &a1, uint4 d, uint64_t s0,
+                                        uint64_t s1) {
+    const uint64_t v0 = ((uint64_t)d.y << 32) | d.x;
+    const uint64_t v1 = ((uint64_t)d.w << 32) | d.z;
+    const uint64_t k0 = v0 ^ s0, k1 = v1 ^ s1;
+    a0 += (uint64_t)(uint32_t)k0 * (uint32_t)(k0 >> 32) + v1;
+    a1 += (uint64_t)(uint32_t)k1 * (uint32_t)(k1 >> 32) + v0;
+}
+
+__device__ __forceinline__ uint64_t scramble(uint64_t a, uint64_t key) {
+    a ^= a >> 47;
+    a ^= key;
+    return a * kP32_1;
+}
+
+// 16 bytes of a page slot at byte offset `off`; bytes at or beyond `len` read
+// as zero (zero-padded slot, reading Q7).
+__device__ __forceinline__ uint4 ld_slot16(const uint8_t *pg, uint64_t off, uint64_t len) {
+    if (off + 16 <= len) return ld128(pg + off);
+    uint32_t w[4] = {0, 0, 0, 0};
+    for (uint32_t i = 0; i < 16; ++i)
+        if (off + i < len) w[i >> 2] |= (uint32_t)pg[off + i] << (8 * (i & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// XXH3-64 of this lane's page slot.  G = blocks per page per 8 KiB step
+// (8 for P >= 8 KiB; 4 for P = 4 KiB, two pages per warp).  `pg` is the page
+// base of the lane's group, `len` its logical length (<= P), bpp = P / 1024.
+// Result is valid on the group's chain lanes (lane % (4G) < 4).
+template <int G, bool TAIL>
+__device__ __forceinline__ uint64_t xxh3_slot(const uint8_t *__restrict__ pg, uint64_t len,
+                                              uint32_t bpp, uint32_t lane, const LaneKeys &k) {
+    const uint32_t p = lane & 3;
+    const uint32_t bl = (lane >> 2) % G;       // block slot within the group
+    const bool chain = (lane % (4 * G)) < 4;
+    uint64_t c0 = k.init0, c1 = k.init1;
+    const uint32_t steps = bpp / G;
+    for (uint32_t t = 0; t < steps; ++t) {
+        const uint32_t bi = t * G + bl;        // block index within the page
+        const uint64_t boff = (uint64_t)bi * 1024 + p * 16;
+        uint4 d[16];
+#pragma unroll
+        for (int s = 0; s < 16; ++s)
+            d[s] = TAIL ? ld_slot16(pg, boff + s * 64, len) : ld128(pg + boff + s * 64);
+        uint64_t a0 = 0, a1 = 0;
+#pragma unroll
+        for (int s = 0; s < 15; ++s) accum16(a0, a1, d[s], k.sw[s], k.sw[s + 1]);
+        const bool lastblk = (bi == bpp - 1);
+        accum16(a0, a1, d[15], lastblk ? k.last0 : k.sw[15], lastblk ? k.last1 : k.sw[16]);
+        // serial chain over the step's G blocks (chain lanes only keep results)
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const uint64_t x0 = __shfl_sync(0xffffffffu, a0, lane + 4 * j);
+            const uint64_t x1 = __shfl_sync(0xffffffffu, a1, lane + 4 * j);
+            c0 += x0;
+            c1 += x1;
+            if (t * G + j != bpp - 1) {
+                c0 = scramble(c0, k.scr0);
+                c1 = scramble(c1, k.scr1);
+            }
+        }
+    }
+    // merge: r = P * PRIME64_1 + sum_i fold64((acc[2i]^m[2i]) * (acc[2i+1]^m[2i+1]))
+    const uint64_t x = c0 ^ k.mrg0, y = c1 ^ k.mrg1;
+    uint64_t m = (x * y) ^ __umul64hi(x, y);
+    m += __shfl_xor_sync(0xffffffffu, m, 1);
+    m += __shfl_xor_sync(0xffffffffu, m, 2);
+    uint64_t r = (uint64_t)bpp * 1024 * kP64_1 + m;
+    r ^= r >> 37;
+    r *= kMx1;
+    r ^= r >> 32;
+    (void)chain;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// HASH detect: warp per page group (1 page, or 2 pages when P = 4 KiB).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_detect_hash(
+    const DevRegion *__restrict__ regs, const uint32_t *__restrict__ hash_idx,
+    const uint64_t *__restrict__ hash_grp, uint32_t n_hash, uint64_t n_grp,
+    uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash) {
+    const uint32_t lane = threadIdx.x & 31;
+    LaneKeys k;
+    load_lane_keys(k, lane & 3);
+    const uint64_t wpb = blockDim.x >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
+    uint64_t r_lo = 1, r_hi = 0;
+    DevRegion R{};
+    for (uint64_t w = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); w < n_grp; w += nwarps) {
+        if (w < r_lo || w >= r_hi) {
+            uint32_t r = upper_region(hash_grp, n_hash, w);
+            R = regs[__ldg(hash_idx + r)];
+            r_lo = __ldg(hash_grp + r);
+            r_hi = __ldg(hash_grp + r + 1);
+        }
+        const uint64_t P = 1ull << R.log2p;
+        const uint32_t bpp = (uint32_t)(P >> 10);
+        uint64_t h;
+        uint64_t page;
+        bool valid;
+        if (R.log2p == 12) {  // two 4 KiB pages per warp
+            page = (w - r_lo) * 2 + (lane >> 4);
+            valid = page < R.n_pages;
+            const uint64_t pg = valid ? page : page - 1;  // idle half recomputes its neighbour
+            const uint64_t len = min(P, R.bytes - (pg << 12));
+            const uint8_t *base = R.base + (pg << 12);
+            const bool tail = __any_sync(0xffffffffu, len < P);
+            h = tail ? xxh3_slot<4, true>(base, len, bpp, lane, k)
+                     : xxh3_slot<4, false>(base, len, bpp, lane, k);
+        } else {
+            page = w - r_lo;
+            valid = true;
+            const uint64_t len = min(P, R.bytes - (page << R.log2p));
+            const uint8_t *base = R.base + (page << R.log2p);
+            h = (len < P) ? xxh3_slot<8, true>(base, len, bpp, lane, k)
+                          : xxh3_slot<8, false>(base, len, bpp, lane, k);
+        }
+        const uint32_t G = (R.log2p == 12) ? 4 : 8;
+        if (valid && (lane % (4 * G)) == 0) {
+            const uint64_t g = R.page_base + page;
+            const uint64_t old = R.table[page];
+            newhash[g] = h;
+            flags[g] = (h != old) ? 1 : 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CRUM_VERIFY (restore): recompute XXH3 of every hash-mode slot of the image
+// payload and compare with the listed hash.  Warp per slot (P = 4 KiB slots
+// use the G = 4 path with the upper half-warp duplicating the lower).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_verify_hash(const DevRegion *__restrict__ regs,
+                                                     uint32_t R, const RegStat *__restrict__ rs,
+                                                     const uint8_t *__restrict__ meta,
+                                                     const uint8_t *__restrict__ payload_base,
+                                                     int add_poff, DevStats *st) {
+    const uint32_t lane = threadIdx.x & 31;
+    LaneKeys k;
+    load_lane_keys(k, lane & 3);
+    const uint64_t K = st->K;
+    const uint8_t *payload = payload_base + (add_poff ? st->poff : 0);
+    const uint64_t *hashes = reinterpret_cast<const uint64_t *>(meta + 64 + 48ull * R + round_up(4 * K, 8));
+    const uint64_t wpb = blockDim.x >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
+    for (uint64_t s = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); s < K; s += nwarps) {
+        // the slot's region is the LAST region whose first slot is <= s
+        // (regions listing no slot share `first` with their successor)
+        uint32_t lo = 0, hi = R;
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (rs[mid].first <= s) lo = mid; else hi = mid;
+        }
+        const DevRegion Rg = regs[lo];
+        if (Rg.mode != kModeHash) continue;
+        const uint64_t P = 1ull << Rg.log2p;
+        const uint8_t *slot = payload + rs[lo].payload_base + (s - rs[lo].first) * P;
+        const uint32_t bpp = (uint32_t)(P >> 10);
+        const uint64_t h = (Rg.log2p == 12) ? xxh3_slot<4, false>(slot, P, bpp, lane, k)
+                                            : xxh3_slot<8, false>(slot, P, bpp, lane, k);
+        if (lane == 0 && h != hashes[s]) atomicMax(&st->status, (uint32_t)kStCorrupt);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static inline int grid_for(uint64_t warps, int sms, int per_sm) {
+    uint64_t blocks = (warps + 7) / 8;
+    uint64_t cap = (uint64_t)sms * per_sm;
+    if (blocks > cap) blocks = cap;
+    return blocks ? (int)blocks : 1;
+}
+
+void launch_detect_compare(const Launch &L, const DevRegion *regs, const uint32_t *cmp_idx,
+                           const uint64_t *cmp_seg, uint32_t n_cmp, uint64_t n_seg,
+                           const uint8_t *force, uint8_t *flags) {
+    if (!n_seg) return;
+    k_detect_compare<<<grid_for(n_seg, L.sms, 8), 256, 0, L.stream>>>(regs, cmp_idx, cmp_seg, n_cmp,
+                                                                      n_seg, force, flags);
+    ++*L.counter;
+}
+
+void launch_detect_hash(const Launch &L, const DevRegion *regs, const uint32_t *hash_idx,
+                        const uint64_t *hash_grp, uint32_t n_hash, uint64_t n_grp, uint8_t *flags,
+                        uint64_t *newhash) {
+    if (!n_grp) return;
+    k_detect_hash<<<grid_for(n_grp, L.sms, 8), 256, 0, L.stream>>>(regs, hash_idx, hash_grp, n_hash,
+                                                                   n_grp, flags, newhash);
+    ++*L.counter;
+}
+
+void launch_verify_hash(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
+                        const uint8_t *meta, const uint8_t *payload_base, int add_poff, DevStats *st) {
+    if (!R) return;
+    k_verify_hash<<<L.sms * 4, 256, 0, L.stream>>>(regs, R, rs, meta, payload_base, add_poff, st);
+    ++*L.counter;
+}
+
+}  // namespace crum

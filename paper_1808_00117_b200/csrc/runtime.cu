@@ -1,0 +1,1161 @@
+// runtime.cu -- host runtime of libcrum.so and the C ABI of include/crum.h.
+//
+// Responsibilities: region registry and device
+// descriptors, shadow storage (mirrors / hash tables / force bits), scratch,
+// the gather -> D2H and H2D -> scatter chunk pipelines (side copy stream,
+// events), image header/table validation, error state.  All data-parallel
+// work runs in the kernels of kernels_detect.cu / kernels_image.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/crum.h"
+#include "crum_internal.cuh"
+
+using namespace crum;
+
+namespace {
+
+thread_local std::string g_detail;
+
+void set_detail(const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_detail = buf;
+}
+
+// --- host CRC-32 (zlib) helpers, used for the 60-byte header and to finalise
+// --- the device-computed metadata CRC.
+struct CrcTables {
+    uint32_t byte[256];
+    uint32_t x2n[32];  // x^(2^k) mod P (reflected)
+};
+
+uint32_t gf2_mulmod_host(uint32_t a, uint32_t b) {
+    uint32_t m = 0x80000000u, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+    }
+    return p;
+}
+
+const CrcTables &crc_tables() {
+    static CrcTables t = [] {
+        CrcTables c{};
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t v = i;
+            for (int k = 0; k < 8; ++k) v = (v >> 1) ^ (0xEDB88320u & (0u - (v & 1u)));
+            c.byte[i] = v;
+        }
+        c.x2n[0] = 0x40000000u;  // x^1
+        for (int k = 1; k < 32; ++k) c.x2n[k] = gf2_mulmod_host(c.x2n[k - 1], c.x2n[k - 1]);
+        return c;
+    }();
+    return t;
+}
+
+uint32_t crc32_host(const uint8_t *p, size_t n) {
+    const CrcTables &t = crc_tables();
+    uint32_t c = 0xffffffffu;
+    for (size_t i = 0; i < n; ++i) c = t.byte[(c ^ p[i]) & 0xffu] ^ (c >> 8);
+    return c ^ 0xffffffffu;
+}
+
+uint32_t xpow8n_host(uint64_t n) {
+    const CrcTables &t = crc_tables();
+    uint32_t p = 0x80000000u;
+    uint32_t k = 3;
+    while (n) {
+        if (n & 1) p = gf2_mulmod_host(t.x2n[k & 31], p);
+        n >>= 1;
+        ++k;
+    }
+    return p;
+}
+
+inline uint64_t rd64(const uint8_t *p) {
+    uint64_t v;
+    memcpy(&v, p, 8);
+    return v;
+}
+inline uint32_t rd32(const uint8_t *p) {
+    uint32_t v;
+    memcpy(&v, p, 4);
+    return v;
+}
+
+uint64_t meta_bytes_for(uint64_t R, uint64_t K, bool has_hashes) {
+    return 64 + 48 * R + round_up(4 * K, 8) + (has_hashes ? 8 * K : 0);
+}
+
+struct HostRegion {
+    uint32_t id;
+    uint32_t mode;
+    uint8_t *ptr;
+    uint64_t bytes;
+    uint64_t page_size;
+    uint64_t n_pages;
+    uint32_t log2p;
+    void *shadow;  // device mirror (compare) or hash table (hash)
+};
+
+constexpr uint64_t kDefaultChunk = 64ull << 20;
+constexpr int kRing = 3;
+constexpr uint64_t kMaxTotalPages = 0x7fffffffull;
+
+}  // namespace
+
+struct crum_image {
+    uint8_t *host;
+    uint64_t cap;
+    uint64_t len;
+    int device;
+};
+
+struct crum_ctx {
+    int device = 0;
+    int sms = 148;
+    uint64_t chunk = kDefaultChunk;
+    std::vector<HostRegion> regs;
+    uint32_t next_id = 1;
+    uint64_t N = 0, F = 0;
+    bool poisoned = false;
+    uint64_t launches = 0;
+
+    // device descriptors (rebuilt on register / unregister)
+    DevRegion *d_regs = nullptr;
+    uint32_t *d_cmp_idx = nullptr;
+    uint64_t *d_cmp_seg = nullptr;
+    uint32_t n_cmp = 0;
+    uint64_t n_seg = 0;
+    uint32_t *d_hash_idx = nullptr;
+    uint64_t *d_hash_grp = nullptr;
+    uint32_t n_hash = 0;
+    uint64_t n_grp = 0;
+    bool any_hash = false;
+
+    // per-page arrays (padded to kPagesPerCompactBlock)
+    uint64_t page_cap = 0;
+    uint8_t *d_force = nullptr;
+    uint8_t *d_flags = nullptr;
+    uint64_t *d_newhash = nullptr;
+    uint32_t *d_gids = nullptr;
+    uint32_t *d_blk = nullptr;
+    uint8_t *d_dbg = nullptr;
+
+    RegStat *d_rs = nullptr;
+    uint64_t rs_cap = 0;
+    DevRegion *d_tregs = nullptr;  // restore: descriptors built from an image table
+    uint64_t tregs_cap = 0;
+    DevStats *d_st = nullptr;
+    DevStats *h_st = nullptr;  // pinned
+
+    uint8_t *d_meta = nullptr;  // host path: image metadata [0, poff)
+    uint64_t meta_cap = 0;
+    uint8_t *d_ring[kRing] = {nullptr, nullptr, nullptr};
+    uint64_t ring_cap = 0;
+
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_gather[kRing];
+    cudaEvent_t ev_copy[kRing];
+    cudaEvent_t ev_t[6];
+    cudaEvent_t ev_meta;
+};
+
+namespace {
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) {                                                              \
+            set_detail("%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+            c->poisoned = true;                                                               \
+            return CRUM_E_CUDA;                                                               \
+        }                                                                                     \
+    } while (0)
+
+#define CK_LAUNCH()                                                                           \
+    do {                                                                                      \
+        cudaError_t e_ = cudaGetLastError();                                                  \
+        if (e_ != cudaSuccess) {                                                              \
+            set_detail("kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
+            c->poisoned = true;                                                               \
+            return CRUM_E_CUDA;                                                               \
+        }                                                                                     \
+    } while (0)
+
+#define ENTER(ctx)                                                                            \
+    crum_ctx *c = (ctx);                                                                      \
+    if (!c) {                                                                                 \
+        set_detail("null context");                                                           \
+        return CRUM_E_INVAL;                                                                  \
+    }                                                                                         \
+    if (c->poisoned) {                                                                        \
+        set_detail("context poisoned by an earlier CUDA error");                              \
+        return CRUM_E_CUDA;                                                                   \
+    }                                                                                         \
+    CK(cudaSetDevice(c->device))
+
+Launch launch_of(crum_ctx *c, cudaStream_t s) { return Launch{s, c->sms, &c->launches}; }
+
+uint64_t pad_pages(uint64_t n) { return round_up(n ? n : 1, kPagesPerCompactBlock); }
+
+template <typename T>
+int dev_alloc(crum_ctx *c, T **p, uint64_t bytes) {
+    void *q = nullptr;
+    cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_detail("cudaMalloc(%llu) failed: %s", (unsigned long long)bytes, cudaGetErrorString(e));
+        return CRUM_E_NOMEM;
+    }
+    *p = static_cast<T *>(q);
+    return CRUM_OK;
+}
+
+template <typename T>
+void dev_free(T *&p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+int upload(crum_ctx *c, void *dst, const void *src, uint64_t bytes) {
+    if (bytes) CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    return CRUM_OK;
+}
+
+// Rebuild device descriptors and per-page arrays after the registry changed.
+// `old_force_map`: for each new region index, the page base of that region's
+// force bits in the OLD force array (or UINT64_MAX for a new region -> all 1).
+int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
+    const uint32_t R = (uint32_t)c->regs.size();
+    std::vector<DevRegion> dr(R);
+    std::vector<uint32_t> cmp_idx, hash_idx;
+    std::vector<uint64_t> cmp_seg{0}, hash_grp{0};
+    uint64_t N = 0, F = 0;
+    bool any_hash = false;
+    for (uint32_t r = 0; r < R; ++r) {
+        const HostRegion &h = c->regs[r];
+        DevRegion &d = dr[r];
+        d.base = h.ptr;
+        d.mirror = h.mode == kModeCompare ? static_cast<uint8_t *>(h.shadow) : nullptr;
+        d.table = h.mode == kModeHash ? static_cast<uint64_t *>(h.shadow) : nullptr;
+        d.bytes = h.bytes;
+        d.page_base = N;
+        d.n_pages = h.n_pages;
+        d.log2p = h.log2p;
+        d.mode = h.mode;
+        d.id = h.id;
+        d.aligned32 = (reinterpret_cast<uintptr_t>(h.ptr) & 31) == 0;
+        if (h.mode == kModeCompare) {
+            cmp_idx.push_back(r);
+            cmp_seg.push_back(cmp_seg.back() + (h.bytes + kSegBytes - 1) / kSegBytes);
+        } else {
+            any_hash = true;
+            hash_idx.push_back(r);
+            hash_grp.push_back(hash_grp.back() + (h.log2p == 12 ? (h.n_pages + 1) / 2 : h.n_pages));
+        }
+        N += h.n_pages;
+        F += h.bytes;
+    }
+    // new per-page arrays
+    const uint64_t cap = pad_pages(N);
+    uint8_t *force = nullptr;
+    int st;
+    if ((st = dev_alloc(c, &force, cap))) return st;
+    CK(cudaMemset(force, 0, cap));
+    for (uint32_t r = 0; r < R; ++r) {
+        const uint64_t ob = old_force_base[r];
+        if (ob == UINT64_MAX) {
+            CK(cudaMemset(force + dr[r].page_base, 1, dr[r].n_pages));
+        } else {
+            CK(cudaMemcpy(force + dr[r].page_base, c->d_force + ob, dr[r].n_pages, cudaMemcpyDeviceToDevice));
+        }
+    }
+    if (cap > c->page_cap) {
+        dev_free(c->d_flags);
+        dev_free(c->d_newhash);
+        dev_free(c->d_gids);
+        dev_free(c->d_blk);
+        dev_free(c->d_dbg);
+        c->page_cap = 0;
+        if ((st = dev_alloc(c, &c->d_flags, cap)) || (st = dev_alloc(c, &c->d_newhash, cap * 8)) ||
+            (st = dev_alloc(c, &c->d_gids, cap * 4)) ||
+            (st = dev_alloc(c, &c->d_blk, (cap / kPagesPerCompactBlock) * 4 + 16)) ||
+            (st = dev_alloc(c, &c->d_dbg, cap))) {
+            cudaFree(force);
+            return st;
+        }
+        c->page_cap = cap;
+    }
+    CK(cudaMemset(c->d_flags, 0, c->page_cap));
+    dev_free(c->d_force);
+    c->d_force = force;
+    // descriptors
+    dev_free(c->d_regs);
+    dev_free(c->d_cmp_idx);
+    dev_free(c->d_cmp_seg);
+    dev_free(c->d_hash_idx);
+    dev_free(c->d_hash_grp);
+    if ((st = dev_alloc(c, &c->d_regs, sizeof(DevRegion) * R)) ||
+        (st = dev_alloc(c, &c->d_cmp_idx, 4 * cmp_idx.size())) ||
+        (st = dev_alloc(c, &c->d_cmp_seg, 8 * cmp_seg.size())) ||
+        (st = dev_alloc(c, &c->d_hash_idx, 4 * hash_idx.size())) ||
+        (st = dev_alloc(c, &c->d_hash_grp, 8 * hash_grp.size())))
+        return st;
+    if ((st = upload(c, c->d_regs, dr.data(), sizeof(DevRegion) * R)) ||
+        (st = upload(c, c->d_cmp_idx, cmp_idx.data(), 4 * cmp_idx.size())) ||
+        (st = upload(c, c->d_cmp_seg, cmp_seg.data(), 8 * cmp_seg.size())) ||
+        (st = upload(c, c->d_hash_idx, hash_idx.data(), 4 * hash_idx.size())) ||
+        (st = upload(c, c->d_hash_grp, hash_grp.data(), 8 * hash_grp.size())))
+        return st;
+    c->n_cmp = (uint32_t)cmp_idx.size();
+    c->n_seg = cmp_seg.back();
+    c->n_hash = (uint32_t)hash_idx.size();
+    c->n_grp = hash_grp.back();
+    c->any_hash = any_hash;
+    c->N = N;
+    c->F = F;
+    // per-region scratch and the host-path metadata buffer
+    if (R + 1 > c->rs_cap) {
+        dev_free(c->d_rs);
+        c->rs_cap = 0;
+        if ((st = dev_alloc(c, &c->d_rs, sizeof(RegStat) * (R + 1)))) return st;
+        c->rs_cap = R + 1;
+    }
+    const uint64_t meta_max = round_up(meta_bytes_for(R, N, any_hash), 4096);
+    if (meta_max > c->meta_cap) {
+        dev_free(c->d_meta);
+        c->meta_cap = 0;
+        if ((st = dev_alloc(c, &c->d_meta, meta_max))) return st;
+        c->meta_cap = meta_max;
+    }
+    return CRUM_OK;
+}
+
+int ensure_ring(crum_ctx *c) {
+    if (c->ring_cap >= c->chunk) return CRUM_OK;
+    for (int i = 0; i < kRing; ++i) dev_free(c->d_ring[i]);
+    c->ring_cap = 0;
+    for (int i = 0; i < kRing; ++i) {
+        int st = dev_alloc(c, &c->d_ring[i], c->chunk);
+        if (st) return st;
+    }
+    c->ring_cap = c->chunk;
+    return CRUM_OK;
+}
+
+HostRegion *find_region(crum_ctx *c, uint32_t id, uint32_t *index = nullptr) {
+    for (uint32_t r = 0; r < c->regs.size(); ++r)
+        if (c->regs[r].id == id) {
+            if (index) *index = r;
+            return &c->regs[r];
+        }
+    return nullptr;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+        cudaGetLastError();
+        return 0.f;
+    }
+    return ms;
+}
+
+// A1 + A2 + per-region stats (+ the image metadata and CRCs if meta_img).
+// Enqueued on s; nothing is committed.
+int enqueue_detect_compact(crum_ctx *c, cudaStream_t s, bool full, uint64_t capacity, bool timing) {
+    Launch L = launch_of(c, s);
+    const uint32_t R = (uint32_t)c->regs.size();
+    if (timing) CK(cudaEventRecord(c->ev_t[0], s));
+    CK(cudaMemsetAsync(c->d_flags, 0, pad_pages(c->N), s));
+    if (!full) launch_detect_compare(L, c->d_regs, c->d_cmp_idx, c->d_cmp_seg, c->n_cmp, c->n_seg, c->d_force,
+                                     c->d_flags);
+    launch_detect_hash(L, c->d_regs, c->d_hash_idx, c->d_hash_grp, c->n_hash, c->n_grp, c->d_flags,
+                       c->d_newhash);
+    CK_LAUNCH();
+    if (timing) CK(cudaEventRecord(c->ev_t[1], s));
+    launch_compact(L, c->d_flags, c->d_force, c->N, full ? 1 : 0, c->d_blk, c->d_gids, c->d_st);
+    launch_region_stats(L, c->d_regs, R, c->d_gids, c->d_rs, c->d_st, full ? 1 : 0, c->any_hash ? 1 : 0,
+                        capacity);
+    CK_LAUNCH();
+    return CRUM_OK;
+}
+
+int enqueue_meta(crum_ctx *c, cudaStream_t s, uint8_t *img) {
+    Launch L = launch_of(c, s);
+    const uint32_t R = (uint32_t)c->regs.size();
+    launch_meta(L, c->d_regs, R, c->d_gids, c->d_newhash, c->d_rs, c->d_st, img);
+    launch_crc_meta(L, img, c->d_st, crc_tables().x2n);
+    launch_header(L, img, c->d_st, crc_tables().x2n);
+    CK_LAUNCH();
+    return CRUM_OK;
+}
+
+void fill_report(crum_ctx *c, const DevStats &h, crum_report *rep) {
+    rep->scanned_pages = c->N;
+    rep->scanned_bytes = c->F;
+    rep->dirty_pages = h.K;
+    rep->dirty_bytes = h.dirty_bytes;
+    rep->dirty_runs = h.dirty_runs;
+    rep->image_bytes = h.image_bytes;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char *crum_status_string(int s) {
+    switch (s) {
+        case CRUM_OK: return "ok";
+        case CRUM_E_INVAL: return "invalid argument";
+        case CRUM_E_OVERLAP: return "region overlaps a live region";
+        case CRUM_E_NOREGION: return "unknown region id";
+        case CRUM_E_RANGE: return "range outside the region";
+        case CRUM_E_NOMEM: return "out of device or pinned memory";
+        case CRUM_E_CAPACITY: return "image buffer too small";
+        case CRUM_E_CORRUPT: return "corrupt image";
+        case CRUM_E_MISMATCH: return "image does not match the registered regions";
+        case CRUM_E_BUSY: return "busy";
+        case CRUM_E_DEVICE: return "pointer or device not usable";
+        case CRUM_E_CUDA: return "CUDA error";
+        default: return "unknown status";
+    }
+}
+
+const char *crum_last_error_detail(void) { return g_detail.c_str(); }
+
+uint64_t crum_launch_count(const crum_ctx *c) { return c ? c->launches : 0; }
+
+int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
+    if (!out) return CRUM_E_INVAL;
+    *out = nullptr;
+    if (cfg && (cfg->flags || cfg->reserved || (cfg->chunk_bytes % 4096))) {
+        set_detail("bad crum_config");
+        return CRUM_E_INVAL;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        set_detail("no CUDA device %d", device);
+        return CRUM_E_DEVICE;
+    }
+    crum_ctx *c = new (std::nothrow) crum_ctx();
+    if (!c) return CRUM_E_NOMEM;
+    c->device = device;
+    if (cfg && cfg->chunk_bytes) c->chunk = cfg->chunk_bytes;
+    auto fail = [&](int st) {
+        crum_destroy(c);
+        return st;
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return fail(CRUM_E_CUDA);
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess) return fail(CRUM_E_CUDA);
+    for (int i = 0; i < kRing; ++i) {
+        if (cudaEventCreateWithFlags(&c->ev_gather[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming) != cudaSuccess)
+            return fail(CRUM_E_CUDA);
+    }
+    for (int i = 0; i < 6; ++i)
+        if (cudaEventCreate(&c->ev_t[i]) != cudaSuccess) return fail(CRUM_E_CUDA);
+    if (cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
+    if (cudaMalloc(&c->d_st, sizeof(DevStats)) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    if (cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocDefault) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    cudaMemset(c->d_st, 0, sizeof(DevStats));
+    std::vector<uint64_t> none;
+    int st = rebuild(c, none);
+    if (st) return fail(st);
+    *out = c;
+    return CRUM_OK;
+}
+
+int crum_destroy(crum_ctx *c) {
+    if (!c) return CRUM_E_INVAL;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto &h : c->regs) cudaFree(h.shadow);
+    dev_free(c->d_regs);
+    dev_free(c->d_cmp_idx);
+    dev_free(c->d_cmp_seg);
+    dev_free(c->d_hash_idx);
+    dev_free(c->d_hash_grp);
+    dev_free(c->d_force);
+    dev_free(c->d_flags);
+    dev_free(c->d_newhash);
+    dev_free(c->d_gids);
+    dev_free(c->d_blk);
+    dev_free(c->d_dbg);
+    dev_free(c->d_rs);
+    dev_free(c->d_tregs);
+    dev_free(c->d_st);
+    dev_free(c->d_meta);
+    for (int i = 0; i < kRing; ++i) dev_free(c->d_ring[i]);
+    if (c->h_st) cudaFreeHost(c->h_st);
+    if (c->copy) cudaStreamDestroy(c->copy);
+    for (int i = 0; i < kRing; ++i) {
+        if (c->ev_gather[i]) cudaEventDestroy(c->ev_gather[i]);
+        if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
+    }
+    for (int i = 0; i < 6; ++i)
+        if (c->ev_t[i]) cudaEventDestroy(c->ev_t[i]);
+    if (c->ev_meta) cudaEventDestroy(c->ev_meta);
+    cudaGetLastError();
+    delete c;
+    return CRUM_OK;
+}
+
+int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page_size, uint32_t mode,
+                         uint32_t *region_id_out) {
+    ENTER(ctx);
+    if (!ptr || !region_id_out || bytes == 0) {
+        set_detail("null pointer or zero bytes");
+        return CRUM_E_INVAL;
+    }
+    if (page_size < 4096 || page_size > (2u << 20) || (page_size & (page_size - 1))) {
+        set_detail("page_size %llu not a power of two in [4096, 2 MiB]", (unsigned long long)page_size);
+        return CRUM_E_INVAL;
+    }
+    if (reinterpret_cast<uintptr_t>(ptr) % 16) {
+        set_detail("ptr not 16-byte aligned");
+        return CRUM_E_INVAL;
+    }
+    if (mode != CRUM_MODE_COMPARE && mode != CRUM_MODE_HASH_XXH3) {
+        set_detail("bad mode %u", mode);
+        return CRUM_E_INVAL;
+    }
+    const uint64_t n = bytes / page_size + (bytes % page_size != 0);
+    if (n > 0xffffffffull || c->N + n > kMaxTotalPages) {
+        set_detail("too many pages");
+        return CRUM_E_INVAL;
+    }
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(ptr), hi = lo + bytes;
+    if (hi < lo) return CRUM_E_INVAL;
+    // device accessibility of both ends
+    for (uintptr_t a : {lo, hi - 1}) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, reinterpret_cast<void *>(a)) != cudaSuccess) {
+            cudaGetLastError();
+            set_detail("pointer %p is not a CUDA pointer", reinterpret_cast<void *>(a));
+            return CRUM_E_DEVICE;
+        }
+        const bool ok = (at.type == cudaMemoryTypeManaged) ||
+                        (at.type == cudaMemoryTypeDevice && at.device == c->device);
+        if (!ok) {
+            set_detail("pointer %p is not device/managed memory of device %d", reinterpret_cast<void *>(a),
+                       c->device);
+            return CRUM_E_DEVICE;
+        }
+    }
+    for (const HostRegion &h : c->regs) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(h.ptr), b = a + h.bytes;
+        if (lo < b && a < hi) {
+            set_detail("overlaps region %u", h.id);
+            return CRUM_E_OVERLAP;
+        }
+    }
+    CK(cudaDeviceSynchronize());
+    HostRegion h{};
+    h.mode = mode;
+    h.ptr = static_cast<uint8_t *>(ptr);
+    h.bytes = bytes;
+    h.page_size = page_size;
+    h.n_pages = n;
+    h.log2p = (uint32_t)__builtin_ctzll(page_size);
+    const uint64_t shadow_bytes = mode == kModeCompare ? round_up(bytes, 256) : 8 * n;
+    int st = dev_alloc(c, &h.shadow, shadow_bytes);
+    if (st) return st;
+    CK(cudaMemset(h.shadow, 0, shadow_bytes));
+    // keep old force bits of existing regions, new region all-dirty
+    std::vector<uint64_t> old_base;
+    uint64_t pb = 0;
+    for (const HostRegion &o : c->regs) {
+        old_base.push_back(pb);
+        pb += o.n_pages;
+    }
+    old_base.push_back(UINT64_MAX);
+    h.id = c->next_id;
+    c->regs.push_back(h);
+    st = rebuild(c, old_base);
+    if (st) {
+        c->regs.pop_back();
+        cudaFree(h.shadow);
+        return st;
+    }
+    c->next_id++;
+    *region_id_out = h.id;
+    return CRUM_OK;
+}
+
+int crum_unregister_region(crum_ctx *ctx, uint32_t id) {
+    ENTER(ctx);
+    uint32_t idx;
+    if (!find_region(c, id, &idx)) {
+        set_detail("no region %u", id);
+        return CRUM_E_NOREGION;
+    }
+    CK(cudaDeviceSynchronize());
+    std::vector<uint64_t> old_base;
+    uint64_t pb = 0;
+    for (uint32_t r = 0; r < c->regs.size(); ++r) {
+        if (r != idx) old_base.push_back(pb);
+        pb += c->regs[r].n_pages;
+    }
+    HostRegion gone = c->regs[idx];
+    c->regs.erase(c->regs.begin() + idx);
+    int st = rebuild(c, old_base);
+    if (st) return st;
+    cudaFree(gone.shadow);
+    return CRUM_OK;
+}
+
+int crum_mark_dirty(crum_ctx *ctx, uint32_t id, uint64_t off, uint64_t len) {
+    ENTER(ctx);
+    uint32_t idx;
+    HostRegion *h = find_region(c, id, &idx);
+    if (!h) {
+        set_detail("no region %u", id);
+        return CRUM_E_NOREGION;
+    }
+    if (off > h->bytes || len > h->bytes - off) {
+        set_detail("range [%llu, +%llu) outside region of %llu bytes", (unsigned long long)off,
+                   (unsigned long long)len, (unsigned long long)h->bytes);
+        return CRUM_E_RANGE;
+    }
+    if (!len) return CRUM_OK;
+    uint64_t pb = 0;
+    for (uint32_t r = 0; r < idx; ++r) pb += c->regs[r].n_pages;
+    const uint64_t i0 = off / h->page_size, i1 = (off + len - 1) / h->page_size;
+    // device-synchronous: ordered after every earlier call on any stream and
+    // visible to every later one
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemset(c->d_force + pb + i0, 1, i1 - i0 + 1));
+    CK(cudaDeviceSynchronize());
+    return CRUM_OK;
+}
+
+int crum_image_required_bytes(crum_ctx *ctx, uint64_t max_dirty, uint64_t *out) {
+    ENTER(ctx);
+    if (!out) return CRUM_E_INVAL;
+    const uint64_t K = std::min(max_dirty, c->N);
+    uint64_t payload = 0, maxp = 0;
+    for (const HostRegion &h : c->regs) {
+        payload += h.n_pages * h.page_size;
+        maxp = std::max(maxp, h.page_size);
+    }
+    if (K < c->N && K * maxp < payload) payload = K * maxp;
+    *out = round_up(meta_bytes_for(c->regs.size(), K, c->any_hash), 4096) + payload;
+    return CRUM_OK;
+}
+
+int crum_image_create(crum_ctx *ctx, uint64_t cap, crum_image **out) {
+    ENTER(ctx);
+    if (!out) return CRUM_E_INVAL;
+    crum_image *im = new (std::nothrow) crum_image{nullptr, cap, 0, c->device};
+    if (!im) return CRUM_E_NOMEM;
+    if (cudaHostAlloc(reinterpret_cast<void **>(&im->host), cap ? cap : 1, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        delete im;
+        set_detail("cudaHostAlloc(%llu) failed", (unsigned long long)cap);
+        return CRUM_E_NOMEM;
+    }
+    *out = im;
+    return CRUM_OK;
+}
+
+int crum_image_import(crum_ctx *ctx, const void *bytes, uint64_t len, crum_image **out) {
+    if (!bytes && len) return CRUM_E_INVAL;
+    int st = crum_image_create(ctx, len, out);
+    if (st) return st;
+    if (len) memcpy((*out)->host, bytes, len);
+    (*out)->len = len;
+    return CRUM_OK;
+}
+
+int crum_image_data(const crum_image *img, void **data, uint64_t *len, uint64_t *cap) {
+    if (!img || !data || !len) return CRUM_E_INVAL;
+    *data = img->host;
+    *len = img->len;
+    if (cap) *cap = img->cap;
+    return CRUM_OK;
+}
+
+int crum_image_destroy(crum_image *img) {
+    if (!img) return CRUM_E_INVAL;
+    cudaSetDevice(img->device);
+    cudaFreeHost(img->host);
+    delete img;
+    return CRUM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// A7: sync shadow
+// ---------------------------------------------------------------------------
+int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
+    ENTER(ctx);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int st = enqueue_detect_compact(c, s, false, UINT64_MAX, false);
+    if (st) return st;
+    Launch L = launch_of(c, s);
+    // commit every listed page: at most every page's units
+    uint64_t max_units = 0;
+    for (const HostRegion &h : c->regs) max_units += h.n_pages * (h.page_size >> kSegLog2);
+    launch_gather(L, c->d_regs, (uint32_t)c->regs.size(), c->d_gids, c->d_newhash, c->d_rs, c->d_st, nullptr, 0,
+                  0, c->d_force, 0, max_units);
+    CK_LAUNCH();
+    if (dirty_out) {
+        CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        *dirty_out = c->h_st->K;
+    }
+    return CRUM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// A1-A3 into a device image
+// ---------------------------------------------------------------------------
+int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capacity, void *stream,
+                                  uint32_t flags, crum_report *rep) {
+    ENTER(ctx);
+    if (!dev_image || (flags & ~CRUM_FULL) || (reinterpret_cast<uintptr_t>(dev_image) & 255)) {
+        set_detail("bad device image pointer (must be 256-byte aligned) or flags");
+        return CRUM_E_INVAL;
+    }
+    if (!rep) {
+        uint64_t need;
+        crum_image_required_bytes(c, UINT64_MAX, &need);
+        if (capacity < need) {
+            set_detail("asynchronous device gather needs capacity >= %llu", (unsigned long long)need);
+            return CRUM_E_CAPACITY;
+        }
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool full = flags & CRUM_FULL;
+    const bool timing = rep != nullptr;
+    uint8_t *img = static_cast<uint8_t *>(dev_image);
+    int st = enqueue_detect_compact(c, s, full, capacity, timing);
+    if (st) return st;
+    if ((st = enqueue_meta(c, s, img))) return st;
+    if (timing) CK(cudaEventRecord(c->ev_t[2], s));
+    uint64_t max_units = 0;
+    for (const HostRegion &h : c->regs) max_units += h.n_pages * (h.page_size >> kSegLog2);
+    Launch L = launch_of(c, s);
+    launch_gather(L, c->d_regs, (uint32_t)c->regs.size(), c->d_gids, c->d_newhash, c->d_rs, c->d_st, img, 0, 1,
+                  c->d_force, 0, max_units);
+    CK_LAUNCH();
+    if (timing) {
+        CK(cudaEventRecord(c->ev_t[3], s));
+        CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const DevStats h = *c->h_st;
+        memset(rep, 0, sizeof *rep);
+        fill_report(c, h, rep);
+        rep->t_detect_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
+        rep->t_compact_ms = ev_ms(c->ev_t[1], c->ev_t[2]);
+        rep->t_gather_ms = ev_ms(c->ev_t[2], c->ev_t[3]);
+        rep->t_total_ms = ev_ms(c->ev_t[0], c->ev_t[3]);
+        if (h.status == kStCapacity) {
+            set_detail("image needs %llu bytes, capacity %llu", (unsigned long long)h.image_bytes,
+                       (unsigned long long)capacity);
+            return CRUM_E_CAPACITY;
+        }
+    }
+    return CRUM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// A1-A4 into a pinned host image: metadata on the device, payload gathered
+// chunk by chunk into a device ring and copied D2H on the copy stream.
+// ---------------------------------------------------------------------------
+int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_t flags, crum_report *rep) {
+    ENTER(ctx);
+    if (!img || (flags & ~CRUM_FULL)) {
+        set_detail("null image or bad flags");
+        return CRUM_E_INVAL;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool full = flags & CRUM_FULL;
+    int st = ensure_ring(c);
+    if (st) return st;
+    if ((st = enqueue_detect_compact(c, s, full, UINT64_MAX, true))) return st;
+    if ((st = enqueue_meta(c, s, c->d_meta))) return st;
+    CK(cudaEventRecord(c->ev_t[2], s));
+    CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const DevStats h = *c->h_st;
+    if (h.image_bytes > img->cap) {
+        if (rep) {
+            memset(rep, 0, sizeof *rep);
+            fill_report(c, h, rep);
+        }
+        set_detail("image needs %llu bytes, capacity %llu", (unsigned long long)h.image_bytes,
+                   (unsigned long long)img->cap);
+        return CRUM_E_CAPACITY;
+    }
+    // metadata (with zero padding up to poff) -> host
+    CK(cudaEventRecord(c->ev_meta, s));
+    CK(cudaStreamWaitEvent(c->copy, c->ev_meta, 0));
+    CK(cudaEventRecord(c->ev_t[4], c->copy));
+    CK(cudaMemcpyAsync(img->host, c->d_meta, h.poff, cudaMemcpyDeviceToHost, c->copy));
+    // payload chunks
+    Launch L = launch_of(c, s);
+    const uint64_t units_per_chunk = c->chunk >> kSegLog2;
+    const uint32_t R = (uint32_t)c->regs.size();
+    uint64_t chunk_idx = 0;
+    for (uint64_t u0 = 0; u0 < h.total_units; u0 += units_per_chunk, ++chunk_idx) {
+        const uint64_t u1 = std::min(h.total_units, u0 + units_per_chunk);
+        const int slot = (int)(chunk_idx % kRing);
+        if (chunk_idx >= (uint64_t)kRing) CK(cudaStreamWaitEvent(s, c->ev_copy[slot], 0));
+        launch_gather(L, c->d_regs, R, c->d_gids, c->d_newhash, c->d_rs, c->d_st, c->d_ring[slot], u0, 0,
+                      c->d_force, u0, u1);
+        CK_LAUNCH();
+        CK(cudaEventRecord(c->ev_gather[slot], s));
+        CK(cudaStreamWaitEvent(c->copy, c->ev_gather[slot], 0));
+        CK(cudaMemcpyAsync(img->host + h.poff + (u0 << kSegLog2), c->d_ring[slot], (u1 - u0) << kSegLog2,
+                           cudaMemcpyDeviceToHost, c->copy));
+        CK(cudaEventRecord(c->ev_copy[slot], c->copy));
+    }
+    CK(cudaEventRecord(c->ev_t[3], s));
+    CK(cudaEventRecord(c->ev_t[5], c->copy));
+    CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(c->copy));
+    img->len = h.image_bytes;
+    if (rep) {
+        memset(rep, 0, sizeof *rep);
+        fill_report(c, *c->h_st, rep);
+        rep->t_detect_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
+        rep->t_compact_ms = ev_ms(c->ev_t[1], c->ev_t[2]);
+        rep->t_gather_ms = ev_ms(c->ev_t[2], c->ev_t[3]);
+        rep->t_copy_ms = ev_ms(c->ev_t[4], c->ev_t[5]);
+        rep->t_total_ms = ev_ms(c->ev_t[0], c->ev_t[5]);
+    }
+    return CRUM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// A6: restore scatter
+// ---------------------------------------------------------------------------
+namespace {
+
+struct ParsedImage {
+    uint32_t flags, R;
+    uint64_t K, meta, poff, payload;
+    std::vector<RegStat> rs;
+    std::vector<DevRegion> tregs;
+};
+
+// Host-side checks of the header and region table (all CORRUPT conditions
+// that do not need the id list), then the live-set comparison is done by the
+// caller AFTER the device checks.  hdr: 64 bytes; tab: 48 * R bytes.
+int parse_header(const uint8_t *hdr, uint64_t len, ParsedImage &p) {
+    if (len < 64 || memcmp(hdr, "CRUM", 4) != 0) return CRUM_E_CORRUPT;
+    if (crc32_host(hdr, 60) != rd32(hdr + 60)) return CRUM_E_CORRUPT;
+    const uint32_t version = rd32(hdr + 4);
+    p.flags = rd32(hdr + 8);
+    p.R = rd32(hdr + 12);
+    p.K = rd64(hdr + 16);
+    p.meta = rd64(hdr + 24);
+    p.poff = rd64(hdr + 32);
+    p.payload = rd64(hdr + 40);
+    if (version != 1 || (p.flags & ~3u) || rd64(hdr + 52) != 0) return CRUM_E_CORRUPT;
+    if (p.K > kMaxTotalPages || p.R > 0x7fffffffu) return CRUM_E_CORRUPT;
+    if (p.meta != meta_bytes_for(p.R, p.K, p.flags & 2u) || p.poff != round_up(p.meta, 4096)) return CRUM_E_CORRUPT;
+    if (len < p.poff || len - p.poff < p.payload) return CRUM_E_CORRUPT;
+    return CRUM_OK;
+}
+
+int parse_table(const uint8_t *tab, ParsedImage &p) {
+    p.rs.assign(p.R, RegStat{});
+    p.tregs.assign(p.R, DevRegion{});
+    uint64_t sum = 0, pay = 0;
+    bool any_hash = false;
+    for (uint32_t k = 0; k < p.R; ++k) {
+        const uint8_t *e = tab + 48ull * k;
+        const uint32_t mode = rd32(e + 4);
+        const uint64_t bytes = rd64(e + 8), ps = rd64(e + 16), np = rd64(e + 24), nd = rd64(e + 32),
+                       first = rd64(e + 40);
+        if (mode > 1 || ps < 4096 || ps > (2u << 20) || (ps & (ps - 1)) || bytes == 0) return CRUM_E_CORRUPT;
+        if (np != bytes / ps + (bytes % ps != 0) || nd > np || first != sum) return CRUM_E_CORRUPT;
+        if ((p.flags & 1u) && nd != np) return CRUM_E_CORRUPT;
+        if (mode == 1) any_hash = true;
+        p.rs[k].first = first;
+        p.rs[k].n_dirty = nd;
+        p.rs[k].payload_base = pay;
+        p.rs[k].unit_base = pay >> kSegLog2;
+        DevRegion &d = p.tregs[k];
+        d.bytes = bytes;
+        d.n_pages = np;
+        d.log2p = (uint32_t)__builtin_ctzll(ps);
+        d.mode = mode;
+        d.id = rd32(e);
+        sum += nd;
+        pay += nd * ps;
+    }
+    if (sum != p.K || pay != p.payload || any_hash != ((p.flags & 2u) != 0)) return CRUM_E_CORRUPT;
+    return CRUM_OK;
+}
+
+int check_live(crum_ctx *c, const uint8_t *tab, const ParsedImage &p) {
+    if (p.R != c->regs.size()) return CRUM_E_MISMATCH;
+    for (uint32_t k = 0; k < p.R; ++k) {
+        const uint8_t *e = tab + 48ull * k;
+        const HostRegion &h = c->regs[k];
+        if (rd32(e) != h.id || rd32(e + 4) != h.mode || rd64(e + 8) != h.bytes || rd64(e + 16) != h.page_size ||
+            rd64(e + 24) != h.n_pages)
+            return CRUM_E_MISMATCH;
+    }
+    return CRUM_OK;
+}
+
+// Common restore body.  host_img != nullptr: image in pinned host memory
+// (payload goes H2D in chunks); else dev_img holds the whole image.
+int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img, uint64_t len, cudaStream_t s,
+                   uint32_t flags, crum_report *rep) {
+    ParsedImage p;
+    uint8_t hdr[64];
+    if (len < 64) {
+        set_detail("image shorter than its header");
+        return CRUM_E_CORRUPT;
+    }
+    if (host_img) {
+        memcpy(hdr, host_img, 64);
+    } else {
+        CK(cudaMemcpyAsync(hdr, dev_img, 64, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    int st = parse_header(hdr, len, p);
+    if (st) {
+        set_detail("bad image header");
+        return st;
+    }
+    std::vector<uint8_t> tab(48ull * p.R);
+    if (p.R) {
+        if (host_img) {
+            memcpy(tab.data(), host_img + 64, tab.size());
+        } else {
+            CK(cudaMemcpyAsync(tab.data(), dev_img + 64, tab.size(), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+    }
+    if ((st = parse_table(tab.data(), p))) {
+        set_detail("bad image region table");
+        return st;
+    }
+    const bool timing = rep != nullptr;
+    if (timing) CK(cudaEventRecord(c->ev_t[0], s));
+    // metadata on the device
+    const uint8_t *meta = dev_img;
+    if (host_img) {
+        if (p.meta > c->meta_cap) {
+            dev_free(c->d_meta);
+            c->meta_cap = 0;
+            if ((st = dev_alloc(c, &c->d_meta, round_up(p.meta, 4096)))) return st;
+            c->meta_cap = round_up(p.meta, 4096);
+        }
+        CK(cudaMemcpyAsync(c->d_meta, host_img, p.meta, cudaMemcpyHostToDevice, s));
+        meta = c->d_meta;
+    }
+    if (p.R + 1 > c->rs_cap) {
+        dev_free(c->d_rs);
+        c->rs_cap = 0;
+        if ((st = dev_alloc(c, &c->d_rs, sizeof(RegStat) * (p.R + 1)))) return st;
+        c->rs_cap = p.R + 1;
+    }
+    if (p.R > c->tregs_cap) {
+        dev_free(c->d_tregs);
+        c->tregs_cap = 0;
+        if ((st = dev_alloc(c, &c->d_tregs, sizeof(DevRegion) * p.R))) return st;
+        c->tregs_cap = p.R;
+    }
+    DevStats hs{};
+    hs.K = p.K;
+    hs.meta_bytes = p.meta;
+    hs.poff = p.poff;
+    hs.payload_bytes = p.payload;
+    hs.image_bytes = p.poff + p.payload;
+    hs.total_units = p.payload >> kSegLog2;
+    hs.img_flags = p.flags;
+    hs.n_regions = p.R;
+    *c->h_st = hs;
+    CK(cudaMemcpyAsync(c->d_st, c->h_st, sizeof(DevStats), cudaMemcpyHostToDevice, s));
+    if (p.R) {
+        CK(cudaMemcpyAsync(c->d_rs, p.rs.data(), sizeof(RegStat) * p.R, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(c->d_tregs, p.tregs.data(), sizeof(DevRegion) * p.R, cudaMemcpyHostToDevice, s));
+    }
+    Launch L = launch_of(c, s);
+    launch_crc_meta(L, meta, c->d_st, crc_tables().x2n);
+    launch_restore_validate(L, c->d_tregs, p.R, c->d_rs, meta, c->d_st);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    {
+        const DevStats h = *c->h_st;
+        const uint64_t mlen = p.meta - 64;
+        const uint32_t meta_crc = h.crc_acc ^ gf2_mulmod_host(0xffffffffu, xpow8n_host(mlen)) ^ 0xffffffffu;
+        if (meta_crc != rd32(hdr + 48) || h.status != kStOk) {
+            set_detail(meta_crc != rd32(hdr + 48) ? "metadata CRC mismatch" : "bad page id list");
+            return CRUM_E_CORRUPT;
+        }
+    }
+    if ((st = check_live(c, tab.data(), p))) {
+        set_detail("image region table does not match the registered regions");
+        return st;
+    }
+    // CRUM_VERIFY: hash every hash-mode slot before writing anything
+    uint8_t *d_payload_tmp = nullptr;
+    const uint8_t *payload_dev = dev_img;  // with add_poff
+    int add_poff = 1;
+    if ((flags & CRUM_VERIFY) && c->any_hash && p.K) {
+        if (host_img) {
+            if ((st = dev_alloc(c, &d_payload_tmp, p.payload))) return st;
+            CK(cudaMemcpyAsync(d_payload_tmp, host_img + p.poff, p.payload, cudaMemcpyHostToDevice, s));
+            payload_dev = d_payload_tmp;
+            add_poff = 0;
+        }
+        launch_verify_hash(L, c->d_regs, p.R, c->d_rs, meta, payload_dev, add_poff, c->d_st);
+        CK_LAUNCH();
+        CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (c->h_st->status != kStOk) {
+            cudaFree(d_payload_tmp);
+            set_detail("CRUM_VERIFY: a hash-mode slot does not match its listed hash");
+            return CRUM_E_CORRUPT;
+        }
+    }
+    if (timing) CK(cudaEventRecord(c->ev_t[1], s));
+    const uint64_t units = p.payload >> kSegLog2;
+    if (!host_img || d_payload_tmp) {
+        launch_scatter(L, c->d_regs, p.R, c->d_rs, meta, c->d_st, payload_dev, 0, add_poff, c->d_force, 0, units);
+        CK_LAUNCH();
+        if (timing) {
+            CK(cudaEventRecord(c->ev_t[4], s));
+            CK(cudaEventRecord(c->ev_t[5], s));
+        }
+    } else {
+        if ((st = ensure_ring(c))) return st;
+        const uint64_t upc = c->chunk >> kSegLog2;
+        uint64_t ci = 0;
+        CK(cudaEventRecord(c->ev_meta, s));
+        CK(cudaStreamWaitEvent(c->copy, c->ev_meta, 0));
+        if (timing) CK(cudaEventRecord(c->ev_t[4], c->copy));
+        for (uint64_t u0 = 0; u0 < units; u0 += upc, ++ci) {
+            const uint64_t u1 = std::min(units, u0 + upc);
+            const int slot = (int)(ci % kRing);
+            if (ci >= (uint64_t)kRing) CK(cudaStreamWaitEvent(c->copy, c->ev_gather[slot], 0));
+            CK(cudaMemcpyAsync(c->d_ring[slot], host_img + p.poff + (u0 << kSegLog2), (u1 - u0) << kSegLog2,
+                               cudaMemcpyHostToDevice, c->copy));
+            CK(cudaEventRecord(c->ev_copy[slot], c->copy));
+            CK(cudaStreamWaitEvent(s, c->ev_copy[slot], 0));
+            launch_scatter(L, c->d_regs, p.R, c->d_rs, meta, c->d_st, c->d_ring[slot], u0, 0, c->d_force, u0, u1);
+            CK_LAUNCH();
+            CK(cudaEventRecord(c->ev_gather[slot], s));
+        }
+        if (timing) CK(cudaEventRecord(c->ev_t[5], c->copy));
+    }
+    if (timing) CK(cudaEventRecord(c->ev_t[3], s));
+    CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(c->copy));
+    if (d_payload_tmp) cudaFree(d_payload_tmp);
+    if (rep) {
+        memset(rep, 0, sizeof *rep);
+        fill_report(c, *c->h_st, rep);
+        rep->image_bytes = p.poff + p.payload;
+        rep->t_compact_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
+        rep->t_gather_ms = ev_ms(c->ev_t[1], c->ev_t[3]);
+        rep->t_copy_ms = ev_ms(c->ev_t[4], c->ev_t[5]);
+        rep->t_total_ms = ev_ms(c->ev_t[0], c->ev_t[3]);
+    }
+    return CRUM_OK;
+}
+
+}  // namespace
+
+int crum_restore_scatter(crum_ctx *ctx, const crum_image *img, void *stream, uint32_t flags, crum_report *rep) {
+    ENTER(ctx);
+    if (!img || (flags & ~CRUM_VERIFY)) {
+        set_detail("null image or bad flags");
+        return CRUM_E_INVAL;
+    }
+    return restore_common(c, img->host, nullptr, img->len, static_cast<cudaStream_t>(stream), flags, rep);
+}
+
+int crum_restore_scatter_device(crum_ctx *ctx, const void *dev_image, uint64_t len, void *stream, uint32_t flags,
+                                crum_report *rep) {
+    ENTER(ctx);
+    if (!dev_image || (flags & ~CRUM_VERIFY) || (reinterpret_cast<uintptr_t>(dev_image) & 255)) {
+        set_detail("bad device image pointer (must be 256-byte aligned) or flags");
+        return CRUM_E_INVAL;
+    }
+    return restore_common(c, nullptr, static_cast<const uint8_t *>(dev_image), len,
+                          static_cast<cudaStream_t>(stream), flags, rep);
+}
+
+// ---------------------------------------------------------------------------
+// test hooks
+// ---------------------------------------------------------------------------
+int crum_debug_detect(crum_ctx *ctx, void *stream, uint8_t *host_flags, uint64_t n) {
+    ENTER(ctx);
+    if (!host_flags || n != c->N) {
+        set_detail("host_flags must hold exactly %llu pages", (unsigned long long)c->N);
+        return CRUM_E_INVAL;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Launch L = launch_of(c, s);
+    CK(cudaMemsetAsync(c->d_flags, 0, pad_pages(c->N), s));
+    launch_detect_compare(L, c->d_regs, c->d_cmp_idx, c->d_cmp_seg, c->n_cmp, c->n_seg, c->d_force, c->d_flags);
+    launch_detect_hash(L, c->d_regs, c->d_hash_idx, c->d_hash_grp, c->n_hash, c->n_grp, c->d_flags,
+                       c->d_newhash);
+    launch_export_flags(L, c->d_flags, c->d_force, c->N, c->d_dbg);
+    CK_LAUNCH();
+    if (n) CK(cudaMemcpyAsync(host_flags, c->d_dbg, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return CRUM_OK;
+}
+
+int crum_debug_export(crum_ctx *ctx, uint32_t id, int what, void *host_buf, uint64_t len) {
+    ENTER(ctx);
+    uint32_t idx;
+    HostRegion *h = find_region(c, id, &idx);
+    if (!h) return CRUM_E_NOREGION;
+    if (!host_buf) return CRUM_E_INVAL;
+    CK(cudaDeviceSynchronize());
+    uint64_t pb = 0;
+    for (uint32_t r = 0; r < idx; ++r) pb += c->regs[r].n_pages;
+    switch (what) {
+        case CRUM_EXPORT_FORCE:
+            if (len != h->n_pages) return CRUM_E_INVAL;
+            CK(cudaMemcpy(host_buf, c->d_force + pb, len, cudaMemcpyDeviceToHost));
+            return CRUM_OK;
+        case CRUM_EXPORT_HASHES:
+            if (h->mode != kModeHash || len != 8 * h->n_pages) return CRUM_E_INVAL;
+            CK(cudaMemcpy(host_buf, h->shadow, len, cudaMemcpyDeviceToHost));
+            return CRUM_OK;
+        case CRUM_EXPORT_MIRROR:
+            if (h->mode != kModeCompare || len != h->bytes) return CRUM_E_INVAL;
+            CK(cudaMemcpy(host_buf, h->shadow, len, cudaMemcpyDeviceToHost));
+            return CRUM_OK;
+        default:
+            return CRUM_E_INVAL;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// synth.cu -- device implementation of the seeded input recipe of
+// synth/__init__.py (bench/test inputs only; holds none of the method).
+#include "crum_internal.cuh"
+#include "../../include/crum.h"
+#include "../../include/crum_synth.h"
+
+namespace crum {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_synth_fill(uint8_t *p, uint64_t bytes, uint64_t seed, uint64_t r, uint64_t woff) {
+    const uint64_t nw = bytes / 8;
+    const uint64_t key = seed ^ (r << 40);
+    uint64_t *w = reinterpret_cast<uint64_t *>(p);
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nw;
+         j += (uint64_t)gridDim.x * blockDim.x)
+        w[j] = splitmix64(key ^ (woff + j));
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (bytes & 7)) {
+        const uint64_t v = splitmix64(key ^ (woff + nw));
+        for (uint64_t b = nw * 8; b < bytes; ++b) p[b] = (uint8_t)(v >> (8 * (b - nw * 8)));
+    }
+}
+
+// One block per listed page.
+__global__ void k_synth_write(uint8_t *p, uint64_t bytes, uint64_t page_size, const uint32_t *pages,
+                              uint64_t seed, uint64_t epoch, uint64_t r, int touch) {
+    const uint64_t i = pages[blockIdx.x];
+    const uint64_t m = splitmix64((seed + 2) ^ (epoch << 56) ^ (r << 40) ^ i) | 1ull;
+    const uint64_t lo = i * page_size;
+    const uint64_t hi = min(lo + page_size, bytes);
+    const uint64_t nfull = (hi - lo) / 8;
+    uint64_t *w = reinterpret_cast<uint64_t *>(p + lo);
+    if (touch) {
+        if (threadIdx.x == 0) {
+            const uint64_t wlo = lo + ((hi - lo - 1) / 8) * 8;
+            for (uint64_t b = wlo; b < hi; ++b) p[b] ^= (uint8_t)(m >> (8 * (b - wlo)));
+        }
+        return;
+    }
+    for (uint64_t j = threadIdx.x; j < nfull; j += blockDim.x) w[j] ^= m;
+    if (threadIdx.x == 0)
+        for (uint64_t b = lo + nfull * 8; b < hi; ++b) p[b] ^= (uint8_t)(m >> (8 * (b - lo - nfull * 8)));
+}
+
+__global__ void k_scrub(uint4 *p, uint64_t n) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (uint64_t)gridDim.x * blockDim.x)
+        p[j] = make_uint4((uint32_t)j, 0, 0, 0);
+}
+
+void launch_synth_fill(cudaStream_t s, uint8_t *p, uint64_t bytes, uint64_t seed, uint64_t r,
+                       uint64_t woff) {
+    k_synth_fill<<<148 * 8, 256, 0, s>>>(p, bytes, seed, r, woff);
+}
+void launch_synth_write(cudaStream_t s, uint8_t *p, uint64_t bytes, uint64_t page_size,
+                        const uint32_t *pages, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t r,
+                        int touch) {
+    for (uint64_t b0 = 0; b0 < n; b0 += (1u << 30))
+        k_synth_write<<<(unsigned)min(n - b0, (uint64_t)1 << 30), 256, 0, s>>>(p, bytes, page_size, pages + b0,
+                                                                          seed, epoch, r, touch);
+}
+void launch_synth_scrub(cudaStream_t s, uint8_t *p, uint64_t bytes) {
+    k_scrub<<<148 * 8, 256, 0, s>>>(reinterpret_cast<uint4 *>(p), bytes / 16);
+}
+
+}  // namespace crum
+
+extern "C" int crum_synth_fill(void *dev_ptr, uint64_t bytes, uint64_t seed, uint64_t region_index,
+                               uint64_t word_offset, void *stream) {
+    if (!dev_ptr || (reinterpret_cast<uintptr_t>(dev_ptr) & 7)) return CRUM_E_INVAL;
+    if (!bytes) return CRUM_OK;
+    crum::launch_synth_fill((cudaStream_t)stream, (uint8_t *)dev_ptr, bytes, seed, region_index, word_offset);
+    return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
+}
+
+extern "C" int crum_synth_write_pages(void *dev_ptr, uint64_t bytes, uint64_t page_size,
+                                      const uint32_t *dev_pages, uint64_t n_pages, uint64_t seed,
+                                      uint64_t epoch, uint64_t region_index, int touch, void *stream) {
+    if (!dev_ptr || (reinterpret_cast<uintptr_t>(dev_ptr) & 7) || (page_size & 7) || !page_size)
+        return CRUM_E_INVAL;
+    if (!n_pages) return CRUM_OK;
+    if (!dev_pages) return CRUM_E_INVAL;
+    crum::launch_synth_write((cudaStream_t)stream, (uint8_t *)dev_ptr, bytes, page_size, dev_pages, n_pages,
+                             seed, epoch, region_index, touch);
+    return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
+}
+
+extern "C" int crum_synth_scrub(void *dev_ptr, uint64_t bytes, void *stream) {
+    if (!dev_ptr || (reinterpret_cast<uintptr_t>(dev_ptr) & 15)) return CRUM_E_INVAL;
+    crum::launch_synth_scrub((cudaStream_t)stream, (uint8_t *)dev_ptr, bytes);
+    return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
+}

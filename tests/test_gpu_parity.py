@@ -1,0 +1,310 @@
+"""GPU parity: libcrum.so (through the C ABI) vs the CPU oracle, element by
+element on the same seeded inputs (bit-exact: flags, ids, hashes, image
+bytes, restored regions, snapshots).  Sizes span several tiles and ragged
+tails; the C2 (1 GiB) case runs in the launch configuration bench.py times."""
+import numpy as np
+import pytest
+import xxhash
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+KiB, MiB, GiB = 1 << 10, 1 << 20, 1 << 30
+C, H = 0, 1
+
+MIXED = [
+    (4 * MiB, 4 * KiB, C),                 # C1 shape
+    (3 * 64 * KiB + 1234, 64 * KiB, H),    # ragged tail, hash
+    (5 * 4 * KiB + 17, 4 * KiB, H),        # odd page count at 4 KiB (two pages per warp)
+    (2 * MiB + 4 * KiB + 100, 2 * MiB, C),  # 2 MiB pages, tiny tail page
+    (2 * MiB * 2 + 300, 2 * MiB, H),
+    (12 * KiB + 256, 4 * KiB, C),          # HPGMG-like small box region
+    (64 * KiB * 7, 64 * KiB, C),
+]
+
+
+@pytest.fixture(scope="module")
+def crum():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1808_00117_b200 import crum as m
+    assert torch.cuda.is_available()
+    return m
+
+
+def mkpair(specs, seed_idx, **kw):
+    from tests.gpu_pair import Pair
+    return Pair(specs, synth.seed(seed_idx), **kw)
+
+
+def test_synth_device_matches_numpy(crum):
+    for nb in (8, 13, 4096, 65536 + 5):
+        d = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        crum.synth_fill(d, nb, synth.seed(1), 3)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy(), synth.region_content(synth.seed(1), 3, nb))
+
+
+@pytest.mark.parametrize("misalign", [0, 16])
+def test_detect_parity_mixed(crum, misalign):
+    p = mkpair(MIXED, 10, misalign=misalign)
+    assert p.g.debug_detect(p.N).tolist() == [1] * p.N       # all force-dirty at register
+    assert np.array_equal(p.g.debug_detect(p.N), p.oracle_flags())
+    assert p.g.sync_shadow() == p.o.sync_shadow() == p.N
+    assert p.shadows_equal()
+    assert p.g.sync_shadow() == 0 and p.o.sync_shadow() == 0
+    for epoch, d in ((1, 0.1), (2, 0.5), (3, 1.0), (4, 0.0)):
+        p.write(epoch, d)
+        assert p.regions_equal()
+        want = p.oracle_flags()
+        assert np.array_equal(p.g.debug_detect(p.N), want), epoch
+        assert p.g.sync_shadow() == p.o.sync_shadow() == int(want.sum())
+        assert p.shadows_equal()
+    p.write(5, 0.3, touch=True)                               # one word per page
+    assert np.array_equal(p.g.debug_detect(p.N), p.oracle_flags())
+
+
+def test_exhaustive_single_byte_flips(crum):
+    for mode in (C, H):
+        p = mkpair([(2 * 4096, 4096, mode)], 11)
+        p.g.sync_shadow()
+        d = p.dev[0]
+        step = 1 if mode == C else 5
+        for pos in range(0, 8192, step):
+            d[pos] ^= 1
+            f = p.g.debug_detect(2)
+            assert f.tolist() == [int(pos < 4096), int(pos >= 4096)], (mode, pos)
+            d[pos] ^= 1
+
+
+def test_hash_table_matches_library(crum):
+    specs = [(3 * 64 * KiB + 999, 64 * KiB, H), (2 * MiB + 5, 2 * MiB, H), (9 * 4096 + 1, 4096, H)]
+    p = mkpair(specs, 12)
+    p.g.sync_shadow()
+    for (nb, P, _), rg, h in zip(specs, p.rid_g, p.host):
+        got = p.g.debug_export(rg, crum.EXPORT_HASHES, synth.n_pages(nb, P))
+        for i in range(len(got)):
+            seg = h[i * P:(i + 1) * P].tobytes()
+            assert int(got[i]) == xxhash.xxh3_64_intdigest(seg + b"\0" * (P - len(seg))), (P, i)
+
+
+@pytest.mark.parametrize("chunk", [0, 64 * KiB])
+def test_gather_image_bit_exact(crum, chunk):
+    p = mkpair(MIXED, 13, chunk_bytes=chunk)
+    img = p.g.new_image()
+    for epoch, d, flags in ((0, 0, 0), (1, 0.1, 0), (2, 0.5, 0), (3, 0.0, 0), (4, 0.2, 1), (5, 1.0, 0)):
+        if epoch:
+            p.write(epoch, d)
+        st, want, rep_o = p.o.checkpoint_gather(flags=flags)
+        assert st == 0
+        rep = p.g.checkpoint_gather(img, flags=flags)
+        assert img.length == len(want)
+        assert img.tobytes() == want.tobytes(), epoch
+        for k in ("dirty_pages", "dirty_bytes", "dirty_runs", "image_bytes", "scanned_pages", "scanned_bytes"):
+            assert rep[k] == rep_o[k], (epoch, k)
+        assert p.shadows_equal()
+
+
+def test_gather_device_image_bit_exact(crum):
+    p = mkpair(MIXED, 14)
+    cap = p.g.image_required_bytes()
+    buf = torch.empty(cap + 4096, dtype=torch.uint8, device="cuda")
+    for epoch, d in ((0, 0), (1, 0.25), (2, 0.0)):
+        if epoch:
+            p.write(epoch, d)
+        st, want, _ = p.o.checkpoint_gather()
+        rep = p.g.checkpoint_gather_device(buf, cap)
+        assert rep["image_bytes"] == len(want)
+        assert buf[:len(want)].cpu().numpy().tobytes() == want.tobytes()
+    # asynchronous form (no report) then a synchronous read of the header
+    p.write(3, 0.4)
+    st, want, _ = p.o.checkpoint_gather()
+    p.g.checkpoint_gather_device(buf, cap, report=False)
+    torch.cuda.synchronize()
+    assert buf[:len(want)].cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_capacity_error_commits_nothing(crum):
+    p = mkpair(MIXED[:3], 15)
+    small = p.g.new_image(4096)
+    st, rep = p.g.checkpoint_gather(small, raise_on_error=False)
+    assert st == crum.E_CAPACITY and rep["image_bytes"] > 4096
+    assert p.g.debug_detect(p.N).tolist() == [1] * p.N       # force bits untouched
+    buf = torch.empty(8192, dtype=torch.uint8, device="cuda")
+    st, rep = p.g.checkpoint_gather_device(buf, 8192, raise_on_error=False)
+    assert st == crum.E_CAPACITY
+    assert p.g.debug_detect(p.N).tolist() == [1] * p.N
+    st, _ = p.g.checkpoint_gather_device(buf, 8192, report=False, raise_on_error=False)
+    assert st == crum.E_CAPACITY                               # async form: checked on the host
+
+
+def test_restore_chain_parity(crum):
+    p = mkpair(MIXED, 16)
+    imgs, states = [], []
+    for epoch in range(4):
+        if epoch:
+            p.write(epoch, 0.3)
+        img = p.g.new_image()
+        p.g.checkpoint_gather(img)
+        imgs.append(img)
+        states.append([h.copy() for h in p.host])
+    # restart: fresh context, zeroed regions; replay the chain (VERIFY on odd steps)
+    q = crum.Context(0, chunk_bytes=128 * KiB)
+    zs = []
+    for nb, P, mode in MIXED:
+        z = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        zs.append(z)
+        q.register_region(z, nb, P, mode)
+    for k, img in enumerate(imgs):
+        rep = q.restore_scatter(img, flags=crum.VERIFY if k % 2 else 0)
+        assert rep["dirty_pages"] == (sum(synth.n_pages(nb, P) for nb, P, _ in MIXED) if k == 0 else rep["dirty_pages"])
+        torch.cuda.synchronize()
+        for z, want in zip(zs, states[k]):
+            assert np.array_equal(z.cpu().numpy(), want), k
+    assert q.sync_shadow() == 0
+
+
+def test_restore_device_and_errors(crum):
+    specs = [(3 * 4096, 4096, C), (2 * 4096 + 7, 4096, H)]
+    p = mkpair(specs, 17)
+    img = p.g.new_image()
+    p.g.checkpoint_gather(img)
+    raw = img.view().copy()
+    meta = int.from_bytes(raw[24:32].tobytes(), "little")
+    q = crum.Context(0)
+    zs = []
+    for nb, P, mode in specs:
+        z = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        zs.append(z)
+        q.register_region(z, nb, P, mode)
+    # every single-byte corruption of the header + metadata is rejected, nothing written
+    for pos in range(meta):
+        bad = raw.copy()
+        bad[pos] ^= 0x10
+        st, _ = q.restore_scatter(q.import_image(bad), raise_on_error=False)
+        assert st == crum.E_CORRUPT, pos
+    st, _ = q.restore_scatter(q.import_image(raw[:-1]), raise_on_error=False)
+    assert st == crum.E_CORRUPT
+    assert all(int(z.sum()) == 0 for z in zs)
+    # VERIFY catches a tampered hash-mode slot
+    bad = raw.copy()
+    bad[-1] ^= 0xFF
+    st, _ = q.restore_scatter(q.import_image(bad), flags=crum.VERIFY, raise_on_error=False)
+    assert st == crum.E_CORRUPT
+    # table != live set
+    r = crum.Context(0)
+    z = torch.zeros(4 * 4096, dtype=torch.uint8, device="cuda")
+    r.register_region(z, 4 * 4096, 4096, C)
+    st, _ = r.restore_scatter(r.import_image(raw), raise_on_error=False)
+    assert st == crum.E_MISMATCH
+    # device-resident image restore
+    dimg = torch.from_numpy(raw).cuda()
+    dbuf = torch.empty(len(raw) + 256, dtype=torch.uint8, device="cuda")
+    dbuf[:len(raw)].copy_(dimg)
+    q.restore_scatter_device(dbuf, len(raw), flags=crum.VERIFY)
+    torch.cuda.synchronize()
+    for z, h in zip(zs, p.host):
+        assert np.array_equal(z.cpu().numpy(), h)
+    # oracle agrees on the same images
+    o2 = p.o  # regions match the image's table
+    assert o2.restore_scatter(raw)[0] == 0
+
+
+def test_mark_dirty_parity(crum):
+    p = mkpair([(8 * 4096, 4096, C), (4 * 64 * KiB, 64 * KiB, H)], 18)
+    p.g.sync_shadow()
+    p.o.sync_shadow()
+    for (rid_o, rid_g), (off, ln) in zip([(p.rid_o[0], p.rid_g[0])] * 3 + [(p.rid_o[1], p.rid_g[1])],
+                                         [(4095, 2), (5 * 4096, 0), (7 * 4096, 4096), (65536 * 2 + 1, 1)]):
+        assert p.g.mark_dirty(rid_g, off, ln) == p.o.mark_dirty(rid_o, off, ln) == 0
+    assert p.g.mark_dirty(p.rid_g[0], 8 * 4096, 1) == crum.E_RANGE
+    assert p.g.mark_dirty(999, 0, 1) == crum.E_NOREGION
+    assert np.array_equal(p.g.debug_detect(p.N), p.oracle_flags())
+    st, want, _ = p.o.checkpoint_gather()
+    img = p.g.new_image()
+    p.g.checkpoint_gather(img)
+    assert img.tobytes() == want.tobytes()
+
+
+def test_register_errors(crum):
+    g = crum.Context(0)
+    t = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    a = t.data_ptr()
+    assert g.try_register(0, 4096, 4096) == crum.E_INVAL
+    assert g.try_register(a, 0, 4096) == crum.E_INVAL
+    assert g.try_register(a, 4096, 2048) == crum.E_INVAL
+    assert g.try_register(a, 4096, 12288) == crum.E_INVAL
+    assert g.try_register(a + 8, 4096, 4096) == crum.E_INVAL
+    assert g.try_register(a, 4096, 4096, 5) == crum.E_INVAL
+    h = np.zeros(8192, dtype=np.uint8)
+    assert g.try_register(h.ctypes.data // 16 * 16 + 16, 4096, 4096) == crum.E_DEVICE
+    assert g.try_register(a, 65536, 4096) == 0
+    assert g.try_register(a + 4096, 4096, 4096) == crum.E_OVERLAP
+    assert g.try_register(a + 65536, 4096, 4096) == 0
+    g.unregister_region(1)
+    with pytest.raises(crum.CrumError):
+        g.unregister_region(1)
+
+
+def test_unregister_keeps_other_state(crum):
+    specs = [(4 * 4096, 4096, C), (4 * 4096, 4096, H), (4 * 4096, 4096, C)]
+    p = mkpair(specs, 19)
+    p.g.sync_shadow()
+    p.o.sync_shadow()
+    p.write(1, 0.5)
+    p.g.unregister_region(p.rid_g[1])
+    p.o.unregister(p.rid_o[1])
+    del p.specs[1], p.host[1], p.dev[1], p.rid_o[1], p.rid_g[1]
+    assert np.array_equal(p.g.debug_detect(p.N), p.oracle_flags())
+    st, want, _ = p.o.checkpoint_gather()
+    img = p.g.new_image()
+    p.g.checkpoint_gather(img)
+    assert img.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("mode", [C, H])
+@pytest.mark.parametrize("P", [64 * KiB, 2 * MiB])
+def test_c2_full_size_parity(crum, mode, P):
+    """Config 2 (1 GiB region) in the bench launch configuration, d = 10%:
+    the whole image (ids, hashes, payload) compared with the oracle."""
+    p = mkpair([(GiB, P, mode)], 2)
+    img = p.g.new_image()
+    p.g.checkpoint_gather(img)
+    p.o.checkpoint_gather()
+    p.write(1, 0.1)
+    st, want, rep_o = p.o.checkpoint_gather()
+    rep = p.g.checkpoint_gather(img)
+    assert rep["dirty_pages"] == rep_o["dirty_pages"] == synth.dirty_count(0.1, GiB // P)
+    assert img.length == len(want)
+    assert np.array_equal(img.view(), want)
+
+
+def test_c3_multi_region_sampled(crum):
+    """Config 3 shape (Rodinia-style region mix), 2 replicas, 64 KiB pages:
+    full checkpoint, 10% incremental, restore onto zeros, compared exactly."""
+    sizes = synth.c3_region_sizes(replicas=2)
+    specs = [(s, 64 * KiB, C if i % 3 else H) for i, s in enumerate(sizes)]
+    p = mkpair(specs, 3)
+    img0 = p.g.new_image()
+    p.g.checkpoint_gather(img0)
+    st, want0, _ = p.o.checkpoint_gather()
+    assert np.array_equal(img0.view(), want0)
+    p.write(1, 0.1)
+    img1 = p.g.new_image()
+    p.g.checkpoint_gather(img1)
+    st, want1, _ = p.o.checkpoint_gather()
+    assert np.array_equal(img1.view(), want1)
+    q = crum.Context(0)
+    zs = []
+    for nb, P, mode in specs:
+        z = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        zs.append(z)
+        q.register_region(z, nb, P, mode)
+    q.restore_scatter(img0)
+    q.restore_scatter(img1, flags=crum.VERIFY)
+    torch.cuda.synchronize()
+    for z, h in zip(zs, p.host):
+        assert np.array_equal(z.cpu().numpy(), h)
