@@ -1,0 +1,358 @@
+#!/usr/bin/env python3
+"""bench.py -- checkpointed GB/s of the shadow-page sync hot path on B200.
+
+A "step" is one coordinated checkpoint of the whole registered footprint:
+A5 barrier -> A1 detect -> A2 compact -> A3 gather + commit (-> A4 copy-out for
+the e2e figure) -> A5 all-reduce of the dirty/image bytes.  Before every step
+the "application" rewrites a seeded d-fraction of the pages (synth writer
+kernel) and L2 is scrubbed with a 256 MiB write; both run outside the step's
+CUDA events.  Inputs live in HBM (2 GiB > 126 MB L2 for C2).
+
+  value  = F / T_dev : registered bytes per second with the image written to
+           a device buffer (crum_checkpoint_gather_device), device-event time.
+  e2e    = F / T_ckpt: same step through crum_checkpoint_gather into a pinned
+           host image (D2H of the image inside the timed region).
+  restore: F / T_restore through crum_restore_scatter (H2D inside).
+
+Default workload (N=1): BASELINE.json configs[1] -- C2, one 1 GiB region,
+64 KiB pages, 10% of pages rewritten per step, compare mode.
+
+Multi-GPU: `python -m torch.distributed.run --nproc-per-node N bench.py --gpus N`
+(one region set per rank, weak scaling, NCCL barrier + all-reduce only).
+`--impl reference` times the CPU oracle (oracle/) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import signal
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "checkpointed GB/s (dirty detect+gather) at 1/2/4/8 B200; % of HBM roofline"
+KiB, MiB, GiB = 1 << 10, 1 << 20, 1 << 30
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="crum", choices=["crum", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--mode", default="compare", choices=["compare", "hash"])
+    ap.add_argument("--page", type=int, default=64 * KiB)
+    ap.add_argument("--dirty", type=float, default=0.10)
+    ap.add_argument("--region-gib", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def workload(args, rank: int):
+    """(specs, description).  specs: list of (nbytes, page_size, mode)."""
+    mode = 0 if args.mode == "compare" else 1
+    if args.config == "c1":
+        return [(4 * MiB, 4 * KiB, mode)], f"C1: one 4 MiB region, 4 KiB pages, {args.dirty:.0%} dirty, {args.mode}"
+    if args.config == "c2":
+        nb = int(args.region_gib * GiB)
+        return [(nb, args.page, mode)], (f"C2: one {args.region_gib:g} GiB region, {args.page // KiB} KiB pages, "
+                                         f"{args.dirty:.0%} dirty, {args.mode}")
+    if args.config == "c3":
+        sizes = synth.c3_region_sizes(20)
+        return [(s, args.page, mode) for s in sizes], (f"C3: Rodinia-style 220 regions (15.96 GiB), "
+                                                       f"{args.page // KiB} KiB pages, {args.dirty:.0%} dirty, {args.mode}")
+    big, small = synth.c4_region_sizes(synth.seed(4) + rank)
+    specs = [(s, 64 * KiB, mode) for s in big] + [(s, 4 * KiB, mode) for s in small]
+    return specs, f"C4: HPGMG-style 56 + 4096 regions (64.2 GiB) per GPU, 10% dirty, {args.mode}"
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def read_traffic(key: str):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(key)
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.path = f"/tmp/crum_clocks_{os.getpid()}.csv"
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.send_signal(signal.SIGTERM)
+        self.p.wait()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7 and f[0].isdigit():
+                rows.append(f)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "samples": len(rows),
+                "reasons": reasons}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_steps(specs, S, dirty, seconds: float, max_steps: int, min_steps: int = 1):
+    """Time oracle checkpoint_gather on the same workload (host copies),
+    writer outside the timing.  Returns (per-step seconds list, F, sample)."""
+    from oracle import oracle
+    o = oracle.Oracle()
+    host = []
+    for r, (nb, P, mode) in enumerate(specs):
+        h = oracle.aligned_empty(nb)
+        synth.fill_region(h, S, r)
+        host.append(h)
+        o.register(h, P, mode)
+    cap = o.required_bytes()
+    o.checkpoint_gather(capacity=cap)   # initial full image (epoch 0), untimed
+    times = []
+    t_start = time.perf_counter()
+    epoch = 0
+    while len(times) < max_steps and (len(times) < min_steps or time.perf_counter() - t_start < seconds):
+        epoch += 1
+        for r, (nb, P, _) in enumerate(specs):
+            synth.apply_writer(host[r], P, synth.choose_dirty(S, epoch, r, synth.n_pages(nb, P), dirty), S, epoch, r)
+        t0 = time.perf_counter()
+        st, img, rep = o.checkpoint_gather(capacity=cap)
+        times.append(time.perf_counter() - t0)
+        assert st == 0
+    F = sum(nb for nb, _, _ in specs)
+    return times, F
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    specs, desc = workload(args, 0)
+    S = synth.seed(1)
+    steps = args.warmup + args.steps
+    times, F = oracle_steps(specs, S, args.dirty, seconds=1e9, max_steps=steps, min_steps=steps)
+    t = times[args.warmup:]
+    v = F / statistics.mean(t) / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(statistics.mean(t) * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded splitmix64 words)",
+            "config": {"workload": desc, "footprint_bytes": F},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"the full workload ({F / GiB:g} GiB), {args.steps} timed steps, 1 thread"},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1808_00117_b200 import crum
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    distributed = world > 1
+    if distributed:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    specs, desc = workload(args, rank)
+    S = synth.seed(1) + (rank << 20)
+    F = sum(nb for nb, _, _ in specs)
+
+    ctx = crum.Context(local)
+    regions = []
+    with torch.cuda.stream(stream):
+        for r, (nb, P, mode) in enumerate(specs):
+            t = torch.empty(nb, dtype=torch.uint8, device=dev)
+            crum.synth_fill(t, nb, S, r, stream=stream)
+            regions.append(t)
+            ctx.register_region(t, nb, P, mode)
+    # the dirty pages of every epoch, precomputed on the host (untimed)
+    n_epochs = args.warmup + args.steps + max(3, args.steps // 2) + 2
+    pages = [[torch.from_numpy(synth.choose_dirty(S, e, r, synth.n_pages(nb, P), args.dirty).astype(np.uint32)).to(dev)
+              for r, (nb, P, _) in enumerate(specs)] for e in range(1, n_epochs + 1)]
+    scrub = torch.empty(256 * MiB, dtype=torch.uint8, device=dev)
+    cap = ctx.image_required_bytes()
+    dimg = torch.empty(cap + 256, dtype=torch.uint8, device=dev)
+    # epoch 0: the first (full) checkpoint, untimed
+    ctx.checkpoint_gather_device(dimg, cap, stream=stream)
+
+    def app_epoch(e):
+        for r, (nb, P, _) in enumerate(specs):
+            pg = pages[e - 1][r]
+            crum.synth_write_pages(regions[r], nb, P, pg, pg.numel(), S, e, r, stream=stream)
+        crum.synth_scrub(scrub, scrub.numel(), stream=stream)
+
+    from paper_1808_00117_b200 import coord
+
+    def coordinated(fn):
+        """A5: barrier before detect; all-reduce of {dirty bytes, image bytes} after."""
+        return coord.coordinated(fn).local
+
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    epoch = 0
+    for _ in range(args.warmup):
+        epoch += 1
+        app_epoch(epoch)
+        coordinated(lambda: ctx.checkpoint_gather_device(dimg, cap, stream=stream))
+    torch.cuda.synchronize()
+    if distributed:
+        dist.barrier()
+    clocks = Clocks(local)
+    launches0 = ctx.launch_count
+    t_wall0 = time.perf_counter()
+    reps = []
+    for i in range(args.steps):
+        epoch += 1
+        app_epoch(epoch)
+        ev0[i].record(stream)
+        reps.append(coordinated(lambda: ctx.checkpoint_gather_device(dimg, cap, stream=stream)))
+        ev1[i].record(stream)
+    torch.cuda.synchronize()
+    if distributed:
+        dist.barrier()
+    wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+    launches = ctx.launch_count - launches0
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    T = sum(step_ms) / 1e3
+    det_ms = [r["t_detect_ms"] for r in reps]
+    if distributed:
+        t = torch.tensor([T, sum(det_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        T, det_sum = float(t[0]), float(t[1])
+    else:
+        det_sum = sum(det_ms)
+    value = world * F * args.steps / T / 1e9
+    K = reps[-1]["dirty_pages"]
+    KP = reps[-1]["image_bytes"]
+    peak, peak_src = read_peaks()
+    # dominant kernel: A1 detect (compare: reads region + mirror; hash: region + table)
+    n_pages = sum(synth.n_pages(nb, P) for nb, P, _ in specs)
+    det_bytes = 2 * F if args.mode == "compare" else F + 8 * n_pages + 8 * n_pages
+    det_t = det_sum / args.steps / 1e3
+    achieved = det_bytes / det_t / 1e9
+    payload = reps[-1]["image_bytes"]
+    dev_alg = (2 * F + 2 * payload) if args.mode == "compare" else (F + 16 * n_pages + 2 * payload)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(T * 1e3 / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded splitmix64 words; seeded page choice per epoch)",
+        "config": {"workload": desc, "footprint_bytes_per_gpu": F, "pages_per_gpu": n_pages,
+                   "dirty_pages_per_step": K, "image_bytes_per_step": KP,
+                   "l2": "inputs 2x footprint > 126 MB L2; 256 MiB scrub write before every step",
+                   "timing": "per-step CUDA events around crum_checkpoint_gather_device on its stream; "
+                             "application writer + scrub outside the events",
+                   "wall_ms_per_step_incl_writer": round(wall * 1e3 / args.steps, 3)},
+        "roofline": {"bound": "hbm", "kernel": f"detect_{args.mode}", "achieved": round(achieved, 1),
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "alg_bytes_per_launch": det_bytes, "avg_launch_ms": round(det_t * 1e3, 4),
+                     "traffic": read_traffic(f"detect_{args.mode}")},
+        "device_phase": {"alg_bytes_per_step": dev_alg, "achieved_GBs": round(dev_alg / (T / args.steps) / 1e9, 1),
+                         "frac": round(dev_alg / (T / args.steps) / 1e9 / peak, 4)},
+        "gpu_launches": launches,
+        "gpu_launches_synth": 2 * args.steps * len(specs),
+        "clocks": clk,
+    }
+    # ---- e2e: pinned host image, D2H inside the timed region ----
+    if not args.no_e2e:
+        img = ctx.new_image(cap)
+        ctx.checkpoint_gather(img, stream=stream)
+        e2e_ms, e2e_reps = [], []
+        for i in range(max(3, args.steps // 2)):
+            epoch += 1
+            app_epoch(epoch)
+            torch.cuda.synchronize()
+            if distributed:
+                dist.barrier()
+            t0 = time.perf_counter()
+            e2e_reps.append(coordinated(lambda: ctx.checkpoint_gather(img, stream=stream)))
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        te = statistics.median(e2e_ms) / 1e3
+        if distributed:
+            t = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t[0])
+        line["e2e"] = {"value": round(world * F / te / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": e2e_reps[-1]["image_bytes"], "ms_per_step": round(te * 1e3, 3),
+                       "note": "crum_checkpoint_gather into pinned host memory, host wall clock per call "
+                               "(median); the regions being checkpointed live in HBM by definition",
+                       "link_GBs": round(e2e_reps[-1]["image_bytes"] / max(e2e_reps[-1]["t_copy_ms"], 1e-9) / 1e6, 2)}
+        # restore of the last image onto the live regions (H2D inside)
+        r_ms = []
+        for i in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rr = ctx.restore_scatter(img, stream=stream)
+            r_ms.append((time.perf_counter() - t0) * 1e3)
+        line["restore"] = {"value": round(F / (statistics.median(r_ms) / 1e3) / 1e9, 3), "unit": "GB/s",
+                           "ms_per_call": round(statistics.median(r_ms), 3), "h2d_bytes": rr["image_bytes"]}
+        img.destroy()
+    # ---- cpu_baseline: the oracle on this workload, rank 0 at N=1 only ----
+    if not args.no_cpu_baseline and world == 1:
+        times, Fo = oracle_steps(specs, synth.seed(1), args.dirty, seconds=args.cpu_seconds, max_steps=50)
+        v = Fo / statistics.median(times) / 1e9
+        line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                                "sample": f"{len(times)} oracle checkpoint_gather steps over the same workload "
+                                          f"({Fo / GiB:g} GiB, d={args.dirty}), writer untimed, median"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if distributed:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

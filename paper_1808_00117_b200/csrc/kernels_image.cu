@@ -381,7 +381,9 @@ struct X2N {
 };
 
 __device__ __forceinline__ uint32_t gf2_mulmod(uint32_t a, uint32_t b) {
-    // reflected GF(2)[x] product mod the CRC-32 polynomial
+    // reflected GF(2)[x] product mod the CRC-32 polynomial (loop ends at the
+    // lowest set bit of a, so a == 0 must be handled up front)
+    if (a == 0) return 0;
     uint32_t m = 0x80000000u, p = 0;
     for (;;) {
         if (a & m) {
@@ -429,7 +431,7 @@ __global__ void __launch_bounds__(256) k_crc_meta(const uint8_t *__restrict__ im
         const uint64_t b0 = c * kCrcChunk, b1 = min(len, b0 + kCrcChunk);
         uint32_t raw = 0;
         for (uint64_t b = b0; b < b1; ++b) raw = T[(raw ^ data[b]) & 0xffu] ^ (raw >> 8);
-        acc ^= gf2_mulmod(raw, xpow8n(len - b1, sx));
+        acc ^= gf2_mulmod(xpow8n(len - b1, sx), raw);  // first operand is never 0
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);

@@ -41,6 +41,7 @@ struct CrcTables {
 };
 
 uint32_t gf2_mulmod_host(uint32_t a, uint32_t b) {
+    if (a == 0) return 0;
     uint32_t m = 0x80000000u, p = 0;
     for (;;) {
         if (a & m) {
