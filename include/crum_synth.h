@@ -38,6 +38,11 @@ CRUM_API int crum_synth_write_pages(void *dev_ptr, uint64_t bytes, uint64_t page
 /* Streaming write of `bytes` to scrub L2 between timed repetitions. */
 CRUM_API int crum_synth_scrub(void *dev_ptr, uint64_t bytes, void *stream);
 
+/* Bandwidth probe: 16-byte vectorised copy kernel (blocks <= 0: 8 per SM of a
+ * 148-SM part).  dst/src may be device or mapped pinned host pointers, 16-byte
+ * aligned, bytes a multiple of 16. */
+CRUM_API int crum_probe_copy(void *dst, const void *src, uint64_t bytes, int blocks, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

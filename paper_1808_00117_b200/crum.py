@@ -39,7 +39,7 @@ EXPORTED = (
     "crum_image_data", "crum_image_destroy", "crum_checkpoint_gather", "crum_checkpoint_gather_device",
     "crum_restore_scatter", "crum_restore_scatter_device", "crum_status_string", "crum_last_error_detail",
     "crum_debug_detect", "crum_debug_export", "crum_launch_count",
-    "crum_synth_fill", "crum_synth_write_pages", "crum_synth_scrub",
+    "crum_synth_fill", "crum_synth_write_pages", "crum_synth_scrub", "crum_probe_copy",
 )
 
 
@@ -82,6 +82,7 @@ _sig = {
     "crum_synth_fill": (_i, [_vp, _u64, _u64, _u64, _u64, _vp]),
     "crum_synth_write_pages": (_i, [_vp, _u64, _u64, _vp, _u64, _u64, _u64, _u64, _i, _vp]),
     "crum_synth_scrub": (_i, [_vp, _u64, _vp]),
+    "crum_probe_copy": (_i, [_vp, _vp, _u64, _i, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_L, _name)
@@ -314,3 +315,7 @@ def synth_write_pages(dev_ptr, nbytes: int, page_size: int, dev_pages, n_pages: 
 
 def synth_scrub(dev_ptr, nbytes: int, stream=None):
     _check(_L.crum_synth_scrub(_addr(dev_ptr), nbytes, _stream(stream)), "crum_synth_scrub")
+
+
+def probe_copy(dst, src, nbytes: int, blocks: int = 0, stream=None):
+    _check(_L.crum_probe_copy(_addr(dst), _addr(src), nbytes, blocks, _stream(stream)), "crum_probe_copy")

@@ -95,3 +95,22 @@ extern "C" int crum_synth_scrub(void *dev_ptr, uint64_t bytes, void *stream) {
     crum::launch_synth_scrub((cudaStream_t)stream, (uint8_t *)dev_ptr, bytes);
     return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
 }
+
+// ---------------------------------------------------------------------------
+// Bandwidth probe: 16-byte vectorised copy with a chosen grid,
+// used to measure HBM and SM-driven host-link (zero-copy) bandwidth.
+// ---------------------------------------------------------------------------
+namespace crum {
+__global__ void k_probe_copy(uint4 *__restrict__ dst, const uint4 *__restrict__ src, uint64_t n) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+        dst[j] = src[j];
+}
+}  // namespace crum
+
+extern "C" int crum_probe_copy(void *dst, const void *src, uint64_t bytes, int blocks, void *stream) {
+    if (!dst || !src || ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | bytes) & 15))
+        return CRUM_E_INVAL;
+    crum::k_probe_copy<<<blocks > 0 ? blocks : 148 * 8, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<uint4 *>(dst), reinterpret_cast<const uint4 *>(src), bytes / 16);
+    return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
+}
