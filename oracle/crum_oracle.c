@@ -387,9 +387,23 @@ int orc_sync_shadow(orc_ctx *c, uint64_t *n_out)
 /* ------------------------------------------------------------------ */
 static uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
-static uint64_t meta_bytes_for(uint64_t R, uint64_t K, int has_hashes)
+/* Layout: header | table | zero pad | payload | ids | hashes. */
+static uint64_t payload_offset_for(uint64_t R) { return round_up(64 + 48 * R, 4096); }
+
+static uint64_t tail_bytes_for(uint64_t K, int has_hashes)
 {
-    return 64 + 48 * R + round_up(4 * K, 8) + (has_hashes ? 8 * K : 0);
+    return round_up(4 * K, 8) + (has_hashes ? 8 * K : 0);
+}
+
+/* zlib CRC-32 of the concatenation a || b (one bit at a time). */
+static uint32_t crc32_two(const uint8_t *a, uint64_t na, const uint8_t *b, uint64_t nb)
+{
+    uint32_t c = 0xffffffffu;
+    for (uint64_t i = 0; i < na + nb; ++i) {
+        c ^= i < na ? a[i] : b[i - na];
+        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xedb88320u & (0u - (c & 1u)));
+    }
+    return c ^ 0xffffffffu;
 }
 
 static int any_hash_region(const orc_ctx *c)
@@ -410,7 +424,7 @@ int orc_image_required_bytes(orc_ctx *c, uint64_t max_dirty, uint64_t *out)
         if (c->r[k].page_size > maxp) maxp = c->r[k].page_size;
     }
     if (K < N && K * maxp < payload) payload = K * maxp;
-    *out = round_up(meta_bytes_for(c->n, K, any_hash_region(c)), 4096) + payload;
+    *out = payload_offset_for(c->n) + payload + tail_bytes_for(K, any_hash_region(c));
     return ORC_OK;
 }
 
@@ -441,9 +455,9 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
         }
     }
     const int has_hashes = any_hash_region(c);
-    const uint64_t meta = meta_bytes_for(R, K, has_hashes);
-    const uint64_t poff = round_up(meta, 4096);
-    const uint64_t total = poff + payload;
+    const uint64_t poff = payload_offset_for(R);
+    const uint64_t ids_off = poff + payload;
+    const uint64_t total = ids_off + tail_bytes_for(K, has_hashes);
     if (rep) {
         rep->scanned_pages = N;
         rep->scanned_bytes = scanned_bytes;
@@ -464,11 +478,12 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
     wr32(img + 8, ((flags & ORC_FULL) ? ORC_IMG_FULL : 0) | (has_hashes ? ORC_IMG_HAS_HASHES : 0));
     wr32(img + 12, R);
     wr64(img + 16, K);
-    wr64(img + 24, meta);
-    wr64(img + 32, poff);
-    wr64(img + 40, payload);
+    wr64(img + 24, poff);
+    wr64(img + 32, payload);
+    wr64(img + 40, ids_off);
+    wr64(img + 48, total);
     uint8_t *tab = img + 64;
-    uint8_t *ids = tab + 48 * (uint64_t)R;
+    uint8_t *ids = img + ids_off;
     uint8_t *hashes = ids + round_up(4 * K, 8);
     uint64_t slot = 0, pbyte = 0;
     for (uint32_t k = 0; k < R; ++k) {
@@ -492,7 +507,7 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
         wr64(e + 32, nd);
         wr64(e + 40, first);
     }
-    wr32(img + 48, orc_crc32(img + 64, meta - 64));
+    wr32(img + 56, crc32_two(tab, 48 * (uint64_t)R, ids, total - ids_off));
     wr32(img + 60, orc_crc32(img, 60));
     /* Step 3: commit every listed page. */
     for (uint32_t k = 0; k < R; ++k) {
@@ -514,17 +529,19 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
     if (len < 64 || memcmp(img, "CRUM", 4) != 0) return ORC_E_CORRUPT;
     if (orc_crc32(img, 60) != rd32(img + 60)) return ORC_E_CORRUPT;
     const uint32_t version = rd32(img + 4), iflags = rd32(img + 8), R = rd32(img + 12);
-    const uint64_t K = rd64(img + 16), meta = rd64(img + 24), poff = rd64(img + 32),
-                   payload = rd64(img + 40);
-    if (version != 1 || (iflags & ~3u) != 0 || rd64(img + 52) != 0) return ORC_E_CORRUPT;
+    const uint64_t K = rd64(img + 16), poff = rd64(img + 24), payload = rd64(img + 32),
+                   ids_off = rd64(img + 40), total = rd64(img + 48);
+    if (version != 1 || (iflags & ~3u) != 0) return ORC_E_CORRUPT;
     const int has_hashes = (iflags & ORC_IMG_HAS_HASHES) != 0;
     if (K > ORC_MAX_TOTAL_PAGES || R > 0x7fffffffu) return ORC_E_CORRUPT;
-    if (meta != meta_bytes_for(R, K, has_hashes) || poff != round_up(meta, 4096)) return ORC_E_CORRUPT;
-    if (len < poff || len - poff < payload) return ORC_E_CORRUPT;
-    if (orc_crc32(img + 64, meta - 64) != rd32(img + 48)) return ORC_E_CORRUPT;
+    if (poff != payload_offset_for(R) || payload > (1ull << 62) || ids_off != poff + payload ||
+        total != ids_off + tail_bytes_for(K, has_hashes))
+        return ORC_E_CORRUPT;
+    if (len < total) return ORC_E_CORRUPT;
     const uint8_t *tab = img + 64;
-    const uint8_t *ids = tab + 48 * (uint64_t)R;
+    const uint8_t *ids = img + ids_off;
     const uint8_t *hashes = ids + round_up(4 * K, 8);
+    if (crc32_two(tab, 48 * (uint64_t)R, ids, total - ids_off) != rd32(img + 56)) return ORC_E_CORRUPT;
     /* Structural consistency of the table, ids and hash list. */
     uint64_t sum = 0, pay = 0;
     int any_hash = 0;
@@ -597,7 +614,7 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
         rep->dirty_pages = K;
         rep->dirty_bytes = dirty_bytes;
         rep->dirty_runs = runs;
-        rep->image_bytes = poff + payload;
+        rep->image_bytes = total;
     }
     return ORC_OK;
 }

@@ -55,20 +55,30 @@ struct RegStat {
 // Device-resident bookkeeping of one gather / restore call.
 struct DevStats {
     uint64_t K;
-    uint64_t meta_bytes;
-    uint64_t poff;
+    uint64_t poff;           // payload offset = round_up(64 + 48R, 4096)
     uint64_t payload_bytes;
+    uint64_t ids_off;        // poff + payload_bytes
     uint64_t image_bytes;
     uint64_t dirty_bytes;
     uint64_t dirty_runs;
-    uint64_t total_units;
-    uint32_t status;        // kStOk / kStCapacity / kStCorrupt
-    uint32_t crc_acc;       // XOR of per-chunk raw CRC terms (meta CRC)
-    uint32_t img_flags;     // header flags (bit0 FULL, bit1 HAS_HASHES)
+    uint64_t total_units;    // payload_bytes / 4096
+    uint64_t capacity;       // device image capacity (gather)
+    uint32_t status;         // kStOk / kStCapacity / kStCorrupt
+    uint32_t crc_acc;        // XOR of per-chunk raw CRC terms (meta CRC)
+    uint32_t img_flags;      // header flags (bit0 FULL, bit1 HAS_HASHES)
     uint32_t n_regions;
-    uint64_t capacity;      // device image capacity (gather)
-    uint32_t meta_crc;      // final zlib CRC-32 of [64, meta_bytes)
+    uint32_t meta_crc;       // final zlib CRC-32 of table || ids || hashes
     uint32_t pad0;
+};
+
+// Running totals of the compaction before range c (rb[c]); rb[0] = {0, 0}.
+struct RangeTotals {
+    uint64_t k;
+    uint64_t units;
+};
+
+struct X2N {
+    uint32_t t[32];  // x^(2^k) mod P (reflected CRC-32 polynomial)
 };
 
 struct Launch {
@@ -77,36 +87,99 @@ struct Launch {
     uint64_t *counter;  // incremented per kernel launch
 };
 
+// A2: compaction of pages [p_lo, p_hi) (p_lo % 16 == 0), range index c.
+struct CompactArgs {
+    const uint8_t *flags;
+    const uint8_t *force;
+    const DevRegion *regs;
+    const uint64_t *newhash;
+    uint64_t p_lo, p_hi;
+    uint32_t R;
+    uint32_t tag;          // flags[g] == tag <=> content changed in this checkpoint
+    int full;              // CRUM_FULL: every page listed
+    int has_hashes;
+    int first_range;       // reset per-checkpoint accumulators
+    int final_range;       // finalise: region prefix sums, header fields, table
+    uint32_t c;
+    uint32_t *blk_count;   // per-block dirty pages
+    uint64_t *blk_units;   // per-block 4 KiB units
+    uint32_t *gids;        // slot -> global page id
+    uint64_t *sunit;       // slot -> payload unit offset
+    uint32_t *lids;        // slot -> region-local page id (image ids)
+    uint64_t *lhash;       // slot -> XXH3 (hash regions) or 0 (image hashes)
+    uint32_t *reg_nd;      // per-region dirty count
+    RangeTotals *rb;
+    uint32_t *done;        // last-block counter (self-resetting)
+    RegStat *rs;
+    DevStats *st;
+    uint64_t capacity;
+    uint8_t *head;         // image head (header + table + pad) or nullptr
+};
+
+// A3: gather units [u_lo, u_hi) of the range with totals rb[0] (before) and
+// rb[1] (after).  dst == nullptr: commit only.  Unit u is written at
+// dst + (add_poff ? st->poff : 0) + (u - dst_unit0) * 4096.
+struct GatherArgs {
+    const DevRegion *regs;
+    uint32_t R;
+    int add_poff;
+    const uint32_t *gids;
+    const uint64_t *sunit;
+    const uint64_t *newhash;
+    const RangeTotals *rb;
+    const DevStats *st;
+    uint8_t *dst;
+    uint64_t dst_unit0;
+    uint8_t *force;
+    uint64_t u_lo, u_hi;
+};
+
+// Metadata CRC + tail copy + header (last block).
+struct CrcArgs {
+    uint8_t *head;          // header + table (table already written)
+    uint8_t *tail;          // ids/hashes destination, nullptr: head + st->ids_off
+    const uint32_t *lids;
+    const uint64_t *lhash;
+    const uint32_t *gids;
+    DevStats *st;
+    uint32_t *done;
+    X2N x2n;
+};
+
+// A6: scatter units [u_lo, u_hi); unit u read from src + (u - src_unit0)*4096.
+struct ScatterArgs {
+    const DevRegion *regs;
+    uint32_t R;
+    const RegStat *rs;
+    const uint32_t *ids;
+    const uint64_t *hashes;
+    const DevStats *st;
+    const uint8_t *src;
+    uint64_t src_unit0;
+    uint8_t *force;
+    uint64_t u_lo, u_hi;
+};
+
 // ---- detect (kernels_detect.cu) ----
 void launch_detect_compare(const Launch &L, const DevRegion *regs, const uint32_t *cmp_idx,
-                           const uint64_t *cmp_seg, uint32_t n_cmp, uint64_t n_seg,
-                           const uint8_t *force, uint8_t *flags);
+                           const uint64_t *cmp_seg, uint32_t n_cmp, uint64_t s_lo, uint64_t s_hi,
+                           const uint8_t *force, uint8_t *flags, uint8_t tag);
 void launch_detect_hash(const Launch &L, const DevRegion *regs, const uint32_t *hash_idx,
-                        const uint64_t *hash_grp, uint32_t n_hash, uint64_t n_grp,
-                        uint8_t *flags, uint64_t *newhash);
+                        const uint64_t *hash_grp, uint32_t n_hash, uint64_t w_lo, uint64_t w_hi,
+                        uint8_t *flags, uint64_t *newhash, uint8_t tag);
 void launch_verify_hash(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
-                        const uint8_t *meta, const uint8_t *payload_base, int add_poff, DevStats *st);
+                        const uint64_t *hashes, const uint8_t *payload, uint64_t K, DevStats *st);
 
 // ---- compaction, metadata, gather, scatter, CRC (kernels_image.cu) ----
-void launch_compact(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N,
-                    int full, uint32_t *blk_counts, uint32_t *gids, DevStats *st);
-void launch_region_stats(const Launch &L, const DevRegion *regs, uint32_t R, const uint32_t *gids,
-                         RegStat *rs, DevStats *st, int full, int has_hashes, uint64_t capacity);
-void launch_meta(const Launch &L, const DevRegion *regs, uint32_t R, const uint32_t *gids,
-                 const uint64_t *newhash, const RegStat *rs, DevStats *st, uint8_t *img);
-// dst_base == nullptr: commit only.  Else unit u is written at
-// dst_base + (add_poff ? st->poff : 0) + (u - dst_unit0) * 4096.
-void launch_gather(const Launch &L, const DevRegion *regs, uint32_t R, const uint32_t *gids,
-                   const uint64_t *newhash, const RegStat *rs, const DevStats *st, uint8_t *dst_base,
-                   uint64_t dst_unit0, int add_poff, uint8_t *force, uint64_t unit_lo, uint64_t unit_hi);
-void launch_crc_meta(const Launch &L, const uint8_t *img, DevStats *st, const uint32_t *x2n);
-void launch_header(const Launch &L, uint8_t *img, DevStats *st, const uint32_t *x2n);
-void launch_restore_validate(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
-                             const uint8_t *img, DevStats *st);
-void launch_scatter(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
-                    const uint8_t *meta, const DevStats *st, const uint8_t *src_base, uint64_t src_unit0,
-                    int add_poff, uint8_t *force, uint64_t unit_lo, uint64_t unit_hi);
-void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N,
+void launch_compact(const Launch &L, const CompactArgs &a);
+void launch_gather(const Launch &L, const GatherArgs &a, uint64_t max_units);
+void launch_crc_meta(const Launch &L, const CrcArgs &a, uint64_t max_len);
+void launch_crc_check(const Launch &L, const uint8_t *table, uint64_t tab, const uint8_t *tail, uint64_t tl,
+                      DevStats *st, const X2N &x2n);
+void launch_restore_validate(const Launch &L, const DevRegion *tregs, uint32_t R, const RegStat *rs,
+                             const uint32_t *ids, const uint64_t *hashes, uint64_t K, DevStats *st);
+void launch_scatter(const Launch &L, const ScatterArgs &a);
+void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag,
                          uint8_t *out);
 
 // ---- synthetic inputs (synth.cu) ----

@@ -40,14 +40,14 @@ __device__ __forceinline__ uint4 ld128(const void *p) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_detect_compare(
     const DevRegion *__restrict__ regs, const uint32_t *__restrict__ cmp_idx,
-    const uint64_t *__restrict__ cmp_seg, uint32_t n_cmp, uint64_t n_seg,
-    const uint8_t *__restrict__ force, uint8_t *__restrict__ flags) {
+    const uint64_t *__restrict__ cmp_seg, uint32_t n_cmp, uint64_t s_lo, uint64_t s_hi,
+    const uint8_t *__restrict__ force, uint8_t *__restrict__ flags, uint8_t tag) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
     uint64_t r_lo = 1, r_hi = 0;  // cached segment range of the current region
     DevRegion R{};
-    for (uint64_t s = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); s < n_seg; s += nwarps) {
+    for (uint64_t s = s_lo + (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); s < s_hi; s += nwarps) {
         if (s < r_lo || s >= r_hi) {
             uint32_t r = upper_region(cmp_seg, n_cmp, s);
             R = regs[__ldg(cmp_idx + r)];
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_detect_compare(
         } else {  // logical tail of a partial last page (reading Q7): bytewise
             for (uint32_t o = lane; o < len; o += 32) x |= (uint32_t)(a[o] ^ b[o]);
         }
-        if (__any_sync(0xffffffffu, x != 0) && lane == 0) flags[g] = 1;
+        if (__any_sync(0xffffffffu, x != 0) && lane == 0) flags[g] = tag;
     }
 }
 
@@ -251,8 +251,8 @@ __device__ __forceinline__ uint64_t xxh3_slot(const uint8_t *__restrict__ pg, ui
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_detect_hash(
     const DevRegion *__restrict__ regs, const uint32_t *__restrict__ hash_idx,
-    const uint64_t *__restrict__ hash_grp, uint32_t n_hash, uint64_t n_grp,
-    uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash) {
+    const uint64_t *__restrict__ hash_grp, uint32_t n_hash, uint64_t w_lo, uint64_t w_hi,
+    uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash, uint8_t tag) {
     const uint32_t lane = threadIdx.x & 31;
     LaneKeys k;
     load_lane_keys(k, lane & 3);
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(256) k_detect_hash(
     const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
     uint64_t r_lo = 1, r_hi = 0;
     DevRegion R{};
-    for (uint64_t w = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); w < n_grp; w += nwarps) {
+    for (uint64_t w = w_lo + (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); w < w_hi; w += nwarps) {
         if (w < r_lo || w >= r_hi) {
             uint32_t r = upper_region(hash_grp, n_hash, w);
             R = regs[__ldg(hash_idx + r)];
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(256) k_detect_hash(
             const uint64_t g = R.page_base + page;
             const uint64_t old = R.table[page];
             newhash[g] = h;
-            flags[g] = (h != old) ? 1 : 0;
+            flags[g] = (h != old) ? tag : 0;
         }
     }
 }
@@ -306,15 +306,12 @@ __global__ void __launch_bounds__(256) k_detect_hash(
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_verify_hash(const DevRegion *__restrict__ regs,
                                                      uint32_t R, const RegStat *__restrict__ rs,
-                                                     const uint8_t *__restrict__ meta,
-                                                     const uint8_t *__restrict__ payload_base,
-                                                     int add_poff, DevStats *st) {
+                                                     const uint64_t *__restrict__ hashes,
+                                                     const uint8_t *__restrict__ payload, uint64_t K,
+                                                     DevStats *st) {
     const uint32_t lane = threadIdx.x & 31;
     LaneKeys k;
     load_lane_keys(k, lane & 3);
-    const uint64_t K = st->K;
-    const uint8_t *payload = payload_base + (add_poff ? st->poff : 0);
-    const uint64_t *hashes = reinterpret_cast<const uint64_t *>(meta + 64 + 48ull * R + round_up(4 * K, 8));
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
     for (uint64_t s = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); s < K; s += nwarps) {
@@ -347,27 +344,27 @@ static inline int grid_for(uint64_t warps, int sms, int per_sm) {
 }
 
 void launch_detect_compare(const Launch &L, const DevRegion *regs, const uint32_t *cmp_idx,
-                           const uint64_t *cmp_seg, uint32_t n_cmp, uint64_t n_seg,
-                           const uint8_t *force, uint8_t *flags) {
-    if (!n_seg) return;
-    k_detect_compare<<<grid_for(n_seg, L.sms, 8), 256, 0, L.stream>>>(regs, cmp_idx, cmp_seg, n_cmp,
-                                                                      n_seg, force, flags);
+                           const uint64_t *cmp_seg, uint32_t n_cmp, uint64_t s_lo, uint64_t s_hi,
+                           const uint8_t *force, uint8_t *flags, uint8_t tag) {
+    if (s_hi <= s_lo) return;
+    k_detect_compare<<<grid_for(s_hi - s_lo, L.sms, 8), 256, 0, L.stream>>>(regs, cmp_idx, cmp_seg, n_cmp, s_lo,
+                                                                             s_hi, force, flags, tag);
     ++*L.counter;
 }
 
 void launch_detect_hash(const Launch &L, const DevRegion *regs, const uint32_t *hash_idx,
-                        const uint64_t *hash_grp, uint32_t n_hash, uint64_t n_grp, uint8_t *flags,
-                        uint64_t *newhash) {
-    if (!n_grp) return;
-    k_detect_hash<<<grid_for(n_grp, L.sms, 8), 256, 0, L.stream>>>(regs, hash_idx, hash_grp, n_hash,
-                                                                   n_grp, flags, newhash);
+                        const uint64_t *hash_grp, uint32_t n_hash, uint64_t w_lo, uint64_t w_hi,
+                        uint8_t *flags, uint64_t *newhash, uint8_t tag) {
+    if (w_hi <= w_lo) return;
+    k_detect_hash<<<grid_for(w_hi - w_lo, L.sms, 8), 256, 0, L.stream>>>(regs, hash_idx, hash_grp, n_hash, w_lo,
+                                                                         w_hi, flags, newhash, tag);
     ++*L.counter;
 }
 
 void launch_verify_hash(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
-                        const uint8_t *meta, const uint8_t *payload_base, int add_poff, DevStats *st) {
-    if (!R) return;
-    k_verify_hash<<<L.sms * 4, 256, 0, L.stream>>>(regs, R, rs, meta, payload_base, add_poff, st);
+                        const uint64_t *hashes, const uint8_t *payload, uint64_t K, DevStats *st) {
+    if (!R || !K) return;
+    k_verify_hash<<<L.sms * 4, 256, 0, L.stream>>>(regs, R, rs, hashes, payload, K, st);
     ++*L.counter;
 }
 

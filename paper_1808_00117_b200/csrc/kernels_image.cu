@@ -1,20 +1,25 @@
 // kernels_image.cu -- A2 compact, A3 gather + commit, A6 scatter + commit,
 // and the v1 image metadata (table, ids, hashes, CRC-32s) on the device.
 //
-//  * compaction: two passes over the per-page flags (N bytes + N force bytes,
-//    uint4 loads, 4096 pages per 256-thread block): per-block counts, then
-//    each block sums the counts before it and writes its ids in ascending
-//    order (block scan over per-thread counts).  Deterministic: no atomics
-//    decide positions.
-//  * region stats: one block; per region a binary search of the sorted ids
-//    gives (first, n_dirty), then a block scan gives payload/unit offsets.
-//  * gather / scatter: one warp per 4 KiB unit of payload, 256-bit loads and
-//    stores; the unit -> (region, slot, page) map is a binary search of the
-//    per-region unit prefix.  Commit is fused: mirror <- page (compare),
-//    table <- new hash (hash), force <- 0.
-//  * CRC-32 of the metadata: per-thread 256-byte chunks with a byte table in
-//    shared memory, each chunk's raw CRC shifted to its position by a
-//    GF(2)[x] multiplication by x^(8*bytes_after) mod P, XOR-reduced.
+//  * compaction (per page range [p_lo, p_hi), ranges in ascending order):
+//    two passes over the per-page flags (uint4 loads, 4096 pages per
+//    256-thread block).  Pass 1: per-block (count, 4 KiB units).  Pass 2: each
+//    block sums the totals of the blocks before it (plus the running totals
+//    of earlier ranges), block-scans (count, units) over its threads and
+//    writes, per dirty page in ascending order: the global page id, the
+//    slot's payload unit offset, the region-local id and (hash regions) the
+//    new hash; per-region counts, runs and dirty bytes accumulate with
+//    integer atomics (order-free, deterministic).  Positions are decided by
+//    scans only -- the image is canonical.  The last block to finish (done
+//    counter) publishes the running totals and, for the final range, the
+//    per-region prefix sums, the header fields and the region table.
+//  * gather / scatter: one warp per 8 consecutive 4 KiB payload units, one
+//    binary search per task, 256-bit loads and stores; commit fused.
+//  * CRC-32 of table || ids || hashes: per-thread 64-byte chunks (byte table
+//    in shared memory; zlib's ~0 init folded into chunk 0), each chunk's raw
+//    CRC shifted to its position by a GF(2)[x] product with x^(8*after) mod
+//    P, XOR-reduced; the last block finalises and writes the header.  The
+//    kernel also copies ids/hashes from scratch into the image tail.
 #include "crum_internal.cuh"
 
 namespace crum {
@@ -72,150 +77,13 @@ __device__ uint64_t block_excl_scan(uint64_t v, uint64_t *total) {
     return warp_off[wid] + inc - v;
 }
 
-// ---------------------------------------------------------------------------
-// A2 compaction
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t thread_dirty_mask(const uint8_t *flags, const uint8_t *force,
-                                                      uint64_t base, uint64_t N, int full) {
-    if (full) {
-        if (base >= N) return 0;
-        const uint64_t n = N - base;
-        return n >= 16 ? 0xffffu : ((1u << n) - 1);
-    }
-    const uint4 f = *reinterpret_cast<const uint4 *>(flags + base);
-    const uint4 o = *reinterpret_cast<const uint4 *>(force + base);
-    const uint32_t w[4] = {f.x | o.x, f.y | o.y, f.z | o.z, f.w | o.w};
-    uint32_t m = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) m |= ((w[i] >> (8 * b)) & 0xffu ? 1u : 0u) << (4 * i + b);
-    return m;
+__device__ __forceinline__ uint64_t block_sum(uint64_t v) {
+    uint64_t t;
+    block_excl_scan(v, &t);
+    return t;
 }
 
-__global__ void __launch_bounds__(kCompactThreads) k_compact_count(const uint8_t *__restrict__ flags,
-                                                                  const uint8_t *__restrict__ force,
-                                                                  uint64_t N, int full,
-                                                                  uint32_t *__restrict__ blk) {
-    const uint64_t base = (uint64_t)blockIdx.x * kPagesPerCompactBlock + threadIdx.x * kPagesPerThread;
-    uint32_t c = __popc(thread_dirty_mask(flags, force, base, N, full));
-    c = warp_sum(c);
-    __shared__ uint32_t s[kCompactThreads / 32];
-    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int i = 0; i < kCompactThreads / 32; ++i) t += s[i];
-        blk[blockIdx.x] = t;
-    }
-}
-
-__global__ void __launch_bounds__(kCompactThreads) k_compact_write(
-    const uint8_t *__restrict__ flags, const uint8_t *__restrict__ force, uint64_t N, int full,
-    const uint32_t *__restrict__ blk, uint32_t *__restrict__ gids, DevStats *st) {
-    // offset of this block = sum of the counts of all earlier blocks
-    uint64_t pre = 0;
-    for (uint32_t i = threadIdx.x; i < blockIdx.x; i += blockDim.x) pre += blk[i];
-    pre = warp_sum(pre);
-    __shared__ uint64_t s_pre[kCompactThreads / 32];
-    if ((threadIdx.x & 31) == 0) s_pre[threadIdx.x >> 5] = pre;
-    __syncthreads();
-    uint64_t offset = 0;
-    for (int i = 0; i < kCompactThreads / 32; ++i) offset += s_pre[i];
-
-    const uint64_t base = (uint64_t)blockIdx.x * kPagesPerCompactBlock + threadIdx.x * kPagesPerThread;
-    uint32_t m = thread_dirty_mask(flags, force, base, N, full);
-    uint64_t tot;
-    uint64_t pos = offset + block_excl_scan(__popc(m), &tot);
-    while (m) {
-        const uint32_t b = __ffs(m) - 1;
-        gids[pos++] = (uint32_t)(base + b);
-        m &= m - 1;
-    }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) st->K = offset + tot;
-}
-
-void launch_compact(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N, int full,
-                    uint32_t *blk_counts, uint32_t *gids, DevStats *st) {
-    const uint64_t nblk = (N + kPagesPerCompactBlock - 1) / kPagesPerCompactBlock;
-    if (nblk == 0) {
-        cudaMemsetAsync(&st->K, 0, sizeof(uint64_t), L.stream);
-        return;
-    }
-    k_compact_count<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(flags, force, N, full, blk_counts);
-    k_compact_write<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(flags, force, N, full, blk_counts,
-                                                                      gids, st);
-    *L.counter += 2;
-}
-
-// ---------------------------------------------------------------------------
-// Per-region stats + image header fields (single block).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t lower_bound_u32(const uint32_t *a, uint64_t n, uint64_t key) {
-    uint64_t lo = 0, hi = n;
-    while (lo < hi) {
-        uint64_t mid = (lo + hi) >> 1;
-        if ((uint64_t)a[mid] < key) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
-__global__ void __launch_bounds__(1024) k_region_stats(const DevRegion *__restrict__ regs, uint32_t R,
-                                                       const uint32_t *__restrict__ gids,
-                                                       RegStat *__restrict__ rs, DevStats *st,
-                                                       int full, int has_hashes, uint64_t capacity) {
-    const uint64_t K = st->K;
-    uint64_t carry_pb = 0, carry_u = 0;
-    for (uint32_t r0 = 0; r0 < R; r0 += blockDim.x) {
-        const uint32_t r = r0 + threadIdx.x;
-        uint64_t pb = 0, un = 0, first = 0, nd = 0;
-        if (r < R) {
-            const DevRegion g = regs[r];
-            first = lower_bound_u32(gids, K, g.page_base);
-            nd = lower_bound_u32(gids, K, g.page_base + g.n_pages) - first;
-            pb = nd << g.log2p;
-            un = nd << (g.log2p - kSegLog2);
-        }
-        uint64_t tpb, tun;
-        const uint64_t epb = block_excl_scan(pb, &tpb);
-        const uint64_t eun = block_excl_scan(un, &tun);
-        if (r < R) {
-            rs[r].first = first;
-            rs[r].n_dirty = nd;
-            rs[r].payload_base = carry_pb + epb;
-            rs[r].unit_base = carry_u + eun;
-        }
-        carry_pb += tpb;
-        carry_u += tun;
-    }
-    if (threadIdx.x == 0) {
-        const uint64_t meta = 64 + 48ull * R + round_up(4 * K, 8) + (has_hashes ? 8 * K : 0);
-        const uint64_t poff = round_up(meta, 4096);
-        st->meta_bytes = meta;
-        st->poff = poff;
-        st->payload_bytes = carry_pb;
-        st->total_units = carry_u;
-        st->image_bytes = poff + carry_pb;
-        st->capacity = capacity;
-        st->status = (poff + carry_pb > capacity) ? kStCapacity : kStOk;
-        st->img_flags = (full ? 1u : 0u) | (has_hashes ? 2u : 0u);
-        st->n_regions = R;
-        st->dirty_bytes = 0;
-        st->dirty_runs = 0;
-        st->crc_acc = 0;
-    }
-}
-
-void launch_region_stats(const Launch &L, const DevRegion *regs, uint32_t R, const uint32_t *gids,
-                         RegStat *rs, DevStats *st, int full, int has_hashes, uint64_t capacity) {
-    k_region_stats<<<1, 1024, 0, L.stream>>>(regs, R, gids, rs, st, full, has_hashes, capacity);
-    ++*L.counter;
-}
-
-// ---------------------------------------------------------------------------
-// Image metadata: region table, ids, hash list, zero padding; dirty bytes and
-// runs of the listed pages.
-// ---------------------------------------------------------------------------
+// Largest r with regs[r].page_base <= g.
 __device__ __forceinline__ uint32_t region_of_page(const DevRegion *regs, uint32_t R, uint64_t g) {
     uint32_t lo = 0, hi = R;
     while (hi - lo > 1) {
@@ -225,68 +93,224 @@ __device__ __forceinline__ uint32_t region_of_page(const DevRegion *regs, uint32
     return lo;
 }
 
-__global__ void __launch_bounds__(256) k_meta(const DevRegion *__restrict__ regs, uint32_t R,
-                                              const uint32_t *__restrict__ gids,
-                                              const uint64_t *__restrict__ newhash,
-                                              const RegStat *__restrict__ rs, DevStats *st,
-                                              uint8_t *__restrict__ img) {
-    if (st->status != kStOk) return;
-    const uint64_t K = st->K;
-    const bool has_hashes = (st->img_flags & 2u) != 0;
-    const uint64_t meta = st->meta_bytes, poff = st->poff;
-    uint32_t *ids = reinterpret_cast<uint32_t *>(img + 64 + 48ull * R);
-    uint64_t *hashes = reinterpret_cast<uint64_t *>(img + 64 + 48ull * R + round_up(4 * K, 8));
-    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t r = tid; r < R; r += nth) {
-        const DevRegion g = regs[r];
-        uint8_t *e = img + 64 + 48 * r;
-        reinterpret_cast<uint32_t *>(e)[0] = g.id;
-        reinterpret_cast<uint32_t *>(e)[1] = g.mode;
-        reinterpret_cast<uint64_t *>(e)[1] = g.bytes;
-        reinterpret_cast<uint64_t *>(e)[2] = 1ull << g.log2p;
-        reinterpret_cast<uint64_t *>(e)[3] = g.n_pages;
-        reinterpret_cast<uint64_t *>(e)[4] = rs[r].n_dirty;
-        reinterpret_cast<uint64_t *>(e)[5] = rs[r].first;
+__device__ __forceinline__ uint64_t page_len(const DevRegion &g, uint64_t i) {
+    const uint64_t off = i << g.log2p;
+    return min((uint64_t)1 << g.log2p, (uint64_t)(g.bytes - off));
+}
+
+// ---------------------------------------------------------------------------
+// A2 compaction
+// ---------------------------------------------------------------------------
+// Dirty mask of this thread's 16 pages [base, base+16) within [p_lo, p_hi).
+__device__ __forceinline__ uint32_t thread_mask(const CompactArgs &a, uint64_t base) {
+    uint32_t m = 0;
+    if (base >= a.p_hi) return 0;  // nothing of ours in range (also keeps loads in bounds)
+    if (a.full) {
+#pragma unroll
+        for (int b = 0; b < 16; ++b) m |= (base + b >= a.p_lo && base + b < a.p_hi ? 1u : 0u) << b;
+        return m;
     }
-    uint64_t dbytes = 0, runs = 0;
-    for (uint64_t k = tid; k < K; k += nth) {
-        const uint64_t gid = gids[k];
-        const uint32_t r = region_of_page(regs, R, gid);
-        const DevRegion g = regs[r];
-        const uint64_t i = gid - g.page_base;
-        ids[k] = (uint32_t)i;
-        if (has_hashes) hashes[k] = (g.mode == kModeHash) ? newhash[gid] : 0;
-        dbytes += min((uint64_t)1 << g.log2p, (uint64_t)(g.bytes - (i << g.log2p)));
-        runs += (k == rs[r].first || gids[k - 1] + 1 != gid) ? 1 : 0;
+    const uint4 f = *reinterpret_cast<const uint4 *>(a.flags + base);
+    const uint4 o = *reinterpret_cast<const uint4 *>(a.force + base);
+    const uint32_t fw[4] = {f.x, f.y, f.z, f.w}, ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint32_t fb = (fw[i] >> (8 * b)) & 0xffu, ob = (ow[i] >> (8 * b)) & 0xffu;
+            const uint64_t g = base + 4 * i + b;
+            m |= ((fb == a.tag || ob != 0) && g >= a.p_lo && g < a.p_hi ? 1u : 0u) << (4 * i + b);
+        }
+    return m;
+}
+
+// 4 KiB units of the dirty pages in mask (pages advance through regions).
+__device__ __forceinline__ uint64_t mask_units(const CompactArgs &a, uint64_t base, uint32_t m) {
+    if (!m) return 0;
+    uint32_t r = region_of_page(a.regs, a.R, base + (__ffs(m) - 1));
+    uint64_t next = (r + 1 < a.R) ? a.regs[r + 1].page_base : ~0ull;
+    uint32_t sh = a.regs[r].log2p - kSegLog2;
+    uint64_t u = 0;
+    while (m) {
+        const uint64_t g = base + (__ffs(m) - 1);
+        while (g >= next) {
+            ++r;
+            next = (r + 1 < a.R) ? a.regs[r + 1].page_base : ~0ull;
+            sh = a.regs[r].log2p - kSegLog2;
+        }
+        u += 1ull << sh;
+        m &= m - 1;
     }
-    if (tid == 0 && (K & 1)) ids[K] = 0;
-    for (uint64_t b = meta + tid; b < poff; b += nth) img[b] = 0;
+    return u;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) k_compact_count(CompactArgs a) {
+    if (a.first_range) {
+        for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.R;
+             r += (uint64_t)gridDim.x * blockDim.x)
+            a.reg_nd[r] = 0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.st->dirty_bytes = 0;
+            a.st->dirty_runs = 0;
+            a.st->crc_acc = 0;
+            a.st->status = kStOk;
+        }
+    }
+    const uint64_t base = a.p_lo + (uint64_t)blockIdx.x * kPagesPerCompactBlock + threadIdx.x * kPagesPerThread;
+    const uint32_t m = thread_mask(a, base);
+    const uint64_t c = block_sum(__popc(m));
+    const uint64_t u = block_sum(mask_units(a, base, m));
+    if (threadIdx.x == 0) {
+        a.blk_count[blockIdx.x] = (uint32_t)c;
+        a.blk_units[blockIdx.x] = u;
+    }
+}
+
+__global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a) {
+    __shared__ uint64_t s_off[2];
+    __shared__ bool s_last;
+    // offsets of this block = running totals before this range + earlier blocks
+    uint64_t pc = 0, pu = 0;
+    for (uint32_t i = threadIdx.x; i < blockIdx.x; i += blockDim.x) {
+        pc += a.blk_count[i];
+        pu += a.blk_units[i];
+    }
+    pc = block_sum(pc);
+    pu = block_sum(pu);
+    if (threadIdx.x == 0) {
+        s_off[0] = a.rb[a.c].k + pc;
+        s_off[1] = a.rb[a.c].units + pu;
+    }
+    const uint64_t base = a.p_lo + (uint64_t)blockIdx.x * kPagesPerCompactBlock + threadIdx.x * kPagesPerThread;
+    uint32_t m = thread_mask(a, base);
+    uint64_t tc, tu;
+    const uint64_t ec = block_excl_scan(__popc(m), &tc);
+    const uint64_t eu = block_excl_scan(mask_units(a, base, m), &tu);  // syncs: s_off visible
+    uint64_t pos = s_off[0] + ec, upos = s_off[1] + eu;
+    uint64_t dbytes = 0;
+    if (m) {
+        uint32_t r = region_of_page(a.regs, a.R, base + (__ffs(m) - 1));
+        DevRegion g = a.regs[r];
+        uint64_t next = (r + 1 < a.R) ? a.regs[r + 1].page_base : ~0ull;
+        uint32_t cnt = 0;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            const uint64_t gid = base + b;
+            while (gid >= next) {
+                if (cnt) atomicAdd(a.reg_nd + r, cnt);
+                cnt = 0;
+                ++r;
+                g = a.regs[r];
+                next = (r + 1 < a.R) ? a.regs[r + 1].page_base : ~0ull;
+            }
+            const uint64_t i = gid - g.page_base;
+            a.gids[pos] = (uint32_t)gid;
+            a.sunit[pos] = upos;
+            a.lids[pos] = (uint32_t)i;
+            if (a.has_hashes) a.lhash[pos] = (g.mode == kModeHash) ? a.newhash[gid] : 0;
+            dbytes += page_len(g, i);
+            ++cnt;
+            ++pos;
+            upos += 1ull << (g.log2p - kSegLog2);
+            m &= m - 1;
+        }
+        if (cnt) atomicAdd(a.reg_nd + r, cnt);
+    }
     dbytes = warp_sum(dbytes);
-    runs = warp_sum(runs);
-    if ((threadIdx.x & 31) == 0 && (dbytes | runs)) {
-        atomicAdd(reinterpret_cast<unsigned long long *>(&st->dirty_bytes), (unsigned long long)dbytes);
-        atomicAdd(reinterpret_cast<unsigned long long *>(&st->dirty_runs), (unsigned long long)runs);
+    if ((threadIdx.x & 31) == 0 && dbytes)
+        atomicAdd(reinterpret_cast<unsigned long long *>(&a.st->dirty_bytes), (unsigned long long)dbytes);
+    // ---- last block: publish running totals / finalise ----
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(a.done, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    uint64_t ac = 0, au = 0;
+    for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+        ac += a.blk_count[i];
+        au += a.blk_units[i];
+    }
+    ac = block_sum(ac);
+    au = block_sum(au);
+    const uint64_t K = a.rb[a.c].k + ac, U = a.rb[a.c].units + au;
+    if (threadIdx.x == 0) {
+        a.rb[a.c + 1].k = K;
+        a.rb[a.c + 1].units = U;
+        *a.done = 0;
+    }
+    if (!a.final_range) return;
+    // per-region prefix sums (first slot, payload offset, unit offset) + table
+    uint64_t carry_first = 0, carry_units = 0;
+    for (uint32_t r0 = 0; r0 < a.R; r0 += blockDim.x) {
+        const uint32_t r = r0 + threadIdx.x;
+        uint64_t nd = 0, un = 0;
+        DevRegion g{};
+        if (r < a.R) {
+            g = a.regs[r];
+            nd = *(volatile uint32_t *)(a.reg_nd + r);
+            un = nd << (g.log2p - kSegLog2);
+        }
+        uint64_t tn, tun;
+        const uint64_t en = block_excl_scan(nd, &tn);
+        const uint64_t eun = block_excl_scan(un, &tun);
+        if (r < a.R) {
+            RegStat s;
+            s.first = carry_first + en;
+            s.n_dirty = nd;
+            s.unit_base = carry_units + eun;
+            s.payload_base = s.unit_base << kSegLog2;
+            a.rs[r] = s;
+            if (a.head) {
+                uint8_t *e = a.head + 64 + 48ull * r;
+                reinterpret_cast<uint32_t *>(e)[0] = g.id;
+                reinterpret_cast<uint32_t *>(e)[1] = g.mode;
+                reinterpret_cast<uint64_t *>(e)[1] = g.bytes;
+                reinterpret_cast<uint64_t *>(e)[2] = 1ull << g.log2p;
+                reinterpret_cast<uint64_t *>(e)[3] = g.n_pages;
+                reinterpret_cast<uint64_t *>(e)[4] = nd;
+                reinterpret_cast<uint64_t *>(e)[5] = s.first;
+            }
+        }
+        carry_first += tn;
+        carry_units += tun;
+    }
+    const uint64_t poff = round_up(64 + 48ull * a.R, 4096);
+    const uint64_t payload = U << kSegLog2;
+    (void)carry_units;
+    const uint64_t ids_off = poff + payload;
+    const uint64_t image = ids_off + round_up(4 * K, 8) + (a.has_hashes ? 8 * K : 0);
+    if (a.head)
+        for (uint64_t b = 64 + 48ull * a.R + threadIdx.x; b < poff; b += blockDim.x) a.head[b] = 0;
+    if (threadIdx.x == 0) {
+        DevStats *st = a.st;
+        st->K = K;
+        st->total_units = U;
+        st->poff = poff;
+        st->payload_bytes = payload;
+        st->ids_off = ids_off;
+        st->image_bytes = image;
+        st->capacity = a.capacity;
+        st->status = image > a.capacity ? kStCapacity : kStOk;
+        st->img_flags = (a.full ? 1u : 0u) | (a.has_hashes ? 2u : 0u);
+        st->n_regions = a.R;
     }
 }
 
-void launch_meta(const Launch &L, const DevRegion *regs, uint32_t R, const uint32_t *gids,
-                 const uint64_t *newhash, const RegStat *rs, DevStats *st, uint8_t *img) {
-    k_meta<<<L.sms * 2, 256, 0, L.stream>>>(regs, R, gids, newhash, rs, st, img);
-    ++*L.counter;
+void launch_compact(const Launch &L, const CompactArgs &a) {
+    uint64_t nblk = a.p_hi > a.p_lo ? (a.p_hi - a.p_lo + kPagesPerCompactBlock - 1) / kPagesPerCompactBlock : 0;
+    if (nblk == 0) nblk = 1;  // an empty range still publishes its totals / finalises
+    k_compact_count<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(a);
+    k_compact_write<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(a);
+    *L.counter += 2;
 }
 
 // ---------------------------------------------------------------------------
-// A3 gather + commit (img == nullptr: commit only, i.e. crum_sync_shadow).
+// A3 gather + commit.  Units [u_lo, u_hi) of the range whose running totals
+// are rb[0] (before) and rb[1] (after); dst == nullptr: commit only.
+// Unit u is written at dst + (add_poff ? st->poff : 0) + (u - dst_unit0) * 4096.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t region_of_unit(const RegStat *rs, uint32_t R, uint64_t u) {
-    uint32_t lo = 0, hi = R;
-    while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (rs[mid].unit_base <= u) lo = mid; else hi = mid;
-    }
-    return lo;
-}
+constexpr uint32_t kUnitsPerTask = 8;
 
 // Copy one 4 KiB unit: `len` logical bytes from src (rest zero) to dst_a
 // (full 4 KiB, may be null) and the first `len` bytes to dst_b (may be null).
@@ -325,64 +349,76 @@ __device__ __forceinline__ void copy_unit(const uint8_t *src, uint64_t len, bool
     }
 }
 
-__global__ void __launch_bounds__(256) k_gather(const DevRegion *__restrict__ regs, uint32_t R,
-                                                const uint32_t *__restrict__ gids,
-                                                const uint64_t *__restrict__ newhash,
-                                                const RegStat *__restrict__ rs,
-                                                const DevStats *__restrict__ st,
-                                                uint8_t *__restrict__ dst_base, uint64_t dst_unit0,
-                                                int add_poff, uint8_t *__restrict__ force,
-                                                uint64_t unit_lo, uint64_t unit_hi) {
+// Largest k in [lo, hi) with sunit[k] <= u.
+__device__ __forceinline__ uint64_t slot_of_unit(const uint64_t *sunit, uint64_t lo, uint64_t hi, uint64_t u) {
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (sunit[mid] <= u) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
+    const DevStats *st = a.st;
     if (st->status != kStOk) return;
-    const uint64_t hi = min(unit_hi, st->total_units);
+    const uint64_t k_lo = a.rb[0].k, k_hi = a.rb[1].k;
+    const uint64_t u_lo = max(a.u_lo, a.rb[0].units), u_hi = min(a.u_hi, a.rb[1].units);
+    if (u_hi <= u_lo) return;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
-    uint8_t *payload = dst_base ? dst_base + (add_poff ? st->poff : 0) : nullptr;
-    for (uint64_t u = unit_lo + (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); u < hi; u += nwarps) {
-        const uint32_t r = region_of_unit(rs, R, u);
-        const DevRegion g = regs[r];
-        const RegStat s = rs[r];
-        const uint32_t sh = g.log2p - kSegLog2;
-        const uint64_t ru = u - s.unit_base;
-        const uint64_t j = ru >> sh, seg = ru & ((1ull << sh) - 1);
-        const uint64_t gid = gids[s.first + j];
-        const uint64_t i = gid - g.page_base;
-        const uint64_t off = (i << g.log2p) + (seg << kSegLog2);
-        const uint64_t len = g.bytes > off ? min((uint64_t)kSegBytes, g.bytes - off) : 0;
-        // payload byte offset of unit u is u * 4096 (slots are whole 4 KiB units)
-        uint8_t *dst_img = payload ? payload + ((u - dst_unit0) << kSegLog2) : nullptr;
-        uint8_t *dst_mir = (g.mode == kModeCompare) ? g.mirror + off : nullptr;
-        if (dst_img || dst_mir) copy_unit(g.base + off, len, g.aligned32 != 0, dst_img, dst_mir, lane);
-        if (seg == 0 && lane == 0) {
-            if (g.mode == kModeHash) g.table[i] = newhash[gid];
-            force[gid] = 0;
+    uint8_t *payload = a.dst ? a.dst + (a.add_poff ? st->poff : 0) : nullptr;
+    const uint64_t ntask = (u_hi - u_lo + kUnitsPerTask - 1) / kUnitsPerTask;
+    for (uint64_t t = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); t < ntask; t += nwarps) {
+        const uint64_t u0 = u_lo + t * kUnitsPerTask, u1 = min(u0 + kUnitsPerTask, u_hi);
+        uint64_t k = slot_of_unit(a.sunit, k_lo, k_hi, u0);
+        uint64_t gid = a.gids[k];
+        uint32_t r = region_of_page(a.regs, a.R, gid);
+        DevRegion g = a.regs[r];
+        uint64_t kbase = a.sunit[k];
+        for (uint64_t u = u0; u < u1; ++u) {
+            const uint64_t nxt = (k + 1 < k_hi) ? a.sunit[k + 1] : ~0ull;
+            if (u >= nxt) {
+                ++k;
+                kbase = nxt;
+                gid = a.gids[k];
+                if (r + 1 < a.R && gid >= a.regs[r + 1].page_base) {
+                    r = region_of_page(a.regs, a.R, gid);
+                    g = a.regs[r];
+                }
+            }
+            const uint64_t seg = u - kbase;
+            const uint64_t i = gid - g.page_base;
+            const uint64_t off = (i << g.log2p) + (seg << kSegLog2);
+            const uint64_t len = g.bytes > off ? min((uint64_t)kSegBytes, g.bytes - off) : 0;
+            uint8_t *dst_img = payload ? payload + ((u - a.dst_unit0) << kSegLog2) : nullptr;
+            uint8_t *dst_mir = (g.mode == kModeCompare) ? g.mirror + off : nullptr;
+            if (dst_img || dst_mir) copy_unit(g.base + off, len, g.aligned32 != 0, dst_img, dst_mir, lane);
+            if (seg == 0 && lane == 0) {
+                if (g.mode == kModeHash) g.table[i] = a.newhash[gid];
+                a.force[gid] = 0;
+            }
         }
     }
 }
 
-void launch_gather(const Launch &L, const DevRegion *regs, uint32_t R, const uint32_t *gids,
-                   const uint64_t *newhash, const RegStat *rs, const DevStats *st, uint8_t *dst_base,
-                   uint64_t dst_unit0, int add_poff, uint8_t *force, uint64_t unit_lo, uint64_t unit_hi) {
-    if (unit_hi <= unit_lo || !R) return;
-    uint64_t blocks = (unit_hi - unit_lo + 7) / 8;
+void launch_gather(const Launch &L, const GatherArgs &a, uint64_t max_units) {
+    if (!a.R || !max_units) return;
+    uint64_t blocks = (max_units + kUnitsPerTask * 8 - 1) / (kUnitsPerTask * 8);
     const uint64_t cap = (uint64_t)L.sms * 8;
     if (blocks > cap) blocks = cap;
-    k_gather<<<(unsigned)blocks, 256, 0, L.stream>>>(regs, R, gids, newhash, rs, st, dst_base, dst_unit0,
-                                                     add_poff, force, unit_lo, unit_hi);
+    if (!blocks) blocks = 1;
+    k_gather<<<(unsigned)blocks, 256, 0, L.stream>>>(a);
     ++*L.counter;
 }
 
 // ---------------------------------------------------------------------------
-// CRC-32 (zlib) of the metadata [64, meta_bytes) and the header.
+// CRC-32 (zlib) of table || ids || hashes, copy of the tail into the image,
+// header (last block).
 // ---------------------------------------------------------------------------
-struct X2N {
-    uint32_t t[32];  // x^(2^k) mod P, reflected
-};
-
 __device__ __forceinline__ uint32_t gf2_mulmod(uint32_t a, uint32_t b) {
-    // reflected GF(2)[x] product mod the CRC-32 polynomial (loop ends at the
-    // lowest set bit of a, so a == 0 must be handled up front)
+    // reflected GF(2)[x] product mod the CRC-32 polynomial (the loop ends at
+    // the lowest set bit of a, so a == 0 is handled up front)
     if (a == 0) return 0;
     uint32_t m = 0x80000000u, p = 0;
     for (;;) {
@@ -408,11 +444,109 @@ __device__ __forceinline__ uint32_t xpow8n(uint64_t n, const uint32_t *x2n) {
     return p;
 }
 
-constexpr uint32_t kCrcChunk = 256;
+__device__ __forceinline__ void put32(uint8_t *p, uint32_t v) {
+    for (int i = 0; i < 4; ++i) p[i] = (uint8_t)(v >> (8 * i));
+}
+__device__ __forceinline__ void put64(uint8_t *p, uint64_t v) {
+    for (int i = 0; i < 8; ++i) p[i] = (uint8_t)(v >> (8 * i));
+}
 
-__global__ void __launch_bounds__(256) k_crc_meta(const uint8_t *__restrict__ img, DevStats *st,
-                                                  X2N x2n) {
+constexpr uint32_t kCrcChunk = 64;
+
+// Byte v of the virtual stream table || ids(padded) || hashes.
+__device__ __forceinline__ uint8_t meta_byte(const CrcArgs &a, uint64_t tab, uint64_t idsb, uint64_t K,
+                                             uint64_t v) {
+    if (v < tab) return a.head[64 + v];
+    v -= tab;
+    if (v < idsb) return v < 4 * K ? reinterpret_cast<const uint8_t *>(a.lids)[v] : 0;
+    return reinterpret_cast<const uint8_t *>(a.lhash)[v - idsb];
+}
+
+__global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
+    DevStats *st = a.st;
     if (st->status != kStOk) return;
+    __shared__ uint32_t T[256];
+    __shared__ uint32_t sx[32];
+    __shared__ bool s_last;
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
+        uint32_t c = i;
+        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+        T[i] = c;
+    }
+    if (threadIdx.x < 32) sx[threadIdx.x] = a.x2n.t[threadIdx.x];
+    __syncthreads();
+    const uint64_t K = st->K, R = st->n_regions;
+    const bool hh = (st->img_flags & 2u) != 0;
+    const uint64_t tab = 48 * R, idsb = round_up(4 * K, 8), len = tab + idsb + (hh ? 8 * K : 0);
+    uint8_t *tail = a.tail ? a.tail : a.head + st->ids_off;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    // copy ids (+pad) and hashes into the image tail
+    uint32_t *tids = reinterpret_cast<uint32_t *>(tail);
+    for (uint64_t k = tid; k < idsb / 4; k += nth) tids[k] = k < K ? a.lids[k] : 0u;
+    if (hh) {
+        uint64_t *th = reinterpret_cast<uint64_t *>(tail + idsb);
+        for (uint64_t k = tid; k < K; k += nth) th[k] = a.lhash[k];
+    }
+    // runs of consecutive page ids (a run starts at a region's page 0 or after a gap)
+    uint64_t runs = 0;
+    for (uint64_t k = tid; k < K; k += nth)
+        runs += (k == 0 || a.lids[k] == 0 || a.gids[k - 1] + 1 != a.gids[k]) ? 1 : 0;
+    runs = warp_sum(runs);
+    if ((threadIdx.x & 31) == 0 && runs)
+        atomicAdd(reinterpret_cast<unsigned long long *>(&st->dirty_runs), (unsigned long long)runs);
+    // CRC terms (zlib's ~0 initial register folded into chunk 0)
+    const uint64_t nchunks = (len + kCrcChunk - 1) / kCrcChunk;
+    uint32_t acc = 0;
+    for (uint64_t c = tid; c < nchunks; c += nth) {
+        const uint64_t b0 = c * kCrcChunk, b1 = min(len, b0 + kCrcChunk);
+        uint32_t raw = (c == 0) ? 0xffffffffu : 0u;
+        for (uint64_t b = b0; b < b1; ++b) raw = T[(raw ^ meta_byte(a, tab, idsb, K, b)) & 0xffu] ^ (raw >> 8);
+        acc ^= gf2_mulmod(xpow8n(len - b1, sx), raw);  // first operand is never 0
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicXor(&st->crc_acc, acc);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(a.done, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    *a.done = 0;
+    // empty stream: zlib crc32("") == 0
+    const uint32_t meta_crc = (len == 0) ? 0u : (*(volatile uint32_t *)&st->crc_acc ^ 0xffffffffu);
+    st->meta_crc = meta_crc;
+    uint8_t h[64];
+    h[0] = 'C'; h[1] = 'R'; h[2] = 'U'; h[3] = 'M';
+    put32(h + 4, 1);
+    put32(h + 8, st->img_flags);
+    put32(h + 12, (uint32_t)R);
+    put64(h + 16, K);
+    put64(h + 24, st->poff);
+    put64(h + 32, st->payload_bytes);
+    put64(h + 40, st->ids_off);
+    put64(h + 48, st->image_bytes);
+    put32(h + 56, meta_crc);
+    uint32_t c = 0xffffffffu;
+    for (int i = 0; i < 60; ++i) c = T[(c ^ h[i]) & 0xffu] ^ (c >> 8);
+    put32(h + 60, c ^ 0xffffffffu);
+    for (int i = 0; i < 64; ++i) a.head[i] = h[i];
+}
+
+void launch_crc_meta(const Launch &L, const CrcArgs &a, uint64_t max_len) {
+    uint64_t blocks = (max_len / kCrcChunk + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    if (blocks > (uint64_t)L.sms * 2) blocks = L.sms * 2;
+    k_crc_meta<<<(unsigned)blocks, 256, 0, L.stream>>>(a);
+    ++*L.counter;
+}
+
+// CRC terms only (restore validation): XOR of shifted raw chunk CRCs of
+// table || tail into st->crc_acc (host finalises).
+__global__ void __launch_bounds__(256) k_crc_check(const uint8_t *__restrict__ table, uint64_t tab,
+                                                   const uint8_t *__restrict__ tail, uint64_t tl, DevStats *st,
+                                                   X2N x2n) {
     __shared__ uint32_t T[256];
     __shared__ uint32_t sx[32];
     for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -422,73 +556,41 @@ __global__ void __launch_bounds__(256) k_crc_meta(const uint8_t *__restrict__ im
     }
     if (threadIdx.x < 32) sx[threadIdx.x] = x2n.t[threadIdx.x];
     __syncthreads();
-    const uint64_t len = st->meta_bytes - 64;
-    const uint8_t *data = img + 64;
+    const uint64_t len = tab + tl;
     const uint64_t nchunks = (len + kCrcChunk - 1) / kCrcChunk;
     uint32_t acc = 0;
     for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks;
          c += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t b0 = c * kCrcChunk, b1 = min(len, b0 + kCrcChunk);
-        uint32_t raw = 0;
-        for (uint64_t b = b0; b < b1; ++b) raw = T[(raw ^ data[b]) & 0xffu] ^ (raw >> 8);
-        acc ^= gf2_mulmod(xpow8n(len - b1, sx), raw);  // first operand is never 0
+        uint32_t raw = (c == 0) ? 0xffffffffu : 0u;
+        for (uint64_t b = b0; b < b1; ++b) {
+            const uint8_t v = b < tab ? table[b] : tail[b - tab];
+            raw = T[(raw ^ v) & 0xffu] ^ (raw >> 8);
+        }
+        acc ^= gf2_mulmod(xpow8n(len - b1, sx), raw);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0 && acc) atomicXor(&st->crc_acc, acc);
 }
 
-void launch_crc_meta(const Launch &L, const uint8_t *img, DevStats *st, const uint32_t *x2n) {
-    X2N x;
-    for (int i = 0; i < 32; ++i) x.t[i] = x2n[i];
-    k_crc_meta<<<L.sms * 2, 256, 0, L.stream>>>(img, st, x);
-    ++*L.counter;
-}
-
-__device__ __forceinline__ void put32(uint8_t *p, uint32_t v) {
-    for (int i = 0; i < 4; ++i) p[i] = (uint8_t)(v >> (8 * i));
-}
-__device__ __forceinline__ void put64(uint8_t *p, uint64_t v) {
-    for (int i = 0; i < 8; ++i) p[i] = (uint8_t)(v >> (8 * i));
-}
-
-__global__ void k_header(uint8_t *img, DevStats *st, X2N x2n) {
-    if (st->status != kStOk) return;
-    const uint64_t len = st->meta_bytes - 64;
-    const uint32_t meta_crc = st->crc_acc ^ gf2_mulmod(0xffffffffu, xpow8n(len, x2n.t)) ^ 0xffffffffu;
-    st->meta_crc = meta_crc;
-    uint8_t h[64];
-    h[0] = 'C'; h[1] = 'R'; h[2] = 'U'; h[3] = 'M';
-    put32(h + 4, 1);
-    put32(h + 8, st->img_flags);
-    put32(h + 12, st->n_regions);
-    put64(h + 16, st->K);
-    put64(h + 24, st->meta_bytes);
-    put64(h + 32, st->poff);
-    put64(h + 40, st->payload_bytes);
-    put32(h + 48, meta_crc);
-    put64(h + 52, 0);
-    uint32_t c = 0xffffffffu;
-    for (int i = 0; i < 60; ++i) {
-        c ^= h[i];
-        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
-    }
-    put32(h + 60, c ^ 0xffffffffu);
-    for (int i = 0; i < 64; ++i) img[i] = h[i];
-}
-
-void launch_header(const Launch &L, uint8_t *img, DevStats *st, const uint32_t *x2n) {
-    X2N x;
-    for (int i = 0; i < 32; ++i) x.t[i] = x2n[i];
-    k_header<<<1, 1, 0, L.stream>>>(img, st, x);
+void launch_crc_check(const Launch &L, const uint8_t *table, uint64_t tab, const uint8_t *tail, uint64_t tl,
+                      DevStats *st, const X2N &x2n) {
+    uint64_t blocks = ((tab + tl) / kCrcChunk + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    if (blocks > (uint64_t)L.sms * 2) blocks = L.sms * 2;
+    k_crc_check<<<(unsigned)blocks, 256, 0, L.stream>>>(table, tab, tail, tl, st, x2n);
     ++*L.counter;
 }
 
 // ---------------------------------------------------------------------------
 // A6 restore: validation of the id list, then scatter + commit.
-// rs[] here comes from the image's region table (validated on the host).
+// rs[] comes from the image's region table (validated on the host); tregs
+// are descriptors built from that table (n_pages, mode, page size).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t region_of_slot(const RegStat *rs, uint32_t R, uint64_t k) {
+    // the LAST region whose first slot is <= k (regions listing no slot share
+    // `first` with their successor)
     uint32_t lo = 0, hi = R;
     while (hi - lo > 1) {
         uint32_t mid = (lo + hi) >> 1;
@@ -497,27 +599,24 @@ __device__ __forceinline__ uint32_t region_of_slot(const RegStat *rs, uint32_t R
     return lo;
 }
 
-__global__ void __launch_bounds__(256) k_restore_validate(const DevRegion *__restrict__ regs, uint32_t R,
+__global__ void __launch_bounds__(256) k_restore_validate(const DevRegion *__restrict__ tregs, uint32_t R,
                                                           const RegStat *__restrict__ rs,
-                                                          const uint8_t *__restrict__ img,
+                                                          const uint32_t *__restrict__ ids,
+                                                          const uint64_t *__restrict__ hashes, uint64_t K,
                                                           DevStats *st) {
-    const uint64_t K = st->K;
-    const bool has_hashes = (st->img_flags & 2u) != 0;
-    const uint32_t *ids = reinterpret_cast<const uint32_t *>(img + 64 + 48ull * R);
-    const uint64_t *hashes = reinterpret_cast<const uint64_t *>(img + 64 + 48ull * R + round_up(4 * K, 8));
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
     uint32_t bad = 0;
     uint64_t dbytes = 0, runs = 0;
     for (uint64_t k = tid; k < K; k += nth) {
         const uint32_t r = region_of_slot(rs, R, k);
-        const DevRegion g = regs[r];
+        const DevRegion g = tregs[r];
         const uint64_t i = ids[k];
         const bool first = (k == rs[r].first);
         if (i >= g.n_pages) bad = 1;
         if (!first && ids[k - 1] >= i) bad = 1;
-        if (has_hashes && g.mode == kModeCompare && hashes[k] != 0) bad = 1;
-        if (i < g.n_pages) dbytes += min((uint64_t)1 << g.log2p, (uint64_t)(g.bytes - (i << g.log2p)));
+        if (hashes && g.mode == kModeCompare && hashes[k] != 0) bad = 1;
+        if (i < g.n_pages) dbytes += page_len(g, i);
         runs += (first || ids[k - 1] + 1 != i) ? 1 : 0;
     }
     bad = __any_sync(0xffffffffu, bad);
@@ -532,42 +631,40 @@ __global__ void __launch_bounds__(256) k_restore_validate(const DevRegion *__res
     }
 }
 
-void launch_restore_validate(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
-                             const uint8_t *img, DevStats *st) {
-    if (!R) return;
-    k_restore_validate<<<L.sms * 2, 256, 0, L.stream>>>(regs, R, rs, img, st);
+void launch_restore_validate(const Launch &L, const DevRegion *tregs, uint32_t R, const RegStat *rs,
+                             const uint32_t *ids, const uint64_t *hashes, uint64_t K, DevStats *st) {
+    if (!R || !K) return;
+    k_restore_validate<<<L.sms * 2, 256, 0, L.stream>>>(tregs, R, rs, ids, hashes, K, st);
     ++*L.counter;
 }
 
-__global__ void __launch_bounds__(256) k_scatter(const DevRegion *__restrict__ regs, uint32_t R,
-                                                 const RegStat *__restrict__ rs,
-                                                 const uint8_t *__restrict__ meta,
-                                                 const DevStats *__restrict__ st,
-                                                 const uint8_t *__restrict__ src_base, uint64_t src_unit0,
-                                                 int add_poff, uint8_t *__restrict__ force,
-                                                 uint64_t unit_lo, uint64_t unit_hi) {
-    if (st->status != kStOk) return;
-    const uint64_t K = st->K;
-    const uint32_t *ids = reinterpret_cast<const uint32_t *>(meta + 64 + 48ull * R);
-    const uint64_t *hashes = reinterpret_cast<const uint64_t *>(meta + 64 + 48ull * R + round_up(4 * K, 8));
-    const uint8_t *payload = src_base + (add_poff ? st->poff : 0);
-    const uint64_t hi = min(unit_hi, st->total_units);
+__device__ __forceinline__ uint32_t region_of_unit(const RegStat *rs, uint32_t R, uint64_t u) {
+    uint32_t lo = 0, hi = R;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (rs[mid].unit_base <= u) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_scatter(ScatterArgs a) {
+    if (a.st->status != kStOk) return;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
-    for (uint64_t u = unit_lo + (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); u < hi; u += nwarps) {
-        const uint32_t r = region_of_unit(rs, R, u);
-        const DevRegion g = regs[r];
-        const RegStat s = rs[r];
+    for (uint64_t u = a.u_lo + (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); u < a.u_hi; u += nwarps) {
+        const uint32_t r = region_of_unit(a.rs, a.R, u);
+        const DevRegion g = a.regs[r];
+        const RegStat s = a.rs[r];
         const uint32_t sh = g.log2p - kSegLog2;
         const uint64_t ru = u - s.unit_base;
         const uint64_t j = ru >> sh, seg = ru & ((1ull << sh) - 1);
         const uint64_t k = s.first + j;
-        const uint64_t i = ids[k];
+        const uint64_t i = a.ids[k];
         const uint64_t off = (i << g.log2p) + (seg << kSegLog2);
         if (g.bytes > off) {
             const uint64_t len = min((uint64_t)kSegBytes, g.bytes - off);
-            const uint8_t *src = payload + ((u - src_unit0) << kSegLog2);
+            const uint8_t *src = a.src + ((u - a.src_unit0) << kSegLog2);
             uint8_t *dst_mir = (g.mode == kModeCompare) ? g.mirror + off : nullptr;
             if (len == kSegBytes) {
                 copy_unit(src, len, g.aligned32 != 0, g.base + off, dst_mir, lane);
@@ -579,37 +676,34 @@ __global__ void __launch_bounds__(256) k_scatter(const DevRegion *__restrict__ r
             }
         }
         if (seg == 0 && lane == 0) {
-            if (g.mode == kModeHash) g.table[i] = hashes[k];
-            force[g.page_base + i] = 0;
+            if (g.mode == kModeHash) g.table[i] = a.hashes[k];
+            a.force[g.page_base + i] = 0;
         }
     }
 }
 
-void launch_scatter(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
-                    const uint8_t *meta, const DevStats *st, const uint8_t *src_base, uint64_t src_unit0,
-                    int add_poff, uint8_t *force, uint64_t unit_lo, uint64_t unit_hi) {
-    if (unit_hi <= unit_lo || !R) return;
-    uint64_t blocks = (unit_hi - unit_lo + 7) / 8;
+void launch_scatter(const Launch &L, const ScatterArgs &a) {
+    if (a.u_hi <= a.u_lo || !a.R) return;
+    uint64_t blocks = (a.u_hi - a.u_lo + 7) / 8;
     const uint64_t cap = (uint64_t)L.sms * 8;
     if (blocks > cap) blocks = cap;
-    k_scatter<<<(unsigned)blocks, 256, 0, L.stream>>>(regs, R, rs, meta, st, src_base, src_unit0, add_poff,
-                                                      force, unit_lo, unit_hi);
+    k_scatter<<<(unsigned)blocks, 256, 0, L.stream>>>(a);
     ++*L.counter;
 }
 
 // ---------------------------------------------------------------------------
-// debug: flags | force, global page order
+// debug: (flags == tag) | force, global page order
 // ---------------------------------------------------------------------------
-__global__ void k_export_flags(const uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t *out) {
+__global__ void k_export_flags(const uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag, uint8_t *out) {
     for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < N;
          g += (uint64_t)gridDim.x * blockDim.x)
-        out[g] = (flags[g] | force[g]) ? 1 : 0;
+        out[g] = (flags[g] == tag || force[g]) ? 1 : 0;
 }
 
-void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N,
+void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag,
                          uint8_t *out) {
     if (!N) return;
-    k_export_flags<<<L.sms * 4, 256, 0, L.stream>>>(flags, force, N, out);
+    k_export_flags<<<L.sms * 4, 256, 0, L.stream>>>(flags, force, N, tag, out);
     ++*L.counter;
 }
 

@@ -2,9 +2,10 @@
 //
 // Responsibilities: region registry and device
 // descriptors, shadow storage (mirrors / hash tables / force bits), scratch,
-// the gather -> D2H and H2D -> scatter chunk pipelines (side copy stream,
-// events), image header/table validation, error state.  All data-parallel
-// work runs in the kernels of kernels_detect.cu / kernels_image.cu.
+// the range-pipelined gather -> D2H and the chunked H2D -> scatter paths
+// (side streams, events), image header/table validation, error state.  All
+// data-parallel work runs in the kernels of kernels_detect.cu and
+// kernels_image.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,11 +34,11 @@ void set_detail(const char *fmt, ...) {
     g_detail = buf;
 }
 
-// --- host CRC-32 (zlib) helpers, used for the 60-byte header and to finalise
-// --- the device-computed metadata CRC.
+// --- host CRC-32 (zlib) helpers: the 60-byte header check and the device
+// --- CRC kernels' x^(2^k) table.
 struct CrcTables {
     uint32_t byte[256];
-    uint32_t x2n[32];  // x^(2^k) mod P (reflected)
+    X2N x2n;  // x^(2^k) mod P (reflected)
 };
 
 uint32_t gf2_mulmod_host(uint32_t a, uint32_t b) {
@@ -62,8 +63,8 @@ const CrcTables &crc_tables() {
             for (int k = 0; k < 8; ++k) v = (v >> 1) ^ (0xEDB88320u & (0u - (v & 1u)));
             c.byte[i] = v;
         }
-        c.x2n[0] = 0x40000000u;  // x^1
-        for (int k = 1; k < 32; ++k) c.x2n[k] = gf2_mulmod_host(c.x2n[k - 1], c.x2n[k - 1]);
+        c.x2n.t[0] = 0x40000000u;  // x^1
+        for (int k = 1; k < 32; ++k) c.x2n.t[k] = gf2_mulmod_host(c.x2n.t[k - 1], c.x2n.t[k - 1]);
         return c;
     }();
     return t;
@@ -74,18 +75,6 @@ uint32_t crc32_host(const uint8_t *p, size_t n) {
     uint32_t c = 0xffffffffu;
     for (size_t i = 0; i < n; ++i) c = t.byte[(c ^ p[i]) & 0xffu] ^ (c >> 8);
     return c ^ 0xffffffffu;
-}
-
-uint32_t xpow8n_host(uint64_t n) {
-    const CrcTables &t = crc_tables();
-    uint32_t p = 0x80000000u;
-    uint32_t k = 3;
-    while (n) {
-        if (n & 1) p = gf2_mulmod_host(t.x2n[k & 31], p);
-        n >>= 1;
-        ++k;
-    }
-    return p;
 }
 
 inline uint64_t rd64(const uint8_t *p) {
@@ -99,9 +88,9 @@ inline uint32_t rd32(const uint8_t *p) {
     return v;
 }
 
-uint64_t meta_bytes_for(uint64_t R, uint64_t K, bool has_hashes) {
-    return 64 + 48 * R + round_up(4 * K, 8) + (has_hashes ? 8 * K : 0);
-}
+// Image format v1 layout.
+uint64_t payload_offset_for(uint64_t R) { return round_up(64 + 48 * R, 4096); }
+uint64_t tail_bytes_for(uint64_t K, bool has_hashes) { return round_up(4 * K, 8) + (has_hashes ? 8 * K : 0); }
 
 struct HostRegion {
     uint32_t id;
@@ -112,10 +101,19 @@ struct HostRegion {
     uint64_t n_pages;
     uint32_t log2p;
     void *shadow;  // device mirror (compare) or hash table (hash)
+    uint64_t page_base;
+};
+
+// A page range of the pipelined host path, with the matching compare-segment
+// and hash-group ranges of the detect kernels.
+struct Range {
+    uint64_t p_lo, p_hi, s_lo, s_hi, w_lo, w_hi;
 };
 
 constexpr uint64_t kDefaultChunk = 64ull << 20;
 constexpr int kRing = 3;
+constexpr int kMaxRanges = 32;
+constexpr uint64_t kMinRangeBytes = 128ull << 20;
 constexpr uint64_t kMaxTotalPages = 0x7fffffffull;
 
 }  // namespace
@@ -132,21 +130,22 @@ struct crum_ctx {
     int sms = 148;
     uint64_t chunk = kDefaultChunk;
     std::vector<HostRegion> regs;
+    std::vector<Range> ranges;
+    Range all{};
     uint32_t next_id = 1;
-    uint64_t N = 0, F = 0;
+    uint64_t N = 0, F = 0, max_units = 0;
     bool poisoned = false;
     uint64_t launches = 0;
+    uint8_t tag = 0;
 
     // device descriptors (rebuilt on register / unregister)
     DevRegion *d_regs = nullptr;
     uint32_t *d_cmp_idx = nullptr;
     uint64_t *d_cmp_seg = nullptr;
     uint32_t n_cmp = 0;
-    uint64_t n_seg = 0;
     uint32_t *d_hash_idx = nullptr;
     uint64_t *d_hash_grp = nullptr;
     uint32_t n_hash = 0;
-    uint64_t n_grp = 0;
     bool any_hash = false;
 
     // per-page arrays (padded to kPagesPerCompactBlock)
@@ -155,24 +154,34 @@ struct crum_ctx {
     uint8_t *d_flags = nullptr;
     uint64_t *d_newhash = nullptr;
     uint32_t *d_gids = nullptr;
-    uint32_t *d_blk = nullptr;
+    uint64_t *d_sunit = nullptr;
+    uint32_t *d_lids = nullptr;
+    uint64_t *d_lhash = nullptr;
+    uint32_t *d_blk_count = nullptr;
+    uint64_t *d_blk_units = nullptr;
     uint8_t *d_dbg = nullptr;
 
+    uint32_t *d_reg_nd = nullptr;
     RegStat *d_rs = nullptr;
     uint64_t rs_cap = 0;
     DevRegion *d_tregs = nullptr;  // restore: descriptors built from an image table
     uint64_t tregs_cap = 0;
+    RangeTotals *d_rb = nullptr;   // kMaxRanges + 1
+    RangeTotals *h_rb = nullptr;   // pinned mirror
+    uint32_t *d_done = nullptr;    // [0] compaction, [1] crc
     DevStats *d_st = nullptr;
-    DevStats *h_st = nullptr;  // pinned
+    DevStats *h_st = nullptr;      // pinned
 
-    uint8_t *d_meta = nullptr;  // host path: image metadata [0, poff)
+    uint8_t *d_meta = nullptr;     // host path: image head [0, poff) then the tail
     uint64_t meta_cap = 0;
     uint8_t *d_ring[kRing] = {nullptr, nullptr, nullptr};
     uint64_t ring_cap = 0;
 
-    cudaStream_t copy = nullptr;
+    cudaStream_t copy = nullptr;    // D2H / H2D
+    cudaStream_t gstream = nullptr; // gathers of the pipelined host path
     cudaEvent_t ev_gather[kRing];
     cudaEvent_t ev_copy[kRing];
+    cudaEvent_t ev_range[kMaxRanges];
     cudaEvent_t ev_t[6];
     cudaEvent_t ev_meta;
 };
@@ -217,6 +226,7 @@ uint64_t pad_pages(uint64_t n) { return round_up(n ? n : 1, kPagesPerCompactBloc
 
 template <typename T>
 int dev_alloc(crum_ctx *c, T **p, uint64_t bytes) {
+    (void)c;
     void *q = nullptr;
     cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
     if (e != cudaSuccess) {
@@ -239,18 +249,43 @@ int upload(crum_ctx *c, void *dst, const void *src, uint64_t bytes) {
     return CRUM_OK;
 }
 
+// Compare segments / hash groups of the pages before global page p.
+uint64_t seg_at(const crum_ctx *c, uint64_t p) {
+    uint64_t s = 0;
+    for (const HostRegion &h : c->regs) {
+        if (h.mode != kModeCompare) continue;
+        if (p >= h.page_base + h.n_pages) s += (h.bytes + kSegBytes - 1) / kSegBytes;
+        else if (p > h.page_base) s += (p - h.page_base) << (h.log2p - kSegLog2);
+    }
+    return s;
+}
+uint64_t grp_at(const crum_ctx *c, uint64_t p, bool ceil) {
+    uint64_t w = 0;
+    for (const HostRegion &h : c->regs) {
+        if (h.mode != kModeHash) continue;
+        const uint64_t k = p >= h.page_base + h.n_pages ? h.n_pages : (p > h.page_base ? p - h.page_base : 0);
+        w += h.log2p == kSegLog2 ? (ceil ? (k + 1) / 2 : k / 2) : k;
+    }
+    return w;
+}
+
+Range make_range(const crum_ctx *c, uint64_t lo, uint64_t hi) {
+    return Range{lo, hi, seg_at(c, lo), seg_at(c, hi), grp_at(c, lo, false), grp_at(c, hi, true)};
+}
+
 // Rebuild device descriptors and per-page arrays after the registry changed.
-// `old_force_map`: for each new region index, the page base of that region's
-// force bits in the OLD force array (or UINT64_MAX for a new region -> all 1).
+// old_force_base[r]: page base of region r's force bits in the OLD force
+// array, or UINT64_MAX for a new region (all force-dirty).
 int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
     const uint32_t R = (uint32_t)c->regs.size();
     std::vector<DevRegion> dr(R);
     std::vector<uint32_t> cmp_idx, hash_idx;
     std::vector<uint64_t> cmp_seg{0}, hash_grp{0};
-    uint64_t N = 0, F = 0;
+    uint64_t N = 0, F = 0, units = 0;
     bool any_hash = false;
     for (uint32_t r = 0; r < R; ++r) {
-        const HostRegion &h = c->regs[r];
+        HostRegion &h = c->regs[r];
+        h.page_base = N;
         DevRegion &d = dr[r];
         d.base = h.ptr;
         d.mirror = h.mode == kModeCompare ? static_cast<uint8_t *>(h.shadow) : nullptr;
@@ -272,8 +307,8 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
         }
         N += h.n_pages;
         F += h.bytes;
+        units += h.n_pages << (h.log2p - kSegLog2);
     }
-    // new per-page arrays
     const uint64_t cap = pad_pages(N);
     uint8_t *force = nullptr;
     int st;
@@ -291,12 +326,18 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
         dev_free(c->d_flags);
         dev_free(c->d_newhash);
         dev_free(c->d_gids);
-        dev_free(c->d_blk);
+        dev_free(c->d_sunit);
+        dev_free(c->d_lids);
+        dev_free(c->d_lhash);
+        dev_free(c->d_blk_count);
+        dev_free(c->d_blk_units);
         dev_free(c->d_dbg);
         c->page_cap = 0;
+        const uint64_t nblk = cap / kPagesPerCompactBlock + 1;
         if ((st = dev_alloc(c, &c->d_flags, cap)) || (st = dev_alloc(c, &c->d_newhash, cap * 8)) ||
-            (st = dev_alloc(c, &c->d_gids, cap * 4)) ||
-            (st = dev_alloc(c, &c->d_blk, (cap / kPagesPerCompactBlock) * 4 + 16)) ||
+            (st = dev_alloc(c, &c->d_gids, cap * 4)) || (st = dev_alloc(c, &c->d_sunit, cap * 8)) ||
+            (st = dev_alloc(c, &c->d_lids, cap * 4 + 8)) || (st = dev_alloc(c, &c->d_lhash, cap * 8)) ||
+            (st = dev_alloc(c, &c->d_blk_count, nblk * 4)) || (st = dev_alloc(c, &c->d_blk_units, nblk * 8)) ||
             (st = dev_alloc(c, &c->d_dbg, cap))) {
             cudaFree(force);
             return st;
@@ -304,6 +345,7 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
         c->page_cap = cap;
     }
     CK(cudaMemset(c->d_flags, 0, c->page_cap));
+    c->tag = 0;
     dev_free(c->d_force);
     c->d_force = force;
     // descriptors
@@ -312,11 +354,12 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
     dev_free(c->d_cmp_seg);
     dev_free(c->d_hash_idx);
     dev_free(c->d_hash_grp);
+    dev_free(c->d_reg_nd);
     if ((st = dev_alloc(c, &c->d_regs, sizeof(DevRegion) * R)) ||
         (st = dev_alloc(c, &c->d_cmp_idx, 4 * cmp_idx.size())) ||
         (st = dev_alloc(c, &c->d_cmp_seg, 8 * cmp_seg.size())) ||
         (st = dev_alloc(c, &c->d_hash_idx, 4 * hash_idx.size())) ||
-        (st = dev_alloc(c, &c->d_hash_grp, 8 * hash_grp.size())))
+        (st = dev_alloc(c, &c->d_hash_grp, 8 * hash_grp.size())) || (st = dev_alloc(c, &c->d_reg_nd, 4 * R + 4)))
         return st;
     if ((st = upload(c, c->d_regs, dr.data(), sizeof(DevRegion) * R)) ||
         (st = upload(c, c->d_cmp_idx, cmp_idx.data(), 4 * cmp_idx.size())) ||
@@ -325,26 +368,47 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
         (st = upload(c, c->d_hash_grp, hash_grp.data(), 8 * hash_grp.size())))
         return st;
     c->n_cmp = (uint32_t)cmp_idx.size();
-    c->n_seg = cmp_seg.back();
     c->n_hash = (uint32_t)hash_idx.size();
-    c->n_grp = hash_grp.back();
     c->any_hash = any_hash;
     c->N = N;
     c->F = F;
-    // per-region scratch and the host-path metadata buffer
+    c->max_units = units;
+    // per-region scratch and the host-path metadata buffer (head + tail)
     if (R + 1 > c->rs_cap) {
         dev_free(c->d_rs);
         c->rs_cap = 0;
         if ((st = dev_alloc(c, &c->d_rs, sizeof(RegStat) * (R + 1)))) return st;
         c->rs_cap = R + 1;
     }
-    const uint64_t meta_max = round_up(meta_bytes_for(R, N, any_hash), 4096);
+    const uint64_t meta_max = payload_offset_for(R) + tail_bytes_for(N, true) + 4096;
     if (meta_max > c->meta_cap) {
         dev_free(c->d_meta);
         c->meta_cap = 0;
         if ((st = dev_alloc(c, &c->d_meta, meta_max))) return st;
         c->meta_cap = meta_max;
     }
+    // page ranges of the pipelined host path: ~F/8 bytes each (>= 128 MiB),
+    // boundaries on multiples of 16 pages
+    c->all = make_range(c, 0, N);
+    c->ranges.clear();
+    const uint64_t target = std::max(kMinRangeBytes, F / 8);
+    uint64_t lo = 0, acc = 0;
+    for (uint32_t r = 0; r < R; ++r) {
+        const HostRegion &h = c->regs[r];
+        for (uint64_t i = 0; i < h.n_pages; ++i) {
+            const uint64_t g = h.page_base + i;
+            if (acc >= target && g % 16 == 0 && (int)c->ranges.size() < kMaxRanges - 1) {
+                c->ranges.push_back(make_range(c, lo, g));
+                lo = g;
+                acc = 0;
+            }
+            // whole pages at a time is fine for large regions; skip ahead in big steps
+            const uint64_t step = std::min<uint64_t>(h.n_pages - i, 16 - (g % 16));
+            acc += step * h.page_size;
+            i += step - 1;
+        }
+    }
+    c->ranges.push_back(make_range(c, lo, N));
     return CRUM_OK;
 }
 
@@ -378,35 +442,94 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
     return ms;
 }
 
-// A1 + A2 + per-region stats (+ the image metadata and CRCs if meta_img).
-// Enqueued on s; nothing is committed.
-int enqueue_detect_compact(crum_ctx *c, cudaStream_t s, bool full, uint64_t capacity, bool timing) {
-    Launch L = launch_of(c, s);
-    const uint32_t R = (uint32_t)c->regs.size();
-    if (timing) CK(cudaEventRecord(c->ev_t[0], s));
-    CK(cudaMemsetAsync(c->d_flags, 0, pad_pages(c->N), s));
-    if (!full) launch_detect_compare(L, c->d_regs, c->d_cmp_idx, c->d_cmp_seg, c->n_cmp, c->n_seg, c->d_force,
-                                     c->d_flags);
-    launch_detect_hash(L, c->d_regs, c->d_hash_idx, c->d_hash_grp, c->n_hash, c->n_grp, c->d_flags,
-                       c->d_newhash);
-    CK_LAUNCH();
-    if (timing) CK(cudaEventRecord(c->ev_t[1], s));
-    launch_compact(L, c->d_flags, c->d_force, c->N, full ? 1 : 0, c->d_blk, c->d_gids, c->d_st);
-    launch_region_stats(L, c->d_regs, R, c->d_gids, c->d_rs, c->d_st, full ? 1 : 0, c->any_hash ? 1 : 0,
-                        capacity);
-    CK_LAUNCH();
+// Next per-checkpoint flag tag (1..255); on wrap the flags array is cleared.
+int next_tag(crum_ctx *c, cudaStream_t s) {
+    if (c->tag == 255 || c->tag == 0) {
+        CK(cudaMemsetAsync(c->d_flags, 0, c->page_cap, s));
+        c->tag = 0;
+    }
+    ++c->tag;
     return CRUM_OK;
 }
 
-int enqueue_meta(crum_ctx *c, cudaStream_t s, uint8_t *img) {
+void enqueue_detect(crum_ctx *c, cudaStream_t s, const Range &rg, bool full) {
     Launch L = launch_of(c, s);
-    const uint32_t R = (uint32_t)c->regs.size();
-    launch_meta(L, c->d_regs, R, c->d_gids, c->d_newhash, c->d_rs, c->d_st, img);
-    launch_crc_meta(L, img, c->d_st, crc_tables().x2n);
-    launch_header(L, img, c->d_st, crc_tables().x2n);
-    CK_LAUNCH();
-    return CRUM_OK;
+    if (!full)
+        launch_detect_compare(L, c->d_regs, c->d_cmp_idx, c->d_cmp_seg, c->n_cmp, rg.s_lo, rg.s_hi, c->d_force,
+                              c->d_flags, c->tag);
+    launch_detect_hash(L, c->d_regs, c->d_hash_idx, c->d_hash_grp, c->n_hash, rg.w_lo, rg.w_hi, c->d_flags,
+                       c->d_newhash, c->tag);
 }
+
+CompactArgs compact_args(crum_ctx *c, const Range &rg, uint32_t ci, bool first, bool final, bool full,
+                         uint64_t capacity, uint8_t *head) {
+    CompactArgs a{};
+    a.flags = c->d_flags;
+    a.force = c->d_force;
+    a.regs = c->d_regs;
+    a.newhash = c->d_newhash;
+    a.p_lo = rg.p_lo;
+    a.p_hi = rg.p_hi;
+    a.R = (uint32_t)c->regs.size();
+    a.tag = c->tag;
+    a.full = full ? 1 : 0;
+    a.has_hashes = c->any_hash ? 1 : 0;
+    a.first_range = first ? 1 : 0;
+    a.final_range = final ? 1 : 0;
+    a.c = ci;
+    a.blk_count = c->d_blk_count;
+    a.blk_units = c->d_blk_units;
+    a.gids = c->d_gids;
+    a.sunit = c->d_sunit;
+    a.lids = c->d_lids;
+    a.lhash = c->d_lhash;
+    a.reg_nd = c->d_reg_nd;
+    a.rb = c->d_rb;
+    a.done = c->d_done;
+    a.rs = c->d_rs;
+    a.st = c->d_st;
+    a.capacity = capacity;
+    a.head = head;
+    return a;
+}
+
+// Compaction of one range (an empty range still runs one block, whose "last
+// block" step advances the running totals and finalises).
+void enqueue_compact(crum_ctx *c, cudaStream_t s, const CompactArgs &a) { launch_compact(launch_of(c, s), a); }
+
+CrcArgs crc_args(crum_ctx *c, uint8_t *head, uint8_t *tail) {
+    CrcArgs a{};
+    a.head = head;
+    a.tail = tail;
+    a.lids = c->d_lids;
+    a.lhash = c->d_lhash;
+    a.gids = c->d_gids;
+    a.st = c->d_st;
+    a.done = c->d_done + 1;
+    a.x2n = crc_tables().x2n;
+    return a;
+}
+
+GatherArgs gather_args(crum_ctx *c, uint32_t ci, uint8_t *dst, uint64_t dst_unit0, bool add_poff, uint64_t u_lo,
+                       uint64_t u_hi) {
+    GatherArgs a{};
+    a.regs = c->d_regs;
+    a.R = (uint32_t)c->regs.size();
+    a.add_poff = add_poff ? 1 : 0;
+    a.gids = c->d_gids;
+    a.sunit = c->d_sunit;
+    a.newhash = c->d_newhash;
+    a.rb = c->d_rb + ci;
+    a.st = c->d_st;
+    a.dst = dst;
+    a.dst_unit0 = dst_unit0;
+    a.force = c->d_force;
+    a.u_lo = u_lo;
+    a.u_hi = u_hi;
+    return a;
+}
+
+uint64_t crc_max_len(const crum_ctx *c) { return 48ull * c->regs.size() + 12 * c->N + 8; }
 
 void fill_report(crum_ctx *c, const DevStats &h, crum_report *rep) {
     rep->scanned_pages = c->N;
@@ -469,18 +592,28 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     };
     if (cudaSetDevice(device) != cudaSuccess) return fail(CRUM_E_CUDA);
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
-    if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess) return fail(CRUM_E_CUDA);
+    if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(CRUM_E_CUDA);
     for (int i = 0; i < kRing; ++i) {
         if (cudaEventCreateWithFlags(&c->ev_gather[i], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming) != cudaSuccess)
             return fail(CRUM_E_CUDA);
     }
+    for (int i = 0; i < kMaxRanges; ++i)
+        if (cudaEventCreateWithFlags(&c->ev_range[i], cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
     for (int i = 0; i < 6; ++i)
         if (cudaEventCreate(&c->ev_t[i]) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaMalloc(&c->d_st, sizeof(DevStats)) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    if (cudaMalloc(&c->d_rb, sizeof(RangeTotals) * (kMaxRanges + 1)) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    if (cudaMalloc(&c->d_done, 16) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocDefault) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    if (cudaHostAlloc(&c->h_rb, sizeof(RangeTotals) * (kMaxRanges + 1), cudaHostAllocDefault) != cudaSuccess)
+        return fail(CRUM_E_NOMEM);
     cudaMemset(c->d_st, 0, sizeof(DevStats));
+    cudaMemset(c->d_rb, 0, sizeof(RangeTotals) * (kMaxRanges + 1));
+    cudaMemset(c->d_done, 0, 16);
     std::vector<uint64_t> none;
     int st = rebuild(c, none);
     if (st) return fail(st);
@@ -502,19 +635,30 @@ int crum_destroy(crum_ctx *c) {
     dev_free(c->d_flags);
     dev_free(c->d_newhash);
     dev_free(c->d_gids);
-    dev_free(c->d_blk);
+    dev_free(c->d_sunit);
+    dev_free(c->d_lids);
+    dev_free(c->d_lhash);
+    dev_free(c->d_blk_count);
+    dev_free(c->d_blk_units);
     dev_free(c->d_dbg);
+    dev_free(c->d_reg_nd);
     dev_free(c->d_rs);
     dev_free(c->d_tregs);
+    dev_free(c->d_rb);
+    dev_free(c->d_done);
     dev_free(c->d_st);
     dev_free(c->d_meta);
     for (int i = 0; i < kRing; ++i) dev_free(c->d_ring[i]);
     if (c->h_st) cudaFreeHost(c->h_st);
+    if (c->h_rb) cudaFreeHost(c->h_rb);
     if (c->copy) cudaStreamDestroy(c->copy);
+    if (c->gstream) cudaStreamDestroy(c->gstream);
     for (int i = 0; i < kRing; ++i) {
         if (c->ev_gather[i]) cudaEventDestroy(c->ev_gather[i]);
         if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
     }
+    for (int i = 0; i < kMaxRanges; ++i)
+        if (c->ev_range[i]) cudaEventDestroy(c->ev_range[i]);
     for (int i = 0; i < 6; ++i)
         if (c->ev_t[i]) cudaEventDestroy(c->ev_t[i]);
     if (c->ev_meta) cudaEventDestroy(c->ev_meta);
@@ -549,7 +693,6 @@ int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page
     }
     const uintptr_t lo = reinterpret_cast<uintptr_t>(ptr), hi = lo + bytes;
     if (hi < lo) return CRUM_E_INVAL;
-    // device accessibility of both ends
     for (uintptr_t a : {lo, hi - 1}) {
         cudaPointerAttributes at{};
         if (cudaPointerGetAttributes(&at, reinterpret_cast<void *>(a)) != cudaSuccess) {
@@ -584,13 +727,8 @@ int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page
     int st = dev_alloc(c, &h.shadow, shadow_bytes);
     if (st) return st;
     CK(cudaMemset(h.shadow, 0, shadow_bytes));
-    // keep old force bits of existing regions, new region all-dirty
     std::vector<uint64_t> old_base;
-    uint64_t pb = 0;
-    for (const HostRegion &o : c->regs) {
-        old_base.push_back(pb);
-        pb += o.n_pages;
-    }
+    for (const HostRegion &o : c->regs) old_base.push_back(o.page_base);
     old_base.push_back(UINT64_MAX);
     h.id = c->next_id;
     c->regs.push_back(h);
@@ -614,11 +752,8 @@ int crum_unregister_region(crum_ctx *ctx, uint32_t id) {
     }
     CK(cudaDeviceSynchronize());
     std::vector<uint64_t> old_base;
-    uint64_t pb = 0;
-    for (uint32_t r = 0; r < c->regs.size(); ++r) {
-        if (r != idx) old_base.push_back(pb);
-        pb += c->regs[r].n_pages;
-    }
+    for (uint32_t r = 0; r < c->regs.size(); ++r)
+        if (r != idx) old_base.push_back(c->regs[r].page_base);
     HostRegion gone = c->regs[idx];
     c->regs.erase(c->regs.begin() + idx);
     int st = rebuild(c, old_base);
@@ -629,8 +764,7 @@ int crum_unregister_region(crum_ctx *ctx, uint32_t id) {
 
 int crum_mark_dirty(crum_ctx *ctx, uint32_t id, uint64_t off, uint64_t len) {
     ENTER(ctx);
-    uint32_t idx;
-    HostRegion *h = find_region(c, id, &idx);
+    HostRegion *h = find_region(c, id);
     if (!h) {
         set_detail("no region %u", id);
         return CRUM_E_NOREGION;
@@ -641,13 +775,11 @@ int crum_mark_dirty(crum_ctx *ctx, uint32_t id, uint64_t off, uint64_t len) {
         return CRUM_E_RANGE;
     }
     if (!len) return CRUM_OK;
-    uint64_t pb = 0;
-    for (uint32_t r = 0; r < idx; ++r) pb += c->regs[r].n_pages;
     const uint64_t i0 = off / h->page_size, i1 = (off + len - 1) / h->page_size;
     // device-synchronous: ordered after every earlier call on any stream and
     // visible to every later one
     CK(cudaDeviceSynchronize());
-    CK(cudaMemset(c->d_force + pb + i0, 1, i1 - i0 + 1));
+    CK(cudaMemset(c->d_force + h->page_base + i0, 1, i1 - i0 + 1));
     CK(cudaDeviceSynchronize());
     return CRUM_OK;
 }
@@ -662,7 +794,7 @@ int crum_image_required_bytes(crum_ctx *ctx, uint64_t max_dirty, uint64_t *out) 
         maxp = std::max(maxp, h.page_size);
     }
     if (K < c->N && K * maxp < payload) payload = K * maxp;
-    *out = round_up(meta_bytes_for(c->regs.size(), K, c->any_hash), 4096) + payload;
+    *out = payload_offset_for(c->regs.size()) + payload + tail_bytes_for(K, c->any_hash);
     return CRUM_OK;
 }
 
@@ -707,19 +839,18 @@ int crum_image_destroy(crum_image *img) {
 }
 
 // ---------------------------------------------------------------------------
-// A7: sync shadow
+// A7: sync shadow = detect + compact + commit (no image)
 // ---------------------------------------------------------------------------
 int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
     ENTER(ctx);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    int st = enqueue_detect_compact(c, s, false, UINT64_MAX, false);
-    if (st) return st;
+    int st;
+    if ((st = next_tag(c, s))) return st;
+    CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
+    enqueue_detect(c, s, c->all, false);
+    enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, false, UINT64_MAX, nullptr));
     Launch L = launch_of(c, s);
-    // commit every listed page: at most every page's units
-    uint64_t max_units = 0;
-    for (const HostRegion &h : c->regs) max_units += h.n_pages * (h.page_size >> kSegLog2);
-    launch_gather(L, c->d_regs, (uint32_t)c->regs.size(), c->d_gids, c->d_newhash, c->d_rs, c->d_st, nullptr, 0,
-                  0, c->d_force, 0, max_units);
+    launch_gather(L, gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX), c->max_units);
     CK_LAUNCH();
     if (dirty_out) {
         CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
@@ -730,7 +861,8 @@ int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
 }
 
 // ---------------------------------------------------------------------------
-// A1-A3 into a device image
+// A1-A3 into a device image: detect, compact (+ table, header fields),
+// gather (+ commit), CRC (+ tail, header).  Fully stream-ordered.
 // ---------------------------------------------------------------------------
 int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capacity, void *stream,
                                   uint32_t flags, crum_report *rep) {
@@ -751,27 +883,30 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     const bool full = flags & CRUM_FULL;
     const bool timing = rep != nullptr;
     uint8_t *img = static_cast<uint8_t *>(dev_image);
-    int st = enqueue_detect_compact(c, s, full, capacity, timing);
-    if (st) return st;
-    if ((st = enqueue_meta(c, s, img))) return st;
+    int st;
+    if (timing) CK(cudaEventRecord(c->ev_t[0], s));
+    if ((st = next_tag(c, s))) return st;
+    CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
+    enqueue_detect(c, s, c->all, full);
+    if (timing) CK(cudaEventRecord(c->ev_t[1], s));
+    enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, full, capacity, img));
     if (timing) CK(cudaEventRecord(c->ev_t[2], s));
-    uint64_t max_units = 0;
-    for (const HostRegion &h : c->regs) max_units += h.n_pages * (h.page_size >> kSegLog2);
     Launch L = launch_of(c, s);
-    launch_gather(L, c->d_regs, (uint32_t)c->regs.size(), c->d_gids, c->d_newhash, c->d_rs, c->d_st, img, 0, 1,
-                  c->d_force, 0, max_units);
+    launch_gather(L, gather_args(c, 0, img, 0, true, 0, UINT64_MAX), c->max_units);
+    if (timing) CK(cudaEventRecord(c->ev_t[3], s));
+    launch_crc_meta(L, crc_args(c, img, nullptr), crc_max_len(c));
     CK_LAUNCH();
     if (timing) {
-        CK(cudaEventRecord(c->ev_t[3], s));
+        CK(cudaEventRecord(c->ev_t[4], s));
         CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         const DevStats h = *c->h_st;
         memset(rep, 0, sizeof *rep);
         fill_report(c, h, rep);
         rep->t_detect_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
-        rep->t_compact_ms = ev_ms(c->ev_t[1], c->ev_t[2]);
+        rep->t_compact_ms = ev_ms(c->ev_t[1], c->ev_t[2]) + ev_ms(c->ev_t[3], c->ev_t[4]);
         rep->t_gather_ms = ev_ms(c->ev_t[2], c->ev_t[3]);
-        rep->t_total_ms = ev_ms(c->ev_t[0], c->ev_t[3]);
+        rep->t_total_ms = ev_ms(c->ev_t[0], c->ev_t[4]);
         if (h.status == kStCapacity) {
             set_detail("image needs %llu bytes, capacity %llu", (unsigned long long)h.image_bytes,
                        (unsigned long long)capacity);
@@ -782,8 +917,13 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
 }
 
 // ---------------------------------------------------------------------------
-// A1-A4 into a pinned host image: metadata on the device, payload gathered
-// chunk by chunk into a device ring and copied D2H on the copy stream.
+// A1-A4 into a pinned host image.  The page space is cut into ranges; for
+// each range detect + compact run on the caller's stream, the host reads the
+// range's running totals and immediately enqueues gathers (side stream, into
+// a ring of device chunks) and D2H copies (copy stream) of its payload, so
+// the host-link transfer of range c overlaps the detection of range c+1.
+// If the image cannot hold a worst-case image, the call first waits for all
+// ranges and checks capacity before committing anything.
 // ---------------------------------------------------------------------------
 int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_t flags, crum_report *rep) {
     ENTER(ctx);
@@ -795,56 +935,89 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     const bool full = flags & CRUM_FULL;
     int st = ensure_ring(c);
     if (st) return st;
-    if ((st = enqueue_detect_compact(c, s, full, UINT64_MAX, true))) return st;
-    if ((st = enqueue_meta(c, s, c->d_meta))) return st;
-    CK(cudaEventRecord(c->ev_t[2], s));
-    CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const DevStats h = *c->h_st;
-    if (h.image_bytes > img->cap) {
-        if (rep) {
-            memset(rep, 0, sizeof *rep);
-            fill_report(c, h, rep);
-        }
-        set_detail("image needs %llu bytes, capacity %llu", (unsigned long long)h.image_bytes,
-                   (unsigned long long)img->cap);
-        return CRUM_E_CAPACITY;
-    }
-    // metadata (with zero padding up to poff) -> host
-    CK(cudaEventRecord(c->ev_meta, s));
-    CK(cudaStreamWaitEvent(c->copy, c->ev_meta, 0));
-    CK(cudaEventRecord(c->ev_t[4], c->copy));
-    CK(cudaMemcpyAsync(img->host, c->d_meta, h.poff, cudaMemcpyDeviceToHost, c->copy));
-    // payload chunks
-    Launch L = launch_of(c, s);
-    const uint64_t units_per_chunk = c->chunk >> kSegLog2;
-    const uint32_t R = (uint32_t)c->regs.size();
-    uint64_t chunk_idx = 0;
-    for (uint64_t u0 = 0; u0 < h.total_units; u0 += units_per_chunk, ++chunk_idx) {
-        const uint64_t u1 = std::min(h.total_units, u0 + units_per_chunk);
-        const int slot = (int)(chunk_idx % kRing);
-        if (chunk_idx >= (uint64_t)kRing) CK(cudaStreamWaitEvent(s, c->ev_copy[slot], 0));
-        launch_gather(L, c->d_regs, R, c->d_gids, c->d_newhash, c->d_rs, c->d_st, c->d_ring[slot], u0, 0,
-                      c->d_force, u0, u1);
+    uint64_t worst;
+    crum_image_required_bytes(c, UINT64_MAX, &worst);
+    const bool pipelined = img->cap >= worst;
+    const uint32_t nr = (uint32_t)c->ranges.size();
+    CK(cudaEventRecord(c->ev_t[0], s));
+    if ((st = next_tag(c, s))) return st;
+    CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
+    for (uint32_t ci = 0; ci < nr; ++ci) {
+        const Range &rg = c->ranges[ci];
+        enqueue_detect(c, s, rg, full);
+        enqueue_compact(c, s,
+                        compact_args(c, rg, ci, ci == 0, ci + 1 == nr, full, UINT64_MAX, c->d_meta));
         CK_LAUNCH();
-        CK(cudaEventRecord(c->ev_gather[slot], s));
-        CK(cudaStreamWaitEvent(c->copy, c->ev_gather[slot], 0));
-        CK(cudaMemcpyAsync(img->host + h.poff + (u0 << kSegLog2), c->d_ring[slot], (u1 - u0) << kSegLog2,
-                           cudaMemcpyDeviceToHost, c->copy));
-        CK(cudaEventRecord(c->ev_copy[slot], c->copy));
+        CK(cudaMemcpyAsync(c->h_rb + ci + 1, c->d_rb + ci + 1, sizeof(RangeTotals), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(c->ev_range[ci], s));
     }
-    CK(cudaEventRecord(c->ev_t[3], s));
-    CK(cudaEventRecord(c->ev_t[5], c->copy));
+    CK(cudaEventRecord(c->ev_t[1], s));
+    // metadata: CRC + tail into d_meta (tail after the head [0, poff))
+    const uint64_t poff = payload_offset_for(c->regs.size());
+    Launch L = launch_of(c, s);
+    launch_crc_meta(L, crc_args(c, c->d_meta, c->d_meta + poff), crc_max_len(c));
+    CK_LAUNCH();
     CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(cudaEventRecord(c->ev_meta, s));
+    if (!pipelined) {
+        CK(cudaEventSynchronize(c->ev_meta));
+        if (c->h_st->image_bytes > img->cap) {
+            if (rep) {
+                memset(rep, 0, sizeof *rep);
+                fill_report(c, *c->h_st, rep);
+            }
+            set_detail("image needs %llu bytes, capacity %llu", (unsigned long long)c->h_st->image_bytes,
+                       (unsigned long long)img->cap);
+            return CRUM_E_CAPACITY;
+        }
+    }
+    // payload: per range, gathers into the ring + D2H
+    Launch G = launch_of(c, c->gstream);
+    const uint64_t upc = c->chunk >> kSegLog2;
+    uint64_t chunk_idx = 0;
+    bool copy_started = false;
+    c->h_rb[0] = RangeTotals{0, 0};
+    for (uint32_t ci = 0; ci < nr; ++ci) {
+        CK(cudaEventSynchronize(c->ev_range[ci]));
+        const uint64_t U0 = c->h_rb[ci].units, U1 = c->h_rb[ci + 1].units;
+        if (U1 > U0) CK(cudaStreamWaitEvent(c->gstream, c->ev_range[ci], 0));
+        for (uint64_t u0 = U0; u0 < U1; u0 += upc, ++chunk_idx) {
+            const uint64_t u1 = std::min(U1, u0 + upc);
+            const int slot = (int)(chunk_idx % kRing);
+            if (chunk_idx >= (uint64_t)kRing) CK(cudaStreamWaitEvent(c->gstream, c->ev_copy[slot], 0));
+            launch_gather(G, gather_args(c, ci, c->d_ring[slot], u0, false, u0, u1), u1 - u0);
+            CK_LAUNCH();
+            CK(cudaEventRecord(c->ev_gather[slot], c->gstream));
+            CK(cudaStreamWaitEvent(c->copy, c->ev_gather[slot], 0));
+            if (!copy_started) {
+                CK(cudaEventRecord(c->ev_t[4], c->copy));
+                copy_started = true;
+            }
+            CK(cudaMemcpyAsync(img->host + poff + (u0 << kSegLog2), c->d_ring[slot], (u1 - u0) << kSegLog2,
+                               cudaMemcpyDeviceToHost, c->copy));
+            CK(cudaEventRecord(c->ev_copy[slot], c->copy));
+        }
+    }
+    // header + table, then ids/hashes
+    CK(cudaEventSynchronize(c->ev_meta));
+    const DevStats h = *c->h_st;
+    CK(cudaStreamWaitEvent(c->copy, c->ev_meta, 0));
+    if (!copy_started) CK(cudaEventRecord(c->ev_t[4], c->copy));
+    CK(cudaMemcpyAsync(img->host, c->d_meta, poff, cudaMemcpyDeviceToHost, c->copy));
+    if (h.image_bytes > h.ids_off)
+        CK(cudaMemcpyAsync(img->host + h.ids_off, c->d_meta + poff, h.image_bytes - h.ids_off,
+                           cudaMemcpyDeviceToHost, c->copy));
+    CK(cudaEventRecord(c->ev_t[5], c->copy));
+    CK(cudaEventRecord(c->ev_t[3], c->gstream));
+    CK(cudaStreamSynchronize(c->gstream));
     CK(cudaStreamSynchronize(c->copy));
+    CK(cudaStreamSynchronize(s));
     img->len = h.image_bytes;
     if (rep) {
         memset(rep, 0, sizeof *rep);
-        fill_report(c, *c->h_st, rep);
+        fill_report(c, h, rep);
         rep->t_detect_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
-        rep->t_compact_ms = ev_ms(c->ev_t[1], c->ev_t[2]);
-        rep->t_gather_ms = ev_ms(c->ev_t[2], c->ev_t[3]);
+        rep->t_gather_ms = ev_ms(c->ev_t[0], c->ev_t[3]);
         rep->t_copy_ms = ev_ms(c->ev_t[4], c->ev_t[5]);
         rep->t_total_ms = ev_ms(c->ev_t[0], c->ev_t[5]);
     }
@@ -858,14 +1031,13 @@ namespace {
 
 struct ParsedImage {
     uint32_t flags, R;
-    uint64_t K, meta, poff, payload;
+    uint64_t K, poff, payload, ids_off, image;
     std::vector<RegStat> rs;
     std::vector<DevRegion> tregs;
 };
 
-// Host-side checks of the header and region table (all CORRUPT conditions
-// that do not need the id list), then the live-set comparison is done by the
-// caller AFTER the device checks.  hdr: 64 bytes; tab: 48 * R bytes.
+// Host-side checks of the header (every CORRUPT condition that needs no
+// device data).
 int parse_header(const uint8_t *hdr, uint64_t len, ParsedImage &p) {
     if (len < 64 || memcmp(hdr, "CRUM", 4) != 0) return CRUM_E_CORRUPT;
     if (crc32_host(hdr, 60) != rd32(hdr + 60)) return CRUM_E_CORRUPT;
@@ -873,13 +1045,16 @@ int parse_header(const uint8_t *hdr, uint64_t len, ParsedImage &p) {
     p.flags = rd32(hdr + 8);
     p.R = rd32(hdr + 12);
     p.K = rd64(hdr + 16);
-    p.meta = rd64(hdr + 24);
-    p.poff = rd64(hdr + 32);
-    p.payload = rd64(hdr + 40);
-    if (version != 1 || (p.flags & ~3u) || rd64(hdr + 52) != 0) return CRUM_E_CORRUPT;
+    p.poff = rd64(hdr + 24);
+    p.payload = rd64(hdr + 32);
+    p.ids_off = rd64(hdr + 40);
+    p.image = rd64(hdr + 48);
+    if (version != 1 || (p.flags & ~3u)) return CRUM_E_CORRUPT;
     if (p.K > kMaxTotalPages || p.R > 0x7fffffffu) return CRUM_E_CORRUPT;
-    if (p.meta != meta_bytes_for(p.R, p.K, p.flags & 2u) || p.poff != round_up(p.meta, 4096)) return CRUM_E_CORRUPT;
-    if (len < p.poff || len - p.poff < p.payload) return CRUM_E_CORRUPT;
+    if (p.poff != payload_offset_for(p.R) || p.payload > (1ull << 62) || p.ids_off != p.poff + p.payload ||
+        p.image != p.ids_off + tail_bytes_for(p.K, p.flags & 2u))
+        return CRUM_E_CORRUPT;
+    if (len < p.image) return CRUM_E_CORRUPT;
     return CRUM_OK;
 }
 
@@ -960,20 +1135,33 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
         set_detail("bad image region table");
         return st;
     }
+    const bool hh = (p.flags & 2u) != 0;
+    const uint64_t tail_len = p.image - p.ids_off;
+    const uint64_t tab_len = 48ull * p.R;
     const bool timing = rep != nullptr;
     if (timing) CK(cudaEventRecord(c->ev_t[0], s));
-    // metadata on the device
-    const uint8_t *meta = dev_img;
+    // table + tail on the device
+    const uint8_t *d_table, *d_tail;
     if (host_img) {
-        if (p.meta > c->meta_cap) {
+        const uint64_t need = round_up(tab_len, 16) + tail_len + 16;
+        if (need > c->meta_cap) {
             dev_free(c->d_meta);
             c->meta_cap = 0;
-            if ((st = dev_alloc(c, &c->d_meta, round_up(p.meta, 4096)))) return st;
-            c->meta_cap = round_up(p.meta, 4096);
+            if ((st = dev_alloc(c, &c->d_meta, need))) return st;
+            c->meta_cap = need;
         }
-        CK(cudaMemcpyAsync(c->d_meta, host_img, p.meta, cudaMemcpyHostToDevice, s));
-        meta = c->d_meta;
+        if (tab_len) CK(cudaMemcpyAsync(c->d_meta, host_img + 64, tab_len, cudaMemcpyHostToDevice, s));
+        if (tail_len)
+            CK(cudaMemcpyAsync(c->d_meta + round_up(tab_len, 16), host_img + p.ids_off, tail_len,
+                               cudaMemcpyHostToDevice, s));
+        d_table = c->d_meta;
+        d_tail = c->d_meta + round_up(tab_len, 16);
+    } else {
+        d_table = dev_img + 64;
+        d_tail = dev_img + p.ids_off;
     }
+    const uint32_t *d_ids = reinterpret_cast<const uint32_t *>(d_tail);
+    const uint64_t *d_hashes = hh ? reinterpret_cast<const uint64_t *>(d_tail + round_up(4 * p.K, 8)) : nullptr;
     if (p.R + 1 > c->rs_cap) {
         dev_free(c->d_rs);
         c->rs_cap = 0;
@@ -988,10 +1176,10 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
     }
     DevStats hs{};
     hs.K = p.K;
-    hs.meta_bytes = p.meta;
     hs.poff = p.poff;
     hs.payload_bytes = p.payload;
-    hs.image_bytes = p.poff + p.payload;
+    hs.ids_off = p.ids_off;
+    hs.image_bytes = p.image;
     hs.total_units = p.payload >> kSegLog2;
     hs.img_flags = p.flags;
     hs.n_regions = p.R;
@@ -1002,17 +1190,16 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
         CK(cudaMemcpyAsync(c->d_tregs, p.tregs.data(), sizeof(DevRegion) * p.R, cudaMemcpyHostToDevice, s));
     }
     Launch L = launch_of(c, s);
-    launch_crc_meta(L, meta, c->d_st, crc_tables().x2n);
-    launch_restore_validate(L, c->d_tregs, p.R, c->d_rs, meta, c->d_st);
+    if (tab_len + tail_len) launch_crc_check(L, d_table, tab_len, d_tail, tail_len, c->d_st, crc_tables().x2n);
+    launch_restore_validate(L, c->d_tregs, p.R, c->d_rs, d_ids, d_hashes, p.K, c->d_st);
     CK_LAUNCH();
     CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     {
         const DevStats h = *c->h_st;
-        const uint64_t mlen = p.meta - 64;
-        const uint32_t meta_crc = h.crc_acc ^ gf2_mulmod_host(0xffffffffu, xpow8n_host(mlen)) ^ 0xffffffffu;
-        if (meta_crc != rd32(hdr + 48) || h.status != kStOk) {
-            set_detail(meta_crc != rd32(hdr + 48) ? "metadata CRC mismatch" : "bad page id list");
+        const uint32_t meta_crc = (tab_len + tail_len == 0) ? 0u : (h.crc_acc ^ 0xffffffffu);
+        if (meta_crc != rd32(hdr + 56) || h.status != kStOk) {
+            set_detail(meta_crc != rd32(hdr + 56) ? "metadata CRC mismatch" : "bad page id list");
             return CRUM_E_CORRUPT;
         }
     }
@@ -1022,16 +1209,14 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
     }
     // CRUM_VERIFY: hash every hash-mode slot before writing anything
     uint8_t *d_payload_tmp = nullptr;
-    const uint8_t *payload_dev = dev_img;  // with add_poff
-    int add_poff = 1;
+    const uint8_t *payload_dev = dev_img ? dev_img + p.poff : nullptr;
     if ((flags & CRUM_VERIFY) && c->any_hash && p.K) {
         if (host_img) {
             if ((st = dev_alloc(c, &d_payload_tmp, p.payload))) return st;
             CK(cudaMemcpyAsync(d_payload_tmp, host_img + p.poff, p.payload, cudaMemcpyHostToDevice, s));
             payload_dev = d_payload_tmp;
-            add_poff = 0;
         }
-        launch_verify_hash(L, c->d_regs, p.R, c->d_rs, meta, payload_dev, add_poff, c->d_st);
+        launch_verify_hash(L, c->d_regs, p.R, c->d_rs, d_hashes, payload_dev, p.K, c->d_st);
         CK_LAUNCH();
         CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1043,8 +1228,20 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
     }
     if (timing) CK(cudaEventRecord(c->ev_t[1], s));
     const uint64_t units = p.payload >> kSegLog2;
-    if (!host_img || d_payload_tmp) {
-        launch_scatter(L, c->d_regs, p.R, c->d_rs, meta, c->d_st, payload_dev, 0, add_poff, c->d_force, 0, units);
+    ScatterArgs sa{};
+    sa.regs = c->d_regs;
+    sa.R = p.R;
+    sa.rs = c->d_rs;
+    sa.ids = d_ids;
+    sa.hashes = d_hashes;
+    sa.st = c->d_st;
+    sa.force = c->d_force;
+    if (payload_dev) {
+        sa.src = payload_dev;
+        sa.src_unit0 = 0;
+        sa.u_lo = 0;
+        sa.u_hi = units;
+        launch_scatter(L, sa);
         CK_LAUNCH();
         if (timing) {
             CK(cudaEventRecord(c->ev_t[4], s));
@@ -1065,7 +1262,11 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
                                cudaMemcpyHostToDevice, c->copy));
             CK(cudaEventRecord(c->ev_copy[slot], c->copy));
             CK(cudaStreamWaitEvent(s, c->ev_copy[slot], 0));
-            launch_scatter(L, c->d_regs, p.R, c->d_rs, meta, c->d_st, c->d_ring[slot], u0, 0, c->d_force, u0, u1);
+            sa.src = c->d_ring[slot];
+            sa.src_unit0 = u0;
+            sa.u_lo = u0;
+            sa.u_hi = u1;
+            launch_scatter(L, sa);
             CK_LAUNCH();
             CK(cudaEventRecord(c->ev_gather[slot], s));
         }
@@ -1079,7 +1280,7 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
     if (rep) {
         memset(rep, 0, sizeof *rep);
         fill_report(c, *c->h_st, rep);
-        rep->image_bytes = p.poff + p.payload;
+        rep->image_bytes = p.image;
         rep->t_compact_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
         rep->t_gather_ms = ev_ms(c->ev_t[1], c->ev_t[3]);
         rep->t_copy_ms = ev_ms(c->ev_t[4], c->ev_t[5]);
@@ -1120,12 +1321,10 @@ int crum_debug_detect(crum_ctx *ctx, void *stream, uint8_t *host_flags, uint64_t
         return CRUM_E_INVAL;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    Launch L = launch_of(c, s);
-    CK(cudaMemsetAsync(c->d_flags, 0, pad_pages(c->N), s));
-    launch_detect_compare(L, c->d_regs, c->d_cmp_idx, c->d_cmp_seg, c->n_cmp, c->n_seg, c->d_force, c->d_flags);
-    launch_detect_hash(L, c->d_regs, c->d_hash_idx, c->d_hash_grp, c->n_hash, c->n_grp, c->d_flags,
-                       c->d_newhash);
-    launch_export_flags(L, c->d_flags, c->d_force, c->N, c->d_dbg);
+    int st;
+    if ((st = next_tag(c, s))) return st;
+    enqueue_detect(c, s, c->all, false);
+    launch_export_flags(launch_of(c, s), c->d_flags, c->d_force, c->N, c->tag, c->d_dbg);
     CK_LAUNCH();
     if (n) CK(cudaMemcpyAsync(host_flags, c->d_dbg, n, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1134,17 +1333,14 @@ int crum_debug_detect(crum_ctx *ctx, void *stream, uint8_t *host_flags, uint64_t
 
 int crum_debug_export(crum_ctx *ctx, uint32_t id, int what, void *host_buf, uint64_t len) {
     ENTER(ctx);
-    uint32_t idx;
-    HostRegion *h = find_region(c, id, &idx);
+    HostRegion *h = find_region(c, id);
     if (!h) return CRUM_E_NOREGION;
     if (!host_buf) return CRUM_E_INVAL;
     CK(cudaDeviceSynchronize());
-    uint64_t pb = 0;
-    for (uint32_t r = 0; r < idx; ++r) pb += c->regs[r].n_pages;
     switch (what) {
         case CRUM_EXPORT_FORCE:
             if (len != h->n_pages) return CRUM_E_INVAL;
-            CK(cudaMemcpy(host_buf, c->d_force + pb, len, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(host_buf, c->d_force + h->page_base, len, cudaMemcpyDeviceToHost));
             return CRUM_OK;
         case CRUM_EXPORT_HASHES:
             if (h->mode != kModeHash || len != 8 * h->n_pages) return CRUM_E_INVAL;

@@ -1,8 +1,11 @@
-"""Independent image-format v1 builder/parser for tests (DESIGN.md "Image
-format"), written with library routines only: struct, zlib.crc32 and
+"""Independent image-format v1 builder/parser for tests,
+written with library routines only: struct, zlib.crc32 and
 xxhash.xxh3_64_intdigest.  It pins the oracle's image assembly and is reused by
 the GPU parity tests to decode images.  Imports neither oracle/ nor the
 product package.
+
+Layout: header(64) | table(48R) | zero pad to payload_offset | payload |
+        ids (u32, padded to 8 B) | hashes (u64, if any hash-mode region)
 """
 from __future__ import annotations
 
@@ -12,7 +15,7 @@ import zlib
 import numpy as np
 import xxhash
 
-HDR = struct.Struct("<4sIIIQQQQI8sI")  # 64 bytes
+HDR = struct.Struct("<4sIIIQQQQQII")  # 64 bytes
 ENTRY = struct.Struct("<IIQQQQQ")      # 48 bytes
 assert HDR.size == 64 and ENTRY.size == 48
 
@@ -32,8 +35,7 @@ def build_image(regions, listed, full=False) -> bytes:
     R = len(regions)
     K = sum(len(l) for l in listed)
     has_hashes = any(r["mode"] == 1 for r in regions)
-    meta = 64 + 48 * R + round_up(4 * K, 8) + (8 * K if has_hashes else 0)
-    poff = round_up(meta, 4096)
+    poff = round_up(64 + 48 * R, 4096)
     table, ids, hashes, payload = b"", b"", b"", []
     first = 0
     for r, l in zip(regions, listed):
@@ -48,25 +50,33 @@ def build_image(regions, listed, full=False) -> bytes:
                 hashes += struct.pack("<Q", xxhash.xxh3_64_intdigest(s) if r["mode"] == 1 else 0)
             payload.append(s)
     ids += b"\0" * (round_up(4 * K, 8) - 4 * K)
-    body = table + ids + hashes
-    assert 64 + len(body) == meta
-    flags = (1 if full else 0) | (2 if has_hashes else 0)
     pay = b"".join(payload)
-    hdr0 = struct.pack("<4sIIIQQQQI8s", b"CRUM", 1, flags, R, K, meta, poff, len(pay),
-                       zlib.crc32(body), b"\0" * 8)
+    tail = ids + hashes
+    ids_off = poff + len(pay)
+    total = ids_off + len(tail)
+    flags = (1 if full else 0) | (2 if has_hashes else 0)
+    hdr0 = struct.pack("<4sIIIQQQQQI", b"CRUM", 1, flags, R, K, poff, len(pay), ids_off, total,
+                       zlib.crc32(table + tail))
     hdr = hdr0 + struct.pack("<I", zlib.crc32(hdr0))
-    return hdr + body + b"\0" * (poff - meta) + pay
+    out = hdr + table + b"\0" * (poff - 64 - len(table)) + pay + tail
+    assert len(out) == total
+    return out
 
 
 def parse_image(img: bytes):
     img = bytes(img)
-    magic, ver, flags, R, K, meta, poff, paylen, mcrc, _res, hcrc = HDR.unpack_from(img, 0)
+    magic, ver, flags, R, K, poff, paylen, ids_off, total, mcrc, hcrc = HDR.unpack_from(img, 0)
     table = [ENTRY.unpack_from(img, 64 + 48 * k) for k in range(R)]
-    ids_off = 64 + 48 * R
     ids = list(struct.unpack_from(f"<{K}I", img, ids_off)) if K else []
     hashes = []
     if flags & 2 and K:
         hashes = list(struct.unpack_from(f"<{K}Q", img, ids_off + round_up(4 * K, 8)))
-    return dict(magic=magic, version=ver, flags=flags, R=R, K=K, meta=meta, poff=poff,
-                payload_bytes=paylen, meta_crc=mcrc, header_crc=hcrc, table=table, ids=ids,
+    return dict(magic=magic, version=ver, flags=flags, R=R, K=K, poff=poff, payload_bytes=paylen,
+                ids_off=ids_off, image_bytes=total, meta_crc=mcrc, header_crc=hcrc, table=table, ids=ids,
                 hashes=hashes)
+
+
+def meta_positions(img: bytes):
+    """Byte positions covered by the two CRCs (header, table, ids, hashes)."""
+    p = parse_image(img)
+    return list(range(0, 64 + 48 * p["R"])) + list(range(p["ids_off"], p["image_bytes"]))

@@ -124,9 +124,8 @@ def test_corruption_and_truncation_detected(oracle_mod):
     S = synth.seed(7)
     o, mems, rids = make_ctx(oracle_mod, [(3 * 4096, 4096, 0), (2 * 4096, 4096, 1)], S)
     st, img, _ = o.checkpoint_gather()
-    meta = imgfmt.parse_image(img)["meta"]
     before = [m.copy() for m in mems]
-    for pos in range(meta):
+    for pos in imgfmt.meta_positions(img):
         bad = img.copy()
         bad[pos] ^= 0x04
         assert o.restore_scatter(bad)[0] == oracle_mod.E_CORRUPT, pos
@@ -136,7 +135,7 @@ def test_corruption_and_truncation_detected(oracle_mod):
         assert np.array_equal(m, b)
     # payload of a hash-mode slot tampered: only VERIFY notices
     bad = img.copy()
-    bad[-1] ^= 0xFF
+    bad[imgfmt.parse_image(img)["ids_off"] - 1] ^= 0xFF   # last byte of the last (hash-mode) slot
     assert o.restore_scatter(bad, oracle_mod.VERIFY)[0] == oracle_mod.E_CORRUPT
     assert o.restore_scatter(bad)[0] == 0
 
