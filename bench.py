@@ -210,7 +210,7 @@ def main():
     S = synth.seed(1) + (rank << 20)
     F = sum(nb for nb, _, _ in specs)
 
-    ctx = crum.Context(local)
+    ctx = crum.Context(local, timing=True)
     regions = []
     with torch.cuda.stream(stream):
         for r, (nb, P, mode) in enumerate(specs):
@@ -240,13 +240,22 @@ def main():
         """A5: barrier before detect; all-reduce of {dirty bytes, image bytes} after."""
         return coord.coordinated(fn).local
 
+    def device_step():
+        """One checkpoint into the device image, stream-asynchronous; with N > 1
+        the coordinated all-reduce needs the totals, so the step waits for them."""
+        if distributed:
+            return coordinated(lambda: (ctx.checkpoint_gather_device(dimg, cap, stream=stream, report=False),
+                                        ctx.last_report())[1])
+        ctx.checkpoint_gather_device(dimg, cap, stream=stream, report=False)
+        return None
+
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     epoch = 0
     for _ in range(args.warmup):
         epoch += 1
         app_epoch(epoch)
-        coordinated(lambda: ctx.checkpoint_gather_device(dimg, cap, stream=stream))
+        device_step()
     torch.cuda.synchronize()
     if distributed:
         dist.barrier()
@@ -258,8 +267,9 @@ def main():
         epoch += 1
         app_epoch(epoch)
         ev0[i].record(stream)
-        reps.append(coordinated(lambda: ctx.checkpoint_gather_device(dimg, cap, stream=stream)))
+        device_step()
         ev1[i].record(stream)
+        reps.append(ctx.last_report())  # after ev1: the wait is outside the timed interval
     torch.cuda.synchronize()
     if distributed:
         dist.barrier()

@@ -86,9 +86,14 @@ typedef struct crum_image crum_image; /* library-owned pinned host buffer holdin
 
 typedef struct {
     uint64_t chunk_bytes; /* host-link pipeline chunk (0 = 64 MiB); multiple of 4096 */
-    uint32_t flags;       /* reserved, must be 0 */
+    uint32_t flags;       /* 0 or CRUM_CFG_TIMING */
     uint32_t reserved;    /* must be 0 */
 } crum_config;
+
+/* crum_config.flags: record CUDA events around the phases of EVERY call (also
+ * asynchronous ones), so crum_last_report can return phase times without the
+ * call itself waiting. */
+enum { CRUM_CFG_TIMING = 1u << 0 };
 
 /* Outcome of a sync / gather / restore.  Times are CUDA-event milliseconds
  * on the call's stream (0 when not measured). */
@@ -199,6 +204,12 @@ CRUM_API int crum_restore_scatter(crum_ctx *ctx, const crum_image *img, void *st
                          crum_report *report_out);
 CRUM_API int crum_restore_scatter_device(crum_ctx *ctx, const void *dev_image, uint64_t len, void *stream,
                                 uint32_t flags, crum_report *report_out);
+
+/* Report of the most recent sync / gather / restore call on ctx: waits for
+ * that call's work to finish, then fills counters and (if events were
+ * recorded: a report was requested or CRUM_CFG_TIMING is set) phase times.
+ * Errors: INVAL (null, or no call yet), CUDA. */
+CRUM_API int crum_last_report(crum_ctx *ctx, crum_report *report_out);
 
 /* Status text; thread-local detail of the last error on this thread. */
 CRUM_API const char *crum_status_string(int status);

@@ -29,6 +29,7 @@ E_INVAL, E_OVERLAP, E_NOREGION, E_RANGE, E_NOMEM = -1, -2, -3, -4, -5
 E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY, E_DEVICE, E_CUDA = -6, -7, -8, -9, -10, -11
 MODE_COMPARE, MODE_HASH = 0, 1
 FULL, VERIFY = 1, 2
+CFG_TIMING = 1
 EXPORT_FORCE, EXPORT_HASHES, EXPORT_MIRROR = 0, 1, 2
 ALL_PAGES = (1 << 64) - 1
 
@@ -38,7 +39,7 @@ EXPORTED = (
     "crum_sync_shadow", "crum_image_required_bytes", "crum_image_create", "crum_image_import",
     "crum_image_data", "crum_image_destroy", "crum_checkpoint_gather", "crum_checkpoint_gather_device",
     "crum_restore_scatter", "crum_restore_scatter_device", "crum_status_string", "crum_last_error_detail",
-    "crum_debug_detect", "crum_debug_export", "crum_launch_count",
+    "crum_debug_detect", "crum_debug_export", "crum_launch_count", "crum_last_report",
     "crum_synth_fill", "crum_synth_write_pages", "crum_synth_scrub", "crum_probe_copy",
 )
 
@@ -79,6 +80,7 @@ _sig = {
     "crum_debug_detect": (_i, [_vp, _vp, _vp, _u64]),
     "crum_debug_export": (_i, [_vp, _u32, _i, _vp, _u64]),
     "crum_launch_count": (_u64, [_vp]),
+    "crum_last_report": (_i, [_vp, C.POINTER(Report)]),
     "crum_synth_fill": (_i, [_vp, _u64, _u64, _u64, _u64, _vp]),
     "crum_synth_write_pages": (_i, [_vp, _u64, _u64, _vp, _u64, _u64, _u64, _u64, _i, _vp]),
     "crum_synth_scrub": (_i, [_vp, _u64, _vp]),
@@ -180,9 +182,9 @@ class Image:
 class Context:
     """crum_ctx: one per (process, CUDA device)."""
 
-    def __init__(self, device: int = 0, chunk_bytes: int = 0):
+    def __init__(self, device: int = 0, chunk_bytes: int = 0, timing: bool = False):
         self._h = _vp()
-        cfg = Config(chunk_bytes, 0, 0)
+        cfg = Config(chunk_bytes, CFG_TIMING if timing else 0, 0)
         _check(_L.crum_create(device, C.byref(cfg), C.byref(self._h)), "crum_create")
         self.device = device
         self._keep = {}
@@ -294,6 +296,12 @@ class Context:
         out = np.zeros(n, dtype=dtype)
         _check(_L.crum_debug_export(self._h, rid, what, out.ctypes.data, out.nbytes), "crum_debug_export")
         return out
+
+    def last_report(self) -> dict:
+        """Report of the most recent sync/gather/restore (waits for it)."""
+        rep = Report()
+        _check(_L.crum_last_report(self._h, C.byref(rep)), "crum_last_report")
+        return rep.as_dict()
 
     @property
     def launch_count(self) -> int:

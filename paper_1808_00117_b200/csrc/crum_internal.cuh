@@ -78,7 +78,8 @@ struct RangeTotals {
 };
 
 struct X2N {
-    uint32_t t[32];  // x^(2^k) mod P (reflected CRC-32 polynomial)
+    uint32_t t[32];   // x^(2^k) mod P (reflected CRC-32 polynomial)
+    uint32_t pw[32];  // x^(8 * 64 * j) mod P: shift by j 64-byte chunks
 };
 
 struct Launch {
@@ -109,6 +110,7 @@ struct CompactArgs {
     uint64_t *lhash;       // slot -> XXH3 (hash regions) or 0 (image hashes)
     uint32_t *reg_nd;      // per-region dirty count
     RangeTotals *rb;
+    RangeTotals *rb_host;  // mapped pinned mirror of rb (host reads it after an event)
     uint32_t *done;        // last-block counter (self-resetting)
     RegStat *rs;
     DevStats *st;
@@ -142,6 +144,7 @@ struct CrcArgs {
     const uint64_t *lhash;
     const uint32_t *gids;
     DevStats *st;
+    DevStats *st_host;      // mapped pinned copy of the final stats, or nullptr
     uint32_t *done;
     X2N x2n;
 };

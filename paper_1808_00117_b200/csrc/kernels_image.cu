@@ -237,6 +237,11 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a
     if (threadIdx.x == 0) {
         a.rb[a.c + 1].k = K;
         a.rb[a.c + 1].units = U;
+        if (a.rb_host) {  // zero-copy store: no copy-engine queue between host and totals
+            volatile RangeTotals *h = a.rb_host + a.c + 1;
+            h->k = K;
+            h->units = U;
+        }
         *a.done = 0;
     }
     if (!a.final_range) return;
@@ -451,41 +456,94 @@ __device__ __forceinline__ void put64(uint8_t *p, uint64_t v) {
     for (int i = 0; i < 8; ++i) p[i] = (uint8_t)(v >> (8 * i));
 }
 
-constexpr uint32_t kCrcChunk = 64;
+// The metadata stream is a whole number of u32 words (48R + round_up(4K,8) +
+// 8K bytes).  A warp takes 32 consecutive 64-byte chunks ("task"): each lane
+// computes its chunk's raw CRC from 16 words held in registers, shifts it by
+// (31 - lane) chunks with one GF(2) product (pw table), the warp XOR-reduces,
+// and one product with x^(8 * bytes after the task) places the task.  Only
+// the last (partial) task shifts per lane.
+constexpr uint32_t kCrcWords = 16;
 
-// Byte v of the virtual stream table || ids(padded) || hashes.
-__device__ __forceinline__ uint8_t meta_byte(const CrcArgs &a, uint64_t tab, uint64_t idsb, uint64_t K,
-                                             uint64_t v) {
-    if (v < tab) return a.head[64 + v];
-    v -= tab;
-    if (v < idsb) return v < 4 * K ? reinterpret_cast<const uint8_t *>(a.lids)[v] : 0;
-    return reinterpret_cast<const uint8_t *>(a.lhash)[v - idsb];
+struct CrcSmem {
+    uint32_t T[256];
+    uint32_t x2n[32];
+    uint32_t pw[32];
+};
+
+__device__ __forceinline__ void crc_smem_init(CrcSmem &sm, const X2N &x) {
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
+        uint32_t c = i;
+        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+        sm.T[i] = c;
+    }
+    if (threadIdx.x < 32) {
+        sm.x2n[threadIdx.x] = x.t[threadIdx.x];
+        sm.pw[threadIdx.x] = x.pw[threadIdx.x];
+    }
+    __syncthreads();
+}
+
+// XOR of the placed CRC terms of this warp's tasks (valid in every lane).
+// zlib's ~0 initial register is folded into chunk 0.
+template <class WordFn>
+__device__ __forceinline__ uint32_t crc_stream_terms(const WordFn &word, uint64_t nwords, const CrcSmem &sm) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t nchunks = (nwords + kCrcWords - 1) / kCrcWords;
+    const uint64_t ntasks = (nchunks + 31) / 32;
+    const uint64_t len = nwords * 4;
+    uint32_t acc = 0;
+    for (uint64_t t = gw; t < ntasks; t += nwarps) {
+        const uint64_t c = t * 32 + lane;
+        const uint64_t w0 = c * kCrcWords;
+        uint32_t v[kCrcWords];
+#pragma unroll
+        for (int j = 0; j < (int)kCrcWords; ++j) v[j] = (w0 + j < nwords) ? word(w0 + j) : 0u;
+        uint32_t raw = (c == 0) ? 0xffffffffu : 0u;
+#pragma unroll
+        for (int j = 0; j < (int)kCrcWords; ++j) {
+            if (w0 + j < nwords) {
+                raw ^= v[j];
+                raw = sm.T[raw & 0xffu] ^ (raw >> 8);
+                raw = sm.T[raw & 0xffu] ^ (raw >> 8);
+                raw = sm.T[raw & 0xffu] ^ (raw >> 8);
+                raw = sm.T[raw & 0xffu] ^ (raw >> 8);
+            }
+        }
+        const bool full_task = (t * 32 + 32) * kCrcWords <= nwords;
+        uint32_t term;
+        if (full_task) {
+            term = gf2_mulmod(sm.pw[31 - lane], raw);  // first operand is never 0
+        } else {
+            const uint64_t end = min(len, (c + 1) * kCrcWords * 4);
+            term = (c < nchunks) ? gf2_mulmod(xpow8n(len - end, sm.x2n), raw) : 0u;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) term ^= __shfl_xor_sync(0xffffffffu, term, o);
+        if (full_task) term = gf2_mulmod(xpow8n(len - (t * 32 + 32) * kCrcWords * 4, sm.x2n), term);
+        acc ^= term;
+    }
+    return acc;
 }
 
 __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
     DevStats *st = a.st;
     if (st->status != kStOk) return;
-    __shared__ uint32_t T[256];
-    __shared__ uint32_t sx[32];
+    __shared__ CrcSmem sm;
     __shared__ bool s_last;
-    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
-        uint32_t c = i;
-        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
-        T[i] = c;
-    }
-    if (threadIdx.x < 32) sx[threadIdx.x] = a.x2n.t[threadIdx.x];
-    __syncthreads();
+    crc_smem_init(sm, a.x2n);
     const uint64_t K = st->K, R = st->n_regions;
     const bool hh = (st->img_flags & 2u) != 0;
-    const uint64_t tab = 48 * R, idsb = round_up(4 * K, 8), len = tab + idsb + (hh ? 8 * K : 0);
+    const uint64_t tabw = 12 * R, idsw = round_up(4 * K, 8) / 4, nwords = tabw + idsw + (hh ? 2 * K : 0);
     uint8_t *tail = a.tail ? a.tail : a.head + st->ids_off;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
     // copy ids (+pad) and hashes into the image tail
     uint32_t *tids = reinterpret_cast<uint32_t *>(tail);
-    for (uint64_t k = tid; k < idsb / 4; k += nth) tids[k] = k < K ? a.lids[k] : 0u;
+    for (uint64_t k = tid; k < idsw; k += nth) tids[k] = k < K ? a.lids[k] : 0u;
     if (hh) {
-        uint64_t *th = reinterpret_cast<uint64_t *>(tail + idsb);
+        uint64_t *th = reinterpret_cast<uint64_t *>(tail + 4 * idsw);
         for (uint64_t k = tid; k < K; k += nth) th[k] = a.lhash[k];
     }
     // runs of consecutive page ids (a run starts at a region's page 0 or after a gap)
@@ -495,17 +553,18 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
     runs = warp_sum(runs);
     if ((threadIdx.x & 31) == 0 && runs)
         atomicAdd(reinterpret_cast<unsigned long long *>(&st->dirty_runs), (unsigned long long)runs);
-    // CRC terms (zlib's ~0 initial register folded into chunk 0)
-    const uint64_t nchunks = (len + kCrcChunk - 1) / kCrcChunk;
-    uint32_t acc = 0;
-    for (uint64_t c = tid; c < nchunks; c += nth) {
-        const uint64_t b0 = c * kCrcChunk, b1 = min(len, b0 + kCrcChunk);
-        uint32_t raw = (c == 0) ? 0xffffffffu : 0u;
-        for (uint64_t b = b0; b < b1; ++b) raw = T[(raw ^ meta_byte(a, tab, idsb, K, b)) & 0xffu] ^ (raw >> 8);
-        acc ^= gf2_mulmod(xpow8n(len - b1, sx), raw);  // first operand is never 0
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+    // CRC of table || ids(padded) || hashes, read from the table and the scratch
+    const uint32_t *tabp = reinterpret_cast<const uint32_t *>(a.head + 64);
+    const uint32_t *lids = a.lids;
+    const uint64_t *lhash = a.lhash;
+    auto word = [&](uint64_t w) -> uint32_t {
+        if (w < tabw) return tabp[w];
+        w -= tabw;
+        if (w < idsw) return w < K ? lids[w] : 0u;
+        w -= idsw;
+        return (uint32_t)(lhash[w >> 1] >> (32 * (w & 1)));
+    };
+    const uint32_t acc = crc_stream_terms(word, nwords, sm);
     if ((threadIdx.x & 31) == 0 && acc) atomicXor(&st->crc_acc, acc);
     __threadfence();
     __syncthreads();
@@ -515,7 +574,7 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
     __threadfence();
     *a.done = 0;
     // empty stream: zlib crc32("") == 0
-    const uint32_t meta_crc = (len == 0) ? 0u : (*(volatile uint32_t *)&st->crc_acc ^ 0xffffffffu);
+    const uint32_t meta_crc = (nwords == 0) ? 0u : (*(volatile uint32_t *)&st->crc_acc ^ 0xffffffffu);
     st->meta_crc = meta_crc;
     uint8_t h[64];
     h[0] = 'C'; h[1] = 'R'; h[2] = 'U'; h[3] = 'M';
@@ -529,57 +588,43 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
     put64(h + 48, st->image_bytes);
     put32(h + 56, meta_crc);
     uint32_t c = 0xffffffffu;
-    for (int i = 0; i < 60; ++i) c = T[(c ^ h[i]) & 0xffu] ^ (c >> 8);
+    for (int i = 0; i < 60; ++i) c = sm.T[(c ^ h[i]) & 0xffu] ^ (c >> 8);
     put32(h + 60, c ^ 0xffffffffu);
     for (int i = 0; i < 64; ++i) a.head[i] = h[i];
+    if (a.st_host) {
+        const uint64_t *src = reinterpret_cast<const uint64_t *>(st);
+        volatile uint64_t *dst = reinterpret_cast<volatile uint64_t *>(a.st_host);
+        for (uint32_t i = 0; i < sizeof(DevStats) / 8; ++i) dst[i] = src[i];
+    }
 }
 
 void launch_crc_meta(const Launch &L, const CrcArgs &a, uint64_t max_len) {
-    uint64_t blocks = (max_len / kCrcChunk + 255) / 256;
+    uint64_t blocks = (max_len / (kCrcWords * 4 * 32) + 7) / 8;  // 8 warps per block, 1 task each
     if (blocks < 1) blocks = 1;
     if (blocks > (uint64_t)L.sms * 2) blocks = L.sms * 2;
     k_crc_meta<<<(unsigned)blocks, 256, 0, L.stream>>>(a);
     ++*L.counter;
 }
 
-// CRC terms only (restore validation): XOR of shifted raw chunk CRCs of
-// table || tail into st->crc_acc (host finalises).
-__global__ void __launch_bounds__(256) k_crc_check(const uint8_t *__restrict__ table, uint64_t tab,
-                                                   const uint8_t *__restrict__ tail, uint64_t tl, DevStats *st,
+// CRC terms only (restore validation): table || tail into st->crc_acc (the
+// host finalises).  Both lengths are multiples of 4.
+__global__ void __launch_bounds__(256) k_crc_check(const uint32_t *__restrict__ table, uint64_t tabw,
+                                                   const uint32_t *__restrict__ tail, uint64_t tailw, DevStats *st,
                                                    X2N x2n) {
-    __shared__ uint32_t T[256];
-    __shared__ uint32_t sx[32];
-    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
-        uint32_t c = i;
-        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
-        T[i] = c;
-    }
-    if (threadIdx.x < 32) sx[threadIdx.x] = x2n.t[threadIdx.x];
-    __syncthreads();
-    const uint64_t len = tab + tl;
-    const uint64_t nchunks = (len + kCrcChunk - 1) / kCrcChunk;
-    uint32_t acc = 0;
-    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks;
-         c += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t b0 = c * kCrcChunk, b1 = min(len, b0 + kCrcChunk);
-        uint32_t raw = (c == 0) ? 0xffffffffu : 0u;
-        for (uint64_t b = b0; b < b1; ++b) {
-            const uint8_t v = b < tab ? table[b] : tail[b - tab];
-            raw = T[(raw ^ v) & 0xffu] ^ (raw >> 8);
-        }
-        acc ^= gf2_mulmod(xpow8n(len - b1, sx), raw);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ CrcSmem sm;
+    crc_smem_init(sm, x2n);
+    auto word = [&](uint64_t w) -> uint32_t { return w < tabw ? table[w] : tail[w - tabw]; };
+    const uint32_t acc = crc_stream_terms(word, tabw + tailw, sm);
     if ((threadIdx.x & 31) == 0 && acc) atomicXor(&st->crc_acc, acc);
 }
 
 void launch_crc_check(const Launch &L, const uint8_t *table, uint64_t tab, const uint8_t *tail, uint64_t tl,
                       DevStats *st, const X2N &x2n) {
-    uint64_t blocks = ((tab + tl) / kCrcChunk + 255) / 256;
+    uint64_t blocks = ((tab + tl) / (kCrcWords * 4 * 32) + 7) / 8;
     if (blocks < 1) blocks = 1;
     if (blocks > (uint64_t)L.sms * 2) blocks = L.sms * 2;
-    k_crc_check<<<(unsigned)blocks, 256, 0, L.stream>>>(table, tab, tail, tl, st, x2n);
+    k_crc_check<<<(unsigned)blocks, 256, 0, L.stream>>>(reinterpret_cast<const uint32_t *>(table), tab / 4,
+                                                        reinterpret_cast<const uint32_t *>(tail), tl / 4, st, x2n);
     ++*L.counter;
 }
 

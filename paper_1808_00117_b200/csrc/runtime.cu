@@ -65,6 +65,9 @@ const CrcTables &crc_tables() {
         }
         c.x2n.t[0] = 0x40000000u;  // x^1
         for (int k = 1; k < 32; ++k) c.x2n.t[k] = gf2_mulmod_host(c.x2n.t[k - 1], c.x2n.t[k - 1]);
+        // pw[j] = x^(512 j): x^512 = x^(2^9)
+        c.x2n.pw[0] = 0x80000000u;  // x^0
+        for (int j = 1; j < 32; ++j) c.x2n.pw[j] = gf2_mulmod_host(c.x2n.t[9], c.x2n.pw[j - 1]);
         return c;
     }();
     return t;
@@ -167,10 +170,12 @@ struct crum_ctx {
     DevRegion *d_tregs = nullptr;  // restore: descriptors built from an image table
     uint64_t tregs_cap = 0;
     RangeTotals *d_rb = nullptr;   // kMaxRanges + 1
-    RangeTotals *h_rb = nullptr;   // pinned mirror
+    RangeTotals *h_rb = nullptr;   // pinned, mapped mirror
     uint32_t *d_done = nullptr;    // [0] compaction, [1] crc
     DevStats *d_st = nullptr;
-    DevStats *h_st = nullptr;      // pinned
+    DevStats *h_st = nullptr;      // pinned, mapped
+    DevStats *dh_st = nullptr;     // its device address
+    RangeTotals *dh_rb = nullptr;  // device address of h_rb (mapped)
 
     uint8_t *d_meta = nullptr;     // host path: image head [0, poff) then the tail
     uint64_t meta_cap = 0;
@@ -184,6 +189,14 @@ struct crum_ctx {
     cudaEvent_t ev_range[kMaxRanges];
     cudaEvent_t ev_t[6];
     cudaEvent_t ev_meta;
+    // CRUM_TRACE=1: per-range timing events of the host path, printed to stderr
+    bool trace = false;
+    cudaEvent_t ev_trace[3 * kMaxRanges] = {};
+    // CRUM_CFG_TIMING and the most recent call (crum_last_report)
+    bool timing_cfg = false;
+    int last_kind = 0;      // 0 none, 1 sync, 2 device gather, 3 host gather, 4 restore
+    bool last_timed = false;
+    cudaEvent_t ev_done = nullptr;
 };
 
 namespace {
@@ -387,11 +400,13 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
         if ((st = dev_alloc(c, &c->d_meta, meta_max))) return st;
         c->meta_cap = meta_max;
     }
-    // page ranges of the pipelined host path: ~F/8 bytes each (>= 128 MiB),
-    // boundaries on multiples of 16 pages
+    // page ranges of the pipelined host path, boundaries on multiples of 16
+    // pages: the first ranges are small (the host link starts early), then
+    // they double up to ~F/8 (>= 128 MiB) each
     c->all = make_range(c, 0, N);
     c->ranges.clear();
-    const uint64_t target = std::max(kMinRangeBytes, F / 8);
+    const uint64_t target_max = std::max(kMinRangeBytes, F / 8);
+    uint64_t target = std::max<uint64_t>(16ull << 20, F / 128);
     uint64_t lo = 0, acc = 0;
     for (uint32_t r = 0; r < R; ++r) {
         const HostRegion &h = c->regs[r];
@@ -401,6 +416,7 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
                 c->ranges.push_back(make_range(c, lo, g));
                 lo = g;
                 acc = 0;
+                target = std::min(target_max, 2 * target);
             }
             // whole pages at a time is fine for large regions; skip ahead in big steps
             const uint64_t step = std::min<uint64_t>(h.n_pages - i, 16 - (g % 16));
@@ -485,6 +501,7 @@ CompactArgs compact_args(crum_ctx *c, const Range &rg, uint32_t ci, bool first, 
     a.lhash = c->d_lhash;
     a.reg_nd = c->d_reg_nd;
     a.rb = c->d_rb;
+    a.rb_host = c->dh_rb;
     a.done = c->d_done;
     a.rs = c->d_rs;
     a.st = c->d_st;
@@ -506,6 +523,7 @@ CrcArgs crc_args(crum_ctx *c, uint8_t *head, uint8_t *tail) {
     a.gids = c->d_gids;
     a.st = c->d_st;
     a.done = c->d_done + 1;
+    a.st_host = c->dh_st;
     a.x2n = crc_tables().x2n;
     return a;
 }
@@ -540,6 +558,42 @@ void fill_report(crum_ctx *c, const DevStats &h, crum_report *rep) {
     rep->image_bytes = h.image_bytes;
 }
 
+enum { kLastNone = 0, kLastSync = 1, kLastDevGather = 2, kLastHostGather = 3, kLastRestore = 4 };
+
+// Phase times of the most recent call from its events (see each call for
+// which events delimit which phase).
+void fill_times(crum_ctx *c, crum_report *rep) {
+    cudaEvent_t *e = c->ev_t;
+    switch (c->last_kind) {
+        case kLastSync:
+            rep->t_detect_ms = ev_ms(e[0], e[1]);
+            rep->t_compact_ms = ev_ms(e[1], e[2]);
+            rep->t_gather_ms = ev_ms(e[2], e[4]);
+            rep->t_total_ms = ev_ms(e[0], e[4]);
+            break;
+        case kLastDevGather:
+            rep->t_detect_ms = ev_ms(e[0], e[1]);
+            rep->t_compact_ms = ev_ms(e[1], e[2]) + ev_ms(e[3], e[4]);
+            rep->t_gather_ms = ev_ms(e[2], e[3]);
+            rep->t_total_ms = ev_ms(e[0], e[4]);
+            break;
+        case kLastHostGather:
+            rep->t_detect_ms = ev_ms(e[0], e[1]);
+            rep->t_gather_ms = ev_ms(e[0], e[3]);
+            rep->t_copy_ms = ev_ms(e[4], e[5]);
+            rep->t_total_ms = ev_ms(e[0], e[5]);
+            break;
+        case kLastRestore:
+            rep->t_compact_ms = ev_ms(e[0], e[1]);
+            rep->t_gather_ms = ev_ms(e[1], e[3]);
+            rep->t_copy_ms = ev_ms(e[4], e[5]);
+            rep->t_total_ms = ev_ms(e[0], e[3]);
+            break;
+        default:
+            break;
+    }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -572,7 +626,7 @@ uint64_t crum_launch_count(const crum_ctx *c) { return c ? c->launches : 0; }
 int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     if (!out) return CRUM_E_INVAL;
     *out = nullptr;
-    if (cfg && (cfg->flags || cfg->reserved || (cfg->chunk_bytes % 4096))) {
+    if (cfg && ((cfg->flags & ~(uint32_t)CRUM_CFG_TIMING) || cfg->reserved || (cfg->chunk_bytes % 4096))) {
         set_detail("bad crum_config");
         return CRUM_E_INVAL;
     }
@@ -586,15 +640,25 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     if (!c) return CRUM_E_NOMEM;
     c->device = device;
     if (cfg && cfg->chunk_bytes) c->chunk = cfg->chunk_bytes;
+    c->timing_cfg = cfg && (cfg->flags & CRUM_CFG_TIMING);
     auto fail = [&](int st) {
         crum_destroy(c);
         return st;
     };
     if (cudaSetDevice(device) != cudaSuccess) return fail(CRUM_E_CUDA);
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
-    if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking) != cudaSuccess)
-        return fail(CRUM_E_CUDA);
+    if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess) return fail(CRUM_E_CUDA);
+    {
+        // gathers of the host path get the highest priority so their blocks are
+        // dispatched ahead of the (long, persistent) detect of later ranges
+        int lo_prio = 0, hi_prio = 0;
+        cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+        if (cudaStreamCreateWithPriority(&c->gstream, cudaStreamNonBlocking, hi_prio) != cudaSuccess)
+            return fail(CRUM_E_CUDA);
+    }
+    c->trace = getenv("CRUM_TRACE") != nullptr;
+    for (int i = 0; i < 3 * kMaxRanges; ++i)
+        if (cudaEventCreate(&c->ev_trace[i]) != cudaSuccess) return fail(CRUM_E_CUDA);
     for (int i = 0; i < kRing; ++i) {
         if (cudaEventCreateWithFlags(&c->ev_gather[i], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming) != cudaSuccess)
@@ -605,12 +669,16 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     for (int i = 0; i < 6; ++i)
         if (cudaEventCreate(&c->ev_t[i]) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
+    if (cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaMalloc(&c->d_st, sizeof(DevStats)) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaMalloc(&c->d_rb, sizeof(RangeTotals) * (kMaxRanges + 1)) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaMalloc(&c->d_done, 16) != cudaSuccess) return fail(CRUM_E_NOMEM);
-    if (cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocDefault) != cudaSuccess) return fail(CRUM_E_NOMEM);
-    if (cudaHostAlloc(&c->h_rb, sizeof(RangeTotals) * (kMaxRanges + 1), cudaHostAllocDefault) != cudaSuccess)
+    if (cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocMapped) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    if (cudaHostAlloc(&c->h_rb, sizeof(RangeTotals) * (kMaxRanges + 1), cudaHostAllocMapped) != cudaSuccess)
         return fail(CRUM_E_NOMEM);
+    if (cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->dh_st), c->h_st, 0) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->dh_rb), c->h_rb, 0) != cudaSuccess)
+        return fail(CRUM_E_CUDA);
     cudaMemset(c->d_st, 0, sizeof(DevStats));
     cudaMemset(c->d_rb, 0, sizeof(RangeTotals) * (kMaxRanges + 1));
     cudaMemset(c->d_done, 0, 16);
@@ -662,6 +730,9 @@ int crum_destroy(crum_ctx *c) {
     for (int i = 0; i < 6; ++i)
         if (c->ev_t[i]) cudaEventDestroy(c->ev_t[i]);
     if (c->ev_meta) cudaEventDestroy(c->ev_meta);
+    if (c->ev_done) cudaEventDestroy(c->ev_done);
+    for (int i = 0; i < 3 * kMaxRanges; ++i)
+        if (c->ev_trace[i]) cudaEventDestroy(c->ev_trace[i]);
     cudaGetLastError();
     delete c;
     return CRUM_OK;
@@ -844,14 +915,22 @@ int crum_image_destroy(crum_image *img) {
 int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
     ENTER(ctx);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool timing = c->timing_cfg;
     int st;
+    if (timing) CK(cudaEventRecord(c->ev_t[0], s));
     if ((st = next_tag(c, s))) return st;
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
     enqueue_detect(c, s, c->all, false);
+    if (timing) CK(cudaEventRecord(c->ev_t[1], s));
     enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, false, UINT64_MAX, nullptr));
+    if (timing) CK(cudaEventRecord(c->ev_t[2], s));
     Launch L = launch_of(c, s);
     launch_gather(L, gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX), c->max_units);
     CK_LAUNCH();
+    if (timing) CK(cudaEventRecord(c->ev_t[4], s));
+    CK(cudaEventRecord(c->ev_done, s));
+    c->last_kind = kLastSync;
+    c->last_timed = timing;
     if (dirty_out) {
         CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -881,7 +960,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool full = flags & CRUM_FULL;
-    const bool timing = rep != nullptr;
+    const bool timing = rep != nullptr || c->timing_cfg;
     uint8_t *img = static_cast<uint8_t *>(dev_image);
     int st;
     if (timing) CK(cudaEventRecord(c->ev_t[0], s));
@@ -896,17 +975,17 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     if (timing) CK(cudaEventRecord(c->ev_t[3], s));
     launch_crc_meta(L, crc_args(c, img, nullptr), crc_max_len(c));
     CK_LAUNCH();
-    if (timing) {
-        CK(cudaEventRecord(c->ev_t[4], s));
+    if (timing) CK(cudaEventRecord(c->ev_t[4], s));
+    CK(cudaEventRecord(c->ev_done, s));
+    c->last_kind = kLastDevGather;
+    c->last_timed = timing;
+    if (rep) {
         CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         const DevStats h = *c->h_st;
         memset(rep, 0, sizeof *rep);
         fill_report(c, h, rep);
-        rep->t_detect_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
-        rep->t_compact_ms = ev_ms(c->ev_t[1], c->ev_t[2]) + ev_ms(c->ev_t[3], c->ev_t[4]);
-        rep->t_gather_ms = ev_ms(c->ev_t[2], c->ev_t[3]);
-        rep->t_total_ms = ev_ms(c->ev_t[0], c->ev_t[4]);
+        fill_times(c, rep);
         if (h.status == kStCapacity) {
             set_detail("image needs %llu bytes, capacity %llu", (unsigned long long)h.image_bytes,
                        (unsigned long long)capacity);
@@ -948,8 +1027,8 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
         enqueue_compact(c, s,
                         compact_args(c, rg, ci, ci == 0, ci + 1 == nr, full, UINT64_MAX, c->d_meta));
         CK_LAUNCH();
-        CK(cudaMemcpyAsync(c->h_rb + ci + 1, c->d_rb + ci + 1, sizeof(RangeTotals), cudaMemcpyDeviceToHost, s));
-        CK(cudaEventRecord(c->ev_range[ci], s));
+        CK(cudaEventRecord(c->ev_range[ci], s));  // h_rb[ci + 1] written by the kernel (mapped)
+        if (c->trace) CK(cudaEventRecord(c->ev_trace[3 * ci], s));
     }
     CK(cudaEventRecord(c->ev_t[1], s));
     // metadata: CRC + tail into d_meta (tail after the head [0, poff))
@@ -957,8 +1036,7 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     Launch L = launch_of(c, s);
     launch_crc_meta(L, crc_args(c, c->d_meta, c->d_meta + poff), crc_max_len(c));
     CK_LAUNCH();
-    CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
-    CK(cudaEventRecord(c->ev_meta, s));
+    CK(cudaEventRecord(c->ev_meta, s));  // h_st written by the CRC kernel's last block (mapped)
     if (!pipelined) {
         CK(cudaEventSynchronize(c->ev_meta));
         if (c->h_st->image_bytes > img->cap) {
@@ -997,6 +1075,10 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
                                cudaMemcpyDeviceToHost, c->copy));
             CK(cudaEventRecord(c->ev_copy[slot], c->copy));
         }
+        if (c->trace) {
+            CK(cudaEventRecord(c->ev_trace[3 * ci + 1], c->gstream));
+            CK(cudaEventRecord(c->ev_trace[3 * ci + 2], c->copy));
+        }
     }
     // header + table, then ids/hashes
     CK(cudaEventSynchronize(c->ev_meta));
@@ -1012,14 +1094,26 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     CK(cudaStreamSynchronize(c->gstream));
     CK(cudaStreamSynchronize(c->copy));
     CK(cudaStreamSynchronize(s));
+    CK(cudaEventRecord(c->ev_done, s));
+    c->last_kind = kLastHostGather;
+    c->last_timed = true;
     img->len = h.image_bytes;
+    if (c->trace) {
+        fprintf(stderr, "[crum trace] gather: %u ranges, K=%llu, payload=%llu B, t_detect_all=%.3f ms\n", nr,
+                (unsigned long long)h.K, (unsigned long long)h.payload_bytes, ev_ms(c->ev_t[0], c->ev_t[1]));
+        for (uint32_t ci = 0; ci < nr; ++ci)
+            fprintf(stderr, "[crum trace]  range %2u pages [%llu,%llu) units %llu: compacted %.3f  gathered %.3f  "
+                            "copied %.3f ms\n",
+                    ci, (unsigned long long)c->ranges[ci].p_lo, (unsigned long long)c->ranges[ci].p_hi,
+                    (unsigned long long)(c->h_rb[ci + 1].units - c->h_rb[ci].units),
+                    ev_ms(c->ev_t[0], c->ev_trace[3 * ci]), ev_ms(c->ev_t[0], c->ev_trace[3 * ci + 1]),
+                    ev_ms(c->ev_t[0], c->ev_trace[3 * ci + 2]));
+        fprintf(stderr, "[crum trace]  meta copied %.3f ms\n", ev_ms(c->ev_t[0], c->ev_t[5]));
+    }
     if (rep) {
         memset(rep, 0, sizeof *rep);
         fill_report(c, h, rep);
-        rep->t_detect_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
-        rep->t_gather_ms = ev_ms(c->ev_t[0], c->ev_t[3]);
-        rep->t_copy_ms = ev_ms(c->ev_t[4], c->ev_t[5]);
-        rep->t_total_ms = ev_ms(c->ev_t[0], c->ev_t[5]);
+        fill_times(c, rep);
     }
     return CRUM_OK;
 }
@@ -1138,7 +1232,7 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
     const bool hh = (p.flags & 2u) != 0;
     const uint64_t tail_len = p.image - p.ids_off;
     const uint64_t tab_len = 48ull * p.R;
-    const bool timing = rep != nullptr;
+    const bool timing = rep != nullptr || c->timing_cfg;
     if (timing) CK(cudaEventRecord(c->ev_t[0], s));
     // table + tail on the device
     const uint8_t *d_table, *d_tail;
@@ -1277,14 +1371,14 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
     CK(cudaStreamSynchronize(s));
     CK(cudaStreamSynchronize(c->copy));
     if (d_payload_tmp) cudaFree(d_payload_tmp);
+    CK(cudaEventRecord(c->ev_done, s));
+    c->last_kind = kLastRestore;
+    c->last_timed = timing;
     if (rep) {
         memset(rep, 0, sizeof *rep);
         fill_report(c, *c->h_st, rep);
         rep->image_bytes = p.image;
-        rep->t_compact_ms = ev_ms(c->ev_t[0], c->ev_t[1]);
-        rep->t_gather_ms = ev_ms(c->ev_t[1], c->ev_t[3]);
-        rep->t_copy_ms = ev_ms(c->ev_t[4], c->ev_t[5]);
-        rep->t_total_ms = ev_ms(c->ev_t[0], c->ev_t[3]);
+        fill_times(c, rep);
     }
     return CRUM_OK;
 }
@@ -1309,6 +1403,20 @@ int crum_restore_scatter_device(crum_ctx *ctx, const void *dev_image, uint64_t l
     }
     return restore_common(c, nullptr, static_cast<const uint8_t *>(dev_image), len,
                           static_cast<cudaStream_t>(stream), flags, rep);
+}
+
+int crum_last_report(crum_ctx *ctx, crum_report *rep) {
+    ENTER(ctx);
+    if (!rep || c->last_kind == kLastNone) {
+        set_detail(rep ? "no call to report on" : "null report");
+        return CRUM_E_INVAL;
+    }
+    CK(cudaEventSynchronize(c->ev_done));
+    CK(cudaMemcpy(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost));
+    memset(rep, 0, sizeof *rep);
+    fill_report(c, *c->h_st, rep);
+    if (c->last_timed) fill_times(c, rep);
+    return CRUM_OK;
 }
 
 // ---------------------------------------------------------------------------
