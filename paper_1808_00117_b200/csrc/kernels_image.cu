@@ -457,11 +457,12 @@ __device__ __forceinline__ void put64(uint8_t *p, uint64_t v) {
 }
 
 // The metadata stream is a whole number of u32 words (48R + round_up(4K,8) +
-// 8K bytes).  A warp takes 32 consecutive 64-byte chunks ("task"): each lane
-// computes its chunk's raw CRC from 16 words held in registers, shifts it by
-// (31 - lane) chunks with one GF(2) product (pw table), the warp XOR-reduces,
-// and one product with x^(8 * bytes after the task) places the task.  Only
-// the last (partial) task shifts per lane.
+// 8K bytes).  It is cut into 64-byte chunks counted from the END, so chunk i
+// is followed by exactly 64*i bytes: its raw CRC is placed by a product with
+// x^(512 i).  A warp takes 32 consecutive chunks (a "task"): lane j shifts by
+// pw[j] = x^(512 j), the warp XOR-reduces, and task t is shifted once more by
+// x^(8 * 2048 t).  The (possibly short) chunk holding byte 0 carries zlib's
+// ~0 initial register.
 constexpr uint32_t kCrcWords = 16;
 
 struct CrcSmem {
@@ -484,7 +485,6 @@ __device__ __forceinline__ void crc_smem_init(CrcSmem &sm, const X2N &x) {
 }
 
 // XOR of the placed CRC terms of this warp's tasks (valid in every lane).
-// zlib's ~0 initial register is folded into chunk 0.
 template <class WordFn>
 __device__ __forceinline__ uint32_t crc_stream_terms(const WordFn &word, uint64_t nwords, const CrcSmem &sm) {
     const uint32_t lane = threadIdx.x & 31;
@@ -492,36 +492,33 @@ __device__ __forceinline__ uint32_t crc_stream_terms(const WordFn &word, uint64_
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t nchunks = (nwords + kCrcWords - 1) / kCrcWords;
     const uint64_t ntasks = (nchunks + 31) / 32;
-    const uint64_t len = nwords * 4;
     uint32_t acc = 0;
     for (uint64_t t = gw; t < ntasks; t += nwarps) {
-        const uint64_t c = t * 32 + lane;
-        const uint64_t w0 = c * kCrcWords;
-        uint32_t v[kCrcWords];
+        const uint64_t i = t * 32 + lane;
+        uint32_t raw = 0;
+        if (i < nchunks) {
+            const uint64_t wend = nwords - i * kCrcWords;
+            const uint64_t wbeg = wend > kCrcWords ? wend - kCrcWords : 0;
+            const uint32_t n = (uint32_t)(wend - wbeg);
+            uint32_t v[kCrcWords];
 #pragma unroll
-        for (int j = 0; j < (int)kCrcWords; ++j) v[j] = (w0 + j < nwords) ? word(w0 + j) : 0u;
-        uint32_t raw = (c == 0) ? 0xffffffffu : 0u;
+            for (int j = 0; j < (int)kCrcWords; ++j) v[j] = (uint32_t)j < n ? word(wbeg + j) : 0u;
+            raw = (wbeg == 0) ? 0xffffffffu : 0u;
 #pragma unroll
-        for (int j = 0; j < (int)kCrcWords; ++j) {
-            if (w0 + j < nwords) {
-                raw ^= v[j];
-                raw = sm.T[raw & 0xffu] ^ (raw >> 8);
-                raw = sm.T[raw & 0xffu] ^ (raw >> 8);
-                raw = sm.T[raw & 0xffu] ^ (raw >> 8);
-                raw = sm.T[raw & 0xffu] ^ (raw >> 8);
+            for (int j = 0; j < (int)kCrcWords; ++j) {
+                if ((uint32_t)j < n) {
+                    raw ^= v[j];
+                    raw = sm.T[raw & 0xffu] ^ (raw >> 8);
+                    raw = sm.T[raw & 0xffu] ^ (raw >> 8);
+                    raw = sm.T[raw & 0xffu] ^ (raw >> 8);
+                    raw = sm.T[raw & 0xffu] ^ (raw >> 8);
+                }
             }
         }
-        const bool full_task = (t * 32 + 32) * kCrcWords <= nwords;
-        uint32_t term;
-        if (full_task) {
-            term = gf2_mulmod(sm.pw[31 - lane], raw);  // first operand is never 0
-        } else {
-            const uint64_t end = min(len, (c + 1) * kCrcWords * 4);
-            term = (c < nchunks) ? gf2_mulmod(xpow8n(len - end, sm.x2n), raw) : 0u;
-        }
+        uint32_t term = gf2_mulmod(sm.pw[lane], raw);  // first operand is never 0
 #pragma unroll
         for (int o = 16; o; o >>= 1) term ^= __shfl_xor_sync(0xffffffffu, term, o);
-        if (full_task) term = gf2_mulmod(xpow8n(len - (t * 32 + 32) * kCrcWords * 4, sm.x2n), term);
+        if (t) term = gf2_mulmod(xpow8n(t * 32 * kCrcWords * 4, sm.x2n), term);
         acc ^= term;
     }
     return acc;

@@ -184,6 +184,8 @@ struct crum_ctx {
 
     cudaStream_t copy = nullptr;    // D2H / H2D
     cudaStream_t gstream = nullptr; // gathers of the pipelined host path
+    cudaStream_t aux = nullptr;     // device path: metadata CRC beside the gather
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_gather[kRing];
     cudaEvent_t ev_copy[kRing];
     cudaEvent_t ev_range[kMaxRanges];
@@ -670,6 +672,10 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
         if (cudaEventCreate(&c->ev_t[i]) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
+    if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return fail(CRUM_E_CUDA);
     if (cudaMalloc(&c->d_st, sizeof(DevStats)) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaMalloc(&c->d_rb, sizeof(RangeTotals) * (kMaxRanges + 1)) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaMalloc(&c->d_done, 16) != cudaSuccess) return fail(CRUM_E_NOMEM);
@@ -721,6 +727,9 @@ int crum_destroy(crum_ctx *c) {
     if (c->h_rb) cudaFreeHost(c->h_rb);
     if (c->copy) cudaStreamDestroy(c->copy);
     if (c->gstream) cudaStreamDestroy(c->gstream);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (int i = 0; i < kRing; ++i) {
         if (c->ev_gather[i]) cudaEventDestroy(c->ev_gather[i]);
         if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
@@ -970,10 +979,15 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     if (timing) CK(cudaEventRecord(c->ev_t[1], s));
     enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, full, capacity, img));
     if (timing) CK(cudaEventRecord(c->ev_t[2], s));
+    // metadata CRC (+ tail, header) on a side stream beside the payload gather
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    launch_crc_meta(launch_of(c, c->aux), crc_args(c, img, nullptr), crc_max_len(c));
+    CK(cudaEventRecord(c->ev_join, c->aux));
     Launch L = launch_of(c, s);
     launch_gather(L, gather_args(c, 0, img, 0, true, 0, UINT64_MAX), c->max_units);
     if (timing) CK(cudaEventRecord(c->ev_t[3], s));
-    launch_crc_meta(L, crc_args(c, img, nullptr), crc_max_len(c));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     CK_LAUNCH();
     if (timing) CK(cudaEventRecord(c->ev_t[4], s));
     CK(cudaEventRecord(c->ev_done, s));
@@ -1018,25 +1032,33 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     crum_image_required_bytes(c, UINT64_MAX, &worst);
     const bool pipelined = img->cap >= worst;
     const uint32_t nr = (uint32_t)c->ranges.size();
+    const uint64_t poff = payload_offset_for(c->regs.size());
     CK(cudaEventRecord(c->ev_t[0], s));
     if ((st = next_tag(c, s))) return st;
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
-    for (uint32_t ci = 0; ci < nr; ++ci) {
+    // detect + compact of range ci on the caller's stream; after the last range
+    // the metadata CRC + tail go into d_meta (tail after the head [0, poff))
+    uint32_t enq = 0;
+    auto enqueue_range = [&](uint32_t ci) -> int {
         const Range &rg = c->ranges[ci];
         enqueue_detect(c, s, rg, full);
-        enqueue_compact(c, s,
-                        compact_args(c, rg, ci, ci == 0, ci + 1 == nr, full, UINT64_MAX, c->d_meta));
+        enqueue_compact(c, s, compact_args(c, rg, ci, ci == 0, ci + 1 == nr, full, UINT64_MAX, c->d_meta));
         CK_LAUNCH();
         CK(cudaEventRecord(c->ev_range[ci], s));  // h_rb[ci + 1] written by the kernel (mapped)
         if (c->trace) CK(cudaEventRecord(c->ev_trace[3 * ci], s));
-    }
-    CK(cudaEventRecord(c->ev_t[1], s));
-    // metadata: CRC + tail into d_meta (tail after the head [0, poff))
-    const uint64_t poff = payload_offset_for(c->regs.size());
-    Launch L = launch_of(c, s);
-    launch_crc_meta(L, crc_args(c, c->d_meta, c->d_meta + poff), crc_max_len(c));
-    CK_LAUNCH();
-    CK(cudaEventRecord(c->ev_meta, s));  // h_st written by the CRC kernel's last block (mapped)
+        if (ci + 1 == nr) {
+            CK(cudaEventRecord(c->ev_t[1], s));
+            launch_crc_meta(launch_of(c, s), crc_args(c, c->d_meta, c->d_meta + poff), crc_max_len(c));
+            CK_LAUNCH();
+            CK(cudaEventRecord(c->ev_meta, s));  // h_st written by the CRC kernel's last block (mapped)
+        }
+        return CRUM_OK;
+    };
+    // keep the GPU two ranges ahead of the host (all of them if capacity must
+    // be checked before anything is committed)
+    const uint32_t ahead = pipelined ? 2 : nr;
+    while (enq < nr && enq < ahead)
+        if ((st = enqueue_range(enq++))) return st;
     if (!pipelined) {
         CK(cudaEventSynchronize(c->ev_meta));
         if (c->h_st->image_bytes > img->cap) {
@@ -1056,6 +1078,8 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     bool copy_started = false;
     c->h_rb[0] = RangeTotals{0, 0};
     for (uint32_t ci = 0; ci < nr; ++ci) {
+        while (enq < nr && enq <= ci + 2)
+            if ((st = enqueue_range(enq++))) return st;
         CK(cudaEventSynchronize(c->ev_range[ci]));
         const uint64_t U0 = c->h_rb[ci].units, U1 = c->h_rb[ci + 1].units;
         if (U1 > U0) CK(cudaStreamWaitEvent(c->gstream, c->ev_range[ci], 0));
