@@ -43,6 +43,14 @@ CRUM_API int crum_synth_scrub(void *dev_ptr, uint64_t bytes, void *stream);
  * aligned, bytes a multiple of 16. */
 CRUM_API int crum_probe_copy(void *dst, const void *src, uint64_t bytes, int blocks, void *stream);
 
+/* Config-5 footprint: cudaMallocManaged of `bytes`; [0, device_bytes) gets
+ * PreferredLocation = device (prefetched there), the rest PreferredLocation =
+ * CPU + AccessedBy = device (prefetched to host), so GPU scans read it over
+ * the host link without migrating it.  *out receives the managed pointer.
+ * Errors: INVAL, DEVICE, NOMEM, CUDA.  Free with crum_synth_free_managed. */
+CRUM_API int crum_synth_alloc_managed(void **out, uint64_t bytes, int device, uint64_t device_bytes);
+CRUM_API int crum_synth_free_managed(void *p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,6 +41,7 @@ EXPORTED = (
     "crum_restore_scatter", "crum_restore_scatter_device", "crum_status_string", "crum_last_error_detail",
     "crum_debug_detect", "crum_debug_export", "crum_launch_count", "crum_last_report",
     "crum_synth_fill", "crum_synth_write_pages", "crum_synth_scrub", "crum_probe_copy",
+    "crum_synth_alloc_managed", "crum_synth_free_managed",
 )
 
 
@@ -85,6 +86,8 @@ _sig = {
     "crum_synth_write_pages": (_i, [_vp, _u64, _u64, _vp, _u64, _u64, _u64, _u64, _i, _vp]),
     "crum_synth_scrub": (_i, [_vp, _u64, _vp]),
     "crum_probe_copy": (_i, [_vp, _vp, _u64, _i, _vp]),
+    "crum_synth_alloc_managed": (_i, [C.POINTER(_vp), _u64, _i, _u64]),
+    "crum_synth_free_managed": (_i, [_vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_L, _name)
@@ -327,3 +330,29 @@ def synth_scrub(dev_ptr, nbytes: int, stream=None):
 
 def probe_copy(dst, src, nbytes: int, blocks: int = 0, stream=None):
     _check(_L.crum_probe_copy(_addr(dst), _addr(src), nbytes, blocks, _stream(stream)), "crum_probe_copy")
+
+
+class ManagedBuffer:
+    """Config-5 managed (UVM) allocation; .ptr / .nbytes like a raw buffer."""
+
+    def __init__(self, nbytes: int, device: int = 0, device_bytes: int | None = None):
+        p = _vp()
+        _check(_L.crum_synth_alloc_managed(C.byref(p), nbytes, device,
+                                           nbytes if device_bytes is None else device_bytes),
+               "crum_synth_alloc_managed")
+        self.ptr = p.value
+        self.nbytes = nbytes
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def free(self):
+        if self.ptr:
+            _L.crum_synth_free_managed(self.ptr)
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

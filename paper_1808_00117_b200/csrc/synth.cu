@@ -114,3 +114,47 @@ extern "C" int crum_probe_copy(void *dst, const void *src, uint64_t bytes, int b
         reinterpret_cast<uint4 *>(dst), reinterpret_cast<const uint4 *>(src), bytes / 16);
     return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
 }
+
+// ---------------------------------------------------------------------------
+// Oversubscribed UVM footprints (config 5): a managed allocation whose first
+// `device_bytes` prefer the GPU and whose rest prefers host memory and is
+// mapped for direct GPU access (so scans read it over the host link instead
+// of migrating it), prefetched into place.
+// ---------------------------------------------------------------------------
+extern "C" int crum_synth_alloc_managed(void **out, uint64_t bytes, int device, uint64_t device_bytes) {
+    if (!out || !bytes || device_bytes > bytes) return CRUM_E_INVAL;
+    *out = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess) return CRUM_E_DEVICE;
+    void *p = nullptr;
+    if (cudaMallocManaged(&p, bytes, cudaMemAttachGlobal) != cudaSuccess) {
+        cudaGetLastError();
+        return CRUM_E_NOMEM;
+    }
+    uint8_t *b = static_cast<uint8_t *>(p);
+    const uint64_t host_bytes = bytes - device_bytes;
+    cudaError_t e = cudaSuccess;
+    if (device_bytes) {
+        if (e == cudaSuccess) e = cudaMemAdvise(b, device_bytes, cudaMemAdviseSetPreferredLocation, device);
+        if (e == cudaSuccess) e = cudaMemPrefetchAsync(b, device_bytes, device, 0);
+    }
+    if (host_bytes) {
+        if (e == cudaSuccess)
+            e = cudaMemAdvise(b + device_bytes, host_bytes, cudaMemAdviseSetPreferredLocation, cudaCpuDeviceId);
+        if (e == cudaSuccess) e = cudaMemAdvise(b + device_bytes, host_bytes, cudaMemAdviseSetAccessedBy, device);
+        if (e == cudaSuccess) e = cudaMemPrefetchAsync(b + device_bytes, host_bytes, cudaCpuDeviceId, 0);
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(p);
+        return CRUM_E_CUDA;
+    }
+    *out = p;
+    return CRUM_OK;
+}
+
+extern "C" int crum_synth_free_managed(void *p) {
+    if (!p) return CRUM_E_INVAL;
+    cudaDeviceSynchronize();
+    return cudaFree(p) == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
+}

@@ -1,0 +1,192 @@
+"""GPU parity at BASELINE.json's full sizes (C3 16 GiB, C4 64 GiB, C5 240 GiB
+oversubscribed UVM), in the launch configuration bench.py times.  The oracle
+cannot hold these footprints, so the checks are (a) properties that hold at
+any size -- K and the id list equal the written set exactly, both CRC-32s
+verify (zlib), restoring the image onto its own state changes nothing and a
+sync afterwards finds 0 dirty pages -- and (b) sampled slots the oracle
+computes one by one: slot bytes from the seeded recipe, and for hash-mode
+slots the listed hash vs the oracle's XXH3 of the expected slot."""
+import struct
+import zlib
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+KiB, MiB, GiB = 1 << 10, 1 << 20, 1 << 30
+
+
+@pytest.fixture(scope="module")
+def crum():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1808_00117_b200 import crum as m
+    return m
+
+
+def expected_page(S, r, nbytes, P, i, writes):
+    """Page i of region r after the epochs in `writes` ({epoch: set(pages)})."""
+    lo = i * P
+    ln = min(P, nbytes - lo)
+    b = synth.region_content(S, r, ln, word_offset=lo // 8)
+    full = ln // 8 * 8
+    for e in sorted(writes):
+        if i in writes[e]:
+            m = synth.page_mask(S, e, r, np.array([i]))[0]
+            b[:full].view(np.uint64)[:] ^= np.uint64(m)
+            if ln > full:
+                b[full:ln] ^= np.frombuffer(np.uint64(m).tobytes(), dtype=np.uint8)[:ln - full]
+    return b
+
+
+def check_image(img_head, img_tail, fetch_slot, specs, rids, S, writes_by_region, epoch, rng, nsample=64):
+    """img_head: bytes [0, 64+48R); img_tail: bytes [ids_off, image_bytes);
+    fetch_slot(offset, n) -> bytes of the image at payload offset."""
+    from oracle import oracle
+    from tests import imgfmt
+    hdr = imgfmt.HDR.unpack_from(img_head, 0)
+    magic, ver, flags, R, K, poff, paylen, ids_off, total, mcrc, hcrc = hdr
+    assert magic == b"CRUM" and ver == 1 and R == len(specs)
+    assert zlib.crc32(img_head[:60]) == hcrc
+    table = img_head[64:64 + 48 * R]
+    assert zlib.crc32(table + img_tail) == mcrc
+    # ids == the pages written in `epoch`, exactly
+    ids = list(struct.unpack_from(f"<{K}I", img_tail, 0)) if K else []
+    hashes = list(struct.unpack_from(f"<{K}Q", img_tail, (4 * K + 7) // 8 * 8)) if (flags & 2) and K else []
+    want_total = 0
+    entries = [imgfmt.ENTRY.unpack_from(table, 48 * k) for k in range(R)]
+    slot_of = []
+    pay = 0
+    for r, ((nb, P, mode), e, rid) in enumerate(zip(specs, entries, rids)):
+        want = sorted(writes_by_region[r].get(epoch, set()))
+        eid, emode, ebytes, eps, enp, nd, first = e
+        assert (eid, emode, ebytes, eps, enp) == (rid, mode, nb, P, synth.n_pages(nb, P))
+        assert nd == len(want) and first == want_total
+        assert ids[first:first + nd] == want
+        for j, i in enumerate(want):
+            slot_of.append((r, i, pay + j * P, first + j))
+        pay += nd * P
+        want_total += nd
+    assert K == want_total and paylen == pay and ids_off == poff + pay
+    # sampled slots: bytes and (hash mode) the listed hash vs the oracle's XXH3
+    if slot_of:
+        picks = set(rng.choice(len(slot_of), size=min(nsample, len(slot_of)), replace=False).tolist())
+        picks |= {0, len(slot_of) - 1}
+        for p in sorted(picks):
+            r, i, off, k = slot_of[p]
+            nb, P, mode = specs[r]
+            exp = expected_page(S, r, nb, P, i, writes_by_region[r])
+            got = fetch_slot(off, P)
+            slot = np.zeros(P, dtype=np.uint8)
+            slot[:len(exp)] = exp
+            assert np.array_equal(np.frombuffer(got, dtype=np.uint8), slot), (r, i)
+            if flags & 2:
+                want_h = oracle.xxh3_64(slot) if mode == 1 else 0
+                assert hashes[k] == want_h, (r, i)
+
+
+def make_regions(crum, specs, S, managed=None):
+    g = crum.Context(0)
+    regs, rids = [], []
+    for r, (nb, P, mode) in enumerate(specs):
+        if managed is not None:
+            t = managed[r]
+        else:
+            t = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        crum.synth_fill(t, nb, S, r)
+        regs.append(t)
+    torch.cuda.synchronize()
+    for r, (nb, P, mode) in enumerate(specs):
+        rids.append(g.register_region(regs[r], nb, P, mode))
+    return g, regs, rids
+
+
+def write_epoch(crum, regs, specs, S, epoch, d, writes):
+    for r, (nb, P, _) in enumerate(specs):
+        pages = synth.choose_dirty(S, epoch, r, synth.n_pages(nb, P), d)
+        writes[r][epoch] = set(pages.tolist())
+        if len(pages):
+            dp = torch.from_numpy(pages.astype(np.uint32)).cuda()
+            crum.synth_write_pages(regs[r], nb, P, dp, len(pages), S, epoch, r)
+    torch.cuda.synchronize()
+
+
+def run_incremental(crum, specs, S, managed=None, d=0.1, host_image=True, nsample=64):
+    g, regs, rids = make_regions(crum, specs, S, managed)
+    N = sum(synth.n_pages(nb, P) for nb, P, _ in specs)
+    assert g.sync_shadow() == N          # epoch 0: commit everything (all force-dirty)
+    writes = [dict() for _ in specs]
+    write_epoch(crum, regs, specs, S, 1, d, writes)
+    rng = np.random.default_rng(S)
+    R = len(specs)
+    if host_image:
+        img = g.new_image(g.image_required_bytes(sum(synth.dirty_count(d, synth.n_pages(nb, P))
+                                                     for nb, P, _ in specs)))
+        rep = g.checkpoint_gather(img)
+        v = img.view()
+        head = v[:64 + 48 * R].tobytes()
+        ids_off = struct.unpack_from("<Q", head, 40)[0]
+        tail = v[ids_off:img.length].tobytes()
+        poff = struct.unpack_from("<Q", head, 24)[0]
+        fetch = lambda off, n: v[poff + off:poff + off + n].tobytes()
+    else:
+        raise NotImplementedError
+    check_image(head, tail, fetch, specs, rids, S, writes, 1, rng, nsample)
+    assert rep["dirty_pages"] == sum(len(w[1]) for w in writes)
+    # restoring the image onto its own state changes nothing; nothing is dirty after
+    g.restore_scatter(img)
+    assert g.sync_shadow() == 0
+    return g, regs, img
+
+
+@pytest.fixture(autouse=True)
+def _release_memory():
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    yield
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def test_c3_fullsize_sampled(crum):
+    sizes = synth.c3_region_sizes(20)
+    specs = [(s, 64 * KiB, 0 if i % 3 else 1) for i, s in enumerate(sizes)]
+    g, regs, img = run_incremental(crum, specs, synth.seed(3))
+    img.destroy()
+    g.close()
+
+
+def test_c4_fullsize_sampled(crum):
+    big, small = synth.c4_region_sizes(synth.seed(4))
+    specs = [(s, 64 * KiB, 0) for s in big] + [(s, 4 * KiB, 0) for s in small]
+    assert abs(sum(s for s, _, _ in specs) / GiB - 64.19) < 0.05
+    g, regs, img = run_incremental(crum, specs, synth.seed(4), nsample=96)
+    img.destroy()
+    g.close()
+
+
+def test_c5_oversubscribed_sampled(crum):
+    """240 GiB of managed memory on one GPU: 150 GiB device-preferred, 90 GiB
+    host-preferred + accessed-by (read over the host link), hash mode, 2 MiB
+    pages, 10% rewritten."""
+    import os
+    free, _ = torch.cuda.mem_get_info()
+    mem_total = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    if mem_total < 150 * GiB:
+        pytest.skip("host RAM too small for the C5 footprint")
+    region = 120 * GiB
+    dev_pref = [75 * GiB, 75 * GiB]
+    bufs = [crum.ManagedBuffer(region, 0, dp) for dp in dev_pref]
+    specs = [(region, 2 * MiB, 1), (region, 2 * MiB, 1)]
+    try:
+        g, regs, img = run_incremental(crum, specs, synth.seed(5), managed=bufs, nsample=24)
+        img.destroy()
+        g.close()
+    finally:
+        for b in bufs:
+            b.free()
