@@ -129,6 +129,9 @@ CRUM_API int crum_destroy(crum_ctx *ctx);
  * table (HASH_XXH3).  Every page starts force-dirty ("all the pages in the
  * regions are marked as dirty"), so the first sync/gather
  * lists all n = ceil(bytes/page_size) pages.
+ * ptr may be device memory of the context's device, managed (UVM) memory, or
+ * pinned host memory mapped at the same address (cudaHostAlloc under UVA):
+ * host-resident pages are then read over the host link.
  * Preconditions: ptr 16-byte aligned, accessible from the context's device;
  * bytes > 0; page_size a power of two in [4096, 2 MiB]; n < 2^32 and the
  * context's total page count < 2^31; no overlap with a live region.

@@ -780,8 +780,12 @@ int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page
             set_detail("pointer %p is not a CUDA pointer", reinterpret_cast<void *>(a));
             return CRUM_E_DEVICE;
         }
+        // device memory of this device, managed memory, or pinned host memory
+        // mapped at the same address (UVA): host-resident pages the kernels
+        // read over the host link (oversubscribed footprints, config 5)
         const bool ok = (at.type == cudaMemoryTypeManaged) ||
-                        (at.type == cudaMemoryTypeDevice && at.device == c->device);
+                        (at.type == cudaMemoryTypeDevice && at.device == c->device) ||
+                        (at.type == cudaMemoryTypeHost && at.devicePointer == reinterpret_cast<void *>(a));
         if (!ok) {
             set_detail("pointer %p is not device/managed memory of device %d", reinterpret_cast<void *>(a),
                        c->device);

@@ -170,19 +170,36 @@ def test_c4_fullsize_sampled(crum):
     g.close()
 
 
-def test_c5_oversubscribed_sampled(crum):
-    """240 GiB of managed memory on one GPU: 150 GiB device-preferred, 90 GiB
-    host-preferred + accessed-by (read over the host link), hash mode, 2 MiB
-    pages, 10% rewritten (SURVEY.md sec. 8(d) C5)."""
-    import os
-    free, _ = torch.cuda.mem_get_info()
-    mem_total = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
-    if mem_total < 150 * GiB:
-        pytest.skip("host RAM too small for the C5 footprint")
-    region = 120 * GiB
-    dev_pref = [75 * GiB, 75 * GiB]
-    bufs = [crum.ManagedBuffer(region, 0, dp) for dp in dev_pref]
+def test_c5_managed_host_resident_sampled(crum):
+    """UVM (managed) regions with host-resident pages, C5 shape at the scale
+    the GPU box's sandbox allows (it caps cudaMallocManaged at ~56 GiB in
+    total): 2 x 24 GiB managed, 37.5% of each host-preferred
+    + accessed-by (read over the host link, as 90 of C5's 240 GiB), hash mode,
+    2 MiB pages, 10% rewritten."""
+    region = 24 * GiB
+    bufs = [crum.ManagedBuffer(region, 0, 15 * GiB) for _ in range(2)]
     specs = [(region, 2 * MiB, 1), (region, 2 * MiB, 1)]
+    try:
+        g, regs, img = run_incremental(crum, specs, synth.seed(5), managed=bufs, nsample=24)
+        img.destroy()
+        g.close()
+    finally:
+        for b in bufs:
+            b.free()
+
+
+def test_c5_oversubscribed_hostmapped_sampled(crum):
+    """A footprint larger than HBM (192 GiB > 178 GiB): 160 GiB of device
+    regions plus 32 GiB of pinned host memory mapped into the GPU's address
+    space (host-resident pages read over the host link), hash mode, 2 MiB
+    pages, 10% rewritten."""
+    import os
+    if os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") < 96 * GiB:
+        pytest.skip("host RAM too small")
+    host = [torch.empty(16 * GiB, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    dev = [80 * GiB, 80 * GiB]
+    bufs = [torch.empty(n, dtype=torch.uint8, device="cuda") for n in dev] + host
+    specs = [(b.numel(), 2 * MiB, 1) for b in bufs]
     try:
         g, regs, img = run_incremental(crum, specs, synth.seed(5), managed=bufs, nsample=24)
         img.destroy()
