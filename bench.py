@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="crum", choices=["crum", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--mode", default="compare", choices=["compare", "hash"])
     ap.add_argument("--page", type=int, default=64 * KiB)
     ap.add_argument("--dirty", type=float, default=0.10)
@@ -74,9 +74,19 @@ def workload(args, rank: int):
         sizes = synth.c3_region_sizes(20)
         return [(s, args.page, mode) for s in sizes], (f"C3: Rodinia-style 220 regions (15.96 GiB), "
                                                        f"{args.page // KiB} KiB pages, {args.dirty:.0%} dirty, {args.mode}")
+    if args.config == "c5":
+        # 240 GiB per GPU: 150 GiB of HBM regions + 90 GiB of host-resident
+        # (UVA-mapped pinned) regions read over the host link; hash mode
+        specs = [(75 * GiB, 2 * MiB, 1), (75 * GiB, 2 * MiB, 1), (45 * GiB, 2 * MiB, 1), (45 * GiB, 2 * MiB, 1)]
+        return specs, "C5: 240 GiB per GPU (150 GiB HBM + 90 GiB host-resident), 2 MiB pages, 10% dirty, hash"
     big, small = synth.c4_region_sizes(synth.seed(4) + rank)
     specs = [(s, 64 * KiB, mode) for s in big] + [(s, 4 * KiB, mode) for s in small]
     return specs, f"C4: HPGMG-style 56 + 4096 regions (64.2 GiB) per GPU, 10% dirty, {args.mode}"
+
+
+def host_resident(args):
+    """Indices of the regions that live in host memory (config 5)."""
+    return {2, 3} if args.config == "c5" else set()
 
 
 def read_peaks():
@@ -162,11 +172,29 @@ def oracle_steps(specs, S, dirty, seconds: float, max_steps: int, min_steps: int
     return times, F
 
 
+def oracle_sample(specs, limit: int = 1 << 30):
+    """The whole workload when it is at most ~2 GiB, else its first regions up
+    to ~1 GiB (the last one truncated to whole pages): a bounded sample for
+    the single-threaded CPU oracle, same shapes and page sizes."""
+    F = sum(nb for nb, _, _ in specs)
+    if F <= 2 * limit:
+        return specs, "the same workload"
+    out, acc = [], 0
+    for nb, P, mode in specs:
+        take = min(nb, max(P, (limit - acc) // P * P))
+        out.append((take, P, mode))
+        acc += take
+        if acc >= limit:
+            break
+    return out, f"a {len(out)}-region slice of the workload"
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     specs, desc = workload(args, 0)
+    specs, what = oracle_sample(specs)
     S = synth.seed(1)
     steps = args.warmup + args.steps
     times, F = oracle_steps(specs, S, args.dirty, seconds=1e9, max_steps=steps, min_steps=steps)
@@ -178,7 +206,7 @@ def run_reference(args):
             "data": "synthetic (seeded splitmix64 words)",
             "config": {"workload": desc, "footprint_bytes": F},
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": f"the full workload ({F / GiB:g} GiB), {args.steps} timed steps, 1 thread"},
+                             "sample": f"{what} ({F / GiB:g} GiB), {args.steps} timed steps, 1 thread"},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -214,7 +242,10 @@ def main():
     regions = []
     with torch.cuda.stream(stream):
         for r, (nb, P, mode) in enumerate(specs):
-            t = torch.empty(nb, dtype=torch.uint8, device=dev)
+            if r in host_resident(args):
+                t = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+            else:
+                t = torch.empty(nb, dtype=torch.uint8, device=dev)
             crum.synth_fill(t, nb, S, r, stream=stream)
             regions.append(t)
             ctx.register_region(t, nb, P, mode)
@@ -223,10 +254,18 @@ def main():
     pages = [[torch.from_numpy(synth.choose_dirty(S, e, r, synth.n_pages(nb, P), args.dirty).astype(np.uint32)).to(dev)
               for r, (nb, P, _) in enumerate(specs)] for e in range(1, n_epochs + 1)]
     scrub = torch.empty(256 * MiB, dtype=torch.uint8, device=dev)
-    cap = ctx.image_required_bytes()
+    # image capacity: a worst-case image when it fits beside the footprint
+    # (asynchronous device path), else the exact bound for this dirty ratio
+    # (the call then checks capacity itself and waits)
+    worst = ctx.image_required_bytes()
+    k_exp = sum(synth.dirty_count(args.dirty, synth.n_pages(nb, P)) for nb, P, _ in specs)
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    cap = worst if worst + (1 << 30) < free_b - 2 * (1 << 30) and len(host_resident(args)) == 0 else \
+        ctx.image_required_bytes(k_exp)
+    async_ok = cap >= worst
     dimg = torch.empty(cap + 256, dtype=torch.uint8, device=dev)
     # epoch 0: the first (full) checkpoint, untimed
-    ctx.checkpoint_gather_device(dimg, cap, stream=stream)
+    ctx.sync_shadow(stream)   # epoch 0: commit the whole footprint (every page starts force-dirty)
 
     def app_epoch(e):
         for r, (nb, P, _) in enumerate(specs):
@@ -244,9 +283,9 @@ def main():
         """One checkpoint into the device image, stream-asynchronous; with N > 1
         the coordinated all-reduce needs the totals, so the step waits for them."""
         if distributed:
-            return coordinated(lambda: (ctx.checkpoint_gather_device(dimg, cap, stream=stream, report=False),
+            return coordinated(lambda: (ctx.checkpoint_gather_device(dimg, cap, stream=stream, report=not async_ok),
                                         ctx.last_report())[1])
-        ctx.checkpoint_gather_device(dimg, cap, stream=stream, report=False)
+        ctx.checkpoint_gather_device(dimg, cap, stream=stream, report=not async_ok)
         return None
 
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -353,10 +392,11 @@ def main():
         img.destroy()
     # ---- cpu_baseline: the oracle on this workload, rank 0 at N=1 only ----
     if not args.no_cpu_baseline and world == 1:
-        times, Fo = oracle_steps(specs, synth.seed(1), args.dirty, seconds=args.cpu_seconds, max_steps=50)
+        sample, what = oracle_sample(specs)
+        times, Fo = oracle_steps(sample, synth.seed(1), args.dirty, seconds=args.cpu_seconds, max_steps=50)
         v = Fo / statistics.median(times) / 1e9
         line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                                "sample": f"{len(times)} oracle checkpoint_gather steps over the same workload "
+                                "sample": f"{len(times)} oracle checkpoint_gather steps over {what} "
                                           f"({Fo / GiB:g} GiB, d={args.dirty}), writer untimed, median"}
     if rank == 0:
         print(json.dumps(line), flush=True)

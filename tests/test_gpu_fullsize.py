@@ -200,10 +200,7 @@ def test_c5_oversubscribed_hostmapped_sampled(crum):
     dev = [80 * GiB, 80 * GiB]
     bufs = [torch.empty(n, dtype=torch.uint8, device="cuda") for n in dev] + host
     specs = [(b.numel(), 2 * MiB, 1) for b in bufs]
-    try:
-        g, regs, img = run_incremental(crum, specs, synth.seed(5), managed=bufs, nsample=24)
-        img.destroy()
-        g.close()
-    finally:
-        for b in bufs:
-            b.free()
+    g, regs, img = run_incremental(crum, specs, synth.seed(5), managed=bufs, nsample=24)
+    img.destroy()
+    g.close()
+    del bufs, host, regs
