@@ -170,6 +170,11 @@ void launch_detect_compare(const Launch &L, const DevRegion *regs, const uint32_
 void launch_detect_hash(const Launch &L, const DevRegion *regs, const uint32_t *hash_idx,
                         const uint64_t *hash_grp, uint32_t n_hash, uint64_t w_lo, uint64_t w_hi,
                         uint8_t *flags, uint64_t *newhash, uint8_t tag);
+// pages of P >= kBigHashPage bytes: one CTA per page (warp specialised)
+constexpr uint32_t kBigHashLog2 = 16;
+void launch_detect_hash_big(const Launch &L, const DevRegion *regs, const uint32_t *big_idx,
+                            const uint64_t *big_pg, uint32_t n_big, uint64_t w_lo, uint64_t w_hi,
+                            uint8_t *flags, uint64_t *newhash, uint8_t tag);
 void launch_verify_hash(const Launch &L, const DevRegion *regs, uint32_t R, const RegStat *rs,
                         const uint64_t *hashes, const uint8_t *payload, uint64_t K, DevStats *st);
 

@@ -300,6 +300,117 @@ __global__ void __launch_bounds__(256) k_detect_hash(
 }
 
 // ---------------------------------------------------------------------------
+// HASH detect for large pages (P >= 64 KiB): one CTA per page, warp
+// specialised.  Warps 0..7 ("producers") compute the accumulate sums of 64
+// consecutive 1 KiB blocks per round (8 blocks each, the lane layout of
+// xxh3_slot) into a double-buffered shared-memory ring; warp 8 ("chain") runs
+// the serial scramble chain over them, one lane per accumulator lane, while
+// the producers stream the next round.  Hand-off uses named barriers:
+// FULL[b] (ids 1, 2: producers arrive, chain syncs) and EMPTY[b] (ids 3, 4:
+// chain arrives, producers sync).  The round counter q runs across the
+// CTA's pages so barrier generations stay paired.
+// ---------------------------------------------------------------------------
+constexpr int kBigProducers = 8;
+constexpr int kBigThreads = (kBigProducers + 1) * 32;
+constexpr int kRoundBlocks = kBigProducers * 8;  // 64 KiB of page per round
+
+__device__ __forceinline__ void bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(kBigThreads, 2) k_detect_hash_big(
+    const DevRegion *__restrict__ regs, const uint32_t *__restrict__ big_idx,
+    const uint64_t *__restrict__ big_pg, uint32_t n_big, uint64_t w_lo, uint64_t w_hi,
+    uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash, uint8_t tag) {
+    __shared__ uint64_t S[2][kRoundBlocks][8];
+    __shared__ uint64_t sw[24], slast[8], smerge[8], sinit[8];
+    if (threadIdx.x < 24) sw[threadIdx.x] = c_xxh.w[threadIdx.x];
+    if (threadIdx.x < 8) {
+        slast[threadIdx.x] = c_xxh.last[threadIdx.x];
+        smerge[threadIdx.x] = c_xxh.merge[threadIdx.x];
+        sinit[threadIdx.x] = c_xxh.init[threadIdx.x];
+    }
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t q = 0;
+    uint64_t r_lo = 1, r_hi = 0;
+    DevRegion R{};
+    for (uint64_t w = w_lo + blockIdx.x; w < w_hi; w += gridDim.x) {
+        if (w < r_lo || w >= r_hi) {
+            const uint32_t r = upper_region(big_pg, n_big, w);
+            R = regs[__ldg(big_idx + r)];
+            r_lo = __ldg(big_pg + r);
+            r_hi = __ldg(big_pg + r + 1);
+        }
+        const uint64_t page = w - r_lo;
+        const uint64_t P = 1ull << R.log2p;
+        const uint32_t bpp = (uint32_t)(P >> 10);
+        const uint32_t rounds = bpp / kRoundBlocks;
+        const uint64_t len = min(P, R.bytes - (page << R.log2p));
+        const uint8_t *pg = R.base + (page << R.log2p);
+        if (warp < kBigProducers) {
+            const uint32_t p = lane & 3, b = lane >> 2;
+            for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
+                const uint32_t buf = q & 1;
+                const uint32_t bi = rr * kRoundBlocks + warp * 8 + b;
+                const uint64_t boff = (uint64_t)bi * 1024 + p * 16;
+                uint4 d[16];
+                if (len == P) {
+#pragma unroll
+                    for (int s = 0; s < 16; ++s) d[s] = ld128(pg + boff + s * 64);
+                } else {
+#pragma unroll
+                    for (int s = 0; s < 16; ++s) d[s] = ld_slot16(pg, boff + s * 64, len);
+                }
+                uint64_t a0 = 0, a1 = 0;
+#pragma unroll
+                for (int s = 0; s < 15; ++s) accum16(a0, a1, d[s], sw[s + 2 * p], sw[s + 2 * p + 1]);
+                const bool lastblk = (bi == bpp - 1);
+                accum16(a0, a1, d[15], lastblk ? slast[2 * p] : sw[15 + 2 * p],
+                        lastblk ? slast[2 * p + 1] : sw[16 + 2 * p]);
+                if (q >= 2) bar_sync(3 + buf, kBigThreads);  // the chain has drained this buffer
+                S[buf][warp * 8 + b][2 * p] = a0;
+                S[buf][warp * 8 + b][2 * p + 1] = a1;
+                bar_arrive(1 + buf, kBigThreads);
+            }
+        } else {
+            const uint32_t l = lane & 7;
+            const uint64_t key = sw[16 + l];
+            uint64_t acc = sinit[l];
+            for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
+                const uint32_t buf = q & 1;
+                bar_sync(1 + buf, kBigThreads);
+                const uint32_t b0 = rr * kRoundBlocks;
+#pragma unroll 8
+                for (int j = 0; j < kRoundBlocks; ++j) {
+                    acc += S[buf][j][l];
+                    if (b0 + j != bpp - 1) acc = scramble(acc, key);
+                }
+                bar_arrive(3 + buf, kBigThreads);
+            }
+            // merge: r = P * PRIME64_1 + sum_i fold64((acc[2i]^m[2i]) * (acc[2i+1]^m[2i+1]))
+            const uint64_t x = acc ^ smerge[l];
+            const uint64_t y = __shfl_down_sync(0xffffffffu, x, 1);
+            uint64_t m = ((l & 1) == 0) ? ((x * y) ^ __umul64hi(x, y)) : 0;
+            m += __shfl_xor_sync(0xffffffffu, m, 2);
+            m += __shfl_xor_sync(0xffffffffu, m, 4);
+            uint64_t h = P * kP64_1 + m;
+            h ^= h >> 37;
+            h *= kMx1;
+            h ^= h >> 32;
+            if (lane == 0) {
+                const uint64_t g = R.page_base + page;
+                newhash[g] = h;
+                flags[g] = (h != R.table[page]) ? tag : 0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // CRUM_VERIFY (restore): recompute XXH3 of every hash-mode slot of the image
 // payload and compare with the listed hash.  Warp per slot (P = 4 KiB slots
 // use the G = 4 path with the upper half-warp duplicating the lower).
@@ -358,6 +469,18 @@ void launch_detect_hash(const Launch &L, const DevRegion *regs, const uint32_t *
     if (w_hi <= w_lo) return;
     k_detect_hash<<<grid_for(w_hi - w_lo, L.sms, 8), 256, 0, L.stream>>>(regs, hash_idx, hash_grp, n_hash, w_lo,
                                                                          w_hi, flags, newhash, tag);
+    ++*L.counter;
+}
+
+void launch_detect_hash_big(const Launch &L, const DevRegion *regs, const uint32_t *big_idx,
+                            const uint64_t *big_pg, uint32_t n_big, uint64_t w_lo, uint64_t w_hi,
+                            uint8_t *flags, uint64_t *newhash, uint8_t tag) {
+    if (w_hi <= w_lo) return;
+    uint64_t blocks = w_hi - w_lo;
+    const uint64_t cap = (uint64_t)L.sms * 2;
+    if (blocks > cap) blocks = cap;
+    k_detect_hash_big<<<(unsigned)blocks, kBigThreads, 0, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo, w_hi,
+                                                                      flags, newhash, tag);
     ++*L.counter;
 }
 

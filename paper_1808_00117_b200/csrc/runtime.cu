@@ -110,7 +110,7 @@ struct HostRegion {
 // A page range of the pipelined host path, with the matching compare-segment
 // and hash-group ranges of the detect kernels.
 struct Range {
-    uint64_t p_lo, p_hi, s_lo, s_hi, w_lo, w_hi;
+    uint64_t p_lo, p_hi, s_lo, s_hi, w_lo, w_hi, v_lo, v_hi;
 };
 
 constexpr uint64_t kDefaultChunk = 64ull << 20;
@@ -149,6 +149,9 @@ struct crum_ctx {
     uint32_t *d_hash_idx = nullptr;
     uint64_t *d_hash_grp = nullptr;
     uint32_t n_hash = 0;
+    uint32_t *d_big_idx = nullptr;   // hash regions with P >= 64 KiB (CTA per page)
+    uint64_t *d_big_pg = nullptr;
+    uint32_t n_big = 0;
     bool any_hash = false;
 
     // per-page arrays (padded to kPagesPerCompactBlock)
@@ -277,15 +280,25 @@ uint64_t seg_at(const crum_ctx *c, uint64_t p) {
 uint64_t grp_at(const crum_ctx *c, uint64_t p, bool ceil) {
     uint64_t w = 0;
     for (const HostRegion &h : c->regs) {
-        if (h.mode != kModeHash) continue;
+        if (h.mode != kModeHash || h.log2p >= kBigHashLog2) continue;
         const uint64_t k = p >= h.page_base + h.n_pages ? h.n_pages : (p > h.page_base ? p - h.page_base : 0);
         w += h.log2p == kSegLog2 ? (ceil ? (k + 1) / 2 : k / 2) : k;
     }
     return w;
 }
 
+uint64_t big_at(const crum_ctx *c, uint64_t p) {
+    uint64_t w = 0;
+    for (const HostRegion &h : c->regs) {
+        if (h.mode != kModeHash || h.log2p < kBigHashLog2) continue;
+        w += p >= h.page_base + h.n_pages ? h.n_pages : (p > h.page_base ? p - h.page_base : 0);
+    }
+    return w;
+}
+
 Range make_range(const crum_ctx *c, uint64_t lo, uint64_t hi) {
-    return Range{lo, hi, seg_at(c, lo), seg_at(c, hi), grp_at(c, lo, false), grp_at(c, hi, true)};
+    return Range{lo, hi, seg_at(c, lo), seg_at(c, hi), grp_at(c, lo, false), grp_at(c, hi, true), big_at(c, lo),
+                 big_at(c, hi)};
 }
 
 // Rebuild device descriptors and per-page arrays after the registry changed.
@@ -294,8 +307,8 @@ Range make_range(const crum_ctx *c, uint64_t lo, uint64_t hi) {
 int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
     const uint32_t R = (uint32_t)c->regs.size();
     std::vector<DevRegion> dr(R);
-    std::vector<uint32_t> cmp_idx, hash_idx;
-    std::vector<uint64_t> cmp_seg{0}, hash_grp{0};
+    std::vector<uint32_t> cmp_idx, hash_idx, big_idx;
+    std::vector<uint64_t> cmp_seg{0}, hash_grp{0}, big_pg{0};
     uint64_t N = 0, F = 0, units = 0;
     bool any_hash = false;
     for (uint32_t r = 0; r < R; ++r) {
@@ -318,7 +331,13 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
         } else {
             any_hash = true;
             hash_idx.push_back(r);
-            hash_grp.push_back(hash_grp.back() + (h.log2p == 12 ? (h.n_pages + 1) / 2 : h.n_pages));
+            if (h.log2p >= kBigHashLog2) {
+                big_idx.push_back(r);
+                big_pg.push_back(big_pg.back() + h.n_pages);
+            } else {
+                hash_idx.push_back(r);
+                hash_grp.push_back(hash_grp.back() + (h.log2p == 12 ? (h.n_pages + 1) / 2 : h.n_pages));
+            }
         }
         N += h.n_pages;
         F += h.bytes;
@@ -369,21 +388,27 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
     dev_free(c->d_cmp_seg);
     dev_free(c->d_hash_idx);
     dev_free(c->d_hash_grp);
+    dev_free(c->d_big_idx);
+    dev_free(c->d_big_pg);
     dev_free(c->d_reg_nd);
     if ((st = dev_alloc(c, &c->d_regs, sizeof(DevRegion) * R)) ||
         (st = dev_alloc(c, &c->d_cmp_idx, 4 * cmp_idx.size())) ||
         (st = dev_alloc(c, &c->d_cmp_seg, 8 * cmp_seg.size())) ||
         (st = dev_alloc(c, &c->d_hash_idx, 4 * hash_idx.size())) ||
-        (st = dev_alloc(c, &c->d_hash_grp, 8 * hash_grp.size())) || (st = dev_alloc(c, &c->d_reg_nd, 4 * R + 4)))
+        (st = dev_alloc(c, &c->d_hash_grp, 8 * hash_grp.size())) || (st = dev_alloc(c, &c->d_reg_nd, 4 * R + 4)) ||
+        (st = dev_alloc(c, &c->d_big_idx, 4 * big_idx.size())) || (st = dev_alloc(c, &c->d_big_pg, 8 * big_pg.size())))
         return st;
     if ((st = upload(c, c->d_regs, dr.data(), sizeof(DevRegion) * R)) ||
         (st = upload(c, c->d_cmp_idx, cmp_idx.data(), 4 * cmp_idx.size())) ||
         (st = upload(c, c->d_cmp_seg, cmp_seg.data(), 8 * cmp_seg.size())) ||
         (st = upload(c, c->d_hash_idx, hash_idx.data(), 4 * hash_idx.size())) ||
-        (st = upload(c, c->d_hash_grp, hash_grp.data(), 8 * hash_grp.size())))
+        (st = upload(c, c->d_hash_grp, hash_grp.data(), 8 * hash_grp.size())) ||
+        (st = upload(c, c->d_big_idx, big_idx.data(), 4 * big_idx.size())) ||
+        (st = upload(c, c->d_big_pg, big_pg.data(), 8 * big_pg.size())))
         return st;
     c->n_cmp = (uint32_t)cmp_idx.size();
     c->n_hash = (uint32_t)hash_idx.size();
+    c->n_big = (uint32_t)big_idx.size();
     c->any_hash = any_hash;
     c->N = N;
     c->F = F;
@@ -475,6 +500,8 @@ void enqueue_detect(crum_ctx *c, cudaStream_t s, const Range &rg, bool full) {
     if (!full)
         launch_detect_compare(L, c->d_regs, c->d_cmp_idx, c->d_cmp_seg, c->n_cmp, rg.s_lo, rg.s_hi, c->d_force,
                               c->d_flags, c->tag);
+    launch_detect_hash_big(L, c->d_regs, c->d_big_idx, c->d_big_pg, c->n_big, rg.v_lo, rg.v_hi, c->d_flags,
+                           c->d_newhash, c->tag);
     launch_detect_hash(L, c->d_regs, c->d_hash_idx, c->d_hash_grp, c->n_hash, rg.w_lo, rg.w_hi, c->d_flags,
                        c->d_newhash, c->tag);
 }
@@ -705,6 +732,8 @@ int crum_destroy(crum_ctx *c) {
     dev_free(c->d_cmp_seg);
     dev_free(c->d_hash_idx);
     dev_free(c->d_hash_grp);
+    dev_free(c->d_big_idx);
+    dev_free(c->d_big_pg);
     dev_free(c->d_force);
     dev_free(c->d_flags);
     dev_free(c->d_newhash);
