@@ -330,7 +330,6 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
             cmp_seg.push_back(cmp_seg.back() + (h.bytes + kSegBytes - 1) / kSegBytes);
         } else {
             any_hash = true;
-            hash_idx.push_back(r);
             if (h.log2p >= kBigHashLog2) {
                 big_idx.push_back(r);
                 big_pg.push_back(big_pg.back() + h.n_pages);
