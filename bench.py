@@ -328,13 +328,24 @@ def main():
     K = reps[-1]["dirty_pages"]
     KP = reps[-1]["image_bytes"]
     peak, peak_src = read_peaks()
-    # dominant kernel: A1 detect (compare: reads region + mirror; hash: region + table)
+    # dominant kernel.  Single-pass path (all compare, P <= 64 KiB): the fused
+    # detect+compact+gather kernel, algorithmic bytes = read region + mirror
+    # (2F) + write image payload + mirror (2 KP).  Otherwise A1 detect:
+    # compare reads region + mirror (2F); hash reads region + table and writes
+    # the new hashes (F + 16 N).
     n_pages = sum(synth.n_pages(nb, P) for nb, P, _ in specs)
-    det_bytes = 2 * F if args.mode == "compare" else F + 8 * n_pages + 8 * n_pages
+    payload = reps[-1]["image_bytes"]
+    fused = bool(reps[-1].get("path", 0) & 1)
+    if fused:
+        kname = "fused_compare"
+        det_bytes = 2 * F + 2 * payload
+    else:
+        kname = f"detect_{args.mode}"
+        det_bytes = 2 * F if args.mode == "compare" else F + 16 * n_pages
     det_t = det_sum / args.steps / 1e3
     achieved = det_bytes / det_t / 1e9
-    payload = reps[-1]["image_bytes"]
     dev_alg = (2 * F + 2 * payload) if args.mode == "compare" else (F + 16 * n_pages + 2 * payload)
+    traffic_key = f"{kname}:{args.config}:{args.page}:{args.dirty}"
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(T * 1e3 / args.steps, 4), "higher_is_better": True,
@@ -346,10 +357,10 @@ def main():
                    "timing": "per-step CUDA events around crum_checkpoint_gather_device on its stream; "
                              "application writer + scrub outside the events",
                    "wall_ms_per_step_incl_writer": round(wall * 1e3 / args.steps, 3)},
-        "roofline": {"bound": "hbm", "kernel": f"detect_{args.mode}", "achieved": round(achieved, 1),
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1),
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "alg_bytes_per_launch": det_bytes, "avg_launch_ms": round(det_t * 1e3, 4),
-                     "traffic": read_traffic(f"detect_{args.mode}")},
+                     "traffic": read_traffic(traffic_key), "traffic_key": traffic_key},
         "device_phase": {"alg_bytes_per_step": dev_alg, "achieved_GBs": round(dev_alg / (T / args.steps) / 1e9, 1),
                          "frac": round(dev_alg / (T / args.steps) / 1e9 / peak, 4)},
         "gpu_launches": launches,

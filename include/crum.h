@@ -109,7 +109,12 @@ typedef struct {
     double t_gather_ms;      /* A3: gather + commit (restore: scatter + commit) */
     double t_copy_ms;        /* A4: host-link copy (D2H for gather, H2D for restore) */
     double t_total_ms;       /* whole call, first enqueue to completion */
+    uint32_t path;           /* bit0 CRUM_PATH_FUSED: single-pass detect+compact+gather kernel ran
+                                (t_detect_ms then covers all three, t_gather_ms is 0) */
+    uint32_t reserved;
 } crum_report;
+
+enum { CRUM_PATH_FUSED = 1u << 0 };
 
 /* ---------------------------------------------------------------------------
  * Context.  crum_create binds to CUDA device `device` (cudaSetDevice is

@@ -30,6 +30,7 @@ E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY, E_DEVICE, E_CUDA = -6, -7, -8, -9, -1
 MODE_COMPARE, MODE_HASH = 0, 1
 FULL, VERIFY = 1, 2
 CFG_TIMING = 1
+PATH_FUSED = 1
 EXPORT_FORCE, EXPORT_HASHES, EXPORT_MIRROR = 0, 1, 2
 ALL_PAGES = (1 << 64) - 1
 
@@ -53,7 +54,8 @@ class Report(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("scanned_pages", "scanned_bytes", "dirty_pages", "dirty_bytes",
                                           "dirty_runs", "image_bytes")] + \
                [(n, C.c_double) for n in ("t_detect_ms", "t_compact_ms", "t_gather_ms", "t_copy_ms",
-                                          "t_total_ms")]
+                                          "t_total_ms")] + \
+               [("path", C.c_uint32), ("reserved", C.c_uint32)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

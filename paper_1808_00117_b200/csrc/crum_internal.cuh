@@ -163,6 +163,37 @@ struct ScatterArgs {
     uint64_t u_lo, u_hi;
 };
 
+// Single-pass checkpoint (all regions COMPARE, P <= 64 KiB): detect +
+// decoupled look-back compaction + gather + commit in one persistent kernel.
+constexpr uint32_t kFusedMaxLog2P = 16;
+constexpr uint32_t kFusedMinTileLog2 = 15;   // tile = max(P, 32 KiB)
+struct FusedScratch {
+    uint32_t ticket;          // next tile to claim
+    uint32_t done;            // tiles finished
+    uint64_t dirty_bytes;     // accumulated logical bytes of listed pages
+};
+struct FusedArgs {
+    const DevRegion *regs;
+    uint32_t R;
+    uint32_t tag;             // 1..255, also tags the look-back status words
+    const uint64_t *tile_base;// per region: first tile (prefix, R + 1 entries)
+    uint64_t n_tiles;
+    uint64_t *status;         // per tile: tag | state | count | units
+    FusedScratch *fs;
+    uint8_t *force;
+    uint8_t *img;             // device image (payload at poff)
+    uint64_t poff;
+    uint32_t *gids;
+    uint64_t *sunit;
+    uint32_t *lids;
+    uint32_t *reg_nd;
+    RegStat *rs;
+    DevStats *st;
+    uint64_t capacity;
+};
+void launch_fused_compare(const Launch &L, const FusedArgs &a, int blocks);
+int fused_blocks_per_sm();
+
 // ---- detect (kernels_detect.cu) ----
 void launch_detect_compare(const Launch &L, const DevRegion *regs, const uint32_t *cmp_idx,
                            const uint64_t *cmp_seg, uint32_t n_cmp, uint64_t s_lo, uint64_t s_hi,

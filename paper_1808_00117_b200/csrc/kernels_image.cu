@@ -749,4 +749,256 @@ void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *f
     ++*L.counter;
 }
 
+// ===========================================================================
+// Single-pass checkpoint for contexts whose regions are all COMPARE mode with
+// pages <= 64 KiB (SURVEY.md sec. 7.3 hard part 1): one persistent kernel does
+// A1 detect, A2 compaction and A3 gather + commit.
+//
+//  * Work unit: a tile of max(P, 32 KiB) bytes of one region, claimed through
+//    a ticket counter (so every predecessor of a tile is held by a running
+//    CTA: the look-back below cannot deadlock).
+//  * Detect: 8 warps compare 4 KiB segments (LDG.256, as k_detect_compare)
+//    and mark the tile's dirty pages in shared memory.
+//  * Compaction: the tile publishes its (dirty pages, 4 KiB units) aggregate,
+//    then warp 0 looks back over predecessor status words 32 at a time
+//    (decoupled look-back) until it meets an inclusive prefix; the tile's
+//    slot and payload offsets follow.  Deterministic: offsets come from
+//    prefix sums only, so the image is canonical.
+//  * Gather + commit: the dirty pages (just read, so L2-resident) are copied
+//    to the image payload and the mirror; slot metadata (ids) is written for
+//    the CRC kernel; force bits cleared.
+//  * The last CTA to finish a tile finalises (region table, header fields).
+// Status word: [63:56] tag, [55:54] state (1 aggregate, 2 inclusive prefix),
+// [53:27] dirty pages, [26:0] units (so footprints < 512 GiB).
+// ===========================================================================
+constexpr uint32_t kFusedThreads = 256;
+constexpr uint64_t kStAgg = 1, kStPrefix = 2;
+
+__device__ __forceinline__ uint64_t pack_status(uint32_t tag, uint64_t state, uint64_t cnt, uint64_t units) {
+    return ((uint64_t)tag << 56) | (state << 54) | ((cnt & 0x7ffffffull) << 27) | (units & 0x7ffffffull);
+}
+__device__ __forceinline__ void st_release(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void ld256(const void *p, uint32_t (&r)[8]) {
+    asm volatile("ld.global.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7])
+                 : "l"(p));
+}
+
+__global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
+    __shared__ uint32_t s_dirty[8];
+    __shared__ uint32_t s_pidx[8];
+    __shared__ uint64_t s_t;
+    __shared__ uint64_t s_excl[2];
+    __shared__ uint32_t s_cnt;
+    __shared__ bool s_last;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (;;) {
+        if (threadIdx.x == 0) s_t = atomicAdd(&a.fs->ticket, 1u);
+        if (threadIdx.x < 8) s_dirty[threadIdx.x] = 0;
+        __syncthreads();
+        const uint64_t t = s_t;
+        if (t >= a.n_tiles) break;
+        // tile -> region, byte range
+        uint32_t r;
+        {
+            uint32_t lo = 0, hi = a.R;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (__ldg(a.tile_base + mid) <= t) lo = mid; else hi = mid;
+            }
+            r = lo;
+        }
+        const DevRegion g = a.regs[r];
+        const uint32_t tlog = max(g.log2p, kFusedMinTileLog2);
+        const uint64_t off0 = (t - __ldg(a.tile_base + r)) << tlog;
+        const uint64_t tlen = min((uint64_t)1 << tlog, g.bytes - off0);
+        const uint64_t i0 = off0 >> g.log2p;                          // first page of the tile
+        const uint32_t npg = (uint32_t)((tlen + (1ull << g.log2p) - 1) >> g.log2p);
+        const uint32_t nseg = (uint32_t)((tlen + kSegBytes - 1) >> kSegLog2);
+        // ---- A1 detect ----
+        for (uint32_t s = warp; s < nseg; s += kFusedThreads / 32) {
+            const uint32_t j = (s << kSegLog2) >> g.log2p;            // page within the tile
+            if (a.force[g.page_base + i0 + j]) continue;               // dirty by force
+            const uint64_t off = off0 + ((uint64_t)s << kSegLog2);
+            const uint64_t len = g.bytes - off;
+            const uint8_t *pa = g.base + off, *pb = g.mirror + off;
+            uint32_t x = 0;
+            if (len >= kSegBytes && g.aligned32) {
+                uint32_t va[4][8], vb[4][8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    ld256(pa + i * 1024 + lane * 32, va[i]);
+                    ld256(pb + i * 1024 + lane * 32, vb[i]);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) x |= va[i][k] ^ vb[i][k];
+            } else if (len >= kSegBytes) {
+                for (int i = 0; i < 8; ++i) {
+                    const uint4 u = *reinterpret_cast<const uint4 *>(pa + i * 512 + lane * 16);
+                    const uint4 v = *reinterpret_cast<const uint4 *>(pb + i * 512 + lane * 16);
+                    x |= (u.x ^ v.x) | (u.y ^ v.y) | (u.z ^ v.z) | (u.w ^ v.w);
+                }
+            } else {
+                for (uint32_t o = lane; o < len; o += 32) x |= (uint32_t)(pa[o] ^ pb[o]);
+            }
+            if (__any_sync(0xffffffffu, x != 0) && lane == 0) s_dirty[j] = 1;
+        }
+        __syncthreads();
+        // ---- A2 compaction: aggregate, look-back, inclusive prefix ----
+        if (warp == 0) {
+            const uint64_t gp = g.page_base + i0 + lane;
+            const bool d = lane < npg && (s_dirty[lane] || a.force[gp]);
+            const uint32_t bal = __ballot_sync(0xffffffffu, d);
+            const uint32_t cnt = __popc(bal);
+            const uint32_t up = 1u << (g.log2p - kSegLog2);
+            if (d) s_pidx[__popc(bal & ((1u << lane) - 1))] = lane;
+            if (lane == 0) st_release(a.status + t, pack_status(a.tag, kStAgg, cnt, (uint64_t)cnt * up));
+            uint64_t ec = 0, eu = 0;
+            int64_t top = (int64_t)t - 1;
+            while (top >= 0) {
+                const int64_t idx = top - (int64_t)lane;
+                uint64_t v = pack_status(a.tag, kStPrefix, 0, 0);   // before tile 0: prefix 0
+                uint32_t stt = (uint32_t)kStPrefix;
+                if (idx >= 0) {
+                    do {
+                        v = ld_acquire(a.status + idx);
+                        stt = ((v >> 56) == a.tag) ? (uint32_t)((v >> 54) & 3) : 0u;
+                    } while (stt == 0);
+                }
+                const uint32_t pm = __ballot_sync(0xffffffffu, stt == kStPrefix);
+                const int first = pm ? __ffs(pm) - 1 : 32;
+                uint64_t c = ((int)lane <= first) ? ((v >> 27) & 0x7ffffffull) : 0;
+                uint64_t u = ((int)lane <= first) ? (v & 0x7ffffffull) : 0;
+                ec += warp_sum(c);
+                eu += warp_sum(u);
+                if (pm) break;
+                top -= 32;
+            }
+            if (lane == 0) {
+                st_release(a.status + t, pack_status(a.tag, kStPrefix, ec + cnt, eu + (uint64_t)cnt * up));
+                s_excl[0] = ec;
+                s_excl[1] = eu;
+                s_cnt = cnt;
+            }
+        }
+        __syncthreads();
+        const uint32_t cnt = s_cnt;
+        const uint64_t ec = s_excl[0], eu = s_excl[1];
+        // ---- A3 gather + commit ----
+        const uint32_t upl = g.log2p - kSegLog2;
+        const uint32_t up = 1u << upl;
+        const uint32_t nunits = cnt << upl;
+        for (uint32_t u = warp; u < nunits; u += kFusedThreads / 32) {
+            const uint32_t rank = u >> upl, seg = u & (up - 1);
+            const uint64_t i = i0 + s_pidx[rank];
+            const uint64_t off = (i << g.log2p) + ((uint64_t)seg << kSegLog2);
+            const uint64_t len = g.bytes > off ? min((uint64_t)kSegBytes, g.bytes - off) : 0;
+            copy_unit(g.base + off, len, g.aligned32 != 0, a.img + a.poff + ((eu + u) << kSegLog2), g.mirror + off,
+                      lane);
+        }
+        if (threadIdx.x < cnt) {
+            const uint32_t rank = threadIdx.x;
+            const uint64_t i = i0 + s_pidx[rank];
+            const uint64_t k = ec + rank;
+            a.gids[k] = (uint32_t)(g.page_base + i);
+            a.sunit[k] = eu + ((uint64_t)rank << upl);
+            a.lids[k] = (uint32_t)i;
+            a.force[g.page_base + i] = 0;
+            const uint64_t db = page_len(g, i);
+            atomicAdd(reinterpret_cast<unsigned long long *>(&a.fs->dirty_bytes), (unsigned long long)db);
+            if (rank == 0) atomicAdd(a.reg_nd + r, cnt);
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = (atomicAdd(&a.fs->done, 1u) == a.n_tiles - 1);
+        __syncthreads();
+        if (s_last) break;
+    }
+    if (!s_last) return;
+    // ---- finalise (the CTA that finished the last tile) ----
+    __threadfence();
+    const uint64_t fin = ld_acquire(a.status + a.n_tiles - 1);
+    const uint64_t K = (fin >> 27) & 0x7ffffffull, U = fin & 0x7ffffffull;
+    uint64_t carry_first = 0, carry_units = 0;
+    for (uint32_t r0 = 0; r0 < a.R; r0 += blockDim.x) {
+        const uint32_t r = r0 + threadIdx.x;
+        uint64_t nd = 0, un = 0;
+        DevRegion g{};
+        if (r < a.R) {
+            g = a.regs[r];
+            nd = *(volatile uint32_t *)(a.reg_nd + r);
+            un = nd << (g.log2p - kSegLog2);
+        }
+        uint64_t tn, tun;
+        const uint64_t en = block_excl_scan(nd, &tn);
+        const uint64_t eun = block_excl_scan(un, &tun);
+        if (r < a.R) {
+            RegStat s;
+            s.first = carry_first + en;
+            s.n_dirty = nd;
+            s.unit_base = carry_units + eun;
+            s.payload_base = s.unit_base << kSegLog2;
+            a.rs[r] = s;
+            a.reg_nd[r] = 0;  // ready for the next checkpoint
+            uint8_t *e = a.img + 64 + 48ull * r;
+            reinterpret_cast<uint32_t *>(e)[0] = g.id;
+            reinterpret_cast<uint32_t *>(e)[1] = g.mode;
+            reinterpret_cast<uint64_t *>(e)[1] = g.bytes;
+            reinterpret_cast<uint64_t *>(e)[2] = 1ull << g.log2p;
+            reinterpret_cast<uint64_t *>(e)[3] = g.n_pages;
+            reinterpret_cast<uint64_t *>(e)[4] = nd;
+            reinterpret_cast<uint64_t *>(e)[5] = s.first;
+        }
+        carry_first += tn;
+        carry_units += tun;
+    }
+    const uint64_t poff = a.poff;
+    for (uint64_t b = 64 + 48ull * a.R + threadIdx.x; b < poff; b += blockDim.x) a.img[b] = 0;
+    if (threadIdx.x == 0) {
+        DevStats *st = a.st;
+        const uint64_t payload = U << kSegLog2;
+        const uint64_t ids_off = poff + payload;
+        st->K = K;
+        st->total_units = U;
+        st->poff = poff;
+        st->payload_bytes = payload;
+        st->ids_off = ids_off;
+        st->image_bytes = ids_off + round_up(4 * K, 8);
+        st->capacity = a.capacity;
+        st->status = st->image_bytes > a.capacity ? kStCapacity : kStOk;
+        st->img_flags = 0;
+        st->n_regions = a.R;
+        st->dirty_bytes = a.fs->dirty_bytes;
+        st->dirty_runs = 0;
+        st->crc_acc = 0;
+        a.fs->dirty_bytes = 0;
+        a.fs->ticket = 0;
+        a.fs->done = 0;
+    }
+}
+
+int fused_blocks_per_sm() {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fused_compare, kFusedThreads, 0) != cudaSuccess) {
+        cudaGetLastError();
+        n = 2;
+    }
+    return n > 0 ? n : 1;
+}
+
+void launch_fused_compare(const Launch &L, const FusedArgs &a, int blocks) {
+    k_fused_compare<<<blocks, kFusedThreads, 0, L.stream>>>(a);
+    ++*L.counter;
+}
+
 }  // namespace crum

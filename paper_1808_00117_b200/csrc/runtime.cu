@@ -154,6 +154,15 @@ struct crum_ctx {
     uint32_t n_big = 0;
     bool any_hash = false;
 
+    // single-pass (fused) checkpoint: all regions COMPARE with P <= 64 KiB
+    bool fused_ok = false;
+    uint64_t *d_tile_base = nullptr;
+    uint64_t n_tiles = 0;
+    uint64_t *d_status = nullptr;
+    FusedScratch *d_fs = nullptr;
+    int fused_bps = 1;
+    bool last_fused = false;
+
     // per-page arrays (padded to kPagesPerCompactBlock)
     uint64_t page_cap = 0;
     uint8_t *d_force = nullptr;
@@ -412,6 +421,29 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
     c->N = N;
     c->F = F;
     c->max_units = units;
+    // single-pass eligibility and its tile map
+    {
+        bool ok = R > 0 && (units >> 27) == 0;
+        std::vector<uint64_t> tb{0};
+        for (const HostRegion &h : c->regs) {
+            ok = ok && h.mode == kModeCompare && h.log2p <= kFusedMaxLog2P;
+            const uint32_t tl = std::max(h.log2p, kFusedMinTileLog2);
+            tb.push_back(tb.back() + ((h.bytes + (1ull << tl) - 1) >> tl));
+        }
+        dev_free(c->d_tile_base);
+        dev_free(c->d_status);
+        c->fused_ok = false;
+        c->n_tiles = 0;
+        if (ok) {
+            if ((st = dev_alloc(c, &c->d_tile_base, 8 * tb.size())) ||
+                (st = dev_alloc(c, &c->d_status, 8 * (tb.back() + 1))))
+                return st;
+            if ((st = upload(c, c->d_tile_base, tb.data(), 8 * tb.size()))) return st;
+            CK(cudaMemset(c->d_status, 0, 8 * (tb.back() + 1)));
+            c->n_tiles = tb.back();
+            c->fused_ok = true;
+        }
+    }
     // per-region scratch and the host-path metadata buffer (head + tail)
     if (R + 1 > c->rs_cap) {
         dev_free(c->d_rs);
@@ -488,6 +520,7 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 int next_tag(crum_ctx *c, cudaStream_t s) {
     if (c->tag == 255 || c->tag == 0) {
         CK(cudaMemsetAsync(c->d_flags, 0, c->page_cap, s));
+        if (c->d_status) CK(cudaMemsetAsync(c->d_status, 0, 8 * (c->n_tiles + 1), s));
         c->tag = 0;
     }
     ++c->tag;
@@ -586,7 +619,7 @@ void fill_report(crum_ctx *c, const DevStats &h, crum_report *rep) {
     rep->image_bytes = h.image_bytes;
 }
 
-enum { kLastNone = 0, kLastSync = 1, kLastDevGather = 2, kLastHostGather = 3, kLastRestore = 4 };
+enum { kLastNone = 0, kLastSync = 1, kLastDevGather = 2, kLastHostGather = 3, kLastRestore = 4, kLastDevFused = 5 };
 
 // Phase times of the most recent call from its events (see each call for
 // which events delimit which phase).
@@ -598,6 +631,12 @@ void fill_times(crum_ctx *c, crum_report *rep) {
             rep->t_compact_ms = ev_ms(e[1], e[2]);
             rep->t_gather_ms = ev_ms(e[2], e[4]);
             rep->t_total_ms = ev_ms(e[0], e[4]);
+            break;
+        case kLastDevFused:
+            rep->t_detect_ms = ev_ms(e[0], e[1]);   // detect + compact + gather (one kernel)
+            rep->t_compact_ms = ev_ms(e[1], e[4]);  // metadata CRC + header
+            rep->t_total_ms = ev_ms(e[0], e[4]);
+            rep->path = CRUM_PATH_FUSED;
             break;
         case kLastDevGather:
             rep->t_detect_ms = ev_ms(e[0], e[1]);
@@ -705,6 +744,9 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     if (cudaMalloc(&c->d_st, sizeof(DevStats)) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaMalloc(&c->d_rb, sizeof(RangeTotals) * (kMaxRanges + 1)) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaMalloc(&c->d_done, 16) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    if (cudaMalloc(&c->d_fs, sizeof(FusedScratch)) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    cudaMemset(c->d_fs, 0, sizeof(FusedScratch));
+    c->fused_bps = fused_blocks_per_sm();
     if (cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocMapped) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaHostAlloc(&c->h_rb, sizeof(RangeTotals) * (kMaxRanges + 1), cudaHostAllocMapped) != cudaSuccess)
         return fail(CRUM_E_NOMEM);
@@ -743,6 +785,9 @@ int crum_destroy(crum_ctx *c) {
     dev_free(c->d_blk_count);
     dev_free(c->d_blk_units);
     dev_free(c->d_dbg);
+    dev_free(c->d_tile_base);
+    dev_free(c->d_status);
+    dev_free(c->d_fs);
     dev_free(c->d_reg_nd);
     dev_free(c->d_rs);
     dev_free(c->d_tregs);
@@ -1004,6 +1049,49 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     const bool timing = rep != nullptr || c->timing_cfg;
     uint8_t *img = static_cast<uint8_t *>(dev_image);
     int st;
+    uint64_t worst = 0;
+    crum_image_required_bytes(c, UINT64_MAX, &worst);
+    if (c->fused_ok && !full && capacity >= worst && !getenv("CRUM_NO_FUSED")) {
+        // single pass: detect + compact + gather + commit in one kernel, then
+        // the metadata CRC / tail / header
+        if (timing) CK(cudaEventRecord(c->ev_t[0], s));
+        if ((st = next_tag(c, s))) return st;
+        FusedArgs fa{};
+        fa.regs = c->d_regs;
+        fa.R = (uint32_t)c->regs.size();
+        fa.tag = c->tag;
+        fa.tile_base = c->d_tile_base;
+        fa.n_tiles = c->n_tiles;
+        fa.status = c->d_status;
+        fa.fs = c->d_fs;
+        fa.force = c->d_force;
+        fa.img = img;
+        fa.poff = payload_offset_for(c->regs.size());
+        fa.gids = c->d_gids;
+        fa.sunit = c->d_sunit;
+        fa.lids = c->d_lids;
+        fa.reg_nd = c->d_reg_nd;
+        fa.rs = c->d_rs;
+        fa.st = c->d_st;
+        fa.capacity = capacity;
+        Launch L = launch_of(c, s);
+        launch_fused_compare(L, fa, c->sms * c->fused_bps);
+        if (timing) CK(cudaEventRecord(c->ev_t[1], s));
+        launch_crc_meta(L, crc_args(c, img, nullptr), crc_max_len(c));
+        CK_LAUNCH();
+        if (timing) CK(cudaEventRecord(c->ev_t[4], s));
+        CK(cudaEventRecord(c->ev_done, s));
+        c->last_kind = kLastDevFused;
+        c->last_timed = timing;
+        if (rep) {
+            CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            memset(rep, 0, sizeof *rep);
+            fill_report(c, *c->h_st, rep);
+            fill_times(c, rep);
+        }
+        return CRUM_OK;
+    }
     if (timing) CK(cudaEventRecord(c->ev_t[0], s));
     if ((st = next_tag(c, s))) return st;
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
