@@ -771,7 +771,7 @@ void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *f
 // Status word: [63:56] tag, [55:54] state (1 aggregate, 2 inclusive prefix),
 // [53:27] dirty pages, [26:0] units (so footprints < 512 GiB).
 // ===========================================================================
-constexpr uint32_t kFusedThreads = 256;
+constexpr uint32_t kFusedThreads = 128;
 constexpr uint64_t kStAgg = 1, kStPrefix = 2;
 
 __device__ __forceinline__ uint64_t pack_status(uint32_t tag, uint64_t state, uint64_t cnt, uint64_t units) {
@@ -792,19 +792,28 @@ __device__ __forceinline__ void ld256(const void *p, uint32_t (&r)[8]) {
                  : "l"(p));
 }
 
+// Warp-exclusive scan of u64 (returns exclusive prefix, *total = warp sum).
+__device__ __forceinline__ uint64_t warp_excl_scan(uint64_t v, uint64_t *total) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (uint32_t)o) inc += t;
+    }
+    *total = __shfl_sync(0xffffffffu, inc, 31);
+    return inc - v;
+}
+
+// Each WARP owns one tile at a time: no block barriers, so while one warp
+// waits in its look-back the SM's other warps keep streaming.
 __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
-    __shared__ uint32_t s_dirty[8];
-    __shared__ uint32_t s_pidx[8];
-    __shared__ uint64_t s_t;
-    __shared__ uint64_t s_excl[2];
-    __shared__ uint32_t s_cnt;
-    __shared__ bool s_last;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lane = threadIdx.x & 31;
+    bool last = false;
     for (;;) {
-        if (threadIdx.x == 0) s_t = atomicAdd(&a.fs->ticket, 1u);
-        if (threadIdx.x < 8) s_dirty[threadIdx.x] = 0;
-        __syncthreads();
-        const uint64_t t = s_t;
+        uint64_t t = 0;
+        if (lane == 0) t = atomicAdd(&a.fs->ticket, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= a.n_tiles) break;
         // tile -> region, byte range
         uint32_t r;
@@ -820,14 +829,17 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
         const uint32_t tlog = max(g.log2p, kFusedMinTileLog2);
         const uint64_t off0 = (t - __ldg(a.tile_base + r)) << tlog;
         const uint64_t tlen = min((uint64_t)1 << tlog, g.bytes - off0);
-        const uint64_t i0 = off0 >> g.log2p;                          // first page of the tile
+        const uint64_t i0 = off0 >> g.log2p;  // first page of the tile
         const uint32_t npg = (uint32_t)((tlen + (1ull << g.log2p) - 1) >> g.log2p);
         const uint32_t nseg = (uint32_t)((tlen + kSegBytes - 1) >> kSegLog2);
-        // ---- A1 detect ----
-        for (uint32_t s = warp; s < nseg; s += kFusedThreads / 32) {
-            const uint32_t j = (s << kSegLog2) >> g.log2p;            // page within the tile
-            if (a.force[g.page_base + i0 + j]) continue;               // dirty by force
-            const uint64_t off = off0 + ((uint64_t)s << kSegLog2);
+        const uint32_t spl = g.log2p - kSegLog2;  // log2 segments per page
+        // ---- A1 detect: force bits, then 4 KiB segments; a page found dirty
+        // stops being compared (its bytes are gathered below anyway) ----
+        uint32_t dmask = __ballot_sync(0xffffffffu, lane < npg && a.force[g.page_base + i0 + lane] != 0);
+        for (uint32_t sg = 0; sg < nseg; ++sg) {
+            const uint32_t j = sg >> spl;
+            if ((dmask >> j) & 1u) continue;
+            const uint64_t off = off0 + ((uint64_t)sg << kSegLog2);
             const uint64_t len = g.bytes - off;
             const uint8_t *pa = g.base + off, *pb = g.mirror + off;
             uint32_t x = 0;
@@ -851,87 +863,81 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
             } else {
                 for (uint32_t o = lane; o < len; o += 32) x |= (uint32_t)(pa[o] ^ pb[o]);
             }
-            if (__any_sync(0xffffffffu, x != 0) && lane == 0) s_dirty[j] = 1;
+            if (__any_sync(0xffffffffu, x != 0)) dmask |= 1u << j;
         }
-        __syncthreads();
         // ---- A2 compaction: aggregate, look-back, inclusive prefix ----
-        if (warp == 0) {
-            const uint64_t gp = g.page_base + i0 + lane;
-            const bool d = lane < npg && (s_dirty[lane] || a.force[gp]);
-            const uint32_t bal = __ballot_sync(0xffffffffu, d);
-            const uint32_t cnt = __popc(bal);
-            const uint32_t up = 1u << (g.log2p - kSegLog2);
-            if (d) s_pidx[__popc(bal & ((1u << lane) - 1))] = lane;
-            if (lane == 0) st_release(a.status + t, pack_status(a.tag, kStAgg, cnt, (uint64_t)cnt * up));
-            uint64_t ec = 0, eu = 0;
-            int64_t top = (int64_t)t - 1;
-            while (top >= 0) {
-                const int64_t idx = top - (int64_t)lane;
-                uint64_t v = pack_status(a.tag, kStPrefix, 0, 0);   // before tile 0: prefix 0
-                uint32_t stt = (uint32_t)kStPrefix;
-                if (idx >= 0) {
-                    do {
-                        v = ld_acquire(a.status + idx);
-                        stt = ((v >> 56) == a.tag) ? (uint32_t)((v >> 54) & 3) : 0u;
-                    } while (stt == 0);
-                }
-                const uint32_t pm = __ballot_sync(0xffffffffu, stt == kStPrefix);
-                const int first = pm ? __ffs(pm) - 1 : 32;
-                uint64_t c = ((int)lane <= first) ? ((v >> 27) & 0x7ffffffull) : 0;
-                uint64_t u = ((int)lane <= first) ? (v & 0x7ffffffull) : 0;
-                ec += warp_sum(c);
-                eu += warp_sum(u);
-                if (pm) break;
-                top -= 32;
+        const uint32_t cnt = __popc(dmask);
+        const uint64_t ucnt = (uint64_t)cnt << spl;
+        if (lane == 0) st_release(a.status + t, pack_status(a.tag, kStAgg, cnt, ucnt));
+        uint64_t ec = 0, eu = 0;
+        int64_t top = (int64_t)t - 1;
+        while (top >= 0) {
+            const int64_t idx = top - (int64_t)lane;
+            uint64_t v = pack_status(a.tag, kStPrefix, 0, 0);  // before tile 0: prefix 0
+            uint32_t stt = (uint32_t)kStPrefix;
+            if (idx >= 0) {
+                do {
+                    v = ld_acquire(a.status + idx);
+                    stt = ((v >> 56) == a.tag) ? (uint32_t)((v >> 54) & 3) : 0u;
+                } while (stt == 0);
             }
-            if (lane == 0) {
-                st_release(a.status + t, pack_status(a.tag, kStPrefix, ec + cnt, eu + (uint64_t)cnt * up));
-                s_excl[0] = ec;
-                s_excl[1] = eu;
-                s_cnt = cnt;
+            const uint32_t pm = __ballot_sync(0xffffffffu, stt == kStPrefix);
+            const int first = pm ? __ffs(pm) - 1 : 32;
+            const uint64_t c = ((int)lane <= first) ? ((v >> 27) & 0x7ffffffull) : 0;
+            const uint64_t u = ((int)lane <= first) ? (v & 0x7ffffffull) : 0;
+            ec += warp_sum(c);
+            eu += warp_sum(u);
+            if (pm) break;
+            top -= 32;
+        }
+        if (lane == 0) st_release(a.status + t, pack_status(a.tag, kStPrefix, ec + cnt, eu + ucnt));
+        // ---- A3 gather + commit: the tile's dirty pages, ascending ----
+        uint32_t m = dmask;
+        for (uint32_t rank = 0; m; ++rank, m &= m - 1) {
+            const uint32_t j = __ffs(m) - 1;
+            const uint64_t i = i0 + j;
+            const uint64_t pg_off = i << g.log2p;
+            const uint64_t dst_u = eu + ((uint64_t)rank << spl);
+            for (uint32_t sg = 0; sg < (1u << spl); ++sg) {
+                const uint64_t off = pg_off + ((uint64_t)sg << kSegLog2);
+                const uint64_t len = g.bytes > off ? min((uint64_t)kSegBytes, g.bytes - off) : 0;
+                copy_unit(g.base + off, len, g.aligned32 != 0, a.img + a.poff + ((dst_u + sg) << kSegLog2),
+                          g.mirror + off, lane);
             }
         }
-        __syncthreads();
-        const uint32_t cnt = s_cnt;
-        const uint64_t ec = s_excl[0], eu = s_excl[1];
-        // ---- A3 gather + commit ----
-        const uint32_t upl = g.log2p - kSegLog2;
-        const uint32_t up = 1u << upl;
-        const uint32_t nunits = cnt << upl;
-        for (uint32_t u = warp; u < nunits; u += kFusedThreads / 32) {
-            const uint32_t rank = u >> upl, seg = u & (up - 1);
-            const uint64_t i = i0 + s_pidx[rank];
-            const uint64_t off = (i << g.log2p) + ((uint64_t)seg << kSegLog2);
-            const uint64_t len = g.bytes > off ? min((uint64_t)kSegBytes, g.bytes - off) : 0;
-            copy_unit(g.base + off, len, g.aligned32 != 0, a.img + a.poff + ((eu + u) << kSegLog2), g.mirror + off,
-                      lane);
-        }
-        if (threadIdx.x < cnt) {
-            const uint32_t rank = threadIdx.x;
-            const uint64_t i = i0 + s_pidx[rank];
+        uint64_t db = 0;
+        if (lane < 32 && ((dmask >> lane) & 1u)) {
+            const uint32_t rank = __popc(dmask & ((1u << lane) - 1));
+            const uint64_t i = i0 + lane;
             const uint64_t k = ec + rank;
             a.gids[k] = (uint32_t)(g.page_base + i);
-            a.sunit[k] = eu + ((uint64_t)rank << upl);
+            a.sunit[k] = eu + ((uint64_t)rank << spl);
             a.lids[k] = (uint32_t)i;
             a.force[g.page_base + i] = 0;
-            const uint64_t db = page_len(g, i);
+            db = page_len(g, i);
+        }
+        db = warp_sum(db);
+        if (lane == 0 && cnt) {
             atomicAdd(reinterpret_cast<unsigned long long *>(&a.fs->dirty_bytes), (unsigned long long)db);
-            if (rank == 0) atomicAdd(a.reg_nd + r, cnt);
+            atomicAdd(a.reg_nd + r, cnt);
         }
         __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) s_last = (atomicAdd(&a.fs->done, 1u) == a.n_tiles - 1);
-        __syncthreads();
-        if (s_last) break;
+        uint32_t f = 0;
+        if (lane == 0) f = atomicAdd(&a.fs->done, 1u);
+        f = __shfl_sync(0xffffffffu, f, 0);
+        if (f == a.n_tiles - 1) {
+            last = true;
+            break;
+        }
     }
-    if (!s_last) return;
-    // ---- finalise (the CTA that finished the last tile) ----
+    if (!last) return;
+    // ---- finalise (the warp that finished the last tile) ----
     __threadfence();
     const uint64_t fin = ld_acquire(a.status + a.n_tiles - 1);
     const uint64_t K = (fin >> 27) & 0x7ffffffull, U = fin & 0x7ffffffull;
     uint64_t carry_first = 0, carry_units = 0;
-    for (uint32_t r0 = 0; r0 < a.R; r0 += blockDim.x) {
-        const uint32_t r = r0 + threadIdx.x;
+    for (uint32_t r0 = 0; r0 < a.R; r0 += 32) {
+        const uint32_t r = r0 + lane;
         uint64_t nd = 0, un = 0;
         DevRegion g{};
         if (r < a.R) {
@@ -940,8 +946,8 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
             un = nd << (g.log2p - kSegLog2);
         }
         uint64_t tn, tun;
-        const uint64_t en = block_excl_scan(nd, &tn);
-        const uint64_t eun = block_excl_scan(un, &tun);
+        const uint64_t en = warp_excl_scan(nd, &tn);
+        const uint64_t eun = warp_excl_scan(un, &tun);
         if (r < a.R) {
             RegStat s;
             s.first = carry_first + en;
@@ -963,8 +969,8 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
         carry_units += tun;
     }
     const uint64_t poff = a.poff;
-    for (uint64_t b = 64 + 48ull * a.R + threadIdx.x; b < poff; b += blockDim.x) a.img[b] = 0;
-    if (threadIdx.x == 0) {
+    for (uint64_t b = 64 + 48ull * a.R + lane; b < poff; b += 32) a.img[b] = 0;
+    if (lane == 0) {
         DevStats *st = a.st;
         const uint64_t payload = U << kSegLog2;
         const uint64_t ids_off = poff + payload;
