@@ -1051,7 +1051,10 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     int st;
     uint64_t worst = 0;
     crum_image_required_bytes(c, UINT64_MAX, &worst);
-    if (c->fused_ok && !full && capacity >= worst && !getenv("CRUM_NO_FUSED")) {
+    // The single-pass kernel is opt-in (CRUM_FUSED=1): measured on B200 it ties
+    // the multi-kernel path on C2 and trails it by ~2% on C3.
+    static const bool fused_env = getenv("CRUM_FUSED") != nullptr;
+    if (c->fused_ok && fused_env && !full && capacity >= worst) {
         // single pass: detect + compact + gather + commit in one kernel, then
         // the metadata CRC / tail / header
         if (timing) CK(cudaEventRecord(c->ev_t[0], s));
