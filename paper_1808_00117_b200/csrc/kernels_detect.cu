@@ -148,16 +148,21 @@ constexpr uint64_t kMx1 = 0x165667919E3779F9ull;
 
 // Per-lane constants: lane p (= lane & 3) owns accumulator lanes 2p, 2p+1.
 struct LaneKeys {
-    uint64_t sw[17];           // stripe keys: word (s + 2p), s = 0..16
+    const uint64_t *sw;        // stripe keys in shared memory: sw[s] = word (s + 2p), s = 0..16
     uint64_t last0, last1;     // last-stripe keys for lanes 2p, 2p+1
     uint64_t scr0, scr1;       // scramble keys
     uint64_t mrg0, mrg1;       // merge keys
     uint64_t init0, init1;     // initial accumulators
 };
 
-__device__ __forceinline__ void load_lane_keys(LaneKeys &k, uint32_t p) {
-#pragma unroll
-    for (int j = 0; j < 17; ++j) k.sw[j] = c_xxh.w[2 * p + j];
+// The 24 secret words are staged in shared memory (keeps ~34 registers per
+// thread free for loads in flight); call with all threads, then sync.
+__device__ __forceinline__ void stage_secret(uint64_t *s_w) {
+    if (threadIdx.x < 24) s_w[threadIdx.x] = c_xxh.w[threadIdx.x];
+}
+
+__device__ __forceinline__ void load_lane_keys(LaneKeys &k, uint32_t p, const uint64_t *s_w) {
+    k.sw = s_w + 2 * p;
     k.last0 = c_xxh.last[2 * p];
     k.last1 = c_xxh.last[2 * p + 1];
     k.scr0 = c_xxh.w[16 + 2 * p];
@@ -249,13 +254,16 @@ __device__ __forceinline__ uint64_t xxh3_slot(const uint8_t *__restrict__ pg, ui
 // ---------------------------------------------------------------------------
 // HASH detect: warp per page group (1 page, or 2 pages when P = 4 KiB).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_detect_hash(
+__global__ void __launch_bounds__(256, 2) k_detect_hash(
     const DevRegion *__restrict__ regs, const uint32_t *__restrict__ hash_idx,
     const uint64_t *__restrict__ hash_grp, uint32_t n_hash, uint64_t w_lo, uint64_t w_hi,
     uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash, uint8_t tag) {
     const uint32_t lane = threadIdx.x & 31;
+    __shared__ uint64_t s_w[24];
+    stage_secret(s_w);
+    __syncthreads();
     LaneKeys k;
-    load_lane_keys(k, lane & 3);
+    load_lane_keys(k, lane & 3, s_w);
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
     uint64_t r_lo = 1, r_hi = 0;
@@ -421,8 +429,11 @@ __global__ void __launch_bounds__(256) k_verify_hash(const DevRegion *__restrict
                                                      const uint8_t *__restrict__ payload, uint64_t K,
                                                      DevStats *st) {
     const uint32_t lane = threadIdx.x & 31;
+    __shared__ uint64_t s_w[24];
+    stage_secret(s_w);
+    __syncthreads();
     LaneKeys k;
-    load_lane_keys(k, lane & 3);
+    load_lane_keys(k, lane & 3, s_w);
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
     for (uint64_t s = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); s < K; s += nwarps) {
