@@ -807,7 +807,7 @@ __device__ __forceinline__ uint64_t warp_excl_scan(uint64_t v, uint64_t *total) 
 
 // Each WARP owns one tile at a time: no block barriers, so while one warp
 // waits in its look-back the SM's other warps keep streaming.
-__global__ void __launch_bounds__(kFusedThreads, 8) k_fused_compare(FusedArgs a) {
+__global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
     const uint32_t lane = threadIdx.x & 31;
     bool last = false;
     for (;;) {
