@@ -111,7 +111,6 @@ struct HostRegion {
 // and hash-group ranges of the detect kernels.
 struct Range {
     uint64_t p_lo, p_hi, s_lo, s_hi, w_lo, w_hi, v_lo, v_hi;
-    uint64_t units;  // 4 KiB units of all pages in the range (gather grid bound)
 };
 
 constexpr uint64_t kDefaultChunk = 64ull << 20;
@@ -134,8 +133,7 @@ struct crum_ctx {
     int sms = 148;
     uint64_t chunk = kDefaultChunk;
     std::vector<HostRegion> regs;
-    std::vector<Range> ranges;   // host-image pipeline
-    std::vector<Range> dranges;  // device-image pipeline
+    std::vector<Range> ranges;
     Range all{};
     uint32_t next_id = 1;
     uint64_t N = 0, F = 0, max_units = 0;
@@ -308,13 +306,8 @@ uint64_t big_at(const crum_ctx *c, uint64_t p) {
 }
 
 Range make_range(const crum_ctx *c, uint64_t lo, uint64_t hi) {
-    uint64_t units = 0;
-    for (const HostRegion &h : c->regs) {
-        const uint64_t a = std::max(lo, h.page_base), b = std::min(hi, h.page_base + h.n_pages);
-        if (b > a) units += (b - a) << (h.log2p - kSegLog2);
-    }
     return Range{lo, hi, seg_at(c, lo), seg_at(c, hi), grp_at(c, lo, false), grp_at(c, hi, true), big_at(c, lo),
-                 big_at(c, hi), units};
+                 big_at(c, hi)};
 }
 
 // Rebuild device descriptors and per-page arrays after the registry changed.
@@ -490,27 +483,6 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
         }
     }
     c->ranges.push_back(make_range(c, lo, N));
-    // device-image pipeline: ~F/8 per range (>= 64 MiB), at most 8 ranges
-    c->dranges.clear();
-    {
-        const uint64_t dt = std::max<uint64_t>(64ull << 20, F / 8);
-        uint64_t dlo = 0, dacc = 0;
-        for (uint32_t r = 0; r < R; ++r) {
-            const HostRegion &h = c->regs[r];
-            for (uint64_t i = 0; i < h.n_pages; ++i) {
-                const uint64_t g = h.page_base + i;
-                if (dacc >= dt && g % 16 == 0 && c->dranges.size() < 7) {
-                    c->dranges.push_back(make_range(c, dlo, g));
-                    dlo = g;
-                    dacc = 0;
-                }
-                const uint64_t step = std::min<uint64_t>(h.n_pages - i, 16 - (g % 16));
-                dacc += step * h.page_size;
-                i += step - 1;
-            }
-        }
-        c->dranges.push_back(make_range(c, dlo, N));
-    }
     return CRUM_OK;
 }
 
@@ -647,10 +619,7 @@ void fill_report(crum_ctx *c, const DevStats &h, crum_report *rep) {
     rep->image_bytes = h.image_bytes;
 }
 
-enum {
-    kLastNone = 0, kLastSync = 1, kLastDevGather = 2, kLastHostGather = 3, kLastRestore = 4, kLastDevFused = 5,
-    kLastDevPipe = 6
-};
+enum { kLastNone = 0, kLastSync = 1, kLastDevGather = 2, kLastHostGather = 3, kLastRestore = 4, kLastDevFused = 5 };
 
 // Phase times of the most recent call from its events (see each call for
 // which events delimit which phase).
@@ -661,11 +630,6 @@ void fill_times(crum_ctx *c, crum_report *rep) {
             rep->t_detect_ms = ev_ms(e[0], e[1]);
             rep->t_compact_ms = ev_ms(e[1], e[2]);
             rep->t_gather_ms = ev_ms(e[2], e[4]);
-            rep->t_total_ms = ev_ms(e[0], e[4]);
-            break;
-        case kLastDevPipe:
-            rep->t_detect_ms = ev_ms(e[0], e[1]);   // all ranges' detect (gathers of earlier ranges overlap)
-            rep->t_gather_ms = ev_ms(e[1], e[4]);   // compaction + gather + CRC tail after the last detect
             rep->t_total_ms = ev_ms(e[0], e[4]);
             break;
         case kLastDevFused:
@@ -1121,53 +1085,6 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
         if (timing) CK(cudaEventRecord(c->ev_t[4], s));
         CK(cudaEventRecord(c->ev_done, s));
         c->last_kind = kLastDevFused;
-        c->last_timed = timing;
-        if (rep) {
-            CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            memset(rep, 0, sizeof *rep);
-            fill_report(c, *c->h_st, rep);
-            fill_times(c, rep);
-        }
-        return CRUM_OK;
-    }
-    if (capacity >= worst && c->dranges.size() > 1 && !getenv("CRUM_NO_DPIPE")) {
-        // Range pipeline: detect of every range back to back on the caller's
-        // stream; compaction + gather of range c on the high-priority side
-        // stream as soon as its detect is done (commits before the final
-        // capacity check are safe: capacity >= worst case).
-        const uint32_t nr = (uint32_t)c->dranges.size();
-        if (timing) CK(cudaEventRecord(c->ev_t[0], s));
-        if ((st = next_tag(c, s))) return st;
-        CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
-        for (uint32_t ci = 0; ci < nr; ++ci) {
-            enqueue_detect(c, s, c->dranges[ci], full);
-            CK(cudaEventRecord(c->ev_range[ci], s));
-        }
-        if (timing) CK(cudaEventRecord(c->ev_t[1], s));
-        Launch G = launch_of(c, c->gstream);
-        for (uint32_t ci = 0; ci < nr; ++ci) {
-            CK(cudaStreamWaitEvent(c->gstream, c->ev_range[ci], 0));
-            CompactArgs ca = compact_args(c, c->dranges[ci], ci, ci == 0, ci + 1 == nr, full, capacity, img);
-            ca.rb_host = nullptr;
-            enqueue_compact(c, c->gstream, ca);
-            if (ci + 1 == nr) {
-                CK(cudaEventRecord(c->ev_fork, c->gstream));
-                CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-                CrcArgs cr = crc_args(c, img, nullptr);
-                cr.st_host = nullptr;
-                launch_crc_meta(launch_of(c, c->aux), cr, crc_max_len(c));
-                CK(cudaEventRecord(c->ev_join, c->aux));
-            }
-            launch_gather(G, gather_args(c, ci, img, 0, true, 0, UINT64_MAX), c->dranges[ci].units);
-        }
-        CK_LAUNCH();
-        CK(cudaEventRecord(c->ev_meta, c->gstream));
-        CK(cudaStreamWaitEvent(s, c->ev_meta, 0));
-        CK(cudaStreamWaitEvent(s, c->ev_join, 0));
-        if (timing) CK(cudaEventRecord(c->ev_t[4], s));
-        CK(cudaEventRecord(c->ev_done, s));
-        c->last_kind = kLastDevPipe;
         c->last_timed = timing;
         if (rep) {
             CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
