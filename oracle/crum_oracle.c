@@ -39,7 +39,7 @@ enum {
     ORC_E_MISMATCH = -8,
 };
 
-enum { ORC_MODE_COMPARE = 0, ORC_MODE_HASH = 1 };
+enum { ORC_MODE_COMPARE = 0, ORC_MODE_HASH = 1, ORC_MODE_TRACKED = 2 };
 enum { ORC_FULL = 1u, ORC_VERIFY = 2u };
 enum { ORC_IMG_FULL = 1u, ORC_IMG_HAS_HASHES = 2u };
 
@@ -270,7 +270,7 @@ int orc_register_region(orc_ctx *c, uint8_t *ptr, uint64_t bytes, uint64_t page_
     if (page_size < ORC_MIN_PAGE || page_size > ORC_MAX_PAGE || (page_size & (page_size - 1)))
         return ORC_E_INVAL;
     if (((uintptr_t)ptr) % 16 != 0) return ORC_E_INVAL;
-    if (mode != ORC_MODE_COMPARE && mode != ORC_MODE_HASH) return ORC_E_INVAL;
+    if (mode != ORC_MODE_COMPARE && mode != ORC_MODE_HASH && mode != ORC_MODE_TRACKED) return ORC_E_INVAL;
     uint64_t n = bytes / page_size + (bytes % page_size != 0);
     if (n > 0xffffffffull) return ORC_E_INVAL;
     if (total_pages(c) + n > ORC_MAX_TOTAL_PAGES) return ORC_E_INVAL;
@@ -288,9 +288,9 @@ int orc_register_region(orc_ctx *c, uint8_t *ptr, uint64_t bytes, uint64_t page_
     g.n_pages = n;
     g.force = (uint8_t *)malloc(n);
     if (mode == ORC_MODE_COMPARE) g.mirror = (uint8_t *)calloc(1, bytes);
-    else g.table = (uint64_t *)calloc(n, sizeof(uint64_t));
+    else if (mode == ORC_MODE_HASH) g.table = (uint64_t *)calloc(n, sizeof(uint64_t));
     orc_region *nr = (orc_region *)realloc(c->r, (c->n + 1) * sizeof(orc_region));
-    if (!g.force || (!g.mirror && !g.table) || !nr) {
+    if (!g.force || (mode != ORC_MODE_TRACKED && !g.mirror && !g.table) || !nr) {
         free_region(&g);
         if (nr) c->r = nr;
         return ORC_E_NOMEM;
@@ -329,12 +329,27 @@ int orc_mark_dirty(orc_ctx *c, uint32_t id, uint64_t off, uint64_t len)
     return ORC_OK;
 }
 
+/* Batch form of MarkPageAsDirty: force bits of the listed page indices. */
+int orc_mark_pages(orc_ctx *c, uint32_t id, const uint32_t *pages, uint64_t n)
+{
+    if (!c || (!pages && n)) return ORC_E_INVAL;
+    orc_region *g = find(c, id);
+    if (!g) return ORC_E_NOREGION;
+    for (uint64_t k = 0; k < n; ++k)
+        if (pages[k] >= g->n_pages) return ORC_E_RANGE;
+    for (uint64_t k = 0; k < n; ++k) g->force[pages[k]] = 1;
+    return ORC_OK;
+}
+
 /* Detect (pure): D_r = { i : force[i] or content changed since commit }.
  * Reading Q1: "dirty" = bytes differ from the last committed snapshot
- * (compare: memcmp over the logical length; hash: H(r,i) != table[i]). */
+ * (compare: memcmp over the logical length; hash: H(r,i) != table[i]).
+ * TRACKED mode is the paper's own write-based rule (Alg. 1 MarkPageAsDirty,
+ * PAPER.md:412): a page is dirty iff it was marked since its last commit. */
 static int page_dirty(const orc_region *g, uint64_t i)
 {
     if (g->force[i]) return 1;
+    if (g->mode == ORC_MODE_TRACKED) return 0;
     if (g->mode == ORC_MODE_COMPARE) {
         uint64_t off = i * g->page_size;
         return memcmp(g->cur + off, g->mirror + off, page_len(g, i)) != 0;
@@ -357,7 +372,7 @@ static void commit_page(orc_region *g, uint64_t i)
     if (g->mode == ORC_MODE_COMPARE) {
         uint64_t off = i * g->page_size;
         memcpy(g->mirror + off, g->cur + off, page_len(g, i));
-    } else {
+    } else if (g->mode == ORC_MODE_HASH) {
         g->table[i] = page_hash(g, i);
     }
     g->force[i] = 0;
@@ -550,7 +565,7 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
         uint32_t mode = rd32(e + 4);
         uint64_t bytes = rd64(e + 8), ps = rd64(e + 16), np = rd64(e + 24), nd = rd64(e + 32),
                  first = rd64(e + 40);
-        if (mode > 1 || ps < ORC_MIN_PAGE || ps > ORC_MAX_PAGE || (ps & (ps - 1)) || bytes == 0)
+        if (mode > 2 || ps < ORC_MIN_PAGE || ps > ORC_MAX_PAGE || (ps & (ps - 1)) || bytes == 0)
             return ORC_E_CORRUPT;
         if (np != bytes / ps + (bytes % ps != 0) || nd > np || first != sum) return ORC_E_CORRUPT;
         if ((iflags & ORC_IMG_FULL) && nd != np) return ORC_E_CORRUPT;
@@ -560,7 +575,7 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
             uint32_t id = rd32(ids + 4 * (first + j));
             if (id >= np) return ORC_E_CORRUPT;
             if (j > 0 && id <= rd32(ids + 4 * (first + j - 1))) return ORC_E_CORRUPT;
-            if (has_hashes && mode == ORC_MODE_COMPARE && rd64(hashes + 8 * (first + j)) != 0)
+            if (has_hashes && mode != ORC_MODE_HASH && rd64(hashes + 8 * (first + j)) != 0)
                 return ORC_E_CORRUPT;
         }
         sum += nd;
@@ -601,7 +616,7 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
             uint64_t l = page_len(g, i);
             memcpy(g->cur + i * g->page_size, img + poff + pbyte, l);
             if (g->mode == ORC_MODE_COMPARE) memcpy(g->mirror + i * g->page_size, img + poff + pbyte, l);
-            else g->table[i] = rd64(hashes + 8 * (first + j));
+            else if (g->mode == ORC_MODE_HASH) g->table[i] = rd64(hashes + 8 * (first + j));
             g->force[i] = 0;
             dirty_bytes += l;
             if (j == 0 || rd32(ids + 4 * (first + j - 1)) + 1 != i) runs++;

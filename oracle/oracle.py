@@ -25,7 +25,7 @@ _lib = None
 
 OK, E_INVAL, E_OVERLAP, E_NOREGION, E_RANGE, E_NOMEM, E_CAPACITY, E_CORRUPT, E_MISMATCH = (
     0, -1, -2, -3, -4, -5, -6, -7, -8)
-MODE_COMPARE, MODE_HASH = 0, 1
+MODE_COMPARE, MODE_HASH, MODE_TRACKED = 0, 1, 2
 FULL, VERIFY = 1, 2
 
 
@@ -64,6 +64,7 @@ def lib():
         L.orc_register_region.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, u32p]
         L.orc_unregister_region.argtypes = [C.c_void_p, C.c_uint32]
         L.orc_mark_dirty.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint64]
+        L.orc_mark_pages.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]
         L.orc_detect.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
         L.orc_sync_shadow.argtypes = [C.c_void_p, u64p]
         L.orc_image_required_bytes.argtypes = [C.c_void_p, C.c_uint64, u64p]
@@ -77,7 +78,7 @@ def lib():
         L.orc_get_hashes.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
         L.orc_get_mirror.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
         L.orc_page_hash.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, u64p]
-        for f in ("orc_register_region", "orc_unregister_region", "orc_mark_dirty", "orc_detect",
+        for f in ("orc_register_region", "orc_unregister_region", "orc_mark_dirty", "orc_mark_pages", "orc_detect",
                   "orc_sync_shadow", "orc_image_required_bytes", "orc_checkpoint_gather",
                   "orc_restore_scatter", "orc_get_force", "orc_get_hashes", "orc_get_mirror",
                   "orc_page_hash"):
@@ -151,6 +152,10 @@ class Oracle:
 
     def mark_dirty(self, rid: int, off: int, length: int) -> int:
         return self._L.orc_mark_dirty(self._h, rid, off, length)
+
+    def mark_pages(self, rid: int, pages) -> int:
+        a = np.ascontiguousarray(np.asarray(pages, dtype=np.uint32))
+        return self._L.orc_mark_pages(self._h, rid, a.ctypes.data if a.size else None, a.size)
 
     def n_pages(self, rid: int) -> int:
         _, b, p, _ = self._regions[rid]

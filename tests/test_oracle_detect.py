@@ -169,3 +169,24 @@ def test_region_ids_monotonic_never_reused(oracle_mod):
     assert (r1, r2) == (1, 2)
     o.unregister(r1)
     assert o.register(a, 4096) == 3
+
+
+def test_tracked_mode_dirty_is_exactly_the_marked_set(oracle_mod):
+    """CRUM_MODE_TRACKED follows Alg. 1's write rule:
+    a page is dirty iff marked since its last commit -- content changes that
+    were not marked are NOT listed, marked pages are listed even if unchanged."""
+    o = oracle_mod.Oracle()
+    P = 4096
+    mem = oracle_mod.aligned_empty(10 * P + 100)
+    synth.fill_region(mem, synth.seed(3), 0)
+    rid = o.register(mem, P, oracle_mod.MODE_TRACKED)
+    assert o.detect(rid).tolist() == [1] * 11            # all pages start dirty (PAPER.md:436-437)
+    assert o.sync_shadow() == 11 and o.sync_shadow() == 0
+    mem[3 * P + 5] ^= 0xFF                                 # unmarked change: not dirty
+    assert o.detect(rid).sum() == 0
+    assert o.mark_pages(rid, [1, 7, 10]) == 0              # marked (7 and 10 unchanged, 10 partial)
+    assert np.flatnonzero(o.detect(rid)).tolist() == [1, 7, 10]
+    assert o.mark_pages(rid, [11]) == oracle_mod.E_RANGE
+    assert o.mark_pages(999, [0]) == oracle_mod.E_NOREGION
+    assert o.sync_shadow() == 3 and o.detect(rid).sum() == 0
+    assert o.try_register(mem.ctypes.data, 4096, 4096, mode=3) == oracle_mod.E_INVAL

@@ -198,3 +198,30 @@ def test_deterministic_image(oracle_mod):
         dirty_epoch(mems, SPECS, S, 1, 0.5)
         imgs.append(o.checkpoint_gather()[1].tobytes())
     assert imgs[0] == imgs[1]
+
+
+def test_tracked_mode_image_and_restore(oracle_mod):
+    """Images of TRACKED regions list the marked pages with the bytes they hold
+    at gather time; hash entries are 0; restore replays them."""
+    S = synth.seed(11)
+    specs = [(6 * 4096 + 10, 4096, 2), (2 * 65536, 65536, 1), (3 * 4096, 4096, 0)]
+    o, mems, rids = make_ctx(oracle_mod, specs, S)
+    st, img0, _ = o.checkpoint_gather()
+    regions = [dict(id=rid, mode=md, cur=m, page_size=P) for rid, m, (_, P, md) in zip(rids, mems, specs)]
+    mems[0][2 * 4096] ^= 1
+    mems[0][5 * 4096 + 3] ^= 1
+    o.mark_pages(rids[0], [2, 6])                          # page 5 changed but unmarked; 6 marked, unchanged
+    mems[2][4096] ^= 1                                      # compare region: found by content
+    st, img, rep = o.checkpoint_gather()
+    assert bytes(img) == imgfmt.build_image(regions, [[2, 6], [], [1]])
+    z = [oracle_mod.aligned_empty(nb) for nb, _, _ in specs]
+    o2 = oracle_mod.Oracle()
+    for zz, (nb, P, md) in zip(z, specs):
+        zz[:] = 0
+        o2.register(zz, P, md)
+    assert o2.restore_scatter(img0)[0] == 0 and o2.restore_scatter(img)[0] == 0
+    want0 = mems[0].copy()
+    assert np.array_equal(z[1], mems[1]) and np.array_equal(z[2], mems[2])
+    # page 5's unmarked change is (by definition) not in the images
+    assert not np.array_equal(z[0], want0)
+    assert np.array_equal(z[0][:5 * 4096], want0[:5 * 4096]) and np.array_equal(z[0][6 * 4096:], want0[6 * 4096:])
