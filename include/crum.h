@@ -72,7 +72,12 @@ enum crum_status {
 /* Per-region dirty-detection mode (reading Q1/Q8). */
 typedef enum {
     CRUM_MODE_COMPARE = 0,   /* device byte mirror of the region, per-page compare */
-    CRUM_MODE_HASH_XXH3 = 1  /* 8 B per page: XXH3-64 (seed 0) of the zero-padded page slot */
+    CRUM_MODE_HASH_XXH3 = 1, /* 8 B per page: XXH3-64 (seed 0) of the zero-padded page slot */
+    CRUM_MODE_TRACKED = 2    /* no shadow: a page is dirty iff it was marked since its last commit
+                                (Alg. 1 MarkPageAsDirty on writes) -- by
+                                crum_mark_dirty[_pages] or, inside application kernels, by
+                                crum_mark_write() of include/crum_device.h.  Unmarked writes are
+                                not captured. */
 } crum_mode;
 
 /* Call flags. */
@@ -153,6 +158,26 @@ CRUM_API int crum_unregister_region(crum_ctx *ctx, uint32_t region_id);
  * bit of every page overlapping [offset, offset+len).  len == 0 is a no-op.
  * Errors: NOREGION, RANGE (offset+len > bytes). */
 CRUM_API int crum_mark_dirty(crum_ctx *ctx, uint32_t region_id, uint64_t offset, uint64_t len);
+
+/* Stream-ordered batch marking: sets the force bit of page dev_pages[k]
+ * (region-local page indices, a DEVICE array of n u32) for k < n, after all
+ * prior work on `stream`.  Indices >= the region's page count are ignored.
+ * Errors: NOREGION, INVAL (dev_pages NULL with n > 0), CUDA. */
+CRUM_API int crum_mark_dirty_pages(crum_ctx *ctx, uint32_t region_id, const uint32_t *dev_pages, uint64_t n,
+                                   void *stream);
+
+/* Device-side marking handle of one region: application kernels call
+ * crum_mark_write(tracker, offset, len) (include/crum_device.h) after writing
+ * [offset, offset+len) of the region.  `force` points at the region's force
+ * bits in device memory; it is invalidated by the next register/unregister on
+ * the context (call crum_region_tracker again). */
+typedef struct {
+    uint8_t *force;     /* device pointer: one byte per page */
+    uint64_t bytes;     /* region bytes */
+    uint32_t log2_page; /* log2(page_size) */
+    uint32_t reserved;
+} crum_tracker;
+CRUM_API int crum_region_tracker(crum_ctx *ctx, uint32_t region_id, crum_tracker *out);
 
 /* ---------------------------------------------------------------------------
  * Alg. 1 "CUDA call" event: detect the dirty pages of every

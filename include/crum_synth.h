@@ -35,6 +35,15 @@ CRUM_API int crum_synth_write_pages(void *dev_ptr, uint64_t bytes, uint64_t page
                            const uint32_t *dev_pages, uint64_t n_pages, uint64_t seed,
                            uint64_t epoch, uint64_t region_index, int touch, void *stream);
 
+/* Same writer for a CRUM_MODE_TRACKED region: each written page is also marked
+ * through `tracker` (crum_region_tracker) with crum_mark_write() of
+ * include/crum_device.h, inside the writer kernel -- the way an application
+ * kernel marks what it writes. */
+CRUM_API int crum_synth_write_pages_tracked(void *dev_ptr, uint64_t bytes, uint64_t page_size,
+                                           const uint32_t *dev_pages, uint64_t n_pages, uint64_t seed,
+                                           uint64_t epoch, uint64_t region_index, int touch,
+                                           const void *tracker /* const crum_tracker* */, void *stream);
+
 /* Streaming write of `bytes` to scrub L2 between timed repetitions. */
 CRUM_API int crum_synth_scrub(void *dev_ptr, uint64_t bytes, void *stream);
 

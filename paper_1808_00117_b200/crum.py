@@ -29,6 +29,7 @@ E_INVAL, E_OVERLAP, E_NOREGION, E_RANGE, E_NOMEM = -1, -2, -3, -4, -5
 E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY, E_DEVICE, E_CUDA = -6, -7, -8, -9, -10, -11
 MODE_COMPARE, MODE_HASH = 0, 1
 FULL, VERIFY = 1, 2
+MODE_TRACKED = 2
 CFG_TIMING = 1
 PATH_FUSED = 1
 EXPORT_FORCE, EXPORT_HASHES, EXPORT_MIRROR = 0, 1, 2
@@ -42,8 +43,14 @@ EXPORTED = (
     "crum_restore_scatter", "crum_restore_scatter_device", "crum_status_string", "crum_last_error_detail",
     "crum_debug_detect", "crum_debug_export", "crum_launch_count", "crum_last_report",
     "crum_synth_fill", "crum_synth_write_pages", "crum_synth_scrub", "crum_probe_copy",
-    "crum_synth_alloc_managed", "crum_synth_free_managed",
+    "crum_synth_alloc_managed", "crum_synth_free_managed", "crum_synth_write_pages_tracked",
+    "crum_mark_dirty_pages", "crum_region_tracker",
 )
+
+
+class Tracker(C.Structure):
+    """crum_tracker: device-side marking handle of a TRACKED region."""
+    _fields_ = [("force", C.c_void_p), ("bytes", C.c_uint64), ("log2_page", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class Config(C.Structure):
@@ -90,6 +97,10 @@ _sig = {
     "crum_probe_copy": (_i, [_vp, _vp, _u64, _i, _vp]),
     "crum_synth_alloc_managed": (_i, [C.POINTER(_vp), _u64, _i, _u64]),
     "crum_synth_free_managed": (_i, [_vp]),
+    "crum_synth_write_pages_tracked": (_i, [_vp, _u64, _u64, _vp, _u64, _u64, _u64, _u64, _i, C.POINTER(Tracker),
+                                           _vp]),
+    "crum_mark_dirty_pages": (_i, [_vp, _u32, _vp, _u64, _vp]),
+    "crum_region_tracker": (_i, [_vp, _u32, C.POINTER(Tracker)]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_L, _name)
@@ -234,6 +245,16 @@ class Context:
     def mark_dirty(self, rid: int, offset: int, length: int) -> int:
         return _L.crum_mark_dirty(self._h, rid, offset, length)
 
+    def mark_dirty_pages(self, rid: int, dev_pages, n: int, stream=None) -> int:
+        """Stream-ordered: force bits of the region-local page indices in the
+        device u32 array dev_pages[0..n)."""
+        return _L.crum_mark_dirty_pages(self._h, rid, _addr(dev_pages) if n else None, n, _stream(stream))
+
+    def region_tracker(self, rid: int) -> Tracker:
+        t = Tracker()
+        _check(_L.crum_region_tracker(self._h, rid, C.byref(t)), "crum_region_tracker")
+        return t
+
     # -- Alg. 1 "CUDA call" (PAPER.md:417-422)
     def sync_shadow(self, stream=None, wait: bool = True):
         n = _u64()
@@ -324,6 +345,13 @@ def synth_write_pages(dev_ptr, nbytes: int, page_size: int, dev_pages, n_pages: 
     _check(_L.crum_synth_write_pages(_addr(dev_ptr), nbytes, page_size, _addr(dev_pages) if n_pages else None,
                                      n_pages, seed, epoch, region_index, int(touch), _stream(stream)),
            "crum_synth_write_pages")
+
+
+def synth_write_pages_tracked(dev_ptr, nbytes: int, page_size: int, dev_pages, n_pages: int, seed: int, epoch: int,
+                              region_index: int, tracker: Tracker, touch: bool = False, stream=None):
+    _check(_L.crum_synth_write_pages_tracked(_addr(dev_ptr), nbytes, page_size, _addr(dev_pages) if n_pages else None,
+                                             n_pages, seed, epoch, region_index, int(touch), C.byref(tracker),
+                                             _stream(stream)), "crum_synth_write_pages_tracked")
 
 
 def synth_scrub(dev_ptr, nbytes: int, stream=None):

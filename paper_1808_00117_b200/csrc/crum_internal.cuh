@@ -20,6 +20,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../../include/crum.h"
+
 namespace crum {
 
 constexpr uint32_t kSegLog2 = 12;              // 4 KiB work segment (min page size)
@@ -28,7 +30,7 @@ constexpr uint32_t kPagesPerThread = 16;       // compaction: one uint4 of flags
 constexpr uint32_t kCompactThreads = 256;
 constexpr uint32_t kPagesPerCompactBlock = kPagesPerThread * kCompactThreads;  // 4096
 
-enum : uint32_t { kModeCompare = 0, kModeHash = 1 };
+enum : uint32_t { kModeCompare = 0, kModeHash = 1, kModeTracked = 2 };
 enum : uint32_t { kStOk = 0, kStCapacity = 6, kStCorrupt = 7 };
 
 struct DevRegion {
@@ -218,6 +220,7 @@ void launch_crc_check(const Launch &L, const uint8_t *table, uint64_t tab, const
 void launch_restore_validate(const Launch &L, const DevRegion *tregs, uint32_t R, const RegStat *rs,
                              const uint32_t *ids, const uint64_t *hashes, uint64_t K, DevStats *st);
 void launch_scatter(const Launch &L, const ScatterArgs &a);
+void launch_mark_pages(const Launch &L, uint8_t *force, uint64_t n_pages, const uint32_t *pages, uint64_t n);
 void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag,
                          uint8_t *out);
 
@@ -226,7 +229,7 @@ void launch_synth_fill(cudaStream_t s, uint8_t *p, uint64_t bytes, uint64_t seed
                        uint64_t word_offset);
 void launch_synth_write(cudaStream_t s, uint8_t *p, uint64_t bytes, uint64_t page_size,
                         const uint32_t *pages, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t r,
-                        int touch);
+                        int touch, const crum_tracker *t);
 void launch_synth_scrub(cudaStream_t s, uint8_t *p, uint64_t bytes);
 
 // ---- small device helpers shared by the kernel files ----

@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(256) k_restore_validate(const DevRegion *__res
         const bool first = (k == rs[r].first);
         if (i >= g.n_pages) bad = 1;
         if (!first && ids[k - 1] >= i) bad = 1;
-        if (hashes && g.mode == kModeCompare && hashes[k] != 0) bad = 1;
+        if (hashes && g.mode != kModeHash && hashes[k] != 0) bad = 1;
         if (i < g.n_pages) dbytes += page_len(g, i);
         runs += (first || ids[k - 1] + 1 != i) ? 1 : 0;
     }
@@ -736,6 +736,22 @@ void launch_scatter(const Launch &L, const ScatterArgs &a) {
 // ---------------------------------------------------------------------------
 // debug: (flags == tag) | force, global page order
 // ---------------------------------------------------------------------------
+// crum_mark_dirty_pages: force[pages[k]] = 1 for in-range indices.
+__global__ void k_mark_pages(uint8_t *force, uint64_t n_pages, const uint32_t *pages, uint64_t n) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = pages[k];
+        if (i < n_pages) force[i] = 1;
+    }
+}
+
+void launch_mark_pages(const Launch &L, uint8_t *force, uint64_t n_pages, const uint32_t *pages, uint64_t n) {
+    if (!n) return;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > (uint64_t)L.sms * 8) blocks = L.sms * 8;
+    k_mark_pages<<<(unsigned)blocks, 256, 0, L.stream>>>(force, n_pages, pages, n);
+    ++*L.counter;
+}
+
 __global__ void k_export_flags(const uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag, uint8_t *out) {
     for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < N;
          g += (uint64_t)gridDim.x * blockDim.x)

@@ -337,7 +337,7 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
         if (h.mode == kModeCompare) {
             cmp_idx.push_back(r);
             cmp_seg.push_back(cmp_seg.back() + (h.bytes + kSegBytes - 1) / kSegBytes);
-        } else {
+        } else if (h.mode == kModeHash) {
             any_hash = true;
             if (h.log2p >= kBigHashLog2) {
                 big_idx.push_back(r);
@@ -835,7 +835,7 @@ int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page
         set_detail("ptr not 16-byte aligned");
         return CRUM_E_INVAL;
     }
-    if (mode != CRUM_MODE_COMPARE && mode != CRUM_MODE_HASH_XXH3) {
+    if (mode != CRUM_MODE_COMPARE && mode != CRUM_MODE_HASH_XXH3 && mode != CRUM_MODE_TRACKED) {
         set_detail("bad mode %u", mode);
         return CRUM_E_INVAL;
     }
@@ -880,10 +880,14 @@ int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page
     h.page_size = page_size;
     h.n_pages = n;
     h.log2p = (uint32_t)__builtin_ctzll(page_size);
-    const uint64_t shadow_bytes = mode == kModeCompare ? round_up(bytes, 256) : 8 * n;
-    int st = dev_alloc(c, &h.shadow, shadow_bytes);
-    if (st) return st;
-    CK(cudaMemset(h.shadow, 0, shadow_bytes));
+    // shadow: compare -> byte mirror, hash -> u64 table, tracked -> none
+    const uint64_t shadow_bytes = mode == kModeCompare ? round_up(bytes, 256) : mode == kModeHash ? 8 * n : 0;
+    int st = CRUM_OK;
+    h.shadow = nullptr;
+    if (shadow_bytes) {
+        if ((st = dev_alloc(c, &h.shadow, shadow_bytes))) return st;
+        CK(cudaMemset(h.shadow, 0, shadow_bytes));
+    }
     std::vector<uint64_t> old_base;
     for (const HostRegion &o : c->regs) old_base.push_back(o.page_base);
     old_base.push_back(UINT64_MAX);
@@ -938,6 +942,39 @@ int crum_mark_dirty(crum_ctx *ctx, uint32_t id, uint64_t off, uint64_t len) {
     CK(cudaDeviceSynchronize());
     CK(cudaMemset(c->d_force + h->page_base + i0, 1, i1 - i0 + 1));
     CK(cudaDeviceSynchronize());
+    return CRUM_OK;
+}
+
+int crum_mark_dirty_pages(crum_ctx *ctx, uint32_t id, const uint32_t *dev_pages, uint64_t n, void *stream) {
+    ENTER(ctx);
+    HostRegion *h = find_region(c, id);
+    if (!h) {
+        set_detail("no region %u", id);
+        return CRUM_E_NOREGION;
+    }
+    if (!n) return CRUM_OK;
+    if (!dev_pages) {
+        set_detail("null page list");
+        return CRUM_E_INVAL;
+    }
+    launch_mark_pages(launch_of(c, static_cast<cudaStream_t>(stream)), c->d_force + h->page_base, h->n_pages,
+                      dev_pages, n);
+    CK_LAUNCH();
+    return CRUM_OK;
+}
+
+int crum_region_tracker(crum_ctx *ctx, uint32_t id, crum_tracker *out) {
+    ENTER(ctx);
+    HostRegion *h = find_region(c, id);
+    if (!h) {
+        set_detail("no region %u", id);
+        return CRUM_E_NOREGION;
+    }
+    if (!out) return CRUM_E_INVAL;
+    out->force = c->d_force + h->page_base;
+    out->bytes = h->bytes;
+    out->log2_page = h->log2p;
+    out->reserved = 0;
     return CRUM_OK;
 }
 
@@ -1309,7 +1346,7 @@ int parse_table(const uint8_t *tab, ParsedImage &p) {
         const uint32_t mode = rd32(e + 4);
         const uint64_t bytes = rd64(e + 8), ps = rd64(e + 16), np = rd64(e + 24), nd = rd64(e + 32),
                        first = rd64(e + 40);
-        if (mode > 1 || ps < 4096 || ps > (2u << 20) || (ps & (ps - 1)) || bytes == 0) return CRUM_E_CORRUPT;
+        if (mode > 2 || ps < 4096 || ps > (2u << 20) || (ps & (ps - 1)) || bytes == 0) return CRUM_E_CORRUPT;
         if (np != bytes / ps + (bytes % ps != 0) || nd > np || first != sum) return CRUM_E_CORRUPT;
         if ((p.flags & 1u) && nd != np) return CRUM_E_CORRUPT;
         if (mode == 1) any_hash = true;

@@ -3,6 +3,7 @@
 #include "crum_internal.cuh"
 #include "../../include/crum.h"
 #include "../../include/crum_synth.h"
+#include "../../include/crum_device.h"
 
 namespace crum {
 
@@ -28,8 +29,10 @@ __global__ void k_synth_fill(uint8_t *p, uint64_t bytes, uint64_t seed, uint64_t
 
 // One block per listed page.
 __global__ void k_synth_write(uint8_t *p, uint64_t bytes, uint64_t page_size, const uint32_t *pages,
-                              uint64_t seed, uint64_t epoch, uint64_t r, int touch) {
+                              uint64_t seed, uint64_t epoch, uint64_t r, int touch, crum_tracker t) {
     const uint64_t i = pages[blockIdx.x];
+    // a TRACKED region's writer marks what it writes (include/crum_device.h)
+    if (t.force && threadIdx.x == 0) crum_mark_write(t, i * page_size, page_size);
     const uint64_t m = splitmix64((seed + 2) ^ (epoch << 56) ^ (r << 40) ^ i) | 1ull;
     const uint64_t lo = i * page_size;
     const uint64_t hi = min(lo + page_size, bytes);
@@ -59,10 +62,12 @@ void launch_synth_fill(cudaStream_t s, uint8_t *p, uint64_t bytes, uint64_t seed
 }
 void launch_synth_write(cudaStream_t s, uint8_t *p, uint64_t bytes, uint64_t page_size,
                         const uint32_t *pages, uint64_t n, uint64_t seed, uint64_t epoch, uint64_t r,
-                        int touch) {
+                        int touch, const crum_tracker *t) {
+    crum_tracker tr{};
+    if (t) tr = *t;
     for (uint64_t b0 = 0; b0 < n; b0 += (1u << 30))
         k_synth_write<<<(unsigned)min(n - b0, (uint64_t)1 << 30), 256, 0, s>>>(p, bytes, page_size, pages + b0,
-                                                                          seed, epoch, r, touch);
+                                                                          seed, epoch, r, touch, tr);
 }
 void launch_synth_scrub(cudaStream_t s, uint8_t *p, uint64_t bytes) {
     k_scrub<<<148 * 8, 256, 0, s>>>(reinterpret_cast<uint4 *>(p), bytes / 16);
@@ -86,7 +91,20 @@ extern "C" int crum_synth_write_pages(void *dev_ptr, uint64_t bytes, uint64_t pa
     if (!n_pages) return CRUM_OK;
     if (!dev_pages) return CRUM_E_INVAL;
     crum::launch_synth_write((cudaStream_t)stream, (uint8_t *)dev_ptr, bytes, page_size, dev_pages, n_pages,
-                             seed, epoch, region_index, touch);
+                             seed, epoch, region_index, touch, nullptr);
+    return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
+}
+
+extern "C" int crum_synth_write_pages_tracked(void *dev_ptr, uint64_t bytes, uint64_t page_size,
+                                              const uint32_t *dev_pages, uint64_t n_pages, uint64_t seed,
+                                              uint64_t epoch, uint64_t region_index, int touch,
+                                              const void *tracker, void *stream) {
+    if (!dev_ptr || (reinterpret_cast<uintptr_t>(dev_ptr) & 7) || (page_size & 7) || !page_size || !tracker)
+        return CRUM_E_INVAL;
+    if (!n_pages) return CRUM_OK;
+    if (!dev_pages) return CRUM_E_INVAL;
+    crum::launch_synth_write((cudaStream_t)stream, (uint8_t *)dev_ptr, bytes, page_size, dev_pages, n_pages,
+                             seed, epoch, region_index, touch, static_cast<const crum_tracker *>(tracker));
     return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
 }
 

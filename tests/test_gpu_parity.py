@@ -311,3 +311,52 @@ def test_c3_multi_region_sampled(crum):
     torch.cuda.synchronize()
     for z, h in zip(zs, p.host):
         assert np.array_equal(z.cpu().numpy(), h)
+
+
+def test_tracked_mode_parity(crum):
+    """CRUM_MODE_TRACKED (Alg. 1 write rule): pages marked in-kernel by the
+    writer (crum_mark_write of include/crum_device.h), marked by the
+    stream-ordered batch call, and an unmarked change -- images bit-exact with
+    the oracle given the same marks."""
+    T = 2
+    specs = [(6 * 4096 + 10, 4096, T), (5 * 65536, 65536, T), (3 * 4096, 4096, C), (2 * 65536, 65536, H)]
+    p = mkpair(specs, 21)
+    img = p.g.new_image()
+    p.g.checkpoint_gather(img)
+    st, want, _ = p.o.checkpoint_gather()
+    assert img.tobytes() == want.tobytes()
+    # epoch 1: the writer marks what it writes in regions 0 and 1
+    for r in (0, 1):
+        nb, P, _ = specs[r]
+        pages = synth.choose_dirty(p.S, 1, r, synth.n_pages(nb, P), 0.4)
+        synth.apply_writer(p.host[r], P, pages, p.S, 1, r)
+        p.o.mark_pages(p.rid_o[r], pages)
+        dp = torch.from_numpy(pages.astype(np.uint32)).cuda()
+        crum.synth_write_pages_tracked(p.dev[r], nb, P, dp, len(pages), p.S, 1, r, p.g.region_tracker(p.rid_g[r]))
+    # an unmarked change (not captured by definition) and a batch mark of an unchanged page
+    p.host[0][4096 * 5 + 7] ^= 1
+    p.dev[0][4096 * 5 + 7] ^= 1
+    marks = np.array([3], dtype=np.uint32)
+    p.o.mark_pages(p.rid_o[1], marks)
+    assert p.g.mark_dirty_pages(p.rid_g[1], torch.from_numpy(marks).cuda(), 1) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(p.g.debug_detect(p.N), p.oracle_flags())
+    st, want, _ = p.o.checkpoint_gather()
+    rep = p.g.checkpoint_gather(img)
+    assert img.tobytes() == want.tobytes()
+    assert p.g.sync_shadow() == p.o.sync_shadow() == 0
+    # restore of both images onto zeroed tracked regions reproduces the marked state
+    q = crum.Context(0)
+    zs = []
+    for nb, P, mode in specs:
+        z = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        zs.append(z)
+        q.register_region(z, nb, P, mode)
+    st, full_want, _ = p.o.checkpoint_gather(flags=crum.FULL)
+    full = p.g.new_image()
+    p.g.checkpoint_gather(full, flags=crum.FULL)
+    assert full.tobytes() == full_want.tobytes()
+    q.restore_scatter(full)
+    torch.cuda.synchronize()
+    for z, h in zip(zs, p.host):
+        assert np.array_equal(z.cpu().numpy(), h)
