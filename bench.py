@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="crum", choices=["crum", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--mode", default="compare", choices=["compare", "hash"])
+    ap.add_argument("--mode", default="compare", choices=["compare", "hash", "tracked"])
     ap.add_argument("--page", type=int, default=64 * KiB)
     ap.add_argument("--dirty", type=float, default=0.10)
     ap.add_argument("--region-gib", type=float, default=1.0)
@@ -63,7 +63,7 @@ def parse():
 
 def workload(args, rank: int):
     """(specs, description).  specs: list of (nbytes, page_size, mode)."""
-    mode = 0 if args.mode == "compare" else 1
+    mode = {"compare": 0, "hash": 1, "tracked": 2}[args.mode]
     if args.config == "c1":
         return [(4 * MiB, 4 * KiB, mode)], f"C1: one 4 MiB region, 4 KiB pages, {args.dirty:.0%} dirty, {args.mode}"
     if args.config == "c2":
@@ -162,8 +162,11 @@ def oracle_steps(specs, S, dirty, seconds: float, max_steps: int, min_steps: int
     epoch = 0
     while len(times) < max_steps and (len(times) < min_steps or time.perf_counter() - t_start < seconds):
         epoch += 1
-        for r, (nb, P, _) in enumerate(specs):
-            synth.apply_writer(host[r], P, synth.choose_dirty(S, epoch, r, synth.n_pages(nb, P), dirty), S, epoch, r)
+        for r, (nb, P, mode) in enumerate(specs):
+            pages = synth.choose_dirty(S, epoch, r, synth.n_pages(nb, P), dirty)
+            synth.apply_writer(host[r], P, pages, S, epoch, r)
+            if mode == 2:  # TRACKED: the writer marks what it writes
+                o.mark_pages(r + 1, pages)
         t0 = time.perf_counter()
         st, img, rep = o.checkpoint_gather(capacity=cap)
         times.append(time.perf_counter() - t0)
@@ -249,6 +252,7 @@ def main():
             crum.synth_fill(t, nb, S, r, stream=stream)
             regions.append(t)
             ctx.register_region(t, nb, P, mode)
+    trackers = [ctx.region_tracker(r + 1) for r in range(len(specs))] if args.mode == "tracked" else None
     # the dirty pages of every epoch, precomputed on the host (untimed)
     n_epochs = args.warmup + args.steps + max(3, args.steps // 2) + 2
     pages = [[torch.from_numpy(synth.choose_dirty(S, e, r, synth.n_pages(nb, P), args.dirty).astype(np.uint32)).to(dev)
@@ -270,7 +274,12 @@ def main():
     def app_epoch(e):
         for r, (nb, P, _) in enumerate(specs):
             pg = pages[e - 1][r]
-            crum.synth_write_pages(regions[r], nb, P, pg, pg.numel(), S, e, r, stream=stream)
+            if trackers:
+                # TRACKED: the application's writer marks what it writes (crum_device.h)
+                crum.synth_write_pages_tracked(regions[r], nb, P, pg, pg.numel(), S, e, r, trackers[r],
+                                               stream=stream)
+            else:
+                crum.synth_write_pages(regions[r], nb, P, pg, pg.numel(), S, e, r, stream=stream)
         crum.synth_scrub(scrub, scrub.numel(), stream=stream)
 
     from paper_1808_00117_b200 import coord
@@ -317,7 +326,7 @@ def main():
     launches = ctx.launch_count - launches0
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
     T = sum(step_ms) / 1e3
-    det_ms = [r["t_detect_ms"] for r in reps]
+    det_ms = [r["t_gather_ms"] if args.mode == "tracked" else r["t_detect_ms"] for r in reps]
     if distributed:
         t = torch.tensor([T, sum(det_ms)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -340,11 +349,12 @@ def main():
         kname = "fused_compare"
         det_bytes = 2 * F + 2 * payload
     else:
-        kname = f"detect_{args.mode}"
-        det_bytes = 2 * F if args.mode == "compare" else F + 16 * n_pages
+        kname = "gather" if args.mode == "tracked" else f"detect_{args.mode}"
+        det_bytes = {"compare": 2 * F, "hash": F + 16 * n_pages, "tracked": 2 * payload}[args.mode]
     det_t = det_sum / args.steps / 1e3
     achieved = det_bytes / det_t / 1e9
-    dev_alg = (2 * F + 2 * payload) if args.mode == "compare" else (F + 16 * n_pages + 2 * payload)
+    dev_alg = {"compare": 2 * F + 2 * payload, "hash": F + 16 * n_pages + 2 * payload,
+               "tracked": n_pages + 2 * payload}[args.mode]
     traffic_key = f"{kname}:{args.config}:{args.page}:{args.dirty}"
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
