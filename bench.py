@@ -26,10 +26,12 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import shutil
 import signal
 import statistics
 import subprocess
 import sys
+import tempfile
 import time
 
 import numpy as np
@@ -254,7 +256,7 @@ def main():
             ctx.register_region(t, nb, P, mode)
     trackers = [ctx.region_tracker(r + 1) for r in range(len(specs))] if args.mode == "tracked" else None
     # the dirty pages of every epoch, precomputed on the host (untimed)
-    n_epochs = args.warmup + args.steps + max(3, args.steps // 2) + 2
+    n_epochs = args.warmup + args.steps + max(3, args.steps // 2) + max(4, args.steps // 2) + 2
     pages = [[torch.from_numpy(synth.choose_dirty(S, e, r, synth.n_pages(nb, P), args.dirty).astype(np.uint32)).to(dev)
               for r, (nb, P, _) in enumerate(specs)] for e in range(1, n_epochs + 1)]
     scrub = torch.empty(256 * MiB, dtype=torch.uint8, device=dev)
@@ -410,6 +412,37 @@ def main():
             r_ms.append((time.perf_counter() - t0) * 1e3)
         line["restore"] = {"value": round(F / (statistics.median(r_ms) / 1e3) / 1e9, 3), "unit": "GB/s",
                            "ms_per_call": round(statistics.median(r_ms), 3), "h2d_bytes": rr["image_bytes"]}
+        # forked checkpoint (sec. 3.3): the application pauses for
+        # the gather only; a writer thread persists the image while the next epoch runs
+        img2 = ctx.new_image(cap)
+        tmpd = tempfile.mkdtemp(prefix="crum_bench_")
+        pause_ms, w_ms = [], []
+        try:
+            for i in range(max(4, args.steps // 2)):
+                epoch += 1
+                app_epoch(epoch)
+                torch.cuda.synchronize()
+                im = (img, img2)[i % 2]
+                im.persist_wait()
+                t0 = time.perf_counter()
+                ctx.checkpoint_gather(im, stream=stream)
+                pause_ms.append((time.perf_counter() - t0) * 1e3)
+                im.persist(os.path.join(tmpd, f"r{rank}_{i % 2}.crum"))
+            img.persist_wait()
+            img2.persist_wait()
+            t0 = time.perf_counter()
+            img2.persist(os.path.join(tmpd, f"r{rank}_w.crum"))
+            img2.persist_wait()
+            w_ms.append((time.perf_counter() - t0) * 1e3)
+        finally:
+            shutil.rmtree(tmpd, ignore_errors=True)
+        line["forked"] = {"pause_ms": round(statistics.median(pause_ms), 3),
+                          "persist_GBs": round(img2.length / (w_ms[0] / 1e3) / 1e9, 3),
+                          "persist_ms": round(w_ms[0], 3), "image_bytes": img2.length,
+                          "note": "gather wall time with the previous image's writer in flight (two "
+                                  "alternating pinned images); persist = one image written to "
+                                  "tempfile.gettempdir() without fsync"}
+        img2.destroy()
         img.destroy()
     # ---- cpu_baseline: the oracle on this workload, rank 0 at N=1 only ----
     if not args.no_cpu_baseline and world == 1:

@@ -64,9 +64,10 @@ enum crum_status {
     CRUM_E_CAPACITY = -6,  /* image buffer too small; report->image_bytes = required size */
     CRUM_E_CORRUPT = -7,   /* bad magic/version/CRC/sizes/ids, or a hash mismatch under CRUM_VERIFY */
     CRUM_E_MISMATCH = -8,  /* image region table != live registered set */
-    CRUM_E_BUSY = -9,      /* reserved */
+    CRUM_E_BUSY = -9,      /* gather into an image whose persist is still in flight */
     CRUM_E_DEVICE = -10,   /* ptr not accessible from the context's device; no such device */
-    CRUM_E_CUDA = -11      /* underlying CUDA error (sticky) */
+    CRUM_E_CUDA = -11,     /* underlying CUDA error (sticky) */
+    CRUM_E_IO = -12        /* file I/O failed (persist / load); detail via crum_last_error_detail */
 };
 
 /* Per-region dirty-detection mode (reading Q1/Q8). */
@@ -200,6 +201,29 @@ CRUM_API int crum_image_create(crum_ctx *ctx, uint64_t capacity_bytes, crum_imag
 CRUM_API int crum_image_import(crum_ctx *ctx, const void *bytes, uint64_t len, crum_image **out);
 CRUM_API int crum_image_data(const crum_image *img, void **data_out, uint64_t *len_out, uint64_t *capacity_out);
 CRUM_API int crum_image_destroy(crum_image *img);
+
+/* ---------------------------------------------------------------------------
+ * Asynchronous ("forked") persistence, the paper's forked checkpoint
+ * (sec. 3.3): once the GPU has been drained into the pinned
+ * image, a writer thread stores it to `path` while the application goes on;
+ * the pause is the gather alone.  While a persist is in flight the image is
+ * busy: a gather into it returns CRUM_E_BUSY (SPEC.md:441
+ * "ConcurrentCheckpoint"), so applications alternate two images; restoring
+ * from it is allowed (the writer only reads it).
+ *   crum_image_persist: start writing img[0, len) to path (created/truncated);
+ *     flags: CRUM_PERSIST_FSYNC (fsync before completion).  Errors: INVAL, BUSY.
+ *   crum_image_persist_wait: wait for the writer; returns its outcome (OK or
+ *     CRUM_E_IO); OK if none is in flight.
+ *   crum_image_persist_busy: *busy_out = 1 while the writer runs.
+ *   crum_image_load: new pinned image holding the file's bytes (restart from
+ *     storage).  Errors: INVAL, IO, NOMEM.
+ * crum_image_destroy waits for an in-flight writer first.
+ * ------------------------------------------------------------------------- */
+enum { CRUM_PERSIST_FSYNC = 1u << 0 };
+CRUM_API int crum_image_persist(crum_image *img, const char *path, uint32_t flags);
+CRUM_API int crum_image_persist_wait(crum_image *img);
+CRUM_API int crum_image_persist_busy(const crum_image *img, int *busy_out);
+CRUM_API int crum_image_load(crum_ctx *ctx, const char *path, crum_image **out);
 
 /* ---------------------------------------------------------------------------
  * sec. 3.4 checkpoint drain as an incremental gather (DESIGN

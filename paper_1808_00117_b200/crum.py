@@ -26,12 +26,13 @@ _L = C.CDLL(LIB_PATH)
 
 OK = 0
 E_INVAL, E_OVERLAP, E_NOREGION, E_RANGE, E_NOMEM = -1, -2, -3, -4, -5
-E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY, E_DEVICE, E_CUDA = -6, -7, -8, -9, -10, -11
+E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY, E_DEVICE, E_CUDA, E_IO = -6, -7, -8, -9, -10, -11, -12
 MODE_COMPARE, MODE_HASH = 0, 1
 FULL, VERIFY = 1, 2
 MODE_TRACKED = 2
 CFG_TIMING = 1
 PATH_FUSED = 1
+PERSIST_FSYNC = 1
 EXPORT_FORCE, EXPORT_HASHES, EXPORT_MIRROR = 0, 1, 2
 ALL_PAGES = (1 << 64) - 1
 
@@ -45,6 +46,7 @@ EXPORTED = (
     "crum_synth_fill", "crum_synth_write_pages", "crum_synth_scrub", "crum_probe_copy",
     "crum_synth_alloc_managed", "crum_synth_free_managed", "crum_synth_write_pages_tracked",
     "crum_mark_dirty_pages", "crum_region_tracker",
+    "crum_image_persist", "crum_image_persist_wait", "crum_image_persist_busy", "crum_image_load",
 )
 
 
@@ -101,6 +103,10 @@ _sig = {
                                            _vp]),
     "crum_mark_dirty_pages": (_i, [_vp, _u32, _vp, _u64, _vp]),
     "crum_region_tracker": (_i, [_vp, _u32, C.POINTER(Tracker)]),
+    "crum_image_persist": (_i, [_vp, C.c_char_p, _u32]),
+    "crum_image_persist_wait": (_i, [_vp]),
+    "crum_image_persist_busy": (_i, [_vp, C.POINTER(_i)]),
+    "crum_image_load": (_i, [_vp, C.c_char_p, C.POINTER(_vp)]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_L, _name)
@@ -142,10 +148,13 @@ def _addr(x) -> int:
 class Image:
     """A library-owned pinned host image (crum_image)."""
 
-    def __init__(self, ctx: "Context", capacity: int | None = None, data: bytes | np.ndarray | None = None):
+    def __init__(self, ctx: "Context", capacity: int | None = None, data: bytes | np.ndarray | None = None,
+                 path: str | None = None):
         self._h = _vp()
         self._ctx = ctx
-        if data is not None:
+        if path is not None:
+            _check(_L.crum_image_load(ctx._h, os.fsencode(path), C.byref(self._h)), "crum_image_load")
+        elif data is not None:
             buf = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray)
                                        else data.view(np.uint8).reshape(-1))
             _check(_L.crum_image_import(ctx._h, buf.ctypes.data if buf.nbytes else None, buf.nbytes,
@@ -182,6 +191,22 @@ class Image:
 
     def tobytes(self) -> bytes:
         return self.view().tobytes()
+
+    # -- forked checkpoint (sec. 3.3): persist on a writer thread
+    def persist(self, path: str, fsync: bool = False):
+        """Start writing the image to `path`; returns at once."""
+        _check(_L.crum_image_persist(self._h, os.fsencode(path), PERSIST_FSYNC if fsync else 0),
+               "crum_image_persist")
+
+    def persist_wait(self):
+        """Wait for the writer; raises CrumError(CRUM_E_IO) if it failed."""
+        _check(_L.crum_image_persist_wait(self._h), "crum_image_persist_wait")
+
+    @property
+    def busy(self) -> bool:
+        b = _i()
+        _check(_L.crum_image_persist_busy(self._h, C.byref(b)), "crum_image_persist_busy")
+        return bool(b.value)
 
     def destroy(self):
         if self._h and self._h.value:
@@ -271,6 +296,10 @@ class Context:
 
     def import_image(self, data) -> Image:
         return Image(self, data=data)
+
+    def load_image(self, path: str) -> Image:
+        """Restart from storage: a new pinned image holding the file's bytes."""
+        return Image(self, path=path)
 
     # -- sec. 3.4 drain (PAPER.md:543-554)
     def checkpoint_gather(self, image: Image, stream=None, flags: int = 0, raise_on_error: bool = True):

@@ -8,8 +8,15 @@
 // kernels_image.cu.
 #include <cuda_runtime.h>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <cerrno>
 #include <cstdarg>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -126,6 +133,11 @@ struct crum_image {
     uint64_t cap;
     uint64_t len;
     int device;
+    // asynchronous persistence (writer thread)
+    std::thread writer;
+    std::atomic<int> busy{0};
+    int result = 0;
+    std::string error;
 };
 
 struct crum_ctx {
@@ -682,6 +694,7 @@ const char *crum_status_string(int s) {
         case CRUM_E_BUSY: return "busy";
         case CRUM_E_DEVICE: return "pointer or device not usable";
         case CRUM_E_CUDA: return "CUDA error";
+        case CRUM_E_IO: return "file I/O error";
         default: return "unknown status";
     }
 }
@@ -1026,9 +1039,107 @@ int crum_image_data(const crum_image *img, void **data, uint64_t *len, uint64_t 
 
 int crum_image_destroy(crum_image *img) {
     if (!img) return CRUM_E_INVAL;
+    if (img->writer.joinable()) img->writer.join();
     cudaSetDevice(img->device);
     cudaFreeHost(img->host);
     delete img;
+    return CRUM_OK;
+}
+
+namespace {
+// Write all of [p, p+n) to fd (short writes and EINTR handled).
+bool write_all(int fd, const uint8_t *p, uint64_t n) {
+    while (n) {
+        const ssize_t w = ::write(fd, p, std::min<uint64_t>(n, 1ull << 30));
+        if (w < 0) {
+            if (errno == EINTR) continue;
+            return false;
+        }
+        p += w;
+        n -= (uint64_t)w;
+    }
+    return true;
+}
+}  // namespace
+
+int crum_image_persist(crum_image *img, const char *path, uint32_t flags) {
+    if (!img || !path || (flags & ~(uint32_t)CRUM_PERSIST_FSYNC)) {
+        set_detail("null image/path or bad flags");
+        return CRUM_E_INVAL;
+    }
+    if (img->busy.load()) {
+        set_detail("image is being persisted");
+        return CRUM_E_BUSY;
+    }
+    if (img->writer.joinable()) img->writer.join();
+    img->busy.store(1);
+    img->result = CRUM_OK;
+    img->error.clear();
+    const std::string dst(path);
+    img->writer = std::thread([img, dst, flags]() {
+        const int fd = ::open(dst.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+        bool ok = fd >= 0;
+        if (ok) ok = write_all(fd, img->host, img->len);
+        if (ok && (flags & CRUM_PERSIST_FSYNC)) ok = ::fsync(fd) == 0;
+        if (fd >= 0 && ::close(fd) != 0) ok = false;
+        if (!ok) {
+            img->result = CRUM_E_IO;
+            img->error = "persist " + dst + ": " + strerror(errno);
+        }
+        img->busy.store(0);
+    });
+    return CRUM_OK;
+}
+
+int crum_image_persist_wait(crum_image *img) {
+    if (!img) return CRUM_E_INVAL;
+    if (img->writer.joinable()) img->writer.join();
+    if (img->result != CRUM_OK) set_detail("%s", img->error.c_str());
+    return img->result;
+}
+
+int crum_image_persist_busy(const crum_image *img, int *busy_out) {
+    if (!img || !busy_out) return CRUM_E_INVAL;
+    *busy_out = img->busy.load();
+    return CRUM_OK;
+}
+
+int crum_image_load(crum_ctx *ctx, const char *path, crum_image **out) {
+    if (!path || !out) return CRUM_E_INVAL;
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) {
+        set_detail("open %s: %s", path, strerror(errno));
+        return CRUM_E_IO;
+    }
+    struct stat sb;
+    if (::fstat(fd, &sb) != 0) {
+        ::close(fd);
+        set_detail("stat %s: %s", path, strerror(errno));
+        return CRUM_E_IO;
+    }
+    const uint64_t len = (uint64_t)sb.st_size;
+    int st = crum_image_create(ctx, len, out);
+    if (st) {
+        ::close(fd);
+        return st;
+    }
+    uint8_t *p = (*out)->host;
+    uint64_t n = len;
+    while (n) {
+        const ssize_t r = ::read(fd, p, std::min<uint64_t>(n, 1ull << 30));
+        if (r < 0 && errno == EINTR) continue;
+        if (r <= 0) {
+            ::close(fd);
+            crum_image_destroy(*out);
+            *out = nullptr;
+            set_detail("read %s: %s", path, r < 0 ? strerror(errno) : "short file");
+            return CRUM_E_IO;
+        }
+        p += r;
+        n -= (uint64_t)r;
+    }
+    ::close(fd);
+    (*out)->len = len;
     return CRUM_OK;
 }
 
@@ -1183,6 +1294,10 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     if (!img || (flags & ~CRUM_FULL)) {
         set_detail("null image or bad flags");
         return CRUM_E_INVAL;
+    }
+    if (img->busy.load()) {
+        set_detail("image is being persisted (alternate two images)");
+        return CRUM_E_BUSY;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool full = flags & CRUM_FULL;
@@ -1575,6 +1690,7 @@ int crum_restore_scatter(crum_ctx *ctx, const crum_image *img, void *stream, uin
         set_detail("null image or bad flags");
         return CRUM_E_INVAL;
     }
+    // reading an image that is being persisted is safe (the writer only reads)
     return restore_common(c, img->host, nullptr, img->len, static_cast<cudaStream_t>(stream), flags, rep);
 }
 
