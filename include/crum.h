@@ -262,6 +262,46 @@ CRUM_API int crum_restore_scatter(crum_ctx *ctx, const crum_image *img, void *st
 CRUM_API int crum_restore_scatter_device(crum_ctx *ctx, const void *dev_image, uint64_t len, void *stream,
                                 uint32_t flags, crum_report *report_out);
 
+/* ---------------------------------------------------------------------------
+ * Lazy restore with exponential prefetch: the paper's read-fault heuristic
+ * (sec. 4.2: "for small shadow UVM regions, it reads in all
+ * of the data ... for a read fault on a large shadow UVM region, it starts off
+ * by only reading the data for just one page containing the faulting address.
+ * On subsequent read faults on the same region ... we exponentially increase
+ * (by powers of 2) the number of pages read in"), applied to restart.
+ *
+ * crum_restore_begin: every check of crum_restore_scatter (CRUM_VERIFY
+ *   included), nothing written.  The image must stay alive and unchanged until
+ *   crum_restore_end (gathers into it and crum_image_destroy return BUSY).
+ *   While the session is open, register / unregister / sync / gather /
+ *   restore / crum_destroy on ctx return CRUM_E_BUSY; crum_mark_dirty[_pages]
+ *   and application writes to fetched pages are fine.  Errors: as
+ *   crum_restore_scatter, plus BUSY (a session is already open).
+ * crum_restore_fetch: the application is about to read page `page` of
+ *   region `region_id` (a "read fault").  If the page is already present,
+ *   nothing happens (*covered_out = 0).  Otherwise the fault's window is made
+ *   present: the whole region if it has at most 8 pages, else pages
+ *   [page, page + w) clamped at the region end, where w is 1 on the region's
+ *   first fault and doubles after each fault (reading L1-L3).
+ *   Pages of the window already present are skipped; image slots of the rest
+ *   are written (region bytes + commit, as crum_restore_scatter) by kernels
+ *   on `stream`, reading the pinned image in place.  *covered_out = pages newly
+ *   present, *restored_out = image slots written (either may be NULL).
+ *   Stream-asynchronous: wait on `stream` before reading the pages elsewhere.
+ *   Errors: INVAL, NOREGION, RANGE (page >= n_r), CUDA.
+ * crum_restore_end: writes every slot not written yet, waits, closes the
+ *   session (always, even on error).  report_out (may be NULL) as
+ *   crum_restore_scatter's (dirty_pages = K of the image).
+ * Result: begin + any fetch sequence + end leaves regions, snapshots and
+ * force bits exactly as crum_restore_scatter of the same image.
+ * ------------------------------------------------------------------------- */
+typedef struct crum_restore_session crum_restore_session;
+CRUM_API int crum_restore_begin(crum_ctx *ctx, crum_image *img, void *stream, uint32_t flags,
+                                crum_restore_session **out);
+CRUM_API int crum_restore_fetch(crum_restore_session *session, uint32_t region_id, uint64_t page, void *stream,
+                                uint64_t *covered_out, uint64_t *restored_out);
+CRUM_API int crum_restore_end(crum_restore_session *session, void *stream, crum_report *report_out);
+
 /* Report of the most recent sync / gather / restore call on ctx: waits for
  * that call's work to finish, then fills counters and (if events were
  * recorded: a report was requested or CRUM_CFG_TIMING is set) phase times.

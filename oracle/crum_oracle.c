@@ -20,6 +20,10 @@
  *   orc_detect       -- brute-force Python bytes comparison, exhaustive flips
  *   sync / gather / restore -- invariants restore(ckpt(x)) == x, sync;sync==0,
  *                        dirty set == written set, numpy-assembled image bytes.
+ *   lazy restore     -- fault count of a sequential read = ceil(log2(n+1)),
+ *                        window sizes 1,2,4,..; windows hold the image's bytes
+ *                        (independent parser) and nothing else changes;
+ *                        begin+fetches+end == restore_scatter.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -37,6 +41,7 @@ enum {
     ORC_E_CAPACITY = -6,
     ORC_E_CORRUPT = -7,
     ORC_E_MISMATCH = -8,
+    ORC_E_BUSY = -9,
 };
 
 enum { ORC_MODE_COMPARE = 0, ORC_MODE_HASH = 1, ORC_MODE_TRACKED = 2 };
@@ -65,10 +70,19 @@ typedef struct {
     uint8_t *force;      /* per-page force-dirty bit (Q3) */
 } orc_region;
 
+/* An open lazy restore (sec. 4.2 read-fault heuristic applied to restart). */
+typedef struct {
+    const uint8_t *img;  /* the validated image (caller keeps it alive) */
+    uint8_t **present;   /* per region, per page: read in already */
+    uint64_t *window;    /* per region: pages the next fault reads */
+    uint8_t *written;    /* per slot: restored already */
+} orc_session;
+
 typedef struct {
     orc_region *r;       /* ascending id order */
     uint32_t n;
     uint32_t next_id;
+    orc_session *sess;   /* open lazy restore, or NULL */
 } orc_ctx;
 
 /* ------------------------------------------------------------------ */
@@ -256,6 +270,13 @@ static void free_region(orc_region *g)
 void orc_destroy(orc_ctx *c)
 {
     if (!c) return;
+    if (c->sess) {
+        for (uint32_t k = 0; k < c->n; ++k) free(c->sess->present[k]);
+        free(c->sess->present);
+        free(c->sess->window);
+        free(c->sess->written);
+        free(c->sess);
+    }
     for (uint32_t k = 0; k < c->n; ++k) free_region(&c->r[k]);
     free(c->r);
     free(c);
@@ -266,6 +287,7 @@ void orc_destroy(orc_ctx *c)
 int orc_register_region(orc_ctx *c, uint8_t *ptr, uint64_t bytes, uint64_t page_size,
                         uint32_t mode, uint32_t *id_out)
 {
+    if (c && c->sess) return ORC_E_BUSY;
     if (!c || !ptr || !id_out || bytes == 0) return ORC_E_INVAL;
     if (page_size < ORC_MIN_PAGE || page_size > ORC_MAX_PAGE || (page_size & (page_size - 1)))
         return ORC_E_INVAL;
@@ -305,6 +327,7 @@ int orc_register_region(orc_ctx *c, uint8_t *ptr, uint64_t bytes, uint64_t page_
 
 int orc_unregister_region(orc_ctx *c, uint32_t id)
 {
+    if (c && c->sess) return ORC_E_BUSY;
     if (!c) return ORC_E_INVAL;
     for (uint32_t k = 0; k < c->n; ++k) {
         if (c->r[k].id != id) continue;
@@ -382,6 +405,7 @@ static void commit_page(orc_region *g, uint64_t i)
  * commit all of it; return sum |D_r|. */
 int orc_sync_shadow(orc_ctx *c, uint64_t *n_out)
 {
+    if (c && c->sess) return ORC_E_BUSY;
     if (!c) return ORC_E_INVAL;
     uint64_t total = 0;
     for (uint32_t k = 0; k < c->n; ++k) {
@@ -450,6 +474,7 @@ int orc_image_required_bytes(orc_ctx *c, uint64_t max_dirty, uint64_t *out)
 int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap,
                           orc_report *rep)
 {
+    if (c && c->sess) return ORC_E_BUSY;
     if (!c || !img || (flags & ~ORC_FULL)) return ORC_E_INVAL;
     const uint32_t R = c->n;
     uint64_t N = total_pages(c);
@@ -534,13 +559,9 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
     return ORC_OK;
 }
 
-/* Restart data movement (sec. 3.4, PAPER.md:563-565; reading Q11): validate
- * everything first, then write each listed page's logical bytes back and
- * commit it (mirror <- slot / table <- listed hash, force <- 0). */
-int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t flags,
-                        orc_report *rep)
+/* Every check a restore makes before writing anything (reading Q11). */
+static int validate_image(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t flags)
 {
-    if (!c || !img || (flags & ~ORC_VERIFY)) return ORC_E_INVAL;
     if (len < 64 || memcmp(img, "CRUM", 4) != 0) return ORC_E_CORRUPT;
     if (orc_crc32(img, 60) != rd32(img + 60)) return ORC_E_CORRUPT;
     const uint32_t version = rd32(img + 4), iflags = rd32(img + 8), R = rd32(img + 12);
@@ -605,6 +626,35 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
             }
         }
     }
+    return ORC_OK;
+}
+
+/* Write slot `slot` (page i of region g, payload bytes at src) back and commit
+ * it: cur and mirror <- the logical bytes, table <- listed hash, force <- 0. */
+static void restore_slot(orc_region *g, uint64_t i, const uint8_t *src, const uint8_t *hashes, uint64_t slot)
+{
+    uint64_t l = page_len(g, i);
+    memcpy(g->cur + i * g->page_size, src, l);
+    if (g->mode == ORC_MODE_COMPARE) memcpy(g->mirror + i * g->page_size, src, l);
+    else if (g->mode == ORC_MODE_HASH) g->table[i] = rd64(hashes + 8 * slot);
+    g->force[i] = 0;
+}
+
+/* Restart data movement (sec. 3.4, PAPER.md:563-565; reading Q11): validate
+ * everything first, then write each listed page's logical bytes back and
+ * commit it (mirror <- slot / table <- listed hash, force <- 0). */
+int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t flags,
+                        orc_report *rep)
+{
+    if (!c || !img || (flags & ~ORC_VERIFY)) return ORC_E_INVAL;
+    if (c->sess) return ORC_E_BUSY;
+    int st = validate_image(c, img, len, flags);
+    if (st) return st;
+    const uint32_t R = rd32(img + 12);
+    const uint64_t K = rd64(img + 16), poff = rd64(img + 24), ids_off = rd64(img + 40), total = rd64(img + 48);
+    const uint8_t *tab = img + 64;
+    const uint8_t *ids = img + ids_off;
+    const uint8_t *hashes = ids + round_up(4 * K, 8);
     /* Apply. */
     uint64_t pbyte = 0, dirty_bytes = 0, runs = 0, scanned = 0;
     for (uint32_t k = 0; k < R; ++k) {
@@ -613,12 +663,8 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
         scanned += g->bytes;
         for (uint64_t j = 0; j < nd; ++j) {
             uint64_t i = rd32(ids + 4 * (first + j));
-            uint64_t l = page_len(g, i);
-            memcpy(g->cur + i * g->page_size, img + poff + pbyte, l);
-            if (g->mode == ORC_MODE_COMPARE) memcpy(g->mirror + i * g->page_size, img + poff + pbyte, l);
-            else if (g->mode == ORC_MODE_HASH) g->table[i] = rd64(hashes + 8 * (first + j));
-            g->force[i] = 0;
-            dirty_bytes += l;
+            restore_slot(g, i, img + poff + pbyte, hashes, first + j);
+            dirty_bytes += page_len(g, i);
             if (j == 0 || rd32(ids + 4 * (first + j - 1)) + 1 != i) runs++;
             pbyte += g->page_size;
         }
@@ -631,6 +677,143 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
         rep->dirty_runs = runs;
         rep->image_bytes = total;
     }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Lazy restore: the paper's read-fault heuristic (sec. 4.2,           */
+/* PAPER.md:783-793) applied to restart.  "For small shadow UVM        */
+/* regions, it reads in all of the data ... for a read fault on a      */
+/* large shadow UVM region, it starts off by only reading the data for */
+/* just one page containing the faulting address.  On subsequent read  */
+/* faults on the same region ... we exponentially increase (by powers  */
+/* of 2) the number of pages read in."  Readings L1-L3:    */
+/* small = at most 8 pages; the window starts at the faulting page and */
+/* is clamped at the region end; a fault on a page already read in is  */
+/* no fault; the window stops doubling at 2^62.                        */
+/* ------------------------------------------------------------------ */
+#define ORC_SMALL_REGION_PAGES 8ull
+
+int orc_restore_begin(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t flags)
+{
+    if (!c || !img || (flags & ~ORC_VERIFY)) return ORC_E_INVAL;
+    if (c->sess) return ORC_E_BUSY;
+    int st = validate_image(c, img, len, flags);
+    if (st) return st;
+    orc_session *s = (orc_session *)calloc(1, sizeof *s);
+    s->img = img;
+    s->present = (uint8_t **)calloc(c->n ? c->n : 1, sizeof(uint8_t *));
+    s->window = (uint64_t *)calloc(c->n ? c->n : 1, sizeof(uint64_t));
+    for (uint32_t k = 0; k < c->n; ++k) {
+        s->present[k] = (uint8_t *)calloc(c->r[k].n_pages, 1);
+        s->window[k] = 1;
+    }
+    s->written = (uint8_t *)calloc(rd64(img + 16) + 1, 1);
+    c->sess = s;
+    return ORC_OK;
+}
+
+/* Table entry k of the session's image: slots [first, first+nd), page size ps. */
+static void entry_of(const uint8_t *img, uint32_t k, uint64_t *first, uint64_t *nd)
+{
+    *nd = rd64(img + 64 + 48 * (uint64_t)k + 32);
+    *first = rd64(img + 64 + 48 * (uint64_t)k + 40);
+}
+
+/* Byte offset inside the payload of slot `slot` of table entry k. */
+static uint64_t slot_payload_offset(const orc_ctx *c, const uint8_t *img, uint32_t k, uint64_t slot)
+{
+    uint64_t off = 0, first, nd;
+    for (uint32_t q = 0; q < k; ++q) {
+        entry_of(img, q, &first, &nd);
+        off += nd * c->r[q].page_size;
+    }
+    entry_of(img, k, &first, &nd);
+    return off + (slot - first) * c->r[k].page_size;
+}
+
+/* Write slot `slot` of the session's image (page i of region k) back. */
+static void session_restore_slot(orc_ctx *c, uint32_t k, uint64_t i, uint64_t slot)
+{
+    const uint8_t *img = c->sess->img;
+    const uint64_t K = rd64(img + 16), poff = rd64(img + 24), ids_off = rd64(img + 40);
+    const uint8_t *hashes = img + ids_off + round_up(4 * K, 8);
+    restore_slot(&c->r[k], i, img + poff + slot_payload_offset(c, img, k, slot), hashes, slot);
+    c->sess->written[slot] = 1;
+}
+
+/* A read fault on page `page` of region `id`. */
+int orc_restore_fetch(orc_ctx *c, uint32_t id, uint64_t page, uint64_t *covered, uint64_t *restored)
+{
+    if (!c || !c->sess || !covered || !restored) return ORC_E_INVAL;
+    uint32_t k = 0;
+    while (k < c->n && c->r[k].id != id) ++k;
+    if (k == c->n) return ORC_E_NOREGION;
+    orc_region *g = &c->r[k];
+    if (page >= g->n_pages) return ORC_E_RANGE;
+    orc_session *s = c->sess;
+    *covered = 0;
+    *restored = 0;
+    if (s->present[k][page]) return ORC_OK;   /* already read in: no fault */
+    uint64_t lo, hi;
+    if (g->n_pages <= ORC_SMALL_REGION_PAGES) {
+        lo = 0;                                /* small region: all of it */
+        hi = g->n_pages;
+    } else {
+        lo = page;                             /* window pages from the faulting one */
+        hi = g->n_pages - page < s->window[k] ? g->n_pages : page + s->window[k];
+        if (s->window[k] < (1ull << 62)) s->window[k] *= 2;
+    }
+    const uint8_t *ids = s->img + rd64(s->img + 40);
+    uint64_t first, nd;
+    entry_of(s->img, k, &first, &nd);
+    for (uint64_t i = lo; i < hi; ++i) {
+        if (s->present[k][i]) continue;
+        s->present[k][i] = 1;
+        (*covered)++;
+        for (uint64_t j = 0; j < nd; ++j) {    /* is page i listed in the image? */
+            if (rd32(ids + 4 * (first + j)) == i) {
+                session_restore_slot(c, k, i, first + j);
+                (*restored)++;
+                break;
+            }
+        }
+    }
+    return ORC_OK;
+}
+
+/* Close the session: every slot not yet written is written now. */
+int orc_restore_end(orc_ctx *c, orc_report *rep)
+{
+    if (!c || !c->sess) return ORC_E_INVAL;
+    orc_session *s = c->sess;
+    const uint8_t *ids = s->img + rd64(s->img + 40);
+    uint64_t dirty_bytes = 0, runs = 0, scanned = 0;
+    for (uint32_t k = 0; k < c->n; ++k) {
+        uint64_t first, nd;
+        entry_of(s->img, k, &first, &nd);
+        scanned += c->r[k].bytes;
+        for (uint64_t j = 0; j < nd; ++j) {
+            uint64_t i = rd32(ids + 4 * (first + j));
+            if (!s->written[first + j]) session_restore_slot(c, k, i, first + j);
+            dirty_bytes += page_len(&c->r[k], i);
+            if (j == 0 || rd32(ids + 4 * (first + j - 1)) + 1 != i) runs++;
+        }
+    }
+    if (rep) {
+        rep->scanned_pages = total_pages(c);
+        rep->scanned_bytes = scanned;
+        rep->dirty_pages = rd64(s->img + 16);
+        rep->dirty_bytes = dirty_bytes;
+        rep->dirty_runs = runs;
+        rep->image_bytes = rd64(s->img + 48);
+    }
+    for (uint32_t k = 0; k < c->n; ++k) free(s->present[k]);
+    free(s->present);
+    free(s->window);
+    free(s->written);
+    free(s);
+    c->sess = NULL;
     return ORC_OK;
 }
 

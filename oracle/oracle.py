@@ -23,8 +23,8 @@ _LIB = os.path.join(_HERE, "liboracle_crum.so")
 _lock = threading.Lock()
 _lib = None
 
-OK, E_INVAL, E_OVERLAP, E_NOREGION, E_RANGE, E_NOMEM, E_CAPACITY, E_CORRUPT, E_MISMATCH = (
-    0, -1, -2, -3, -4, -5, -6, -7, -8)
+OK, E_INVAL, E_OVERLAP, E_NOREGION, E_RANGE, E_NOMEM, E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY = (
+    0, -1, -2, -3, -4, -5, -6, -7, -8, -9)
 MODE_COMPARE, MODE_HASH, MODE_TRACKED = 0, 1, 2
 FULL, VERIFY = 1, 2
 
@@ -78,7 +78,10 @@ def lib():
         L.orc_get_hashes.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
         L.orc_get_mirror.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
         L.orc_page_hash.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, u64p]
-        for f in ("orc_register_region", "orc_unregister_region", "orc_mark_dirty", "orc_mark_pages", "orc_detect",
+        L.orc_restore_begin.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32]
+        L.orc_restore_fetch.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, u64p, u64p]
+        L.orc_restore_end.argtypes = [C.c_void_p, C.POINTER(Report)]
+        for f in ("orc_restore_begin", "orc_restore_fetch", "orc_restore_end","orc_register_region", "orc_unregister_region", "orc_mark_dirty", "orc_mark_pages", "orc_detect",
                   "orc_sync_shadow", "orc_image_required_bytes", "orc_checkpoint_gather",
                   "orc_restore_scatter", "orc_get_force", "orc_get_hashes", "orc_get_mirror",
                   "orc_page_hash"):
@@ -189,6 +192,26 @@ class Oracle:
         image = np.ascontiguousarray(image, dtype=np.uint8)
         rep = Report()
         st = self._L.orc_restore_scatter(self._h, _ptr(image) if image.nbytes else 0, image.nbytes, flags, C.byref(rep))
+        return st, rep.as_dict()
+
+    # -- lazy restore: the sec. 4.2 read-fault heuristic applied to restart
+    def restore_begin(self, image: np.ndarray, flags: int = 0) -> int:
+        image = np.ascontiguousarray(image, dtype=np.uint8)
+        st = self._L.orc_restore_begin(self._h, _ptr(image) if image.nbytes else 0, image.nbytes, flags)
+        if st == OK:
+            self._sess_img = image          # the oracle reads it until restore_end
+        return st
+
+    def restore_fetch(self, rid: int, page: int):
+        """Returns (status, pages newly present, image slots written)."""
+        cov, res = C.c_uint64(0), C.c_uint64(0)
+        st = self._L.orc_restore_fetch(self._h, rid, page, C.byref(cov), C.byref(res))
+        return st, cov.value, res.value
+
+    def restore_end(self):
+        rep = Report()
+        st = self._L.orc_restore_end(self._h, C.byref(rep))
+        self._sess_img = None
         return st, rep.as_dict()
 
     def force_bits(self, rid: int) -> np.ndarray:

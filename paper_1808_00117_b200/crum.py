@@ -47,6 +47,7 @@ EXPORTED = (
     "crum_synth_alloc_managed", "crum_synth_free_managed", "crum_synth_write_pages_tracked",
     "crum_mark_dirty_pages", "crum_region_tracker",
     "crum_image_persist", "crum_image_persist_wait", "crum_image_persist_busy", "crum_image_load",
+    "crum_restore_begin", "crum_restore_fetch", "crum_restore_end",
 )
 
 
@@ -107,6 +108,9 @@ _sig = {
     "crum_image_persist_wait": (_i, [_vp]),
     "crum_image_persist_busy": (_i, [_vp, C.POINTER(_i)]),
     "crum_image_load": (_i, [_vp, C.c_char_p, C.POINTER(_vp)]),
+    "crum_restore_begin": (_i, [_vp, _vp, _vp, _u32, C.POINTER(_vp)]),
+    "crum_restore_fetch": (_i, [_vp, _u32, _u64, _vp, C.POINTER(_u64), C.POINTER(_u64)]),
+    "crum_restore_end": (_i, [_vp, _vp, C.POINTER(Report)]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_L, _name)
@@ -210,12 +214,52 @@ class Image:
 
     def destroy(self):
         if self._h and self._h.value:
-            _L.crum_image_destroy(self._h)
+            _check(_L.crum_image_destroy(self._h), "crum_image_destroy")   # BUSY: a restore session reads it
             self._h = _vp()
 
     def __del__(self):
         try:
             self.destroy()
+        except Exception:
+            pass
+
+
+class RestoreSession:
+    """An open lazy restore (crum_restore_begin .. crum_restore_end): the
+    sec. 4.2 read-fault heuristic applied to restart."""
+
+    def __init__(self, ctx: "Context", image: Image, stream=None, flags: int = 0):
+        self._h = _vp()
+        self._ctx, self._img = ctx, image
+        _check(_L.crum_restore_begin(ctx._h, image._h, _stream(stream), flags, C.byref(self._h)),
+               "crum_restore_begin")
+
+    def fetch(self, region_id: int, page: int, stream=None):
+        """Read fault on (region, page): returns (pages newly present, slots written)."""
+        cov, res = _u64(), _u64()
+        _check(_L.crum_restore_fetch(self._h, region_id, page, _stream(stream), C.byref(cov), C.byref(res)),
+               "crum_restore_fetch")
+        return cov.value, res.value
+
+    def end(self, stream=None) -> dict:
+        rep = Report()
+        h, self._h = self._h, _vp()
+        if not (h and h.value):
+            raise CrumError(E_INVAL, "crum_restore_end: session already closed")
+        _check(_L.crum_restore_end(h, _stream(stream), C.byref(rep)), "crum_restore_end")
+        return rep.as_dict()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        if self._h and self._h.value:
+            self.end()
+
+    def __del__(self):
+        try:
+            if self._h and self._h.value:
+                self.end()
         except Exception:
             pass
 
@@ -328,6 +372,10 @@ class Context:
             _check(st, "crum_restore_scatter")
             return rep.as_dict()
         return st, rep.as_dict()
+
+    def restore_begin(self, image: Image, stream=None, flags: int = 0) -> RestoreSession:
+        """Lazy restore: validate now, restore on fetch() / end()."""
+        return RestoreSession(self, image, stream, flags)
 
     def restore_scatter_device(self, dev_ptr, length: int, stream=None, flags: int = 0, report: bool = True,
                                raise_on_error: bool = True):

@@ -702,6 +702,7 @@ __global__ void __launch_bounds__(256) k_scatter(ScatterArgs a) {
         const uint64_t ru = u - s.unit_base;
         const uint64_t j = ru >> sh, seg = ru & ((1ull << sh) - 1);
         const uint64_t k = s.first + j;
+        if (a.skip && a.skip[k]) continue;
         const uint64_t i = a.ids[k];
         const uint64_t off = (i << g.log2p) + (seg << kSegLog2);
         if (g.bytes > off) {
@@ -720,6 +721,7 @@ __global__ void __launch_bounds__(256) k_scatter(ScatterArgs a) {
         if (seg == 0 && lane == 0) {
             if (g.mode == kModeHash) g.table[i] = a.hashes[k];
             a.force[g.page_base + i] = 0;
+            if (a.mark) a.mark[k] = 1;
         }
     }
 }

@@ -138,10 +138,12 @@ struct crum_image {
     std::atomic<int> busy{0};
     int result = 0;
     std::string error;
+    int sessions = 0;  // open lazy-restore sessions reading this image
 };
 
 struct crum_ctx {
     int device = 0;
+    crum_restore_session *session = nullptr;  // open lazy restore (blocks other state changes)
     int sms = 148;
     uint64_t chunk = kDefaultChunk;
     std::vector<HostRegion> regs;
@@ -258,6 +260,12 @@ namespace {
         return CRUM_E_CUDA;                                                                   \
     }                                                                                         \
     CK(cudaSetDevice(c->device))
+
+#define NOT_IN_SESSION(c)                                                                     \
+    if ((c)->session) {                                                                       \
+        set_detail("a lazy restore session is open (crum_restore_end first)");               \
+        return CRUM_E_BUSY;                                                                   \
+    }
 
 Launch launch_of(crum_ctx *c, cudaStream_t s) { return Launch{s, c->sms, &c->launches}; }
 
@@ -778,6 +786,7 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
 
 int crum_destroy(crum_ctx *c) {
     if (!c) return CRUM_E_INVAL;
+    NOT_IN_SESSION(c);
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     for (auto &h : c->regs) cudaFree(h.shadow);
@@ -836,6 +845,7 @@ int crum_destroy(crum_ctx *c) {
 int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page_size, uint32_t mode,
                          uint32_t *region_id_out) {
     ENTER(ctx);
+    NOT_IN_SESSION(c);
     if (!ptr || !region_id_out || bytes == 0) {
         set_detail("null pointer or zero bytes");
         return CRUM_E_INVAL;
@@ -919,6 +929,7 @@ int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page
 
 int crum_unregister_region(crum_ctx *ctx, uint32_t id) {
     ENTER(ctx);
+    NOT_IN_SESSION(c);
     uint32_t idx;
     if (!find_region(c, id, &idx)) {
         set_detail("no region %u", id);
@@ -1010,7 +1021,7 @@ int crum_image_create(crum_ctx *ctx, uint64_t cap, crum_image **out) {
     if (!out) return CRUM_E_INVAL;
     crum_image *im = new (std::nothrow) crum_image{nullptr, cap, 0, c->device};
     if (!im) return CRUM_E_NOMEM;
-    if (cudaHostAlloc(reinterpret_cast<void **>(&im->host), cap ? cap : 1, cudaHostAllocDefault) != cudaSuccess) {
+    if (cudaHostAlloc(reinterpret_cast<void **>(&im->host), cap ? cap : 1, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
         cudaGetLastError();
         delete im;
         set_detail("cudaHostAlloc(%llu) failed", (unsigned long long)cap);
@@ -1039,6 +1050,10 @@ int crum_image_data(const crum_image *img, void **data, uint64_t *len, uint64_t 
 
 int crum_image_destroy(crum_image *img) {
     if (!img) return CRUM_E_INVAL;
+    if (img->sessions) {
+        set_detail("a lazy restore session reads this image");
+        return CRUM_E_BUSY;
+    }
     if (img->writer.joinable()) img->writer.join();
     cudaSetDevice(img->device);
     cudaFreeHost(img->host);
@@ -1148,6 +1163,7 @@ int crum_image_load(crum_ctx *ctx, const char *path, crum_image **out) {
 // ---------------------------------------------------------------------------
 int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
     ENTER(ctx);
+    NOT_IN_SESSION(c);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool timing = c->timing_cfg;
     int st;
@@ -1180,6 +1196,7 @@ int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
 int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capacity, void *stream,
                                   uint32_t flags, crum_report *rep) {
     ENTER(ctx);
+    NOT_IN_SESSION(c);
     if (!dev_image || (flags & ~CRUM_FULL) || (reinterpret_cast<uintptr_t>(dev_image) & 255)) {
         set_detail("bad device image pointer (must be 256-byte aligned) or flags");
         return CRUM_E_INVAL;
@@ -1291,12 +1308,14 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
 // ---------------------------------------------------------------------------
 int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_t flags, crum_report *rep) {
     ENTER(ctx);
+    NOT_IN_SESSION(c);
     if (!img || (flags & ~CRUM_FULL)) {
         set_detail("null image or bad flags");
         return CRUM_E_INVAL;
     }
-    if (img->busy.load()) {
-        set_detail("image is being persisted (alternate two images)");
+    if (img->busy.load() || img->sessions) {
+        set_detail(img->sessions ? "a lazy restore session reads this image"
+                                 : "image is being persisted (alternate two images)");
         return CRUM_E_BUSY;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1496,9 +1515,24 @@ int check_live(crum_ctx *c, const uint8_t *tab, const ParsedImage &p) {
 
 // Common restore body.  host_img != nullptr: image in pinned host memory
 // (payload goes H2D in chunks); else dev_img holds the whole image.
-int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img, uint64_t len, cudaStream_t s,
-                   uint32_t flags, crum_report *rep) {
+// Validated restore: the parsed image, its metadata on the device, and the
+// payload's device address when it is already device-visible.
+struct PreparedRestore {
     ParsedImage p;
+    std::vector<uint8_t> tab;
+    const uint32_t *d_ids = nullptr;
+    const uint64_t *d_hashes = nullptr;
+    const uint8_t *payload_dev = nullptr;
+    uint8_t *d_payload_tmp = nullptr;  // CRUM_VERIFY staging of a host payload (caller frees)
+    DevStats hst{};                    // K, dirty bytes, runs of the image
+};
+
+// Every check of a restore (header, table, metadata CRC, ids, live set,
+// CRUM_VERIFY) before anything is written.  On return the table and tail
+// are in c->d_meta (host image) and the region stats in c->d_rs / c->d_st.
+int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img, uint64_t len, cudaStream_t s,
+                    uint32_t flags, bool timing, PreparedRestore &pr) {
+    ParsedImage &p = pr.p;
     uint8_t hdr[64];
     if (len < 64) {
         set_detail("image shorter than its header");
@@ -1515,7 +1549,8 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
         set_detail("bad image header");
         return st;
     }
-    std::vector<uint8_t> tab(48ull * p.R);
+    std::vector<uint8_t> &tab = pr.tab;
+    tab.resize(48ull * p.R);
     if (p.R) {
         if (host_img) {
             memcpy(tab.data(), host_img + 64, tab.size());
@@ -1531,7 +1566,6 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
     const bool hh = (p.flags & 2u) != 0;
     const uint64_t tail_len = p.image - p.ids_off;
     const uint64_t tab_len = 48ull * p.R;
-    const bool timing = rep != nullptr || c->timing_cfg;
     if (timing) CK(cudaEventRecord(c->ev_t[0], s));
     // table + tail on the device
     const uint8_t *d_table, *d_tail;
@@ -1595,6 +1629,7 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
             set_detail(meta_crc != rd32(hdr + 56) ? "metadata CRC mismatch" : "bad page id list");
             return CRUM_E_CORRUPT;
         }
+        pr.hst = h;
     }
     if ((st = check_live(c, tab.data(), p))) {
         set_detail("image region table does not match the registered regions");
@@ -1619,6 +1654,25 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
             return CRUM_E_CORRUPT;
         }
     }
+    pr.d_ids = d_ids;
+    pr.d_hashes = d_hashes;
+    pr.payload_dev = payload_dev;
+    pr.d_payload_tmp = d_payload_tmp;
+    return CRUM_OK;
+}
+
+int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img, uint64_t len, cudaStream_t s,
+                   uint32_t flags, crum_report *rep) {
+    const bool timing = rep != nullptr || c->timing_cfg;
+    PreparedRestore pr;
+    int st = prepare_restore(c, host_img, dev_img, len, s, flags, timing, pr);
+    if (st) return st;
+    const ParsedImage &p = pr.p;
+    const uint32_t *d_ids = pr.d_ids;
+    const uint64_t *d_hashes = pr.d_hashes;
+    const uint8_t *payload_dev = pr.payload_dev;
+    uint8_t *d_payload_tmp = pr.d_payload_tmp;
+    Launch L = launch_of(c, s);
     if (timing) CK(cudaEventRecord(c->ev_t[1], s));
     const uint64_t units = p.payload >> kSegLog2;
     ScatterArgs sa{};
@@ -1686,6 +1740,7 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
 
 int crum_restore_scatter(crum_ctx *ctx, const crum_image *img, void *stream, uint32_t flags, crum_report *rep) {
     ENTER(ctx);
+    NOT_IN_SESSION(c);
     if (!img || (flags & ~CRUM_VERIFY)) {
         set_detail("null image or bad flags");
         return CRUM_E_INVAL;
@@ -1697,12 +1752,248 @@ int crum_restore_scatter(crum_ctx *ctx, const crum_image *img, void *stream, uin
 int crum_restore_scatter_device(crum_ctx *ctx, const void *dev_image, uint64_t len, void *stream, uint32_t flags,
                                 crum_report *rep) {
     ENTER(ctx);
+    NOT_IN_SESSION(c);
     if (!dev_image || (flags & ~CRUM_VERIFY) || (reinterpret_cast<uintptr_t>(dev_image) & 255)) {
         set_detail("bad device image pointer (must be 256-byte aligned) or flags");
         return CRUM_E_INVAL;
     }
     return restore_common(c, nullptr, static_cast<const uint8_t *>(dev_image), len,
                           static_cast<cudaStream_t>(stream), flags, rep);
+}
+
+// ---------------------------------------------------------------------------
+// Lazy restore with exponential prefetch (sec. 4.2 heuristic, PAPER.md:783-793;
+// SURVEY.md sec. 8(f) #3).  begin validates everything (as crum_restore_scatter)
+// and writes nothing; every fetch is the analog of a read fault on a page of a
+// region: it restores the window the heuristic names, reading the image's
+// slots straight from the mapped pinned image (zero-copy) or, after
+// CRUM_VERIFY, from the verified device copy; end restores what is left.
+// ---------------------------------------------------------------------------
+struct crum_restore_session {
+    crum_ctx *c = nullptr;
+    crum_image *img = nullptr;
+    ParsedImage p;
+    std::vector<uint8_t> tab;
+    const uint8_t *payload_src = nullptr;   // device-visible payload
+    uint8_t *d_payload_tmp = nullptr;       // owned (CRUM_VERIFY copy)
+    uint8_t *d_tail = nullptr;              // owned copy of ids (+ hashes)
+    RegStat *d_rs = nullptr;
+    DevStats *d_st = nullptr;
+    uint8_t *d_done = nullptr;              // per slot: written
+    std::vector<uint8_t> covered;           // per global page: present (fetched)
+    std::vector<uint64_t> window;           // per region: pages the next fault reads
+    DevStats hst{};
+    uint64_t restored = 0, covered_pages = 0;
+};
+
+namespace {
+constexpr uint64_t kSmallRegionPages = 8;  // DESIGN.md reading: "small" = at most 8 pages
+
+void session_free(crum_restore_session *ss) {
+    dev_free(ss->d_payload_tmp);
+    dev_free(ss->d_tail);
+    dev_free(ss->d_rs);
+    dev_free(ss->d_st);
+    dev_free(ss->d_done);
+}
+
+// Scatter slots [klo, khi) of table entry k (all of them uncovered until now).
+int session_scatter_slots(crum_restore_session *ss, uint32_t k, uint64_t klo, uint64_t khi, cudaStream_t s) {
+    crum_ctx *c = ss->c;
+    const RegStat &r = ss->p.rs[k];
+    const uint32_t sh = c->regs[k].log2p - kSegLog2;
+    ScatterArgs sa{};
+    sa.regs = c->d_regs;
+    sa.R = ss->p.R;
+    sa.rs = ss->d_rs;
+    sa.ids = reinterpret_cast<const uint32_t *>(ss->d_tail);
+    sa.hashes = (ss->p.flags & 2u) ? reinterpret_cast<const uint64_t *>(ss->d_tail + round_up(4 * ss->p.K, 8))
+                                   : nullptr;
+    sa.st = ss->d_st;
+    sa.src = ss->payload_src;
+    sa.src_unit0 = 0;
+    sa.force = c->d_force;
+    sa.u_lo = r.unit_base + ((klo - r.first) << sh);
+    sa.u_hi = r.unit_base + ((khi - r.first) << sh);
+    sa.mark = ss->d_done;
+    launch_scatter(launch_of(c, s), sa);
+    CK_LAUNCH();
+    return CRUM_OK;
+}
+}  // namespace
+
+int crum_restore_begin(crum_ctx *ctx, crum_image *img, void *stream, uint32_t flags, crum_restore_session **out) {
+    ENTER(ctx);
+    NOT_IN_SESSION(c);
+    if (!img || !out || (flags & ~CRUM_VERIFY)) {
+        set_detail("null image/out or bad flags");
+        return CRUM_E_INVAL;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PreparedRestore pr;
+    int st = prepare_restore(c, img->host, nullptr, img->len, s, flags, false, pr);
+    if (st) {
+        dev_free(pr.d_payload_tmp);
+        return st;
+    }
+    auto *ss = new (std::nothrow) crum_restore_session;
+    if (!ss) {
+        dev_free(pr.d_payload_tmp);
+        return CRUM_E_NOMEM;
+    }
+    ss->c = c;
+    ss->img = img;
+    ss->p = pr.p;
+    ss->tab = pr.tab;
+    ss->hst = pr.hst;
+    ss->d_payload_tmp = pr.d_payload_tmp;
+    const ParsedImage &p = ss->p;
+    const uint64_t tail_len = p.image - p.ids_off;
+    if ((st = dev_alloc(c, &ss->d_tail, tail_len + 16)) || (st = dev_alloc(c, &ss->d_rs, sizeof(RegStat) * (p.R + 1))) ||
+        (st = dev_alloc(c, &ss->d_st, sizeof(DevStats))) || (st = dev_alloc(c, &ss->d_done, p.K + 1))) {
+        session_free(ss);
+        delete ss;
+        return st;
+    }
+    if (ss->d_payload_tmp) {
+        ss->payload_src = ss->d_payload_tmp;
+    } else {
+        void *dp = nullptr;
+        CK(cudaHostGetDevicePointer(&dp, img->host, 0));
+        ss->payload_src = static_cast<const uint8_t *>(dp) + p.poff;
+    }
+    if (tail_len) CK(cudaMemcpyAsync(ss->d_tail, pr.d_ids, tail_len, cudaMemcpyDeviceToDevice, s));
+    if (p.R) CK(cudaMemcpyAsync(ss->d_rs, c->d_rs, sizeof(RegStat) * p.R, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ss->d_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(ss->d_done, 0, p.K + 1, s));
+    CK(cudaStreamSynchronize(s));
+    ss->covered.assign(c->N, 0);
+    ss->window.assign(p.R, 1);
+    img->sessions++;
+    c->session = ss;
+    *out = ss;
+    return CRUM_OK;
+}
+
+int crum_restore_fetch(crum_restore_session *ss, uint32_t region_id, uint64_t page, void *stream,
+                       uint64_t *covered_out, uint64_t *restored_out) {
+    if (!ss) {
+        set_detail("null session");
+        return CRUM_E_INVAL;
+    }
+    crum_ctx *c = ss->c;
+    if (c->poisoned) {
+        set_detail("context poisoned by an earlier CUDA error");
+        return CRUM_E_CUDA;
+    }
+    CK(cudaSetDevice(c->device));
+    uint32_t k = 0;
+    while (k < c->regs.size() && c->regs[k].id != region_id) ++k;
+    if (k == c->regs.size()) {
+        set_detail("no region %u", region_id);
+        return CRUM_E_NOREGION;
+    }
+    const HostRegion &h = c->regs[k];
+    if (page >= h.n_pages) {
+        set_detail("page %llu outside region %u", (unsigned long long)page, region_id);
+        return CRUM_E_RANGE;
+    }
+    uint64_t newly = 0, restored = 0;
+    uint8_t *cov = ss->covered.data() + h.page_base;
+    if (!cov[page]) {
+        // the window of this fault (sec. 4.2): whole small region; otherwise
+        // `window` pages from the faulting one, clamped at the region end
+        uint64_t lo = 0, hi = h.n_pages;
+        if (h.n_pages > kSmallRegionPages) {
+            lo = page;
+            hi = page + std::min(ss->window[k], h.n_pages - page);
+            if (ss->window[k] < (1ull << 62)) ss->window[k] *= 2;
+        }
+        const RegStat &r = ss->p.rs[k];
+        const uint8_t *ids = ss->img->host + ss->p.ids_off;
+        auto id_at = [&](uint64_t slot) { return (uint64_t)rd32(ids + 4 * slot); };
+        // first slot of the region whose page id is >= x
+        auto lower = [&](uint64_t x) {
+            uint64_t a = r.first, b = r.first + r.n_dirty;
+            while (a < b) {
+                const uint64_t m = (a + b) / 2;
+                if (id_at(m) < x) a = m + 1;
+                else b = m;
+            }
+            return a;
+        };
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        for (uint64_t x = lo; x < hi;) {
+            if (cov[x]) {
+                ++x;
+                continue;
+            }
+            uint64_t y = x;
+            while (y < hi && !cov[y]) cov[y++] = 1;
+            newly += y - x;
+            const uint64_t klo = lower(x), khi = lower(y);
+            if (khi > klo) {
+                int st = session_scatter_slots(ss, k, klo, khi, s);
+                if (st) return st;
+                restored += khi - klo;
+            }
+            x = y;
+        }
+        ss->covered_pages += newly;
+        ss->restored += restored;
+    }
+    if (covered_out) *covered_out = newly;
+    if (restored_out) *restored_out = restored;
+    return CRUM_OK;
+}
+
+int crum_restore_end(crum_restore_session *ss, void *stream, crum_report *rep) {
+    if (!ss) {
+        set_detail("null session");
+        return CRUM_E_INVAL;
+    }
+    crum_ctx *c = ss->c;
+    int st = CRUM_OK;
+    if (!c->poisoned && cudaSetDevice(c->device) == cudaSuccess) {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (ss->restored < ss->p.K) {
+            // every slot not yet written, in one launch (written ones skipped)
+            ScatterArgs sa{};
+            sa.regs = c->d_regs;
+            sa.R = ss->p.R;
+            sa.rs = ss->d_rs;
+            sa.ids = reinterpret_cast<const uint32_t *>(ss->d_tail);
+            sa.hashes = (ss->p.flags & 2u)
+                            ? reinterpret_cast<const uint64_t *>(ss->d_tail + round_up(4 * ss->p.K, 8))
+                            : nullptr;
+            sa.st = ss->d_st;
+            sa.src = ss->payload_src;
+            sa.force = c->d_force;
+            sa.u_lo = 0;
+            sa.u_hi = ss->p.payload >> kSegLog2;
+            sa.skip = ss->d_done;
+            launch_scatter(launch_of(c, s), sa);
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            set_detail("lazy restore end: %s", cudaGetErrorString(e));
+            c->poisoned = true;
+            st = CRUM_E_CUDA;
+        }
+    } else {
+        st = CRUM_E_CUDA;
+    }
+    if (rep) {
+        memset(rep, 0, sizeof *rep);
+        fill_report(c, ss->hst, rep);
+        rep->image_bytes = ss->p.image;
+    }
+    session_free(ss);
+    ss->img->sessions--;
+    c->session = nullptr;
+    delete ss;
+    return st;
 }
 
 int crum_last_report(crum_ctx *ctx, crum_report *rep) {
