@@ -45,8 +45,8 @@ enum {
 };
 
 enum { ORC_MODE_COMPARE = 0, ORC_MODE_HASH = 1, ORC_MODE_TRACKED = 2 };
-enum { ORC_FULL = 1u, ORC_VERIFY = 2u };
-enum { ORC_IMG_FULL = 1u, ORC_IMG_HAS_HASHES = 2u };
+enum { ORC_FULL = 1u, ORC_VERIFY = 2u, ORC_COMPRESS = 4u };
+enum { ORC_IMG_FULL = 1u, ORC_IMG_HAS_HASHES = 2u, ORC_IMG_COMPRESSED = 4u };
 
 #define ORC_MIN_PAGE 4096ull
 #define ORC_MAX_PAGE (2ull << 20)
@@ -73,6 +73,7 @@ typedef struct {
 /* An open lazy restore (sec. 4.2 read-fault heuristic applied to restart). */
 typedef struct {
     const uint8_t *img;  /* the validated image (caller keeps it alive) */
+    uint8_t *upay;       /* decoded payload of a compressed image (owned), or NULL */
     uint8_t **present;   /* per region, per page: read in already */
     uint64_t *window;    /* per region: pages the next fault reads */
     uint8_t *written;    /* per slot: restored already */
@@ -275,6 +276,7 @@ void orc_destroy(orc_ctx *c)
         free(c->sess->present);
         free(c->sess->window);
         free(c->sess->written);
+        free(c->sess->upay);
         free(c->sess);
     }
     for (uint32_t k = 0; k < c->n; ++k) free_region(&c->r[k]);
@@ -463,8 +465,87 @@ int orc_image_required_bytes(orc_ctx *c, uint64_t max_dirty, uint64_t *out)
         if (c->r[k].page_size > maxp) maxp = c->r[k].page_size;
     }
     if (K < N && K * maxp < payload) payload = K * maxp;
-    *out = payload_offset_for(c->n) + payload + tail_bytes_for(K, any_hash_region(c));
+    /* + the unit-size table a compressed image carries (reading Z2) */
+    *out = payload_offset_for(c->n) + payload + tail_bytes_for(K, any_hash_region(c)) +
+           round_up(2 * (payload / 4096), 8);
     return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Unit codec of compressed images (readings  */
+/* Z1-Z2 in DESIGN.md; the paper compresses with gzip -1 / LZ4 on the */
+/* CPU, and names no codec for this path).          */
+/* A 4096-byte unit is 1024 little-endian 32-bit words w[0..1023].    */
+/* Word j is predicted by w[j-2] (by 0 for j < 2); L is the set of j  */
+/* with w[j] != prediction.  The encoding of the unit is:             */
+/*   |L| == 0                 -> nothing (0 bytes; the unit is zero)  */
+/*   128 + 4|L| < 4096        -> a 128-byte bitmap (bit j of byte j/8 */
+/*                               set iff j in L) then w[j], j in L    */
+/*                               ascending, little-endian             */
+/*   otherwise                -> the 4096 raw bytes                   */
+/* ------------------------------------------------------------------ */
+#define ORC_UNIT 4096ull
+#define ORC_UNIT_WORDS 1024ull
+
+static uint32_t unit_word(const uint8_t *u, uint64_t j) { return rd32(u + 4 * j); }
+
+static int z_literal(const uint8_t *u, uint64_t j)
+{
+    uint32_t pred = j < 2 ? 0u : unit_word(u, j - 2);
+    return unit_word(u, j) != pred;
+}
+
+/* Encode one unit into out (room for 4096 bytes); returns the encoded size. */
+uint64_t orc_z_encode(const uint8_t *u, uint8_t *out)
+{
+    uint64_t n = 0;
+    for (uint64_t j = 0; j < ORC_UNIT_WORDS; ++j) n += (uint64_t)z_literal(u, j);
+    if (n == 0) return 0;
+    if (128 + 4 * n >= ORC_UNIT) {
+        memcpy(out, u, ORC_UNIT);
+        return ORC_UNIT;
+    }
+    memset(out, 0, 128);
+    uint64_t pos = 128;
+    for (uint64_t j = 0; j < ORC_UNIT_WORDS; ++j) {
+        if (!z_literal(u, j)) continue;
+        out[j / 8] |= (uint8_t)(1u << (j % 8));
+        wr32(out + pos, unit_word(u, j));
+        pos += 4;
+    }
+    return pos;
+}
+
+/* A valid encoded size: 0, 4096, or 128 + 4n with 1 <= n < 992. */
+static int z_size_ok(uint64_t cs)
+{
+    return cs == 0 || cs == ORC_UNIT || (cs >= 132 && cs < ORC_UNIT && cs % 4 == 0);
+}
+
+/* Decode one unit of encoded size cs from in; 0 if the encoding is
+ * inconsistent (bitmap population != literal count). */
+int orc_z_decode(const uint8_t *in, uint64_t cs, uint8_t *u)
+{
+    if (!z_size_ok(cs)) return 0;
+    if (cs == ORC_UNIT) {
+        memcpy(u, in, ORC_UNIT);
+        return 1;
+    }
+    memset(u, 0, ORC_UNIT);
+    if (cs == 0) return 1;
+    uint64_t pos = 128;
+    for (uint64_t j = 0; j < ORC_UNIT_WORDS; ++j) {
+        uint32_t w;
+        if (in[j / 8] & (1u << (j % 8))) {
+            if (pos + 4 > cs) return 0;
+            w = rd32(in + pos);
+            pos += 4;
+        } else {
+            w = j < 2 ? 0u : unit_word(u, j - 2);
+        }
+        wr32(u + 4 * j, w);
+    }
+    return pos == cs;
 }
 
 /* Checkpoint drain as an incremental gather (sec. 3.4, PAPER.md:547-551;
@@ -475,7 +556,7 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
                           orc_report *rep)
 {
     if (c && c->sess) return ORC_E_BUSY;
-    if (!c || !img || (flags & ~ORC_FULL)) return ORC_E_INVAL;
+    if (!c || !img || (flags & ~(ORC_FULL | ORC_COMPRESS))) return ORC_E_INVAL;
     const uint32_t R = c->n;
     uint64_t N = total_pages(c);
     /* Step 1: the listed pages (global order: region table order, page index). */
@@ -495,9 +576,39 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
         }
     }
     const int has_hashes = any_hash_region(c);
+    const int z = (flags & ORC_COMPRESS) != 0;
     const uint64_t poff = payload_offset_for(R);
-    const uint64_t ids_off = poff + payload;
-    const uint64_t total = ids_off + tail_bytes_for(K, has_hashes);
+    /* Compressed images (readings Z1-Z2): the slots are laid out as usual,
+     * then every 4 KiB unit is encoded; the payload is the encoded units back
+     * to back, zero-padded to a multiple of 4096; the tail gains the u16
+     * encoded size of every unit. */
+    const uint64_t U = payload / ORC_UNIT;
+    uint8_t *zbuf = NULL;
+    uint16_t *zsz = NULL;
+    uint64_t zbytes = 0;
+    if (z) {
+        uint8_t *upay = (uint8_t *)calloc(payload ? payload : 1, 1);
+        uint64_t pb = 0;
+        for (uint32_t k = 0; k < R; ++k) {
+            orc_region *g = &c->r[k];
+            for (uint64_t i = 0; i < g->n_pages; ++i) {
+                if (!listed[k][i]) continue;
+                memcpy(upay + pb, g->cur + i * g->page_size, page_len(g, i));
+                pb += g->page_size;
+            }
+        }
+        zbuf = (uint8_t *)malloc(payload ? payload : 1);
+        zsz = (uint16_t *)malloc(U ? 2 * U : 2);
+        for (uint64_t u = 0; u < U; ++u) {
+            uint64_t cs = orc_z_encode(upay + u * ORC_UNIT, zbuf + zbytes);
+            zsz[u] = (uint16_t)(cs == ORC_UNIT ? 4096 : cs);
+            zbytes += cs;
+        }
+        free(upay);
+    }
+    const uint64_t pay_field = z ? round_up(zbytes, ORC_UNIT) : payload;
+    const uint64_t ids_off = poff + pay_field;
+    const uint64_t total = ids_off + tail_bytes_for(K, has_hashes) + (z ? round_up(2 * U, 8) : 0);
     if (rep) {
         rep->scanned_pages = N;
         rep->scanned_bytes = scanned_bytes;
@@ -509,17 +620,20 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
     if (cap < total) {
         for (uint32_t k = 0; k < R; ++k) free(listed[k]);
         free(listed);
+        free(zbuf);
+        free(zsz);
         return ORC_E_CAPACITY;
     }
     /* Step 2: assemble. */
     memset(img, 0, total);
     memcpy(img, "CRUM", 4);
     wr32(img + 4, 1);
-    wr32(img + 8, ((flags & ORC_FULL) ? ORC_IMG_FULL : 0) | (has_hashes ? ORC_IMG_HAS_HASHES : 0));
+    wr32(img + 8, ((flags & ORC_FULL) ? ORC_IMG_FULL : 0) | (has_hashes ? ORC_IMG_HAS_HASHES : 0) |
+                      (z ? ORC_IMG_COMPRESSED : 0));
     wr32(img + 12, R);
     wr64(img + 16, K);
     wr64(img + 24, poff);
-    wr64(img + 32, payload);
+    wr64(img + 32, pay_field);
     wr64(img + 40, ids_off);
     wr64(img + 48, total);
     uint8_t *tab = img + 64;
@@ -533,7 +647,7 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
             if (!listed[k][i]) continue;
             wr32(ids + 4 * slot, (uint32_t)i);
             if (has_hashes) wr64(hashes + 8 * slot, g->mode == ORC_MODE_HASH ? page_hash(g, i) : 0);
-            memcpy(img + poff + pbyte, g->cur + i * g->page_size, page_len(g, i));
+            if (!z) memcpy(img + poff + pbyte, g->cur + i * g->page_size, page_len(g, i));
             pbyte += g->page_size;
             slot++;
             nd++;
@@ -546,6 +660,16 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
         wr64(e + 24, g->n_pages);
         wr64(e + 32, nd);
         wr64(e + 40, first);
+    }
+    if (z) {
+        memcpy(img + poff, zbuf, zbytes);
+        uint8_t *zt = ids + tail_bytes_for(K, has_hashes);
+        for (uint64_t u = 0; u < U; ++u) {
+            zt[2 * u] = (uint8_t)zsz[u];
+            zt[2 * u + 1] = (uint8_t)(zsz[u] >> 8);
+        }
+        free(zbuf);
+        free(zsz);
     }
     wr32(img + 56, crc32_two(tab, 48 * (uint64_t)R, ids, total - ids_off));
     wr32(img + 60, orc_crc32(img, 60));
@@ -560,18 +684,26 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
 }
 
 /* Every check a restore makes before writing anything (reading Q11). */
-static int validate_image(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t flags)
+/* *upay_out: for a compressed image, the decoded payload (malloc'ed, the
+ * caller frees it); NULL otherwise (the payload is read in place). */
+static int validate_image(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t flags, uint8_t **upay_out)
 {
+    *upay_out = NULL;
     if (len < 64 || memcmp(img, "CRUM", 4) != 0) return ORC_E_CORRUPT;
     if (orc_crc32(img, 60) != rd32(img + 60)) return ORC_E_CORRUPT;
     const uint32_t version = rd32(img + 4), iflags = rd32(img + 8), R = rd32(img + 12);
     const uint64_t K = rd64(img + 16), poff = rd64(img + 24), payload = rd64(img + 32),
                    ids_off = rd64(img + 40), total = rd64(img + 48);
-    if (version != 1 || (iflags & ~3u) != 0) return ORC_E_CORRUPT;
+    if (version != 1 || (iflags & ~7u) != 0) return ORC_E_CORRUPT;
     const int has_hashes = (iflags & ORC_IMG_HAS_HASHES) != 0;
+    const int z = (iflags & ORC_IMG_COMPRESSED) != 0;
     if (K > ORC_MAX_TOTAL_PAGES || R > 0x7fffffffu) return ORC_E_CORRUPT;
-    if (poff != payload_offset_for(R) || payload > (1ull << 62) || ids_off != poff + payload ||
-        total != ids_off + tail_bytes_for(K, has_hashes))
+    if (poff != payload_offset_for(R) || payload > (1ull << 62) || ids_off != poff + payload)
+        return ORC_E_CORRUPT;
+    if (!z && total != ids_off + tail_bytes_for(K, has_hashes)) return ORC_E_CORRUPT;
+    /* compressed: the exact length needs the unit count (from the table) */
+    if (z && (payload % ORC_UNIT != 0 || total < ids_off + tail_bytes_for(K, has_hashes) ||
+              total > ids_off + tail_bytes_for(K, has_hashes) + (1ull << 62)))
         return ORC_E_CORRUPT;
     if (len < total) return ORC_E_CORRUPT;
     const uint8_t *tab = img + 64;
@@ -602,7 +734,23 @@ static int validate_image(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t
         sum += nd;
         pay += nd * ps;
     }
-    if (sum != K || pay != payload || any_hash != has_hashes) return ORC_E_CORRUPT;
+    if (sum != K || (!z && pay != payload) || any_hash != has_hashes) return ORC_E_CORRUPT;
+    /* Compressed: one valid u16 size per 4 KiB unit, summing to the payload
+     * length before its zero padding (readings Z1-Z2). */
+    const uint8_t *zt = ids + tail_bytes_for(K, has_hashes);
+    const uint64_t U = pay / ORC_UNIT;
+    if (z) {
+        if (total != ids_off + tail_bytes_for(K, has_hashes) + round_up(2 * U, 8)) return ORC_E_CORRUPT;
+        uint64_t zb = 0;
+        for (uint64_t u = 0; u < U; ++u) {
+            uint64_t cs = (uint64_t)zt[2 * u] | ((uint64_t)zt[2 * u + 1] << 8);
+            if (!z_size_ok(cs)) return ORC_E_CORRUPT;
+            zb += cs;
+        }
+        for (uint64_t q = 2 * U; q < round_up(2 * U, 8); ++q)
+            if (zt[q] != 0) return ORC_E_CORRUPT;
+        if (round_up(zb, ORC_UNIT) != payload) return ORC_E_CORRUPT;
+    }
     /* The table must describe the live registered set (reading Q11). */
     if (R != c->n) return ORC_E_MISMATCH;
     for (uint32_t k = 0; k < R; ++k) {
@@ -612,6 +760,23 @@ static int validate_image(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t
             rd64(e + 16) != g->page_size || rd64(e + 24) != g->n_pages)
             return ORC_E_MISMATCH;
     }
+    /* Compressed: decode every unit (a size that disagrees with its bitmap
+     * is CORRUPT) before anything is written. */
+    const uint8_t *pl = img + poff;
+    if (z) {
+        uint8_t *upay = (uint8_t *)malloc(pay ? pay : 1);
+        uint64_t zb = 0;
+        for (uint64_t u = 0; u < U; ++u) {
+            uint64_t cs = (uint64_t)zt[2 * u] | ((uint64_t)zt[2 * u + 1] << 8);
+            if (!orc_z_decode(img + poff + zb, cs, upay + u * ORC_UNIT)) {
+                free(upay);
+                return ORC_E_CORRUPT;
+            }
+            zb += cs;
+        }
+        pl = upay;
+        *upay_out = upay;
+    }
     /* CRUM_VERIFY: recompute the hash of every hash-mode slot. */
     if (flags & ORC_VERIFY) {
         uint64_t pbyte = 0;
@@ -620,8 +785,11 @@ static int validate_image(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t
             uint64_t first = rd64(tab + 48 * (uint64_t)k + 40), nd = rd64(tab + 48 * (uint64_t)k + 32);
             for (uint64_t j = 0; j < nd; ++j) {
                 if (g->mode == ORC_MODE_HASH &&
-                    orc_xxh3_64(img + poff + pbyte, g->page_size) != rd64(hashes + 8 * (first + j)))
+                    orc_xxh3_64(pl + pbyte, g->page_size) != rd64(hashes + 8 * (first + j))) {
+                    free(*upay_out);
+                    *upay_out = NULL;
                     return ORC_E_CORRUPT;
+                }
                 pbyte += g->page_size;
             }
         }
@@ -648,10 +816,12 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
 {
     if (!c || !img || (flags & ~ORC_VERIFY)) return ORC_E_INVAL;
     if (c->sess) return ORC_E_BUSY;
-    int st = validate_image(c, img, len, flags);
+    uint8_t *upay;
+    int st = validate_image(c, img, len, flags, &upay);
     if (st) return st;
     const uint32_t R = rd32(img + 12);
     const uint64_t K = rd64(img + 16), poff = rd64(img + 24), ids_off = rd64(img + 40), total = rd64(img + 48);
+    const uint8_t *pl = upay ? upay : img + poff;
     const uint8_t *tab = img + 64;
     const uint8_t *ids = img + ids_off;
     const uint8_t *hashes = ids + round_up(4 * K, 8);
@@ -663,7 +833,7 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
         scanned += g->bytes;
         for (uint64_t j = 0; j < nd; ++j) {
             uint64_t i = rd32(ids + 4 * (first + j));
-            restore_slot(g, i, img + poff + pbyte, hashes, first + j);
+            restore_slot(g, i, pl + pbyte, hashes, first + j);
             dirty_bytes += page_len(g, i);
             if (j == 0 || rd32(ids + 4 * (first + j - 1)) + 1 != i) runs++;
             pbyte += g->page_size;
@@ -677,6 +847,7 @@ int orc_restore_scatter(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t f
         rep->dirty_runs = runs;
         rep->image_bytes = total;
     }
+    free(upay);
     return ORC_OK;
 }
 
@@ -698,10 +869,12 @@ int orc_restore_begin(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t fla
 {
     if (!c || !img || (flags & ~ORC_VERIFY)) return ORC_E_INVAL;
     if (c->sess) return ORC_E_BUSY;
-    int st = validate_image(c, img, len, flags);
+    uint8_t *upay;
+    int st = validate_image(c, img, len, flags, &upay);
     if (st) return st;
     orc_session *s = (orc_session *)calloc(1, sizeof *s);
     s->img = img;
+    s->upay = upay;
     s->present = (uint8_t **)calloc(c->n ? c->n : 1, sizeof(uint8_t *));
     s->window = (uint64_t *)calloc(c->n ? c->n : 1, sizeof(uint64_t));
     for (uint32_t k = 0; k < c->n; ++k) {
@@ -738,7 +911,8 @@ static void session_restore_slot(orc_ctx *c, uint32_t k, uint64_t i, uint64_t sl
     const uint8_t *img = c->sess->img;
     const uint64_t K = rd64(img + 16), poff = rd64(img + 24), ids_off = rd64(img + 40);
     const uint8_t *hashes = img + ids_off + round_up(4 * K, 8);
-    restore_slot(&c->r[k], i, img + poff + slot_payload_offset(c, img, k, slot), hashes, slot);
+    const uint8_t *pl = c->sess->upay ? c->sess->upay : img + poff;
+    restore_slot(&c->r[k], i, pl + slot_payload_offset(c, img, k, slot), hashes, slot);
     c->sess->written[slot] = 1;
 }
 
@@ -812,6 +986,7 @@ int orc_restore_end(orc_ctx *c, orc_report *rep)
     free(s->present);
     free(s->window);
     free(s->written);
+    free(s->upay);
     free(s);
     c->sess = NULL;
     return ORC_OK;

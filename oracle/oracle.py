@@ -26,7 +26,7 @@ _lib = None
 OK, E_INVAL, E_OVERLAP, E_NOREGION, E_RANGE, E_NOMEM, E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY = (
     0, -1, -2, -3, -4, -5, -6, -7, -8, -9)
 MODE_COMPARE, MODE_HASH, MODE_TRACKED = 0, 1, 2
-FULL, VERIFY = 1, 2
+FULL, VERIFY, COMPRESS = 1, 2, 4
 
 
 class OracleError(RuntimeError):
@@ -78,6 +78,10 @@ def lib():
         L.orc_get_hashes.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
         L.orc_get_mirror.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
         L.orc_page_hash.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, u64p]
+        L.orc_z_encode.argtypes = [C.c_void_p, C.c_void_p]
+        L.orc_z_encode.restype = C.c_uint64
+        L.orc_z_decode.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
+        L.orc_z_decode.restype = C.c_int
         L.orc_restore_begin.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32]
         L.orc_restore_fetch.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, u64p, u64p]
         L.orc_restore_end.argtypes = [C.c_void_p, C.POINTER(Report)]
@@ -104,6 +108,23 @@ def crc32(data) -> int:
     a = np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data
     a = np.ascontiguousarray(a, dtype=np.uint8)
     return int(lib().orc_crc32(_ptr(a), a.nbytes))
+
+
+def z_encode(unit) -> bytes:
+    """The oracle's unit codec (readings Z1-Z2): encode 4096 bytes."""
+    a = np.ascontiguousarray(np.frombuffer(bytes(unit), dtype=np.uint8))
+    assert a.nbytes == 4096
+    out = np.zeros(4096, dtype=np.uint8)
+    n = int(lib().orc_z_encode(_ptr(a), _ptr(out)))
+    return out[:n].tobytes()
+
+
+def z_decode(enc: bytes):
+    """Decode one unit; None if the encoding is invalid."""
+    a = np.frombuffer(bytes(enc) + b"\0", dtype=np.uint8)
+    out = np.zeros(4096, dtype=np.uint8)
+    ok = lib().orc_z_decode(_ptr(a), len(enc), _ptr(out))
+    return out.tobytes() if ok else None
 
 
 def aligned_empty(nbytes: int, align: int = 256) -> np.ndarray:

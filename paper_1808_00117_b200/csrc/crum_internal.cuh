@@ -136,9 +136,6 @@ struct GatherArgs {
     uint64_t dst_unit0;
     uint8_t *force;
     uint64_t u_lo, u_hi;
-    const uint8_t *skip;   // lazy restore: slots with skip[k] != 0 are left alone (may be null)
-    uint8_t *mark;         // lazy restore: mark[k] = 1 for every slot written (may be null;
-                           // never the same array as skip within one launch)
 };
 
 // Metadata CRC + tail copy + header (last block).

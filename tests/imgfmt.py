@@ -29,7 +29,22 @@ def slot_bytes(cur: np.ndarray, page_size: int, i: int) -> bytes:
     return seg + b"\0" * (page_size - len(seg))
 
 
-def build_image(regions, listed, full=False) -> bytes:
+def z_encode_unit(unit: bytes) -> bytes:
+    """DESIGN.md readings Z1-Z2, restated with numpy: 1024 LE u32 words, word j
+    predicted by word j-2 (0 for j < 2); literals = mispredicted words;
+    0 literals -> b""; 128 + 4n < 4096 -> LSB-first bitmap + literals; else raw."""
+    w = np.frombuffer(unit, dtype="<u4")
+    pred = np.concatenate([np.zeros(2, dtype="<u4"), w[:-2]])
+    lit = w != pred
+    n = int(lit.sum())
+    if n == 0:
+        return b""
+    if 128 + 4 * n >= 4096:
+        return bytes(unit)
+    return np.packbits(lit, bitorder="little").tobytes() + w[lit].astype("<u4").tobytes()
+
+
+def build_image(regions, listed, full=False, compress=False) -> bytes:
     """regions: list of dicts {id, mode, cur (np.uint8 array), page_size};
     listed: list (same order) of ascending page-index lists."""
     R = len(regions)
@@ -52,9 +67,15 @@ def build_image(regions, listed, full=False) -> bytes:
     ids += b"\0" * (round_up(4 * K, 8) - 4 * K)
     pay = b"".join(payload)
     tail = ids + hashes
+    if compress:
+        units = [z_encode_unit(pay[u:u + 4096]) for u in range(0, len(pay), 4096)]
+        zs = b"".join(struct.pack("<H", len(e)) for e in units)
+        tail += zs + b"\0" * (round_up(len(zs), 8) - len(zs))
+        pay = b"".join(units)
+        pay += b"\0" * (round_up(len(pay), 4096) - len(pay))
     ids_off = poff + len(pay)
     total = ids_off + len(tail)
-    flags = (1 if full else 0) | (2 if has_hashes else 0)
+    flags = (1 if full else 0) | (2 if has_hashes else 0) | (4 if compress else 0)
     hdr0 = struct.pack("<4sIIIQQQQQI", b"CRUM", 1, flags, R, K, poff, len(pay), ids_off, total,
                        zlib.crc32(table + tail))
     hdr = hdr0 + struct.pack("<I", zlib.crc32(hdr0))
@@ -71,9 +92,14 @@ def parse_image(img: bytes):
     hashes = []
     if flags & 2 and K:
         hashes = list(struct.unpack_from(f"<{K}Q", img, ids_off + round_up(4 * K, 8)))
+    zsizes = []
+    if flags & 4:
+        U = sum(e[5] * e[3] for e in table) // 4096
+        zoff = ids_off + round_up(4 * K, 8) + (8 * K if flags & 2 else 0)
+        zsizes = list(struct.unpack_from(f"<{U}H", img, zoff)) if U else []
     return dict(magic=magic, version=ver, flags=flags, R=R, K=K, poff=poff, payload_bytes=paylen,
                 ids_off=ids_off, image_bytes=total, meta_crc=mcrc, header_crc=hcrc, table=table, ids=ids,
-                hashes=hashes)
+                hashes=hashes, zsizes=zsizes)
 
 
 def meta_positions(img: bytes):
