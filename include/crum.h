@@ -83,8 +83,17 @@ typedef enum {
 
 /* Call flags. */
 enum {
-    CRUM_FULL = 1u << 0,   /* gather: list every page (the paper's full drain) */
-    CRUM_VERIFY = 1u << 1  /* restore: recompute and check every hash-mode slot before writing */
+    CRUM_FULL = 1u << 0,    /* gather: list every page (the paper's full drain) */
+    CRUM_VERIFY = 1u << 1,  /* restore: recompute and check every hash-mode slot before writing */
+    CRUM_COMPRESS = 1u << 2 /* gather: compressed image (readings Z1-Z2; the paper's
+                               in-memory compression before writing):
+                               every 4 KiB payload unit is encoded on the GPU -- 1024 LE u32
+                               words, word j predicted by word j-2; 0 mispredicted words -> 0
+                               bytes; else a 128-byte bitmap + the mispredicted words if shorter
+                               than 4096, else raw -- and only encoded bytes cross the host link
+                               (the encoder stores straight into the mapped pinned image).
+                               Restore decodes transparently.  Image flag bit2; the tail gains a
+                               u16 encoded size per unit after the hashes (padded to 8). */
 };
 
 typedef struct crum_ctx crum_ctx;     /* one per (process, CUDA device) */
@@ -116,11 +125,14 @@ typedef struct {
     double t_copy_ms;        /* A4: host-link copy (D2H for gather, H2D for restore) */
     double t_total_ms;       /* whole call, first enqueue to completion */
     uint32_t path;           /* bit0 CRUM_PATH_FUSED: single-pass detect+compact+gather kernel ran
-                                (t_detect_ms then covers all three, t_gather_ms is 0) */
+                                (t_detect_ms then covers all three, t_gather_ms is 0);
+                                bit1 CRUM_PATH_COMPRESSED: compressed gather (t_compact_ms includes
+                                the encoded-size pass, t_gather_ms is encode + commit, including
+                                the host-link stores for a pinned image; t_copy_ms is 0) */
     uint32_t reserved;
 } crum_report;
 
-enum { CRUM_PATH_FUSED = 1u << 0 };
+enum { CRUM_PATH_FUSED = 1u << 0, CRUM_PATH_COMPRESSED = 1u << 1 };
 
 /* ---------------------------------------------------------------------------
  * Context.  crum_create binds to CUDA device `device` (cudaSetDevice is
@@ -190,7 +202,8 @@ CRUM_API int crum_region_tracker(crum_ctx *ctx, uint32_t region_id, crum_tracker
 CRUM_API int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_pages_out);
 
 /* Upper bound on the image size when at most max_dirty_pages are listed
- * (pass UINT64_MAX for "every page"). */
+ * (pass UINT64_MAX for "every page"), plain or CRUM_COMPRESS (it includes the
+ * 2 bytes per 4 KiB unit of a compressed image's unit-size table). */
 CRUM_API int crum_image_required_bytes(crum_ctx *ctx, uint64_t max_dirty_pages, uint64_t *bytes_out);
 
 /* Pinned host images (cudaHostAlloc).  crum_image_import copies `len` bytes

@@ -28,10 +28,10 @@ OK = 0
 E_INVAL, E_OVERLAP, E_NOREGION, E_RANGE, E_NOMEM = -1, -2, -3, -4, -5
 E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY, E_DEVICE, E_CUDA, E_IO = -6, -7, -8, -9, -10, -11, -12
 MODE_COMPARE, MODE_HASH = 0, 1
-FULL, VERIFY = 1, 2
+FULL, VERIFY, COMPRESS = 1, 2, 4
 MODE_TRACKED = 2
 CFG_TIMING = 1
-PATH_FUSED = 1
+PATH_FUSED, PATH_COMPRESSED = 1, 2
 PERSIST_FSYNC = 1
 EXPORT_FORCE, EXPORT_HASHES, EXPORT_MIRROR = 0, 1, 2
 ALL_PAGES = (1 << 64) - 1

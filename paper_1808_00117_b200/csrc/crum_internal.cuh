@@ -67,7 +67,7 @@ struct DevStats {
     uint64_t capacity;       // device image capacity (gather)
     uint32_t status;         // kStOk / kStCapacity / kStCorrupt
     uint32_t crc_acc;        // XOR of per-chunk raw CRC terms (meta CRC)
-    uint32_t img_flags;      // header flags (bit0 FULL, bit1 HAS_HASHES)
+    uint32_t img_flags;      // header flags (bit0 FULL, bit1 HAS_HASHES, bit2 COMPRESSED)
     uint32_t n_regions;
     uint32_t meta_crc;       // final zlib CRC-32 of table || ids || hashes
     uint32_t pad0;
@@ -149,6 +149,7 @@ struct CrcArgs {
     DevStats *st_host;      // mapped pinned copy of the final stats, or nullptr
     uint32_t *done;
     X2N x2n;
+    const uint16_t *zsz;    // compressed image: per-unit encoded sizes (tail after the hashes)
 };
 
 // A6: scatter units [u_lo, u_hi); unit u read from src + (u - src_unit0)*4096.
@@ -223,6 +224,17 @@ void launch_crc_check(const Launch &L, const uint8_t *table, uint64_t tab, const
 void launch_restore_validate(const Launch &L, const DevRegion *tregs, uint32_t R, const RegStat *rs,
                              const uint32_t *ids, const uint64_t *hashes, uint64_t K, DevStats *st);
 void launch_scatter(const Launch &L, const ScatterArgs &a);
+
+// Compressed images (readings Z1-Z2): encoded sizes, their scan
+// (kZScanBlock units per local block), encode + commit, decode.
+constexpr uint32_t kZScanBlock = 2048;
+void launch_zsize(const Launch &L, const GatherArgs &a, uint16_t *zsz, uint64_t max_units);
+void launch_zscan(const Launch &L, const uint16_t *zsz, DevStats *st, uint32_t *zloc, uint64_t *zblk,
+                  uint64_t max_units, int gather, uint8_t *img, uint64_t capacity);
+void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, const uint64_t *zblk, uint8_t *img,
+                   uint64_t max_units);
+void launch_zdecode(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
+                    const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t units);
 void launch_mark_pages(const Launch &L, uint8_t *force, uint64_t n_pages, const uint32_t *pages, uint64_t n);
 void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag,
                          uint8_t *out);

@@ -532,7 +532,11 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
     crc_smem_init(sm, a.x2n);
     const uint64_t K = st->K, R = st->n_regions;
     const bool hh = (st->img_flags & 2u) != 0;
-    const uint64_t tabw = 12 * R, idsw = round_up(4 * K, 8) / 4, nwords = tabw + idsw + (hh ? 2 * K : 0);
+    const bool zz = (st->img_flags & 4u) != 0;  // compressed: + the u16 unit sizes
+    const uint64_t U = st->total_units;
+    const uint64_t zw = zz ? round_up(2 * U, 8) / 4 : 0;
+    const uint64_t tabw = 12 * R, idsw = round_up(4 * K, 8) / 4, hw = hh ? 2 * K : 0;
+    const uint64_t nwords = tabw + idsw + hw + zw;
     uint8_t *tail = a.tail ? a.tail : a.head + st->ids_off;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
@@ -542,6 +546,11 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
     if (hh) {
         uint64_t *th = reinterpret_cast<uint64_t *>(tail + 4 * idsw);
         for (uint64_t k = tid; k < K; k += nth) th[k] = a.lhash[k];
+    }
+    const uint16_t *zsz = a.zsz;
+    if (zz) {
+        uint16_t *tz = reinterpret_cast<uint16_t *>(tail + 4 * (idsw + hw));
+        for (uint64_t q = tid; q < 2 * zw; q += nth) tz[q] = q < U ? zsz[q] : (uint16_t)0;
     }
     // runs of consecutive page ids (a run starts at a region's page 0 or after a gap)
     uint64_t runs = 0;
@@ -559,7 +568,10 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
         w -= tabw;
         if (w < idsw) return w < K ? lids[w] : 0u;
         w -= idsw;
-        return (uint32_t)(lhash[w >> 1] >> (32 * (w & 1)));
+        if (w < hw) return (uint32_t)(lhash[w >> 1] >> (32 * (w & 1)));
+        w -= hw;
+        const uint64_t q = 2 * w;
+        return (q < U ? (uint32_t)zsz[q] : 0u) | ((q + 1 < U ? (uint32_t)zsz[q + 1] : 0u) << 16);
     };
     const uint32_t acc = crc_stream_terms(word, nwords, sm);
     if ((threadIdx.x & 31) == 0 && acc) atomicXor(&st->crc_acc, acc);
@@ -1022,6 +1034,296 @@ int fused_blocks_per_sm() {
 
 void launch_fused_compare(const Launch &L, const FusedArgs &a, int blocks) {
     k_fused_compare<<<blocks, kFusedThreads, 0, L.stream>>>(a);
+    ++*L.counter;
+}
+
+
+// ===========================================================================
+// Compressed images (readings Z1-Z2).
+// A 4 KiB unit is 1024 LE u32 words; word j is predicted by word j-2 (0 for
+// j < 2).  Encoding: no mispredicted word -> 0 bytes; 128 + 4n < 4096 ->
+// 128-byte bitmap of the n mispredicted words + those words; else raw.
+// One warp per unit: lane l holds words 32i + l (i = 0..31), so the
+// prediction is a shfl_up by 2 (lanes 0/1 take lanes 30/31 of the previous
+// row) and the bitmap rows are 32 ballots.
+// ===========================================================================
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// w[i] = word 32i + lane of the unit at p (len logical bytes, rest zero).
+__device__ __forceinline__ void z_load_unit(const uint8_t *p, uint64_t len, uint32_t lane, uint32_t (&w)[32]) {
+    if (len >= kSegBytes && ((reinterpret_cast<uintptr_t>(p) & 3) == 0)) {
+        const uint32_t *q = reinterpret_cast<const uint32_t *>(p);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) w[i] = __ldg(q + 32 * i + lane);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const uint64_t b = 4ull * (32 * i + lane);
+            uint32_t v = 0;
+            for (int k = 0; k < 4; ++k)
+                if (b + k < len) v |= (uint32_t)p[b + k] << (8 * k);
+            w[i] = v;
+        }
+    }
+}
+
+// Bitmap rows of the mispredicted words; returns their count.
+__device__ __forceinline__ uint32_t z_bitmap(const uint32_t (&w)[32], uint32_t lane, uint32_t (&bm)[32]) {
+    uint32_t c30 = 0, c31 = 0, n = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const uint32_t up = __shfl_up_sync(0xffffffffu, w[i], 2);
+        const uint32_t pred = lane >= 2 ? up : (lane == 0 ? c30 : c31);
+        c30 = __shfl_sync(0xffffffffu, w[i], 30);
+        c31 = __shfl_sync(0xffffffffu, w[i], 31);
+        bm[i] = __ballot_sync(0xffffffffu, w[i] != pred);
+        n += __popc(bm[i]);
+    }
+    return n;
+}
+
+__device__ __forceinline__ uint32_t z_size_of(uint32_t n) {
+    return n == 0 ? 0u : (128u + 4u * n < kSegBytes ? 128u + 4u * n : (uint32_t)kSegBytes);
+}
+
+// Unit u of the gather -> (region, page, byte offset, logical length).
+struct ZUnit {
+    DevRegion g;
+    uint64_t gid, i, off, len, seg;
+};
+__device__ __forceinline__ ZUnit z_unit(const GatherArgs &a, uint64_t k_lo, uint64_t k_hi, uint64_t u) {
+    ZUnit z;
+    const uint64_t k = slot_of_unit(a.sunit, k_lo, k_hi, u);
+    z.gid = a.gids[k];
+    z.g = a.regs[region_of_page(a.regs, a.R, z.gid)];
+    z.seg = u - a.sunit[k];
+    z.i = z.gid - z.g.page_base;
+    z.off = (z.i << z.g.log2p) + (z.seg << kSegLog2);
+    z.len = z.g.bytes > z.off ? min((uint64_t)kSegBytes, z.g.bytes - z.off) : 0;
+    return z;
+}
+
+// Pass 1: encoded size of every unit of the gather.
+__global__ void __launch_bounds__(256) k_zsize(GatherArgs a, uint16_t *zsz) {
+    const DevStats *st = a.st;
+    if (st->status != kStOk) return;
+    const uint64_t k_lo = a.rb[0].k, k_hi = a.rb[1].k, U = a.rb[1].units;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+        const ZUnit z = z_unit(a, k_lo, k_hi, u);
+        uint32_t w[32], bm[32];
+        z_load_unit(z.g.base + z.off, z.len, lane, w);
+        const uint32_t n = z_bitmap(w, lane, bm);
+        if (lane == 0) zsz[u] = (uint16_t)z_size_of(n);
+    }
+}
+
+// Local exclusive prefix of the sizes inside blocks of kZScanBlock units.
+// validate: a size other than 0, 4096 or 128 + 4n (1 <= n < 992) is CORRUPT.
+__global__ void __launch_bounds__(256) k_zscan_local(const uint16_t *zsz, DevStats *st, uint32_t *zloc,
+                                                    uint64_t *zblk, int validate) {
+    const uint64_t U = st->total_units;
+    const uint64_t base = (uint64_t)blockIdx.x * kZScanBlock;
+    if (base >= U) return;
+    constexpr uint32_t per = kZScanBlock / 256;
+    uint32_t v[per];
+    uint64_t sum = 0;
+    bool bad = false;
+#pragma unroll
+    for (uint32_t j = 0; j < per; ++j) {
+        const uint64_t u = base + threadIdx.x * per + j;
+        v[j] = u < U ? zsz[u] : 0u;
+        bad |= !(v[j] == 0 || v[j] == kSegBytes || (v[j] >= 132 && v[j] < kSegBytes && (v[j] & 3) == 0));
+        sum += v[j];
+    }
+    uint64_t tot;
+    uint64_t ex = block_excl_scan(sum, &tot);
+#pragma unroll
+    for (uint32_t j = 0; j < per; ++j) {
+        const uint64_t u = base + threadIdx.x * per + j;
+        if (u < U) zloc[u] = (uint32_t)ex;
+        ex += v[j];
+    }
+    if (threadIdx.x == 0) zblk[blockIdx.x] = tot;
+    if (validate && bad) st->status = kStCorrupt;
+}
+
+// Exclusive scan of the block totals (one block).  Gather: set the
+// compressed image's sizes, check capacity, zero the payload padding of img.
+// Restore: the sizes must sum to the header's payload length before padding,
+// and the size table's padding must be zero.
+__global__ void __launch_bounds__(1024) k_zscan_top(uint64_t *zblk, DevStats *st, int gather, uint8_t *img,
+                                                   uint64_t capacity, const uint16_t *zsz) {
+    const uint64_t U = st->total_units;
+    const uint64_t nblk = (U + kZScanBlock - 1) / kZScanBlock;
+    uint64_t carry = 0;
+    for (uint64_t b0 = 0; b0 < nblk; b0 += blockDim.x) {
+        const uint64_t b = b0 + threadIdx.x;
+        const uint64_t v = b < nblk ? zblk[b] : 0;
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan(v, &tot);
+        if (b < nblk) zblk[b] = carry + ex;
+        carry += tot;
+    }
+    const uint64_t Z = carry;
+    const uint64_t zpay = round_up(Z, kSegBytes);
+    if (gather) {
+        if (st->status != kStOk) return;
+        const uint64_t K = st->K;
+        const uint64_t ids_off = st->poff + zpay;
+        const uint64_t image = ids_off + round_up(4 * K, 8) + ((st->img_flags & 2u) ? 8 * K : 0) + round_up(2 * U, 8);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            st->payload_bytes = zpay;
+            st->ids_off = ids_off;
+            st->image_bytes = image;
+            st->img_flags |= 4u;
+            if (image > capacity) st->status = kStCapacity;
+        }
+        if (img && image <= capacity)
+            for (uint64_t b = st->poff + Z + threadIdx.x; b < st->poff + zpay; b += blockDim.x) img[b] = 0;
+    } else if (threadIdx.x == 0) {
+        bool bad = zpay != st->payload_bytes;
+        for (uint64_t q = U; q < round_up(U, 4); ++q) bad |= zsz[q] != 0;
+        if (bad) st->status = kStCorrupt;
+    }
+}
+
+// Pass 2: encode every unit at its offset and commit it (as k_gather).
+__global__ void __launch_bounds__(256) k_zwrite(GatherArgs a, const uint32_t *zloc, const uint64_t *zblk,
+                                               uint8_t *img) {
+    const DevStats *st = a.st;
+    if (st->status != kStOk) return;
+    const uint64_t k_lo = a.rb[0].k, k_hi = a.rb[1].k, U = a.rb[1].units;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint8_t *payload = img ? img + st->poff : nullptr;
+    for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+        const ZUnit z = z_unit(a, k_lo, k_hi, u);
+        if (payload) {
+            uint32_t w[32], bm[32];
+            z_load_unit(z.g.base + z.off, z.len, lane, w);
+            const uint32_t n = z_bitmap(w, lane, bm);
+            const uint32_t cs = z_size_of(n);
+            uint32_t *out = reinterpret_cast<uint32_t *>(payload + zblk[u / kZScanBlock] + zloc[u]);
+            if (cs == kSegBytes) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) out[32 * i + lane] = w[i];
+            } else if (cs) {
+                const uint32_t lt = lanemask_lt();
+                uint32_t pos = 0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    if (lane == (uint32_t)i) out[i] = bm[i];
+                    if ((bm[i] >> lane) & 1u) out[32 + pos + __popc(bm[i] & lt)] = w[i];
+                    pos += __popc(bm[i]);
+                }
+            }
+        }
+        uint8_t *dst_mir = (z.g.mode == kModeCompare) ? z.g.mirror + z.off : nullptr;
+        if (dst_mir) copy_unit(z.g.base + z.off, z.len, z.g.aligned32 != 0, nullptr, dst_mir, lane);
+        if (z.seg == 0 && lane == 0) {
+            if (z.g.mode == kModeHash) z.g.table[z.i] = a.newhash[z.gid];
+            a.force[z.gid] = 0;
+        }
+    }
+}
+
+// Restore: decode every unit of the compressed payload at src into dst
+// (unit u at dst + 4096u).  A bitmap whose population disagrees with the
+// unit's size is CORRUPT.
+__global__ void __launch_bounds__(256) k_zdecode(const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
+                                                const uint64_t *zblk, DevStats *st, uint8_t *dst) {
+    if (st->status != kStOk) return;
+    const uint64_t U = st->total_units;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+        const uint32_t cs = zsz[u];
+        const uint32_t *in = reinterpret_cast<const uint32_t *>(src + zblk[u / kZScanBlock] + zloc[u]);
+        uint32_t *out = reinterpret_cast<uint32_t *>(dst + (u << kSegLog2));
+        if (cs == kSegBytes) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) out[32 * i + lane] = in[32 * i + lane];
+            continue;
+        }
+        if (cs == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) out[32 * i + lane] = 0u;
+            continue;
+        }
+        const uint32_t mine = in[lane];
+        uint32_t n = __popc(mine);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+        if (128u + 4u * n != cs) {
+            if (lane == 0) st->status = kStCorrupt;
+            continue;
+        }
+        const uint32_t lt = lanemask_lt();
+        uint32_t pos = 0, c30 = 0, c31 = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const uint32_t row = __shfl_sync(0xffffffffu, mine, i);
+            bool f = (row >> lane) & 1u;
+            uint32_t v = f ? in[32 + pos + __popc(row & lt)] : 0u;
+            pos += __popc(row);
+            // nearest literal at or before this word in its parity class
+#pragma unroll
+            for (int d = 2; d < 32; d <<= 1) {
+                const uint32_t v2 = __shfl_up_sync(0xffffffffu, v, d);
+                const bool f2 = __shfl_up_sync(0xffffffffu, (uint32_t)f, d) != 0;
+                if (lane >= (uint32_t)d && !f) {
+                    v = v2;
+                    f = f2;
+                }
+            }
+            if (!f) v = (lane & 1) ? c31 : c30;
+            c30 = __shfl_sync(0xffffffffu, v, 30);
+            c31 = __shfl_sync(0xffffffffu, v, 31);
+            out[32 * i + lane] = v;
+        }
+    }
+}
+
+static unsigned z_grid(const Launch &L, uint64_t units) {
+    uint64_t blocks = (units + 7) / 8;
+    const uint64_t cap = (uint64_t)L.sms * 8;
+    if (blocks > cap) blocks = cap;
+    return (unsigned)(blocks ? blocks : 1);
+}
+
+void launch_zsize(const Launch &L, const GatherArgs &a, uint16_t *zsz, uint64_t max_units) {
+    if (!max_units) return;
+    k_zsize<<<z_grid(L, max_units), 256, 0, L.stream>>>(a, zsz);
+    ++*L.counter;
+}
+
+void launch_zscan(const Launch &L, const uint16_t *zsz, DevStats *st, uint32_t *zloc, uint64_t *zblk,
+                  uint64_t max_units, int gather, uint8_t *img, uint64_t capacity) {
+    const uint64_t nblk = (max_units + kZScanBlock - 1) / kZScanBlock;
+    k_zscan_local<<<(unsigned)(nblk ? nblk : 1), 256, 0, L.stream>>>(zsz, st, zloc, zblk, gather ? 0 : 1);
+    k_zscan_top<<<1, 1024, 0, L.stream>>>(zblk, st, gather, img, capacity, zsz);
+    *L.counter += 2;
+}
+
+void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, const uint64_t *zblk, uint8_t *img,
+                   uint64_t max_units) {
+    if (!max_units) return;
+    k_zwrite<<<z_grid(L, max_units), 256, 0, L.stream>>>(a, zloc, zblk, img);
+    ++*L.counter;
+}
+
+void launch_zdecode(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
+                    const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t units) {
+    if (!units) return;
+    k_zdecode<<<z_grid(L, units), 256, 0, L.stream>>>(src, zsz, zloc, zblk, st, dst);
     ++*L.counter;
 }
 

@@ -198,6 +198,11 @@ struct crum_ctx {
     RangeTotals *d_rb = nullptr;   // kMaxRanges + 1
     RangeTotals *h_rb = nullptr;   // pinned, mapped mirror
     uint32_t *d_done = nullptr;    // [0] compaction, [1] crc
+    // compressed images: per-unit encoded sizes, local offsets, block offsets
+    uint16_t *d_zsz = nullptr;
+    uint32_t *d_zloc = nullptr;
+    uint64_t *d_zblk = nullptr;
+    uint64_t z_cap = 0;            // units the three arrays hold
     DevStats *d_st = nullptr;
     DevStats *h_st = nullptr;      // pinned, mapped
     DevStats *dh_st = nullptr;     // its device address
@@ -506,6 +511,21 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
     return CRUM_OK;
 }
 
+// Scratch of compressed gathers / restores for `units` 4 KiB units.
+int ensure_z(crum_ctx *c, uint64_t units) {
+    if (c->z_cap >= units && c->d_zsz) return CRUM_OK;
+    dev_free(c->d_zsz);
+    dev_free(c->d_zloc);
+    dev_free(c->d_zblk);
+    c->z_cap = 0;
+    int st;
+    if ((st = dev_alloc(c, &c->d_zsz, 2 * (units + 8))) || (st = dev_alloc(c, &c->d_zloc, 4 * (units + 8))) ||
+        (st = dev_alloc(c, &c->d_zblk, 8 * (units / kZScanBlock + 2))))
+        return st;
+    c->z_cap = units;
+    return CRUM_OK;
+}
+
 int ensure_ring(crum_ctx *c) {
     if (c->ring_cap >= c->chunk) return CRUM_OK;
     for (int i = 0; i < kRing; ++i) dev_free(c->d_ring[i]);
@@ -606,6 +626,7 @@ CrcArgs crc_args(crum_ctx *c, uint8_t *head, uint8_t *tail) {
     a.done = c->d_done + 1;
     a.st_host = c->dh_st;
     a.x2n = crc_tables().x2n;
+    a.zsz = c->d_zsz;
     return a;
 }
 
@@ -628,7 +649,7 @@ GatherArgs gather_args(crum_ctx *c, uint32_t ci, uint8_t *dst, uint64_t dst_unit
     return a;
 }
 
-uint64_t crc_max_len(const crum_ctx *c) { return 48ull * c->regs.size() + 12 * c->N + 8; }
+uint64_t crc_max_len(const crum_ctx *c) { return 48ull * c->regs.size() + 12 * c->N + 2 * c->max_units + 16; }
 
 void fill_report(crum_ctx *c, const DevStats &h, crum_report *rep) {
     rep->scanned_pages = c->N;
@@ -815,6 +836,9 @@ int crum_destroy(crum_ctx *c) {
     dev_free(c->d_tregs);
     dev_free(c->d_rb);
     dev_free(c->d_done);
+    dev_free(c->d_zsz);
+    dev_free(c->d_zloc);
+    dev_free(c->d_zblk);
     dev_free(c->d_st);
     dev_free(c->d_meta);
     for (int i = 0; i < kRing; ++i) dev_free(c->d_ring[i]);
@@ -1012,7 +1036,10 @@ int crum_image_required_bytes(crum_ctx *ctx, uint64_t max_dirty, uint64_t *out) 
         maxp = std::max(maxp, h.page_size);
     }
     if (K < c->N && K * maxp < payload) payload = K * maxp;
-    *out = payload_offset_for(c->regs.size()) + payload + tail_bytes_for(K, c->any_hash);
+    // + the unit-size table of a compressed image (an encoded unit is never
+    // longer than the unit)
+    *out = payload_offset_for(c->regs.size()) + payload + tail_bytes_for(K, c->any_hash) +
+           round_up(2 * (payload >> kSegLog2), 8);
     return CRUM_OK;
 }
 
@@ -1161,6 +1188,66 @@ int crum_image_load(crum_ctx *ctx, const char *path, crum_image **out) {
 // ---------------------------------------------------------------------------
 // A7: sync shadow = detect + compact + commit (no image)
 // ---------------------------------------------------------------------------
+namespace {
+// CRUM_COMPRESS (readings Z1-Z2): detect, compact (+ table),
+// encoded size of every unit and their scan (+ the image's sizes, capacity
+// check), then the metadata CRC (+ tail incl. unit sizes, header) on the side
+// stream beside encode + commit.  `img` is a device buffer or the mapped
+// device address of a pinned host image (then the encoder's stores cross the
+// host link directly: only encoded bytes move).  Capacity failures commit
+// nothing (every later kernel checks the status).
+int enqueue_gather_z(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, bool full, bool timing) {
+    int st;
+    if ((st = ensure_z(c, c->max_units))) return st;
+    uint8_t *head = capacity >= payload_offset_for(c->regs.size()) ? img : nullptr;
+    if (timing) CK(cudaEventRecord(c->ev_t[0], s));
+    if ((st = next_tag(c, s))) return st;
+    CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
+    enqueue_detect(c, s, c->all, full);
+    if (timing) CK(cudaEventRecord(c->ev_t[1], s));
+    enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, full, UINT64_MAX, head));
+    Launch L = launch_of(c, s);
+    const GatherArgs ga = gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX);
+    launch_zsize(L, ga, c->d_zsz, c->max_units);
+    launch_zscan(L, c->d_zsz, c->d_st, c->d_zloc, c->d_zblk, c->max_units, 1, head, capacity);
+    CK_LAUNCH();
+    if (timing) CK(cudaEventRecord(c->ev_t[2], s));
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    launch_crc_meta(launch_of(c, c->aux), crc_args(c, head, nullptr), crc_max_len(c));
+    CK(cudaEventRecord(c->ev_join, c->aux));
+    launch_zwrite(L, ga, c->d_zloc, c->d_zblk, head, c->max_units);
+    if (timing) CK(cudaEventRecord(c->ev_t[3], s));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    CK_LAUNCH();
+    if (timing) CK(cudaEventRecord(c->ev_t[4], s));
+    CK(cudaEventRecord(c->ev_done, s));
+    c->last_kind = kLastDevGather;
+    c->last_timed = timing;
+    return CRUM_OK;
+}
+
+// Report + status of a finished compressed gather.
+int finish_gather_z(crum_ctx *c, cudaStream_t s, uint64_t capacity, crum_report *rep, DevStats *out) {
+    CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const DevStats h = *c->h_st;
+    if (out) *out = h;
+    if (rep) {
+        memset(rep, 0, sizeof *rep);
+        fill_report(c, h, rep);
+        fill_times(c, rep);
+        rep->path |= CRUM_PATH_COMPRESSED;
+    }
+    if (h.status == kStCapacity) {
+        set_detail("image needs %llu bytes, capacity %llu", (unsigned long long)h.image_bytes,
+                   (unsigned long long)capacity);
+        return CRUM_E_CAPACITY;
+    }
+    return CRUM_OK;
+}
+}  // namespace
+
 int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
     ENTER(ctx);
     NOT_IN_SESSION(c);
@@ -1197,7 +1284,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
                                   uint32_t flags, crum_report *rep) {
     ENTER(ctx);
     NOT_IN_SESSION(c);
-    if (!dev_image || (flags & ~CRUM_FULL) || (reinterpret_cast<uintptr_t>(dev_image) & 255)) {
+    if (!dev_image || (flags & ~(CRUM_FULL | CRUM_COMPRESS)) || (reinterpret_cast<uintptr_t>(dev_image) & 255)) {
         set_detail("bad device image pointer (must be 256-byte aligned) or flags");
         return CRUM_E_INVAL;
     }
@@ -1219,6 +1306,10 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     // The single-pass kernel is opt-in (CRUM_FUSED=1): measured on B200 it ties
     // the multi-kernel path on C2 and trails it by ~2% on C3.
     static const bool fused_env = getenv("CRUM_FUSED") != nullptr;
+    if (flags & CRUM_COMPRESS) {
+        if ((st = enqueue_gather_z(c, s, img, capacity, full, timing))) return st;
+        return rep ? finish_gather_z(c, s, capacity, rep, nullptr) : CRUM_OK;
+    }
     if (c->fused_ok && fused_env && !full && capacity >= worst) {
         // single pass: detect + compact + gather + commit in one kernel, then
         // the metadata CRC / tail / header
@@ -1309,7 +1400,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
 int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_t flags, crum_report *rep) {
     ENTER(ctx);
     NOT_IN_SESSION(c);
-    if (!img || (flags & ~CRUM_FULL)) {
+    if (!img || (flags & ~(CRUM_FULL | CRUM_COMPRESS))) {
         set_detail("null image or bad flags");
         return CRUM_E_INVAL;
     }
@@ -1320,6 +1411,17 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool full = flags & CRUM_FULL;
+    if (flags & CRUM_COMPRESS) {
+        // encoded straight into the pinned image through its mapped address
+        void *dimg = nullptr;
+        CK(cudaHostGetDevicePointer(&dimg, img->host, 0));
+        int st = enqueue_gather_z(c, s, static_cast<uint8_t *>(dimg), img->cap, full, true);
+        if (st) return st;
+        DevStats h;
+        st = finish_gather_z(c, s, img->cap, rep, &h);
+        if (st == CRUM_OK) img->len = h.image_bytes;
+        return st;
+    }
     int st = ensure_ring(c);
     if (st) return st;
     uint64_t worst;
@@ -1444,6 +1546,7 @@ namespace {
 struct ParsedImage {
     uint32_t flags, R;
     uint64_t K, poff, payload, ids_off, image;
+    uint64_t upayload = 0;  // payload bytes before compression (= payload unless flag bit2)
     std::vector<RegStat> rs;
     std::vector<DevRegion> tregs;
 };
@@ -1461,10 +1564,15 @@ int parse_header(const uint8_t *hdr, uint64_t len, ParsedImage &p) {
     p.payload = rd64(hdr + 32);
     p.ids_off = rd64(hdr + 40);
     p.image = rd64(hdr + 48);
-    if (version != 1 || (p.flags & ~3u)) return CRUM_E_CORRUPT;
+    if (version != 1 || (p.flags & ~7u)) return CRUM_E_CORRUPT;
     if (p.K > kMaxTotalPages || p.R > 0x7fffffffu) return CRUM_E_CORRUPT;
-    if (p.poff != payload_offset_for(p.R) || p.payload > (1ull << 62) || p.ids_off != p.poff + p.payload ||
-        p.image != p.ids_off + tail_bytes_for(p.K, p.flags & 2u))
+    if (p.poff != payload_offset_for(p.R) || p.payload > (1ull << 62) || p.ids_off != p.poff + p.payload)
+        return CRUM_E_CORRUPT;
+    const uint64_t tail = tail_bytes_for(p.K, p.flags & 2u);
+    if (!(p.flags & 4u) && p.image != p.ids_off + tail) return CRUM_E_CORRUPT;
+    // compressed: the exact length needs the unit count (parse_table)
+    if ((p.flags & 4u) && ((p.payload & (kSegBytes - 1)) || p.image < p.ids_off + tail ||
+                           p.image - p.ids_off - tail > (1ull << 62)))
         return CRUM_E_CORRUPT;
     if (len < p.image) return CRUM_E_CORRUPT;
     return CRUM_OK;
@@ -1497,7 +1605,11 @@ int parse_table(const uint8_t *tab, ParsedImage &p) {
         sum += nd;
         pay += nd * ps;
     }
-    if (sum != p.K || pay != p.payload || any_hash != ((p.flags & 2u) != 0)) return CRUM_E_CORRUPT;
+    const bool z = (p.flags & 4u) != 0;
+    if (sum != p.K || (!z && pay != p.payload) || any_hash != ((p.flags & 2u) != 0)) return CRUM_E_CORRUPT;
+    if (z && p.image != p.ids_off + tail_bytes_for(p.K, p.flags & 2u) + round_up(2 * (pay >> kSegLog2), 8))
+        return CRUM_E_CORRUPT;
+    p.upayload = pay;
     return CRUM_OK;
 }
 
@@ -1607,7 +1719,7 @@ int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img
     hs.payload_bytes = p.payload;
     hs.ids_off = p.ids_off;
     hs.image_bytes = p.image;
-    hs.total_units = p.payload >> kSegLog2;
+    hs.total_units = p.upayload >> kSegLog2;
     hs.img_flags = p.flags;
     hs.n_regions = p.R;
     *c->h_st = hs;
@@ -1619,6 +1731,14 @@ int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img
     Launch L = launch_of(c, s);
     if (tab_len + tail_len) launch_crc_check(L, d_table, tab_len, d_tail, tail_len, c->d_st, crc_tables().x2n);
     launch_restore_validate(L, c->d_tregs, p.R, c->d_rs, d_ids, d_hashes, p.K, c->d_st);
+    // compressed: every unit size valid, sizes summing to the payload (readings Z1-Z2)
+    const bool zimg = (p.flags & 4u) != 0;
+    const uint64_t zunits = p.upayload >> kSegLog2;
+    const uint16_t *d_zsz = reinterpret_cast<const uint16_t *>(d_tail + tail_bytes_for(p.K, hh));
+    if (zimg) {
+        if ((st = ensure_z(c, zunits))) return st;
+        launch_zscan(L, d_zsz, c->d_st, c->d_zloc, c->d_zblk, zunits, 0, nullptr, 0);
+    }
     CK_LAUNCH();
     CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1635,13 +1755,35 @@ int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img
         set_detail("image region table does not match the registered regions");
         return st;
     }
-    // CRUM_VERIFY: hash every hash-mode slot before writing anything
     uint8_t *d_payload_tmp = nullptr;
     const uint8_t *payload_dev = dev_img ? dev_img + p.poff : nullptr;
-    if ((flags & CRUM_VERIFY) && c->any_hash && p.K) {
+    // compressed: decode every unit into device memory first (a bitmap that
+    // disagrees with its unit's size is CORRUPT); the pinned image is read in
+    // place through its mapped address, so only encoded bytes cross the link
+    if (zimg) {
+        const uint8_t *src = payload_dev;
         if (host_img) {
-            if ((st = dev_alloc(c, &d_payload_tmp, p.payload))) return st;
-            CK(cudaMemcpyAsync(d_payload_tmp, host_img + p.poff, p.payload, cudaMemcpyHostToDevice, s));
+            void *dp = nullptr;
+            CK(cudaHostGetDevicePointer(&dp, const_cast<uint8_t *>(host_img), 0));
+            src = static_cast<const uint8_t *>(dp) + p.poff;
+        }
+        if ((st = dev_alloc(c, &d_payload_tmp, p.upayload))) return st;
+        launch_zdecode(L, src, d_zsz, c->d_zloc, c->d_zblk, c->d_st, d_payload_tmp, zunits);
+        CK_LAUNCH();
+        CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (c->h_st->status != kStOk) {
+            cudaFree(d_payload_tmp);
+            set_detail("compressed unit whose bitmap disagrees with its size");
+            return CRUM_E_CORRUPT;
+        }
+        payload_dev = d_payload_tmp;
+    }
+    // CRUM_VERIFY: hash every hash-mode slot before writing anything
+    if ((flags & CRUM_VERIFY) && c->any_hash && p.K) {
+        if (!payload_dev) {
+            if ((st = dev_alloc(c, &d_payload_tmp, p.upayload))) return st;
+            CK(cudaMemcpyAsync(d_payload_tmp, host_img + p.poff, p.upayload, cudaMemcpyHostToDevice, s));
             payload_dev = d_payload_tmp;
         }
         launch_verify_hash(L, c->d_regs, p.R, c->d_rs, d_hashes, payload_dev, p.K, c->d_st);
@@ -1674,7 +1816,7 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
     uint8_t *d_payload_tmp = pr.d_payload_tmp;
     Launch L = launch_of(c, s);
     if (timing) CK(cudaEventRecord(c->ev_t[1], s));
-    const uint64_t units = p.payload >> kSegLog2;
+    const uint64_t units = p.upayload >> kSegLog2;
     ScatterArgs sa{};
     sa.regs = c->d_regs;
     sa.R = p.R;
@@ -1970,7 +2112,7 @@ int crum_restore_end(crum_restore_session *ss, void *stream, crum_report *rep) {
             sa.src = ss->payload_src;
             sa.force = c->d_force;
             sa.u_lo = 0;
-            sa.u_hi = ss->p.payload >> kSegLog2;
+            sa.u_hi = ss->p.upayload >> kSegLog2;
             sa.skip = ss->d_done;
             launch_scatter(launch_of(c, s), sa);
         }
