@@ -57,6 +57,10 @@ def parse():
     ap.add_argument("--page", type=int, default=64 * KiB)
     ap.add_argument("--dirty", type=float, default=0.10)
     ap.add_argument("--region-gib", type=float, default=1.0)
+    ap.add_argument("--compress", action="store_true", help="CRUM_COMPRESS gathers (DESIGN.md Z1-Z2)")
+    ap.add_argument("--content", default="random", choices=["random", "half"],
+                    help="half: the paper's 50%%-random vectors (PAPER.md:907-912): second half of every "
+                         "region one repeated fp32 value; the writer then rewrites one word per dirty page")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -243,6 +247,9 @@ def main():
     S = synth.seed(1) + (rank << 20)
     F = sum(nb for nb, _, _ in specs)
 
+    gflags = crum.COMPRESS if args.compress else 0
+    if args.compress or args.content != "random":
+        desc += f", content {args.content}" + (", compressed images" if args.compress else "")
     ctx = crum.Context(local, timing=True)
     regions = []
     with torch.cuda.stream(stream):
@@ -252,6 +259,8 @@ def main():
             else:
                 t = torch.empty(nb, dtype=torch.uint8, device=dev)
             crum.synth_fill(t, nb, S, r, stream=stream)
+            if args.content == "half":
+                t[nb // 2 // 4 * 4:].view(torch.float32).fill_(0.25)
             regions.append(t)
             ctx.register_region(t, nb, P, mode)
     trackers = [ctx.region_tracker(r + 1) for r in range(len(specs))] if args.mode == "tracked" else None
@@ -281,7 +290,8 @@ def main():
                 crum.synth_write_pages_tracked(regions[r], nb, P, pg, pg.numel(), S, e, r, trackers[r],
                                                stream=stream)
             else:
-                crum.synth_write_pages(regions[r], nb, P, pg, pg.numel(), S, e, r, stream=stream)
+                crum.synth_write_pages(regions[r], nb, P, pg, pg.numel(), S, e, r, args.content == "half",
+                                       stream=stream)
         crum.synth_scrub(scrub, scrub.numel(), stream=stream)
 
     from paper_1808_00117_b200 import coord
@@ -294,9 +304,10 @@ def main():
         """One checkpoint into the device image, stream-asynchronous; with N > 1
         the coordinated all-reduce needs the totals, so the step waits for them."""
         if distributed:
-            return coordinated(lambda: (ctx.checkpoint_gather_device(dimg, cap, stream=stream, report=not async_ok),
+            return coordinated(lambda: (ctx.checkpoint_gather_device(dimg, cap, stream=stream, flags=gflags,
+                                                                     report=not async_ok),
                                         ctx.last_report())[1])
-        ctx.checkpoint_gather_device(dimg, cap, stream=stream, report=not async_ok)
+        ctx.checkpoint_gather_device(dimg, cap, stream=stream, flags=gflags, report=not async_ok)
         return None
 
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -379,10 +390,14 @@ def main():
         "gpu_launches_synth": 2 * args.steps * len(specs),
         "clocks": clk,
     }
+    if args.compress:
+        line["compression"] = {"image_bytes": reps[-1]["image_bytes"], "dirty_bytes": reps[-1]["dirty_bytes"],
+                               "ratio": round(reps[-1]["dirty_bytes"] / max(reps[-1]["image_bytes"], 1), 3),
+                               "codec": "word-repeat (lag-2) unit codec, DESIGN.md Z1-Z2"}
     # ---- e2e: pinned host image, D2H inside the timed region ----
     if not args.no_e2e:
         img = ctx.new_image(cap)
-        ctx.checkpoint_gather(img, stream=stream)
+        ctx.checkpoint_gather(img, stream=stream, flags=gflags)
         e2e_ms, e2e_reps = [], []
         for i in range(max(3, args.steps // 2)):
             epoch += 1
@@ -391,7 +406,7 @@ def main():
             if distributed:
                 dist.barrier()
             t0 = time.perf_counter()
-            e2e_reps.append(coordinated(lambda: ctx.checkpoint_gather(img, stream=stream)))
+            e2e_reps.append(coordinated(lambda: ctx.checkpoint_gather(img, stream=stream, flags=gflags)))
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         te = statistics.median(e2e_ms) / 1e3
         if distributed:
@@ -402,7 +417,8 @@ def main():
                        "d2h_bytes_per_step": e2e_reps[-1]["image_bytes"], "ms_per_step": round(te * 1e3, 3),
                        "note": "crum_checkpoint_gather into pinned host memory, host wall clock per call "
                                "(median); the regions being checkpointed live in HBM by definition",
-                       "link_GBs": round(e2e_reps[-1]["image_bytes"] / max(e2e_reps[-1]["t_copy_ms"], 1e-9) / 1e6, 2)}
+                       "link_GBs": (round(e2e_reps[-1]["image_bytes"] / e2e_reps[-1]["t_copy_ms"] / 1e6, 2)
+                                    if e2e_reps[-1]["t_copy_ms"] > 0 else None)}
         # restore of the last image onto the live regions (H2D inside)
         r_ms = []
         for i in range(3):
@@ -446,7 +462,7 @@ def main():
                 im = (img, img2)[i % 2]
                 im.persist_wait()
                 t0 = time.perf_counter()
-                ctx.checkpoint_gather(im, stream=stream)
+                ctx.checkpoint_gather(im, stream=stream, flags=gflags)
                 pause_ms.append((time.perf_counter() - t0) * 1e3)
                 im.persist(os.path.join(tmpd, f"r{rank}_{i % 2}.crum"))
             img.persist_wait()

@@ -231,8 +231,8 @@ constexpr uint32_t kZScanBlock = 2048;
 void launch_zsize(const Launch &L, const GatherArgs &a, uint16_t *zsz, uint64_t max_units);
 void launch_zscan(const Launch &L, const uint16_t *zsz, DevStats *st, uint32_t *zloc, uint64_t *zblk,
                   uint64_t max_units, int gather, uint8_t *img, uint64_t capacity);
-void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, const uint64_t *zblk, uint8_t *img,
-                   uint64_t max_units);
+void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, const uint64_t *zblk, uint8_t *dst,
+                   int add_poff, uint64_t u_lo, uint64_t u_hi, uint64_t off0);
 void launch_zdecode(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
                     const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t units);
 void launch_mark_pages(const Launch &L, uint8_t *force, uint64_t n_pages, const uint32_t *pages, uint64_t n);

@@ -1173,6 +1173,8 @@ __global__ void __launch_bounds__(1024) k_zscan_top(uint64_t *zblk, DevStats *st
     }
     const uint64_t Z = carry;
     const uint64_t zpay = round_up(Z, kSegBytes);
+    __syncthreads();
+    if (threadIdx.x == 0) zblk[nblk] = Z;  // the encoded length (chunk end of a host gather)
     if (gather) {
         if (st->status != kStOk) return;
         const uint64_t K = st->K;
@@ -1195,16 +1197,19 @@ __global__ void __launch_bounds__(1024) k_zscan_top(uint64_t *zblk, DevStats *st
     }
 }
 
-// Pass 2: encode every unit at its offset and commit it (as k_gather).
+// Pass 2: encode units [u_lo, u_hi) and commit them (as k_gather).  Unit u
+// goes to dst + (add_poff ? poff : 0) + off(u) - off0, off(u) its offset in
+// the compressed payload (dst == nullptr: commit only).
 __global__ void __launch_bounds__(256) k_zwrite(GatherArgs a, const uint32_t *zloc, const uint64_t *zblk,
-                                               uint8_t *img) {
+                                               uint8_t *dst, int add_poff, uint64_t u_lo, uint64_t u_hi,
+                                               uint64_t off0) {
     const DevStats *st = a.st;
     if (st->status != kStOk) return;
-    const uint64_t k_lo = a.rb[0].k, k_hi = a.rb[1].k, U = a.rb[1].units;
+    const uint64_t k_lo = a.rb[0].k, k_hi = a.rb[1].k, U = min(a.rb[1].units, u_hi);
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    uint8_t *payload = img ? img + st->poff : nullptr;
-    for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+    uint8_t *payload = dst ? dst + (add_poff ? st->poff : 0) - off0 : nullptr;
+    for (uint64_t u = u_lo + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < U; u += nwarps) {
         const ZUnit z = z_unit(a, k_lo, k_hi, u);
         if (payload) {
             uint32_t w[32], bm[32];
@@ -1313,10 +1318,10 @@ void launch_zscan(const Launch &L, const uint16_t *zsz, DevStats *st, uint32_t *
     *L.counter += 2;
 }
 
-void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, const uint64_t *zblk, uint8_t *img,
-                   uint64_t max_units) {
-    if (!max_units) return;
-    k_zwrite<<<z_grid(L, max_units), 256, 0, L.stream>>>(a, zloc, zblk, img);
+void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, const uint64_t *zblk, uint8_t *dst,
+                   int add_poff, uint64_t u_lo, uint64_t u_hi, uint64_t off0) {
+    if (u_hi <= u_lo) return;
+    k_zwrite<<<z_grid(L, u_hi - u_lo), 256, 0, L.stream>>>(a, zloc, zblk, dst, add_poff, u_lo, u_hi, off0);
     ++*L.counter;
 }
 

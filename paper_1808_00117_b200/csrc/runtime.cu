@@ -144,6 +144,7 @@ struct crum_image {
 struct crum_ctx {
     int device = 0;
     crum_restore_session *session = nullptr;  // open lazy restore (blocks other state changes)
+    uint32_t last_path = 0;                   // CRUM_PATH_* bits of the last gather
     int sms = 148;
     uint64_t chunk = kDefaultChunk;
     std::vector<HostRegion> regs;
@@ -203,6 +204,12 @@ struct crum_ctx {
     uint32_t *d_zloc = nullptr;
     uint64_t *d_zblk = nullptr;
     uint64_t z_cap = 0;            // units the three arrays hold
+    uint64_t *h_zblk = nullptr;    // pinned host copy of d_zblk (chunk offsets of a host gather)
+    // restore staging kept across calls (grow-only): decoded / verified payload, encoded payload
+    uint8_t *d_rtmp = nullptr;
+    uint64_t rtmp_cap = 0;
+    uint8_t *d_renc = nullptr;
+    uint64_t renc_cap = 0;
     DevStats *d_st = nullptr;
     DevStats *h_st = nullptr;      // pinned, mapped
     DevStats *dh_st = nullptr;     // its device address
@@ -511,30 +518,50 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
     return CRUM_OK;
 }
 
+// Grow-only device buffer.
+int grow(crum_ctx *c, uint8_t **p, uint64_t *cap, uint64_t bytes) {
+    if (*cap >= bytes && *p) return CRUM_OK;
+    dev_free(*p);
+    *cap = 0;
+    int st = dev_alloc(c, p, bytes);
+    if (st) return st;
+    *cap = bytes;
+    return CRUM_OK;
+}
+
 // Scratch of compressed gathers / restores for `units` 4 KiB units.
 int ensure_z(crum_ctx *c, uint64_t units) {
     if (c->z_cap >= units && c->d_zsz) return CRUM_OK;
     dev_free(c->d_zsz);
     dev_free(c->d_zloc);
     dev_free(c->d_zblk);
+    if (c->h_zblk) cudaFreeHost(c->h_zblk);
+    c->h_zblk = nullptr;
     c->z_cap = 0;
     int st;
     if ((st = dev_alloc(c, &c->d_zsz, 2 * (units + 8))) || (st = dev_alloc(c, &c->d_zloc, 4 * (units + 8))) ||
         (st = dev_alloc(c, &c->d_zblk, 8 * (units / kZScanBlock + 2))))
         return st;
+    if (cudaHostAlloc(reinterpret_cast<void **>(&c->h_zblk), 8 * (units / kZScanBlock + 2), cudaHostAllocDefault) !=
+        cudaSuccess) {
+        c->h_zblk = nullptr;
+        set_detail("cudaHostAlloc of the compressed-chunk table failed");
+        return CRUM_E_NOMEM;
+    }
     c->z_cap = units;
     return CRUM_OK;
 }
 
-int ensure_ring(crum_ctx *c) {
-    if (c->ring_cap >= c->chunk) return CRUM_OK;
+int ensure_ring(crum_ctx *c, uint64_t min_bytes = 0) {
+    const uint64_t want = std::max(c->chunk, min_bytes);
+    if (c->ring_cap >= want) return CRUM_OK;
     for (int i = 0; i < kRing; ++i) dev_free(c->d_ring[i]);
     c->ring_cap = 0;
     for (int i = 0; i < kRing; ++i) {
-        int st = dev_alloc(c, &c->d_ring[i], c->chunk);
+        int st = dev_alloc(c, &c->d_ring[i], want);
         if (st) return st;
     }
-    c->ring_cap = c->chunk;
+    c->ring_cap = want;
     return CRUM_OK;
 }
 
@@ -700,6 +727,7 @@ void fill_times(crum_ctx *c, crum_report *rep) {
         default:
             break;
     }
+    rep->path |= c->last_path;
 }
 
 }  // namespace
@@ -838,7 +866,10 @@ int crum_destroy(crum_ctx *c) {
     dev_free(c->d_done);
     dev_free(c->d_zsz);
     dev_free(c->d_zloc);
+    dev_free(c->d_rtmp);
+    dev_free(c->d_renc);
     dev_free(c->d_zblk);
+    if (c->h_zblk) cudaFreeHost(c->h_zblk);
     dev_free(c->d_st);
     dev_free(c->d_meta);
     for (int i = 0; i < kRing; ++i) dev_free(c->d_ring[i]);
@@ -1196,10 +1227,13 @@ namespace {
 // device address of a pinned host image (then the encoder's stores cross the
 // host link directly: only encoded bytes move).  Capacity failures commit
 // nothing (every later kernel checks the status).
-int enqueue_gather_z(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, bool full, bool timing) {
+int finish_gather_z(crum_ctx *c, cudaStream_t s, uint64_t capacity, crum_report *rep, DevStats *out);
+
+// Sizes: detect, compact (+ table into head), encoded sizes and their scan
+// (+ the image's size fields, capacity check, payload padding into head).
+int enqueue_z_sizes(crum_ctx *c, cudaStream_t s, uint8_t *head, uint64_t capacity, bool full, bool timing) {
     int st;
     if ((st = ensure_z(c, c->max_units))) return st;
-    uint8_t *head = capacity >= payload_offset_for(c->regs.size()) ? img : nullptr;
     if (timing) CK(cudaEventRecord(c->ev_t[0], s));
     if ((st = next_tag(c, s))) return st;
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
@@ -1207,16 +1241,26 @@ int enqueue_gather_z(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
     if (timing) CK(cudaEventRecord(c->ev_t[1], s));
     enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, full, UINT64_MAX, head));
     Launch L = launch_of(c, s);
-    const GatherArgs ga = gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX);
-    launch_zsize(L, ga, c->d_zsz, c->max_units);
+    launch_zsize(L, gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX), c->d_zsz, c->max_units);
     launch_zscan(L, c->d_zsz, c->d_st, c->d_zloc, c->d_zblk, c->max_units, 1, head, capacity);
     CK_LAUNCH();
     if (timing) CK(cudaEventRecord(c->ev_t[2], s));
+    c->last_path = CRUM_PATH_COMPRESSED;
+    return CRUM_OK;
+}
+
+// Device image: the metadata CRC (+ tail incl. unit sizes, header) on the
+// side stream beside encode + commit of every unit.
+int enqueue_gather_z(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, bool full, bool timing) {
+    uint8_t *head = capacity >= payload_offset_for(c->regs.size()) ? img : nullptr;
+    int st = enqueue_z_sizes(c, s, head, capacity, full, timing);
+    if (st) return st;
     CK(cudaEventRecord(c->ev_fork, s));
     CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
     launch_crc_meta(launch_of(c, c->aux), crc_args(c, head, nullptr), crc_max_len(c));
     CK(cudaEventRecord(c->ev_join, c->aux));
-    launch_zwrite(L, ga, c->d_zloc, c->d_zblk, head, c->max_units);
+    launch_zwrite(launch_of(c, s), gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX), c->d_zloc, c->d_zblk, head, 1,
+                  0, c->max_units, 0);
     if (timing) CK(cudaEventRecord(c->ev_t[3], s));
     CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     CK_LAUNCH();
@@ -1225,6 +1269,79 @@ int enqueue_gather_z(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
     c->last_kind = kLastDevGather;
     c->last_timed = timing;
     return CRUM_OK;
+}
+
+// Pinned host image: sizes first (the host waits for them: the encoded
+// offsets at every kZScanBlock-unit boundary become the copy boundaries),
+// then per chunk of whole scan blocks encode + commit into a ring slot on the
+// gather stream and copy the encoded bytes D2H on the copy stream; header,
+// table, tail and padding are stored through the image's mapped address.
+int gather_z_host(crum_ctx *c, crum_image *img, cudaStream_t s, bool full, crum_report *rep) {
+    void *dimg_v = nullptr;
+    CK(cudaHostGetDevicePointer(&dimg_v, img->host, 0));
+    uint8_t *dimg = static_cast<uint8_t *>(dimg_v);
+    uint8_t *head = img->cap >= payload_offset_for(c->regs.size()) ? dimg : nullptr;
+    int st = enqueue_z_sizes(c, s, head, img->cap, full, true);
+    if (st) return st;
+    CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->h_zblk, c->d_zblk, 8 * (c->max_units / kZScanBlock + 2), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const DevStats h0 = *c->h_st;
+    if (h0.status == kStCapacity) {
+        CK(cudaEventRecord(c->ev_t[3], s));
+        CK(cudaEventRecord(c->ev_t[4], s));
+        CK(cudaEventRecord(c->ev_t[5], s));
+        CK(cudaEventRecord(c->ev_done, s));
+        c->last_kind = kLastHostGather;
+        c->last_timed = true;
+        return finish_gather_z(c, s, img->cap, rep, nullptr);
+    }
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    launch_crc_meta(launch_of(c, c->aux), crc_args(c, head, nullptr), crc_max_len(c));
+    CK(cudaEventRecord(c->ev_join, c->aux));
+    const uint64_t U = h0.total_units;
+    // chunks of whole scan blocks: h_zblk[b] = encoded offset of unit b * kZScanBlock,
+    // h_zblk[nblk] = encoded length (k_zscan_top)
+    const uint64_t upc = std::max<uint64_t>(kZScanBlock, (c->ring_cap >> kSegLog2) / kZScanBlock * kZScanBlock);
+    auto off_at = [&](uint64_t u) { return c->h_zblk[(u + kZScanBlock - 1) / kZScanBlock]; };
+    Launch G = launch_of(c, c->gstream);
+    const GatherArgs ga = gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX);
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(c->gstream, c->ev_fork, 0));
+    bool copy_started = false;
+    uint64_t chunk_idx = 0;
+    for (uint64_t u0 = 0; u0 < U; u0 += upc, ++chunk_idx) {
+        const uint64_t u1 = std::min(U, u0 + upc);
+        const int slot = (int)(chunk_idx % kRing);
+        if (chunk_idx >= (uint64_t)kRing) CK(cudaStreamWaitEvent(c->gstream, c->ev_copy[slot], 0));
+        const uint64_t o0 = off_at(u0);
+        launch_zwrite(G, ga, c->d_zloc, c->d_zblk, c->d_ring[slot], 0, u0, u1, o0);
+        CK_LAUNCH();
+        CK(cudaEventRecord(c->ev_gather[slot], c->gstream));
+        CK(cudaStreamWaitEvent(c->copy, c->ev_gather[slot], 0));
+        if (!copy_started) {
+            CK(cudaEventRecord(c->ev_t[4], c->copy));
+            copy_started = true;
+        }
+        const uint64_t o1 = off_at(u1);  // u1 is a block boundary or U (-> the total)
+        if (o1 > o0)
+            CK(cudaMemcpyAsync(img->host + h0.poff + o0, c->d_ring[slot], o1 - o0, cudaMemcpyDeviceToHost, c->copy));
+        CK(cudaEventRecord(c->ev_copy[slot], c->copy));
+    }
+    if (!copy_started) CK(cudaEventRecord(c->ev_t[4], c->copy));
+    CK(cudaEventRecord(c->ev_t[5], c->copy));
+    CK(cudaEventRecord(c->ev_t[3], c->gstream));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    CK(cudaStreamSynchronize(c->gstream));
+    CK(cudaStreamSynchronize(c->copy));
+    CK(cudaEventRecord(c->ev_done, s));
+    c->last_kind = kLastHostGather;
+    c->last_timed = true;
+    DevStats h;
+    st = finish_gather_z(c, s, img->cap, rep, &h);
+    if (st == CRUM_OK) img->len = h.image_bytes;
+    return st;
 }
 
 // Report + status of a finished compressed gather.
@@ -1267,6 +1384,7 @@ int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
     if (timing) CK(cudaEventRecord(c->ev_t[4], s));
     CK(cudaEventRecord(c->ev_done, s));
     c->last_kind = kLastSync;
+    c->last_path = 0;
     c->last_timed = timing;
     if (dirty_out) {
         CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
@@ -1341,6 +1459,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
         if (timing) CK(cudaEventRecord(c->ev_t[4], s));
         CK(cudaEventRecord(c->ev_done, s));
         c->last_kind = kLastDevFused;
+        c->last_path = 0;
         c->last_timed = timing;
         if (rep) {
             CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
@@ -1370,6 +1489,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     CK_LAUNCH();
     if (timing) CK(cudaEventRecord(c->ev_t[4], s));
     CK(cudaEventRecord(c->ev_done, s));
+    c->last_path = 0;
     c->last_kind = kLastDevGather;
     c->last_timed = timing;
     if (rep) {
@@ -1412,16 +1532,10 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool full = flags & CRUM_FULL;
     if (flags & CRUM_COMPRESS) {
-        // encoded straight into the pinned image through its mapped address
-        void *dimg = nullptr;
-        CK(cudaHostGetDevicePointer(&dimg, img->host, 0));
-        int st = enqueue_gather_z(c, s, static_cast<uint8_t *>(dimg), img->cap, full, true);
-        if (st) return st;
-        DevStats h;
-        st = finish_gather_z(c, s, img->cap, rep, &h);
-        if (st == CRUM_OK) img->len = h.image_bytes;
-        return st;
+        int st = ensure_ring(c, (uint64_t)kZScanBlock << kSegLog2);  // a slot holds >= one scan block
+        return st ? st : gather_z_host(c, img, s, full, rep);
     }
+    c->last_path = 0;
     int st = ensure_ring(c);
     if (st) return st;
     uint64_t worst;
@@ -1635,7 +1749,8 @@ struct PreparedRestore {
     const uint32_t *d_ids = nullptr;
     const uint64_t *d_hashes = nullptr;
     const uint8_t *payload_dev = nullptr;
-    uint8_t *d_payload_tmp = nullptr;  // CRUM_VERIFY staging of a host payload (caller frees)
+    uint8_t *d_payload_tmp = nullptr;  // decoded / CRUM_VERIFY staging of the payload
+    bool tmp_owned = false;            // the caller frees d_payload_tmp (else it is c->d_rtmp)
     DevStats hst{};                    // K, dirty bytes, runs of the image
 };
 
@@ -1643,7 +1758,18 @@ struct PreparedRestore {
 // CRUM_VERIFY) before anything is written.  On return the table and tail
 // are in c->d_meta (host image) and the region stats in c->d_rs / c->d_st.
 int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img, uint64_t len, cudaStream_t s,
-                    uint32_t flags, bool timing, PreparedRestore &pr) {
+                    uint32_t flags, bool timing, PreparedRestore &pr, bool cached) {
+    // payload staging: the context's grow-only buffer, or one owned by the caller
+    auto tmp_alloc = [&](uint8_t **q, uint64_t bytes) -> int {
+        if (!cached) return dev_alloc(c, q, bytes);
+        int e = grow(c, &c->d_rtmp, &c->rtmp_cap, bytes);
+        *q = c->d_rtmp;
+        return e;
+    };
+    auto tmp_free = [&](uint8_t *q) {
+        if (!cached && q) cudaFree(q);
+    };
+    pr.tmp_owned = !cached;
     ParsedImage &p = pr.p;
     uint8_t hdr[64];
     if (len < 64) {
@@ -1758,22 +1884,22 @@ int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img
     uint8_t *d_payload_tmp = nullptr;
     const uint8_t *payload_dev = dev_img ? dev_img + p.poff : nullptr;
     // compressed: decode every unit into device memory first (a bitmap that
-    // disagrees with its unit's size is CORRUPT); the pinned image is read in
-    // place through its mapped address, so only encoded bytes cross the link
+    // disagrees with its unit's size is CORRUPT); a pinned image's encoded
+    // payload crosses the link once (copy engine), then decodes from HBM
     if (zimg) {
         const uint8_t *src = payload_dev;
         if (host_img) {
-            void *dp = nullptr;
-            CK(cudaHostGetDevicePointer(&dp, const_cast<uint8_t *>(host_img), 0));
-            src = static_cast<const uint8_t *>(dp) + p.poff;
+            if ((st = grow(c, &c->d_renc, &c->renc_cap, p.payload))) return st;
+            CK(cudaMemcpyAsync(c->d_renc, host_img + p.poff, p.payload, cudaMemcpyHostToDevice, s));
+            src = c->d_renc;
         }
-        if ((st = dev_alloc(c, &d_payload_tmp, p.upayload))) return st;
+        if ((st = tmp_alloc(&d_payload_tmp, p.upayload))) return st;
         launch_zdecode(L, src, d_zsz, c->d_zloc, c->d_zblk, c->d_st, d_payload_tmp, zunits);
         CK_LAUNCH();
         CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (c->h_st->status != kStOk) {
-            cudaFree(d_payload_tmp);
+            tmp_free(d_payload_tmp);
             set_detail("compressed unit whose bitmap disagrees with its size");
             return CRUM_E_CORRUPT;
         }
@@ -1782,7 +1908,7 @@ int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img
     // CRUM_VERIFY: hash every hash-mode slot before writing anything
     if ((flags & CRUM_VERIFY) && c->any_hash && p.K) {
         if (!payload_dev) {
-            if ((st = dev_alloc(c, &d_payload_tmp, p.upayload))) return st;
+            if ((st = tmp_alloc(&d_payload_tmp, p.upayload))) return st;
             CK(cudaMemcpyAsync(d_payload_tmp, host_img + p.poff, p.upayload, cudaMemcpyHostToDevice, s));
             payload_dev = d_payload_tmp;
         }
@@ -1791,7 +1917,7 @@ int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img
         CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (c->h_st->status != kStOk) {
-            cudaFree(d_payload_tmp);
+            tmp_free(d_payload_tmp);
             set_detail("CRUM_VERIFY: a hash-mode slot does not match its listed hash");
             return CRUM_E_CORRUPT;
         }
@@ -1807,7 +1933,7 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
                    uint32_t flags, crum_report *rep) {
     const bool timing = rep != nullptr || c->timing_cfg;
     PreparedRestore pr;
-    int st = prepare_restore(c, host_img, dev_img, len, s, flags, timing, pr);
+    int st = prepare_restore(c, host_img, dev_img, len, s, flags, timing, pr, true);
     if (st) return st;
     const ParsedImage &p = pr.p;
     const uint32_t *d_ids = pr.d_ids;
@@ -1865,9 +1991,10 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
     CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     CK(cudaStreamSynchronize(c->copy));
-    if (d_payload_tmp) cudaFree(d_payload_tmp);
+    if (d_payload_tmp && pr.tmp_owned) cudaFree(d_payload_tmp);
     CK(cudaEventRecord(c->ev_done, s));
     c->last_kind = kLastRestore;
+    c->last_path = 0;
     c->last_timed = timing;
     if (rep) {
         memset(rep, 0, sizeof *rep);
@@ -1973,7 +2100,7 @@ int crum_restore_begin(crum_ctx *ctx, crum_image *img, void *stream, uint32_t fl
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     PreparedRestore pr;
-    int st = prepare_restore(c, img->host, nullptr, img->len, s, flags, false, pr);
+    int st = prepare_restore(c, img->host, nullptr, img->len, s, flags, false, pr, false);
     if (st) {
         dev_free(pr.d_payload_tmp);
         return st;
