@@ -38,4 +38,51 @@ q.restore_scatter(full, flags=crum.VERIFY)
 q.restore_scatter_device(dimg, len(want), flags=crum.VERIFY)
 torch.cuda.synchronize()
 assert all(np.array_equal(z.cpu().numpy(), h) for z, h in zip(zs, p.host))
-print("sanitize workload ok; launches", p.g.launch_count + q.launch_count)
+# compressed images: host (ring + copy engine) and device gathers, restore (eager, lazy)
+for h, d in zip(p.host, p.dev):
+    h[h.nbytes // 2:] = 0
+    d.copy_(torch.from_numpy(h))
+torch.cuda.synchronize()
+p.g.mark_dirty(1, 0, SPECS[0][0])
+p.o.mark_dirty(1, 0, SPECS[0][0])
+zimg = p.g.new_image()
+for e, d in ((5, 0.4), (6, 0.0)):
+    p.write(e, d, touch=True)
+    st, want, _ = p.o.checkpoint_gather(flags=crum.COMPRESS)
+    p.g.checkpoint_gather(zimg, flags=crum.COMPRESS)
+    assert zimg.tobytes() == want.tobytes(), e
+p.write(7, 0.3, touch=True)
+st, want, _ = p.o.checkpoint_gather(flags=crum.COMPRESS)
+p.g.checkpoint_gather_device(dimg, cap, flags=crum.COMPRESS)
+assert dimg[:len(want)].cpu().numpy().tobytes() == want.tobytes()
+fz = p.g.new_image()
+p.g.checkpoint_gather(fz, flags=crum.FULL | crum.COMPRESS)
+q.restore_scatter(fz, flags=crum.VERIFY)
+torch.cuda.synchronize()
+assert all(np.array_equal(z.cpu().numpy(), h) for z, h in zip(zs, p.host))
+r = crum.Context(0)
+zr = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for nb, _, _ in SPECS]
+for z, (nb, P, m) in zip(zr, SPECS):
+    r.register_region(z, nb, P, m)
+sess = r.restore_begin(fz)
+for rid, pg in ((1, 3), (1, 4), (2, 0), (4, 0), (6, 1)):
+    sess.fetch(rid, pg)
+sess.end()
+torch.cuda.synchronize()
+assert all(np.array_equal(z.cpu().numpy(), h) for z, h in zip(zr, p.host))
+# tracked mode: marks from the host and from a writer kernel
+t = crum.Context(0)
+tb = torch.zeros(64 * 4096, dtype=torch.uint8, device="cuda")
+tid = t.register_region(tb, tb.numel(), 4096, crum.MODE_TRACKED)
+t.sync_shadow()
+pg = torch.tensor([1, 5, 9], dtype=torch.int32, device="cuda")
+t.mark_dirty_pages(tid, pg, 3)
+crum.synth_write_pages_tracked(tb, tb.numel(), 4096, pg, 3, 7, 1, 0, t.region_tracker(tid))
+assert t.sync_shadow() == 3
+# persist + load
+import tempfile
+path = os.path.join(tempfile.mkdtemp(), "img.crum")
+fz.persist(path)
+fz.persist_wait()
+assert r.load_image(path).tobytes() == fz.tobytes()
+print("sanitize workload ok; launches", p.g.launch_count + q.launch_count + r.launch_count + t.launch_count)
