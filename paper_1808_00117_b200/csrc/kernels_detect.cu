@@ -14,6 +14,8 @@
 //    scramble chain across blocks runs on 4 lanes per page fed by 8 shuffles
 //    per 8 KiB.  XXH3 structure: xxhash 0.8 long-input loop (see
 //    DESIGN.md "XXH3 on the GPU"), written here independently of oracle/.
+#include <cstdlib>
+
 #include "crum_internal.cuh"
 
 namespace crum {
@@ -419,6 +421,178 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_detect_hash_big(
 }
 
 // ---------------------------------------------------------------------------
+// HASH detect for large pages, TMA-fed (the default for P >= 64 KiB): three
+// persistent CTAs per SM (three independent scramble chains -- a page's chain
+// is serial, so chains per SM bound the rate).  Warp 5 (the "loader")
+// streams each 32 KiB round of the CTA's pages into a 2-stage shared-memory
+// ring with one cp.async.bulk (UBLKCP) per round, completing on the stage's
+// FULL mbarrier (tx bytes); the partial rounds of a region's last page are
+// copied by the loader's lanes with zero fill instead.  Warps 0..3 compute
+// the 32 block accumulate sums of a round from shared memory (same lane
+// layout as above) and release the stage on its EMPTY mbarrier (4
+// arrivals); warp 4 runs the scramble chain over the block sums (named
+// barriers 1-4, 160 threads).  192 KiB per SM are in flight with no
+// registers held.
+// ---------------------------------------------------------------------------
+constexpr int kTmaCompute = 4;                                  // compute warps
+constexpr int kTmaRB = kTmaCompute * 8;                           // blocks per round
+constexpr int kTmaStages = 2;
+constexpr uint32_t kTmaRound = (uint32_t)kTmaRB * 1024u;         // 32 KiB
+constexpr int kTmaChainThreads = (kTmaCompute + 1) * 32;          // named-barrier participants
+constexpr int kTmaThreads = kTmaChainThreads + 32;                // + loader warp
+constexpr int kTmaCtasPerSm = 3;                                  // 3 scramble chains per SM
+constexpr size_t kTmaSmem = (size_t)kTmaStages * kTmaRound;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
+    const DevRegion *__restrict__ regs, const uint32_t *__restrict__ big_idx,
+    const uint64_t *__restrict__ big_pg, uint32_t n_big, uint64_t w_lo, uint64_t w_hi,
+    uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash, uint8_t tag) {
+    extern __shared__ __align__(1024) uint8_t ring[];  // kTmaStages x kTmaRound
+    __shared__ uint64_t S[2][kTmaRB][8];
+    __shared__ __align__(8) uint64_t full_bar[kTmaStages], empty_bar[kTmaStages];
+    __shared__ uint64_t sw[24], slast[8], smerge[8], sinit[8];
+    if (threadIdx.x < 24) sw[threadIdx.x] = c_xxh.w[threadIdx.x];
+    if (threadIdx.x < 8) {
+        slast[threadIdx.x] = c_xxh.last[threadIdx.x];
+        smerge[threadIdx.x] = c_xxh.merge[threadIdx.x];
+        sinit[threadIdx.x] = c_xxh.init[threadIdx.x];
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kTmaStages; ++i) {
+            mbar_init(&full_bar[i], 1);
+            mbar_init(&empty_bar[i], kTmaCompute);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t q = 0;  // round counter across this CTA's pages (stage = q % 3, use = q / 3)
+    uint64_t r_lo = 1, r_hi = 0;
+    DevRegion R{};
+    for (uint64_t w = w_lo + blockIdx.x; w < w_hi; w += gridDim.x) {
+        if (w < r_lo || w >= r_hi) {
+            const uint32_t r = upper_region(big_pg, n_big, w);
+            R = regs[__ldg(big_idx + r)];
+            r_lo = __ldg(big_pg + r);
+            r_hi = __ldg(big_pg + r + 1);
+        }
+        const uint64_t page = w - r_lo;
+        const uint64_t P = 1ull << R.log2p;
+        const uint32_t bpp = (uint32_t)(P >> 10);
+        const uint32_t rounds = bpp / kTmaRB;
+        const uint64_t len = min(P, R.bytes - (page << R.log2p));
+        const uint8_t *pg = R.base + (page << R.log2p);
+        if (warp == kTmaCompute + 1) {
+            // loader
+            for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
+                const uint32_t st = q % kTmaStages, use = q / kTmaStages;
+                if (use) mbar_wait(&empty_bar[st], (use - 1) & 1);
+                uint8_t *dst = ring + (size_t)st * kTmaRound;
+                const uint64_t off = (uint64_t)rr * kTmaRound;
+                if (off + kTmaRound <= len) {
+                    if (lane == 0) {
+                        mbar_arrive_tx(&full_bar[st], kTmaRound);
+                        bulk_g2s(dst, pg + off, kTmaRound, &full_bar[st]);
+                    }
+                } else {
+                    // partial round of a region's last page: zero-padded copy
+                    for (uint32_t o = lane * 16; o < kTmaRound; o += 512)
+                        *reinterpret_cast<uint4 *>(dst + o) = ld_slot16(pg, off + o, len);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&full_bar[st]);
+                }
+            }
+        } else if (warp < kTmaCompute) {
+            const uint32_t p = lane & 3, b = lane >> 2;
+            for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
+                const uint32_t st = q % kTmaStages, use = q / kTmaStages;
+                const uint32_t buf = q & 1;
+                const uint32_t bl = warp * 8 + b;  // block within the round
+                const uint32_t bi = rr * kTmaRB + bl;
+                mbar_wait(&full_bar[st], use & 1);
+                const uint8_t *src = ring + (size_t)st * kTmaRound + bl * 1024 + p * 16;
+                uint4 d[16];
+#pragma unroll
+                for (int s2 = 0; s2 < 16; ++s2) d[s2] = *reinterpret_cast<const uint4 *>(src + s2 * 64);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[st]);
+                uint64_t a0 = 0, a1 = 0;
+#pragma unroll
+                for (int s2 = 0; s2 < 15; ++s2) accum16(a0, a1, d[s2], sw[s2 + 2 * p], sw[s2 + 2 * p + 1]);
+                const bool lastblk = (bi == bpp - 1);
+                accum16(a0, a1, d[15], lastblk ? slast[2 * p] : sw[15 + 2 * p],
+                        lastblk ? slast[2 * p + 1] : sw[16 + 2 * p]);
+                if (q >= 2) bar_sync(3 + buf, kTmaChainThreads);  // the chain has drained this buffer
+                S[buf][bl][2 * p] = a0;
+                S[buf][bl][2 * p + 1] = a1;
+                bar_arrive(1 + buf, kTmaChainThreads);
+            }
+        } else {
+            const uint32_t l = lane & 7;
+            const uint64_t key = sw[16 + l];
+            uint64_t acc = sinit[l];
+            for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
+                const uint32_t buf = q & 1;
+                bar_sync(1 + buf, kTmaChainThreads);
+                const uint32_t b0 = rr * kTmaRB;
+#pragma unroll 8
+                for (int j = 0; j < kTmaRB; ++j) {
+                    acc += S[buf][j][l];
+                    if (b0 + j != bpp - 1) acc = scramble(acc, key);
+                }
+                bar_arrive(3 + buf, kTmaChainThreads);
+            }
+            const uint64_t x = acc ^ smerge[l];
+            const uint64_t y = __shfl_down_sync(0xffffffffu, x, 1);
+            uint64_t m = ((l & 1) == 0) ? ((x * y) ^ __umul64hi(x, y)) : 0;
+            m += __shfl_xor_sync(0xffffffffu, m, 2);
+            m += __shfl_xor_sync(0xffffffffu, m, 4);
+            uint64_t h = P * kP64_1 + m;
+            h ^= h >> 37;
+            h *= kMx1;
+            h ^= h >> 32;
+            if (lane == 0) {
+                const uint64_t g = R.page_base + page;
+                newhash[g] = h;
+                flags[g] = (h != R.table[page]) ? tag : 0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // CRUM_VERIFY (restore): recompute XXH3 of every hash-mode slot of the image
 // payload and compare with the listed hash.  Warp per slot (P = 4 KiB slots
 // use the G = 4 path with the upper half-warp duplicating the lower).
@@ -488,8 +662,23 @@ void launch_detect_hash_big(const Launch &L, const DevRegion *regs, const uint32
                             uint8_t *flags, uint64_t *newhash, uint8_t tag) {
     if (w_hi <= w_lo) return;
     uint64_t blocks = w_hi - w_lo;
+    // TMA-fed kernel by default; CRUM_HASH_NO_TMA=1 selects the register-staged one
+    static const bool no_tma = getenv("CRUM_HASH_NO_TMA") != nullptr;
+    if (!no_tma) {
+        cudaFuncSetAttribute(k_detect_hash_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+        // a page's scramble chain is serial: give every CTA the same number of
+        // pages (e.g. 512 x 2 MiB pages -> 256 CTAs x 2, not 444 CTAs x 1-2)
+        const uint64_t cap = (uint64_t)L.sms * kTmaCtasPerSm;
+        const uint64_t per = (blocks + cap - 1) / cap;
+        blocks = (blocks + per - 1) / per;
+        k_detect_hash_tma<<<(unsigned)blocks, kTmaThreads, kTmaSmem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo,
+                                                                                 w_hi, flags, newhash, tag);
+        ++*L.counter;
+        return;
+    }
     const uint64_t cap = (uint64_t)L.sms * 2;
-    if (blocks > cap) blocks = cap;
+    const uint64_t per = (blocks + cap - 1) / cap;
+    blocks = (blocks + per - 1) / per;
     k_detect_hash_big<<<(unsigned)blocks, kBigThreads, 0, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo, w_hi,
                                                                       flags, newhash, tag);
     ++*L.counter;
