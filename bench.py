@@ -5,7 +5,7 @@ A "step" is one coordinated checkpoint of the whole registered footprint:
 A5 barrier -> A1 detect -> A2 compact -> A3 gather + commit (-> A4 copy-out for
 the e2e figure) -> A5 all-reduce of the dirty/image bytes.  Before every step
 the "application" rewrites a seeded d-fraction of the pages (synth writer
-kernel) and L2 is scrubbed with a 256 MiB write; both run outside the step's
+kernel) and L2 is scrubbed with a 256 MiB streaming read; both run outside the step's
 CUDA events.  Inputs live in HBM (2 GiB > 126 MB L2 for C2).
 
   value  = F / T_dev : registered bytes per second with the image written to
@@ -336,6 +336,19 @@ def main():
         dist.barrier()
     wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
+    # context for fractions above 1.0: a plain streaming READ (no writes) of the
+    # first HBM region, timed the same way; the denominator stays the measured copy
+    rd_t = regions[0] if regions[0].is_cuda else scrub
+    rd_n = min(rd_t.numel(), GiB) // 16 * 16
+    e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rd_ms = []
+    for _ in range(5):
+        e_a.record(stream)
+        crum.synth_scrub(rd_t, rd_n, stream=stream)
+        e_b.record(stream)
+        e_b.synchronize()
+        rd_ms.append(e_a.elapsed_time(e_b))
+    read_stream = rd_n / (min(rd_ms) / 1e3) / 1e9
     launches = ctx.launch_count - launches0
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
     T = sum(step_ms) / 1e3
@@ -366,7 +379,9 @@ def main():
         det_bytes = {"compare": 2 * F, "hash": F + 16 * n_pages, "tracked": 2 * payload}[args.mode]
     det_t = det_sum / args.steps / 1e3
     achieved = det_bytes / det_t / 1e9
-    dev_alg = {"compare": 2 * F + 2 * payload, "hash": F + 16 * n_pages + 2 * payload,
+    # whole device phase: detect + gather reads/writes (compare also rewrites the
+    # mirror of every listed page: + KP)
+    dev_alg = {"compare": 2 * F + 3 * payload, "hash": F + 16 * n_pages + 2 * payload,
                "tracked": n_pages + 2 * payload}[args.mode]
     traffic_key = f"{kname}:{args.config}:{args.page}:{args.dirty}"
     line = {
@@ -376,14 +391,18 @@ def main():
         "data": "synthetic (seeded splitmix64 words; seeded page choice per epoch)",
         "config": {"workload": desc, "footprint_bytes_per_gpu": F, "pages_per_gpu": n_pages,
                    "dirty_pages_per_step": K, "image_bytes_per_step": KP,
-                   "l2": "inputs 2x footprint > 126 MB L2; 256 MiB scrub write before every step",
+                   "l2": "inputs 2x footprint > 126 MB L2; a 256 MiB streaming read before every step evicts L2 "
+                         "(the writer's dirty lines are written back there, untimed) and leaves it clean",
                    "timing": "per-step CUDA events around crum_checkpoint_gather_device on its stream; "
                              "application writer + scrub outside the events",
                    "wall_ms_per_step_incl_writer": round(wall * 1e3 / args.steps, 3)},
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1),
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "alg_bytes_per_launch": det_bytes, "avg_launch_ms": round(det_t * 1e3, 4),
-                     "traffic": read_traffic(traffic_key), "traffic_key": traffic_key},
+                     "traffic": read_traffic(traffic_key), "traffic_key": traffic_key,
+                     "read_stream_GBs": round(read_stream, 1),
+                     "note": "peak = measured copy (read+write); a read-only stream measured here reaches "
+                             "read_stream_GBs, so read-dominated kernels can exceed frac 1.0"},
         "device_phase": {"alg_bytes_per_step": dev_alg, "achieved_GBs": round(dev_alg / (T / args.steps) / 1e9, 1),
                          "frac": round(dev_alg / (T / args.steps) / 1e9 / peak, 4)},
         "gpu_launches": launches,

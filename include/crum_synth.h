@@ -44,7 +44,8 @@ CRUM_API int crum_synth_write_pages_tracked(void *dev_ptr, uint64_t bytes, uint6
                                            uint64_t epoch, uint64_t region_index, int touch,
                                            const void *tracker /* const crum_tracker* */, void *stream);
 
-/* Streaming write of `bytes` to scrub L2 between timed repetitions. */
+/* Streaming read of `bytes` (device buffer) between timed repetitions: evicts
+ * L2 (writing dirty lines back outside the timed region), leaves it clean. */
 CRUM_API int crum_synth_scrub(void *dev_ptr, uint64_t bytes, void *stream);
 
 /* Bandwidth probe: 16-byte vectorised copy kernel (blocks <= 0: 8 per SM of a

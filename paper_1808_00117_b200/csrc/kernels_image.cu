@@ -1054,37 +1054,29 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// w[i] = word 32i + lane of the unit at p (len logical bytes, rest zero).
-__device__ __forceinline__ void z_load_unit(const uint8_t *p, uint64_t len, uint32_t lane, uint32_t (&w)[32]) {
-    if (len >= kSegBytes && ((reinterpret_cast<uintptr_t>(p) & 3) == 0)) {
-        const uint32_t *q = reinterpret_cast<const uint32_t *>(p);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) w[i] = __ldg(q + 32 * i + lane);
-    } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const uint64_t b = 4ull * (32 * i + lane);
-            uint32_t v = 0;
-            for (int k = 0; k < 4; ++k)
-                if (b + k < len) v |= (uint32_t)p[b + k] << (8 * k);
-            w[i] = v;
-        }
-    }
+// Row i (0..7) of a unit, as this lane sees it: the 16 bytes at 512 i + 16 lane
+// (words 128 i + 4 lane + t, t = 0..3); bytes at or beyond len read as zero.
+__device__ __forceinline__ uint4 z_row(const uint8_t *p, uint64_t len, uint32_t i, uint32_t lane) {
+    const uint64_t o = 512ull * i + 16ull * lane;
+    if (o + 16 <= len) return __ldg(reinterpret_cast<const uint4 *>(p + o));
+    uint32_t w[4] = {0, 0, 0, 0};
+    for (uint32_t k = 0; k < 16; ++k)
+        if (o + k < len) w[k >> 2] |= (uint32_t)p[o + k] << (8 * (k & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// Bitmap rows of the mispredicted words; returns their count.
-__device__ __forceinline__ uint32_t z_bitmap(const uint32_t (&w)[32], uint32_t lane, uint32_t (&bm)[32]) {
-    uint32_t c30 = 0, c31 = 0, n = 0;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const uint32_t up = __shfl_up_sync(0xffffffffu, w[i], 2);
-        const uint32_t pred = lane >= 2 ? up : (lane == 0 ? c30 : c31);
-        c30 = __shfl_sync(0xffffffffu, w[i], 30);
-        c31 = __shfl_sync(0xffffffffu, w[i], 31);
-        bm[i] = __ballot_sync(0xffffffffu, w[i] != pred);
-        n += __popc(bm[i]);
+// Mispredicted-word nibble of this lane for row v (bit t <-> word 4 lane + t);
+// (cz, cw) carry words 128 i - 2, 128 i - 1 (lane 31's z, w of the previous row).
+__device__ __forceinline__ uint32_t z_nibble(const uint4 &v, uint32_t lane, uint32_t &cz, uint32_t &cw) {
+    uint32_t pz = __shfl_up_sync(0xffffffffu, v.z, 1), pw = __shfl_up_sync(0xffffffffu, v.w, 1);
+    if (lane == 0) {
+        pz = cz;
+        pw = cw;
     }
-    return n;
+    cz = __shfl_sync(0xffffffffu, v.z, 31);
+    cw = __shfl_sync(0xffffffffu, v.w, 31);
+    return (uint32_t)(v.x != pz) | ((uint32_t)(v.y != pw) << 1) | ((uint32_t)(v.z != v.x) << 2) |
+           ((uint32_t)(v.w != v.y) << 3);
 }
 
 __device__ __forceinline__ uint32_t z_size_of(uint32_t n) {
@@ -1108,8 +1100,8 @@ __device__ __forceinline__ ZUnit z_unit(const GatherArgs &a, uint64_t k_lo, uint
     return z;
 }
 
-// Pass 1: encoded size of every unit of the gather.
-__global__ void __launch_bounds__(256) k_zsize(GatherArgs a, uint16_t *zsz) {
+// Pass 1: encoded size of every unit of the gather (8 x 16 B per lane).
+__global__ void __launch_bounds__(256, 2) k_zsize(GatherArgs a, uint16_t *zsz) {
     const DevStats *st = a.st;
     if (st->status != kStOk) return;
     const uint64_t k_lo = a.rb[0].k, k_hi = a.rb[1].k, U = a.rb[1].units;
@@ -1117,9 +1109,14 @@ __global__ void __launch_bounds__(256) k_zsize(GatherArgs a, uint16_t *zsz) {
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
         const ZUnit z = z_unit(a, k_lo, k_hi, u);
-        uint32_t w[32], bm[32];
-        z_load_unit(z.g.base + z.off, z.len, lane, w);
-        const uint32_t n = z_bitmap(w, lane, bm);
+        const uint8_t *p = z.g.base + z.off;
+        uint4 v[8];
+#pragma unroll
+        for (uint32_t i = 0; i < 8; ++i) v[i] = z_row(p, z.len, i, lane);
+        uint32_t cz = 0, cw = 0, n = 0;
+#pragma unroll
+        for (uint32_t i = 0; i < 8; ++i) n += __popc(z_nibble(v[i], lane, cz, cw));
+        n = __reduce_add_sync(0xffffffffu, n);
         if (lane == 0) zsz[u] = (uint16_t)z_size_of(n);
     }
 }
@@ -1200,7 +1197,7 @@ __global__ void __launch_bounds__(1024) k_zscan_top(uint64_t *zblk, DevStats *st
 // Pass 2: encode units [u_lo, u_hi) and commit them (as k_gather).  Unit u
 // goes to dst + (add_poff ? poff : 0) + off(u) - off0, off(u) its offset in
 // the compressed payload (dst == nullptr: commit only).
-__global__ void __launch_bounds__(256) k_zwrite(GatherArgs a, const uint32_t *zloc, const uint64_t *zblk,
+__global__ void __launch_bounds__(256, 2) k_zwrite(GatherArgs a, const uint32_t *zloc, const uint64_t *zblk,
                                                uint8_t *dst, int add_poff, uint64_t u_lo, uint64_t u_hi,
                                                uint64_t off0) {
     const DevStats *st = a.st;
@@ -1212,22 +1209,52 @@ __global__ void __launch_bounds__(256) k_zwrite(GatherArgs a, const uint32_t *zl
     for (uint64_t u = u_lo + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < U; u += nwarps) {
         const ZUnit z = z_unit(a, k_lo, k_hi, u);
         if (payload) {
-            uint32_t w[32], bm[32];
-            z_load_unit(z.g.base + z.off, z.len, lane, w);
-            const uint32_t n = z_bitmap(w, lane, bm);
+            const uint8_t *p = z.g.base + z.off;
+            uint4 v[8];
+#pragma unroll
+            for (uint32_t i = 0; i < 8; ++i) v[i] = z_row(p, z.len, i, lane);
+            uint32_t nib[8], cz = 0, cw = 0, n = 0;
+#pragma unroll
+            for (uint32_t i = 0; i < 8; ++i) {
+                nib[i] = z_nibble(v[i], lane, cz, cw);
+                n += __popc(nib[i]);
+            }
+            n = __reduce_add_sync(0xffffffffu, n);
             const uint32_t cs = z_size_of(n);
             uint32_t *out = reinterpret_cast<uint32_t *>(payload + zblk[u / kZScanBlock] + zloc[u]);
             if (cs == kSegBytes) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) out[32 * i + lane] = w[i];
+                for (uint32_t i = 0; i < 8; ++i) {
+                    uint32_t *o = out + 128 * i + 4 * lane;
+                    o[0] = v[i].x;
+                    o[1] = v[i].y;
+                    o[2] = v[i].z;
+                    o[3] = v[i].w;
+                }
             } else if (cs) {
-                const uint32_t lt = lanemask_lt();
-                uint32_t pos = 0;
+                uint32_t base = 32;  // literals follow the 32 bitmap words
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    if (lane == (uint32_t)i) out[i] = bm[i];
-                    if ((bm[i] >> lane) & 1u) out[32 + pos + __popc(bm[i] & lt)] = w[i];
-                    pos += __popc(bm[i]);
+                for (uint32_t i = 0; i < 8; ++i) {
+                    // bitmap words 4i .. 4i+3: word 4i + m holds lanes 8m .. 8m+7, 4 bits each
+                    uint32_t x = nib[i] << (4 * (lane & 7));
+                    x |= __shfl_xor_sync(0xffffffffu, x, 1);
+                    x |= __shfl_xor_sync(0xffffffffu, x, 2);
+                    x |= __shfl_xor_sync(0xffffffffu, x, 4);
+                    if ((lane & 7) == 0) out[4 * i + (lane >> 3)] = x;
+                    // literal ranks: warp-exclusive prefix of the nibble populations
+                    const uint32_t c = __popc(nib[i]);
+                    uint32_t inc = c;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+                        if (lane >= (uint32_t)d) inc += y;
+                    }
+                    uint32_t pos = base + inc - c;
+                    if (nib[i] & 1u) out[pos++] = v[i].x;
+                    if (nib[i] & 2u) out[pos++] = v[i].y;
+                    if (nib[i] & 4u) out[pos++] = v[i].z;
+                    if (nib[i] & 8u) out[pos++] = v[i].w;
+                    base += __shfl_sync(0xffffffffu, inc, 31);
                 }
             }
         }
@@ -1263,36 +1290,65 @@ __global__ void __launch_bounds__(256) k_zdecode(const uint8_t *src, const uint1
             for (int i = 0; i < 32; ++i) out[32 * i + lane] = 0u;
             continue;
         }
-        const uint32_t mine = in[lane];
-        uint32_t n = __popc(mine);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+        const uint32_t mine = in[lane];  // bitmap word `lane`
+        const uint32_t n = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mine));
         if (128u + 4u * n != cs) {
             if (lane == 0) st->status = kStCorrupt;
             continue;
         }
-        const uint32_t lt = lanemask_lt();
-        uint32_t pos = 0, c30 = 0, c31 = 0;
+        uint32_t base = 32, ce = 0, co = 0;  // literal cursor; carries of the even / odd word classes
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const uint32_t row = __shfl_sync(0xffffffffu, mine, i);
-            bool f = (row >> lane) & 1u;
-            uint32_t v = f ? in[32 + pos + __popc(row & lt)] : 0u;
-            pos += __popc(row);
-            // nearest literal at or before this word in its parity class
+        for (uint32_t i = 0; i < 8; ++i) {
+            const uint32_t nib = (__shfl_sync(0xffffffffu, mine, 4 * i + (lane >> 3)) >> (4 * (lane & 7))) & 15u;
+            const uint32_t c = __popc(nib);
+            uint32_t inc = c;
 #pragma unroll
-            for (int d = 2; d < 32; d <<= 1) {
-                const uint32_t v2 = __shfl_up_sync(0xffffffffu, v, d);
-                const bool f2 = __shfl_up_sync(0xffffffffu, (uint32_t)f, d) != 0;
-                if (lane >= (uint32_t)d && !f) {
-                    v = v2;
-                    f = f2;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= (uint32_t)d) inc += y;
+            }
+            uint32_t pos = base + inc - c;
+            uint32_t lx = 0, ly = 0, lz = 0, lw = 0;
+            if (nib & 1u) lx = in[pos++];
+            if (nib & 2u) ly = in[pos++];
+            if (nib & 4u) lz = in[pos++];
+            if (nib & 8u) lw = in[pos++];
+            base += __shfl_sync(0xffffffffu, inc, 31);
+            // even class: ... x_l, z_l, x_{l+1} ...; odd class: ... y_l, w_l ...
+            // last literal of this lane's pair, then an inclusive segmented scan over lanes
+            bool fe = (nib & 5u) != 0, fo = (nib & 10u) != 0;
+            uint32_t ve = (nib & 4u) ? lz : lx, vo = (nib & 8u) ? lw : ly;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t ve2 = __shfl_up_sync(0xffffffffu, ve, d);
+                const uint32_t vo2 = __shfl_up_sync(0xffffffffu, vo, d);
+                const bool fe2 = __shfl_up_sync(0xffffffffu, (uint32_t)fe, d) != 0;
+                const bool fo2 = __shfl_up_sync(0xffffffffu, (uint32_t)fo, d) != 0;
+                if (lane >= (uint32_t)d) {
+                    if (!fe) {
+                        ve = ve2;
+                        fe = fe2;
+                    }
+                    if (!fo) {
+                        vo = vo2;
+                        fo = fo2;
+                    }
                 }
             }
-            if (!f) v = (lane & 1) ? c31 : c30;
-            c30 = __shfl_sync(0xffffffffu, v, 30);
-            c31 = __shfl_sync(0xffffffffu, v, 31);
-            out[32 * i + lane] = v;
+            // value flowing into this lane: the last literal of the lanes before it, else the row carry
+            uint32_t ie = __shfl_up_sync(0xffffffffu, ve, 1), io = __shfl_up_sync(0xffffffffu, vo, 1);
+            const bool ife = __shfl_up_sync(0xffffffffu, (uint32_t)fe, 1) != 0;
+            const bool ifo = __shfl_up_sync(0xffffffffu, (uint32_t)fo, 1) != 0;
+            if (lane == 0 || !ife) ie = ce;
+            if (lane == 0 || !ifo) io = co;
+            uint4 o;
+            o.x = (nib & 1u) ? lx : ie;
+            o.y = (nib & 2u) ? ly : io;
+            o.z = (nib & 4u) ? lz : o.x;
+            o.w = (nib & 8u) ? lw : o.y;
+            ce = __shfl_sync(0xffffffffu, o.z, 31);
+            co = __shfl_sync(0xffffffffu, o.w, 31);
+            *reinterpret_cast<uint4 *>(out + 128 * i + 4 * lane) = o;
         }
     }
 }
