@@ -1083,22 +1083,46 @@ __device__ __forceinline__ uint32_t z_size_of(uint32_t n) {
     return n == 0 ? 0u : (128u + 4u * n < kSegBytes ? 128u + 4u * n : (uint32_t)kSegBytes);
 }
 
-// Unit u of the gather -> (region, page, byte offset, logical length).
+// Unit u of the gather -> (region, page, byte offset, logical length), walked
+// in tasks of kUnitsPerTask consecutive units: one binary search per task,
+// then the slot / region advance incrementally (as k_gather).
 struct ZUnit {
     DevRegion g;
     uint64_t gid, i, off, len, seg;
 };
-__device__ __forceinline__ ZUnit z_unit(const GatherArgs &a, uint64_t k_lo, uint64_t k_hi, uint64_t u) {
-    ZUnit z;
-    const uint64_t k = slot_of_unit(a.sunit, k_lo, k_hi, u);
-    z.gid = a.gids[k];
-    z.g = a.regs[region_of_page(a.regs, a.R, z.gid)];
-    z.seg = u - a.sunit[k];
-    z.i = z.gid - z.g.page_base;
-    z.off = (z.i << z.g.log2p) + (z.seg << kSegLog2);
-    z.len = z.g.bytes > z.off ? min((uint64_t)kSegBytes, z.g.bytes - z.off) : 0;
-    return z;
-}
+struct ZCursor {
+    const GatherArgs &a;
+    uint64_t k_hi, k, kbase, gid;
+    uint32_t r;
+    DevRegion g;
+    __device__ ZCursor(const GatherArgs &a_, uint64_t k_lo, uint64_t k_hi_, uint64_t u0) : a(a_), k_hi(k_hi_) {
+        k = slot_of_unit(a.sunit, k_lo, k_hi, u0);
+        gid = a.gids[k];
+        r = region_of_page(a.regs, a.R, gid);
+        g = a.regs[r];
+        kbase = a.sunit[k];
+    }
+    __device__ ZUnit at(uint64_t u) {  // u >= the previous call's u
+        const uint64_t nxt = (k + 1 < k_hi) ? a.sunit[k + 1] : ~0ull;
+        if (u >= nxt) {
+            k = slot_of_unit(a.sunit, k, k_hi, u);
+            kbase = a.sunit[k];
+            gid = a.gids[k];
+            if (r + 1 < a.R && gid >= a.regs[r + 1].page_base) {
+                r = region_of_page(a.regs, a.R, gid);
+                g = a.regs[r];
+            }
+        }
+        ZUnit z;
+        z.g = g;
+        z.gid = gid;
+        z.seg = u - kbase;
+        z.i = gid - g.page_base;
+        z.off = (z.i << g.log2p) + (z.seg << kSegLog2);
+        z.len = g.bytes > z.off ? min((uint64_t)kSegBytes, g.bytes - z.off) : 0;
+        return z;
+    }
+};
 
 // Pass 1: encoded size of every unit of the gather (8 x 16 B per lane).
 __global__ void __launch_bounds__(256, 2) k_zsize(GatherArgs a, uint16_t *zsz) {
@@ -1107,17 +1131,22 @@ __global__ void __launch_bounds__(256, 2) k_zsize(GatherArgs a, uint16_t *zsz) {
     const uint64_t k_lo = a.rb[0].k, k_hi = a.rb[1].k, U = a.rb[1].units;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
-        const ZUnit z = z_unit(a, k_lo, k_hi, u);
-        const uint8_t *p = z.g.base + z.off;
-        uint4 v[8];
+    const uint64_t ntask = (U + kUnitsPerTask - 1) / kUnitsPerTask;
+    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntask; t += nwarps) {
+        const uint64_t u0 = t * kUnitsPerTask, u1 = min(u0 + kUnitsPerTask, U);
+        ZCursor cur(a, k_lo, k_hi, u0);
+        for (uint64_t u = u0; u < u1; ++u) {
+            const ZUnit z = cur.at(u);
+            const uint8_t *p = z.g.base + z.off;
+            uint4 v[8];
 #pragma unroll
-        for (uint32_t i = 0; i < 8; ++i) v[i] = z_row(p, z.len, i, lane);
-        uint32_t cz = 0, cw = 0, n = 0;
+            for (uint32_t i = 0; i < 8; ++i) v[i] = z_row(p, z.len, i, lane);
+            uint32_t cz = 0, cw = 0, n = 0;
 #pragma unroll
-        for (uint32_t i = 0; i < 8; ++i) n += __popc(z_nibble(v[i], lane, cz, cw));
-        n = __reduce_add_sync(0xffffffffu, n);
-        if (lane == 0) zsz[u] = (uint16_t)z_size_of(n);
+            for (uint32_t i = 0; i < 8; ++i) n += __popc(z_nibble(v[i], lane, cz, cw));
+            n = __reduce_add_sync(0xffffffffu, n);
+            if (lane == 0) zsz[u] = (uint16_t)z_size_of(n);
+        }
     }
 }
 
@@ -1206,8 +1235,12 @@ __global__ void __launch_bounds__(256, 2) k_zwrite(GatherArgs a, const uint32_t 
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     uint8_t *payload = dst ? dst + (add_poff ? st->poff : 0) - off0 : nullptr;
-    for (uint64_t u = u_lo + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < U; u += nwarps) {
-        const ZUnit z = z_unit(a, k_lo, k_hi, u);
+    const uint64_t ntask = U > u_lo ? (U - u_lo + kUnitsPerTask - 1) / kUnitsPerTask : 0;
+    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntask; t += nwarps) {
+      const uint64_t u0 = u_lo + t * kUnitsPerTask, u1 = min(u0 + kUnitsPerTask, U);
+      ZCursor cur(a, k_lo, k_hi, u0);
+      for (uint64_t u = u0; u < u1; ++u) {
+        const ZUnit z = cur.at(u);
         if (payload) {
             const uint8_t *p = z.g.base + z.off;
             uint4 v[8];
@@ -1264,6 +1297,7 @@ __global__ void __launch_bounds__(256, 2) k_zwrite(GatherArgs a, const uint32_t 
             if (z.g.mode == kModeHash) z.g.table[z.i] = a.newhash[z.gid];
             a.force[z.gid] = 0;
         }
+      }
     }
 }
 
