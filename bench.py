@@ -243,6 +243,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
+    if args.config == "c5":
+        args.mode = "hash"  # C5 is defined in hash mode
     specs, desc = workload(args, rank)
     S = synth.seed(1) + (rank << 20)
     F = sum(nb for nb, _, _ in specs)
@@ -339,7 +341,7 @@ def main():
     # context for fractions above 1.0: a plain streaming READ (no writes) of the
     # first HBM region, timed the same way; the denominator stays the measured copy
     rd_t = regions[0] if regions[0].is_cuda else scrub
-    rd_n = min(rd_t.numel(), GiB) // 16 * 16
+    rd_n = min(rd_t.numel(), GiB) // 32 * 32
     e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     rd_ms = []
     for _ in range(5):
