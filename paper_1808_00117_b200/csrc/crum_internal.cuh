@@ -92,7 +92,7 @@ struct Launch {
 
 // A2: compaction of pages [p_lo, p_hi) (p_lo % 16 == 0), range index c.
 struct CompactArgs {
-    const uint8_t *flags;
+    uint8_t *flags;        // detect marks (== tag); the write pass clears its range's bytes
     const uint8_t *force;
     const DevRegion *regs;
     const uint64_t *newhash;
@@ -236,7 +236,7 @@ void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, c
 void launch_zdecode(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
                     const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t units);
 void launch_mark_pages(const Launch &L, uint8_t *force, uint64_t n_pages, const uint32_t *pages, uint64_t n);
-void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag,
+void launch_export_flags(const Launch &L, uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag,
                          uint8_t *out);
 
 // ---- synthetic inputs (synth.cu) ----

@@ -183,6 +183,16 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a
     }
     const uint64_t base = a.p_lo + (uint64_t)blockIdx.x * kPagesPerCompactBlock + threadIdx.x * kPagesPerThread;
     uint32_t m = thread_mask(a, base);
+    // consume the detect marks of this range (so the next checkpoint starts
+    // from zero flags and one constant tag suffices: no per-call clearing)
+    if (base < a.p_hi) {
+        if (base >= a.p_lo && base + kPagesPerThread <= a.p_hi) {
+            *reinterpret_cast<uint4 *>(a.flags + base) = make_uint4(0, 0, 0, 0);
+        } else {
+            for (uint32_t b = 0; b < kPagesPerThread; ++b)
+                if (base + b >= a.p_lo && base + b < a.p_hi) a.flags[base + b] = 0;
+        }
+    }
     uint64_t tc, tu;
     const uint64_t ec = block_excl_scan(__popc(m), &tc);
     const uint64_t eu = block_excl_scan(mask_units(a, base, m), &tu);  // syncs: s_off visible
@@ -766,13 +776,15 @@ void launch_mark_pages(const Launch &L, uint8_t *force, uint64_t n_pages, const 
     ++*L.counter;
 }
 
-__global__ void k_export_flags(const uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag, uint8_t *out) {
+__global__ void k_export_flags(uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag, uint8_t *out) {
     for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < N;
-         g += (uint64_t)gridDim.x * blockDim.x)
+         g += (uint64_t)gridDim.x * blockDim.x) {
         out[g] = (flags[g] == tag || force[g]) ? 1 : 0;
+        flags[g] = 0;  // consumed (as by compaction)
+    }
 }
 
-void launch_export_flags(const Launch &L, const uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag,
+void launch_export_flags(const Launch &L, uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag,
                          uint8_t *out) {
     if (!N) return;
     k_export_flags<<<L.sms * 4, 256, 0, L.stream>>>(flags, force, N, tag, out);

@@ -583,10 +583,14 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
     return ms;
 }
 
-// Next per-checkpoint flag tag (1..255); on wrap the flags array is cleared.
+// Detect marks changed pages with kFlagTag; compaction (and the debug export)
+// clear the marks they consume, so the flags are zero between calls.
+constexpr uint8_t kFlagTag = 1;
+
+// Next per-checkpoint tag of the single-pass kernel's look-back status words
+// (1..255); on wrap the status array is cleared.
 int next_tag(crum_ctx *c, cudaStream_t s) {
     if (c->tag == 255 || c->tag == 0) {
-        CK(cudaMemsetAsync(c->d_flags, 0, c->page_cap, s));
         if (c->d_status) CK(cudaMemsetAsync(c->d_status, 0, 8 * (c->n_tiles + 1), s));
         c->tag = 0;
     }
@@ -598,11 +602,11 @@ void enqueue_detect(crum_ctx *c, cudaStream_t s, const Range &rg, bool full) {
     Launch L = launch_of(c, s);
     if (!full)
         launch_detect_compare(L, c->d_regs, c->d_cmp_idx, c->d_cmp_seg, c->n_cmp, rg.s_lo, rg.s_hi, c->d_force,
-                              c->d_flags, c->tag);
+                              c->d_flags, kFlagTag);
     launch_detect_hash_big(L, c->d_regs, c->d_big_idx, c->d_big_pg, c->n_big, rg.v_lo, rg.v_hi, c->d_flags,
-                           c->d_newhash, c->tag);
+                           c->d_newhash, kFlagTag);
     launch_detect_hash(L, c->d_regs, c->d_hash_idx, c->d_hash_grp, c->n_hash, rg.w_lo, rg.w_hi, c->d_flags,
-                       c->d_newhash, c->tag);
+                       c->d_newhash, kFlagTag);
 }
 
 CompactArgs compact_args(crum_ctx *c, const Range &rg, uint32_t ci, bool first, bool final, bool full,
@@ -615,7 +619,7 @@ CompactArgs compact_args(crum_ctx *c, const Range &rg, uint32_t ci, bool first, 
     a.p_lo = rg.p_lo;
     a.p_hi = rg.p_hi;
     a.R = (uint32_t)c->regs.size();
-    a.tag = c->tag;
+    a.tag = kFlagTag;
     a.full = full ? 1 : 0;
     a.has_hashes = c->any_hash ? 1 : 0;
     a.first_range = first ? 1 : 0;
@@ -1235,7 +1239,6 @@ int enqueue_z_sizes(crum_ctx *c, cudaStream_t s, uint8_t *head, uint64_t capacit
     int st;
     if ((st = ensure_z(c, c->max_units))) return st;
     if (timing) CK(cudaEventRecord(c->ev_t[0], s));
-    if ((st = next_tag(c, s))) return st;
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
     enqueue_detect(c, s, c->all, full);
     if (timing) CK(cudaEventRecord(c->ev_t[1], s));
@@ -1372,7 +1375,6 @@ int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
     const bool timing = c->timing_cfg;
     int st;
     if (timing) CK(cudaEventRecord(c->ev_t[0], s));
-    if ((st = next_tag(c, s))) return st;
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
     enqueue_detect(c, s, c->all, false);
     if (timing) CK(cudaEventRecord(c->ev_t[1], s));
@@ -1471,7 +1473,6 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
         return CRUM_OK;
     }
     if (timing) CK(cudaEventRecord(c->ev_t[0], s));
-    if ((st = next_tag(c, s))) return st;
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
     enqueue_detect(c, s, c->all, full);
     if (timing) CK(cudaEventRecord(c->ev_t[1], s));
@@ -1544,7 +1545,6 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     const uint32_t nr = (uint32_t)c->ranges.size();
     const uint64_t poff = payload_offset_for(c->regs.size());
     CK(cudaEventRecord(c->ev_t[0], s));
-    if ((st = next_tag(c, s))) return st;
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
     // detect + compact of range ci on the caller's stream; after the last range
     // the metadata CRC + tail go into d_meta (tail after the head [0, poff))
@@ -2290,9 +2290,8 @@ int crum_debug_detect(crum_ctx *ctx, void *stream, uint8_t *host_flags, uint64_t
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int st;
-    if ((st = next_tag(c, s))) return st;
     enqueue_detect(c, s, c->all, false);
-    launch_export_flags(launch_of(c, s), c->d_flags, c->d_force, c->N, c->tag, c->d_dbg);
+    launch_export_flags(launch_of(c, s), c->d_flags, c->d_force, c->N, kFlagTag, c->d_dbg);
     CK_LAUNCH();
     if (n) CK(cudaMemcpyAsync(host_flags, c->d_dbg, n, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
