@@ -383,9 +383,12 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * wpb;
     uint8_t *payload = a.dst ? a.dst + (a.add_poff ? st->poff : 0) : nullptr;
-    const uint64_t ntask = (u_hi - u_lo + kUnitsPerTask - 1) / kUnitsPerTask;
+    // units per task: up to kUnitsPerTask (one slot search per task), fewer
+    // when the dirty set is small so every warp gets work
+    const uint64_t upt = max((uint64_t)1, min((uint64_t)kUnitsPerTask, (u_hi - u_lo + nwarps - 1) / nwarps));
+    const uint64_t ntask = (u_hi - u_lo + upt - 1) / upt;
     for (uint64_t t = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); t < ntask; t += nwarps) {
-        const uint64_t u0 = u_lo + t * kUnitsPerTask, u1 = min(u0 + kUnitsPerTask, u_hi);
+        const uint64_t u0 = u_lo + t * upt, u1 = min(u0 + upt, u_hi);
         uint64_t k = slot_of_unit(a.sunit, k_lo, k_hi, u0);
         uint64_t gid = a.gids[k];
         uint32_t r = region_of_page(a.regs, a.R, gid);
@@ -1143,9 +1146,10 @@ __global__ void __launch_bounds__(256, 2) k_zsize(GatherArgs a, uint16_t *zsz) {
     const uint64_t k_lo = a.rb[0].k, k_hi = a.rb[1].k, U = a.rb[1].units;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t ntask = (U + kUnitsPerTask - 1) / kUnitsPerTask;
+    const uint64_t upt = max((uint64_t)1, min((uint64_t)kUnitsPerTask, (U + nwarps - 1) / nwarps));
+    const uint64_t ntask = (U + upt - 1) / upt;
     for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntask; t += nwarps) {
-        const uint64_t u0 = t * kUnitsPerTask, u1 = min(u0 + kUnitsPerTask, U);
+        const uint64_t u0 = t * upt, u1 = min(u0 + upt, U);
         ZCursor cur(a, k_lo, k_hi, u0);
         for (uint64_t u = u0; u < u1; ++u) {
             const ZUnit z = cur.at(u);
@@ -1247,9 +1251,11 @@ __global__ void __launch_bounds__(256, 2) k_zwrite(GatherArgs a, const uint32_t 
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     uint8_t *payload = dst ? dst + (add_poff ? st->poff : 0) - off0 : nullptr;
-    const uint64_t ntask = U > u_lo ? (U - u_lo + kUnitsPerTask - 1) / kUnitsPerTask : 0;
+    const uint64_t nu = U > u_lo ? U - u_lo : 0;
+    const uint64_t upt = max((uint64_t)1, min((uint64_t)kUnitsPerTask, (nu + nwarps - 1) / nwarps));
+    const uint64_t ntask = (nu + upt - 1) / upt;
     for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntask; t += nwarps) {
-      const uint64_t u0 = u_lo + t * kUnitsPerTask, u1 = min(u0 + kUnitsPerTask, U);
+      const uint64_t u0 = u_lo + t * upt, u1 = min(u0 + upt, U);
       ZCursor cur(a, k_lo, k_hi, u0);
       for (uint64_t u = u0; u < u1; ++u) {
         const ZUnit z = cur.at(u);

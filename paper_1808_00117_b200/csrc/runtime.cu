@@ -145,6 +145,15 @@ struct crum_ctx {
     int device = 0;
     crum_restore_session *session = nullptr;  // open lazy restore (blocks other state changes)
     uint32_t last_path = 0;                   // CRUM_PATH_* bits of the last gather
+    // CUDA graph of the asynchronous device gather (one cached instance)
+    cudaStream_t gcap = nullptr;              // capture stream
+    cudaGraphExec_t g_exec = nullptr;
+    uint64_t g_nk = 0;                        // kernels per replay
+    uint64_t graph_epoch = 1;                 // bumped by every allocation / rebuild
+    uint64_t g_epoch = 0;
+    uint8_t *g_img = nullptr;
+    uint64_t g_cap = 0;
+    uint32_t g_flags = 0;
     int sms = 148;
     uint64_t chunk = kDefaultChunk;
     std::vector<HostRegion> regs;
@@ -285,7 +294,7 @@ uint64_t pad_pages(uint64_t n) { return round_up(n ? n : 1, kPagesPerCompactBloc
 
 template <typename T>
 int dev_alloc(crum_ctx *c, T **p, uint64_t bytes) {
-    (void)c;
+    ++c->graph_epoch;  // a captured graph may hold the pointer this replaces
     void *q = nullptr;
     cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
     if (e != cudaSuccess) {
@@ -811,6 +820,7 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
         if (cudaEventCreate(&c->ev_t[i]) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
+    if (cudaStreamCreateWithFlags(&c->gcap, cudaStreamNonBlocking) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
@@ -882,6 +892,8 @@ int crum_destroy(crum_ctx *c) {
     if (c->copy) cudaStreamDestroy(c->copy);
     if (c->gstream) cudaStreamDestroy(c->gstream);
     if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+    if (c->gcap) cudaStreamDestroy(c->gcap);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (int i = 0; i < kRing; ++i) {
@@ -1231,6 +1243,84 @@ namespace {
 // device address of a pinned host image (then the encoder's stores cross the
 // host link directly: only encoded bytes move).  Capacity failures commit
 // nothing (every later kernel checks the status).
+// A1-A3 into a device image (stream-ordered): detect, compact (+ table,
+// header fields), gather (+ commit), and on the side stream the metadata CRC
+// (+ tail, header).
+// Timing / completion events are recorded as external event nodes so they
+// also fire when the sequence runs as a captured graph.
+int enqueue_gather_dev(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, bool full, bool timing,
+                       bool capturing = false) {
+    const unsigned evf = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[0], s, evf));
+    CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
+    enqueue_detect(c, s, c->all, full);
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[1], s, evf));
+    // device path: no mapped-host mirrors of the totals (only the host pipeline reads them)
+    CompactArgs ca = compact_args(c, c->all, 0, true, true, full, capacity, img);
+    ca.rb_host = nullptr;
+    enqueue_compact(c, s, ca);
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[2], s, evf));
+    // metadata CRC (+ tail, header) on a side stream beside the payload gather
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    CrcArgs cra = crc_args(c, img, nullptr);
+    cra.st_host = nullptr;
+    launch_crc_meta(launch_of(c, c->aux), cra, crc_max_len(c));
+    CK(cudaEventRecord(c->ev_join, c->aux));
+    Launch L = launch_of(c, s);
+    launch_gather(L, gather_args(c, 0, img, 0, true, 0, UINT64_MAX), c->max_units);
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[3], s, evf));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    CK_LAUNCH();
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[4], s, evf));
+    CK(cudaEventRecordWithFlags(c->ev_done, s, evf));
+    return CRUM_OK;
+}
+
+// The same sequence as a CUDA graph: captured on the context's capture stream
+// the first time a (image, capacity, flags) triple is seen in this registry
+// generation, then replayed on `s`.  CRUM_E_BUSY: capture unavailable, the
+// caller enqueues directly.
+int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, uint32_t flags, bool timing) {
+    if (c->g_exec == nullptr || c->g_epoch != c->graph_epoch || c->g_img != img || c->g_cap != capacity ||
+        c->g_flags != flags) {
+        if (c->g_exec) {
+            cudaGraphExecDestroy(c->g_exec);
+            c->g_exec = nullptr;
+        }
+        const uint64_t l0 = c->launches;
+        if (cudaStreamBeginCapture(c->gcap, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+            cudaGetLastError();
+            return CRUM_E_BUSY;
+        }
+        const int st = enqueue_gather_dev(c, c->gcap, img, capacity, (flags & CRUM_FULL) != 0, timing, true);
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(c->gcap, &g);
+        const uint64_t nk = c->launches - l0;
+        c->launches = l0;
+        if (st || e != cudaSuccess || !g) {
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            return st ? st : CRUM_E_BUSY;
+        }
+        const cudaError_t ei = cudaGraphInstantiate(&c->g_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ei != cudaSuccess) {
+            cudaGetLastError();
+            c->g_exec = nullptr;
+            return CRUM_E_BUSY;
+        }
+        c->g_nk = nk;
+        c->g_epoch = c->graph_epoch;
+        c->g_img = img;
+        c->g_cap = capacity;
+        c->g_flags = flags;
+    }
+    CK(cudaGraphLaunch(c->g_exec, s));
+    c->launches += c->g_nk;
+    return CRUM_OK;
+}
+
 int finish_gather_z(crum_ctx *c, cudaStream_t s, uint64_t capacity, crum_report *rep, DevStats *out);
 
 // Sizes: detect, compact (+ table into head), encoded sizes and their scan
@@ -1378,7 +1468,9 @@ int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
     enqueue_detect(c, s, c->all, false);
     if (timing) CK(cudaEventRecord(c->ev_t[1], s));
-    enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, false, UINT64_MAX, nullptr));
+    CompactArgs ca = compact_args(c, c->all, 0, true, true, false, UINT64_MAX, nullptr);
+    ca.rb_host = nullptr;
+    enqueue_compact(c, s, ca);
     if (timing) CK(cudaEventRecord(c->ev_t[2], s));
     Launch L = launch_of(c, s);
     launch_gather(L, gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX), c->max_units);
@@ -1472,24 +1564,21 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
         }
         return CRUM_OK;
     }
-    if (timing) CK(cudaEventRecord(c->ev_t[0], s));
-    CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
-    enqueue_detect(c, s, c->all, full);
-    if (timing) CK(cudaEventRecord(c->ev_t[1], s));
-    enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, full, capacity, img));
-    if (timing) CK(cudaEventRecord(c->ev_t[2], s));
-    // metadata CRC (+ tail, header) on a side stream beside the payload gather
-    CK(cudaEventRecord(c->ev_fork, s));
-    CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-    launch_crc_meta(launch_of(c, c->aux), crc_args(c, img, nullptr), crc_max_len(c));
-    CK(cudaEventRecord(c->ev_join, c->aux));
-    Launch L = launch_of(c, s);
-    launch_gather(L, gather_args(c, 0, img, 0, true, 0, UINT64_MAX), c->max_units);
-    if (timing) CK(cudaEventRecord(c->ev_t[3], s));
-    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
-    CK_LAUNCH();
-    if (timing) CK(cudaEventRecord(c->ev_t[4], s));
-    CK(cudaEventRecord(c->ev_done, s));
+    static const bool graphs_on = getenv("CRUM_NO_GRAPH") == nullptr;
+    if (!rep && graphs_on) {
+        // asynchronous call: replay the captured sequence (one launch instead of
+        // ~8 API calls; the small configurations are launch-bound)
+        if ((st = gather_dev_graph(c, s, img, capacity, flags, timing)) != CRUM_E_BUSY) {
+            if (st == CRUM_OK) {
+                c->last_kind = kLastDevGather;
+                c->last_timed = timing;
+                c->last_path = 0;
+            }
+            return st;
+        }
+        // capture not possible here: enqueue directly
+    }
+    if ((st = enqueue_gather_dev(c, s, img, capacity, full, timing))) return st;
     c->last_path = 0;
     c->last_kind = kLastDevGather;
     c->last_timed = timing;

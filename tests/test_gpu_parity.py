@@ -360,3 +360,40 @@ def test_tracked_mode_parity(crum):
     torch.cuda.synchronize()
     for z, h in zip(zs, p.host):
         assert np.array_equal(z.cpu().numpy(), h)
+
+
+def test_async_device_gather_graph_replays(crum):
+    """The asynchronous device gather is captured once as a CUDA graph and
+    replayed: replays, a second image buffer (recapture) and a registration
+    in between (invalidation) all stay bit-exact with the oracle."""
+    p = mkpair(MIXED[:5], 18)
+    cap = p.g.image_required_bytes()
+    bufs = [torch.empty(cap + 256, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    st, want, _ = p.o.checkpoint_gather()
+    p.g.checkpoint_gather_device(bufs[0], cap)                 # epoch 0 (with report)
+    for epoch in range(1, 9):
+        p.write(epoch, 0.2 if epoch % 3 else 0.0)
+        st, want, _ = p.o.checkpoint_gather()
+        b = bufs[(epoch // 3) % 2]
+        n0 = p.g.launch_count
+        p.g.checkpoint_gather_device(b, cap, report=False)     # graph replay (or capture)
+        torch.cuda.synchronize()
+        assert p.g.launch_count > n0                           # replays count their kernels
+        assert b[:len(want)].cpu().numpy().tobytes() == want.tobytes(), epoch
+        assert p.shadows_equal(), epoch
+    # a new region invalidates the captured graph
+    from oracle import oracle
+    nb, P = 3 * 4096 + 5, 4096
+    h = oracle.aligned_empty(nb)
+    synth.fill_region(h, synth.seed(19), 9)
+    d = torch.from_numpy(h.copy()).cuda()
+    p.o.register(h, P, C)
+    p.g.register_region(d, nb, P, C)
+    cap = p.g.image_required_bytes()
+    big = torch.empty(cap + 256, dtype=torch.uint8, device="cuda")
+    for epoch in (20, 21):
+        p.write(epoch, 0.3)
+        st, want, _ = p.o.checkpoint_gather()
+        p.g.checkpoint_gather_device(big, cap, report=False)
+        torch.cuda.synchronize()
+        assert big[:len(want)].cpu().numpy().tobytes() == want.tobytes(), epoch
