@@ -166,9 +166,19 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_count(CompactArgs a
     }
 }
 
+constexpr uint32_t kRegAgg = 64;  // per-block region counters kept in shared memory
+
 __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a) {
     __shared__ uint64_t s_off[2];
     __shared__ bool s_last;
+    // per-region dirty counts are aggregated in shared memory for the (usually
+    // one or few) regions this block's pages fall in, then added once per block
+    // (per-thread atomics on one global counter serialise at L2)
+    __shared__ uint32_t s_rcnt[kRegAgg];
+    __shared__ uint32_t s_r0;
+    if (threadIdx.x < kRegAgg) s_rcnt[threadIdx.x] = 0;
+    if (threadIdx.x == 0)
+        s_r0 = region_of_page(a.regs, a.R, a.p_lo + (uint64_t)blockIdx.x * kPagesPerCompactBlock);
     // offsets of this block = running totals before this range + earlier blocks
     uint64_t pc = 0, pu = 0;
     for (uint32_t i = threadIdx.x; i < blockIdx.x; i += blockDim.x) {
@@ -207,7 +217,10 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a
             const int b = __ffs(m) - 1;
             const uint64_t gid = base + b;
             while (gid >= next) {
-                if (cnt) atomicAdd(a.reg_nd + r, cnt);
+                if (cnt) {
+                    if (r - s_r0 < kRegAgg) atomicAdd(&s_rcnt[r - s_r0], cnt);
+                    else atomicAdd(a.reg_nd + r, cnt);
+                }
                 cnt = 0;
                 ++r;
                 g = a.regs[r];
@@ -224,8 +237,14 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a
             upos += 1ull << (g.log2p - kSegLog2);
             m &= m - 1;
         }
-        if (cnt) atomicAdd(a.reg_nd + r, cnt);
+        if (cnt) {
+            if (r - s_r0 < kRegAgg) atomicAdd(&s_rcnt[r - s_r0], cnt);
+            else atomicAdd(a.reg_nd + r, cnt);
+        }
     }
+    __syncthreads();
+    if (threadIdx.x < kRegAgg && s_rcnt[threadIdx.x] && s_r0 + threadIdx.x < a.R)
+        atomicAdd(a.reg_nd + s_r0 + threadIdx.x, s_rcnt[threadIdx.x]);
     dbytes = warp_sum(dbytes);
     if ((threadIdx.x & 31) == 0 && dbytes)
         atomicAdd(reinterpret_cast<unsigned long long *>(&a.st->dirty_bytes), (unsigned long long)dbytes);
