@@ -440,6 +440,28 @@ def main():
                                "(median); the regions being checkpointed live in HBM by definition",
                        "link_GBs": (round(e2e_reps[-1]["image_bytes"] / e2e_reps[-1]["t_copy_ms"] / 1e6, 2)
                                     if e2e_reps[-1]["t_copy_ms"] > 0 else None)}
+        # host-link roofline: a plain pinned D2H copy of the same size, timed live
+        nb = max(min(e2e_reps[-1]["image_bytes"], 1 << 30), 1 << 20)
+        hsrc = torch.empty(nb, dtype=torch.uint8, device=dev)
+        hdst = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+        l_ms = []
+        for _ in range(3):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            with torch.cuda.stream(stream):
+                hdst.copy_(hsrc, non_blocking=True)
+            b_.record(stream)
+            b_.synchronize()
+            l_ms.append(a_.elapsed_time(b_))
+        link_peak = nb / (min(l_ms) / 1e3) / 1e9
+        # the copy-out overlaps detection, so the e2e bound is the slower of the
+        # link copy of the image and the device-only step
+        e2e_ideal = world * F / max(e2e_reps[-1]["image_bytes"] / (link_peak * 1e9), T / args.steps)
+        line["e2e"]["link_roofline"] = {"peak_GBs": round(link_peak, 2), "source": "pinned D2H copy of the "
+                                        "image's size timed in this run",
+                                        "frac": round(line["e2e"]["value"] / (e2e_ideal / 1e9), 4),
+                                        "ideal_value": round(e2e_ideal / 1e9, 1)}
+        del hsrc, hdst
         # restore of the last image onto the live regions (H2D inside)
         r_ms = []
         for i in range(3):
