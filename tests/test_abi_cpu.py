@@ -62,6 +62,19 @@ def test_cpu_side_argument_checks(crum):
     assert L.crum_destroy(None) == crum.E_INVAL
     assert L.crum_sync_shadow(None, None, None) == crum.E_INVAL
     assert L.crum_image_destroy(None) == crum.E_INVAL
+    # the widened rows' calls reject null handles before touching CUDA
+    assert L.crum_image_persist(None, b"/tmp/x", 0) == crum.E_INVAL
+    assert L.crum_image_persist_wait(None) == crum.E_INVAL
+    busy = C.c_int(7)
+    assert L.crum_image_persist_busy(None, C.byref(busy)) == crum.E_INVAL
+    assert L.crum_image_load(None, None, C.byref(h)) == crum.E_INVAL
+    assert L.crum_image_load(None, b"/nonexistent/crum/image", C.byref(h)) == crum.E_IO
+    assert L.crum_restore_begin(None, None, None, 0, C.byref(h)) == crum.E_INVAL
+    cov, res = C.c_uint64(), C.c_uint64()
+    assert L.crum_restore_fetch(None, 1, 0, None, C.byref(cov), C.byref(res)) == crum.E_INVAL
+    assert L.crum_restore_end(None, None, None) == crum.E_INVAL
+    assert L.crum_mark_dirty_pages(None, 1, None, 0, None) == crum.E_INVAL
+    assert L.crum_status_string(crum.E_IO) == b"file I/O error"
     try:
         import torch
         has_gpu = torch.cuda.is_available()
