@@ -411,7 +411,8 @@ def main():
     clk = clocks.stop()
     # context for fractions above 1.0: a plain streaming READ (no writes) of the
     # first HBM region, timed the same way; the denominator stays the measured copy
-    rd_t = regions[0] if regions[0].is_cuda else scrub
+    dev_regs = [t for t in regions if t.is_cuda]
+    rd_t = max(dev_regs + [scrub], key=lambda t: t.numel())  # the largest HBM buffer
     rd_n = min(rd_t.numel(), GiB) // 32 * 32
     e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     rd_ms = []
