@@ -147,13 +147,19 @@ struct crum_ctx {
     uint32_t last_path = 0;                   // CRUM_PATH_* bits of the last gather
     // CUDA graph of the asynchronous device gather (one cached instance)
     cudaStream_t gcap = nullptr;              // capture stream
-    cudaGraphExec_t g_exec = nullptr;
-    uint64_t g_nk = 0;                        // kernels per replay
     uint64_t graph_epoch = 1;                 // bumped by every allocation / rebuild
-    uint64_t g_epoch = 0;
-    uint8_t *g_img = nullptr;
-    uint64_t g_cap = 0;
-    uint32_t g_flags = 0;
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        uint64_t nk = 0;                      // kernels per replay
+        uint64_t epoch = 0;
+        uint8_t *img = nullptr;
+        uint64_t cap = 0;
+        uint32_t flags = 0;
+        uint64_t used = 0;                    // LRU stamp
+    };
+    static constexpr int kGraphs = 4;         // e.g. two alternating images x {device, host}
+    GraphEntry graphs[kGraphs];
+    uint64_t graph_clock = 0;
     int sms = 148;
     uint64_t chunk = kDefaultChunk;
     std::vector<HostRegion> regs;
@@ -561,6 +567,10 @@ int ensure_z(crum_ctx *c, uint64_t units) {
     return CRUM_OK;
 }
 
+// Host images whose worst case is at most this (and at most one pipeline
+// chunk) take the zero-copy path.
+constexpr uint64_t kSmallImage = 16ull << 20;
+
 int ensure_ring(crum_ctx *c, uint64_t min_bytes = 0) {
     const uint64_t want = std::max(c->chunk, min_bytes);
     if (c->ring_cap >= want) return CRUM_OK;
@@ -892,7 +902,8 @@ int crum_destroy(crum_ctx *c) {
     if (c->copy) cudaStreamDestroy(c->copy);
     if (c->gstream) cudaStreamDestroy(c->gstream);
     if (c->aux) cudaStreamDestroy(c->aux);
-    if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+    for (auto &g : c->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     if (c->gcap) cudaStreamDestroy(c->gcap);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -1282,11 +1293,20 @@ int enqueue_gather_dev(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capac
 // generation, then replayed on `s`.  CRUM_E_BUSY: capture unavailable, the
 // caller enqueues directly.
 int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, uint32_t flags, bool timing) {
-    if (c->g_exec == nullptr || c->g_epoch != c->graph_epoch || c->g_img != img || c->g_cap != capacity ||
-        c->g_flags != flags) {
-        if (c->g_exec) {
-            cudaGraphExecDestroy(c->g_exec);
-            c->g_exec = nullptr;
+    flags |= timing ? 0x80000000u : 0u;  // the key includes whether events are recorded
+    crum_ctx::GraphEntry *e = nullptr, *victim = &c->graphs[0];
+    for (auto &g : c->graphs) {
+        if (g.exec && g.epoch == c->graph_epoch && g.img == img && g.cap == capacity && g.flags == flags) {
+            e = &g;
+            break;
+        }
+        if (!g.exec || g.used < victim->used) victim = &g;
+    }
+    if (!e) {
+        e = victim;
+        if (e->exec) {
+            cudaGraphExecDestroy(e->exec);
+            e->exec = nullptr;
         }
         const uint64_t l0 = c->launches;
         if (cudaStreamBeginCapture(c->gcap, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
@@ -1295,29 +1315,30 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
         }
         const int st = enqueue_gather_dev(c, c->gcap, img, capacity, (flags & CRUM_FULL) != 0, timing, true);
         cudaGraph_t g = nullptr;
-        const cudaError_t e = cudaStreamEndCapture(c->gcap, &g);
+        const cudaError_t ce = cudaStreamEndCapture(c->gcap, &g);
         const uint64_t nk = c->launches - l0;
         c->launches = l0;
-        if (st || e != cudaSuccess || !g) {
+        if (st || ce != cudaSuccess || !g) {
             if (g) cudaGraphDestroy(g);
             cudaGetLastError();
             return st ? st : CRUM_E_BUSY;
         }
-        const cudaError_t ei = cudaGraphInstantiate(&c->g_exec, g, 0);
+        const cudaError_t ei = cudaGraphInstantiate(&e->exec, g, 0);
         cudaGraphDestroy(g);
         if (ei != cudaSuccess) {
             cudaGetLastError();
-            c->g_exec = nullptr;
+            e->exec = nullptr;
             return CRUM_E_BUSY;
         }
-        c->g_nk = nk;
-        c->g_epoch = c->graph_epoch;
-        c->g_img = img;
-        c->g_cap = capacity;
-        c->g_flags = flags;
+        e->nk = nk;
+        e->epoch = c->graph_epoch;
+        e->img = img;
+        e->cap = capacity;
+        e->flags = flags;
     }
-    CK(cudaGraphLaunch(c->g_exec, s));
-    c->launches += c->g_nk;
+    e->used = ++c->graph_clock;
+    CK(cudaGraphLaunch(e->exec, s));
+    c->launches += e->nk;
     return CRUM_OK;
 }
 
@@ -1626,10 +1647,34 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
         return st ? st : gather_z_host(c, img, s, full, rep);
     }
     c->last_path = 0;
-    int st = ensure_ring(c);
-    if (st) return st;
     uint64_t worst;
     crum_image_required_bytes(c, UINT64_MAX, &worst);
+    static const bool graphs_on = getenv("CRUM_NO_GRAPH") == nullptr;
+    if (worst <= std::min(kSmallImage, c->chunk) && img->cap >= worst) {
+        // small footprint: latency-bound, so run the device sequence (a replayed
+        // graph) with the image's mapped address as the destination -- the
+        // kernels' stores cross the host link directly, no staging, no copies
+        void *dimg = nullptr;
+        CK(cudaHostGetDevicePointer(&dimg, img->host, 0));
+        uint8_t *d = static_cast<uint8_t *>(dimg);
+        int st = graphs_on ? gather_dev_graph(c, s, d, img->cap, flags, true) : CRUM_E_BUSY;
+        if (st == CRUM_E_BUSY) st = enqueue_gather_dev(c, s, d, img->cap, full, true);
+        if (st) return st;
+        c->last_kind = kLastDevGather;
+        c->last_timed = true;
+        CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const DevStats h = *c->h_st;
+        img->len = h.image_bytes;
+        if (rep) {
+            memset(rep, 0, sizeof *rep);
+            fill_report(c, h, rep);
+            fill_times(c, rep);
+        }
+        return CRUM_OK;
+    }
+    int st = ensure_ring(c);
+    if (st) return st;
     const bool pipelined = img->cap >= worst;
     const uint32_t nr = (uint32_t)c->ranges.size();
     const uint64_t poff = payload_offset_for(c->regs.size());
