@@ -20,6 +20,8 @@
 //    CRC shifted to its position by a GF(2)[x] product with x^(8*after) mod
 //    P, XOR-reduced; the last block finalises and writes the header.  The
 //    kernel also copies ids/hashes from scratch into the image tail.
+#include <cstdlib>
+
 #include "crum_internal.cuh"
 
 namespace crum {
@@ -166,6 +168,66 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_count(CompactArgs a
     }
 }
 
+// Final range: per-region prefix sums (first slot, payload offset, unit
+// offset), the image table, header fields and the capacity verdict.
+__device__ void compact_finalize(const CompactArgs &a, uint64_t K, uint64_t U) {
+    // per-region prefix sums (first slot, payload offset, unit offset) + table
+    uint64_t carry_first = 0, carry_units = 0;
+    for (uint32_t r0 = 0; r0 < a.R; r0 += blockDim.x) {
+        const uint32_t r = r0 + threadIdx.x;
+        uint64_t nd = 0, un = 0;
+        DevRegion g{};
+        if (r < a.R) {
+            g = a.regs[r];
+            nd = *(volatile uint32_t *)(a.reg_nd + r);
+            un = nd << (g.log2p - kSegLog2);
+        }
+        uint64_t tn, tun;
+        const uint64_t en = block_excl_scan(nd, &tn);
+        const uint64_t eun = block_excl_scan(un, &tun);
+        if (r < a.R) {
+            RegStat s;
+            s.first = carry_first + en;
+            s.n_dirty = nd;
+            s.unit_base = carry_units + eun;
+            s.payload_base = s.unit_base << kSegLog2;
+            a.rs[r] = s;
+            if (a.head) {
+                uint8_t *e = a.head + 64 + 48ull * r;
+                reinterpret_cast<uint32_t *>(e)[0] = g.id;
+                reinterpret_cast<uint32_t *>(e)[1] = g.mode;
+                reinterpret_cast<uint64_t *>(e)[1] = g.bytes;
+                reinterpret_cast<uint64_t *>(e)[2] = 1ull << g.log2p;
+                reinterpret_cast<uint64_t *>(e)[3] = g.n_pages;
+                reinterpret_cast<uint64_t *>(e)[4] = nd;
+                reinterpret_cast<uint64_t *>(e)[5] = s.first;
+            }
+        }
+        carry_first += tn;
+        carry_units += tun;
+    }
+    const uint64_t poff = round_up(64 + 48ull * a.R, 4096);
+    const uint64_t payload = U << kSegLog2;
+    (void)carry_units;
+    const uint64_t ids_off = poff + payload;
+    const uint64_t image = ids_off + round_up(4 * K, 8) + (a.has_hashes ? 8 * K : 0);
+    if (a.head)
+        for (uint64_t b = 64 + 48ull * a.R + threadIdx.x; b < poff; b += blockDim.x) a.head[b] = 0;
+    if (threadIdx.x == 0) {
+        DevStats *st = a.st;
+        st->K = K;
+        st->total_units = U;
+        st->poff = poff;
+        st->payload_bytes = payload;
+        st->ids_off = ids_off;
+        st->image_bytes = image;
+        st->capacity = a.capacity;
+        st->status = image > a.capacity ? kStCapacity : kStOk;
+        st->img_flags = (a.full ? 1u : 0u) | (a.has_hashes ? 2u : 0u);
+        st->n_regions = a.R;
+    }
+}
+
 constexpr uint32_t kRegAgg = 64;  // per-block region counters kept in shared memory
 
 __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a) {
@@ -273,67 +335,180 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a
         }
         *a.done = 0;
     }
-    if (!a.final_range) return;
-    // per-region prefix sums (first slot, payload offset, unit offset) + table
-    uint64_t carry_first = 0, carry_units = 0;
-    for (uint32_t r0 = 0; r0 < a.R; r0 += blockDim.x) {
-        const uint32_t r = r0 + threadIdx.x;
-        uint64_t nd = 0, un = 0;
-        DevRegion g{};
-        if (r < a.R) {
-            g = a.regs[r];
-            nd = *(volatile uint32_t *)(a.reg_nd + r);
-            un = nd << (g.log2p - kSegLog2);
+    if (a.final_range) compact_finalize(a, K, U);
+}
+
+// ---------------------------------------------------------------------------
+// A2 in one pass (default): the blocks take logical ids from a ticket, publish
+// their (pages, units) aggregates in 64-bit status words and find their
+// exclusive prefix by decoupled look-back (so a block never waits on one that
+// has not started), then write ids / unit offsets as k_compact_write does.
+// Status word: [63:62] 1 aggregate / 2 inclusive prefix, [61:31] pages,
+// [30:0] 4 KiB units.  The words (blk_units reinterpreted) and the ticket
+// (done[2]) are reset by the last block, so every launch starts from zero.
+// On the first range logical block 0 zeroes the per-call accumulators before
+// it publishes; every other block touches them only after its look-back.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t cpack(uint64_t flag, uint64_t cnt, uint64_t units) {
+    return (flag << 62) | ((cnt & 0x7fffffffull) << 31) | (units & 0x7fffffffull);
+}
+__device__ __forceinline__ void st_rel64(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acq64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs a) {
+    __shared__ uint64_t s_off[2];
+    __shared__ uint32_t s_blk;
+    __shared__ bool s_last;
+    __shared__ uint32_t s_rcnt[kRegAgg];
+    __shared__ uint32_t s_r0;
+    uint64_t *status = a.blk_units;
+    uint32_t *ticket = a.done + 2;
+    if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
+    if (threadIdx.x < kRegAgg) s_rcnt[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t blk = s_blk;
+    if (threadIdx.x == 0) s_r0 = region_of_page(a.regs, a.R, a.p_lo + (uint64_t)blk * kPagesPerCompactBlock);
+    if (a.first_range && blk == 0) {
+        for (uint32_t r = threadIdx.x; r < a.R; r += blockDim.x) a.reg_nd[r] = 0;
+        if (threadIdx.x == 0) {
+            a.st->dirty_bytes = 0;
+            a.st->dirty_runs = 0;
+            a.st->crc_acc = 0;
+            a.st->status = kStOk;
         }
-        uint64_t tn, tun;
-        const uint64_t en = block_excl_scan(nd, &tn);
-        const uint64_t eun = block_excl_scan(un, &tun);
-        if (r < a.R) {
-            RegStat s;
-            s.first = carry_first + en;
-            s.n_dirty = nd;
-            s.unit_base = carry_units + eun;
-            s.payload_base = s.unit_base << kSegLog2;
-            a.rs[r] = s;
-            if (a.head) {
-                uint8_t *e = a.head + 64 + 48ull * r;
-                reinterpret_cast<uint32_t *>(e)[0] = g.id;
-                reinterpret_cast<uint32_t *>(e)[1] = g.mode;
-                reinterpret_cast<uint64_t *>(e)[1] = g.bytes;
-                reinterpret_cast<uint64_t *>(e)[2] = 1ull << g.log2p;
-                reinterpret_cast<uint64_t *>(e)[3] = g.n_pages;
-                reinterpret_cast<uint64_t *>(e)[4] = nd;
-                reinterpret_cast<uint64_t *>(e)[5] = s.first;
+        __threadfence();
+    }
+    const uint64_t base = a.p_lo + (uint64_t)blk * kPagesPerCompactBlock + threadIdx.x * kPagesPerThread;
+    uint32_t m = thread_mask(a, base);
+    if (base < a.p_hi) {  // consume this range's detect marks (see k_compact_write)
+        if (base >= a.p_lo && base + kPagesPerThread <= a.p_hi) {
+            *reinterpret_cast<uint4 *>(a.flags + base) = make_uint4(0, 0, 0, 0);
+        } else {
+            for (uint32_t b = 0; b < kPagesPerThread; ++b)
+                if (base + b >= a.p_lo && base + b < a.p_hi) a.flags[base + b] = 0;
+        }
+    }
+    uint64_t tc, tu;
+    const uint64_t ec = block_excl_scan(__popc(m), &tc);
+    const uint64_t eu = block_excl_scan(mask_units(a, base, m), &tu);  // syncs: s_r0 visible
+    if (threadIdx.x < 32) {
+        const uint32_t lane = threadIdx.x;
+        uint64_t pc = 0, pu = 0;
+        if (blk == 0) {
+            if (lane == 0) st_rel64(status, cpack(2, tc, tu));
+        } else {
+            if (lane == 0) st_rel64(status + blk, cpack(1, tc, tu));
+            int64_t top = (int64_t)blk - 1;
+            while (top >= 0) {
+                const int64_t idx = top - (int64_t)lane;
+                uint64_t v = cpack(2, 0, 0);  // before block 0: prefix 0
+                uint32_t flag = 2;
+                if (idx >= 0) {
+                    do {
+                        v = ld_acq64(status + idx);
+                        flag = (uint32_t)(v >> 62);
+                    } while (flag == 0);
+                }
+                const uint32_t pm = __ballot_sync(0xffffffffu, flag == 2);
+                const int first = pm ? __ffs(pm) - 1 : 32;
+                const uint64_t c = ((int)lane <= first) ? ((v >> 31) & 0x7fffffffull) : 0;
+                const uint64_t u = ((int)lane <= first) ? (v & 0x7fffffffull) : 0;
+                pc += warp_sum(c);
+                pu += warp_sum(u);
+                if (pm) break;
+                top -= 32;
             }
+            if (lane == 0) st_rel64(status + blk, cpack(2, pc + tc, pu + tu));
         }
-        carry_first += tn;
-        carry_units += tun;
+        if (lane == 0) {
+            s_off[0] = a.rb[a.c].k + pc;
+            s_off[1] = a.rb[a.c].units + pu;
+        }
     }
-    const uint64_t poff = round_up(64 + 48ull * a.R, 4096);
-    const uint64_t payload = U << kSegLog2;
-    (void)carry_units;
-    const uint64_t ids_off = poff + payload;
-    const uint64_t image = ids_off + round_up(4 * K, 8) + (a.has_hashes ? 8 * K : 0);
-    if (a.head)
-        for (uint64_t b = 64 + 48ull * a.R + threadIdx.x; b < poff; b += blockDim.x) a.head[b] = 0;
+    __syncthreads();
+    uint64_t pos = s_off[0] + ec, upos = s_off[1] + eu;
+    uint64_t dbytes = 0;
+    if (m) {
+        uint32_t r = region_of_page(a.regs, a.R, base + (__ffs(m) - 1));
+        DevRegion g = a.regs[r];
+        uint64_t next = (r + 1 < a.R) ? a.regs[r + 1].page_base : ~0ull;
+        uint32_t cnt = 0;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            const uint64_t gid = base + b;
+            while (gid >= next) {
+                if (cnt) {
+                    if (r - s_r0 < kRegAgg) atomicAdd(&s_rcnt[r - s_r0], cnt);
+                    else atomicAdd(a.reg_nd + r, cnt);
+                }
+                cnt = 0;
+                ++r;
+                g = a.regs[r];
+                next = (r + 1 < a.R) ? a.regs[r + 1].page_base : ~0ull;
+            }
+            const uint64_t i = gid - g.page_base;
+            a.gids[pos] = (uint32_t)gid;
+            a.sunit[pos] = upos;
+            a.lids[pos] = (uint32_t)i;
+            if (a.has_hashes) a.lhash[pos] = (g.mode == kModeHash) ? a.newhash[gid] : 0;
+            dbytes += page_len(g, i);
+            ++cnt;
+            ++pos;
+            upos += 1ull << (g.log2p - kSegLog2);
+            m &= m - 1;
+        }
+        if (cnt) {
+            if (r - s_r0 < kRegAgg) atomicAdd(&s_rcnt[r - s_r0], cnt);
+            else atomicAdd(a.reg_nd + r, cnt);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < kRegAgg && s_rcnt[threadIdx.x] && s_r0 + threadIdx.x < a.R)
+        atomicAdd(a.reg_nd + s_r0 + threadIdx.x, s_rcnt[threadIdx.x]);
+    dbytes = warp_sum(dbytes);
+    if ((threadIdx.x & 31) == 0 && dbytes)
+        atomicAdd(reinterpret_cast<unsigned long long *>(&a.st->dirty_bytes), (unsigned long long)dbytes);
+    // ---- last block: totals, reset of the look-back state, finalise ----
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(a.done, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const uint64_t vlast = ld_acq64(status + gridDim.x - 1);  // inclusive prefix of the last block
+    const uint64_t K = a.rb[a.c].k + ((vlast >> 31) & 0x7fffffffull);
+    const uint64_t U = a.rb[a.c].units + (vlast & 0x7fffffffull);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) status[i] = 0;
     if (threadIdx.x == 0) {
-        DevStats *st = a.st;
-        st->K = K;
-        st->total_units = U;
-        st->poff = poff;
-        st->payload_bytes = payload;
-        st->ids_off = ids_off;
-        st->image_bytes = image;
-        st->capacity = a.capacity;
-        st->status = image > a.capacity ? kStCapacity : kStOk;
-        st->img_flags = (a.full ? 1u : 0u) | (a.has_hashes ? 2u : 0u);
-        st->n_regions = a.R;
+        a.rb[a.c + 1].k = K;
+        a.rb[a.c + 1].units = U;
+        if (a.rb_host) {
+            volatile RangeTotals *h = a.rb_host + a.c + 1;
+            h->k = K;
+            h->units = U;
+        }
+        *a.done = 0;
+        *ticket = 0;
     }
+    if (a.final_range) compact_finalize(a, K, U);
 }
 
 void launch_compact(const Launch &L, const CompactArgs &a) {
     uint64_t nblk = a.p_hi > a.p_lo ? (a.p_hi - a.p_lo + kPagesPerCompactBlock - 1) / kPagesPerCompactBlock : 0;
     if (nblk == 0) nblk = 1;  // an empty range still publishes its totals / finalises
+    static const bool two_pass = getenv("CRUM_COMPACT2") != nullptr;
+    if (!two_pass) {
+        k_compact_onepass<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(a);
+        ++*L.counter;
+        return;
+    }
     k_compact_count<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(a);
     k_compact_write<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(a);
     *L.counter += 2;

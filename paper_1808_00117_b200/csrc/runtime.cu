@@ -434,6 +434,8 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
         c->page_cap = cap;
     }
     CK(cudaMemset(c->d_flags, 0, c->page_cap));
+    // single-pass compaction: look-back status words start (and are left) zero
+    CK(cudaMemset(c->d_blk_units, 0, 8 * (c->page_cap / kPagesPerCompactBlock + 1)));
     c->tag = 0;
     dev_free(c->d_force);
     c->d_force = force;
