@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--content", default="random", choices=["random", "half"],
                     help="half: the paper's 50%%-random vectors (PAPER.md:907-912): second half of every "
                          "region one repeated fp32 value; the writer then rewrites one word per dirty page")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test the multi-rank path with several ranks sharing fewer GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -307,12 +309,16 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     distributed = world > 1
     if distributed:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
+    red_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")  # where collectives run
     stream = torch.cuda.Stream(device=dev)
     if args.config == "c5":
         args.mode = "hash"  # C5 is defined in hash mode
@@ -428,7 +434,7 @@ def main():
     T = sum(step_ms) / 1e3
     det_ms = [r["t_gather_ms"] if args.mode == "tracked" else r["t_detect_ms"] for r in reps]
     if distributed:
-        t = torch.tensor([T, sum(det_ms)], dtype=torch.float64, device=dev)
+        t = torch.tensor([T, sum(det_ms)], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         T, det_sum = float(t[0]), float(t[1])
     else:
@@ -503,7 +509,7 @@ def main():
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         te = statistics.median(e2e_ms) / 1e3
         if distributed:
-            t = torch.tensor([te], dtype=torch.float64, device=dev)
+            t = torch.tensor([te], dtype=torch.float64, device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t[0])
         line["e2e"] = {"value": round(world * F / te / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
