@@ -108,6 +108,7 @@ struct CompactArgs {
     uint64_t *blk_units;   // per-block 4 KiB units
     uint32_t *gids;        // slot -> global page id
     uint64_t *sunit;       // slot -> payload unit offset
+    uint32_t *u2s;         // payload unit -> slot (every unit of every listed page)
     uint32_t *lids;        // slot -> region-local page id (image ids)
     uint64_t *lhash;       // slot -> XXH3 (hash regions) or 0 (image hashes)
     uint32_t *reg_nd;      // per-region dirty count
@@ -129,6 +130,7 @@ struct GatherArgs {
     int add_poff;
     const uint32_t *gids;
     const uint64_t *sunit;
+    const uint32_t *u2s;
     const uint64_t *newhash;
     const RangeTotals *rb;
     const DevStats *st;

@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a
             const uint64_t i = gid - g.page_base;
             a.gids[pos] = (uint32_t)gid;
             a.sunit[pos] = upos;
+            for (uint32_t j = 0; j < (1u << (g.log2p - kSegLog2)); ++j) a.u2s[upos + j] = (uint32_t)pos;
             a.lids[pos] = (uint32_t)i;
             if (a.has_hashes) a.lhash[pos] = (g.mode == kModeHash) ? a.newhash[gid] : 0;
             dbytes += page_len(g, i);
@@ -455,6 +456,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs
             const uint64_t i = gid - g.page_base;
             a.gids[pos] = (uint32_t)gid;
             a.sunit[pos] = upos;
+            for (uint32_t j = 0; j < (1u << (g.log2p - kSegLog2)); ++j) a.u2s[upos + j] = (uint32_t)pos;
             a.lids[pos] = (uint32_t)i;
             if (a.has_hashes) a.lhash[pos] = (g.mode == kModeHash) ? a.newhash[gid] : 0;
             dbytes += page_len(g, i);
@@ -583,7 +585,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     const uint64_t ntask = (u_hi - u_lo + upt - 1) / upt;
     for (uint64_t t = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5); t < ntask; t += nwarps) {
         const uint64_t u0 = u_lo + t * upt, u1 = min(u0 + upt, u_hi);
-        uint64_t k = slot_of_unit(a.sunit, k_lo, k_hi, u0);
+        uint64_t k = a.u2s[u0];  // slot of the task's first unit (compaction's map)
         uint64_t gid = a.gids[k];
         uint32_t r = region_of_page(a.regs, a.R, gid);
         DevRegion g = a.regs[r];
@@ -1305,7 +1307,7 @@ struct ZCursor {
     uint32_t r;
     DevRegion g;
     __device__ ZCursor(const GatherArgs &a_, uint64_t k_lo, uint64_t k_hi_, uint64_t u0) : a(a_), k_hi(k_hi_) {
-        k = slot_of_unit(a.sunit, k_lo, k_hi, u0);
+        k = a.u2s[u0];
         gid = a.gids[k];
         r = region_of_page(a.regs, a.R, gid);
         g = a.regs[r];
@@ -1314,7 +1316,7 @@ struct ZCursor {
     __device__ ZUnit at(uint64_t u) {  // u >= the previous call's u
         const uint64_t nxt = (k + 1 < k_hi) ? a.sunit[k + 1] : ~0ull;
         if (u >= nxt) {
-            k = slot_of_unit(a.sunit, k, k_hi, u);
+            k = a.u2s[u];
             kbase = a.sunit[k];
             gid = a.gids[k];
             if (r + 1 < a.R && gid >= a.regs[r + 1].page_base) {

@@ -200,6 +200,8 @@ struct crum_ctx {
     uint64_t *d_newhash = nullptr;
     uint32_t *d_gids = nullptr;
     uint64_t *d_sunit = nullptr;
+    uint32_t *d_u2s = nullptr;     // payload unit -> slot (written by compaction)
+    uint64_t u2s_cap = 0;
     uint32_t *d_lids = nullptr;
     uint64_t *d_lhash = nullptr;
     uint32_t *d_blk_count = nullptr;
@@ -470,6 +472,12 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
     c->N = N;
     c->F = F;
     c->max_units = units;
+    if (units + 1 > c->u2s_cap) {
+        dev_free(c->d_u2s);
+        c->u2s_cap = 0;
+        if ((st = dev_alloc(c, &c->d_u2s, 4 * (units + 1)))) return st;
+        c->u2s_cap = units + 1;
+    }
     // single-pass eligibility and its tile map
     {
         bool ok = R > 0 && (units >> 27) == 0;
@@ -650,6 +658,7 @@ CompactArgs compact_args(crum_ctx *c, const Range &rg, uint32_t ci, bool first, 
     a.blk_units = c->d_blk_units;
     a.gids = c->d_gids;
     a.sunit = c->d_sunit;
+    a.u2s = c->d_u2s;
     a.lids = c->d_lids;
     a.lhash = c->d_lhash;
     a.reg_nd = c->d_reg_nd;
@@ -690,6 +699,7 @@ GatherArgs gather_args(crum_ctx *c, uint32_t ci, uint8_t *dst, uint64_t dst_unit
     a.add_poff = add_poff ? 1 : 0;
     a.gids = c->d_gids;
     a.sunit = c->d_sunit;
+    a.u2s = c->d_u2s;
     a.newhash = c->d_newhash;
     a.rb = c->d_rb + ci;
     a.st = c->d_st;
@@ -877,6 +887,7 @@ int crum_destroy(crum_ctx *c) {
     dev_free(c->d_newhash);
     dev_free(c->d_gids);
     dev_free(c->d_sunit);
+    dev_free(c->d_u2s);
     dev_free(c->d_lids);
     dev_free(c->d_lhash);
     dev_free(c->d_blk_count);
