@@ -236,7 +236,12 @@ void launch_zscan(const Launch &L, const uint16_t *zsz, DevStats *st, uint32_t *
 void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, const uint64_t *zblk, uint8_t *dst,
                    int add_poff, uint64_t u_lo, uint64_t u_hi, uint64_t off0);
 void launch_zdecode(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
-                    const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t units);
+                    const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t units, uint64_t u_lo = 0,
+                    int rebase = 0);
+void launch_zfetch(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
+                   const uint64_t *zblk, uint64_t u_lo, uint64_t u_hi, uint8_t *dst);
+void launch_zcheck(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
+                   const uint64_t *zblk, DevStats *st, uint64_t units);
 void launch_mark_pages(const Launch &L, uint8_t *force, uint64_t n_pages, const uint32_t *pages, uint64_t n);
 void launch_export_flags(const Launch &L, uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag,
                          uint8_t *out);

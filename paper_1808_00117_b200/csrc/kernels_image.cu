@@ -1519,15 +1519,18 @@ __global__ void __launch_bounds__(256, 2) k_zwrite(GatherArgs a, const uint32_t 
 // (unit u at dst + 4096u).  A bitmap whose population disagrees with the
 // unit's size is CORRUPT.
 __global__ void __launch_bounds__(256) k_zdecode(const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
-                                                const uint64_t *zblk, DevStats *st, uint8_t *dst) {
+                                                const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t u_lo,
+                                                uint64_t u_hi, int rebase) {
     if (st->status != kStOk) return;
-    const uint64_t U = st->total_units;
+    const uint64_t U = min(u_hi, st->total_units);
+    // rebase: src holds the payload from unit u_lo's encoding on (k_zfetch)
+    const uint64_t off0 = rebase ? zblk[u_lo / kZScanBlock] + zloc[u_lo] : 0;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+    for (uint64_t u = u_lo + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < U; u += nwarps) {
         const uint32_t cs = zsz[u];
-        const uint32_t *in = reinterpret_cast<const uint32_t *>(src + zblk[u / kZScanBlock] + zloc[u]);
-        uint32_t *out = reinterpret_cast<uint32_t *>(dst + (u << kSegLog2));
+        const uint32_t *in = reinterpret_cast<const uint32_t *>(src + (zblk[u / kZScanBlock] + zloc[u] - off0));
+        uint32_t *out = reinterpret_cast<uint32_t *>(dst + ((u - u_lo) << kSegLog2));
         if (cs == kSegBytes) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) out[32 * i + lane] = in[32 * i + lane];
@@ -1630,9 +1633,67 @@ void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, c
 }
 
 void launch_zdecode(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
-                    const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t units) {
+                    const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t units, uint64_t u_lo, int rebase) {
     if (!units) return;
-    k_zdecode<<<z_grid(L, units), 256, 0, L.stream>>>(src, zsz, zloc, zblk, st, dst);
+    k_zdecode<<<z_grid(L, units), 256, 0, L.stream>>>(src, zsz, zloc, zblk, st, dst, u_lo, u_lo + units, rebase);
+    ++*L.counter;
+}
+
+// Lazy restore of a compressed image: copy the encoded bytes of units
+// [u_lo, u_hi) -- one contiguous byte range of the payload -- from `src`
+// (e.g. a pinned image's mapped address) into `dst` with every thread (wide,
+// coalesced reads across the host link), so the decode then reads HBM.
+// dst receives payload bytes [off(u_lo), off(u_hi)) at dst[0..).
+__global__ void __launch_bounds__(256) k_zfetch(const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
+                                               const uint64_t *zblk, uint64_t u_lo, uint64_t u_hi, uint8_t *dst) {
+    if (u_hi <= u_lo) return;
+    const uint64_t b0 = zblk[u_lo / kZScanBlock] + zloc[u_lo];
+    const uint64_t b1 = zblk[(u_hi - 1) / kZScanBlock] + zloc[u_hi - 1] + zsz[u_hi - 1];
+    const uint64_t n4 = (b1 - b0) / 4;  // encodings are whole u32 words, offsets 4-aligned
+    const uint32_t *s4 = reinterpret_cast<const uint32_t *>(src + b0);
+    uint32_t *d4 = reinterpret_cast<uint32_t *>(dst);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n4; i += 4 * stride) {
+        const uint32_t a = s4[i], b = s4[i + stride], c = s4[i + 2 * stride], d = s4[i + 3 * stride];
+        d4[i] = a;
+        d4[i + stride] = b;
+        d4[i + 2 * stride] = c;
+        d4[i + 3 * stride] = d;
+    }
+    for (; i < n4; i += stride) d4[i] = s4[i];
+}
+
+void launch_zfetch(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
+                   const uint64_t *zblk, uint64_t u_lo, uint64_t u_hi, uint8_t *dst) {
+    if (u_hi <= u_lo) return;
+    uint64_t blocks = ((u_hi - u_lo) * 1024 + 255) / 256;  // <= one u32 per thread per unit word
+    if (blocks > (uint64_t)L.sms * 8) blocks = L.sms * 8;
+    k_zfetch<<<(unsigned)(blocks ? blocks : 1), 256, 0, L.stream>>>(src, zsz, zloc, zblk, u_lo, u_hi, dst);
+    ++*L.counter;
+}
+
+// Lazy restore of a compressed image: check every unit's bitmap population
+// against its size (the CORRUPT verdict a full decode would give) reading only
+// the 128-byte bitmaps, in place (e.g. through a pinned image's mapped address).
+__global__ void __launch_bounds__(256) k_zcheck(const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
+                                               const uint64_t *zblk, DevStats *st) {
+    const uint64_t U = st->total_units;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
+        const uint32_t cs = zsz[u];
+        if (cs == 0 || cs == kSegBytes) continue;
+        const uint32_t *in = reinterpret_cast<const uint32_t *>(src + zblk[u / kZScanBlock] + zloc[u]);
+        const uint32_t n = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(in[lane]));
+        if (128u + 4u * n != cs && lane == 0) st->status = kStCorrupt;
+    }
+}
+
+void launch_zcheck(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
+                   const uint64_t *zblk, DevStats *st, uint64_t units) {
+    if (!units) return;
+    k_zcheck<<<z_grid(L, units), 256, 0, L.stream>>>(src, zsz, zloc, zblk, st);
     ++*L.counter;
 }
 

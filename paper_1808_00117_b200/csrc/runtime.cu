@@ -843,6 +843,19 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     if (cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess) return fail(CRUM_E_CUDA);
     if (cudaStreamCreateWithFlags(&c->gcap, cudaStreamNonBlocking) != cudaSuccess) return fail(CRUM_E_CUDA);
+    {
+        // keep freed stream-ordered allocations in the device's default pool
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            // first use of the pool costs milliseconds: pay it here, not in a fault
+            void *w = nullptr;
+            if (cudaMallocAsync(&w, 8ull << 20, c->gcap) == cudaSuccess) cudaFreeAsync(w, c->gcap);
+            cudaStreamSynchronize(c->gcap);
+        }
+        cudaGetLastError();
+    }
     if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
@@ -1898,6 +1911,8 @@ struct PreparedRestore {
     const uint8_t *payload_dev = nullptr;
     uint8_t *d_payload_tmp = nullptr;  // decoded / CRUM_VERIFY staging of the payload
     bool tmp_owned = false;            // the caller frees d_payload_tmp (else it is c->d_rtmp)
+    bool z_lazy = false;               // compressed, checked but not decoded (lazy session)
+    const uint8_t *zsrc = nullptr;     // its encoded payload, device-visible (mapped)
     DevStats hst{};                    // K, dirty bytes, runs of the image
 };
 
@@ -1905,7 +1920,7 @@ struct PreparedRestore {
 // CRUM_VERIFY) before anything is written.  On return the table and tail
 // are in c->d_meta (host image) and the region stats in c->d_rs / c->d_st.
 int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img, uint64_t len, cudaStream_t s,
-                    uint32_t flags, bool timing, PreparedRestore &pr, bool cached) {
+                    uint32_t flags, bool timing, PreparedRestore &pr, bool cached, bool lazy_z = false) {
     // payload staging: the context's grow-only buffer, or one owned by the caller
     auto tmp_alloc = [&](uint8_t **q, uint64_t bytes) -> int {
         if (!cached) return dev_alloc(c, q, bytes);
@@ -2033,7 +2048,22 @@ int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img
     // compressed: decode every unit into device memory first (a bitmap that
     // disagrees with its unit's size is CORRUPT); a pinned image's encoded
     // payload crosses the link once (copy engine), then decodes from HBM
-    if (zimg) {
+    if (zimg && lazy_z && host_img && !(flags & CRUM_VERIFY)) {
+        // lazy session: check every bitmap in place now (same CORRUPT verdict
+        // as a full decode), decode windows on demand later
+        void *dp = nullptr;
+        CK(cudaHostGetDevicePointer(&dp, const_cast<uint8_t *>(host_img), 0));
+        pr.zsrc = static_cast<const uint8_t *>(dp) + p.poff;
+        pr.z_lazy = true;
+        launch_zcheck(L, pr.zsrc, d_zsz, c->d_zloc, c->d_zblk, c->d_st, zunits);
+        CK_LAUNCH();
+        CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (c->h_st->status != kStOk) {
+            set_detail("compressed unit whose bitmap disagrees with its size");
+            return CRUM_E_CORRUPT;
+        }
+    } else if (zimg) {
         const uint8_t *src = payload_dev;
         if (host_img) {
             if ((st = grow(c, &c->d_renc, &c->renc_cap, p.payload))) return st;
@@ -2200,6 +2230,10 @@ struct crum_restore_session {
     std::vector<uint64_t> window;           // per region: pages the next fault reads
     DevStats hst{};
     uint64_t restored = 0, covered_pages = 0;
+    // compressed image restored lazily: windows are decoded on demand from
+    // the pinned image (mapped) into pool buffers, unit offsets from the ctx scan
+    bool z_lazy = false;
+    const uint8_t *zsrc = nullptr;
 };
 
 namespace {
@@ -2232,6 +2266,29 @@ int session_scatter_slots(crum_restore_session *ss, uint32_t k, uint64_t klo, ui
     sa.u_lo = r.unit_base + ((klo - r.first) << sh);
     sa.u_hi = r.unit_base + ((khi - r.first) << sh);
     sa.mark = ss->d_done;
+    if (ss->z_lazy) {
+        // the window's encoded bytes cross the link once (wide zero-copy reads
+        // into a pool buffer), then decode from HBM into another
+        const uint64_t nu = sa.u_hi - sa.u_lo;
+        // window buffers from the stream-ordered pool: no device-wide
+        // synchronisation, memory reused across faults
+        const uint64_t need = nu << kSegLog2;
+        uint8_t *win = nullptr, *enc = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void **>(&win), need, s));
+        CK(cudaMallocAsync(reinterpret_cast<void **>(&enc), need, s));
+        const uint16_t *zsz = reinterpret_cast<const uint16_t *>(
+            ss->d_tail + tail_bytes_for(ss->p.K, (ss->p.flags & 2u) != 0));
+        const Launch L = launch_of(c, s);
+        launch_zfetch(L, ss->zsrc, zsz, c->d_zloc, c->d_zblk, sa.u_lo, sa.u_hi, enc);
+        launch_zdecode(L, enc, zsz, c->d_zloc, c->d_zblk, ss->d_st, win, nu, sa.u_lo, 1);
+        sa.src = win;
+        sa.src_unit0 = sa.u_lo;
+        launch_scatter(L, sa);
+        CK_LAUNCH();
+        CK(cudaFreeAsync(enc, s));
+        CK(cudaFreeAsync(win, s));
+        return CRUM_OK;
+    }
     launch_scatter(launch_of(c, s), sa);
     CK_LAUNCH();
     return CRUM_OK;
@@ -2247,7 +2304,7 @@ int crum_restore_begin(crum_ctx *ctx, crum_image *img, void *stream, uint32_t fl
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     PreparedRestore pr;
-    int st = prepare_restore(c, img->host, nullptr, img->len, s, flags, false, pr, false);
+    int st = prepare_restore(c, img->host, nullptr, img->len, s, flags, false, pr, false, true);
     if (st) {
         dev_free(pr.d_payload_tmp);
         return st;
@@ -2263,6 +2320,9 @@ int crum_restore_begin(crum_ctx *ctx, crum_image *img, void *stream, uint32_t fl
     ss->tab = pr.tab;
     ss->hst = pr.hst;
     ss->d_payload_tmp = pr.d_payload_tmp;
+    ss->z_lazy = pr.z_lazy;
+    ss->zsrc = pr.zsrc;
+
     const ParsedImage &p = ss->p;
     const uint64_t tail_len = p.image - p.ids_off;
     if ((st = dev_alloc(c, &ss->d_tail, tail_len + 16)) || (st = dev_alloc(c, &ss->d_rs, sizeof(RegStat) * (p.R + 1))) ||
@@ -2273,6 +2333,8 @@ int crum_restore_begin(crum_ctx *ctx, crum_image *img, void *stream, uint32_t fl
     }
     if (ss->d_payload_tmp) {
         ss->payload_src = ss->d_payload_tmp;
+    } else if (ss->z_lazy) {
+        ss->payload_src = nullptr;  // windows decode into pool buffers
     } else {
         void *dp = nullptr;
         CK(cudaHostGetDevicePointer(&dp, img->host, 0));
@@ -2372,7 +2434,22 @@ int crum_restore_end(crum_restore_session *ss, void *stream, crum_report *rep) {
     int st = CRUM_OK;
     if (!c->poisoned && cudaSetDevice(c->device) == cudaSuccess) {
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        if (ss->restored < ss->p.K) {
+        if (ss->restored < ss->p.K && ss->z_lazy) {
+            // compressed: the encoded payload crosses the link once, decodes in HBM
+            const uint64_t units = ss->p.upayload >> kSegLog2;
+            int e2 = grow(c, &c->d_renc, &c->renc_cap, ss->p.payload);
+            if (!e2) e2 = grow(c, &c->d_rtmp, &c->rtmp_cap, ss->p.upayload);
+            if (e2) {
+                st = e2;
+            } else {
+                cudaMemcpyAsync(c->d_renc, ss->img->host + ss->p.poff, ss->p.payload, cudaMemcpyHostToDevice, s);
+                const uint16_t *zsz = reinterpret_cast<const uint16_t *>(
+                    ss->d_tail + tail_bytes_for(ss->p.K, (ss->p.flags & 2u) != 0));
+                launch_zdecode(launch_of(c, s), c->d_renc, zsz, c->d_zloc, c->d_zblk, ss->d_st, c->d_rtmp, units, 0);
+                ss->payload_src = c->d_rtmp;
+            }
+        }
+        if (ss->restored < ss->p.K && st == CRUM_OK) {
             // every slot not yet written, in one launch (written ones skipped)
             ScatterArgs sa{};
             sa.regs = c->d_regs;
