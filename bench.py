@@ -97,6 +97,24 @@ def host_resident(args):
     return {2, 3} if args.config == "c5" else set()
 
 
+def pin_to_gpu_node(node: int):
+    """Run this rank's host threads on the CPUs of its GPU's NUMA node (the
+    library also binds the pinned images there): the copy-out of SURVEY.md
+    sec. 8(e) then stays on one socket.  No-op on single-node hosts (-1)."""
+    if node < 0:
+        return
+    try:
+        cpus = set()
+        for part in open(f"/sys/devices/system/node/node{node}/cpulist").read().strip().split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+    except (OSError, ValueError):
+        pass
+
+
 def read_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -311,6 +329,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    pin_to_gpu_node(crum.device_numa_node(local))
     distributed = world > 1
     if distributed:
         if args.dist_backend == "nccl":
@@ -475,7 +494,8 @@ def main():
                          "(the writer's dirty lines are written back there, untimed) and leaves it clean",
                    "timing": "per-step CUDA events around crum_checkpoint_gather_device on its stream; "
                              "application writer + scrub outside the events",
-                   "wall_ms_per_step_incl_writer": round(wall * 1e3 / args.steps, 3)},
+                   "wall_ms_per_step_incl_writer": round(wall * 1e3 / args.steps, 3),
+                   "gpu_numa_node": crum.device_numa_node(local)},
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1),
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "alg_bytes_per_launch": det_bytes, "avg_launch_ms": round(det_t * 1e3, 4),
@@ -516,6 +536,7 @@ def main():
                        "d2h_bytes_per_step": e2e_reps[-1]["image_bytes"], "ms_per_step": round(te * 1e3, 3),
                        "note": "crum_checkpoint_gather into pinned host memory, host wall clock per call "
                                "(median); the regions being checkpointed live in HBM by definition",
+                       "image_numa_node": img.numa_node,
                        "link_GBs": (round(e2e_reps[-1]["image_bytes"] / e2e_reps[-1]["t_copy_ms"] / 1e6, 2)
                                     if e2e_reps[-1]["t_copy_ms"] > 0 else None)}
         # host-link roofline: a plain pinned D2H copy of the same size, timed live

@@ -206,14 +206,30 @@ CRUM_API int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_pages
  * 2 bytes per 4 KiB unit of a compressed image's unit-size table). */
 CRUM_API int crum_image_required_bytes(crum_ctx *ctx, uint64_t max_dirty_pages, uint64_t *bytes_out);
 
-/* Pinned host images (cudaHostAlloc).  crum_image_import copies `len` bytes
- * into a new image (for restart from a file).  crum_image_data exposes the
- * buffer: *data_out (host pointer, owned by the image), *len_out (valid image
+/* Pinned host images, mapped into the device's address space.  On a host
+ * with more than one NUMA node the pages are placed on the node of the
+ * GPU's PCIe root (sysfs numa_node; anonymous mmap + mbind(MPOL_PREFERRED)
+ * + cudaHostRegister), so the copy-out of SURVEY.md sec. 8(e) ("pinned
+ * images must be NUMA-local to each GPU") never crosses the socket link;
+ * otherwise, or if that fails, cudaHostAlloc.  The environment variable
+ * CRUM_NUMA=<node> (read at crum_create) overrides the node, CRUM_NUMA=-1
+ * keeps the default placement.  crum_image_import copies `len` bytes into a
+ * new image (for restart from a file).  crum_image_data exposes the buffer:
+ * *data_out (host pointer, owned by the image), *len_out (valid image
  * length; 0 before the first gather), *capacity_out (may be NULL). */
 CRUM_API int crum_image_create(crum_ctx *ctx, uint64_t capacity_bytes, crum_image **out);
 CRUM_API int crum_image_import(crum_ctx *ctx, const void *bytes, uint64_t len, crum_image **out);
 CRUM_API int crum_image_data(const crum_image *img, void **data_out, uint64_t *len_out, uint64_t *capacity_out);
 CRUM_API int crum_image_destroy(crum_image *img);
+/* *node_out = the NUMA node the image's pages were bound to, -1 for default
+ * placement (single-node host, CRUM_NUMA=-1, or mbind refused by the
+ * sandbox).  Errors: INVAL (null argument). */
+CRUM_API int crum_image_numa_node(const crum_image *img, int *node_out);
+/* *node_out = the host NUMA node of CUDA device `device`'s PCIe function, or
+ * -1 when unknown or when the host has one node (callers use it to pin the
+ * rank's host threads next to its GPU).  Errors: INVAL (null node_out),
+ * DEVICE (no such device). */
+CRUM_API int crum_device_numa_node(int device, int *node_out);
 
 /* ---------------------------------------------------------------------------
  * Asynchronous ("forked") persistence, the paper's forked checkpoint

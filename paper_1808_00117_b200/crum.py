@@ -48,6 +48,7 @@ EXPORTED = (
     "crum_mark_dirty_pages", "crum_region_tracker",
     "crum_image_persist", "crum_image_persist_wait", "crum_image_persist_busy", "crum_image_load",
     "crum_restore_begin", "crum_restore_fetch", "crum_restore_end",
+    "crum_image_numa_node", "crum_device_numa_node",
 )
 
 
@@ -84,6 +85,8 @@ _sig = {
     "crum_image_import": (_i, [_vp, _vp, _u64, C.POINTER(_vp)]),
     "crum_image_data": (_i, [_vp, C.POINTER(_vp), C.POINTER(_u64), C.POINTER(_u64)]),
     "crum_image_destroy": (_i, [_vp]),
+    "crum_image_numa_node": (_i, [_vp, C.POINTER(_i)]),
+    "crum_device_numa_node": (_i, [_i, C.POINTER(_i)]),
     "crum_checkpoint_gather": (_i, [_vp, _vp, _vp, _u32, C.POINTER(Report)]),
     "crum_checkpoint_gather_device": (_i, [_vp, _vp, _u64, _vp, _u32, C.POINTER(Report)]),
     "crum_restore_scatter": (_i, [_vp, _vp, _vp, _u32, C.POINTER(Report)]),
@@ -184,6 +187,13 @@ class Image:
     @property
     def address(self) -> int:
         return self._info()[0]
+
+    @property
+    def numa_node(self) -> int:
+        """Host NUMA node the pinned pages are bound to (-1: default placement)."""
+        n = _i()
+        _check(_L.crum_image_numa_node(self._h, C.byref(n)), "crum_image_numa_node")
+        return n.value
 
     def view(self, full_capacity: bool = False) -> np.ndarray:
         """Zero-copy numpy view of the pinned buffer (valid until destroy)."""
@@ -412,6 +422,13 @@ class Context:
 
 
 # -- synthetic inputs (include/crum_synth.h) --------------------------------
+def device_numa_node(device: int) -> int:
+    """Host NUMA node of CUDA device `device` (-1: unknown or a single-node host)."""
+    n = _i()
+    _check(_L.crum_device_numa_node(device, C.byref(n)), "crum_device_numa_node")
+    return n.value
+
+
 def synth_fill(dev_ptr, nbytes: int, seed: int, region_index: int, word_offset: int = 0, stream=None):
     _check(_L.crum_synth_fill(_addr(dev_ptr), nbytes, seed, region_index, word_offset, _stream(stream)),
            "crum_synth_fill")

@@ -9,12 +9,16 @@
 #include <cuda_runtime.h>
 
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
+#include <cctype>
 #include <cerrno>
+#include <cstdlib>
 #include <cstdarg>
 #include <thread>
 #include <cstdio>
@@ -133,6 +137,8 @@ struct crum_image {
     uint64_t cap;
     uint64_t len;
     int device;
+    uint64_t map_bytes = 0;  // > 0: mmap'ed on the device's NUMA node + cudaHostRegister'ed
+    int numa_node = -1;      // node the pages were bound to (-1: cudaHostAlloc, default policy)
     // asynchronous persistence (writer thread)
     std::thread writer;
     std::atomic<int> busy{0};
@@ -143,6 +149,7 @@ struct crum_image {
 
 struct crum_ctx {
     int device = 0;
+    int numa_node = -1;  // images are bound to this host node (-1: default placement)
     crum_restore_session *session = nullptr;  // open lazy restore (blocks other state changes)
     uint32_t last_path = 0;                   // CRUM_PATH_* bits of the last gather
     // CUDA graph of the asynchronous device gather (one cached instance)
@@ -793,6 +800,63 @@ const char *crum_status_string(int s) {
 
 const char *crum_last_error_detail(void) { return g_detail.c_str(); }
 
+namespace {
+
+// NUMA node of a CUDA device's PCIe function (sysfs), or -1 when unknown or
+// when the host has a single node (then placement is moot).
+int device_numa_node(int device) {
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    for (char *q = bus; *q; ++q) *q = (char)tolower(*q);
+    char path[128];
+    int node = -1;
+    for (const char *fmt : {"/sys/bus/pci/devices/%s/numa_node", "/sys/bus/pci/devices/0000%s/numa_node"}) {
+        snprintf(path, sizeof path, fmt, bus + (strlen(bus) > 12 ? 4 : 0));
+        if (FILE *f = fopen(path, "r")) {
+            if (fscanf(f, "%d", &node) != 1) node = -1;
+            fclose(f);
+            break;
+        }
+    }
+    if (node < 0) return -1;
+    int nodes = 0;
+    for (int n = 0; n < 64; ++n) {
+        snprintf(path, sizeof path, "/sys/devices/system/node/node%d", n);
+        struct stat sb;
+        if (stat(path, &sb) == 0) ++nodes;
+    }
+    return nodes > 1 ? node : -1;
+}
+
+// Pinned, device-mapped host memory whose pages live on `node`: anonymous
+// mmap, mbind(MPOL_PREFERRED) before the first touch, then cudaHostRegister
+// (which faults the pages in under that policy and pins them).  *bound tells
+// whether mbind took effect (a sandbox without CAP_SYS_NICE may refuse it;
+// the memory is still pinned and mapped).  Returns nullptr if the mapping or
+// the registration fails (the caller falls back to cudaHostAlloc).
+uint8_t *numa_pinned_alloc(uint64_t bytes, int node, uint64_t *map_bytes, bool *bound) {
+    const uint64_t pg = (uint64_t)sysconf(_SC_PAGESIZE);
+    const uint64_t len = (bytes + pg - 1) / pg * pg;
+    void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return nullptr;
+    unsigned long mask[16] = {0};
+    mask[node / 64] = 1ul << (node % 64);
+    const long MPOL_PREFERRED_ = 1;
+    *bound = syscall(SYS_mbind, p, len, MPOL_PREFERRED_, mask, (unsigned long)(sizeof mask * 8), 0ul) == 0;
+    if (cudaHostRegister(p, len, cudaHostRegisterMapped | cudaHostRegisterPortable) != cudaSuccess) {
+        cudaGetLastError();
+        munmap(p, len);
+        return nullptr;
+    }
+    *map_bytes = len;
+    return static_cast<uint8_t *>(p);
+}
+
+}  // namespace
+
 uint64_t crum_launch_count(const crum_ctx *c) { return c ? c->launches : 0; }
 
 int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
@@ -819,6 +883,11 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     };
     if (cudaSetDevice(device) != cudaSuccess) return fail(CRUM_E_CUDA);
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    // pinned images go to the host node of the GPU's PCIe root (multi-socket
+    // boxes: the D2H/H2D traffic then never crosses the socket link);
+    // CRUM_NUMA=<node> overrides, CRUM_NUMA=-1 keeps the default placement
+    if (const char *e = getenv("CRUM_NUMA")) c->numa_node = atoi(e) < 0 ? -1 : atoi(e);
+    else c->numa_node = device_numa_node(device);
     if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess) return fail(CRUM_E_CUDA);
     {
         // gathers of the host path get the highest priority so their blocks are
@@ -1127,12 +1196,37 @@ int crum_image_required_bytes(crum_ctx *ctx, uint64_t max_dirty, uint64_t *out) 
     return CRUM_OK;
 }
 
+
+int crum_device_numa_node(int device, int *node_out) {
+    if (!node_out) return CRUM_E_INVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        set_detail("no CUDA device %d", device);
+        return CRUM_E_DEVICE;
+    }
+    *node_out = device_numa_node(device);
+    return CRUM_OK;
+}
+
+int crum_image_numa_node(const crum_image *img, int *node_out) {
+    if (!img || !node_out) return CRUM_E_INVAL;
+    *node_out = img->numa_node;
+    return CRUM_OK;
+}
+
 int crum_image_create(crum_ctx *ctx, uint64_t cap, crum_image **out) {
     ENTER(ctx);
     if (!out) return CRUM_E_INVAL;
     crum_image *im = new (std::nothrow) crum_image{nullptr, cap, 0, c->device};
     if (!im) return CRUM_E_NOMEM;
-    if (cudaHostAlloc(reinterpret_cast<void **>(&im->host), cap ? cap : 1, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    if (c->numa_node >= 0) {
+        bool bound = false;
+        im->host = numa_pinned_alloc(cap ? cap : 1, c->numa_node, &im->map_bytes, &bound);
+        if (im->host && bound) im->numa_node = c->numa_node;
+    }
+    if (!im->host &&
+        cudaHostAlloc(reinterpret_cast<void **>(&im->host), cap ? cap : 1, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
         cudaGetLastError();
         delete im;
         set_detail("cudaHostAlloc(%llu) failed", (unsigned long long)cap);
@@ -1167,7 +1261,12 @@ int crum_image_destroy(crum_image *img) {
     }
     if (img->writer.joinable()) img->writer.join();
     cudaSetDevice(img->device);
-    cudaFreeHost(img->host);
+    if (img->map_bytes) {
+        cudaHostUnregister(img->host);
+        munmap(img->host, img->map_bytes);
+    } else {
+        cudaFreeHost(img->host);
+    }
     delete img;
     return CRUM_OK;
 }

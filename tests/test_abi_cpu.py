@@ -75,6 +75,10 @@ def test_cpu_side_argument_checks(crum):
     assert L.crum_restore_end(None, None, None) == crum.E_INVAL
     assert L.crum_mark_dirty_pages(None, 1, None, 0, None) == crum.E_INVAL
     assert L.crum_status_string(crum.E_IO) == b"file I/O error"
+    node = C.c_int(7)
+    assert L.crum_image_numa_node(None, C.byref(node)) == crum.E_INVAL
+    assert L.crum_device_numa_node(0, None) == crum.E_INVAL
+    assert L.crum_device_numa_node(-1, C.byref(node)) == crum.E_DEVICE
     try:
         import torch
         has_gpu = torch.cuda.is_available()

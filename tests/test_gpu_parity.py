@@ -397,3 +397,31 @@ def test_async_device_gather_graph_replays(crum):
         p.g.checkpoint_gather_device(big, cap, report=False)
         torch.cuda.synchronize()
         assert big[:len(want)].cpu().numpy().tobytes() == want.tobytes(), epoch
+
+
+def test_numa_bound_image_bit_exact(crum, monkeypatch):
+    """A pinned image placed by mmap + mbind + cudaHostRegister (forced with
+    CRUM_NUMA=0, since a single-node box would otherwise take cudaHostAlloc)
+    holds the same bytes as the oracle's image and restores as one."""
+    monkeypatch.setenv("CRUM_NUMA", "0")
+    p = mkpair(MIXED[:4], 27)
+    img = p.g.new_image()
+    assert img.numa_node in (0, -1)          # -1: the sandbox refused mbind (memory still mmap'ed + registered)
+    assert crum.device_numa_node(0) >= -1
+    for epoch, d in ((0, 0), (1, 0.3)):
+        if epoch:
+            p.write(epoch, d)
+        st, want, _ = p.o.checkpoint_gather()
+        p.g.checkpoint_gather(img)
+        assert img.tobytes() == want.tobytes(), epoch
+    # restore the delta onto the previous state of a fresh pair
+    q = mkpair(MIXED[:4], 27)
+    q.g.sync_shadow()
+    q.o.sync_shadow()
+    q.g.restore_scatter(img)
+    torch.cuda.synchronize()
+    assert all(np.array_equal(d.cpu().numpy(), h) for d, h in zip(q.dev, p.host))
+    img.destroy()
+    monkeypatch.setenv("CRUM_NUMA", "-1")
+    ctx = crum.Context(0)
+    assert ctx.new_image(4096).numa_node == -1
