@@ -26,6 +26,7 @@ namespace crum {
 
 constexpr uint32_t kSegLog2 = 12;              // 4 KiB work segment (min page size)
 constexpr uint32_t kSegBytes = 1u << kSegLog2;
+constexpr uint32_t kU2sDirectLog2 = 4;         // compaction: pages of <= 16 units write their unit->slot entries inline
 constexpr uint32_t kPagesPerThread = 16;       // compaction: one uint4 of flags per thread
 constexpr uint32_t kCompactThreads = 256;
 constexpr uint32_t kPagesPerCompactBlock = kPagesPerThread * kCompactThreads;  // 4096

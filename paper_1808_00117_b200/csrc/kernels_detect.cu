@@ -14,6 +14,7 @@
 //    scramble chain across blocks runs on 4 lanes per page fed by 8 shuffles
 //    per 8 KiB.  XXH3 structure: xxhash 0.8 long-input loop (see
 //    DESIGN.md "XXH3 on the GPU"), written here independently of oracle/.
+#include <algorithm>
 #include <cstdlib>
 
 #include "crum_internal.cuh"
@@ -399,7 +400,10 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_detect_hash_big(
                     acc += S[buf][j][l];
                     if (b0 + j != bpp - 1) acc = scramble(acc, key);
                 }
-                bar_arrive(3 + buf, kBigThreads);
+                // arrive once the block sums have landed (acc depends on all of
+                // them; n_big >> 31 is a runtime zero), so the producers' next
+                // stores to S[buf] cannot overtake a read still in flight
+                bar_arrive(3 + buf + (uint32_t)(acc & (n_big >> 31)), kBigThreads);
             }
             // merge: r = P * PRIME64_1 + sum_i fold64((acc[2i]^m[2i]) * (acc[2i+1]^m[2i+1]))
             const uint64_t x = acc ^ smerge[l];
@@ -436,12 +440,12 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_detect_hash_big(
 // ---------------------------------------------------------------------------
 constexpr int kTmaCompute = 4;                                  // compute warps
 constexpr int kTmaRB = kTmaCompute * 8;                           // blocks per round
-constexpr int kTmaStages = 2;
+constexpr int kTmaStages = 2;                                    // default ring depth
+constexpr int kTmaMaxStages = 6;
 constexpr uint32_t kTmaRound = (uint32_t)kTmaRB * 1024u;         // 32 KiB
 constexpr int kTmaChainThreads = (kTmaCompute + 1) * 32;          // named-barrier participants
 constexpr int kTmaThreads = kTmaChainThreads + 32;                // + loader warp
 constexpr int kTmaCtasPerSm = 3;                                  // 3 scramble chains per SM
-constexpr size_t kTmaSmem = (size_t)kTmaStages * kTmaRound;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -478,10 +482,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
     const DevRegion *__restrict__ regs, const uint32_t *__restrict__ big_idx,
     const uint64_t *__restrict__ big_pg, uint32_t n_big, uint64_t w_lo, uint64_t w_hi,
-    uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash, uint8_t tag) {
-    extern __shared__ __align__(1024) uint8_t ring[];  // kTmaStages x kTmaRound
+    uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash, uint8_t tag, uint32_t nst) {
+    extern __shared__ __align__(1024) uint8_t ring[];  // nst x kTmaRound
     __shared__ uint64_t S[2][kTmaRB][8];
-    __shared__ __align__(8) uint64_t full_bar[kTmaStages], empty_bar[kTmaStages];
+    __shared__ __align__(8) uint64_t full_bar[kTmaMaxStages], empty_bar[kTmaMaxStages];
     __shared__ uint64_t sw[24], slast[8], smerge[8], sinit[8];
     if (threadIdx.x < 24) sw[threadIdx.x] = c_xxh.w[threadIdx.x];
     if (threadIdx.x < 8) {
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
         sinit[threadIdx.x] = c_xxh.init[threadIdx.x];
     }
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kTmaStages; ++i) {
+        for (uint32_t i = 0; i < nst; ++i) {
             mbar_init(&full_bar[i], 1);
             mbar_init(&empty_bar[i], kTmaCompute);
         }
@@ -498,7 +502,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
     }
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t q = 0;  // round counter across this CTA's pages (stage = q % 3, use = q / 3)
+    uint32_t q = 0;  // round counter across this CTA's pages (stage = q % nst, use = q / nst)
     uint64_t r_lo = 1, r_hi = 0;
     DevRegion R{};
     for (uint64_t w = w_lo + blockIdx.x; w < w_hi; w += gridDim.x) {
@@ -517,7 +521,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
         if (warp == kTmaCompute + 1) {
             // loader
             for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
-                const uint32_t st = q % kTmaStages, use = q / kTmaStages;
+                const uint32_t st = q % nst, use = q / nst;
                 if (use) mbar_wait(&empty_bar[st], (use - 1) & 1);
                 uint8_t *dst = ring + (size_t)st * kTmaRound;
                 const uint64_t off = (uint64_t)rr * kTmaRound;
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
         } else if (warp < kTmaCompute) {
             const uint32_t p = lane & 3, b = lane >> 2;
             for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
-                const uint32_t st = q % kTmaStages, use = q / kTmaStages;
+                const uint32_t st = q % nst, use = q / nst;
                 const uint32_t buf = q & 1;
                 const uint32_t bl = warp * 8 + b;  // block within the round
                 const uint32_t bi = rr * kTmaRB + bl;
@@ -546,8 +550,19 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
                 uint4 d[16];
 #pragma unroll
                 for (int s2 = 0; s2 < 16; ++s2) d[s2] = *reinterpret_cast<const uint4 *>(src + s2 * 64);
+                // Release the stage as soon as the loads have LANDED, not when
+                // they are issued: the arrive is made data-dependent on every
+                // loaded register (xor fold & a runtime zero the compiler cannot
+                // see through), so its address waits on the LDS scoreboard.
+                // An arrive right after the LDS issue let the next
+                // cp.async.bulk overwrite the stage while reads were still in
+                // flight (rare wrong hashes under load).
+                uint32_t fold = 0;
+#pragma unroll
+                for (int s2 = 0; s2 < 16; ++s2) fold ^= d[s2].x ^ d[s2].y ^ d[s2].z ^ d[s2].w;
+                const uint32_t dep = fold & (nst >> 16);  // nst <= kTmaMaxStages: always 0
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty_bar[st]);
+                if (lane == 0) mbar_arrive(&empty_bar[st] + dep);
                 uint64_t a0 = 0, a1 = 0;
 #pragma unroll
                 for (int s2 = 0; s2 < 15; ++s2) accum16(a0, a1, d[s2], sw[s2 + 2 * p], sw[s2 + 2 * p + 1]);
@@ -572,7 +587,10 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
                     acc += S[buf][j][l];
                     if (b0 + j != bpp - 1) acc = scramble(acc, key);
                 }
-                bar_arrive(3 + buf, kTmaChainThreads);
+                // arrive once the block sums have landed (acc depends on all of
+                // them; nst >> 16 is a runtime zero), so the compute warps'
+                // next stores to S[buf] cannot overtake a read still in flight
+                bar_arrive(3 + buf + (uint32_t)(acc & (nst >> 16)), kTmaChainThreads);
             }
             const uint64_t x = acc ^ smerge[l];
             const uint64_t y = __shfl_down_sync(0xffffffffu, x, 1);
@@ -665,14 +683,28 @@ void launch_detect_hash_big(const Launch &L, const DevRegion *regs, const uint32
     // TMA-fed kernel by default; CRUM_HASH_NO_TMA=1 selects the register-staged one
     static const bool no_tma = getenv("CRUM_HASH_NO_TMA") != nullptr;
     if (!no_tma) {
-        cudaFuncSetAttribute(k_detect_hash_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+        // ring depth and CTAs per SM (CRUM_TMA_STAGES / CRUM_TMA_CTAS override
+        // the defaults for tuning)
+        static const uint32_t nst = [] {
+            const char *e = getenv("CRUM_TMA_STAGES");
+            const int v = e ? atoi(e) : kTmaStages;
+            return (uint32_t)std::min(std::max(v, 2), kTmaMaxStages);
+        }();
+        static const int per_sm = [] {
+            const char *e = getenv("CRUM_TMA_CTAS");
+            return e ? std::min(std::max(atoi(e), 1), kTmaCtasPerSm) : kTmaCtasPerSm;
+        }();
+        const size_t smem = (size_t)nst * kTmaRound;
+        cudaFuncSetAttribute(k_detect_hash_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_detect_hash_tma, kTmaThreads, smem);
         // a page's scramble chain is serial: give every CTA the same number of
         // pages (e.g. 512 x 2 MiB pages -> 256 CTAs x 2, not 444 CTAs x 1-2)
-        const uint64_t cap = (uint64_t)L.sms * kTmaCtasPerSm;
+        const uint64_t cap = (uint64_t)L.sms * (uint64_t)std::max(1, std::min(occ, per_sm));
         const uint64_t per = (blocks + cap - 1) / cap;
         blocks = (blocks + per - 1) / per;
-        k_detect_hash_tma<<<(unsigned)blocks, kTmaThreads, kTmaSmem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo,
-                                                                                 w_hi, flags, newhash, tag);
+        k_detect_hash_tma<<<(unsigned)blocks, kTmaThreads, smem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo,
+                                                                             w_hi, flags, newhash, tag, nst);
         ++*L.counter;
         return;
     }
