@@ -55,7 +55,8 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--mode", default="compare", choices=["compare", "hash", "tracked"])
     ap.add_argument("--page", type=int, default=64 * KiB)
-    ap.add_argument("--dirty", type=float, default=0.10)
+    ap.add_argument("--dirty", type=float, default=None,
+                    help="fraction of pages rewritten per step (default: 1%% for C1, 10%% otherwise, as BASELINE.json)")
     ap.add_argument("--region-gib", type=float, default=1.0)
     ap.add_argument("--compress", action="store_true", help="CRUM_COMPRESS gathers (DESIGN.md Z1-Z2)")
     ap.add_argument("--content", default="random", choices=["random", "half"],
@@ -66,7 +67,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.dirty is None:
+        a.dirty = 0.01 if a.config == "c1" else 0.10
+    return a
 
 
 def workload(args, rank: int):
