@@ -534,6 +534,9 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
                     // partial round of a region's last page: zero-padded copy
                     for (uint32_t o = lane * 16; o < kTmaRound; o += 512)
                         *reinterpret_cast<uint4 *>(dst + o) = ld_slot16(pg, off + o, len);
+                    // order these generic-proxy stores before any later
+                    // cp.async.bulk (async proxy) into the same stage
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&full_bar[st]);
                 }
