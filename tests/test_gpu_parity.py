@@ -425,3 +425,26 @@ def test_numa_bound_image_bit_exact(crum, monkeypatch):
     monkeypatch.setenv("CRUM_NUMA", "-1")
     ctx = crum.Context(0)
     assert ctx.new_image(4096).numa_node == -1
+
+
+@pytest.mark.parametrize("P", [64 * KiB, 2 * MiB])
+def test_hash_detect_repeatable_under_load(crum, P):
+    """Stress of the TMA-fed hash kernel's shared-memory ring (DESIGN.md,
+    "TMA ring rule"): after a sync, every re-detect of an unchanged 1 GiB
+    region must flag nothing -- a stage overwritten while its reads were in
+    flight shows up as a spurious dirty page -- and the committed hashes must
+    equal the library's XXH3 on sampled pages."""
+    nb = GiB
+    d = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    crum.synth_fill(d, nb, synth.seed(31), 0)
+    ctx = crum.Context(0)
+    rid = ctx.register_region(d, nb, P, H)
+    n = nb // P
+    assert ctx.sync_shadow() == n
+    for _ in range(24):
+        assert int(ctx.debug_detect(n).sum()) == 0
+    table = ctx.debug_export(rid, crum.EXPORT_HASHES, n)
+    rng = np.random.default_rng(5)
+    for i in sorted(rng.choice(n, 8, replace=False)):
+        page = d[i * P:(i + 1) * P].cpu().numpy().tobytes()
+        assert int(table[i]) == xxhash.xxh3_64_intdigest(page), i
