@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
 }
 
 // ---------------------------------------------------------------------------
-// HASH detect for large pages, TMA-fed, PAIRED pages (default for P >= 64 KiB).
+// HASH detect for large pages, TMA-fed, PAGE GROUPS (default for P >= 64 KiB).
 // A page's scramble chain is serial (acc <- scramble(acc + S_b) per 1 KiB
 // block) and uses 8 lanes; a CTA that hashes one page at a time leaves 24
 // chain lanes idle and, measured, the chain warp competing for issue slots
@@ -629,8 +629,6 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
 // as in k_detect_hash_tma.
 // ---------------------------------------------------------------------------
 constexpr int kPairStages = 2;
-constexpr uint32_t kHalfBlocks = kTmaRB / 2;         // 16 blocks of each page per round
-constexpr uint32_t kHalfBytes = kHalfBlocks * 1024u;  // 16 KiB
 
 struct PairHalf {
     const uint8_t *pg;   // page base
@@ -639,14 +637,15 @@ struct PairHalf {
     uint64_t old;        // stored hash (table entry)
     uint64_t P;
     uint32_t bpp;        // 1 KiB blocks per page
-    uint32_t rounds;     // bpp / 16; 0 = no page in this half
+    uint32_t rounds;     // bpp / (32 / NP); 0 = no page in this slot
 };
 
 __device__ __forceinline__ void pair_half(const DevRegion *__restrict__ regs, const uint32_t *__restrict__ big_idx,
                                           const uint64_t *__restrict__ big_pg, uint32_t n_big, uint64_t w,
-                                          uint64_t w_hi, PairHalf &h) {
+                                          uint64_t w_hi, uint32_t seg_blocks, PairHalf &h) {
     if (w >= w_hi) {
         h.rounds = 0;
+        h.bpp = 0;
         return;
     }
     const uint32_t r = upper_region(big_pg, n_big, w);
@@ -654,19 +653,31 @@ __device__ __forceinline__ void pair_half(const DevRegion *__restrict__ regs, co
     const uint64_t page = w - __ldg(big_pg + r);
     h.P = 1ull << R.log2p;
     h.bpp = (uint32_t)(h.P >> 10);
-    h.rounds = h.bpp / kHalfBlocks;
+    h.rounds = h.bpp / seg_blocks;
     h.len = min(h.P, R.bytes - (page << R.log2p));
     h.pg = R.base + (page << R.log2p);
     h.g = R.page_base + page;
     h.old = R.table[page];
 }
 
+template <typename T>
+__device__ __forceinline__ T pick4(uint32_t h, T a, T b, T c, T d) {
+    return h == 0 ? a : h == 1 ? b : h == 2 ? c : d;
+}
+
+// NP = pages hashed together (2 or 4): a 32 KiB round carries 32/NP blocks of
+// each page; compute warp w serves page w / (4/NP); chain lanes 8h..8h+7 run
+// page h's chain.
+template <int NP>
 __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_pair(
     const DevRegion *__restrict__ regs, const uint32_t *__restrict__ big_idx,
     const uint64_t *__restrict__ big_pg, uint32_t n_big, uint64_t w_lo, uint64_t w_hi,
     uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash, uint8_t tag, uint32_t zero) {
-    extern __shared__ __align__(1024) uint8_t ring[];  // kPairStages x 32 KiB (half 0 | half 1)
-    __shared__ uint64_t S[2][kTmaRB][8];               // [buf][16 h + block][acc lane]
+    constexpr uint32_t kSegBlocks = kTmaRB / NP;        // blocks of each page per round
+    constexpr uint32_t kSegBytesNP = kSegBlocks * 1024u;
+    constexpr uint32_t kWarpsPerPage = kTmaCompute / NP;
+    extern __shared__ __align__(1024) uint8_t ring[];  // kPairStages x 32 KiB (NP segments)
+    __shared__ uint64_t S[2][kTmaRB][8];               // [buf][kSegBlocks * h + block][acc lane]
     __shared__ __align__(8) uint64_t full_bar[kPairStages], empty_bar[kPairStages];
     __shared__ uint64_t sw[24], slast[8], smerge[8], sinit[8];
     if (threadIdx.x < 24) sw[threadIdx.x] = c_xxh.w[threadIdx.x];
@@ -684,41 +695,50 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_pair
     }
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t q = 0;  // round counter across this CTA's pairs
-    const uint64_t npairs = (w_hi - w_lo + 1) / 2;
-    for (uint64_t t = blockIdx.x; t < npairs; t += gridDim.x) {
-        // every role looks its pages up itself (keeps only what it needs live)
-        PairHalf H0, H1;
-        pair_half(regs, big_idx, big_pg, n_big, w_lo + 2 * t, w_hi, H0);
-        pair_half(regs, big_idx, big_pg, n_big, w_lo + 2 * t + 1, w_hi, H1);
-        const uint32_t rounds = max(H0.rounds, H1.rounds);
+    uint32_t q = 0;  // round counter across this CTA's page groups
+    const uint64_t ngroups = (w_hi - w_lo + NP - 1) / NP;
+    for (uint64_t t = blockIdx.x; t < ngroups; t += gridDim.x) {
+        const uint64_t w0 = w_lo + NP * t;
+        PairHalf H[NP];
+#pragma unroll
+        for (int h = 0; h < NP; ++h) pair_half(regs, big_idx, big_pg, n_big, w0 + h, w_hi, kSegBlocks, H[h]);
+        uint32_t rounds = 0;
+#pragma unroll
+        for (int h = 0; h < NP; ++h) rounds = max(rounds, H[h].rounds);
         if (warp == kTmaCompute + 1) {
-            // loader: per round, each active half's 16 KiB (bulk copy, or a
+            // loader: per round, each active page's segment (bulk copy, or a
             // zero-filled copy by the lanes for a region's partial last page)
             for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
                 const uint32_t st = q % kPairStages, use = q / kPairStages;
                 if (use) mbar_wait(&empty_bar[st], (use - 1) & 1);
                 uint8_t *dst = ring + (size_t)st * kTmaRound;
-                const uint64_t off = (uint64_t)rr * kHalfBytes;
-                // per half: 0 idle, 1 bulk copy, 2 zero-filled copy
-                const int k0 = rr >= H0.rounds ? 0 : (off + kHalfBytes <= H0.len ? 1 : 2);
-                const int k1 = rr >= H1.rounds ? 0 : (off + kHalfBytes <= H1.len ? 1 : 2);
-                if (k0 == 2 || k1 == 2) {
-                    for (uint32_t o = lane * 16; o < kHalfBytes; o += 512) {
-                        if (k0 == 2) *reinterpret_cast<uint4 *>(dst + o) = ld_slot16(H0.pg, off + o, H0.len);
-                        if (k1 == 2)
-                            *reinterpret_cast<uint4 *>(dst + kHalfBytes + o) = ld_slot16(H1.pg, off + o, H1.len);
-                    }
+                const uint64_t off = (uint64_t)rr * kSegBytesNP;
+                int kind[NP];  // 0 idle, 1 bulk copy, 2 zero-filled copy
+                bool any_fill = false;
+                uint32_t tx = 0;
+#pragma unroll
+                for (int h = 0; h < NP; ++h) {
+                    kind[h] = rr >= H[h].rounds ? 0 : (off + kSegBytesNP <= H[h].len ? 1 : 2);
+                    any_fill |= kind[h] == 2;
+                    tx += kind[h] == 1 ? kSegBytesNP : 0u;
+                }
+                if (any_fill) {
+#pragma unroll
+                    for (int h = 0; h < NP; ++h)
+                        if (kind[h] == 2)
+                            for (uint32_t o = lane * 16; o < kSegBytesNP; o += 512)
+                                *reinterpret_cast<uint4 *>(dst + h * kSegBytesNP + o) =
+                                    ld_slot16(H[h].pg, off + o, H[h].len);
                     // order these generic stores before any later bulk copy into the stage
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    const uint32_t tx = (k0 == 1 ? kHalfBytes : 0u) + (k1 == 1 ? kHalfBytes : 0u);
                     if (tx) {
                         mbar_arrive_tx(&full_bar[st], tx);
-                        if (k0 == 1) bulk_g2s(dst, H0.pg + off, kHalfBytes, &full_bar[st]);
-                        if (k1 == 1) bulk_g2s(dst + kHalfBytes, H1.pg + off, kHalfBytes, &full_bar[st]);
+#pragma unroll
+                        for (int h = 0; h < NP; ++h)
+                            if (kind[h] == 1) bulk_g2s(dst + h * kSegBytesNP, H[h].pg + off, kSegBytesNP, &full_bar[st]);
                     } else {
                         mbar_arrive(&full_bar[st]);
                     }
@@ -726,17 +746,23 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_pair
             }
         } else if (warp < kTmaCompute) {
             const uint32_t p = lane & 3, b = lane >> 2;
-            const uint32_t h = warp >> 1;                  // which page of the pair
-            const uint32_t hb = (warp & 1) * 8 + b;         // block within the half-round
-            const uint32_t my_rounds = h ? H1.rounds : H0.rounds, my_bpp = h ? H1.bpp : H0.bpp;
+            const uint32_t h = warp / kWarpsPerPage;                 // page of the group
+            const uint32_t hb = (warp % kWarpsPerPage) * 8 + b;      // block within the page's segment
+            uint32_t my_rounds, my_bpp;
+            if (NP == 2) {
+                my_rounds = h ? H[1 % NP].rounds : H[0].rounds;
+                my_bpp = h ? H[1 % NP].bpp : H[0].bpp;
+            } else {
+                my_rounds = pick4(h, H[0].rounds, H[1 % NP].rounds, H[2 % NP].rounds, H[3 % NP].rounds);
+                my_bpp = pick4(h, H[0].bpp, H[1 % NP].bpp, H[2 % NP].bpp, H[3 % NP].bpp);
+            }
             for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
                 const uint32_t st = q % kPairStages, use = q / kPairStages;
                 const uint32_t buf = q & 1;
-                const bool active = rr < my_rounds;
                 mbar_wait(&full_bar[st], use & 1);
                 uint64_t a0 = 0, a1 = 0;
-                if (active) {
-                    const uint8_t *src = ring + (size_t)st * kTmaRound + h * kHalfBytes + hb * 1024 + p * 16;
+                if (rr < my_rounds) {
+                    const uint8_t *src = ring + (size_t)st * kTmaRound + h * kSegBytesNP + hb * 1024 + p * 16;
                     uint4 d[16];
 #pragma unroll
                     for (int s2 = 0; s2 < 16; ++s2) d[s2] = *reinterpret_cast<const uint4 *>(src + s2 * 64);
@@ -746,7 +772,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_pair
                     for (int s2 = 0; s2 < 16; ++s2) fold ^= d[s2].x ^ d[s2].y ^ d[s2].z ^ d[s2].w;
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty_bar[st] + (fold & zero));
-                    const uint32_t bi = rr * kHalfBlocks + hb;
+                    const uint32_t bi = rr * kSegBlocks + hb;
 #pragma unroll
                     for (int s2 = 0; s2 < 15; ++s2) accum16(a0, a1, d[s2], sw[s2 + 2 * p], sw[s2 + 2 * p + 1]);
                     const bool lastblk = (bi == my_bpp - 1);
@@ -757,24 +783,31 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_pair
                     if (lane == 0) mbar_arrive(&empty_bar[st]);
                 }
                 if (q >= 2) bar_sync(3 + buf, kTmaChainThreads);  // the chain has drained this buffer
-                S[buf][h * kHalfBlocks + hb][2 * p] = a0;
-                S[buf][h * kHalfBlocks + hb][2 * p + 1] = a1;
+                S[buf][h * kSegBlocks + hb][2 * p] = a0;
+                S[buf][h * kSegBlocks + hb][2 * p + 1] = a1;
                 bar_arrive(1 + buf, kTmaChainThreads);
             }
         } else {
             // chain warp: lanes 8h + l run page h's chain on accumulator lane l
-            const uint32_t l = lane & 7, h = (lane >> 3) & 1;
+            const uint32_t l = lane & 7, h = (lane >> 3) % NP;
             const uint64_t key = sw[16 + l];
             uint64_t acc = sinit[l];
-            const uint32_t hr = h ? H1.rounds : H0.rounds, hbpp = h ? H1.bpp : H0.bpp;
+            uint32_t hr, hbpp;
+            if (NP == 2) {
+                hr = h ? H[1 % NP].rounds : H[0].rounds;
+                hbpp = h ? H[1 % NP].bpp : H[0].bpp;
+            } else {
+                hr = pick4(h, H[0].rounds, H[1 % NP].rounds, H[2 % NP].rounds, H[3 % NP].rounds);
+                hbpp = pick4(h, H[0].bpp, H[1 % NP].bpp, H[2 % NP].bpp, H[3 % NP].bpp);
+            }
             for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
                 const uint32_t buf = q & 1;
                 bar_sync(1 + buf, kTmaChainThreads);
-                const uint32_t b0 = rr * kHalfBlocks;
+                const uint32_t b0 = rr * kSegBlocks;
                 if (rr < hr) {
 #pragma unroll 8
-                    for (uint32_t j = 0; j < kHalfBlocks; ++j) {
-                        acc += S[buf][h * kHalfBlocks + j][l];
+                    for (uint32_t j = 0; j < kSegBlocks; ++j) {
+                        acc += S[buf][h * kSegBlocks + j][l];
                         if (b0 + j != hbpp - 1) acc = scramble(acc, key);
                     }
                 }
@@ -787,16 +820,15 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_pair
             uint64_t m = ((l & 1) == 0) ? ((x * y) ^ __umul64hi(x, y)) : 0;
             m += __shfl_xor_sync(0xffffffffu, m, 2);
             m += __shfl_xor_sync(0xffffffffu, m, 4);
-            if ((lane & 7) == 0 && lane < 16 && hr) {
+            if ((lane & 7) == 0 && lane < 8 * NP && hr) {
                 PairHalf Hh;  // looked up again: keeps P / g / old out of the round loop's registers
-                pair_half(regs, big_idx, big_pg, n_big, w_lo + 2 * t + h, w_hi, Hh);
-                const uint64_t P = Hh.P, g = Hh.g, old = Hh.old;
-                uint64_t hv = P * kP64_1 + m;
+                pair_half(regs, big_idx, big_pg, n_big, w0 + h, w_hi, kSegBlocks, Hh);
+                uint64_t hv = Hh.P * kP64_1 + m;
                 hv ^= hv >> 37;
                 hv *= kMx1;
                 hv ^= hv >> 32;
-                newhash[g] = hv;
-                flags[g] = (hv != old) ? tag : 0;
+                newhash[Hh.g] = hv;
+                flags[Hh.g] = (hv != Hh.old) ? tag : 0;
             }
         }
     }
@@ -876,15 +908,24 @@ void launch_detect_hash_big(const Launch &L, const DevRegion *regs, const uint32
     static const bool no_tma = getenv("CRUM_HASH_NO_TMA") != nullptr;
     static const bool tma1 = getenv("CRUM_HASH_TMA1") != nullptr;
     if (!no_tma && !tma1) {
-        const size_t smem = (size_t)kPairStages * kTmaRound;
-        cudaFuncSetAttribute(k_detect_hash_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        // balanced grid over page pairs (every CTA gets the same number)
-        const uint64_t pairs = (blocks + 1) / 2;
+        // pages per CTA group: 2 (CRUM_HASH_NP=4: one page per compute warp,
+        // 8 chain steps per round -- measured slower: 0.865 vs 0.887 of peak on
+        // C2 64 KiB, 0.997 vs 1.021 on C4)
         const uint64_t cap = (uint64_t)L.sms * kTmaCtasPerSm;
-        const uint64_t per = (pairs + cap - 1) / cap;
-        const uint64_t grid = (pairs + per - 1) / per;
-        k_detect_hash_pair<<<(unsigned)grid, kTmaThreads, smem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo, w_hi,
-                                                                           flags, newhash, tag, 0u);
+        static const int np = getenv("CRUM_HASH_NP") && atoi(getenv("CRUM_HASH_NP")) == 4 ? 4 : 2;
+        const size_t smem = (size_t)kPairStages * kTmaRound;
+        const uint64_t groups = (blocks + np - 1) / np;
+        const uint64_t per = (groups + cap - 1) / cap;  // balanced: every CTA gets the same number
+        const uint64_t grid = (groups + per - 1) / per;
+        if (np == 4) {
+            cudaFuncSetAttribute(k_detect_hash_pair<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_detect_hash_pair<4><<<(unsigned)grid, kTmaThreads, smem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo,
+                                                                                  w_hi, flags, newhash, tag, 0u);
+        } else {
+            cudaFuncSetAttribute(k_detect_hash_pair<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_detect_hash_pair<2><<<(unsigned)grid, kTmaThreads, smem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo,
+                                                                                  w_hi, flags, newhash, tag, 0u);
+        }
         ++*L.counter;
         return;
     }
