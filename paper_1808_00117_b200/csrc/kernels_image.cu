@@ -231,22 +231,40 @@ __device__ void compact_finalize(const CompactArgs &a, uint64_t K, uint64_t U) {
 constexpr uint32_t kRegAgg = 64;  // per-block region counters kept in shared memory
 
 // Unit -> slot map entries of pages with more than 2^kU2sDirectLog2 units
-// (128 KiB and larger pages): a thread's dirty pages are walked again by its
-// whole warp in lock step (same region lookups, uniform control flow) and the
-// page's units are stored lane-strided (coalesced), instead of one thread
-// storing up to 512 entries per 2 MiB page serially (which made compaction of
-// 2 MiB pages 3x slower than of 64 KiB pages).  Smaller pages are written
-// inline by their thread.
+// (128 KiB and larger pages).  Smaller pages are written inline by their
+// thread.  The threads that own large dirty pages are listed in shared memory
+// and the block's warps take them in turn: a warp walks the owner's dirty
+// pages in lock step (same region lookups) and stores each large page's
+// entries lane-strided.  (One thread storing a 2 MiB page's 512 entries made
+// compaction of 2 MiB pages 52 us; one warp per owning thread still left
+// the 512-page C2 case -- all pages owned by warp 0 -- at 12 us of 22.)
+// Call with every thread of the block.
+struct U2sSmem {
+    uint32_t n;
+    uint16_t who[kCompactThreads];
+    uint32_t m[kCompactThreads];
+    uint64_t pos[kCompactThreads], upos[kCompactThreads];
+};
+
 __device__ __forceinline__ void u2s_fill_big(const CompactArgs &a, uint64_t base, uint32_t m0, uint64_t pos0,
-                                             uint64_t upos0) {
-    const uint32_t lane = threadIdx.x & 31;
-    uint32_t pend = __ballot_sync(0xffffffffu, m0 != 0);
-    while (pend) {
-        const int L = __ffs(pend) - 1;
-        pend &= pend - 1;
-        uint32_t mm = __shfl_sync(0xffffffffu, m0, L);
-        uint64_t pos = __shfl_sync(0xffffffffu, pos0, L), upos = __shfl_sync(0xffffffffu, upos0, L);
-        const uint64_t b0 = __shfl_sync(0xffffffffu, base, L);
+                                             uint64_t upos0, bool has_big, U2sSmem &sm) {
+    if (threadIdx.x == 0) sm.n = 0;
+    __syncthreads();
+    if (has_big) {
+        const uint32_t i = atomicAdd(&sm.n, 1u);
+        sm.who[i] = (uint16_t)threadIdx.x;
+        sm.m[threadIdx.x] = m0;
+        sm.pos[threadIdx.x] = pos0;
+        sm.upos[threadIdx.x] = upos0;
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const uint64_t blk_base = base - (uint64_t)threadIdx.x * kPagesPerThread;
+    for (uint32_t i = threadIdx.x >> 5; i < sm.n; i += nw) {
+        const uint32_t t = sm.who[i];
+        uint32_t mm = sm.m[t];
+        uint64_t pos = sm.pos[t], upos = sm.upos[t];
+        const uint64_t b0 = blk_base + (uint64_t)t * kPagesPerThread;
         uint32_t r = region_of_page(a.regs, a.R, b0 + (__ffs(mm) - 1));
         uint32_t l2 = a.regs[r].log2p;
         uint64_t next = (r + 1 < a.R) ? a.regs[r + 1].page_base : ~0ull;
@@ -268,6 +286,7 @@ __device__ __forceinline__ void u2s_fill_big(const CompactArgs &a, uint64_t base
 }
 
 __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a) {
+    __shared__ U2sSmem s_u2s;
     __shared__ uint64_t s_off[2];
     __shared__ bool s_last;
     // per-region dirty counts are aggregated in shared memory for the (usually
@@ -307,6 +326,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a
     const uint64_t eu = block_excl_scan(mask_units(a, base, m), &tu);  // syncs: s_off visible
     uint64_t pos = s_off[0] + ec, upos = s_off[1] + eu;
     const uint32_t m0 = m;
+    bool has_big = false;
     const uint64_t pos0 = pos, upos0 = upos;
     uint64_t dbytes = 0;
     if (m) {
@@ -330,7 +350,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a
             const uint64_t i = gid - g.page_base;
             a.gids[pos] = (uint32_t)gid;
             a.sunit[pos] = upos;
-            if (g.log2p - kSegLog2 <= kU2sDirectLog2)
+            if (g.log2p - kSegLog2 > kU2sDirectLog2) has_big = true;
+            else
                 for (uint32_t j = 0; j < (1u << (g.log2p - kSegLog2)); ++j) a.u2s[upos + j] = (uint32_t)pos;
             a.lids[pos] = (uint32_t)i;
             if (a.has_hashes) a.lhash[pos] = (g.mode == kModeHash) ? a.newhash[gid] : 0;
@@ -345,7 +366,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a
             else atomicAdd(a.reg_nd + r, cnt);
         }
     }
-    u2s_fill_big(a, base, m0, pos0, upos0);
+    u2s_fill_big(a, base, m0, pos0, upos0, has_big, s_u2s);
     __syncthreads();
     if (threadIdx.x < kRegAgg && s_rcnt[threadIdx.x] && s_r0 + threadIdx.x < a.R)
         atomicAdd(a.reg_nd + s_r0 + threadIdx.x, s_rcnt[threadIdx.x]);
@@ -404,6 +425,7 @@ __device__ __forceinline__ uint64_t ld_acq64(const uint64_t *p) {
 }
 
 __global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs a) {
+    __shared__ U2sSmem s_u2s;
     __shared__ uint64_t s_off[2];
     __shared__ uint32_t s_blk;
     __shared__ bool s_last;
@@ -411,7 +433,13 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs
     __shared__ uint32_t s_r0;
     uint64_t *status = a.blk_units;
     uint32_t *ticket = a.done + 2;
-    if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
+    // running totals of earlier ranges: loaded up front (thread 0 uses them
+    // after the look-back), so the load overlaps the ticket and the scans
+    RangeTotals rb0{};
+    if (threadIdx.x == 0) {
+        rb0 = a.rb[a.c];
+        s_blk = atomicAdd(ticket, 1u);
+    }
     if (threadIdx.x < kRegAgg) s_rcnt[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t blk = s_blk;
@@ -469,13 +497,14 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs
             if (lane == 0) st_rel64(status + blk, cpack(2, pc + tc, pu + tu));
         }
         if (lane == 0) {
-            s_off[0] = a.rb[a.c].k + pc;
-            s_off[1] = a.rb[a.c].units + pu;
+            s_off[0] = rb0.k + pc;
+            s_off[1] = rb0.units + pu;
         }
     }
     __syncthreads();
     uint64_t pos = s_off[0] + ec, upos = s_off[1] + eu;
     const uint32_t m0 = m;
+    bool has_big = false;
     const uint64_t pos0 = pos, upos0 = upos;
     uint64_t dbytes = 0;
     if (m) {
@@ -499,7 +528,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs
             const uint64_t i = gid - g.page_base;
             a.gids[pos] = (uint32_t)gid;
             a.sunit[pos] = upos;
-            if (g.log2p - kSegLog2 <= kU2sDirectLog2)
+            if (g.log2p - kSegLog2 > kU2sDirectLog2) has_big = true;
+            else
                 for (uint32_t j = 0; j < (1u << (g.log2p - kSegLog2)); ++j) a.u2s[upos + j] = (uint32_t)pos;
             a.lids[pos] = (uint32_t)i;
             if (a.has_hashes) a.lhash[pos] = (g.mode == kModeHash) ? a.newhash[gid] : 0;
@@ -514,7 +544,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs
             else atomicAdd(a.reg_nd + r, cnt);
         }
     }
-    u2s_fill_big(a, base, m0, pos0, upos0);
+    u2s_fill_big(a, base, m0, pos0, upos0, has_big, s_u2s);
     __syncthreads();
     if (threadIdx.x < kRegAgg && s_rcnt[threadIdx.x] && s_r0 + threadIdx.x < a.R)
         atomicAdd(a.reg_nd + s_r0 + threadIdx.x, s_rcnt[threadIdx.x]);
