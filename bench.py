@@ -289,6 +289,49 @@ def oracle_sample(specs, limit: int = 1 << 30):
     return out, f"a {len(out)}-region slice of the workload"
 
 
+def parity_check(args, ctx, crum, regions, specs, S, epoch, stream, dimg, cap, gflags, limit=4 << 30):
+    """Untimed, after the measurements: copy the run's regions to the host,
+    commit both sides (GPU sync_shadow; the oracle registers the copies and
+    syncs), apply one more application epoch to both, then compare the GPU's
+    device image with the oracle's image byte for byte -- the same launch
+    configuration, page sizes and flags the timed steps used."""
+    import torch
+    F = sum(nb for nb, _, _ in specs)
+    if F > limit:
+        return {"checked": False, "why": f"footprint {F / GiB:g} GiB > {limit / GiB:g} GiB host-copy bound; "
+                                         "tests/test_gpu_fullsize.py samples these sizes"}
+    from oracle import oracle
+    torch.cuda.synchronize()
+    ctx.sync_shadow(stream)
+    o = oracle.Oracle()
+    host = []
+    for r, (nb, P, mode) in enumerate(specs):
+        h = oracle.aligned_empty(nb)
+        h[:] = regions[r].cpu().numpy()
+        host.append(h)
+        o.register(h, P, mode)
+    o.sync_shadow()
+    half = args.content == "half"
+    for r, (nb, P, mode) in enumerate(specs):
+        pg = synth.choose_dirty(S, epoch, r, synth.n_pages(nb, P), args.dirty)
+        synth.apply_writer(host[r], P, pg, S, epoch, r, touch=half)
+        dp = torch.from_numpy(pg.astype(np.uint32)).to(regions[r].device)
+        if mode == 2:
+            o.mark_pages(r + 1, pg)
+            crum.synth_write_pages_tracked(regions[r], nb, P, dp, dp.numel(), S, epoch, r,
+                                           ctx.region_tracker(r + 1), stream=stream)
+        else:
+            crum.synth_write_pages(regions[r], nb, P, dp, dp.numel(), S, epoch, r, half, stream=stream)
+    st, want, _ = o.checkpoint_gather(flags=oracle.COMPRESS if gflags & crum.COMPRESS else 0)
+    rep = ctx.checkpoint_gather_device(dimg, cap, stream=stream, flags=gflags)
+    torch.cuda.synchronize()
+    got = dimg[:rep["image_bytes"]].cpu().numpy()
+    ok = st == 0 and got.nbytes == want.nbytes and bool(np.array_equal(got, want))
+    return {"checked": True, "ok": ok, "image_bytes": int(want.nbytes), "dirty_pages": int(rep["dirty_pages"]),
+            "what": "one more epoch after the timed steps: GPU device image vs the oracle's image, "
+                    "byte for byte (both sides committed to the run's state first)"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -645,6 +688,9 @@ def main():
                 "value": round(Ft / statistics.median(tt) / 1e9, 4), "unit": "GB/s", "cores": T,
                 "sample": f"{len(tt)} steps; the sample split into {T} page slices, one oracle per thread, "
                           f"writer untimed, step = slowest thread, median"}
+    # ---- parity of this run's GPU result with the oracle ----
+    if world == 1 and not host_resident(args):
+        line["parity"] = parity_check(args, ctx, crum, regions, specs, S, epoch + 1, stream, dimg, cap, gflags)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if distributed:
