@@ -27,6 +27,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/crum.h"
 #include "crum_internal.cuh"
 
@@ -35,6 +37,13 @@ using namespace crum;
 namespace {
 
 thread_local std::string g_detail;
+
+// NVTX range around an API call (header-only NVTX v3: free unless a tool such
+// as ncu --nvtx is attached); ncu can then select a call's kernels by range.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 void set_detail(const char *fmt, ...) {
     char buf[512];
@@ -1605,6 +1614,7 @@ int finish_gather_z(crum_ctx *c, cudaStream_t s, uint64_t capacity, crum_report 
 }  // namespace
 
 int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
+    NvtxRange nvtx_("crum_sync_shadow");
     ENTER(ctx);
     NOT_IN_SESSION(c);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1640,6 +1650,7 @@ int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
 // ---------------------------------------------------------------------------
 int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capacity, void *stream,
                                   uint32_t flags, crum_report *rep) {
+    NvtxRange nvtx_("crum_checkpoint_gather_device");
     ENTER(ctx);
     NOT_IN_SESSION(c);
     if (!dev_image || (flags & ~(CRUM_FULL | CRUM_COMPRESS)) || (reinterpret_cast<uintptr_t>(dev_image) & 255)) {
@@ -1754,6 +1765,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
 // ranges and checks capacity before committing anything.
 // ---------------------------------------------------------------------------
 int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_t flags, crum_report *rep) {
+    NvtxRange nvtx_("crum_checkpoint_gather");
     ENTER(ctx);
     NOT_IN_SESSION(c);
     if (!img || (flags & ~(CRUM_FULL | CRUM_COMPRESS))) {
@@ -2284,6 +2296,7 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
 }  // namespace
 
 int crum_restore_scatter(crum_ctx *ctx, const crum_image *img, void *stream, uint32_t flags, crum_report *rep) {
+    NvtxRange nvtx_("crum_restore_scatter");
     ENTER(ctx);
     NOT_IN_SESSION(c);
     if (!img || (flags & ~CRUM_VERIFY)) {
@@ -2296,6 +2309,7 @@ int crum_restore_scatter(crum_ctx *ctx, const crum_image *img, void *stream, uin
 
 int crum_restore_scatter_device(crum_ctx *ctx, const void *dev_image, uint64_t len, void *stream, uint32_t flags,
                                 crum_report *rep) {
+    NvtxRange nvtx_("crum_restore_scatter_device");
     ENTER(ctx);
     NOT_IN_SESSION(c);
     if (!dev_image || (flags & ~CRUM_VERIFY) || (reinterpret_cast<uintptr_t>(dev_image) & 255)) {
@@ -2395,6 +2409,7 @@ int session_scatter_slots(crum_restore_session *ss, uint32_t k, uint64_t klo, ui
 }  // namespace
 
 int crum_restore_begin(crum_ctx *ctx, crum_image *img, void *stream, uint32_t flags, crum_restore_session **out) {
+    NvtxRange nvtx_("crum_restore_begin");
     ENTER(ctx);
     NOT_IN_SESSION(c);
     if (!img || !out || (flags & ~CRUM_VERIFY)) {
@@ -2525,6 +2540,7 @@ int crum_restore_fetch(crum_restore_session *ss, uint32_t region_id, uint64_t pa
 }
 
 int crum_restore_end(crum_restore_session *ss, void *stream, crum_report *rep) {
+    NvtxRange nvtx_("crum_restore_end");
     if (!ss) {
         set_detail("null session");
         return CRUM_E_INVAL;
