@@ -530,6 +530,7 @@ def main():
     dev_alg = {"compare": 2 * F + 3 * payload, "hash": F + 16 * n_pages + 2 * payload,
                "tracked": n_pages + 2 * payload}[args.mode]
     traffic_key = f"{kname}:{args.config}:{specs[0][1]}:{args.dirty}"
+    in_bytes = {"compare": 2 * F, "hash": F + 8 * n_pages, "tracked": F}[args.mode]  # what one detect reads
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(T * 1e3 / args.steps, 4), "higher_is_better": True,
@@ -537,8 +538,8 @@ def main():
         "data": "synthetic (seeded splitmix64 words; seeded page choice per epoch)",
         "config": {"workload": desc, "footprint_bytes_per_gpu": F, "pages_per_gpu": n_pages,
                    "dirty_pages_per_step": K, "image_bytes_per_step": KP,
-                   "l2": ((f"inputs {2 * F / MiB:g} MiB (region + shadow) > 126 MB L2; " if 2 * F > 126e6 else
-                           f"inputs {2 * F / MiB:g} MiB (region + shadow) fit in L2, so ") +
+                   "l2": ((f"inputs {in_bytes / MiB:g} MiB (regions + shadow) > 126 MB L2; " if in_bytes > 126e6
+                           else f"inputs {in_bytes / MiB:g} MiB (regions + shadow) fit in L2, so ") +
                           "a 256 MiB streaming read before every step evicts L2 (the writer's dirty lines are "
                           "written back there, untimed) and leaves it clean: every step starts cold"),
                    "timing": "per-step CUDA events around crum_checkpoint_gather_device on its stream; "
