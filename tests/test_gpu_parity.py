@@ -448,3 +448,22 @@ def test_hash_detect_repeatable_under_load(crum, P):
     for i in sorted(rng.choice(n, 8, replace=False)):
         page = d[i * P:(i + 1) * P].cpu().numpy().tobytes()
         assert int(table[i]) == xxhash.xxh3_64_intdigest(page), i
+
+
+def test_hash_page_groups_straddle_regions(crum):
+    """The page-group hash kernel hashes big-page indices 2t, 2t+1 together:
+    with 5 pages of 64 KiB (ragged tail) before 2 pages of 2 MiB (ragged) and
+    3 pages of 64 KiB, the groups (4, 5) and (6, 7) pair pages of different
+    sizes from different regions.  Flags, hashes and images stay bit-exact."""
+    specs = [(4 * 64 * KiB + 100, 64 * KiB, H), (2 * MiB + 5000, 2 * MiB, H), (3 * 64 * KiB, 64 * KiB, H),
+             (7 * 4 * KiB + 9, 4 * KiB, H)]
+    p = mkpair(specs, 41)
+    img = p.g.new_image()
+    for epoch, d in ((0, 0), (1, 0.5), (2, 1.0), (3, 0.3)):
+        if epoch:
+            p.write(epoch, d)
+            assert np.array_equal(p.g.debug_detect(p.N), p.oracle_flags()), epoch
+        st, want, _ = p.o.checkpoint_gather()
+        p.g.checkpoint_gather(img)
+        assert img.tobytes() == want.tobytes(), epoch
+        assert p.shadows_equal()
