@@ -907,7 +907,10 @@ void launch_detect_hash_big(const Launch &L, const DevRegion *regs, const uint32
     // TMA-fed kernel by default; CRUM_HASH_NO_TMA=1 selects the register-staged one
     static const bool no_tma = getenv("CRUM_HASH_NO_TMA") != nullptr;
     static const bool tma1 = getenv("CRUM_HASH_TMA1") != nullptr;
-    if (!no_tma && !tma1) {
+    // Page groups only when there are enough pages to give every CTA slot a
+    // group: a short range (the host pipeline's first 16 MiB range holds only
+    // 8 pages of 2 MiB) finishes sooner with one page per CTA
+    if (!no_tma && !tma1 && blocks >= (uint64_t)L.sms * kTmaCtasPerSm) {
         // pages per CTA group: 2 (CRUM_HASH_NP=4: one page per compute warp,
         // 8 chain steps per round -- measured slower: 0.865 vs 0.887 of peak on
         // C2 64 KiB, 0.997 vs 1.021 on C4)
