@@ -749,17 +749,25 @@ __device__ __forceinline__ void put64(uint8_t *p, uint64_t v) {
 // ~0 initial register.
 constexpr uint32_t kCrcWords = 16;
 
+// Slicing-by-4 tables: T[k][n] = CRC register after byte n followed by k
+// zero bytes, so one 32-bit word costs 4 independent lookups instead of 4
+// dependent ones.
 struct CrcSmem {
-    uint32_t T[256];
+    uint32_t T[4][256];
     uint32_t x2n[32];
     uint32_t pw[32];
 };
 
+__device__ __forceinline__ uint32_t crc_word4(const CrcSmem &sm, uint32_t c) {
+    return sm.T[3][c & 0xffu] ^ sm.T[2][(c >> 8) & 0xffu] ^ sm.T[1][(c >> 16) & 0xffu] ^ sm.T[0][c >> 24];
+}
+
 __device__ __forceinline__ void crc_smem_init(CrcSmem &sm, const X2N &x) {
-    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
-        uint32_t c = i;
-        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
-        sm.T[i] = c;
+    for (uint32_t i = threadIdx.x; i < 1024; i += blockDim.x) {
+        const uint32_t k = i >> 8;
+        uint32_t c = i & 0xffu;
+        for (uint32_t b = 0; b < 8 * (k + 1); ++b) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+        sm.T[k][i & 0xffu] = c;
     }
     if (threadIdx.x < 32) {
         sm.x2n[threadIdx.x] = x.t[threadIdx.x];
@@ -790,13 +798,7 @@ __device__ __forceinline__ uint32_t crc_stream_terms(const WordFn &word, uint64_
             raw = (wbeg == 0) ? 0xffffffffu : 0u;
 #pragma unroll
             for (int j = 0; j < (int)kCrcWords; ++j) {
-                if ((uint32_t)j < n) {
-                    raw ^= v[j];
-                    raw = sm.T[raw & 0xffu] ^ (raw >> 8);
-                    raw = sm.T[raw & 0xffu] ^ (raw >> 8);
-                    raw = sm.T[raw & 0xffu] ^ (raw >> 8);
-                    raw = sm.T[raw & 0xffu] ^ (raw >> 8);
-                }
+                if ((uint32_t)j < n) raw = crc_word4(sm, raw ^ v[j]);
             }
         }
         uint32_t term = gf2_mulmod(sm.pw[lane], raw);  // first operand is never 0
@@ -881,7 +883,9 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
     put64(h + 48, st->image_bytes);
     put32(h + 56, meta_crc);
     uint32_t c = 0xffffffffu;
-    for (int i = 0; i < 60; ++i) c = sm.T[(c ^ h[i]) & 0xffu] ^ (c >> 8);
+    for (int i = 0; i < 60; i += 4)
+        c = crc_word4(sm, c ^ ((uint32_t)h[i] | (uint32_t)h[i + 1] << 8 | (uint32_t)h[i + 2] << 16 |
+                               (uint32_t)h[i + 3] << 24));
     put32(h + 60, c ^ 0xffffffffu);
     for (int i = 0; i < 64; ++i) a.head[i] = h[i];
     if (a.st_host) {
