@@ -435,10 +435,15 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs
     uint32_t *ticket = a.done + 2;
     // running totals of earlier ranges: loaded up front (thread 0 uses them
     // after the look-back), so the load overlaps the ticket and the scans
+    // (a single-block launch needs no ticket, fence or last-block election)
+    __shared__ uint64_t s_rb[2];
+    const bool single = gridDim.x == 1;
     RangeTotals rb0{};
     if (threadIdx.x == 0) {
         rb0 = a.rb[a.c];
-        s_blk = atomicAdd(ticket, 1u);
+        s_rb[0] = rb0.k;
+        s_rb[1] = rb0.units;
+        s_blk = single ? 0u : atomicAdd(ticket, 1u);
     }
     if (threadIdx.x < kRegAgg) s_rcnt[threadIdx.x] = 0;
     __syncthreads();
@@ -552,15 +557,20 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs
     if ((threadIdx.x & 31) == 0 && dbytes)
         atomicAdd(reinterpret_cast<unsigned long long *>(&a.st->dirty_bytes), (unsigned long long)dbytes);
     // ---- last block: totals, reset of the look-back state, finalise ----
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(a.done, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const uint64_t vlast = ld_acq64(status + gridDim.x - 1);  // inclusive prefix of the last block
-    const uint64_t K = a.rb[a.c].k + ((vlast >> 31) & 0x7fffffffull);
-    const uint64_t U = a.rb[a.c].units + (vlast & 0x7fffffffull);
+    if (!single) {
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = (atomicAdd(a.done, 1u) == gridDim.x - 1);
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+    } else {
+        __syncthreads();  // this block's region counts and bytes are in
+    }
+    // inclusive prefix of the last block
+    const uint64_t vlast = single ? cpack(2, tc, tu) : ld_acq64(status + gridDim.x - 1);
+    const uint64_t K = s_rb[0] + ((vlast >> 31) & 0x7fffffffull);
+    const uint64_t U = s_rb[1] + (vlast & 0x7fffffffull);
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) status[i] = 0;
     if (threadIdx.x == 0) {
@@ -860,16 +870,30 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
         return (q < U ? (uint32_t)zsz[q] : 0u) | ((q + 1 < U ? (uint32_t)zsz[q + 1] : 0u) << 16);
     };
     const uint32_t acc = crc_stream_terms(word, nwords, sm);
-    if ((threadIdx.x & 31) == 0 && acc) atomicXor(&st->crc_acc, acc);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(a.done, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
-    __threadfence();
-    *a.done = 0;
+    uint32_t total;
+    if (gridDim.x == 1) {
+        // one block: XOR the warps' terms in shared memory (no atomics, fence
+        // or last-block election)
+        __shared__ uint32_t s_acc[32];
+        if ((threadIdx.x & 31) == 0) s_acc[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x != 0) return;
+        total = st->crc_acc;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) total ^= s_acc[w];
+        st->crc_acc = total;
+    } else {
+        if ((threadIdx.x & 31) == 0 && acc) atomicXor(&st->crc_acc, acc);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = (atomicAdd(a.done, 1u) == gridDim.x - 1);
+        __syncthreads();
+        if (!s_last || threadIdx.x != 0) return;
+        __threadfence();
+        *a.done = 0;
+        total = *(volatile uint32_t *)&st->crc_acc;
+    }
     // empty stream: zlib crc32("") == 0
-    const uint32_t meta_crc = (nwords == 0) ? 0u : (*(volatile uint32_t *)&st->crc_acc ^ 0xffffffffu);
+    const uint32_t meta_crc = (nwords == 0) ? 0u : (total ^ 0xffffffffu);
     st->meta_crc = meta_crc;
     uint8_t h[64];
     h[0] = 'C'; h[1] = 'R'; h[2] = 'U'; h[3] = 'M';
