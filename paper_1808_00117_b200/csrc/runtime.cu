@@ -536,22 +536,31 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
     // they double up to ~F/8 (>= 128 MiB) each
     c->all = make_range(c, 0, N);
     c->ranges.clear();
+    // A range holding large-page hash pages keeps at least one such page per
+    // SM: their per-page scramble chain is serial, so a 16 MiB range of 2 MiB
+    // pages (8 pages) would run on 8 CTAs.  (One page per CTA slot, 3 per SM,
+    // delayed the first copy more than it saved: C2 hash 2 MiB e2e 482 vs 502.)
+    const uint64_t min_big = (uint64_t)std::max(c->sms, 1);
     const uint64_t target_max = std::max(kMinRangeBytes, F / 8);
     uint64_t target = std::max<uint64_t>(16ull << 20, F / 128);
-    uint64_t lo = 0, acc = 0;
+    uint64_t lo = 0, acc = 0, nbig = 0;
     for (uint32_t r = 0; r < R; ++r) {
         const HostRegion &h = c->regs[r];
+        const bool big_hash = h.mode == kModeHash && h.log2p >= 16;
         for (uint64_t i = 0; i < h.n_pages; ++i) {
             const uint64_t g = h.page_base + i;
-            if (acc >= target && g % 16 == 0 && (int)c->ranges.size() < kMaxRanges - 1) {
+            if (acc >= target && (nbig == 0 || nbig >= min_big) && g % 16 == 0 &&
+                (int)c->ranges.size() < kMaxRanges - 1) {
                 c->ranges.push_back(make_range(c, lo, g));
                 lo = g;
                 acc = 0;
+                nbig = 0;
                 target = std::min(target_max, 2 * target);
             }
             // whole pages at a time is fine for large regions; skip ahead in big steps
             const uint64_t step = std::min<uint64_t>(h.n_pages - i, 16 - (g % 16));
             acc += step * h.page_size;
+            if (big_hash) nbig += step;
             i += step - 1;
         }
     }
