@@ -83,7 +83,18 @@ class Live:
                 assert np.array_equal(self.o.mirror(r), self.g.debug_export(r, self.crum.EXPORT_MIRROR, h.nbytes))
 
 
-@pytest.mark.parametrize("seed,chunk", [(1, 0), (2, 64 * KiB)])
+def _soak_cases():
+    """Default: two seeds.  CRUM_SOAK_SEEDS=3-12 (a range) runs an extended
+    soak, alternating the default chunk and 64 KiB chunks."""
+    import os
+    spec = os.environ.get("CRUM_SOAK_SEEDS")
+    if not spec:
+        return [(1, 0), (2, 64 * KiB)]
+    lo, _, hi = spec.partition("-")
+    return [(s, 0 if s % 2 else 64 * KiB) for s in range(int(lo), int(hi or lo) + 1)]
+
+
+@pytest.mark.parametrize("seed,chunk", _soak_cases())
 def test_random_operation_sequence(crum, seed, chunk):
     rng = np.random.default_rng(seed)
     S = synth.seed(200 + seed)
