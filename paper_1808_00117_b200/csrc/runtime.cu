@@ -860,7 +860,11 @@ uint8_t *numa_pinned_alloc(uint64_t bytes, int node, uint64_t *map_bytes, bool *
     const uint64_t len = (bytes + pg - 1) / pg * pg;
     void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
     if (p == MAP_FAILED) return nullptr;
-    unsigned long mask[16] = {0};
+    unsigned long mask[16] = {0};  // nodes 0..1023
+    if (node < 0 || node >= 1024) {
+        munmap(p, len);
+        return nullptr;
+    }
     mask[node / 64] = 1ul << (node % 64);
     const long MPOL_PREFERRED_ = 1;
     *bound = syscall(SYS_mbind, p, len, MPOL_PREFERRED_, mask, (unsigned long)(sizeof mask * 8), 0ul) == 0;
