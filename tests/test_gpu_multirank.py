@@ -19,7 +19,7 @@ def test_two_ranks_share_one_gpu():
     assert torch.cuda.is_available()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29571", "bench.py", "--gpus", "2",
-           "--dist-backend", "gloo", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
+           "--dist-backend", "gloo", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
            "--region-gib", "0.25"]
     out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -29,3 +29,6 @@ def test_two_ranks_share_one_gpu():
     assert d["n_gpus"] == 2 and d["scaling"] == "weak"
     assert d["config"]["footprint_bytes_per_gpu"] == 1 << 28
     assert d["value"] > 0 and d["gpu_launches"] > 0
+    # e2e across ranks: max-over-ranks time, link probe taken by both ranks at once
+    lr = d["e2e"]["link_roofline"]
+    assert d["e2e"]["value"] > 0 and lr["box_peak_GBs"] == pytest.approx(2 * lr["peak_GBs"], rel=1e-3)
