@@ -99,16 +99,50 @@ enum {
 typedef struct crum_ctx crum_ctx;     /* one per (process, CUDA device) */
 typedef struct crum_image crum_image; /* library-owned pinned host buffer holding one image */
 
+/* Per-context configuration (SURVEY.md sec. 8(b)/sec. 5: chunk bytes, pinned
+ * pool bytes, NUMA node, flags).  Every tuning choice of the library lives
+ * here, per context -- the library reads no environment variables. */
 typedef struct {
-    uint64_t chunk_bytes; /* host-link pipeline chunk (0 = 64 MiB); multiple of 4096 */
-    uint32_t flags;       /* 0 or CRUM_CFG_TIMING */
-    uint32_t reserved;    /* must be 0 */
+    uint64_t chunk_bytes;       /* host-link pipeline chunk (0 = 64 MiB); multiple of 4096 */
+    uint64_t pinned_pool_bytes; /* 0: every crum_image is its own pinned allocation.  > 0: one
+                                   pinned, device-mapped pool of this many bytes (multiple of
+                                   4096) is reserved at crum_create on the images' NUMA node and
+                                   images are carved from it (first fit, 4 KiB granules, freed
+                                   ranges coalesce); an image that does not fit gets its own
+                                   allocation.  Pinning is slow (seconds per 8 GiB), the pool
+                                   pays it once. */
+    int32_t numa_node;          /* host node of pinned images and the pool:
+                                   CRUM_NUMA_AUTO (-1): the node of the GPU's PCIe root on a
+                                     multi-node host, default placement otherwise;
+                                   CRUM_NUMA_DEFAULT (-2): default placement (cudaHostAlloc);
+                                   >= 0: that node (anonymous mmap + mbind + cudaHostRegister). */
+    uint32_t flags;             /* CRUM_CFG_* below */
 } crum_config;
 
-/* crum_config.flags: record CUDA events around the phases of EVERY call (also
- * asynchronous ones), so crum_last_report can return phase times without the
- * call itself waiting. */
-enum { CRUM_CFG_TIMING = 1u << 0 };
+enum { CRUM_NUMA_AUTO = -1, CRUM_NUMA_DEFAULT = -2 };
+
+/* Fill *cfg with the defaults (chunk 64 MiB, no pool, CRUM_NUMA_AUTO, no
+ * flags) -- note that a zero-filled struct means NUMA node 0.  Passing
+ * cfg = NULL to crum_create is the same as these defaults.
+ * Errors: INVAL (null cfg). */
+CRUM_API int crum_config_init(crum_config *cfg);
+
+/* crum_config.flags.
+ *   CRUM_CFG_TIMING   record CUDA events around the phases of EVERY call (also
+ *                     asynchronous ones), so crum_last_report can return phase
+ *                     times without the call itself waiting.
+ *   CRUM_CFG_NO_GRAPH never replay a captured CUDA graph for asynchronous device
+ *                     gathers (every launch is enqueued directly).
+ *   CRUM_CFG_FUSED    device-image gathers of a context whose regions are all
+ *                     COMPARE with pages <= 64 KiB run the single-pass kernel
+ *                     (detect + compaction + gather + commit in one launch).
+ *   CRUM_CFG_TRACE    print the host pipeline's per-range times to stderr. */
+enum {
+    CRUM_CFG_TIMING = 1u << 0,
+    CRUM_CFG_NO_GRAPH = 1u << 1,
+    CRUM_CFG_FUSED = 1u << 2,
+    CRUM_CFG_TRACE = 1u << 3
+};
 
 /* Outcome of a sync / gather / restore.  Times are CUDA-event milliseconds
  * on the call's stream (0 when not measured). */
@@ -211,9 +245,10 @@ CRUM_API int crum_image_required_bytes(crum_ctx *ctx, uint64_t max_dirty_pages, 
  * GPU's PCIe root (sysfs numa_node; anonymous mmap + mbind(MPOL_PREFERRED)
  * + cudaHostRegister), so the copy-out of SURVEY.md sec. 8(e) ("pinned
  * images must be NUMA-local to each GPU") never crosses the socket link;
- * otherwise, or if that fails, cudaHostAlloc.  The environment variable
- * CRUM_NUMA=<node> (read at crum_create) overrides the node, CRUM_NUMA=-1
- * keeps the default placement.  crum_image_import copies `len` bytes into a
+ * otherwise, or if that fails, cudaHostAlloc.  crum_config.numa_node
+ * overrides the node.  With crum_config.pinned_pool_bytes > 0 images are
+ * carved from the context's pinned pool when they fit (the context must then
+ * outlive its images).  crum_image_import copies `len` bytes into a
  * new image (for restart from a file).  crum_image_data exposes the buffer:
  * *data_out (host pointer, owned by the image), *len_out (valid image
  * length; 0 before the first gather), *capacity_out (may be NULL). */
@@ -222,9 +257,15 @@ CRUM_API int crum_image_import(crum_ctx *ctx, const void *bytes, uint64_t len, c
 CRUM_API int crum_image_data(const crum_image *img, void **data_out, uint64_t *len_out, uint64_t *capacity_out);
 CRUM_API int crum_image_destroy(crum_image *img);
 /* *node_out = the NUMA node the image's pages were bound to, -1 for default
- * placement (single-node host, CRUM_NUMA=-1, or mbind refused by the
+ * placement (single-node host, CRUM_NUMA_DEFAULT, or mbind refused by the
  * sandbox).  Errors: INVAL (null argument). */
 CRUM_API int crum_image_numa_node(const crum_image *img, int *node_out);
+/* The context's pinned pool (crum_config.pinned_pool_bytes): *bytes_out its
+ * size (0: no pool), *in_use_out bytes currently carved out (4 KiB granules),
+ * *largest_free_out the largest free extent, *images_out images living in it.
+ * Any out pointer may be NULL.  Errors: INVAL (null ctx). */
+CRUM_API int crum_pinned_pool_info(crum_ctx *ctx, uint64_t *bytes_out, uint64_t *in_use_out,
+                                   uint64_t *largest_free_out, uint32_t *images_out);
 /* *node_out = the host NUMA node of CUDA device `device`'s PCIe function, or
  * -1 when unknown or when the host has one node (callers use it to pin the
  * rank's host threads next to its GPU).  Errors: INVAL (null node_out),

@@ -6,8 +6,11 @@ Here each rank owns one GPU and one crum_ctx; page bytes never cross GPUs, so
 the only collectives are:
 
   1. barrier() before A1 (every rank's application epoch has finished),
-  2. all_reduce(SUM) of int64 {dirty bytes, image bytes, dirty pages},
-  3. all_reduce(MAX) of the per-rank checkpoint time (device events).
+  2. all_reduce(MAX) of a failure flag: a rank whose checkpoint raised (e.g.
+     CAPACITY, BUSY) makes EVERY rank raise CoordinatedFailure instead of
+     leaving the others blocked in the next collective,
+  3. all_reduce(SUM) of int64 {dirty bytes, image bytes, dirty pages},
+  4. all_reduce(MAX) of the per-rank checkpoint time (device events).
 
 `local_step` is the per-rank checkpoint (e.g. a bound
 Context.checkpoint_gather call) returning a crum report dict; keeping it a
@@ -19,6 +22,14 @@ from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
+
+
+class CoordinatedFailure(RuntimeError):
+    """The coordinated checkpoint failed on at least one rank (raised on all)."""
+
+    def __init__(self, msg: str, local_error: BaseException | None = None):
+        super().__init__(msg)
+        self.local_error = local_error
 
 
 @dataclass
@@ -46,7 +57,17 @@ def coordinated(local_step, group=None, time_key: str = "t_total_ms") -> GlobalR
                             float(rep.get(time_key, 0.0)), 1)
     dev = _device_for(group)
     dist.barrier(group)
-    rep = local_step()
+    err = None
+    try:
+        rep = local_step()
+    except Exception as e:  # surfaced on every rank below
+        err, rep = e, None
+    failed = torch.tensor([1 if err is not None else 0], dtype=torch.int64, device=dev)
+    dist.all_reduce(failed, op=dist.ReduceOp.MAX, group=group)
+    if int(failed.item()):
+        if err is not None:
+            raise CoordinatedFailure(f"rank {dist.get_rank(group)}: {err}", err) from err
+        raise CoordinatedFailure("coordinated checkpoint failed on another rank")
     sums = torch.tensor([rep["dirty_bytes"], rep["image_bytes"], rep["dirty_pages"]], dtype=torch.int64, device=dev)
     dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
     t = torch.tensor([float(rep.get(time_key, 0.0))], dtype=torch.float64, device=dev)

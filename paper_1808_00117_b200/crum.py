@@ -30,7 +30,8 @@ E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY, E_DEVICE, E_CUDA, E_IO = -6, -7, -8, 
 MODE_COMPARE, MODE_HASH = 0, 1
 FULL, VERIFY, COMPRESS = 1, 2, 4
 MODE_TRACKED = 2
-CFG_TIMING = 1
+CFG_TIMING, CFG_NO_GRAPH, CFG_FUSED, CFG_TRACE = 1, 2, 4, 8
+NUMA_AUTO, NUMA_DEFAULT = -1, -2
 PATH_FUSED, PATH_COMPRESSED = 1, 2
 PERSIST_FSYNC = 1
 EXPORT_FORCE, EXPORT_HASHES, EXPORT_MIRROR = 0, 1, 2
@@ -48,7 +49,7 @@ EXPORTED = (
     "crum_mark_dirty_pages", "crum_region_tracker",
     "crum_image_persist", "crum_image_persist_wait", "crum_image_persist_busy", "crum_image_load",
     "crum_restore_begin", "crum_restore_fetch", "crum_restore_end",
-    "crum_image_numa_node", "crum_device_numa_node",
+    "crum_image_numa_node", "crum_device_numa_node", "crum_config_init", "crum_pinned_pool_info",
 )
 
 
@@ -58,7 +59,9 @@ class Tracker(C.Structure):
 
 
 class Config(C.Structure):
-    _fields_ = [("chunk_bytes", C.c_uint64), ("flags", C.c_uint32), ("reserved", C.c_uint32)]
+    """crum_config (include/crum.h): every tuning choice of the library, per context."""
+    _fields_ = [("chunk_bytes", C.c_uint64), ("pinned_pool_bytes", C.c_uint64), ("numa_node", C.c_int32),
+                ("flags", C.c_uint32)]
 
 
 class Report(C.Structure):
@@ -75,6 +78,8 @@ class Report(C.Structure):
 _vp, _u64, _u32, _i = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int
 _sig = {
     "crum_create": (_i, [_i, C.POINTER(Config), C.POINTER(_vp)]),
+    "crum_config_init": (_i, [C.POINTER(Config)]),
+    "crum_pinned_pool_info": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u32)]),
     "crum_destroy": (_i, [_vp]),
     "crum_register_region": (_i, [_vp, _vp, _u64, _u64, _u32, C.POINTER(_u32)]),
     "crum_unregister_region": (_i, [_vp, _u32]),
@@ -277,9 +282,15 @@ class RestoreSession:
 class Context:
     """crum_ctx: one per (process, CUDA device)."""
 
-    def __init__(self, device: int = 0, chunk_bytes: int = 0, timing: bool = False):
+    def __init__(self, device: int = 0, chunk_bytes: int = 0, timing: bool = False, flags: int = 0,
+                 numa_node: int = NUMA_AUTO, pinned_pool_bytes: int = 0):
         self._h = _vp()
-        cfg = Config(chunk_bytes, CFG_TIMING if timing else 0, 0)
+        cfg = Config()
+        _check(_L.crum_config_init(C.byref(cfg)), "crum_config_init")
+        cfg.chunk_bytes = chunk_bytes
+        cfg.pinned_pool_bytes = pinned_pool_bytes
+        cfg.numa_node = numa_node
+        cfg.flags = flags | (CFG_TIMING if timing else 0)
         _check(_L.crum_create(device, C.byref(cfg), C.byref(self._h)), "crum_create")
         self.device = device
         self._keep = {}
@@ -419,6 +430,13 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(_L.crum_launch_count(self._h))
+
+    def pool_info(self) -> dict:
+        """The context's pinned pool: bytes, in_use, largest_free, images."""
+        b, u, l, n = _u64(), _u64(), _u64(), _u32()
+        _check(_L.crum_pinned_pool_info(self._h, C.byref(b), C.byref(u), C.byref(l), C.byref(n)),
+               "crum_pinned_pool_info")
+        return {"bytes": b.value, "in_use": u.value, "largest_free": l.value, "images": n.value}
 
 
 # -- synthetic inputs (include/crum_synth.h) --------------------------------

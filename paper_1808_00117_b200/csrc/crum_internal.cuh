@@ -105,7 +105,6 @@ struct CompactArgs {
     int first_range;       // reset per-checkpoint accumulators
     int final_range;       // finalise: region prefix sums, header fields, table
     uint32_t c;
-    uint32_t *blk_count;   // per-block dirty pages
     uint64_t *blk_units;   // per-block 4 KiB units
     uint32_t *gids;        // slot -> global page id
     uint64_t *sunit;       // slot -> payload unit offset

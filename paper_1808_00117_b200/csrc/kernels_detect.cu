@@ -15,7 +15,6 @@
 //    per 8 KiB.  XXH3 structure: xxhash 0.8 long-input loop (see
 //    DESIGN.md "XXH3 on the GPU"), written here independently of oracle/.
 #include <algorithm>
-#include <cstdlib>
 
 #include "crum_internal.cuh"
 
@@ -310,118 +309,13 @@ __global__ void __launch_bounds__(256, 2) k_detect_hash(
     }
 }
 
-// ---------------------------------------------------------------------------
-// HASH detect for large pages (P >= 64 KiB): one CTA per page, warp
-// specialised.  Warps 0..7 ("producers") compute the accumulate sums of 64
-// consecutive 1 KiB blocks per round (8 blocks each, the lane layout of
-// xxh3_slot) into a double-buffered shared-memory ring; warp 8 ("chain") runs
-// the serial scramble chain over them, one lane per accumulator lane, while
-// the producers stream the next round.  Hand-off uses named barriers:
-// FULL[b] (ids 1, 2: producers arrive, chain syncs) and EMPTY[b] (ids 3, 4:
-// chain arrives, producers sync).  The round counter q runs across the
-// CTA's pages so barrier generations stay paired.
-// ---------------------------------------------------------------------------
-constexpr int kBigProducers = 8;
-constexpr int kBigThreads = (kBigProducers + 1) * 32;
-constexpr int kRoundBlocks = kBigProducers * 8;  // 64 KiB of page per round
-
+// Named barriers (bar.sync / bar.arrive) pair the compute and chain warps of
+// the TMA-fed hash kernels below.
 __device__ __forceinline__ void bar_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-__global__ void __launch_bounds__(kBigThreads, 2) k_detect_hash_big(
-    const DevRegion *__restrict__ regs, const uint32_t *__restrict__ big_idx,
-    const uint64_t *__restrict__ big_pg, uint32_t n_big, uint64_t w_lo, uint64_t w_hi,
-    uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash, uint8_t tag) {
-    __shared__ uint64_t S[2][kRoundBlocks][8];
-    __shared__ uint64_t sw[24], slast[8], smerge[8], sinit[8];
-    if (threadIdx.x < 24) sw[threadIdx.x] = c_xxh.w[threadIdx.x];
-    if (threadIdx.x < 8) {
-        slast[threadIdx.x] = c_xxh.last[threadIdx.x];
-        smerge[threadIdx.x] = c_xxh.merge[threadIdx.x];
-        sinit[threadIdx.x] = c_xxh.init[threadIdx.x];
-    }
-    __syncthreads();
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t q = 0;
-    uint64_t r_lo = 1, r_hi = 0;
-    DevRegion R{};
-    for (uint64_t w = w_lo + blockIdx.x; w < w_hi; w += gridDim.x) {
-        if (w < r_lo || w >= r_hi) {
-            const uint32_t r = upper_region(big_pg, n_big, w);
-            R = regs[__ldg(big_idx + r)];
-            r_lo = __ldg(big_pg + r);
-            r_hi = __ldg(big_pg + r + 1);
-        }
-        const uint64_t page = w - r_lo;
-        const uint64_t P = 1ull << R.log2p;
-        const uint32_t bpp = (uint32_t)(P >> 10);
-        const uint32_t rounds = bpp / kRoundBlocks;
-        const uint64_t len = min(P, R.bytes - (page << R.log2p));
-        const uint8_t *pg = R.base + (page << R.log2p);
-        if (warp < kBigProducers) {
-            const uint32_t p = lane & 3, b = lane >> 2;
-            for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
-                const uint32_t buf = q & 1;
-                const uint32_t bi = rr * kRoundBlocks + warp * 8 + b;
-                const uint64_t boff = (uint64_t)bi * 1024 + p * 16;
-                uint4 d[16];
-                if (len == P) {
-#pragma unroll
-                    for (int s = 0; s < 16; ++s) d[s] = ld128(pg + boff + s * 64);
-                } else {
-#pragma unroll
-                    for (int s = 0; s < 16; ++s) d[s] = ld_slot16(pg, boff + s * 64, len);
-                }
-                uint64_t a0 = 0, a1 = 0;
-#pragma unroll
-                for (int s = 0; s < 15; ++s) accum16(a0, a1, d[s], sw[s + 2 * p], sw[s + 2 * p + 1]);
-                const bool lastblk = (bi == bpp - 1);
-                accum16(a0, a1, d[15], lastblk ? slast[2 * p] : sw[15 + 2 * p],
-                        lastblk ? slast[2 * p + 1] : sw[16 + 2 * p]);
-                if (q >= 2) bar_sync(3 + buf, kBigThreads);  // the chain has drained this buffer
-                S[buf][warp * 8 + b][2 * p] = a0;
-                S[buf][warp * 8 + b][2 * p + 1] = a1;
-                bar_arrive(1 + buf, kBigThreads);
-            }
-        } else {
-            const uint32_t l = lane & 7;
-            const uint64_t key = sw[16 + l];
-            uint64_t acc = sinit[l];
-            for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
-                const uint32_t buf = q & 1;
-                bar_sync(1 + buf, kBigThreads);
-                const uint32_t b0 = rr * kRoundBlocks;
-#pragma unroll 8
-                for (int j = 0; j < kRoundBlocks; ++j) {
-                    acc += S[buf][j][l];
-                    if (b0 + j != bpp - 1) acc = scramble(acc, key);
-                }
-                // arrive once the block sums have landed (acc depends on all of
-                // them; n_big >> 31 is a runtime zero), so the producers' next
-                // stores to S[buf] cannot overtake a read still in flight
-                bar_arrive(3 + buf + (uint32_t)(acc & (n_big >> 31)), kBigThreads);
-            }
-            // merge: r = P * PRIME64_1 + sum_i fold64((acc[2i]^m[2i]) * (acc[2i+1]^m[2i+1]))
-            const uint64_t x = acc ^ smerge[l];
-            const uint64_t y = __shfl_down_sync(0xffffffffu, x, 1);
-            uint64_t m = ((l & 1) == 0) ? ((x * y) ^ __umul64hi(x, y)) : 0;
-            m += __shfl_xor_sync(0xffffffffu, m, 2);
-            m += __shfl_xor_sync(0xffffffffu, m, 4);
-            uint64_t h = P * kP64_1 + m;
-            h ^= h >> 37;
-            h *= kMx1;
-            h ^= h >> 32;
-            if (lane == 0) {
-                const uint64_t g = R.page_base + page;
-                newhash[g] = h;
-                flags[g] = (h != R.table[page]) ? tag : 0;
-            }
-        }
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -441,7 +335,6 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_detect_hash_big(
 constexpr int kTmaCompute = 4;                                  // compute warps
 constexpr int kTmaRB = kTmaCompute * 8;                           // blocks per round
 constexpr int kTmaStages = 2;                                    // default ring depth
-constexpr int kTmaMaxStages = 6;
 constexpr uint32_t kTmaRound = (uint32_t)kTmaRB * 1024u;         // 32 KiB
 constexpr int kTmaChainThreads = (kTmaCompute + 1) * 32;          // named-barrier participants
 constexpr int kTmaThreads = kTmaChainThreads + 32;                // + loader warp
@@ -485,7 +378,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
     uint8_t *__restrict__ flags, uint64_t *__restrict__ newhash, uint8_t tag, uint32_t nst) {
     extern __shared__ __align__(1024) uint8_t ring[];  // nst x kTmaRound
     __shared__ uint64_t S[2][kTmaRB][8];
-    __shared__ __align__(8) uint64_t full_bar[kTmaMaxStages], empty_bar[kTmaMaxStages];
+    __shared__ __align__(8) uint64_t full_bar[kTmaStages], empty_bar[kTmaStages];
     __shared__ uint64_t sw[24], slast[8], smerge[8], sinit[8];
     if (threadIdx.x < 24) sw[threadIdx.x] = c_xxh.w[threadIdx.x];
     if (threadIdx.x < 8) {
@@ -563,7 +456,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_tma(
                 uint32_t fold = 0;
 #pragma unroll
                 for (int s2 = 0; s2 < 16; ++s2) fold ^= d[s2].x ^ d[s2].y ^ d[s2].z ^ d[s2].w;
-                const uint32_t dep = fold & (nst >> 16);  // nst <= kTmaMaxStages: always 0
+                const uint32_t dep = fold & (nst >> 16);  // nst <= kTmaStages: always 0
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_bar[st] + dep);
                 uint64_t a0 = 0, a1 = 0;
@@ -660,15 +553,11 @@ __device__ __forceinline__ void pair_half(const DevRegion *__restrict__ regs, co
     h.old = R.table[page];
 }
 
-template <typename T>
-__device__ __forceinline__ T pick4(uint32_t h, T a, T b, T c, T d) {
-    return h == 0 ? a : h == 1 ? b : h == 2 ? c : d;
-}
-
-// NP = pages hashed together (2 or 4): a 32 KiB round carries 32/NP blocks of
-// each page; compute warp w serves page w / (4/NP); chain lanes 8h..8h+7 run
-// page h's chain.
-template <int NP>
+// NP = 2 pages hashed together: a 32 KiB round carries 16 blocks of each
+// page; compute warp w serves page w / 2; chain lanes 8h..8h+7 run page h's
+// chain.  (Four pages per CTA, 8 chain steps per round, measured slower:
+// 0.865 vs 0.887 of peak on C2 64 KiB, 0.997 vs 1.021 on C4; removed.)
+constexpr int NP = 2;
 __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_pair(
     const DevRegion *__restrict__ regs, const uint32_t *__restrict__ big_idx,
     const uint64_t *__restrict__ big_pg, uint32_t n_big, uint64_t w_lo, uint64_t w_hi,
@@ -748,14 +637,8 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_pair
             const uint32_t p = lane & 3, b = lane >> 2;
             const uint32_t h = warp / kWarpsPerPage;                 // page of the group
             const uint32_t hb = (warp % kWarpsPerPage) * 8 + b;      // block within the page's segment
-            uint32_t my_rounds, my_bpp;
-            if (NP == 2) {
-                my_rounds = h ? H[1 % NP].rounds : H[0].rounds;
-                my_bpp = h ? H[1 % NP].bpp : H[0].bpp;
-            } else {
-                my_rounds = pick4(h, H[0].rounds, H[1 % NP].rounds, H[2 % NP].rounds, H[3 % NP].rounds);
-                my_bpp = pick4(h, H[0].bpp, H[1 % NP].bpp, H[2 % NP].bpp, H[3 % NP].bpp);
-            }
+            const uint32_t my_rounds = h ? H[1].rounds : H[0].rounds;
+            const uint32_t my_bpp = h ? H[1].bpp : H[0].bpp;
             for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
                 const uint32_t st = q % kPairStages, use = q / kPairStages;
                 const uint32_t buf = q & 1;
@@ -792,14 +675,8 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtasPerSm) k_detect_hash_pair
             const uint32_t l = lane & 7, h = (lane >> 3) % NP;
             const uint64_t key = sw[16 + l];
             uint64_t acc = sinit[l];
-            uint32_t hr, hbpp;
-            if (NP == 2) {
-                hr = h ? H[1 % NP].rounds : H[0].rounds;
-                hbpp = h ? H[1 % NP].bpp : H[0].bpp;
-            } else {
-                hr = pick4(h, H[0].rounds, H[1 % NP].rounds, H[2 % NP].rounds, H[3 % NP].rounds);
-                hbpp = pick4(h, H[0].bpp, H[1 % NP].bpp, H[2 % NP].bpp, H[3 % NP].bpp);
-            }
+            const uint32_t hr = h ? H[1].rounds : H[0].rounds;
+            const uint32_t hbpp = h ? H[1].bpp : H[0].bpp;
             for (uint32_t rr = 0; rr < rounds; ++rr, ++q) {
                 const uint32_t buf = q & 1;
                 bar_sync(1 + buf, kTmaChainThreads);
@@ -903,66 +780,34 @@ void launch_detect_hash_big(const Launch &L, const DevRegion *regs, const uint32
                             const uint64_t *big_pg, uint32_t n_big, uint64_t w_lo, uint64_t w_hi,
                             uint8_t *flags, uint64_t *newhash, uint8_t tag) {
     if (w_hi <= w_lo) return;
-    uint64_t blocks = w_hi - w_lo;
-    // TMA-fed kernel by default; CRUM_HASH_NO_TMA=1 selects the register-staged one
-    static const bool no_tma = getenv("CRUM_HASH_NO_TMA") != nullptr;
-    static const bool tma1 = getenv("CRUM_HASH_TMA1") != nullptr;
+    const uint64_t pages = w_hi - w_lo;
     // Page groups only when there are enough pages to give every CTA slot a
     // group: a short range (the host pipeline's first 16 MiB range holds only
     // 8 pages of 2 MiB) finishes sooner with one page per CTA
-    if (!no_tma && !tma1 && blocks >= (uint64_t)L.sms * kTmaCtasPerSm) {
-        // pages per CTA group: 2 (CRUM_HASH_NP=4: one page per compute warp,
-        // 8 chain steps per round -- measured slower: 0.865 vs 0.887 of peak on
-        // C2 64 KiB, 0.997 vs 1.021 on C4)
+    if (pages >= (uint64_t)L.sms * kTmaCtasPerSm) {
         const uint64_t cap = (uint64_t)L.sms * kTmaCtasPerSm;
-        static const int np = getenv("CRUM_HASH_NP") && atoi(getenv("CRUM_HASH_NP")) == 4 ? 4 : 2;
         const size_t smem = (size_t)kPairStages * kTmaRound;
-        const uint64_t groups = (blocks + np - 1) / np;
+        const uint64_t groups = (pages + NP - 1) / NP;
         const uint64_t per = (groups + cap - 1) / cap;  // balanced: every CTA gets the same number
         const uint64_t grid = (groups + per - 1) / per;
-        if (np == 4) {
-            cudaFuncSetAttribute(k_detect_hash_pair<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_detect_hash_pair<4><<<(unsigned)grid, kTmaThreads, smem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo,
-                                                                                  w_hi, flags, newhash, tag, 0u);
-        } else {
-            cudaFuncSetAttribute(k_detect_hash_pair<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_detect_hash_pair<2><<<(unsigned)grid, kTmaThreads, smem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo,
-                                                                                  w_hi, flags, newhash, tag, 0u);
-        }
+        cudaFuncSetAttribute(k_detect_hash_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_detect_hash_pair<<<(unsigned)grid, kTmaThreads, smem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo, w_hi,
+                                                                            flags, newhash, tag, 0u);
         ++*L.counter;
         return;
     }
-    if (!no_tma) {
-        // ring depth and CTAs per SM (CRUM_TMA_STAGES / CRUM_TMA_CTAS override
-        // the defaults for tuning)
-        static const uint32_t nst = [] {
-            const char *e = getenv("CRUM_TMA_STAGES");
-            const int v = e ? atoi(e) : kTmaStages;
-            return (uint32_t)std::min(std::max(v, 2), kTmaMaxStages);
-        }();
-        static const int per_sm = [] {
-            const char *e = getenv("CRUM_TMA_CTAS");
-            return e ? std::min(std::max(atoi(e), 1), kTmaCtasPerSm) : kTmaCtasPerSm;
-        }();
-        const size_t smem = (size_t)nst * kTmaRound;
-        cudaFuncSetAttribute(k_detect_hash_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_detect_hash_tma, kTmaThreads, smem);
-        // a page's scramble chain is serial: give every CTA the same number of
-        // pages (e.g. 512 x 2 MiB pages -> 256 CTAs x 2, not 444 CTAs x 1-2)
-        const uint64_t cap = (uint64_t)L.sms * (uint64_t)std::max(1, std::min(occ, per_sm));
-        const uint64_t per = (blocks + cap - 1) / cap;
-        blocks = (blocks + per - 1) / per;
-        k_detect_hash_tma<<<(unsigned)blocks, kTmaThreads, smem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo,
-                                                                             w_hi, flags, newhash, tag, nst);
-        ++*L.counter;
-        return;
-    }
-    const uint64_t cap = (uint64_t)L.sms * 2;
-    const uint64_t per = (blocks + cap - 1) / cap;
-    blocks = (blocks + per - 1) / per;
-    k_detect_hash_big<<<(unsigned)blocks, kBigThreads, 0, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo, w_hi,
-                                                                      flags, newhash, tag);
+    const uint32_t nst = kTmaStages;
+    const size_t smem = (size_t)nst * kTmaRound;
+    cudaFuncSetAttribute(k_detect_hash_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_detect_hash_tma, kTmaThreads, smem);
+    // a page's scramble chain is serial: give every CTA the same number of
+    // pages (e.g. 512 x 2 MiB pages -> 256 CTAs x 2, not 444 CTAs x 1-2)
+    const uint64_t cap = (uint64_t)L.sms * (uint64_t)std::max(1, std::min(occ, kTmaCtasPerSm));
+    const uint64_t per = (pages + cap - 1) / cap;
+    const uint64_t blocks = (pages + per - 1) / per;
+    k_detect_hash_tma<<<(unsigned)blocks, kTmaThreads, smem, L.stream>>>(regs, big_idx, big_pg, n_big, w_lo, w_hi,
+                                                                         flags, newhash, tag, nst);
     ++*L.counter;
 }
 

@@ -146,30 +146,6 @@ __device__ __forceinline__ uint64_t mask_units(const CompactArgs &a, uint64_t ba
     return u;
 }
 
-__global__ void __launch_bounds__(kCompactThreads) k_compact_count(CompactArgs a) {
-    if (a.first_range) {
-        for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.R;
-             r += (uint64_t)gridDim.x * blockDim.x)
-            a.reg_nd[r] = 0;
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            a.st->dirty_bytes = 0;
-            a.st->dirty_runs = 0;
-            a.st->crc_acc = 0;
-            a.st->status = kStOk;
-        }
-    }
-    const uint64_t base = a.p_lo + (uint64_t)blockIdx.x * kPagesPerCompactBlock + threadIdx.x * kPagesPerThread;
-    const uint32_t m = thread_mask(a, base);
-    const uint64_t c = block_sum(__popc(m));
-    const uint64_t u = block_sum(mask_units(a, base, m));
-    if (threadIdx.x == 0) {
-        a.blk_count[blockIdx.x] = (uint32_t)c;
-        a.blk_units[blockIdx.x] = u;
-    }
-}
-
-// Final range: per-region prefix sums (first slot, payload offset, unit
-// offset), the image table, header fields and the capacity verdict.
 __device__ void compact_finalize(const CompactArgs &a, uint64_t K, uint64_t U) {
     // per-region prefix sums (first slot, payload offset, unit offset) + table
     uint64_t carry_first = 0, carry_units = 0;
@@ -285,127 +261,12 @@ __device__ __forceinline__ void u2s_fill_big(const CompactArgs &a, uint64_t base
     }
 }
 
-__global__ void __launch_bounds__(kCompactThreads) k_compact_write(CompactArgs a) {
-    __shared__ U2sSmem s_u2s;
-    __shared__ uint64_t s_off[2];
-    __shared__ bool s_last;
-    // per-region dirty counts are aggregated in shared memory for the (usually
-    // one or few) regions this block's pages fall in, then added once per block
-    // (per-thread atomics on one global counter serialise at L2)
-    __shared__ uint32_t s_rcnt[kRegAgg];
-    __shared__ uint32_t s_r0;
-    if (threadIdx.x < kRegAgg) s_rcnt[threadIdx.x] = 0;
-    if (threadIdx.x == 0)
-        s_r0 = region_of_page(a.regs, a.R, a.p_lo + (uint64_t)blockIdx.x * kPagesPerCompactBlock);
-    // offsets of this block = running totals before this range + earlier blocks
-    uint64_t pc = 0, pu = 0;
-    for (uint32_t i = threadIdx.x; i < blockIdx.x; i += blockDim.x) {
-        pc += a.blk_count[i];
-        pu += a.blk_units[i];
-    }
-    pc = block_sum(pc);
-    pu = block_sum(pu);
-    if (threadIdx.x == 0) {
-        s_off[0] = a.rb[a.c].k + pc;
-        s_off[1] = a.rb[a.c].units + pu;
-    }
-    const uint64_t base = a.p_lo + (uint64_t)blockIdx.x * kPagesPerCompactBlock + threadIdx.x * kPagesPerThread;
-    uint32_t m = thread_mask(a, base);
-    // consume the detect marks of this range (so the next checkpoint starts
-    // from zero flags and one constant tag suffices: no per-call clearing)
-    if (base < a.p_hi) {
-        if (base >= a.p_lo && base + kPagesPerThread <= a.p_hi) {
-            *reinterpret_cast<uint4 *>(a.flags + base) = make_uint4(0, 0, 0, 0);
-        } else {
-            for (uint32_t b = 0; b < kPagesPerThread; ++b)
-                if (base + b >= a.p_lo && base + b < a.p_hi) a.flags[base + b] = 0;
-        }
-    }
-    uint64_t tc, tu;
-    const uint64_t ec = block_excl_scan(__popc(m), &tc);
-    const uint64_t eu = block_excl_scan(mask_units(a, base, m), &tu);  // syncs: s_off visible
-    uint64_t pos = s_off[0] + ec, upos = s_off[1] + eu;
-    const uint32_t m0 = m;
-    bool has_big = false;
-    const uint64_t pos0 = pos, upos0 = upos;
-    uint64_t dbytes = 0;
-    if (m) {
-        uint32_t r = region_of_page(a.regs, a.R, base + (__ffs(m) - 1));
-        DevRegion g = a.regs[r];
-        uint64_t next = (r + 1 < a.R) ? a.regs[r + 1].page_base : ~0ull;
-        uint32_t cnt = 0;
-        while (m) {
-            const int b = __ffs(m) - 1;
-            const uint64_t gid = base + b;
-            while (gid >= next) {
-                if (cnt) {
-                    if (r - s_r0 < kRegAgg) atomicAdd(&s_rcnt[r - s_r0], cnt);
-                    else atomicAdd(a.reg_nd + r, cnt);
-                }
-                cnt = 0;
-                ++r;
-                g = a.regs[r];
-                next = (r + 1 < a.R) ? a.regs[r + 1].page_base : ~0ull;
-            }
-            const uint64_t i = gid - g.page_base;
-            a.gids[pos] = (uint32_t)gid;
-            a.sunit[pos] = upos;
-            if (g.log2p - kSegLog2 > kU2sDirectLog2) has_big = true;
-            else
-                for (uint32_t j = 0; j < (1u << (g.log2p - kSegLog2)); ++j) a.u2s[upos + j] = (uint32_t)pos;
-            a.lids[pos] = (uint32_t)i;
-            if (a.has_hashes) a.lhash[pos] = (g.mode == kModeHash) ? a.newhash[gid] : 0;
-            dbytes += page_len(g, i);
-            ++cnt;
-            ++pos;
-            upos += 1ull << (g.log2p - kSegLog2);
-            m &= m - 1;
-        }
-        if (cnt) {
-            if (r - s_r0 < kRegAgg) atomicAdd(&s_rcnt[r - s_r0], cnt);
-            else atomicAdd(a.reg_nd + r, cnt);
-        }
-    }
-    u2s_fill_big(a, base, m0, pos0, upos0, has_big, s_u2s);
-    __syncthreads();
-    if (threadIdx.x < kRegAgg && s_rcnt[threadIdx.x] && s_r0 + threadIdx.x < a.R)
-        atomicAdd(a.reg_nd + s_r0 + threadIdx.x, s_rcnt[threadIdx.x]);
-    dbytes = warp_sum(dbytes);
-    if ((threadIdx.x & 31) == 0 && dbytes)
-        atomicAdd(reinterpret_cast<unsigned long long *>(&a.st->dirty_bytes), (unsigned long long)dbytes);
-    // ---- last block: publish running totals / finalise ----
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(a.done, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    uint64_t ac = 0, au = 0;
-    for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
-        ac += a.blk_count[i];
-        au += a.blk_units[i];
-    }
-    ac = block_sum(ac);
-    au = block_sum(au);
-    const uint64_t K = a.rb[a.c].k + ac, U = a.rb[a.c].units + au;
-    if (threadIdx.x == 0) {
-        a.rb[a.c + 1].k = K;
-        a.rb[a.c + 1].units = U;
-        if (a.rb_host) {  // zero-copy store: no copy-engine queue between host and totals
-            volatile RangeTotals *h = a.rb_host + a.c + 1;
-            h->k = K;
-            h->units = U;
-        }
-        *a.done = 0;
-    }
-    if (a.final_range) compact_finalize(a, K, U);
-}
 
 // ---------------------------------------------------------------------------
 // A2 in one pass (default): the blocks take logical ids from a ticket, publish
 // their (pages, units) aggregates in 64-bit status words and find their
 // exclusive prefix by decoupled look-back (so a block never waits on one that
-// has not started), then write ids / unit offsets as k_compact_write does.
+// has not started), then write ids, unit offsets and the unit->slot map in order.
 // Status word: [63:62] 1 aggregate / 2 inclusive prefix, [61:31] pages,
 // [30:0] 4 KiB units.  The words (blk_units reinterpreted) and the ticket
 // (done[2]) are reset by the last block, so every launch starts from zero.
@@ -461,7 +322,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs
     }
     const uint64_t base = a.p_lo + (uint64_t)blk * kPagesPerCompactBlock + threadIdx.x * kPagesPerThread;
     uint32_t m = thread_mask(a, base);
-    if (base < a.p_hi) {  // consume this range's detect marks (see k_compact_write)
+    if (base < a.p_hi) {  // consume this range's detect marks (flags are zero between calls)
         if (base >= a.p_lo && base + kPagesPerThread <= a.p_hi) {
             *reinterpret_cast<uint4 *>(a.flags + base) = make_uint4(0, 0, 0, 0);
         } else {
@@ -590,15 +451,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_onepass(CompactArgs
 void launch_compact(const Launch &L, const CompactArgs &a) {
     uint64_t nblk = a.p_hi > a.p_lo ? (a.p_hi - a.p_lo + kPagesPerCompactBlock - 1) / kPagesPerCompactBlock : 0;
     if (nblk == 0) nblk = 1;  // an empty range still publishes its totals / finalises
-    static const bool two_pass = getenv("CRUM_COMPACT2") != nullptr;
-    if (!two_pass) {
-        k_compact_onepass<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(a);
-        ++*L.counter;
-        return;
-    }
-    k_compact_count<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(a);
-    k_compact_write<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(a);
-    *L.counter += 2;
+    k_compact_onepass<<<(unsigned)nblk, kCompactThreads, 0, L.stream>>>(a);
+    ++*L.counter;
 }
 
 // ---------------------------------------------------------------------------
@@ -1331,9 +1185,9 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
         st->dirty_bytes = a.fs->dirty_bytes;
         st->dirty_runs = 0;
         st->crc_acc = 0;
-        a.fs->dirty_bytes = 0;
-        a.fs->ticket = 0;
-        a.fs->done = 0;
+        // the ticket / done counters are NOT reset here: a warp that is late
+        // to its final claim must still see ticket >= n_tiles.  The host
+        // zeroes the scratch stream-ordered before every launch.
     }
 }
 

@@ -23,6 +23,8 @@
 #include <thread>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -141,6 +143,66 @@ constexpr uint64_t kMaxTotalPages = 0x7fffffffull;
 
 }  // namespace
 
+namespace {
+// Pinned, device-mapped host pool (crum_config.pinned_pool_bytes): images are
+// carved from it first fit in 4 KiB granules; free extents are kept sorted by
+// offset and coalesce on release.  Images may be destroyed from any thread
+// (the writer thread of a persisting image joins first), so the free list has
+// its own lock.
+struct PinnedPool {
+    uint8_t *base = nullptr;
+    uint64_t bytes = 0;
+    uint64_t map_bytes = 0;  // > 0: mmap + cudaHostRegister (else cudaHostAlloc)
+    int numa_node = -1;
+    std::mutex mu;
+    std::map<uint64_t, uint64_t> free_ext;  // offset -> length
+    uint64_t in_use = 0;
+    uint32_t images = 0;
+
+    uint8_t *carve(uint64_t len) {
+        len = round_up(len ? len : 1, 4096);
+        std::lock_guard<std::mutex> g(mu);
+        for (auto it = free_ext.begin(); it != free_ext.end(); ++it) {
+            if (it->second < len) continue;
+            const uint64_t off = it->first, rest = it->second - len;
+            free_ext.erase(it);
+            if (rest) free_ext.emplace(off + len, rest);
+            in_use += len;
+            ++images;
+            return base + off;
+        }
+        return nullptr;
+    }
+    void release(uint8_t *p, uint64_t len) {
+        len = round_up(len ? len : 1, 4096);
+        std::lock_guard<std::mutex> g(mu);
+        in_use -= len;
+        --images;
+        uint64_t off = (uint64_t)(p - base);
+        auto next = free_ext.lower_bound(off);
+        if (next != free_ext.end() && off + len == next->first) {
+            len += next->second;
+            next = free_ext.erase(next);
+        }
+        if (next != free_ext.begin()) {
+            auto prev = std::prev(next);
+            if (prev->first + prev->second == off) {
+                off = prev->first;
+                len += prev->second;
+                free_ext.erase(prev);
+            }
+        }
+        free_ext.emplace(off, len);
+    }
+    uint64_t largest_free() {
+        std::lock_guard<std::mutex> g(mu);
+        uint64_t m = 0;
+        for (const auto &e : free_ext) m = std::max(m, e.second);
+        return m;
+    }
+};
+}  // namespace
+
 struct crum_image {
     uint8_t *host;
     uint64_t cap;
@@ -148,6 +210,7 @@ struct crum_image {
     int device;
     uint64_t map_bytes = 0;  // > 0: mmap'ed on the device's NUMA node + cudaHostRegister'ed
     int numa_node = -1;      // node the pages were bound to (-1: cudaHostAlloc, default policy)
+    PinnedPool *pool = nullptr;  // carved from the context's pool (released there on destroy)
     // asynchronous persistence (writer thread)
     std::thread writer;
     std::atomic<int> busy{0};
@@ -159,6 +222,9 @@ struct crum_image {
 struct crum_ctx {
     int device = 0;
     int numa_node = -1;  // images are bound to this host node (-1: default placement)
+    PinnedPool *pool = nullptr;  // crum_config.pinned_pool_bytes > 0
+    bool graphs_on = true;       // !CRUM_CFG_NO_GRAPH
+    bool fused_cfg = false;      // CRUM_CFG_FUSED
     crum_restore_session *session = nullptr;  // open lazy restore (blocks other state changes)
     uint32_t last_path = 0;                   // CRUM_PATH_* bits of the last gather
     // CUDA graph of the asynchronous device gather (one cached instance)
@@ -220,7 +286,6 @@ struct crum_ctx {
     uint64_t u2s_cap = 0;
     uint32_t *d_lids = nullptr;
     uint64_t *d_lhash = nullptr;
-    uint32_t *d_blk_count = nullptr;
     uint64_t *d_blk_units = nullptr;
     uint8_t *d_dbg = nullptr;
 
@@ -262,7 +327,7 @@ struct crum_ctx {
     cudaEvent_t ev_range[kMaxRanges];
     cudaEvent_t ev_t[6];
     cudaEvent_t ev_meta;
-    // CRUM_TRACE=1: per-range timing events of the host path, printed to stderr
+    // CRUM_CFG_TRACE: per-range timing events of the host path, printed to stderr
     bool trace = false;
     cudaEvent_t ev_trace[3 * kMaxRanges] = {};
     // CRUM_CFG_TIMING and the most recent call (crum_last_report)
@@ -375,18 +440,22 @@ Range make_range(const crum_ctx *c, uint64_t lo, uint64_t hi) {
                  big_at(c, hi)};
 }
 
-// Rebuild device descriptors and per-page arrays after the registry changed.
-// old_force_base[r]: page base of region r's force bits in the OLD force
+// Rebuild device descriptors and per-page arrays for the registry `regs`
+// (the live one after a register / unregister).  Transactional: every new
+// buffer is allocated and filled into a temporary first; only when all of
+// that succeeded are the old buffers freed and c->regs replaced, so a
+// CRUM_E_NOMEM leaves the context exactly as it was (crum.h conventions).
+// old_force_base[r]: page base of region r's force bits in the CURRENT force
 // array, or UINT64_MAX for a new region (all force-dirty).
-int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
-    const uint32_t R = (uint32_t)c->regs.size();
+int rebuild(crum_ctx *c, std::vector<HostRegion> regs, const std::vector<uint64_t> &old_force_base) {
+    const uint32_t R = (uint32_t)regs.size();
     std::vector<DevRegion> dr(R);
     std::vector<uint32_t> cmp_idx, hash_idx, big_idx;
     std::vector<uint64_t> cmp_seg{0}, hash_grp{0}, big_pg{0};
     uint64_t N = 0, F = 0, units = 0;
     bool any_hash = false;
     for (uint32_t r = 0; r < R; ++r) {
-        HostRegion &h = c->regs[r];
+        HostRegion &h = regs[r];
         h.page_base = N;
         DevRegion &d = dr[r];
         d.base = h.ptr;
@@ -416,71 +485,140 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
         F += h.bytes;
         units += h.n_pages << (h.log2p - kSegLog2);
     }
-    const uint64_t cap = pad_pages(N);
-    uint8_t *force = nullptr;
-    int st;
-    if ((st = dev_alloc(c, &force, cap))) return st;
-    CK(cudaMemset(force, 0, cap));
-    for (uint32_t r = 0; r < R; ++r) {
-        const uint64_t ob = old_force_base[r];
-        if (ob == UINT64_MAX) {
-            CK(cudaMemset(force + dr[r].page_base, 1, dr[r].n_pages));
-        } else {
-            CK(cudaMemcpy(force + dr[r].page_base, c->d_force + ob, dr[r].n_pages, cudaMemcpyDeviceToDevice));
-        }
+    // single-pass eligibility and its tile map
+    bool fused_ok = R > 0 && (units >> 27) == 0;
+    std::vector<uint64_t> tb{0};
+    for (const HostRegion &h : regs) {
+        fused_ok = fused_ok && h.mode == kModeCompare && h.log2p <= kFusedMaxLog2P;
+        const uint32_t tl = std::max(h.log2p, kFusedMinTileLog2);
+        tb.push_back(tb.back() + ((h.bytes + (1ull << tl) - 1) >> tl));
     }
-    if (cap > c->page_cap) {
-        dev_free(c->d_flags);
-        dev_free(c->d_newhash);
-        dev_free(c->d_gids);
-        dev_free(c->d_sunit);
-        dev_free(c->d_lids);
-        dev_free(c->d_lhash);
-        dev_free(c->d_blk_count);
-        dev_free(c->d_blk_units);
-        dev_free(c->d_dbg);
-        c->page_cap = 0;
-        const uint64_t nblk = cap / kPagesPerCompactBlock + 1;
-        if ((st = dev_alloc(c, &c->d_flags, cap)) || (st = dev_alloc(c, &c->d_newhash, cap * 8)) ||
-            (st = dev_alloc(c, &c->d_gids, cap * 4)) || (st = dev_alloc(c, &c->d_sunit, cap * 8)) ||
-            (st = dev_alloc(c, &c->d_lids, cap * 4 + 8)) || (st = dev_alloc(c, &c->d_lhash, cap * 8)) ||
-            (st = dev_alloc(c, &c->d_blk_count, nblk * 4)) || (st = dev_alloc(c, &c->d_blk_units, nblk * 8)) ||
-            (st = dev_alloc(c, &c->d_dbg, cap))) {
-            cudaFree(force);
-            return st;
+    const uint64_t cap = pad_pages(N);
+    const bool grow_pages = cap > c->page_cap;
+    const bool grow_u2s = units + 1 > c->u2s_cap;
+    const bool grow_rs = R + 1 > c->rs_cap;
+    const uint64_t meta_max = payload_offset_for(R) + tail_bytes_for(N, true) + 4096;
+    const bool grow_meta = meta_max > c->meta_cap;
+
+    // ---- phase 1: allocate every new buffer into temporaries ----
+    struct Tmp {
+        uint8_t *force = nullptr, *flags = nullptr, *dbg = nullptr, *meta = nullptr;
+        uint64_t *newhash = nullptr, *sunit = nullptr, *lhash = nullptr, *blk_units = nullptr;
+        uint32_t *gids = nullptr, *lids = nullptr, *u2s = nullptr, *reg_nd = nullptr;
+        DevRegion *regs = nullptr;
+        uint32_t *cmp_idx = nullptr, *hash_idx = nullptr, *big_idx = nullptr;
+        uint64_t *cmp_seg = nullptr, *hash_grp = nullptr, *big_pg = nullptr, *tile_base = nullptr, *status = nullptr;
+        RegStat *rs = nullptr;
+        void free_all() {
+            dev_free(force); dev_free(flags); dev_free(dbg); dev_free(meta); dev_free(newhash); dev_free(sunit);
+            dev_free(lhash); dev_free(blk_units); dev_free(gids); dev_free(lids); dev_free(u2s); dev_free(reg_nd);
+            dev_free(regs); dev_free(cmp_idx); dev_free(hash_idx); dev_free(big_idx); dev_free(cmp_seg);
+            dev_free(hash_grp); dev_free(big_pg); dev_free(tile_base); dev_free(status); dev_free(rs);
         }
+    } t;
+    const uint64_t nblk = cap / kPagesPerCompactBlock + 1;
+    int st = CRUM_OK;
+    auto alloc_all = [&]() -> int {
+        int e;
+        if ((e = dev_alloc(c, &t.force, cap))) return e;
+        if (grow_pages &&
+            ((e = dev_alloc(c, &t.flags, cap)) || (e = dev_alloc(c, &t.newhash, cap * 8)) ||
+             (e = dev_alloc(c, &t.gids, cap * 4)) || (e = dev_alloc(c, &t.sunit, cap * 8)) ||
+             (e = dev_alloc(c, &t.lids, cap * 4 + 8)) || (e = dev_alloc(c, &t.lhash, cap * 8)) ||
+             (e = dev_alloc(c, &t.blk_units, nblk * 8)) || (e = dev_alloc(c, &t.dbg, cap))))
+            return e;
+        if ((e = dev_alloc(c, &t.regs, sizeof(DevRegion) * R)) || (e = dev_alloc(c, &t.cmp_idx, 4 * cmp_idx.size())) ||
+            (e = dev_alloc(c, &t.cmp_seg, 8 * cmp_seg.size())) || (e = dev_alloc(c, &t.hash_idx, 4 * hash_idx.size())) ||
+            (e = dev_alloc(c, &t.hash_grp, 8 * hash_grp.size())) || (e = dev_alloc(c, &t.reg_nd, 4 * R + 4)) ||
+            (e = dev_alloc(c, &t.big_idx, 4 * big_idx.size())) || (e = dev_alloc(c, &t.big_pg, 8 * big_pg.size())))
+            return e;
+        if (grow_u2s && (e = dev_alloc(c, &t.u2s, 4 * (units + 1)))) return e;
+        if (fused_ok && ((e = dev_alloc(c, &t.tile_base, 8 * tb.size())) ||
+                         (e = dev_alloc(c, &t.status, 8 * (tb.back() + 1)))))
+            return e;
+        if (grow_rs && (e = dev_alloc(c, &t.rs, sizeof(RegStat) * (R + 1)))) return e;
+        if (grow_meta && (e = dev_alloc(c, &t.meta, meta_max))) return e;
+        return CRUM_OK;
+    };
+    if ((st = alloc_all())) {
+        t.free_all();
+        return st;
+    }
+    // ---- phase 2: fill them (CUDA errors here poison the context) ----
+    auto fill_all = [&]() -> int {
+        CK(cudaMemset(t.force, 0, cap));
+        for (uint32_t r = 0; r < R; ++r) {
+            const uint64_t ob = old_force_base[r];
+            if (ob == UINT64_MAX) CK(cudaMemset(t.force + dr[r].page_base, 1, dr[r].n_pages));
+            else CK(cudaMemcpy(t.force + dr[r].page_base, c->d_force + ob, dr[r].n_pages, cudaMemcpyDeviceToDevice));
+        }
+        int e;
+        if ((e = upload(c, t.regs, dr.data(), sizeof(DevRegion) * R)) ||
+            (e = upload(c, t.cmp_idx, cmp_idx.data(), 4 * cmp_idx.size())) ||
+            (e = upload(c, t.cmp_seg, cmp_seg.data(), 8 * cmp_seg.size())) ||
+            (e = upload(c, t.hash_idx, hash_idx.data(), 4 * hash_idx.size())) ||
+            (e = upload(c, t.hash_grp, hash_grp.data(), 8 * hash_grp.size())) ||
+            (e = upload(c, t.big_idx, big_idx.data(), 4 * big_idx.size())) ||
+            (e = upload(c, t.big_pg, big_pg.data(), 8 * big_pg.size())))
+            return e;
+        if (fused_ok) {
+            if ((e = upload(c, t.tile_base, tb.data(), 8 * tb.size()))) return e;
+            CK(cudaMemset(t.status, 0, 8 * (tb.back() + 1)));
+        }
+        return CRUM_OK;
+    };
+    if ((st = fill_all())) {
+        t.free_all();
+        return st;
+    }
+    // ---- phase 3: commit (frees cannot fail) ----
+    auto swap_in = [](auto *&dst, auto *&src) {
+        dev_free(dst);
+        dst = src;
+        src = nullptr;
+    };
+    swap_in(c->d_force, t.force);
+    if (grow_pages) {
+        swap_in(c->d_flags, t.flags);
+        swap_in(c->d_newhash, t.newhash);
+        swap_in(c->d_gids, t.gids);
+        swap_in(c->d_sunit, t.sunit);
+        swap_in(c->d_lids, t.lids);
+        swap_in(c->d_lhash, t.lhash);
+        swap_in(c->d_blk_units, t.blk_units);
+        swap_in(c->d_dbg, t.dbg);
         c->page_cap = cap;
     }
+    swap_in(c->d_regs, t.regs);
+    swap_in(c->d_cmp_idx, t.cmp_idx);
+    swap_in(c->d_cmp_seg, t.cmp_seg);
+    swap_in(c->d_hash_idx, t.hash_idx);
+    swap_in(c->d_hash_grp, t.hash_grp);
+    swap_in(c->d_big_idx, t.big_idx);
+    swap_in(c->d_big_pg, t.big_pg);
+    swap_in(c->d_reg_nd, t.reg_nd);
+    if (grow_u2s) {
+        swap_in(c->d_u2s, t.u2s);
+        c->u2s_cap = units + 1;
+    }
+    swap_in(c->d_tile_base, t.tile_base);
+    swap_in(c->d_status, t.status);
+    c->fused_ok = fused_ok;
+    c->n_tiles = fused_ok ? tb.back() : 0;
+    if (grow_rs) {
+        swap_in(c->d_rs, t.rs);
+        c->rs_cap = R + 1;
+    }
+    if (grow_meta) {
+        swap_in(c->d_meta, t.meta);
+        c->meta_cap = meta_max;
+    }
+    // detect marks are zero between calls; single-pass compaction's look-back
+    // status words start (and are left) zero
     CK(cudaMemset(c->d_flags, 0, c->page_cap));
-    // single-pass compaction: look-back status words start (and are left) zero
     CK(cudaMemset(c->d_blk_units, 0, 8 * (c->page_cap / kPagesPerCompactBlock + 1)));
     c->tag = 0;
-    dev_free(c->d_force);
-    c->d_force = force;
-    // descriptors
-    dev_free(c->d_regs);
-    dev_free(c->d_cmp_idx);
-    dev_free(c->d_cmp_seg);
-    dev_free(c->d_hash_idx);
-    dev_free(c->d_hash_grp);
-    dev_free(c->d_big_idx);
-    dev_free(c->d_big_pg);
-    dev_free(c->d_reg_nd);
-    if ((st = dev_alloc(c, &c->d_regs, sizeof(DevRegion) * R)) ||
-        (st = dev_alloc(c, &c->d_cmp_idx, 4 * cmp_idx.size())) ||
-        (st = dev_alloc(c, &c->d_cmp_seg, 8 * cmp_seg.size())) ||
-        (st = dev_alloc(c, &c->d_hash_idx, 4 * hash_idx.size())) ||
-        (st = dev_alloc(c, &c->d_hash_grp, 8 * hash_grp.size())) || (st = dev_alloc(c, &c->d_reg_nd, 4 * R + 4)) ||
-        (st = dev_alloc(c, &c->d_big_idx, 4 * big_idx.size())) || (st = dev_alloc(c, &c->d_big_pg, 8 * big_pg.size())))
-        return st;
-    if ((st = upload(c, c->d_regs, dr.data(), sizeof(DevRegion) * R)) ||
-        (st = upload(c, c->d_cmp_idx, cmp_idx.data(), 4 * cmp_idx.size())) ||
-        (st = upload(c, c->d_cmp_seg, cmp_seg.data(), 8 * cmp_seg.size())) ||
-        (st = upload(c, c->d_hash_idx, hash_idx.data(), 4 * hash_idx.size())) ||
-        (st = upload(c, c->d_hash_grp, hash_grp.data(), 8 * hash_grp.size())) ||
-        (st = upload(c, c->d_big_idx, big_idx.data(), 4 * big_idx.size())) ||
-        (st = upload(c, c->d_big_pg, big_pg.data(), 8 * big_pg.size())))
-        return st;
+    c->regs = std::move(regs);
     c->n_cmp = (uint32_t)cmp_idx.size();
     c->n_hash = (uint32_t)hash_idx.size();
     c->n_big = (uint32_t)big_idx.size();
@@ -488,49 +626,6 @@ int rebuild(crum_ctx *c, const std::vector<uint64_t> &old_force_base) {
     c->N = N;
     c->F = F;
     c->max_units = units;
-    if (units + 1 > c->u2s_cap) {
-        dev_free(c->d_u2s);
-        c->u2s_cap = 0;
-        if ((st = dev_alloc(c, &c->d_u2s, 4 * (units + 1)))) return st;
-        c->u2s_cap = units + 1;
-    }
-    // single-pass eligibility and its tile map
-    {
-        bool ok = R > 0 && (units >> 27) == 0;
-        std::vector<uint64_t> tb{0};
-        for (const HostRegion &h : c->regs) {
-            ok = ok && h.mode == kModeCompare && h.log2p <= kFusedMaxLog2P;
-            const uint32_t tl = std::max(h.log2p, kFusedMinTileLog2);
-            tb.push_back(tb.back() + ((h.bytes + (1ull << tl) - 1) >> tl));
-        }
-        dev_free(c->d_tile_base);
-        dev_free(c->d_status);
-        c->fused_ok = false;
-        c->n_tiles = 0;
-        if (ok) {
-            if ((st = dev_alloc(c, &c->d_tile_base, 8 * tb.size())) ||
-                (st = dev_alloc(c, &c->d_status, 8 * (tb.back() + 1))))
-                return st;
-            if ((st = upload(c, c->d_tile_base, tb.data(), 8 * tb.size()))) return st;
-            CK(cudaMemset(c->d_status, 0, 8 * (tb.back() + 1)));
-            c->n_tiles = tb.back();
-            c->fused_ok = true;
-        }
-    }
-    // per-region scratch and the host-path metadata buffer (head + tail)
-    if (R + 1 > c->rs_cap) {
-        dev_free(c->d_rs);
-        c->rs_cap = 0;
-        if ((st = dev_alloc(c, &c->d_rs, sizeof(RegStat) * (R + 1)))) return st;
-        c->rs_cap = R + 1;
-    }
-    const uint64_t meta_max = payload_offset_for(R) + tail_bytes_for(N, true) + 4096;
-    if (meta_max > c->meta_cap) {
-        dev_free(c->d_meta);
-        c->meta_cap = 0;
-        if ((st = dev_alloc(c, &c->d_meta, meta_max))) return st;
-        c->meta_cap = meta_max;
-    }
     // page ranges of the pipelined host path, boundaries on multiples of 16
     // pages: the first ranges are small (the host link starts early), then
     // they double up to ~F/8 (>= 128 MiB) each
@@ -679,7 +774,6 @@ CompactArgs compact_args(crum_ctx *c, const Range &rg, uint32_t ci, bool first, 
     a.first_range = first ? 1 : 0;
     a.final_range = final ? 1 : 0;
     a.c = ci;
-    a.blk_count = c->d_blk_count;
     a.blk_units = c->d_blk_units;
     a.gids = c->d_gids;
     a.sunit = c->d_sunit;
@@ -877,14 +971,58 @@ uint8_t *numa_pinned_alloc(uint64_t bytes, int node, uint64_t *map_bytes, bool *
     return static_cast<uint8_t *>(p);
 }
 
+// Pinned, device-mapped host memory on `node` (>= 0) or with the default
+// placement (cudaHostAlloc).  *map_bytes > 0 marks the mmap'ed kind;
+// *bound_node = the node mbind took, else -1.
+uint8_t *pinned_alloc(uint64_t bytes, int node, uint64_t *map_bytes, int *bound_node) {
+    *map_bytes = 0;
+    *bound_node = -1;
+    uint8_t *p = nullptr;
+    if (node >= 0) {
+        bool bound = false;
+        p = numa_pinned_alloc(bytes ? bytes : 1, node, map_bytes, &bound);
+        if (p && bound) *bound_node = node;
+    }
+    if (!p) {
+        *map_bytes = 0;
+        if (cudaHostAlloc(reinterpret_cast<void **>(&p), bytes ? bytes : 1,
+                          cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+    }
+    return p;
+}
+
+void pinned_free(uint8_t *p, uint64_t map_bytes) {
+    if (!p) return;
+    if (map_bytes) {
+        cudaHostUnregister(p);
+        munmap(p, map_bytes);
+    } else {
+        cudaFreeHost(p);
+    }
+}
+
 }  // namespace
 
 uint64_t crum_launch_count(const crum_ctx *c) { return c ? c->launches : 0; }
 
+int crum_config_init(crum_config *cfg) {
+    if (!cfg) return CRUM_E_INVAL;
+    cfg->chunk_bytes = 0;
+    cfg->pinned_pool_bytes = 0;
+    cfg->numa_node = CRUM_NUMA_AUTO;
+    cfg->flags = 0;
+    return CRUM_OK;
+}
+
 int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     if (!out) return CRUM_E_INVAL;
     *out = nullptr;
-    if (cfg && ((cfg->flags & ~(uint32_t)CRUM_CFG_TIMING) || cfg->reserved || (cfg->chunk_bytes % 4096))) {
+    const uint32_t kCfgFlags = CRUM_CFG_TIMING | CRUM_CFG_NO_GRAPH | CRUM_CFG_FUSED | CRUM_CFG_TRACE;
+    if (cfg && ((cfg->flags & ~kCfgFlags) || (cfg->chunk_bytes % 4096) || (cfg->pinned_pool_bytes % 4096) ||
+                cfg->numa_node < CRUM_NUMA_DEFAULT || cfg->numa_node >= 1024)) {
         set_detail("bad crum_config");
         return CRUM_E_INVAL;
     }
@@ -899,6 +1037,9 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     c->device = device;
     if (cfg && cfg->chunk_bytes) c->chunk = cfg->chunk_bytes;
     c->timing_cfg = cfg && (cfg->flags & CRUM_CFG_TIMING);
+    c->graphs_on = !(cfg && (cfg->flags & CRUM_CFG_NO_GRAPH));
+    c->fused_cfg = cfg && (cfg->flags & CRUM_CFG_FUSED);
+    c->trace = cfg && (cfg->flags & CRUM_CFG_TRACE);
     auto fail = [&](int st) {
         crum_destroy(c);
         return st;
@@ -907,9 +1048,9 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
     // pinned images go to the host node of the GPU's PCIe root (multi-socket
     // boxes: the D2H/H2D traffic then never crosses the socket link);
-    // CRUM_NUMA=<node> overrides, CRUM_NUMA=-1 keeps the default placement
-    if (const char *e = getenv("CRUM_NUMA")) c->numa_node = atoi(e) < 0 ? -1 : atoi(e);
-    else c->numa_node = device_numa_node(device);
+    // crum_config.numa_node overrides (CRUM_NUMA_DEFAULT: default placement)
+    const int want_node = cfg ? cfg->numa_node : CRUM_NUMA_AUTO;
+    c->numa_node = want_node == CRUM_NUMA_AUTO ? device_numa_node(device) : want_node == CRUM_NUMA_DEFAULT ? -1 : want_node;
     if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess) return fail(CRUM_E_CUDA);
     {
         // gathers of the host path get the highest priority so their blocks are
@@ -919,7 +1060,6 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
         if (cudaStreamCreateWithPriority(&c->gstream, cudaStreamNonBlocking, hi_prio) != cudaSuccess)
             return fail(CRUM_E_CUDA);
     }
-    c->trace = getenv("CRUM_TRACE") != nullptr;
     for (int i = 0; i < 3 * kMaxRanges; ++i)
         if (cudaEventCreate(&c->ev_trace[i]) != cudaSuccess) return fail(CRUM_E_CUDA);
     for (int i = 0; i < kRing; ++i) {
@@ -967,9 +1107,39 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     cudaMemset(c->d_rb, 0, sizeof(RangeTotals) * (kMaxRanges + 1));
     cudaMemset(c->d_done, 0, 16);
     std::vector<uint64_t> none;
-    int st = rebuild(c, none);
+    int st = rebuild(c, {}, none);
     if (st) return fail(st);
+    if (cfg && cfg->pinned_pool_bytes) {
+        PinnedPool *pool = new (std::nothrow) PinnedPool();
+        if (!pool) return fail(CRUM_E_NOMEM);
+        pool->base = pinned_alloc(cfg->pinned_pool_bytes, c->numa_node, &pool->map_bytes, &pool->numa_node);
+        if (!pool->base) {
+            delete pool;
+            set_detail("pinned pool of %llu bytes could not be allocated",
+                       (unsigned long long)cfg->pinned_pool_bytes);
+            return fail(CRUM_E_NOMEM);
+        }
+        pool->bytes = cfg->pinned_pool_bytes;
+        pool->free_ext.emplace(0, pool->bytes);
+        c->pool = pool;
+    }
     *out = c;
+    return CRUM_OK;
+}
+
+int crum_pinned_pool_info(crum_ctx *c, uint64_t *bytes, uint64_t *in_use, uint64_t *largest, uint32_t *images) {
+    if (!c) return CRUM_E_INVAL;
+    PinnedPool *p = c->pool;
+    if (bytes) *bytes = p ? p->bytes : 0;
+    if (largest) *largest = p ? p->largest_free() : 0;
+    if (p) {
+        std::lock_guard<std::mutex> g(p->mu);
+        if (in_use) *in_use = p->in_use;
+        if (images) *images = p->images;
+    } else {
+        if (in_use) *in_use = 0;
+        if (images) *images = 0;
+    }
     return CRUM_OK;
 }
 
@@ -994,7 +1164,6 @@ int crum_destroy(crum_ctx *c) {
     dev_free(c->d_u2s);
     dev_free(c->d_lids);
     dev_free(c->d_lhash);
-    dev_free(c->d_blk_count);
     dev_free(c->d_blk_units);
     dev_free(c->d_dbg);
     dev_free(c->d_tile_base);
@@ -1016,6 +1185,10 @@ int crum_destroy(crum_ctx *c) {
     for (int i = 0; i < kRing; ++i) dev_free(c->d_ring[i]);
     if (c->h_st) cudaFreeHost(c->h_st);
     if (c->h_rb) cudaFreeHost(c->h_rb);
+    if (c->pool) {
+        pinned_free(c->pool->base, c->pool->map_bytes);
+        delete c->pool;
+    }
     if (c->copy) cudaStreamDestroy(c->copy);
     if (c->gstream) cudaStreamDestroy(c->gstream);
     if (c->aux) cudaStreamDestroy(c->aux);
@@ -1114,10 +1287,10 @@ int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page
     for (const HostRegion &o : c->regs) old_base.push_back(o.page_base);
     old_base.push_back(UINT64_MAX);
     h.id = c->next_id;
-    c->regs.push_back(h);
-    st = rebuild(c, old_base);
-    if (st) {
-        c->regs.pop_back();
+    std::vector<HostRegion> regs = c->regs;
+    regs.push_back(h);
+    st = rebuild(c, std::move(regs), old_base);
+    if (st) {  // nothing changed (rebuild is transactional)
         cudaFree(h.shadow);
         return st;
     }
@@ -1138,10 +1311,11 @@ int crum_unregister_region(crum_ctx *ctx, uint32_t id) {
     std::vector<uint64_t> old_base;
     for (uint32_t r = 0; r < c->regs.size(); ++r)
         if (r != idx) old_base.push_back(c->regs[r].page_base);
-    HostRegion gone = c->regs[idx];
-    c->regs.erase(c->regs.begin() + idx);
-    int st = rebuild(c, old_base);
-    if (st) return st;
+    const HostRegion gone = c->regs[idx];
+    std::vector<HostRegion> regs = c->regs;
+    regs.erase(regs.begin() + idx);
+    int st = rebuild(c, std::move(regs), old_base);
+    if (st) return st;  // the region stays registered (rebuild is transactional)
     cudaFree(gone.shadow);
     return CRUM_OK;
 }
@@ -1242,16 +1416,15 @@ int crum_image_create(crum_ctx *ctx, uint64_t cap, crum_image **out) {
     if (!out) return CRUM_E_INVAL;
     crum_image *im = new (std::nothrow) crum_image{nullptr, cap, 0, c->device};
     if (!im) return CRUM_E_NOMEM;
-    if (c->numa_node >= 0) {
-        bool bound = false;
-        im->host = numa_pinned_alloc(cap ? cap : 1, c->numa_node, &im->map_bytes, &bound);
-        if (im->host && bound) im->numa_node = c->numa_node;
+    if (c->pool && (im->host = c->pool->carve(cap))) {
+        im->pool = c->pool;
+        im->numa_node = c->pool->numa_node;
+    } else {
+        im->host = pinned_alloc(cap, c->numa_node, &im->map_bytes, &im->numa_node);
     }
-    if (!im->host &&
-        cudaHostAlloc(reinterpret_cast<void **>(&im->host), cap ? cap : 1, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
-        cudaGetLastError();
+    if (!im->host) {
         delete im;
-        set_detail("cudaHostAlloc(%llu) failed", (unsigned long long)cap);
+        set_detail("pinned allocation of %llu bytes failed", (unsigned long long)cap);
         return CRUM_E_NOMEM;
     }
     *out = im;
@@ -1283,12 +1456,8 @@ int crum_image_destroy(crum_image *img) {
     }
     if (img->writer.joinable()) img->writer.join();
     cudaSetDevice(img->device);
-    if (img->map_bytes) {
-        cudaHostUnregister(img->host);
-        munmap(img->host, img->map_bytes);
-    } else {
-        cudaFreeHost(img->host);
-    }
+    if (img->pool) img->pool->release(img->host, img->cap);
+    else pinned_free(img->host, img->map_bytes);
     delete img;
     return CRUM_OK;
 }
@@ -1685,18 +1854,17 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     int st;
     uint64_t worst = 0;
     crum_image_required_bytes(c, UINT64_MAX, &worst);
-    // The single-pass kernel is opt-in (CRUM_FUSED=1): measured on B200 it ties
-    // the multi-kernel path on C2 and trails it by ~2% on C3.
-    static const bool fused_env = getenv("CRUM_FUSED") != nullptr;
-    if (flags & CRUM_COMPRESS) {
+    // The single-pass kernel is opt-in (CRUM_CFG_FUSED).
+        if (flags & CRUM_COMPRESS) {
         if ((st = enqueue_gather_z(c, s, img, capacity, full, timing))) return st;
         return rep ? finish_gather_z(c, s, capacity, rep, nullptr) : CRUM_OK;
     }
-    if (c->fused_ok && fused_env && !full && capacity >= worst) {
+    if (c->fused_ok && c->fused_cfg && !full && capacity >= worst) {
         // single pass: detect + compact + gather + commit in one kernel, then
         // the metadata CRC / tail / header
         if (timing) CK(cudaEventRecord(c->ev_t[0], s));
         if ((st = next_tag(c, s))) return st;
+        CK(cudaMemsetAsync(c->d_fs, 0, sizeof(FusedScratch), s));
         FusedArgs fa{};
         fa.regs = c->d_regs;
         fa.R = (uint32_t)c->regs.size();
@@ -1734,7 +1902,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
         }
         return CRUM_OK;
     }
-    static const bool graphs_on = getenv("CRUM_NO_GRAPH") == nullptr;
+    const bool graphs_on = c->graphs_on;
     if (!rep && graphs_on) {
         // asynchronous call: replay the captured sequence (one launch instead of
         // ~8 API calls; the small configurations are launch-bound)
@@ -1799,7 +1967,7 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     c->last_path = 0;
     uint64_t worst;
     crum_image_required_bytes(c, UINT64_MAX, &worst);
-    static const bool graphs_on = getenv("CRUM_NO_GRAPH") == nullptr;
+    const bool graphs_on = c->graphs_on;
     if (worst <= std::min(kSmallImage, c->chunk) && img->cap >= worst) {
         // small footprint: latency-bound, so run the device sequence (a replayed
         // graph) with the image's mapped address as the destination -- the

@@ -13,12 +13,14 @@ from paper_1808_00117_b200 import crum
 
 
 class Pair:
-    def __init__(self, specs, S, chunk_bytes: int = 0, misalign: int = 0, device_writer: bool = True):
-        """specs: list of (nbytes, page_size, mode)."""
+    def __init__(self, specs, S, chunk_bytes: int = 0, misalign: int = 0, device_writer: bool = True,
+                 flags: int = 0, **ctx_kw):
+        """specs: list of (nbytes, page_size, mode); flags: crum_config flags
+        (kernel-path variants: CFG_NO_GRAPH, CFG_FUSED)."""
         self.specs = specs
         self.S = S
         self.o = oracle.Oracle()
-        self.g = crum.Context(0, chunk_bytes=chunk_bytes)
+        self.g = crum.Context(0, chunk_bytes=chunk_bytes, flags=flags, **ctx_kw)
         self.host, self.dev, self.rid_o, self.rid_g = [], [], [], []
         self._backing = []
         self.device_writer = device_writer

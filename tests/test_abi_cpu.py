@@ -57,8 +57,14 @@ def test_cpu_side_argument_checks(crum):
     L = crum.lib()
     h = C.c_void_p()
     assert L.crum_create(0, None, None) == crum.E_INVAL
-    bad = crum.Config(4097, 0, 0)
-    assert L.crum_create(0, C.byref(bad), C.byref(h)) == crum.E_INVAL
+    for bad in (crum.Config(4097, 0, -1, 0), crum.Config(0, 4097, -1, 0), crum.Config(0, 0, -3, 0),
+                crum.Config(0, 0, 1024, 0), crum.Config(0, 0, -1, 1 << 9)):
+        assert L.crum_create(0, C.byref(bad), C.byref(h)) == crum.E_INVAL
+    cfg = crum.Config(123, 4096, 5, 7)
+    assert L.crum_config_init(C.byref(cfg)) == crum.OK
+    assert (cfg.chunk_bytes, cfg.pinned_pool_bytes, cfg.numa_node, cfg.flags) == (0, 0, crum.NUMA_AUTO, 0)
+    assert L.crum_config_init(None) == crum.E_INVAL
+    assert L.crum_pinned_pool_info(None, None, None, None, None) == crum.E_INVAL
     assert L.crum_destroy(None) == crum.E_INVAL
     assert L.crum_sync_shadow(None, None, None) == crum.E_INVAL
     assert L.crum_image_destroy(None) == crum.E_INVAL

@@ -79,3 +79,43 @@ def test_coordinated_single_process_passthrough():
     from paper_1808_00117_b200 import coord
     g = coord.coordinated(lambda: {"dirty_bytes": 5, "image_bytes": 9, "dirty_pages": 1, "t_total_ms": 2.5})
     assert (g.dirty_bytes, g.image_bytes, g.dirty_pages, g.max_ms, g.world) == (5, 9, 1, 2.5, 1)
+
+
+def _fail_worker(rank, world, port, out):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_1808_00117_b200 import coord
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def bad_step():
+        if rank == 1:
+            raise RuntimeError("CRUM_E_CAPACITY on rank 1")
+        return {"dirty_bytes": 1, "image_bytes": 2, "dirty_pages": 3, "t_total_ms": 1.0}
+
+    try:
+        coord.coordinated(bad_step)
+        out[rank] = "no error"
+    except coord.CoordinatedFailure as e:
+        out[rank] = ("failed", e.local_error is not None)
+    # the group stays aligned: the next coordinated step completes on both
+    g = coord.coordinated(lambda: {"dirty_bytes": 1, "image_bytes": 2, "dirty_pages": 3, "t_total_ms": 1.0})
+    out[10 + rank] = (g.dirty_bytes, g.image_bytes, g.dirty_pages)
+    dist.destroy_process_group()
+
+
+def test_coordinated_failure_raises_on_every_rank():
+    """A local failure (e.g. CAPACITY) on one rank raises CoordinatedFailure
+    on all ranks instead of leaving the others blocked in a collective."""
+    world = 2
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_fail_worker, args=(world, port, out), nprocs=world, join=True, )
+        res = dict(out)
+    assert res[0] == ("failed", False) and res[1] == ("failed", True)
+    assert res[10] == res[11] == (2, 4, 6)

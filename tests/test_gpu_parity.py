@@ -399,12 +399,12 @@ def test_async_device_gather_graph_replays(crum):
         assert big[:len(want)].cpu().numpy().tobytes() == want.tobytes(), epoch
 
 
-def test_numa_bound_image_bit_exact(crum, monkeypatch):
+def test_numa_bound_image_bit_exact(crum):
     """A pinned image placed by mmap + mbind + cudaHostRegister (forced with
-    CRUM_NUMA=0, since a single-node box would otherwise take cudaHostAlloc)
-    holds the same bytes as the oracle's image and restores as one."""
-    monkeypatch.setenv("CRUM_NUMA", "0")
-    p = mkpair(MIXED[:4], 27)
+    crum_config.numa_node = 0, since a single-node box would otherwise take
+    cudaHostAlloc) holds the same bytes as the oracle's image and restores as
+    one."""
+    p = mkpair(MIXED[:4], 27, numa_node=0)
     img = p.g.new_image()
     assert img.numa_node in (0, -1)          # -1: the sandbox refused mbind (memory still mmap'ed + registered)
     assert crum.device_numa_node(0) >= -1
@@ -422,8 +422,7 @@ def test_numa_bound_image_bit_exact(crum, monkeypatch):
     torch.cuda.synchronize()
     assert all(np.array_equal(d.cpu().numpy(), h) for d, h in zip(q.dev, p.host))
     img.destroy()
-    monkeypatch.setenv("CRUM_NUMA", "-1")
-    ctx = crum.Context(0)
+    ctx = crum.Context(0, numa_node=crum.NUMA_DEFAULT)
     assert ctx.new_image(4096).numa_node == -1
 
 
