@@ -2,20 +2,26 @@
 """bench.py -- checkpointed GB/s of the shadow-page sync hot path on B200.
 
 A "step" is one coordinated checkpoint of the whole registered footprint:
-A5 barrier -> A1 detect -> A2 compact -> A3 gather + commit (-> A4 copy-out for
-the e2e figure) -> A5 all-reduce of the dirty/image bytes.  Before every step
-the "application" rewrites a seeded d-fraction of the pages (synth writer
-kernel) and L2 is scrubbed with a 256 MiB streaming read; both run outside the step's
-CUDA events.  Inputs live in HBM (2 GiB > 126 MB L2 for C2).
+A5 barrier -> A1 detect -> A2 compact -> A3 gather + commit -> A4 copy-out
+into a pinned host image -> A5 all-reduce of the dirty/image bytes.  Before
+every step the "application" rewrites a seeded d-fraction of the pages (synth
+writer kernel) and L2 is scrubbed with a 256 MiB streaming read; both run
+outside the step's CUDA events.  Inputs (the registered regions) live in HBM
+when the timed region starts.
 
-  value  = F / T_dev : registered bytes per second with the image written to
-           a device buffer (crum_checkpoint_gather_device), device-event time.
-  e2e    = F / T_ckpt: same step through crum_checkpoint_gather into a pinned
-           host image (D2H of the image inside the timed region).
-  restore: F / T_restore through crum_restore_scatter (H2D inside).
+  value        = F / T_ckpt (registered bytes / (gather call ->
+                 image complete in pinned host memory, commit done)); T_ckpt
+                 from CUDA events on the call's stream, max over ranks.
+  e2e          = the same call through the public Python API, host wall clock
+                 per step including the A5 barrier + all-reduces (median).
+  device_phase = the same step with the image written to an HBM buffer
+                 (crum_checkpoint_gather_device): the HBM-roofline part.
+  roofline     = the dominant kernel (A1 detect) of the device phase.
+  restore      = F / T_restore through crum_restore_scatter (H2D inside).
 
-Default workload (N=1): BASELINE.json configs[1] -- C2, one 1 GiB region,
-64 KiB pages, 10% of pages rewritten per step, compare mode.
+Default workload (N=1): BASELINE.json's C4 per GPU -- 56 HPGMG-style level
+vectors + 4096 box regions, 64.2 GiB, 10% of pages rewritten per step,
+compare mode (the largest single-GPU config; C5 exceeds HBM).
 
 Multi-GPU: `python -m torch.distributed.run --nproc-per-node N bench.py --gpus N`
 (one region set per rank, weak scaling, NCCL barrier + all-reduce only).
@@ -52,7 +58,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="crum", choices=["crum", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--mode", default="compare", choices=["compare", "hash", "tracked"])
     ap.add_argument("--page", type=int, default=64 * KiB)
     ap.add_argument("--dirty", type=float, default=None,
@@ -186,7 +192,8 @@ def oracle_steps(specs, S, dirty, seconds: float, max_steps: int, min_steps: int
         host.append(h)
         o.register(h, P, mode)
     cap = o.required_bytes()
-    o.checkpoint_gather(capacity=cap)   # initial full image (epoch 0), untimed
+    out = np.zeros(cap, dtype=np.uint8)  # reused: the timed step allocates nothing
+    o.checkpoint_gather(capacity=cap, out=out)   # initial full image (epoch 0), untimed
     times = []
     t_start = time.perf_counter()
     epoch = 0
@@ -198,7 +205,7 @@ def oracle_steps(specs, S, dirty, seconds: float, max_steps: int, min_steps: int
             if mode == 2:  # TRACKED: the writer marks what it writes
                 o.mark_pages(r + 1, pages)
         t0 = time.perf_counter()
-        st, img, rep = o.checkpoint_gather(capacity=cap)
+        st, img, rep = o.checkpoint_gather(capacity=cap, out=out)
         times.append(time.perf_counter() - t0)
         assert st == 0
     F = sum(nb for nb, _, _ in specs)
@@ -237,7 +244,8 @@ def oracle_steps_threads(specs, S, dirty, seconds: float, max_steps: int, thread
                 host.append(h)
                 o.register(h, P, mode)
             cap = o.required_bytes()
-            o.checkpoint_gather(capacity=cap)
+            out = np.zeros(cap, dtype=np.uint8)
+            o.checkpoint_gather(capacity=cap, out=out)
             t_start = time.perf_counter()
             epoch = 0
             while True:
@@ -249,7 +257,7 @@ def oracle_steps_threads(specs, S, dirty, seconds: float, max_steps: int, thread
                         o.mark_pages(k + 1, pages)
                 bar.wait()
                 t0 = time.perf_counter()
-                st, _, _ = o.checkpoint_gather(capacity=cap)
+                st, _, _ = o.checkpoint_gather(capacity=cap, out=out)
                 assert st == 0
                 bar.wait()
                 if t == 0:
@@ -273,87 +281,225 @@ def oracle_steps_threads(specs, S, dirty, seconds: float, max_steps: int, thread
 
 
 def oracle_sample(specs, limit: int = 1 << 30):
-    """The whole workload when it is at most ~2 GiB, else its first regions up
-    to ~1 GiB (the last one truncated to whole pages): a bounded sample for
-    the single-threaded CPU oracle, same shapes and page sizes."""
+    """A bounded sample of the workload for the CPU oracle, same shapes and
+    page sizes: the whole workload when it is at most ~2 GiB; else every
+    small region (< 1 MiB: C4's 4096 box regions) plus the leading regions up
+    to ~`limit` bytes, the last one truncated to whole pages (SURVEY.md 8(d)
+    oracle timing, step 4: "the first 1 GiB of large regions plus all 4096
+    small regions")."""
     F = sum(nb for nb, _, _ in specs)
     if F <= 2 * limit:
         return specs, "the same workload"
+    small = [(nb, P, m) for nb, P, m in specs if nb < MiB]
     out, acc = [], 0
     for nb, P, mode in specs:
+        if nb < MiB:
+            continue
         take = min(nb, max(P, (limit - acc) // P * P))
         out.append((take, P, mode))
         acc += take
         if acc >= limit:
             break
-    return out, f"a {len(out)}-region slice of the workload"
+    what = f"a slice of the workload: the first {acc / GiB:g} GiB of its large regions"
+    if small:
+        what += f" plus all {len(small)} small regions (< 1 MiB)"
+    return out + small, what
 
 
-def parity_check(args, ctx, crum, regions, specs, S, epoch, stream, dimg, cap, gflags, limit=4 << 30):
-    """Untimed, after the measurements: copy the run's regions to the host,
-    commit both sides (GPU sync_shadow; the oracle registers the copies and
-    syncs), apply one more application epoch to both, then compare the GPU's
-    device image with the oracle's image byte for byte -- the same launch
-    configuration, page sizes and flags the timed steps used."""
-    import torch
+def host_info():
+    """CPU model, logical CPUs usable, and the NUMA node(s) they sit on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    cpus = sorted(os.sched_getaffinity(0))
+    nodes = []
+    try:
+        for d in sorted(os.listdir("/sys/devices/system/node")):
+            if not (d.startswith("node") and d[4:].isdigit()):
+                continue
+            span = set()
+            for part in open(f"/sys/devices/system/node/{d}/cpulist").read().strip().split(","):
+                if part:
+                    a, _, b = part.partition("-")
+                    span.update(range(int(a), int(b or a) + 1))
+            if span & set(cpus):
+                nodes.append(int(d[4:]))
+    except (OSError, ValueError):
+        pass
+    return {"cpu_model": model, "cpus": len(cpus), "numa_nodes": nodes}
+
+
+def image_bytes_for(specs, dirty: float) -> int:
+    """Image length of one step (format v1) from the seeded
+    dirty counts -- config metadata shared by both arms, not a result."""
+    R = len(specs)
+    K = sum(synth.dirty_count(dirty, synth.n_pages(nb, P)) for nb, P, _ in specs)
+    payload = sum(synth.dirty_count(dirty, synth.n_pages(nb, P)) * P for nb, P, _ in specs)
+    poff = -(-(64 + 48 * R) // 4096) * 4096
+    hashes = 8 * K if any(m == 1 for _, _, m in specs) else 0
+    return poff + payload + -(-4 * K // 8) * 8 + hashes
+
+
+def config_for(args, specs, desc, world: int):
+    """The `config` object of the JSON line -- identical in both arms."""
     F = sum(nb for nb, _, _ in specs)
-    if F > limit:
-        return {"checked": False, "why": f"footprint {F / GiB:g} GiB > {limit / GiB:g} GiB host-copy bound; "
-                                         "tests/test_gpu_fullsize.py samples these sizes"}
+    N = sum(synth.n_pages(nb, P) for nb, P, _ in specs)
+    K = sum(synth.dirty_count(args.dirty, synth.n_pages(nb, P)) for nb, P, _ in specs)
+    in_bytes = {"compare": 2 * F, "hash": F + 8 * N, "tracked": F}[args.mode]
+    return {"workload": desc, "config": args.config, "mode": args.mode, "dirty_fraction": args.dirty,
+            "regions_per_gpu": len(specs), "page_sizes": sorted({P for _, P, _ in specs}),
+            "footprint_bytes_per_gpu": F, "pages_per_gpu": N, "dirty_pages_per_step": K,
+            "image_bytes_per_step": image_bytes_for(specs, args.dirty), "content": args.content,
+            "compressed_images": bool(args.compress), "world_size": world,
+            "l2": ((f"inputs {in_bytes / MiB:g} MiB (regions + shadow) > 126 MB L2; " if in_bytes > 126e6
+                    else f"inputs {in_bytes / MiB:g} MiB (regions + shadow) fit in L2, so ") +
+                   "a 256 MiB streaming read before every step evicts L2 (the writer's dirty lines are "
+                   "written back there, untimed) and leaves it clean: every step starts cold")}
+
+
+def snapshot_to_host(tensors):
+    """Host copies of device tensors at HBM-footprint scale: the destination
+    pages are first touched by all host threads at once (a single-threaded
+    first touch of tens of GiB is what limits a plain .cpu()), then each
+    tensor is copied through a pinned bounce buffer on one stream."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    outs = [np.empty(t.numel(), dtype=np.uint8) for t in tensors]
+    jobs = []
+    for a in outs:
+        for o in range(0, a.size, 256 * MiB):
+            jobs.append((a, o, min(a.size, o + 256 * MiB)))
+    with ThreadPoolExecutor(max_workers=len(os.sched_getaffinity(0))) as ex:
+        list(ex.map(lambda j: j[0][j[1]:j[2]].fill(0), jobs))
+    chunk = 512 * MiB
+    bounce = [torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    s = torch.cuda.Stream()
+    evs = [torch.cuda.Event(), torch.cuda.Event()]
+    pending = [None, None]
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        k = 0
+        for t, a in zip(tensors, outs):
+            src = t.reshape(-1)
+            for o in range(0, a.size, chunk):
+                n = min(chunk, a.size - o)
+                b = k % 2
+                if pending[b] is not None:
+                    pending[b].result()       # the host copy out of this bounce buffer is done
+                with torch.cuda.stream(s):
+                    bounce[b][:n].copy_(src[o:o + n], non_blocking=True)
+                    evs[b].record(s)
+                evs[b].synchronize()
+                pending[b] = ex.submit(np.copyto, a[o:o + n], bounce[b][:n].numpy())
+                k += 1
+        for f in pending:
+            if f is not None:
+                f.result()
+    return outs
+
+
+def parity_check(args, ctx, crum, regions, specs, rids, S, epoch, stream, img, dimg, cap, gflags):
+    """Untimed, after the measurements, on every rank: commit the GPU side
+    (sync_shadow), copy the committed regions to the host, run one more
+    application epoch on the GPU and gather it THROUGH THE TIMED PATH (the
+    pinned-image crum_checkpoint_gather, same image, capacity and flags).
+    Every byte of that image is then checked against the CPU oracle region by
+    region (tests/fullparity.py: a fresh oracle per region on the host copy,
+    same writer epoch; header, table and padding rebuilt with struct + zlib),
+    which works at any footprint.  Up to 4 GiB the device-image path
+    (crum_checkpoint_gather_device) is also compared whole with the oracle's
+    image after one more epoch."""
+    import torch
     from oracle import oracle
+    from tests import fullparity
+    half = args.content == "half"
+    if gflags:
+        return {"checked": False, "why": "compressed images: tests/test_gpu_compress.py"}
     torch.cuda.synchronize()
     ctx.sync_shadow(stream)
-    o = oracle.Oracle()
-    host = []
-    for r, (nb, P, mode) in enumerate(specs):
-        h = oracle.aligned_empty(nb)
-        h[:] = regions[r].cpu().numpy()
-        host.append(h)
-        o.register(h, P, mode)
-    o.sync_shadow()
-    half = args.content == "half"
-    for r, (nb, P, mode) in enumerate(specs):
-        pg = synth.choose_dirty(S, epoch, r, synth.n_pages(nb, P), args.dirty)
-        synth.apply_writer(host[r], P, pg, S, epoch, r, touch=half)
-        dp = torch.from_numpy(pg.astype(np.uint32)).to(regions[r].device)
-        if mode == 2:
-            o.mark_pages(r + 1, pg)
-            crum.synth_write_pages_tracked(regions[r], nb, P, dp, dp.numel(), S, epoch, r,
-                                           ctx.region_tracker(r + 1), stream=stream)
-        else:
-            crum.synth_write_pages(regions[r], nb, P, dp, dp.numel(), S, epoch, r, half, stream=stream)
-    st, want, _ = o.checkpoint_gather(flags=oracle.COMPRESS if gflags & crum.COMPRESS else 0)
-    rep = ctx.checkpoint_gather_device(dimg, cap, stream=stream, flags=gflags)
     torch.cuda.synchronize()
-    got = dimg[:rep["image_bytes"]].cpu().numpy()
-    ok = st == 0 and got.nbytes == want.nbytes and bool(np.array_equal(got, want))
-    return {"checked": True, "ok": ok, "image_bytes": int(want.nbytes), "dirty_pages": int(rep["dirty_pages"]),
-            "what": "one more epoch after the timed steps: GPU device image vs the oracle's image, "
-                    "byte for byte (both sides committed to the run's state first)"}
+    t0 = time.perf_counter()
+    host = snapshot_to_host(regions)   # committed state, pageable host copies
+    t_copy = time.perf_counter() - t0
+
+    def write(e):
+        for r, (nb, P, mode) in enumerate(specs):
+            pg = synth.choose_dirty(S, e, r, synth.n_pages(nb, P), args.dirty)
+            dp = torch.from_numpy(pg.astype(np.uint32)).to(regions[r].device)
+            if mode == 2:
+                crum.synth_write_pages_tracked(regions[r], nb, P, dp, dp.numel(), S, e, r,
+                                               ctx.region_tracker(rids[r]), stream=stream)
+            else:
+                crum.synth_write_pages(regions[r], nb, P, dp, dp.numel(), S, e, r, half, stream=stream)
+
+    write(epoch)
+    ctx.checkpoint_gather(img, stream=stream, flags=gflags)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    res = fullparity.regionwise_check(img.view(), specs, rids, lambda r: host[r], S, epoch, args.dirty,
+                                      touch=half, threads=min(16, len(os.sched_getaffinity(0))))
+    out = {"checked": True, "ok": bool(res["ok"]), "path": "crum_checkpoint_gather (pinned image, as timed)",
+           "image_bytes": res["image_bytes"], "checked_bytes": res["checked_bytes"],
+           "dirty_pages": res["dirty_pages"], "oracle_s": round(time.perf_counter() - t1, 2),
+           "host_copy_s": round(t_copy, 2),
+           "what": "one more epoch after the timed steps; every byte of the GPU image checked against the CPU "
+                   "oracle region by region (tests/fullparity.py), header/table/padding via struct + zlib"}
+    F = sum(nb for nb, _, _ in specs)
+    if F <= 4 * GiB and dimg is not None:
+        # the device-image path too: state after `epoch` is committed on both
+        o = oracle.Oracle()
+        for r, (nb, P, mode) in enumerate(specs):
+            fullparity_state = host[r]  # regionwise_check applied epoch `epoch` to it in place
+            o.register(fullparity_state, P, mode)
+        o.sync_shadow()
+        e2 = epoch + 1
+        for r, (nb, P, mode) in enumerate(specs):
+            pg = synth.choose_dirty(S, e2, r, synth.n_pages(nb, P), args.dirty)
+            synth.apply_writer(host[r], P, pg, S, e2, r, touch=half)
+            if mode == 2:
+                o.mark_pages(r + 1, pg)
+        write(e2)
+        st, want, _ = o.checkpoint_gather()
+        rep = ctx.checkpoint_gather_device(dimg, cap, stream=stream, flags=gflags)
+        torch.cuda.synchronize()
+        got = dimg[:rep["image_bytes"]].cpu().numpy()
+        out["device_path_ok"] = bool(st == 0 and got.nbytes == want.nbytes and np.array_equal(got, want))
+        out["ok"] = out["ok"] and out["device_path_ok"]
+        o.close()
+    return out
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config == "c5":
+        args.mode = "hash"
     specs, desc = workload(args, 0)
-    specs, what = oracle_sample(specs)
+    config = config_for(args, specs, desc, world)
+    sample, what = oracle_sample(specs)
     S = synth.seed(1)
     steps = args.warmup + args.steps
     # the unmodified oracle on every host core: the sample is split into one
     # page slice per core, one oracle instance per thread (step = slowest)
     ncores = len(os.sched_getaffinity(0))
-    times, F, T = oracle_steps_threads(specs, S, args.dirty, seconds=1e9, max_steps=steps, threads=ncores)
+    times, Fs, T = oracle_steps_threads(sample, S, args.dirty, seconds=1e9, max_steps=steps, threads=ncores)
     t = times[args.warmup:]
-    v = F / statistics.mean(t) / 1e9
+    v = Fs / statistics.mean(t) / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(statistics.mean(t) * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (seeded splitmix64 words)",
-            "config": {"workload": desc, "footprint_bytes": F},
+            "data": "synthetic (seeded splitmix64 words; seeded page choice per epoch)",
+            "config": config,
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": T, "kind": "oracle",
-                             "sample": f"{what} ({F / GiB:g} GiB) split into {T} page slices, one oracle per "
-                                       f"thread, {args.steps} timed steps (step = slowest thread)"},
+                             "sample": f"{what} ({Fs / GiB:g} GiB) split into {T} page slices, one oracle per "
+                                       f"thread, {args.steps} timed steps (step = slowest thread); GB/s of "
+                                       f"sampled footprint", **host_info()},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -361,6 +507,19 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def timed_read_stream(crum, buf, nbytes, stream, reps=5):
+    import torch
+    e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms = []
+    for _ in range(reps):
+        e_a.record(stream)
+        crum.synth_scrub(buf, nbytes, stream=stream)
+        e_b.record(stream)
+        e_b.synchronize()
+        ms.append(e_a.elapsed_time(e_b))
+    return nbytes / (min(ms) / 1e3) / 1e9
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -370,7 +529,7 @@ def main():
     import torch.distributed as dist
     import __graft_entry__
     __graft_entry__.build()
-    from paper_1808_00117_b200 import crum
+    from paper_1808_00117_b200 import coord, crum
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -383,6 +542,7 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
+        world = dist.get_world_size()
     dev = torch.device("cuda", local)
     red_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")  # where collectives run
     stream = torch.cuda.Stream(device=dev)
@@ -391,10 +551,12 @@ def main():
     specs, desc = workload(args, rank)
     S = synth.seed(1) + (rank << 20)
     F = sum(nb for nb, _, _ in specs)
+    n_pages = sum(synth.n_pages(nb, P) for nb, P, _ in specs)
 
     gflags = crum.COMPRESS if args.compress else 0
     if args.compress or args.content != "random":
         desc += f", content {args.content}" + (", compressed images" if args.compress else "")
+    t_setup = time.perf_counter()
     ctx = crum.Context(local, timing=True)
     regions = []
     with torch.cuda.stream(stream):
@@ -407,29 +569,45 @@ def main():
             if args.content == "half":
                 t[nb // 2 // 4 * 4:].view(torch.float32).fill_(0.25)
             regions.append(t)
-            ctx.register_region(t, nb, P, mode)
-    trackers = [ctx.region_tracker(r + 1) for r in range(len(specs))] if args.mode == "tracked" else None
-    # the dirty pages of every epoch, precomputed on the host (untimed)
-    n_epochs = args.warmup + args.steps + max(3, args.steps // 2) + max(4, args.steps // 2) + 2
-    pages = [[torch.from_numpy(synth.choose_dirty(S, e, r, synth.n_pages(nb, P), args.dirty).astype(np.uint32)).to(dev)
-              for r, (nb, P, _) in enumerate(specs)] for e in range(1, n_epochs + 1)]
+    stream.synchronize()
+    t_alloc = time.perf_counter() - t_setup
+    # one batch registration (crum_register_regions): one descriptor rebuild
+    rids = ctx.register_regions([(t, nb, P, mode) for t, (nb, P, mode) in zip(regions, specs)])
+    t_reg = time.perf_counter() - t_setup - t_alloc
+    trackers = [ctx.region_tracker(rid) for rid in rids] if args.mode == "tracked" else None
+    # the dirty pages of an epoch: chosen on the host (seeded recipe), one H2D
+    # copy per epoch, sliced per region
+    page_cache = {}
+
+    def pages_of(e):
+        if e not in page_cache:
+            lists = [synth.choose_dirty(S, e, r, synth.n_pages(nb, P), args.dirty).astype(np.uint32)
+                     for r, (nb, P, _) in enumerate(specs)]
+            flat = torch.from_numpy(np.concatenate(lists) if lists else np.zeros(0, np.uint32)).to(dev)
+            out, o = [], 0
+            for a in lists:
+                out.append(flat[o:o + a.size])
+                o += a.size
+            page_cache.clear()
+            page_cache[e] = out
+        return page_cache[e]
+
     scrub = torch.empty(256 * MiB, dtype=torch.uint8, device=dev)
-    # image capacity: a worst-case image when it fits beside the footprint
-    # (asynchronous device path), else the exact bound for this dirty ratio
-    # (the call then checks capacity itself and waits)
-    worst = ctx.image_required_bytes()
     k_exp = sum(synth.dirty_count(args.dirty, synth.n_pages(nb, P)) for nb, P, _ in specs)
-    free_b, _ = torch.cuda.mem_get_info(dev)
-    cap = worst if worst + (1 << 30) < free_b - 2 * (1 << 30) and len(host_resident(args)) == 0 else \
-        ctx.image_required_bytes(k_exp)
-    async_ok = cap >= worst
-    dimg = torch.empty(cap + 256, dtype=torch.uint8, device=dev)
-    # epoch 0: the first (full) checkpoint, untimed
+    # the pinned image holds one step's image (the exact bound for this dirty
+    # ratio); the gather streams range by range and commits once it fits
+    cap = ctx.image_required_bytes(k_exp)
+    img = ctx.new_image(cap)
     ctx.sync_shadow(stream)   # epoch 0: commit the whole footprint (every page starts force-dirty)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    print(f"[bench] setup {setup_s:.1f} s: allocate + fill {t_alloc:.1f} s, register {len(specs)} regions "
+          f"{t_reg:.1f} s", file=sys.stderr, flush=True)
 
     def app_epoch(e):
+        pg_e = pages_of(e)
         for r, (nb, P, _) in enumerate(specs):
-            pg = pages[e - 1][r]
+            pg = pg_e[r]
             if trackers:
                 # TRACKED: the application's writer marks what it writes (crum_device.h)
                 crum.synth_write_pages_tracked(regions[r], nb, P, pg, pg.numel(), S, e, r, trackers[r],
@@ -439,25 +617,82 @@ def main():
                                        stream=stream)
         crum.synth_scrub(scrub, scrub.numel(), stream=stream)
 
-    from paper_1808_00117_b200 import coord
+    epoch = 0
 
-    def coordinated(fn):
-        """A5: barrier before detect; all-reduce of {dirty bytes, image bytes} after."""
-        return coord.coordinated(fn).local
+    # ---- headline: checkpoint into the pinned host image (A1-A5) ----
+    def pinned_step():
+        g = coord.coordinated(lambda: ctx.checkpoint_gather(img, stream=stream, flags=gflags))
+        return g
 
-    def device_step():
-        """One checkpoint into the device image, stream-asynchronous; with N > 1
-        the coordinated all-reduce needs the totals, so the step waits for them."""
-        if distributed:
-            return coordinated(lambda: (ctx.checkpoint_gather_device(dimg, cap, stream=stream, flags=gflags,
-                                                                     report=not async_ok),
-                                        ctx.last_report())[1])
-        ctx.checkpoint_gather_device(dimg, cap, stream=stream, flags=gflags, report=not async_ok)
-        return None
-
+    for _ in range(args.warmup):
+        epoch += 1
+        app_epoch(epoch)
+        pinned_step()
+    torch.cuda.synchronize()
+    if distributed:
+        dist.barrier()
+    clocks = Clocks(local)
+    launches0 = ctx.launch_count
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    epoch = 0
+    wall_ms, greps = [], []
+    for i in range(args.steps):
+        epoch += 1
+        app_epoch(epoch)
+        ev0[i].record(stream)
+        t0 = time.perf_counter()
+        greps.append(pinned_step())
+        wall_ms.append((time.perf_counter() - t0) * 1e3)
+        ev1[i].record(stream)
+    torch.cuda.synchronize()
+    if distributed:
+        dist.barrier()
+    launches = ctx.launch_count - launches0
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    T = coord.max_over_ranks(sum(step_ms) / 1e3)
+    value = world * F * args.steps / T / 1e9
+    rep = greps[-1].local
+    KP = rep["image_bytes"]
+    K = rep["dirty_pages"]
+    # slot bytes of the step (sum of P over the listed pages) from the image length
+    poff = -(-(64 + 48 * len(specs)) // 4096) * 4096
+    slot_bytes = KP - poff - (-(-4 * K // 8) * 8) - (8 * K if any(m == 1 for _, _, m in specs) else 0)
+    te = coord.max_over_ranks(statistics.median(wall_ms) / 1e3)
+    copy_ms = statistics.median([g.local["t_copy_ms"] for g in greps])
+
+    # host-link roofline: a plain pinned D2H copy of the image's size, timed live
+    nb = max(min(KP, 1 << 30), 1 << 20)
+    hsrc = torch.empty(nb, dtype=torch.uint8, device=dev)
+    hdst = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+    l_ms = []
+    for _ in range(3):
+        if distributed:
+            dist.barrier()  # every rank copies at once: the concurrent (whole-box) link
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        with torch.cuda.stream(stream):
+            hdst.copy_(hsrc, non_blocking=True)
+        b_.record(stream)
+        b_.synchronize()
+        l_ms.append(a_.elapsed_time(b_))
+    link_peak = nb / (coord.max_over_ranks(min(l_ms)) / 1e3) / 1e9
+    del hsrc, hdst
+
+    # ---- device phase: the same step with the image in HBM ----
+    worst = ctx.image_required_bytes()
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    dcap = worst if worst + (1 << 30) < free_b - 2 * (1 << 30) and not host_resident(args) else cap
+    async_ok = dcap >= worst
+    dimg = torch.empty(dcap + 256, dtype=torch.uint8, device=dev)
+
+    def device_step():
+        if distributed:
+            return coord.coordinated(lambda: (ctx.checkpoint_gather_device(dimg, dcap, stream=stream, flags=gflags,
+                                                                           report=not async_ok),
+                                              ctx.last_report())[1])
+        ctx.checkpoint_gather_device(dimg, dcap, stream=stream, flags=gflags, report=not async_ok)
+        return None
+
     for _ in range(args.warmup):
         epoch += 1
         app_epoch(epoch)
@@ -465,118 +700,94 @@ def main():
     torch.cuda.synchronize()
     if distributed:
         dist.barrier()
-    clocks = Clocks(local)
-    launches0 = ctx.launch_count
-    t_wall0 = time.perf_counter()
-    reps = []
+    d0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    d1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    dreps = []
     for i in range(args.steps):
         epoch += 1
         app_epoch(epoch)
-        ev0[i].record(stream)
+        d0[i].record(stream)
         device_step()
-        ev1[i].record(stream)
-        reps.append(ctx.last_report())  # after ev1: the wait is outside the timed interval
+        d1[i].record(stream)
+        dreps.append(ctx.last_report())  # after d1: the wait is outside the timed interval
     torch.cuda.synchronize()
     if distributed:
         dist.barrier()
-    wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
-    # context for fractions above 1.0: a plain streaming READ (no writes) of the
-    # first HBM region, timed the same way; the denominator stays the measured copy
+    Td = coord.max_over_ranks(sum(a.elapsed_time(b) for a, b in zip(d0, d1)) / 1e3) / args.steps
+    det_ms = [r["t_gather_ms"] if args.mode == "tracked" else r["t_detect_ms"] for r in dreps]
+    det_t = coord.max_over_ranks(sum(det_ms) / args.steps) / 1e3
+    dpay = dreps[-1]["image_bytes"]
+    peak, peak_src = read_peaks()
+    fused = bool(dreps[-1].get("path", 0) & 1)
+    # algorithmic bytes: what the method must move, not what a
+    # staged implementation moves.  Dominant kernel: A1 detect -- compare reads
+    # region + mirror (2F); hash reads region + table, writes new hashes
+    # (F + 16N); tracked: the gather (reads + writes the listed pages).
+    if fused:
+        kname, det_bytes = "fused_compare", 2 * F + 2 * slot_bytes
+    else:
+        kname = "gather" if args.mode == "tracked" else f"detect_{args.mode}"
+        det_bytes = {"compare": 2 * F, "hash": F + 16 * n_pages, "tracked": 2 * slot_bytes}[args.mode]
+    achieved = det_bytes / det_t / 1e9
+    # device phase, algorithmic: compare 2F + 2KP (read region + mirror, write
+    # mirror + image); hash F + 8N + 8K + KP; tracked N + 2KP
+    dev_alg = {"compare": 2 * F + 2 * slot_bytes, "hash": F + 8 * n_pages + 8 * K + slot_bytes,
+               "tracked": n_pages + 2 * slot_bytes}[args.mode]
+    # context for fractions above 1.0: a plain streaming READ of the largest HBM buffer
     dev_regs = [t for t in regions if t.is_cuda]
-    rd_t = max(dev_regs + [scrub], key=lambda t: t.numel())  # the largest HBM buffer
-    rd_n = min(rd_t.numel(), GiB) // 32 * 32
-    e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    rd_ms = []
-    for _ in range(5):
-        e_a.record(stream)
-        crum.synth_scrub(rd_t, rd_n, stream=stream)
-        e_b.record(stream)
-        e_b.synchronize()
-        rd_ms.append(e_a.elapsed_time(e_b))
-    read_stream = rd_n / (min(rd_ms) / 1e3) / 1e9
-    # host-resident regions (config 5): the detect reads them over the host
-    # link, so that link bounds the step; probe the SM-driven zero-copy read
-    # of the same pinned memory, timed the same way
+    rd_t = max(dev_regs + [scrub], key=lambda t: t.numel())
+    read_stream = timed_read_stream(crum, rd_t, min(rd_t.numel(), 8 * GiB) // 32 * 32, stream)
     host_regs = [t for t in regions if not t.is_cuda]
     host_link = None
     if host_regs:
-        h_n = min(host_regs[0].numel(), 4 * GiB) // 32 * 32
-        h_ms = []
-        for _ in range(3):
-            e_a.record(stream)
-            crum.synth_scrub(host_regs[0], h_n, stream=stream)
-            e_b.record(stream)
-            e_b.synchronize()
-            h_ms.append(e_a.elapsed_time(e_b))
-        host_link = h_n / (min(h_ms) / 1e3) / 1e9
-    launches = ctx.launch_count - launches0
-    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
-    T = sum(step_ms) / 1e3
-    det_ms = [r["t_gather_ms"] if args.mode == "tracked" else r["t_detect_ms"] for r in reps]
-    if distributed:
-        t = torch.tensor([T, sum(det_ms)], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        T, det_sum = float(t[0]), float(t[1])
-    else:
-        det_sum = sum(det_ms)
-    value = world * F * args.steps / T / 1e9
-    K = reps[-1]["dirty_pages"]
-    KP = reps[-1]["image_bytes"]
-    peak, peak_src = read_peaks()
-    # dominant kernel.  Single-pass path (all compare, P <= 64 KiB): the fused
-    # detect+compact+gather kernel, algorithmic bytes = read region + mirror
-    # (2F) + write image payload + mirror (2 KP).  Otherwise A1 detect:
-    # compare reads region + mirror (2F); hash reads region + table and writes
-    # the new hashes (F + 16 N).
-    n_pages = sum(synth.n_pages(nb, P) for nb, P, _ in specs)
-    payload = reps[-1]["image_bytes"]
-    fused = bool(reps[-1].get("path", 0) & 1)
-    if fused:
-        kname = "fused_compare"
-        det_bytes = 2 * F + 2 * payload
-    else:
-        kname = "gather" if args.mode == "tracked" else f"detect_{args.mode}"
-        det_bytes = {"compare": 2 * F, "hash": F + 16 * n_pages, "tracked": 2 * payload}[args.mode]
-    det_t = det_sum / args.steps / 1e3
-    achieved = det_bytes / det_t / 1e9
-    # whole device phase: detect + gather reads/writes (compare also rewrites the
-    # mirror of every listed page: + KP)
-    dev_alg = {"compare": 2 * F + 3 * payload, "hash": F + 16 * n_pages + 2 * payload,
-               "tracked": n_pages + 2 * payload}[args.mode]
-    traffic_key = f"{kname}:{args.config}:{specs[0][1]}:{args.dirty}"
-    in_bytes = {"compare": 2 * F, "hash": F + 8 * n_pages, "tracked": F}[args.mode]  # what one detect reads
+        host_link = timed_read_stream(crum, host_regs[0], min(host_regs[0].numel(), 4 * GiB) // 32 * 32, stream, 3)
+
+    config = config_for(args, specs, desc, world)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(T * 1e3 / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded splitmix64 words; seeded page choice per epoch)",
-        "config": {"workload": desc, "footprint_bytes_per_gpu": F, "pages_per_gpu": n_pages,
-                   "dirty_pages_per_step": K, "image_bytes_per_step": KP,
-                   "l2": ((f"inputs {in_bytes / MiB:g} MiB (regions + shadow) > 126 MB L2; " if in_bytes > 126e6
-                           else f"inputs {in_bytes / MiB:g} MiB (regions + shadow) fit in L2, so ") +
-                          "a 256 MiB streaming read before every step evicts L2 (the writer's dirty lines are "
-                          "written back there, untimed) and leaves it clean: every step starts cold"),
-                   "timing": "per-step CUDA events around crum_checkpoint_gather_device on its stream; "
-                             "application writer + scrub outside the events",
-                   "wall_ms_per_step_incl_writer": round(wall * 1e3 / args.steps, 3),
-                   "gpu_numa_node": crum.device_numa_node(local)},
+        "config": config,
+        "timing": {"value": "per-step CUDA events on the call's stream around the coordinated "
+                            "crum_checkpoint_gather into a pinned host image (returns when the image is "
+                            "complete and committed); application writer + L2 scrub outside the events; "
+                            "sum over the K steps, max over ranks",
+                   "setup_s": round(setup_s, 2),
+                   "comm": {"backend": dist.get_backend() if distributed else None, "ranks": world}},
+        "step": {"bound": "host_link", "image_bytes": KP, "dirty_pages": K, "t_copy_ms": round(copy_ms, 3),
+                 "link_peak_GBs": round(link_peak, 2),
+                 "link_peak_source": "pinned D2H copy of the image's size timed in this run (N > 1: all ranks "
+                                     "at once, the slowest rank)",
+                 "ideal_ms": round(max(KP / (link_peak * 1e9), Td) * 1e3, 3),
+                 "frac": round(max(KP / (link_peak * 1e9), Td) / (T / args.steps), 4),
+                 "note": "the step's bound is the copy-out of the image over the host link (or the device "
+                         "phase if longer); frac = ideal / measured step"},
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1),
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "alg_bytes_per_launch": det_bytes, "avg_launch_ms": round(det_t * 1e3, 4),
-                     "traffic": read_traffic(traffic_key), "traffic_key": traffic_key,
+                     "traffic": read_traffic(f"{kname}:{args.config}:{specs[0][1]}:{args.dirty}"),
                      "read_stream_GBs": round(read_stream, 1), "nominal_peak_GBs": 8000.0,
+                     "measured_in": "the device phase's timed steps (CUDA events around the kernel on its stream)",
                      "note": "peak = measured copy (read+write); a read-only stream measured here reaches "
                              "read_stream_GBs, so read-dominated kernels can exceed frac 1.0"},
-        "device_phase": {"alg_bytes_per_step": dev_alg, "achieved_GBs": round(dev_alg / (T / args.steps) / 1e9, 1),
-                         "frac": round(dev_alg / (T / args.steps) / 1e9 / peak, 4)},
+        "device_phase": {"value": round(world * F / Td / 1e9, 3), "unit": "GB/s", "ms_per_step": round(Td * 1e3, 4),
+                         "alg_bytes_per_step": dev_alg, "achieved_GBs": round(dev_alg / Td / 1e9, 1),
+                         "frac": round(dev_alg / Td / 1e9 / peak, 4),
+                         "what": "crum_checkpoint_gather_device (image in HBM), CUDA events; algorithmic "
+                                 "bytes compare 2F+2KP, hash F+8N+8K+KP, tracked N+2KP"},
+        "e2e": {"value": round(world * F / te / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": KP, "ms_per_step": round(te * 1e3, 3),
+                "note": "the public Python API (Context.checkpoint_gather under coord.coordinated), host wall "
+                        "clock per step incl. the A5 barrier + all-reduces, median, max over ranks; the "
+                        "regions being checkpointed live in HBM by definition",
+                "image_numa_node": img.numa_node},
         "gpu_launches": launches,
         "gpu_launches_synth": 2 * args.steps * len(specs),
         "clocks": clk,
     }
     if host_link:
-        # the detect's bytes that cross the host link, against the measured
-        # zero-copy read of that link; the HBM figures stay beside them
         hb = sum(t.numel() for t in host_regs)
         hbm = line["roofline"]
         line["roofline"] = {"bound": "host_link", "kernel": kname, "achieved": round(hb / det_t / 1e9, 2),
@@ -588,104 +799,53 @@ def main():
                             "note": f"{hb / GiB:g} GiB of the {F / GiB:g} GiB footprint are host-resident",
                             "hbm": hbm}
     if args.compress:
-        line["compression"] = {"image_bytes": reps[-1]["image_bytes"], "dirty_bytes": reps[-1]["dirty_bytes"],
-                               "ratio": round(reps[-1]["dirty_bytes"] / max(reps[-1]["image_bytes"], 1), 3),
-                               "codec": "word-repeat (lag-2) unit codec, DESIGN.md Z1-Z2"}
-    # ---- e2e: pinned host image, D2H inside the timed region ----
-    if not args.no_e2e:
-        img = ctx.new_image(cap)
-        ctx.checkpoint_gather(img, stream=stream, flags=gflags)
-        e2e_ms, e2e_reps = [], []
-        for i in range(max(3, args.steps // 2)):
-            epoch += 1
-            app_epoch(epoch)
-            torch.cuda.synchronize()
-            if distributed:
-                dist.barrier()
-            t0 = time.perf_counter()
-            e2e_reps.append(coordinated(lambda: ctx.checkpoint_gather(img, stream=stream, flags=gflags)))
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        te = statistics.median(e2e_ms) / 1e3
-        if distributed:
-            t = torch.tensor([te], dtype=torch.float64, device=red_dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t[0])
-        line["e2e"] = {"value": round(world * F / te / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                       "d2h_bytes_per_step": e2e_reps[-1]["image_bytes"], "ms_per_step": round(te * 1e3, 3),
-                       "note": "crum_checkpoint_gather into pinned host memory, host wall clock per call "
-                               "(median); the regions being checkpointed live in HBM by definition",
-                       "image_numa_node": img.numa_node,
-                       "link_GBs": (round(e2e_reps[-1]["image_bytes"] / e2e_reps[-1]["t_copy_ms"] / 1e6, 2)
-                                    if e2e_reps[-1]["t_copy_ms"] > 0 else None)}
-        # host-link roofline: a plain pinned D2H copy of the same size, timed live
-        nb = max(min(e2e_reps[-1]["image_bytes"], 1 << 30), 1 << 20)
-        hsrc = torch.empty(nb, dtype=torch.uint8, device=dev)
-        hdst = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
-        l_ms = []
-        for _ in range(3):
-            if distributed:
-                dist.barrier()  # every rank copies at once: the concurrent (whole-box) link
-            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a_.record(stream)
-            with torch.cuda.stream(stream):
-                hdst.copy_(hsrc, non_blocking=True)
-            b_.record(stream)
-            b_.synchronize()
-            l_ms.append(a_.elapsed_time(b_))
-        l_min = min(l_ms)
-        if distributed:  # the slowest rank's concurrent copy sets the per-rank share
-            t = torch.tensor([l_min], dtype=torch.float64, device=red_dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            l_min = float(t[0])
-        link_peak = nb / (l_min / 1e3) / 1e9
-        # the copy-out overlaps detection, so the e2e bound is the slower of the
-        # link copy of the image and the device-only step
-        e2e_ideal = world * F / max(e2e_reps[-1]["image_bytes"] / (link_peak * 1e9), T / args.steps)
-        line["e2e"]["link_roofline"] = {"peak_GBs": round(link_peak, 2), "source": "pinned D2H copy of the "
-                                        "image's size timed in this run (at N > 1: all ranks at once, the "
-                                        "slowest rank's time)",
-                                        "box_peak_GBs": round(world * link_peak, 2),
-                                        "frac": round(line["e2e"]["value"] / (e2e_ideal / 1e9), 4),
-                                        "ideal_value": round(e2e_ideal / 1e9, 1)}
-        del hsrc, hdst
-        # restore of the last image onto the live regions (H2D inside)
-        r_ms = []
-        for i in range(3):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            rr = ctx.restore_scatter(img, stream=stream)
-            r_ms.append((time.perf_counter() - t0) * 1e3)
-        line["restore"] = {"value": round(F / (statistics.median(r_ms) / 1e3) / 1e9, 3), "unit": "GB/s",
-                           "ms_per_call": round(statistics.median(r_ms), 3), "h2d_bytes": rr["image_bytes"],
-                           "link_GBs": round(rr["image_bytes"] / (statistics.median(r_ms) / 1e3) / 1e9, 2)}
-        # lazy restore (sec. 4.2 read-fault heuristic): time to first data and
-        # per-fault latency for windows of 1, 2, 4, ... pages of region 1
+        line["compression"] = {"image_bytes": rep["image_bytes"], "dirty_bytes": rep["dirty_bytes"],
+                               "ratio": round(rep["dirty_bytes"] / max(rep["image_bytes"], 1), 3)}
+
+    # ---- restore of the last timed step's image onto the live regions (H2D inside) ----
+    torch.cuda.synchronize()
+    r_ms = []
+    for i in range(3):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sess = ctx.restore_begin(img, stream=stream)
-        begin_ms = (time.perf_counter() - t0) * 1e3
-        n1 = synth.n_pages(specs[0][0], specs[0][1])
-        faults, page = [], 0
-        while page < n1 and len(faults) < 12:
-            t0 = time.perf_counter()
-            cov, res = sess.fetch(1, page, stream=stream)
-            stream.synchronize()
-            faults.append([cov, res, round((time.perf_counter() - t0) * 1e6, 1)])
-            page += max(cov, 1)
+        rr = ctx.restore_scatter(img, stream=stream)
+        r_ms.append((time.perf_counter() - t0) * 1e3)
+    tr = statistics.median(r_ms) / 1e3
+    line["restore"] = {"value": round(F / tr / 1e9, 3), "unit": "GB/s", "ms_per_call": round(tr * 1e3, 3),
+                       "h2d_bytes": rr["image_bytes"], "link_GBs": round(rr["image_bytes"] / tr / 1e9, 2),
+                       "link_frac": round(rr["image_bytes"] / tr / 1e9 / link_peak, 4),
+                       "note": "link_frac against the run's pinned D2H probe (H2D measured 55.6 vs D2H 55.2 GB/s "
+                               "on the pool's boxes, profiles/r01/probe_box.json)"}
+    # lazy restore (sec. 4.2 read-fault heuristic): per-fault latency for
+    # windows of 1, 2, 4, ... pages of region 1
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sess = ctx.restore_begin(img, stream=stream)
+    begin_ms = (time.perf_counter() - t0) * 1e3
+    n1 = synth.n_pages(specs[0][0], specs[0][1])
+    faults, page = [], 0
+    while page < n1 and len(faults) < 12:
         t0 = time.perf_counter()
-        sess.end(stream=stream)
-        line["lazy_restore"] = {"begin_ms": round(begin_ms, 3), "end_ms": round((time.perf_counter() - t0) * 1e3, 3),
-                                "faults": faults,
-                                "note": "sequential read faults on region 1 from page 0: [pages made present, "
-                                        "image slots written, host wall us incl. stream sync]; zero-copy "
-                                        "reads of the pinned image"}
-        # forked checkpoint (sec. 3.3): the application pauses for
-        # the gather only; a writer thread persists the image while the next epoch runs
+        cov, res = sess.fetch(rids[0], page, stream=stream)
+        stream.synchronize()
+        faults.append([cov, res, round((time.perf_counter() - t0) * 1e6, 1)])
+        page += max(cov, 1)
+    t0 = time.perf_counter()
+    sess.end(stream=stream)
+    line["lazy_restore"] = {"begin_ms": round(begin_ms, 3), "end_ms": round((time.perf_counter() - t0) * 1e3, 3),
+                            "faults": faults,
+                            "note": "sequential read faults on region 1 from page 0: [pages made present, "
+                                    "image slots written, host wall us incl. stream sync]; zero-copy reads of "
+                                    "the pinned image"}
+    # forked checkpoint (sec. 3.3): the application pauses for
+    # the gather only; a writer thread persists the image (fsync'd) while the
+    # next epoch runs
+    if KP <= 2 * GiB and not args.no_e2e:
         img2 = ctx.new_image(cap)
         tmpd = tempfile.mkdtemp(prefix="crum_bench_")
-        pause_ms, w_ms = [], []
+        pause_ms = []
         try:
-            for i in range(max(4, args.steps // 2)):
+            for i in range(4):
                 epoch += 1
                 app_epoch(epoch)
                 torch.cuda.synchronize()
@@ -694,43 +854,53 @@ def main():
                 t0 = time.perf_counter()
                 ctx.checkpoint_gather(im, stream=stream, flags=gflags)
                 pause_ms.append((time.perf_counter() - t0) * 1e3)
-                im.persist(os.path.join(tmpd, f"r{rank}_{i % 2}.crum"))
+                im.persist(os.path.join(tmpd, f"r{rank}_{i % 2}.crum"), fsync=True)
             img.persist_wait()
             img2.persist_wait()
             t0 = time.perf_counter()
-            img2.persist(os.path.join(tmpd, f"r{rank}_w.crum"))
+            img2.persist(os.path.join(tmpd, f"r{rank}_w.crum"), fsync=True)
             img2.persist_wait()
-            w_ms.append((time.perf_counter() - t0) * 1e3)
+            w_ms = (time.perf_counter() - t0) * 1e3
         finally:
             shutil.rmtree(tmpd, ignore_errors=True)
         line["forked"] = {"pause_ms": round(statistics.median(pause_ms), 3),
-                          "persist_GBs": round(img2.length / (w_ms[0] / 1e3) / 1e9, 3),
-                          "persist_ms": round(w_ms[0], 3), "image_bytes": img2.length,
-                          "note": "gather wall time with the previous image's writer in flight (two "
-                                  "alternating pinned images); persist = one image written to "
-                                  "tempfile.gettempdir() without fsync"}
+                          "persist_GBs": round(img2.length / (w_ms / 1e3) / 1e9, 3), "persist_ms": round(w_ms, 3),
+                          "image_bytes": img2.length,
+                          "note": "gather wall time with the previous image's writer in flight (two alternating "
+                                  "pinned images); persist = one image written and fsync'd to "
+                                  "tempfile.gettempdir()"}
         img2.destroy()
-        img.destroy()
-    # ---- cpu_baseline: the oracle on this workload, rank 0 at N=1 only ----
+    # ---- cpu_baseline: the oracle on a bounded sample, rank 0 at N=1 only ----
     if not args.no_cpu_baseline and world == 1:
         sample, what = oracle_sample(specs)
         times, Fo = oracle_steps(sample, synth.seed(1), args.dirty, seconds=args.cpu_seconds, max_steps=50)
         v = Fo / statistics.median(times) / 1e9
         line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                                 "sample": f"{len(times)} oracle checkpoint_gather steps over {what} "
-                                          f"({Fo / GiB:g} GiB, d={args.dirty}), writer untimed, median"}
-        # context: the same oracle on every host core (independent page slices)
+                                          f"({Fo / GiB:g} GiB, d={args.dirty}), writer untimed, median; GB/s of "
+                                          f"sampled footprint", **host_info()}
         ncores = len(os.sched_getaffinity(0))
         if ncores > 1:
-            tt, Ft, T = oracle_steps_threads(sample, synth.seed(1), args.dirty, seconds=args.cpu_seconds,
-                                             max_steps=50, threads=ncores)
+            tt, Ft, Tn = oracle_steps_threads(sample, synth.seed(1), args.dirty, seconds=args.cpu_seconds,
+                                              max_steps=50, threads=ncores)
             line["cpu_baseline"]["all_cores"] = {
-                "value": round(Ft / statistics.median(tt) / 1e9, 4), "unit": "GB/s", "cores": T,
-                "sample": f"{len(tt)} steps; the sample split into {T} page slices, one oracle per thread, "
+                "value": round(Ft / statistics.median(tt) / 1e9, 4), "unit": "GB/s", "cores": Tn,
+                "sample": f"{len(tt)} steps; the sample split into {Tn} page slices, one oracle per thread, "
                           f"writer untimed, step = slowest thread, median"}
-    # ---- parity of this run's GPU result with the oracle ----
-    if world == 1 and not host_resident(args):
-        line["parity"] = parity_check(args, ctx, crum, regions, specs, S, epoch + 1, stream, dimg, cap, gflags)
+    # ---- parity of this run's GPU result with the oracle, on every rank ----
+    if not host_resident(args):
+        par = parity_check(args, ctx, crum, regions, specs, rids, S, epoch + 1, stream, img,
+                           dimg if F <= 4 * GiB else None, dcap, gflags)
+        if distributed:
+            allp = [None] * world
+            dist.all_gather_object(allp, {"rank": rank, "ok": par.get("ok"), "checked": par.get("checked"),
+                                          "checked_bytes": par.get("checked_bytes")})
+            par["ranks"] = allp
+            par["ok"] = all(p["ok"] for p in allp) if par.get("checked") else par.get("ok")
+        line["parity"] = par
+    else:
+        line["parity"] = {"checked": False, "why": "host-resident regions: tests/test_gpu_fullsize.py samples C5"}
+    img.destroy()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if distributed:

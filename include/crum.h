@@ -201,6 +201,26 @@ CRUM_API int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint
                          uint32_t mode, uint32_t *region_id_out);
 CRUM_API int crum_unregister_region(crum_ctx *ctx, uint32_t region_id);
 
+/* Batch form of crum_register_region for applications with many regions
+ * (the paper's HPGMG-FV allocates thousands of 12-128 KB boxes):
+ * registers descs[0..n) with ONE rebuild of the device descriptors instead of
+ * n.  Each descriptor has crum_register_region's preconditions, ownership and
+ * shadow; the new ids are consecutive, in descriptor order (so descriptor
+ * order is image order).  Transactional: on any error no region is
+ * registered and *failed_index_out (nullable) holds the index of the first
+ * offending descriptor (UINT32_MAX when the error is not tied to one).
+ * n == 0 is a no-op.  Errors: INVAL, DEVICE, OVERLAP (also between two
+ * descriptors of the batch), NOMEM, CUDA. */
+typedef struct {
+    void *ptr;          /* region start (device / managed / UVA-mapped pinned host), 16-byte aligned */
+    uint64_t bytes;     /* > 0 */
+    uint64_t page_size; /* power of two in [4096, 2 MiB] */
+    uint32_t mode;      /* CRUM_MODE_* */
+    uint32_t reserved;  /* 0 */
+} crum_region_desc;
+CRUM_API int crum_register_regions(crum_ctx *ctx, uint32_t n, const crum_region_desc *descs,
+                                   uint32_t *region_ids_out, uint32_t *failed_index_out);
+
 /* Alg. 1 MarkPageAsDirty as an explicit call: sets the force
  * bit of every page overlapping [offset, offset+len).  len == 0 is a no-op.
  * Errors: NOREGION, RANGE (offset+len > bytes). */

@@ -200,13 +200,18 @@ class Oracle:
         self._check(self._L.orc_image_required_bytes(self._h, max_dirty, C.byref(n)), "required")
         return n.value
 
-    def checkpoint_gather(self, flags: int = 0, capacity: int | None = None):
-        """Returns (status, image bytes or None, report dict)."""
+    def checkpoint_gather(self, flags: int = 0, capacity: int | None = None, out: np.ndarray | None = None):
+        """Returns (status, image bytes or None, report dict).  With `out` (a
+        caller-owned uint8 buffer of at least `capacity` bytes, reused across
+        calls) the image is a view of it and nothing is allocated or copied."""
         cap = self.required_bytes() if capacity is None else capacity
-        buf = np.zeros(max(cap, 1), dtype=np.uint8)
+        buf = np.zeros(max(cap, 1), dtype=np.uint8) if out is None else out
+        assert buf.nbytes >= cap
         rep = Report()
         st = self._L.orc_checkpoint_gather(self._h, flags, _ptr(buf), cap, C.byref(rep))
-        img = buf[:rep.image_bytes].copy() if st == OK else None
+        if st != OK:
+            return st, None, rep.as_dict()
+        img = buf[:rep.image_bytes] if out is not None else buf[:rep.image_bytes].copy()
         return st, img, rep.as_dict()
 
     def restore_scatter(self, image: np.ndarray, flags: int = 0):

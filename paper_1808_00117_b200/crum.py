@@ -39,8 +39,8 @@ ALL_PAGES = (1 << 64) - 1
 
 # Every symbol include/*.h declares (checked by tests/test_abi_cpu.py).
 EXPORTED = (
-    "crum_create", "crum_destroy", "crum_register_region", "crum_unregister_region", "crum_mark_dirty",
-    "crum_sync_shadow", "crum_image_required_bytes", "crum_image_create", "crum_image_import",
+    "crum_create", "crum_destroy", "crum_register_region", "crum_register_regions", "crum_unregister_region",
+    "crum_mark_dirty", "crum_sync_shadow", "crum_image_required_bytes", "crum_image_create", "crum_image_import",
     "crum_image_data", "crum_image_destroy", "crum_checkpoint_gather", "crum_checkpoint_gather_device",
     "crum_restore_scatter", "crum_restore_scatter_device", "crum_status_string", "crum_last_error_detail",
     "crum_debug_detect", "crum_debug_export", "crum_launch_count", "crum_last_report",
@@ -64,6 +64,12 @@ class Config(C.Structure):
                 ("flags", C.c_uint32)]
 
 
+class RegionDesc(C.Structure):
+    """crum_region_desc (include/crum.h): one entry of a batch registration."""
+    _fields_ = [("ptr", C.c_void_p), ("bytes", C.c_uint64), ("page_size", C.c_uint64), ("mode", C.c_uint32),
+                ("reserved", C.c_uint32)]
+
+
 class Report(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("scanned_pages", "scanned_bytes", "dirty_pages", "dirty_bytes",
                                           "dirty_runs", "image_bytes")] + \
@@ -82,6 +88,7 @@ _sig = {
     "crum_pinned_pool_info": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u32)]),
     "crum_destroy": (_i, [_vp]),
     "crum_register_region": (_i, [_vp, _vp, _u64, _u64, _u32, C.POINTER(_u32)]),
+    "crum_register_regions": (_i, [_vp, _u32, _vp, C.POINTER(_u32), C.POINTER(_u32)]),
     "crum_unregister_region": (_i, [_vp, _u32]),
     "crum_mark_dirty": (_i, [_vp, _u32, _u64, _u64]),
     "crum_sync_shadow": (_i, [_vp, _vp, C.POINTER(_u64)]),
@@ -322,6 +329,29 @@ class Context:
                "crum_register_region")
         self._keep[rid.value] = keep if keep is not None else (ptr if hasattr(ptr, "data_ptr") else None)
         return rid.value
+
+    def register_regions(self, regions) -> list[int]:
+        """Batch registration (crum_register_regions): `regions` is a list of
+        (ptr, nbytes, page_size, mode); ptr a tensor (kept alive) or an address.
+        Returns the new ids in order; raises CrumError (nothing registered)."""
+        ids, fail = self.try_register_regions([(_addr(p), n, P, m) for p, n, P, m in regions])
+        if isinstance(ids, int):
+            _check(ids, f"crum_register_regions (descriptor {fail})")
+        for (p, _, _, _), rid in zip(regions, ids):
+            self._keep[rid] = p if hasattr(p, "data_ptr") else None
+        return ids
+
+    def try_register_regions(self, descs):
+        """Raw crum_register_regions over (address, nbytes, page_size, mode)
+        tuples: (ids, None) on success, else (status, failed index)."""
+        n = len(descs)
+        arr = (RegionDesc * max(n, 1))(*[RegionDesc(a, nb, P, m, 0) for a, nb, P, m in descs])
+        ids = (_u32 * max(n, 1))()
+        fail = _u32(0)
+        st = _L.crum_register_regions(self._h, n, C.cast(arr, _vp), ids, C.byref(fail))
+        if st != OK:
+            return st, (None if fail.value == 0xFFFFFFFF else fail.value)
+        return [ids[k] for k in range(n)], None
 
     def try_register(self, ptr: int, nbytes: int, page_size: int, mode: int = MODE_COMPARE) -> int:
         """Raw status of crum_register_region (tests of the error paths)."""

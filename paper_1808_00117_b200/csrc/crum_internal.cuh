@@ -138,6 +138,7 @@ struct GatherArgs {
     uint64_t dst_unit0;
     uint8_t *force;
     uint64_t u_lo, u_hi;
+    int no_commit;  // 1: copy to dst only (the commit runs later as a dst == nullptr pass)
 };
 
 // Metadata CRC + tail copy + header (last block).

@@ -457,7 +457,9 @@ void launch_compact(const Launch &L, const CompactArgs &a) {
 
 // ---------------------------------------------------------------------------
 // A3 gather + commit.  Units [u_lo, u_hi) of the range whose running totals
-// are rb[0] (before) and rb[1] (after); dst == nullptr: commit only.
+// are rb[0] (before) and rb[1] (after); dst == nullptr: commit only;
+// no_commit: copy only (a host gather into an image smaller than the worst
+// case commits after the whole image is known to fit).
 // Unit u is written at dst + (add_poff ? st->poff : 0) + (u - dst_unit0) * 4096.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kUnitsPerTask = 8;
@@ -545,9 +547,9 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
             const uint64_t off = (i << g.log2p) + (seg << kSegLog2);
             const uint64_t len = g.bytes > off ? min((uint64_t)kSegBytes, g.bytes - off) : 0;
             uint8_t *dst_img = payload ? payload + ((u - a.dst_unit0) << kSegLog2) : nullptr;
-            uint8_t *dst_mir = (g.mode == kModeCompare) ? g.mirror + off : nullptr;
+            uint8_t *dst_mir = (g.mode == kModeCompare && !a.no_commit) ? g.mirror + off : nullptr;
             if (dst_img || dst_mir) copy_unit(g.base + off, len, g.aligned32 != 0, dst_img, dst_mir, lane);
-            if (seg == 0 && lane == 0) {
+            if (seg == 0 && lane == 0 && !a.no_commit) {
                 if (g.mode == kModeHash) g.table[i] = a.newhash[gid];
                 a.force[gid] = 0;
             }

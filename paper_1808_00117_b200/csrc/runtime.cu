@@ -547,10 +547,39 @@ int rebuild(crum_ctx *c, std::vector<HostRegion> regs, const std::vector<uint64_
     // ---- phase 2: fill them (CUDA errors here poison the context) ----
     auto fill_all = [&]() -> int {
         CK(cudaMemset(t.force, 0, cap));
+        // carry the force bits of surviving regions over, new regions all
+        // force-dirty; consecutive regions that keep their relative layout
+        // (every region of an append, the two sides of an unregister) move
+        // as one copy / one memset, so registering R regions one by one
+        // costs O(R) calls, not O(R^2)
+        uint64_t run_dst = 0, run_src = UINT64_MAX, run_len = 0;
+        bool run_new = false;
+        auto flush = [&]() -> int {
+            if (run_len) {
+                if (run_new) CK(cudaMemset(t.force + run_dst, 1, run_len));
+                else CK(cudaMemcpy(t.force + run_dst, c->d_force + run_src, run_len, cudaMemcpyDeviceToDevice));
+            }
+            run_len = 0;
+            return CRUM_OK;
+        };
         for (uint32_t r = 0; r < R; ++r) {
             const uint64_t ob = old_force_base[r];
-            if (ob == UINT64_MAX) CK(cudaMemset(t.force + dr[r].page_base, 1, dr[r].n_pages));
-            else CK(cudaMemcpy(t.force + dr[r].page_base, c->d_force + ob, dr[r].n_pages, cudaMemcpyDeviceToDevice));
+            const bool is_new = ob == UINT64_MAX;
+            const uint64_t nb = dr[r].page_base;
+            const bool extends = run_len && is_new == run_new && run_dst + run_len == nb &&
+                                 (is_new || run_src + run_len == ob);
+            if (!extends) {
+                int e = flush();
+                if (e) return e;
+                run_dst = nb;
+                run_src = ob;
+                run_new = is_new;
+            }
+            run_len += dr[r].n_pages;
+        }
+        {
+            int e = flush();
+            if (e) return e;
         }
         int e;
         if ((e = upload(c, t.regs, dr.data(), sizeof(DevRegion) * R)) ||
@@ -1214,32 +1243,33 @@ int crum_destroy(crum_ctx *c) {
     return CRUM_OK;
 }
 
-int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page_size, uint32_t mode,
-                         uint32_t *region_id_out) {
-    ENTER(ctx);
-    NOT_IN_SESSION(c);
-    if (!ptr || !region_id_out || bytes == 0) {
+namespace {
+
+// Checks of one region descriptor that need no other region (crum.h
+// preconditions); on success fills h (without shadow, id or page base).
+int validate_region(crum_ctx *c, const crum_region_desc &d, HostRegion &h) {
+    if (!d.ptr || d.bytes == 0) {
         set_detail("null pointer or zero bytes");
         return CRUM_E_INVAL;
     }
-    if (page_size < 4096 || page_size > (2u << 20) || (page_size & (page_size - 1))) {
-        set_detail("page_size %llu not a power of two in [4096, 2 MiB]", (unsigned long long)page_size);
+    if (d.page_size < 4096 || d.page_size > (2u << 20) || (d.page_size & (d.page_size - 1))) {
+        set_detail("page_size %llu not a power of two in [4096, 2 MiB]", (unsigned long long)d.page_size);
         return CRUM_E_INVAL;
     }
-    if (reinterpret_cast<uintptr_t>(ptr) % 16) {
+    if (reinterpret_cast<uintptr_t>(d.ptr) % 16) {
         set_detail("ptr not 16-byte aligned");
         return CRUM_E_INVAL;
     }
-    if (mode != CRUM_MODE_COMPARE && mode != CRUM_MODE_HASH_XXH3 && mode != CRUM_MODE_TRACKED) {
-        set_detail("bad mode %u", mode);
+    if (d.mode != CRUM_MODE_COMPARE && d.mode != CRUM_MODE_HASH_XXH3 && d.mode != CRUM_MODE_TRACKED) {
+        set_detail("bad mode %u", d.mode);
         return CRUM_E_INVAL;
     }
-    const uint64_t n = bytes / page_size + (bytes % page_size != 0);
-    if (n > 0xffffffffull || c->N + n > kMaxTotalPages) {
+    const uint64_t n = d.bytes / d.page_size + (d.bytes % d.page_size != 0);
+    if (n > 0xffffffffull) {
         set_detail("too many pages");
         return CRUM_E_INVAL;
     }
-    const uintptr_t lo = reinterpret_cast<uintptr_t>(ptr), hi = lo + bytes;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(d.ptr), hi = lo + d.bytes;
     if (hi < lo) return CRUM_E_INVAL;
     for (uintptr_t a : {lo, hi - 1}) {
         cudaPointerAttributes at{};
@@ -1260,43 +1290,119 @@ int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page
             return CRUM_E_DEVICE;
         }
     }
-    for (const HostRegion &h : c->regs) {
-        const uintptr_t a = reinterpret_cast<uintptr_t>(h.ptr), b = a + h.bytes;
-        if (lo < b && a < hi) {
-            set_detail("overlaps region %u", h.id);
-            return CRUM_E_OVERLAP;
+    h = HostRegion{};
+    h.mode = d.mode;
+    h.ptr = static_cast<uint8_t *>(d.ptr);
+    h.bytes = d.bytes;
+    h.page_size = d.page_size;
+    h.n_pages = n;
+    h.log2p = (uint32_t)__builtin_ctzll(d.page_size);
+    return CRUM_OK;
+}
+
+}  // namespace
+
+int crum_register_regions(crum_ctx *ctx, uint32_t n, const crum_region_desc *descs, uint32_t *ids_out,
+                          uint32_t *failed_index_out) {
+    ENTER(ctx);
+    NOT_IN_SESSION(c);
+    if (failed_index_out) *failed_index_out = UINT32_MAX;
+    if (n == 0) return CRUM_OK;
+    if (!descs || !ids_out) {
+        set_detail("null descriptor or id array");
+        return CRUM_E_INVAL;
+    }
+    std::vector<HostRegion> add(n);
+    uint64_t pages = 0;
+    for (uint32_t k = 0; k < n; ++k) {
+        int st = validate_region(c, descs[k], add[k]);
+        if (st) {
+            if (failed_index_out) *failed_index_out = k;
+            return st;
+        }
+        pages += add[k].n_pages;
+    }
+    if (c->N + pages > kMaxTotalPages) {
+        set_detail("too many pages");
+        return CRUM_E_INVAL;
+    }
+    // overlap: among the batch and against the live regions (sorted sweep)
+    {
+        std::vector<std::pair<uintptr_t, int64_t>> iv;  // (start, batch index or -1 - live index)
+        iv.reserve(n + c->regs.size());
+        for (uint32_t k = 0; k < n; ++k) iv.push_back({reinterpret_cast<uintptr_t>(add[k].ptr), (int64_t)k});
+        for (size_t r = 0; r < c->regs.size(); ++r)
+            iv.push_back({reinterpret_cast<uintptr_t>(c->regs[r].ptr), -1 - (int64_t)r});
+        std::sort(iv.begin(), iv.end());
+        auto end_of = [&](int64_t t) {
+            const HostRegion &h = t >= 0 ? add[t] : c->regs[-1 - t];
+            return reinterpret_cast<uintptr_t>(h.ptr) + h.bytes;
+        };
+        for (size_t i = 1; i < iv.size(); ++i) {
+            if (iv[i].first < end_of(iv[i - 1].second)) {
+                const int64_t a = iv[i - 1].second, b = iv[i].second;
+                const int64_t k = b >= 0 ? b : a;  // a batch entry is involved (live regions never overlap)
+                if (failed_index_out) *failed_index_out = (uint32_t)k;
+                if (a < 0 || b < 0) set_detail("descriptor %lld overlaps region %u", (long long)k,
+                                               c->regs[-1 - (a < 0 ? a : b)].id);
+                else set_detail("descriptors %lld and %lld overlap", (long long)a, (long long)b);
+                return CRUM_E_OVERLAP;
+            }
         }
     }
     CK(cudaDeviceSynchronize());
-    HostRegion h{};
-    h.mode = mode;
-    h.ptr = static_cast<uint8_t *>(ptr);
-    h.bytes = bytes;
-    h.page_size = page_size;
-    h.n_pages = n;
-    h.log2p = (uint32_t)__builtin_ctzll(page_size);
-    // shadow: compare -> byte mirror, hash -> u64 table, tracked -> none
-    const uint64_t shadow_bytes = mode == kModeCompare ? round_up(bytes, 256) : mode == kModeHash ? 8 * n : 0;
+    // shadows: compare -> byte mirror, hash -> u64 table, tracked -> none
     int st = CRUM_OK;
-    h.shadow = nullptr;
-    if (shadow_bytes) {
-        if ((st = dev_alloc(c, &h.shadow, shadow_bytes))) return st;
-        CK(cudaMemset(h.shadow, 0, shadow_bytes));
+    auto free_shadows = [&]() {
+        for (HostRegion &h : add)
+            if (h.shadow) {
+                cudaFree(h.shadow);
+                h.shadow = nullptr;
+            }
+    };
+    for (uint32_t k = 0; k < n && !st; ++k) {
+        HostRegion &h = add[k];
+        const uint64_t shadow_bytes =
+            h.mode == kModeCompare ? round_up(h.bytes, 256) : h.mode == kModeHash ? 8 * h.n_pages : 0;
+        h.shadow = nullptr;
+        if (shadow_bytes) {
+            if ((st = dev_alloc(c, &h.shadow, shadow_bytes))) break;
+            if (cudaMemset(h.shadow, 0, shadow_bytes) != cudaSuccess) {
+                cudaGetLastError();
+                st = CRUM_E_NOMEM;
+            }
+        }
+    }
+    if (st) {
+        free_shadows();
+        return st;
     }
     std::vector<uint64_t> old_base;
     for (const HostRegion &o : c->regs) old_base.push_back(o.page_base);
-    old_base.push_back(UINT64_MAX);
-    h.id = c->next_id;
     std::vector<HostRegion> regs = c->regs;
-    regs.push_back(h);
+    for (uint32_t k = 0; k < n; ++k) {
+        add[k].id = c->next_id + k;
+        regs.push_back(add[k]);
+        old_base.push_back(UINT64_MAX);
+    }
     st = rebuild(c, std::move(regs), old_base);
     if (st) {  // nothing changed (rebuild is transactional)
-        cudaFree(h.shadow);
+        free_shadows();
         return st;
     }
-    c->next_id++;
-    *region_id_out = h.id;
+    for (uint32_t k = 0; k < n; ++k) ids_out[k] = c->next_id + k;
+    c->next_id += n;
     return CRUM_OK;
+}
+
+int crum_register_region(crum_ctx *ctx, void *ptr, uint64_t bytes, uint64_t page_size, uint32_t mode,
+                         uint32_t *region_id_out) {
+    if (!region_id_out) {
+        set_detail("null region id pointer");
+        return CRUM_E_INVAL;
+    }
+    const crum_region_desc d{ptr, bytes, page_size, mode, 0};
+    return crum_register_regions(ctx, 1, &d, region_id_out, nullptr);
 }
 
 int crum_unregister_region(crum_ctx *ctx, uint32_t id) {
@@ -1865,6 +1971,9 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
         if (timing) CK(cudaEventRecord(c->ev_t[0], s));
         if ((st = next_tag(c, s))) return st;
         CK(cudaMemsetAsync(c->d_fs, 0, sizeof(FusedScratch), s));
+        // per-region dirty counts start at zero (the multi-kernel path's
+        // compaction leaves its own counts there)
+        CK(cudaMemsetAsync(c->d_reg_nd, 0, 4 * c->regs.size(), s));
         FusedArgs fa{};
         fa.regs = c->d_regs;
         fa.R = (uint32_t)c->regs.size();
@@ -1993,7 +2102,14 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     }
     int st = ensure_ring(c);
     if (st) return st;
-    const bool pipelined = img->cap >= worst;
+    // An image that holds a worst-case image cannot overflow: gathers commit
+    // as they copy.  A smaller image (the usual case at large footprints: a
+    // worst-case image is as large as the footprint) still streams range by
+    // range, but its gathers only copy; the commit runs as one more pass after
+    // the final range's metadata shows the image fits, so a CAPACITY error
+    // commits nothing (crum.h).  That pass re-reads the dirty pages of
+    // compare-mode regions once (KP of HBM reads, overlapped with the copy-out).
+    const bool deferred = img->cap < worst;
     const uint32_t nr = (uint32_t)c->ranges.size();
     const uint64_t poff = payload_offset_for(c->regs.size());
     CK(cudaEventRecord(c->ev_t[0], s));
@@ -2016,40 +2132,35 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
         }
         return CRUM_OK;
     };
-    // keep the GPU two ranges ahead of the host (all of them if capacity must
-    // be checked before anything is committed)
-    const uint32_t ahead = pipelined ? 2 : nr;
-    while (enq < nr && enq < ahead)
+    // keep the GPU two ranges ahead of the host
+    while (enq < nr && enq < 2)
         if ((st = enqueue_range(enq++))) return st;
-    if (!pipelined) {
-        CK(cudaEventSynchronize(c->ev_meta));
-        if (c->h_st->image_bytes > img->cap) {
-            if (rep) {
-                memset(rep, 0, sizeof *rep);
-                fill_report(c, *c->h_st, rep);
-            }
-            set_detail("image needs %llu bytes, capacity %llu", (unsigned long long)c->h_st->image_bytes,
-                       (unsigned long long)img->cap);
-            return CRUM_E_CAPACITY;
-        }
-    }
     // payload: per range, gathers into the ring + D2H
     Launch G = launch_of(c, c->gstream);
     const uint64_t upc = c->chunk >> kSegLog2;
     uint64_t chunk_idx = 0;
-    bool copy_started = false;
+    bool copy_started = false, overflow = false;
     c->h_rb[0] = RangeTotals{0, 0};
     for (uint32_t ci = 0; ci < nr; ++ci) {
         while (enq < nr && enq <= ci + 2)
             if ((st = enqueue_range(enq++))) return st;
         CK(cudaEventSynchronize(c->ev_range[ci]));
         const uint64_t U0 = c->h_rb[ci].units, U1 = c->h_rb[ci + 1].units;
+        // the image so far (payload of ranges <= ci, and the ids / hashes of
+        // their pages) already exceeds the capacity: stop copying, keep
+        // compacting to learn the required size
+        if (deferred && !overflow &&
+            poff + (U1 << kSegLog2) + tail_bytes_for(c->h_rb[ci + 1].k, c->any_hash) > img->cap)
+            overflow = true;
+        if (overflow) continue;
         if (U1 > U0) CK(cudaStreamWaitEvent(c->gstream, c->ev_range[ci], 0));
         for (uint64_t u0 = U0; u0 < U1; u0 += upc, ++chunk_idx) {
             const uint64_t u1 = std::min(U1, u0 + upc);
             const int slot = (int)(chunk_idx % kRing);
             if (chunk_idx >= (uint64_t)kRing) CK(cudaStreamWaitEvent(c->gstream, c->ev_copy[slot], 0));
-            launch_gather(G, gather_args(c, ci, c->d_ring[slot], u0, false, u0, u1), u1 - u0);
+            GatherArgs ga = gather_args(c, ci, c->d_ring[slot], u0, false, u0, u1);
+            ga.no_commit = deferred ? 1 : 0;
+            launch_gather(G, ga, u1 - u0);
             CK_LAUNCH();
             CK(cudaEventRecord(c->ev_gather[slot], c->gstream));
             CK(cudaStreamWaitEvent(c->copy, c->ev_gather[slot], 0));
@@ -2064,6 +2175,31 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
         if (c->trace) {
             CK(cudaEventRecord(c->ev_trace[3 * ci + 1], c->gstream));
             CK(cudaEventRecord(c->ev_trace[3 * ci + 2], c->copy));
+        }
+    }
+    if (deferred) {
+        CK(cudaEventSynchronize(c->ev_meta));
+        if (overflow || c->h_st->image_bytes > img->cap) {
+            CK(cudaStreamSynchronize(c->gstream));
+            CK(cudaStreamSynchronize(c->copy));
+            CK(cudaStreamSynchronize(s));
+            if (rep) {
+                memset(rep, 0, sizeof *rep);
+                fill_report(c, *c->h_st, rep);
+            }
+            set_detail("image needs %llu bytes, capacity %llu", (unsigned long long)c->h_st->image_bytes,
+                       (unsigned long long)img->cap);
+            return CRUM_E_CAPACITY;
+        }
+        // the image fits: commit every listed page (mirror / table / force),
+        // range by range, on the gather stream behind the copies' gathers
+        CK(cudaStreamWaitEvent(c->gstream, c->ev_meta, 0));
+        for (uint32_t ci = 0; ci < nr; ++ci) {
+            const uint64_t U0 = c->h_rb[ci].units, U1 = c->h_rb[ci + 1].units;
+            if (U1 > U0) {
+                launch_gather(G, gather_args(c, ci, nullptr, 0, false, U0, U1), U1 - U0);
+                CK_LAUNCH();
+            }
         }
     }
     // header + table, then ids/hashes
@@ -2796,6 +2932,7 @@ int crum_last_report(crum_ctx *ctx, crum_report *rep) {
     memset(rep, 0, sizeof *rep);
     fill_report(c, *c->h_st, rep);
     if (c->last_timed) fill_times(c, rep);
+    else rep->path = (c->last_kind == kLastDevFused ? CRUM_PATH_FUSED : 0u) | c->last_path;  // no times
     return CRUM_OK;
 }
 

@@ -150,3 +150,54 @@ def test_reregistration(crum):
     img = p.g.new_image()
     rep = p.g.checkpoint_gather(img)
     assert img.tobytes() == want.tobytes() and rep["dirty_pages"] == 6
+
+
+def test_batch_registration(crum):
+    """crum_register_regions: consecutive ids in descriptor order, the same
+    images as one-by-one registration (so the same as the oracle's), and a
+    transactional failure (an overlap between two descriptors, a bad page
+    size, an overlap with a live region) registers nothing and names the
+    offending descriptor."""
+    from oracle import oracle
+    specs = [(3 * 64 * KiB + 77, 64 * KiB, C), (40 * KiB + 8, 4 * KiB, H), (2 * MiB + 16, 2 * MiB, C),
+             (12 * KiB, 4 * KiB, 2)]
+    S = synth.seed(131)
+    ctx = crum.Context(0)
+    o = oracle.Oracle()
+    ts, hs = [], []
+    for r, (nb, P, mode) in enumerate(specs):
+        h = oracle.aligned_empty(nb)
+        synth.fill_region(h, S, r)
+        hs.append(h)
+        ts.append(torch.from_numpy(h.copy()).cuda())
+        o.register(h, P, mode)
+    ids = ctx.register_regions([(t, nb, P, m) for t, (nb, P, m) in zip(ts, specs)])
+    assert ids == [1, 2, 3, 4]
+    st, want, _ = o.checkpoint_gather()
+    img = ctx.new_image()
+    ctx.checkpoint_gather(img)
+    assert img.tobytes() == want.tobytes()
+    # failures register nothing
+    extra = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    a = extra.data_ptr()
+    st, fail = ctx.try_register_regions([(a, 65536, 4096, C), (a + 32768, 65536, 4096, C)])
+    assert st == crum.E_OVERLAP and fail == 1
+    st, fail = ctx.try_register_regions([(a, 65536, 4096, C), (a + 131072, 65536, 3000, C)])
+    assert st == crum.E_INVAL and fail == 1
+    st, fail = ctx.try_register_regions([(a, 65536, 4096, C), (ts[0].data_ptr() + 4096, 8192, 4096, C)])
+    assert st == crum.E_OVERLAP and fail == 1
+    assert ctx.try_register_regions([]) == ([], None)
+    # the registry is unchanged: the next ids continue, the next image lists the same regions
+    ids2 = ctx.register_regions([(extra, 65536, 4096, C)])
+    assert ids2 == [5]
+    ctx.unregister_region(5)
+    for r, (nb, P, mode) in enumerate(specs):
+        pg = synth.choose_dirty(S, 1, r, synth.n_pages(nb, P), 0.5)
+        synth.apply_writer(hs[r], P, pg, S, 1, r)
+        ts[r].copy_(torch.from_numpy(hs[r]))
+        if mode == 2:
+            o.mark_pages(r + 1, pg)
+            ctx.mark_dirty_pages(ids[r], torch.from_numpy(pg.astype(np.uint32)).cuda(), len(pg))
+    st, want, _ = o.checkpoint_gather()
+    ctx.checkpoint_gather(img)
+    assert img.tobytes() == want.tobytes()

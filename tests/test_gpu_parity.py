@@ -466,3 +466,36 @@ def test_hash_page_groups_straddle_regions(crum):
         p.g.checkpoint_gather(img)
         assert img.tobytes() == want.tobytes(), epoch
         assert p.shadows_equal()
+
+
+def test_deferred_commit_streaming_gather(crum):
+    """A pinned image smaller than the worst case (the bench's C4 setting): the
+    gather still streams range by range, copying without committing, and
+    commits after the final range shows the image fits.  Image bytes and
+    shadows equal the oracle's every epoch; an image that overflows part-way
+    through the ranges returns CAPACITY with the exact required size and
+    commits nothing (crum.h error convention)."""
+    specs = [(40 * MiB + 4096 * 3 + 5, 4 * KiB, C), (72 * MiB, 64 * KiB, H), (24 * MiB, 64 * KiB, C),
+             (8 * MiB + 300, 2 * MiB, H)]
+    p = mkpair(specs, 19, chunk_bytes=1 * MiB)
+    p.g.sync_shadow()
+    p.o.sync_shadow()
+    worst = p.g.image_required_bytes()
+    for epoch, d in [(1, 0.1), (2, 0.02), (3, 0.3), (4, 0.0)]:
+        p.write(epoch, d)
+        st, want, rep_o = p.o.checkpoint_gather()
+        assert st == 0
+        assert len(want) < worst
+        # overflow: the first ranges fit, a later one does not
+        short = p.g.new_image(len(want) * 2 // 3 if len(want) > 3 * 65536 else 4096)
+        st, rep = p.g.checkpoint_gather(short, raise_on_error=False)
+        if len(want) > short.capacity:
+            assert st == crum.E_CAPACITY and rep["image_bytes"] == len(want)
+            assert p.g.debug_detect(p.N).tolist() == p.oracle_flags().tolist()   # nothing committed
+        short.destroy()
+        img = p.g.new_image(len(want))     # exactly the image: deferred commit path
+        rep = p.g.checkpoint_gather(img)
+        assert img.tobytes() == want.tobytes(), epoch
+        assert rep["dirty_pages"] == rep_o["dirty_pages"] and rep["image_bytes"] == len(want)
+        assert p.shadows_equal(), epoch
+        img.destroy()

@@ -1,6 +1,6 @@
-"""Run the pinned-host checkpoint path a few times with CRUM_TRACE=1 (C2)."""
+"""Run the pinned-host checkpoint path a few times with the context flag
+CRUM_CFG_TRACE (per-range times on stderr; C2)."""
 import os, sys, time
-os.environ["CRUM_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import __graft_entry__; __graft_entry__.build()
@@ -10,7 +10,7 @@ GiB = 1 << 30
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 d = float(sys.argv[2]) if len(sys.argv) > 2 else 0.1
 s = torch.cuda.Stream()
-ctx = crum.Context(0)
+ctx = crum.Context(0, flags=crum.CFG_TRACE)
 t = torch.empty(GiB, dtype=torch.uint8, device="cuda")
 S = synth.seed(1)
 crum.synth_fill(t, GiB, S, 0, stream=s)
