@@ -473,57 +473,184 @@ int orc_image_required_bytes(orc_ctx *c, uint64_t max_dirty, uint64_t *out)
 
 /* ------------------------------------------------------------------ */
 /* Unit codec of compressed images (readings  */
-/* Z1-Z2 in DESIGN.md; the paper compresses with gzip -1 / LZ4 on the */
-/* CPU, and names no codec for this path).          */
-/* A 4096-byte unit is 1024 little-endian 32-bit words w[0..1023].    */
-/* Word j is predicted by w[j-2] (by 0 for j < 2); L is the set of j  */
-/* with w[j] != prediction.  The encoding of the unit is:             */
-/*   |L| == 0                 -> nothing (0 bytes; the unit is zero)  */
-/*   128 + 4|L| < 4096        -> a 128-byte bitmap (bit j of byte j/8 */
-/*                               set iff j in L) then w[j], j in L    */
-/*                               ascending, little-endian             */
-/*   otherwise                -> the 4096 raw bytes                   */
+/* Z2-Z3 in DESIGN.md).  The paper compresses the image with gzip -1  */
+/* or LZ4 before writing it (Table 2): an LZ77      */
+/* match finder plus an entropy coder.  Here every 4096-byte unit is  */
+/* encoded on its own (reading Z3):                                   */
+/*   all bytes zero          -> nothing (encoded size 0)              */
+/*   else the DEFLATE stream below if it is shorter than 4096 bytes,  */
+/*   else the 4096 raw bytes (encoded size 4096).                     */
+/* The DEFLATE stream (RFC 1951) is ONE block, BFINAL = 1, BTYPE = 01 */
+/* (the fixed Huffman codes of RFC 1951 sec. 3.2.6), zero-padded to a */
+/* whole byte, holding this greedy LZ77 parse of the unit u[0..4096): */
+/*   h(p)    = ((LE u32 at u+p) * 2654435761 mod 2^32) >> 20,         */
+/*             for p <= 4092 (a 12-bit hash of the 4 bytes at p);    */
+/*   cand(p) = the largest q < p with h(q) == h(p) -- every position */
+/*             enters the hash table, whether the parse stops there  */
+/*             or not;                                               */
+/*   len(p)  = the largest L <= min(258, 4096 - p) with               */
+/*             u[cand(p) + i] == u[p + i] for all i < L (0 if no      */
+/*             cand; the copy may overlap p);                        */
+/*   parse:  p = 0; while p < 4096: if len(p) >= 4 emit the match     */
+/*           (len(p), distance p - cand(p)) and p += len(p), else     */
+/*           emit the literal u[p] and p += 1; then end-of-block.     */
 /* ------------------------------------------------------------------ */
 #define ORC_UNIT 4096ull
-#define ORC_UNIT_WORDS 1024ull
+#define Z_HASH_BITS 12
+#define Z_MAX_MATCH 258u
+#define Z_MIN_MATCH 4u
 
-static uint32_t unit_word(const uint8_t *u, uint64_t j) { return rd32(u + 4 * j); }
+/* RFC 1951 sec. 3.2.5: length codes 257..285 (base length, extra bits) and
+ * distance codes 0..29 (base distance, extra bits), written out as tables. */
+static const uint16_t z_len_base[29] = {3, 4, 5, 6, 7, 8, 9, 10, 11, 13, 15, 17, 19, 23, 27, 31,
+                                        35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
+static const uint8_t z_len_extra[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2,
+                                        3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
+static const uint16_t z_dist_base[30] = {1, 2, 3, 4, 5, 7, 9, 13, 17, 25, 33, 49, 65, 97, 129, 193,
+                                         257, 385, 513, 769, 1025, 1537, 2049, 3073, 4097, 6145,
+                                         8193, 12289, 16385, 24577};
+static const uint8_t z_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6,
+                                         7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
 
-static int z_literal(const uint8_t *u, uint64_t j)
+/* Bit writer: bits go LSB-first into bytes (RFC 1951 sec. 3.1.1). */
+typedef struct {
+    uint8_t *out;
+    uint64_t cap, nbits;
+} z_bits;
+
+static void z_put(z_bits *w, uint32_t v, uint32_t n) /* n low bits of v, LSB first */
 {
-    uint32_t pred = j < 2 ? 0u : unit_word(u, j - 2);
-    return unit_word(u, j) != pred;
+    for (uint32_t i = 0; i < n; ++i, ++w->nbits) {
+        const uint64_t byte = w->nbits / 8;
+        if (byte >= w->cap) continue; /* counted, not stored: the caller falls back to raw */
+        if ((v >> i) & 1u) w->out[byte] |= (uint8_t)(1u << (w->nbits % 8));
+    }
+}
+
+/* A Huffman code is packed starting with its most significant bit. */
+static void z_put_code(z_bits *w, uint32_t code, uint32_t n)
+{
+    for (uint32_t i = 0; i < n; ++i) z_put(w, (code >> (n - 1 - i)) & 1u, 1);
+}
+
+/* Fixed literal/length code of symbol s (RFC 1951 sec. 3.2.6). */
+static void z_put_litlen(z_bits *w, uint32_t s)
+{
+    if (s <= 143) z_put_code(w, 0x30 + s, 8);
+    else if (s <= 255) z_put_code(w, 0x190 + (s - 144), 9);
+    else if (s <= 279) z_put_code(w, s - 256, 7);
+    else z_put_code(w, 0xC0 + (s - 280), 8);
+}
+
+static void z_put_match(z_bits *w, uint32_t len, uint32_t dist)
+{
+    uint32_t lc = 28;
+    while (z_len_base[lc] > len) --lc;       /* largest base <= len (258 -> code 285) */
+    z_put_litlen(w, 257 + lc);
+    z_put(w, len - z_len_base[lc], z_len_extra[lc]);
+    uint32_t dc = 29;
+    while (z_dist_base[dc] > dist) --dc;
+    z_put_code(w, dc, 5);                     /* fixed distance codes: 5 bits */
+    z_put(w, dist - z_dist_base[dc], z_dist_extra[dc]);
+}
+
+static uint32_t z_hash(const uint8_t *u, uint64_t p)
+{
+    return (uint32_t)(rd32(u + p) * 2654435761u) >> (32 - Z_HASH_BITS);
 }
 
 /* Encode one unit into out (room for 4096 bytes); returns the encoded size. */
 uint64_t orc_z_encode(const uint8_t *u, uint8_t *out)
 {
-    uint64_t n = 0;
-    for (uint64_t j = 0; j < ORC_UNIT_WORDS; ++j) n += (uint64_t)z_literal(u, j);
-    if (n == 0) return 0;
-    if (128 + 4 * n >= ORC_UNIT) {
+    int zero = 1;
+    for (uint64_t i = 0; i < ORC_UNIT; ++i) zero &= u[i] == 0;
+    if (zero) return 0;
+    /* cand(p) for every p: the hash table sees every position in order */
+    int32_t head[1 << Z_HASH_BITS];
+    int32_t cand[ORC_UNIT];
+    for (uint32_t h = 0; h < (1u << Z_HASH_BITS); ++h) head[h] = -1;
+    for (uint64_t p = 0; p < ORC_UNIT; ++p) {
+        cand[p] = -1;
+        if (p + 4 <= ORC_UNIT) {
+            const uint32_t h = z_hash(u, p);
+            cand[p] = head[h];
+            head[h] = (int32_t)p;
+        }
+    }
+    memset(out, 0, ORC_UNIT);
+    z_bits w = {out, ORC_UNIT, 0};
+    z_put(&w, 1, 1); /* BFINAL */
+    z_put(&w, 1, 2); /* BTYPE = 01: fixed Huffman codes */
+    uint64_t p = 0;
+    while (p < ORC_UNIT) {
+        uint32_t len = 0;
+        if (cand[p] >= 0) {
+            const uint64_t q = (uint64_t)cand[p];
+            const uint64_t lim = ORC_UNIT - p < Z_MAX_MATCH ? ORC_UNIT - p : Z_MAX_MATCH;
+            while (len < lim && u[q + len] == u[p + len]) ++len;
+        }
+        if (len >= Z_MIN_MATCH) {
+            z_put_match(&w, len, (uint32_t)(p - (uint64_t)cand[p]));
+            p += len;
+        } else {
+            z_put_litlen(&w, u[p]);
+            p += 1;
+        }
+    }
+    z_put_litlen(&w, 256); /* end of block */
+    const uint64_t nbytes = (w.nbits + 7) / 8;
+    if (nbytes >= ORC_UNIT) {
         memcpy(out, u, ORC_UNIT);
         return ORC_UNIT;
     }
-    memset(out, 0, 128);
-    uint64_t pos = 128;
-    for (uint64_t j = 0; j < ORC_UNIT_WORDS; ++j) {
-        if (!z_literal(u, j)) continue;
-        out[j / 8] |= (uint8_t)(1u << (j % 8));
-        wr32(out + pos, unit_word(u, j));
-        pos += 4;
-    }
-    return pos;
+    return nbytes;
 }
 
-/* A valid encoded size: 0, 4096, or 128 + 4n with 1 <= n < 992. */
-static int z_size_ok(uint64_t cs)
+/* A valid encoded size: anything up to 4096 (what the bytes hold is checked
+ * by the decoder). */
+static int z_size_ok(uint64_t cs) { return cs <= ORC_UNIT; }
+
+/* Bit reader over the cs bytes of a stream. */
+typedef struct {
+    const uint8_t *in;
+    uint64_t nbits, pos;
+    int overrun;
+} z_in;
+
+static uint32_t z_get(z_in *r, uint32_t n) /* n bits, LSB first */
 {
-    return cs == 0 || cs == ORC_UNIT || (cs >= 132 && cs < ORC_UNIT && cs % 4 == 0);
+    uint32_t v = 0;
+    for (uint32_t i = 0; i < n; ++i, ++r->pos) {
+        if (r->pos >= r->nbits) {
+            r->overrun = 1;
+            continue;
+        }
+        v |= (uint32_t)((r->in[r->pos / 8] >> (r->pos % 8)) & 1u) << i;
+    }
+    return v;
 }
 
-/* Decode one unit of encoded size cs from in; 0 if the encoding is
- * inconsistent (bitmap population != literal count). */
+/* Next fixed literal/length symbol, or -1 (RFC 1951 sec. 3.2.6: codes 286,
+ * 287 do not occur in a valid stream). */
+static int z_get_litlen(z_in *r)
+{
+    uint32_t c = 0;
+    for (uint32_t n = 1; n <= 9; ++n) {
+        c = (c << 1) | z_get(r, 1);
+        if (n == 7 && c <= 0x17) return (int)(256 + c);
+        if (n == 8 && c >= 0x30 && c <= 0xBF) return (int)(c - 0x30);
+        if (n == 8 && c >= 0xC0 && c <= 0xC5) return (int)(280 + c - 0xC0);
+        if (n == 8 && c >= 0xC6 && c <= 0xC7) return -1;
+        if (n == 9 && c >= 0x190) return (int)(144 + c - 0x190);
+    }
+    return -1;
+}
+
+/* Decode one unit of encoded size cs from in; 0 if the bytes are not a valid
+ * encoding: a size-0 unit is zero, a size-4096 unit is raw; otherwise the
+ * bytes must be exactly one final fixed-Huffman block that produces exactly
+ * 4096 bytes, every distance within the bytes already produced, ending in
+ * the last byte with zero padding bits. */
 int orc_z_decode(const uint8_t *in, uint64_t cs, uint8_t *u)
 {
     if (!z_size_ok(cs)) return 0;
@@ -533,19 +660,33 @@ int orc_z_decode(const uint8_t *in, uint64_t cs, uint8_t *u)
     }
     memset(u, 0, ORC_UNIT);
     if (cs == 0) return 1;
-    uint64_t pos = 128;
-    for (uint64_t j = 0; j < ORC_UNIT_WORDS; ++j) {
-        uint32_t w;
-        if (in[j / 8] & (1u << (j % 8))) {
-            if (pos + 4 > cs) return 0;
-            w = rd32(in + pos);
-            pos += 4;
-        } else {
-            w = j < 2 ? 0u : unit_word(u, j - 2);
+    z_in r = {in, 8 * cs, 0, 0};
+    if (z_get(&r, 1) != 1 || z_get(&r, 2) != 1) return 0; /* BFINAL = 1, BTYPE = 01 */
+    uint64_t o = 0;
+    for (;;) {
+        const int s = z_get_litlen(&r);
+        if (s < 0 || r.overrun) return 0;
+        if (s == 256) break;
+        if (s < 256) {
+            if (o >= ORC_UNIT) return 0;
+            u[o++] = (uint8_t)s;
+            continue;
         }
-        wr32(u + 4 * j, w);
+        const uint32_t lc = (uint32_t)s - 257;
+        const uint32_t len = z_len_base[lc] + z_get(&r, z_len_extra[lc]);
+        uint32_t dc = 0;
+        for (int i = 0; i < 5; ++i) dc = (dc << 1) | z_get(&r, 1);
+        if (dc >= 30 || r.overrun) return 0;
+        const uint32_t dist = z_dist_base[dc] + z_get(&r, z_dist_extra[dc]);
+        if (r.overrun || dist > o || o + len > ORC_UNIT) return 0;
+        for (uint32_t i = 0; i < len; ++i, ++o) u[o] = u[o - dist];
     }
-    return pos == cs;
+    if (o != ORC_UNIT) return 0;
+    /* the stream ends in its last byte and the padding bits are zero */
+    if ((r.pos + 7) / 8 != cs) return 0;
+    while (r.pos < r.nbits)
+        if (z_get(&r, 1)) return 0;
+    return 1;
 }
 
 /* Checkpoint drain as an incremental gather (sec. 3.4, PAPER.md:547-551;
@@ -578,7 +719,7 @@ int orc_checkpoint_gather(orc_ctx *c, uint32_t flags, uint8_t *img, uint64_t cap
     const int has_hashes = any_hash_region(c);
     const int z = (flags & ORC_COMPRESS) != 0;
     const uint64_t poff = payload_offset_for(R);
-    /* Compressed images (readings Z1-Z2): the slots are laid out as usual,
+    /* Compressed images (readings Z2-Z3): the slots are laid out as usual,
      * then every 4 KiB unit is encoded; the payload is the encoded units back
      * to back, zero-padded to a multiple of 4096; the tail gains the u16
      * encoded size of every unit. */
@@ -736,7 +877,7 @@ static int validate_image(orc_ctx *c, const uint8_t *img, uint64_t len, uint32_t
     }
     if (sum != K || (!z && pay != payload) || any_hash != has_hashes) return ORC_E_CORRUPT;
     /* Compressed: one valid u16 size per 4 KiB unit, summing to the payload
-     * length before its zero padding (readings Z1-Z2). */
+     * length before its zero padding (readings Z2-Z3). */
     const uint8_t *zt = ids + tail_bytes_for(K, has_hashes);
     const uint64_t U = pay / ORC_UNIT;
     if (z) {

@@ -111,7 +111,7 @@ def crc32(data) -> int:
 
 
 def z_encode(unit) -> bytes:
-    """The oracle's unit codec (readings Z1-Z2): encode 4096 bytes."""
+    """The oracle's unit codec (reading Z3: greedy LZ77 + fixed-Huffman DEFLATE): encode 4096 bytes."""
     a = np.ascontiguousarray(np.frombuffer(bytes(unit), dtype=np.uint8))
     assert a.nbytes == 4096
     out = np.zeros(4096, dtype=np.uint8)

@@ -29,19 +29,117 @@ def slot_bytes(cur: np.ndarray, page_size: int, i: int) -> bytes:
     return seg + b"\0" * (page_size - len(seg))
 
 
+# --- unit codec, reading Z3, restated in plain Python ----------
+# RFC 1951 sec. 3.2.5 length / distance code tables, derived here from their
+# ranges instead of copied: lengths 3..258 -> codes 257..285; distances
+# 1..32768 -> codes 0..29.
+def _len_codes():
+    out, base, code = {}, 3, 257
+    for extra, n in [(0, 8), (1, 4), (2, 4), (3, 4), (4, 4), (5, 4)]:
+        for _ in range(n):
+            for L in range(base, base + (1 << extra)):
+                out[L] = (code, extra, L - base)
+            base += 1 << extra
+            code += 1
+    out[258] = (285, 0, 0)          # 258 has its own code (RFC 1951: 284 covers 227-257)
+    return out
+
+
+def _dist_codes():
+    out, base = {}, 1
+    for code in range(30):
+        extra = max(0, code // 2 - 1)
+        for d in range(base, base + (1 << extra)):
+            out[d] = (code, extra, d - base)
+        base += 1 << extra
+    return out
+
+
+_LEN, _DIST = _len_codes(), _dist_codes()
+
+
+def _litlen_code(s):
+    """(code, nbits) of the fixed literal/length code (RFC 1951 sec. 3.2.6)."""
+    if s <= 143:
+        return 0b00110000 + s, 8
+    if s <= 255:
+        return 0b110010000 + s - 144, 9
+    if s <= 279:
+        return s - 256, 7
+    return 0b11000000 + s - 280, 8
+
+
+def z_tokens(unit: bytes):
+    """The greedy parse of reading Z3: list of ("lit", byte) / ("match", len, dist)."""
+    u = bytes(unit)
+    head = {}
+    cand = []
+    for p in range(4096):
+        if p + 4 <= 4096:
+            h = ((int.from_bytes(u[p:p + 4], "little") * 2654435761) & 0xFFFFFFFF) >> 20
+            cand.append(head.get(h))
+            head[h] = p
+        else:
+            cand.append(None)
+    toks, p = [], 0
+    while p < 4096:
+        L = 0
+        q = cand[p]
+        if q is not None:
+            while L < min(258, 4096 - p) and u[q + L] == u[p + L]:
+                L += 1
+        if L >= 4:
+            toks.append(("match", L, p - q))
+            p += L
+        else:
+            toks.append(("lit", u[p]))
+            p += 1
+    return toks
+
+
 def z_encode_unit(unit: bytes) -> bytes:
-    """DESIGN.md readings Z1-Z2, restated with numpy: 1024 LE u32 words, word j
-    predicted by word j-2 (0 for j < 2); literals = mispredicted words;
-    0 literals -> b""; 128 + 4n < 4096 -> LSB-first bitmap + literals; else raw."""
-    w = np.frombuffer(unit, dtype="<u4")
-    pred = np.concatenate([np.zeros(2, dtype="<u4"), w[:-2]])
-    lit = w != pred
-    n = int(lit.sum())
-    if n == 0:
+    """Reading Z3: b"" for a zero unit; else the fixed-Huffman DEFLATE stream
+    of z_tokens() if shorter than 4096 bytes; else the raw unit."""
+    u = bytes(unit)
+    if not any(u):
         return b""
-    if 128 + 4 * n >= 4096:
-        return bytes(unit)
-    return np.packbits(lit, bitorder="little").tobytes() + w[lit].astype("<u4").tobytes()
+    bits = [1, 1, 0]                          # BFINAL = 1, BTYPE = 01 (LSB first)
+
+    def code(c, n):                           # Huffman codes: most significant bit first
+        bits.extend((c >> (n - 1 - i)) & 1 for i in range(n))
+
+    def extra(v, n):                          # extra bits: least significant bit first
+        bits.extend((v >> i) & 1 for i in range(n))
+
+    for t in z_tokens(u):
+        if t[0] == "lit":
+            code(*_litlen_code(t[1]))
+        else:
+            lc, le, lv = _LEN[t[1]]
+            code(*_litlen_code(lc))
+            extra(lv, le)
+            dc, de, dv = _DIST[t[2]]
+            code(dc, 5)
+            extra(dv, de)
+    code(*_litlen_code(256))
+    nbytes = (len(bits) + 7) // 8
+    if nbytes >= 4096:
+        return u
+    bits += [0] * (8 * nbytes - len(bits))
+    return bytes(sum(b << i for i, b in enumerate(bits[8 * k:8 * k + 8])) for k in range(nbytes))
+
+
+def z_decode_unit(enc: bytes) -> bytes:
+    """Inverse for tests: zlib's own inflater (raw DEFLATE, wbits = -15); the
+    stream must end exactly at its last byte."""
+    if len(enc) == 0:
+        return bytes(4096)
+    if len(enc) == 4096:
+        return bytes(enc)
+    d = zlib.decompressobj(-15)
+    out = d.decompress(bytes(enc))
+    assert d.eof and d.unused_data == b"" and len(out) == 4096
+    return out
 
 
 def build_image(regions, listed, full=False, compress=False) -> bytes:
