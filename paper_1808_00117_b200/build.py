@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcrum.so")
-SOURCES = ["runtime.cu", "kernels_detect.cu", "kernels_image.cu", "synth.cu"]
+SOURCES = ["runtime.cu", "kernels_detect.cu", "kernels_image.cu", "kernels_zip.cu", "synth.cu"]
 HEADERS = ["crum_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -228,21 +228,47 @@ void launch_restore_validate(const Launch &L, const DevRegion *tregs, uint32_t R
                              const uint32_t *ids, const uint64_t *hashes, uint64_t K, DevStats *st);
 void launch_scatter(const Launch &L, const ScatterArgs &a);
 
-// Compressed images (readings Z1-Z2): encoded sizes, their scan
-// (kZScanBlock units per local block), encode + commit, decode.
+// Compressed images (kernels_zip.cu; readings Z2-Z3): per 4 KiB
+// payload unit a greedy LZ77 parse coded as one fixed-Huffman DEFLATE block.
+// Offsets of the encoded units: zblk[u / kZScanBlock] + zloc[u] (bytes from
+// the payload start).  A gather encodes chunk by chunk (kZChunkUnits units,
+// a multiple of kZScanBlock): encode -> chunk scan -> pack.
 constexpr uint32_t kZScanBlock = 2048;
-void launch_zsize(const Launch &L, const GatherArgs &a, uint16_t *zsz, uint64_t max_units);
+constexpr uint32_t kZChunkUnits = 16384;   // 64 MiB of units per chunk
+// Encode units [u_lo, u_hi) of the gather (a: unit -> page map) into
+// stage + (u - u_lo) * 4096 (raw layout), sizes into zsz[u].
+void launch_zenc(const Launch &L, const GatherArgs &a, uint64_t u_lo, uint64_t u_hi, uint8_t *stage, uint16_t *zsz);
+// Offsets of units [u_lo, u_hi) (u_lo % kZScanBlock == 0): zloc / zblk from
+// the running total *zrun, which is advanced; *zrun_host (mapped, nullable)
+// receives the new running total.
+void launch_zscan_chunk(const Launch &L, const uint16_t *zsz, uint64_t u_lo, uint64_t u_hi, const DevStats *st,
+                        const RangeTotals *rb, uint32_t *zloc, uint64_t *zblk, uint64_t *zrun,
+                        uint64_t *zrun_host);
+// Move the encodings of units [u_lo, u_hi) from stage to their places:
+// dst + off(u) - (rel ? off(u_lo) : 0); with limit != 0 a unit is written
+// only if poff + off(u) + size <= limit (device image capacity).  rb: the
+// gather's totals (rb[1].units bounds the units).
+void launch_zpack(const Launch &L, const uint8_t *stage, const uint16_t *zsz, const uint32_t *zloc,
+                  const uint64_t *zblk, uint64_t u_lo, uint64_t u_hi, const DevStats *st, const RangeTotals *rb,
+                  uint8_t *dst, int rel, uint64_t limit);
+// After the last chunk: the compressed image's sizes and capacity status
+// (total encoded length *zrun); zero the payload padding of img (nullable).
+void launch_zfinal(const Launch &L, DevStats *st, const uint64_t *zrun, uint8_t *img, uint64_t capacity);
+// Restore: validate the size table (every size <= 4096, the sizes summing to
+// the header's payload length before padding) and compute zloc / zblk.
 void launch_zscan(const Launch &L, const uint16_t *zsz, DevStats *st, uint32_t *zloc, uint64_t *zblk,
-                  uint64_t max_units, int gather, uint8_t *img, uint64_t capacity);
-void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, const uint64_t *zblk, uint8_t *dst,
-                   int add_poff, uint64_t u_lo, uint64_t u_hi, uint64_t off0);
+                  uint64_t max_units);
+// Decode units [u_lo, u_lo + units) from src into dst (unit u at
+// dst + (u - u_lo) * 4096; dst == nullptr: validate only).  rebase: src holds
+// the payload from byte (off(u_lo) & ~3) on (k_zfetch), else from byte 0.
+// An invalid unit sets st->status = CORRUPT.
 void launch_zdecode(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
                     const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t units, uint64_t u_lo = 0,
                     int rebase = 0);
+// Copy the encoded bytes of units [u_lo, u_hi) -- payload bytes
+// [off(u_lo) & ~3, round_up(end, 4)) -- from src to dst (wide reads).
 void launch_zfetch(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
                    const uint64_t *zblk, uint64_t u_lo, uint64_t u_hi, uint8_t *dst);
-void launch_zcheck(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
-                   const uint64_t *zblk, DevStats *st, uint64_t units);
 void launch_mark_pages(const Launch &L, uint8_t *force, uint64_t n_pages, const uint32_t *pages, uint64_t n);
 void launch_export_flags(const Launch &L, uint8_t *flags, const uint8_t *force, uint64_t N, uint8_t tag,
                          uint8_t *out);
@@ -267,5 +293,66 @@ __device__ __forceinline__ uint32_t upper_region(const uint64_t *prefix, uint32_
     }
     return lo;
 }
+
+// ---- block / warp helpers shared by the kernel files ----
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide exclusive scan of one u64 per thread; returns the exclusive
+// prefix, *total = block sum.  blockDim.x must be a multiple of 32, <= 1024.
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t *total) {
+    __shared__ uint64_t warp_off[32];
+    __shared__ uint64_t block_tot;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (uint32_t)o) inc += t;
+    }
+    __syncthreads();  // previous call's readers are done with warp_off / block_tot
+    if (lane == 31) warp_off[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const uint64_t w = lane < nw ? warp_off[lane] : 0;
+        uint64_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint64_t t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= (uint32_t)o) wi += t;
+        }
+        if (lane < nw) warp_off[lane] = wi - w;  // exclusive warp offsets
+        if (lane == 31) block_tot = wi;           // lanes >= nw add 0: lane 31 holds the sum
+    }
+    __syncthreads();
+    if (total) *total = block_tot;
+    return warp_off[wid] + inc - v;
+}
+
+__device__ __forceinline__ uint64_t block_sum(uint64_t v) {
+    uint64_t t;
+    block_excl_scan(v, &t);
+    return t;
+}
+
+// Largest r with regs[r].page_base <= g.
+__device__ __forceinline__ uint32_t region_of_page(const DevRegion *regs, uint32_t R, uint64_t g) {
+    uint32_t lo = 0, hi = R;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (regs[mid].page_base <= g) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint64_t page_len(const DevRegion &g, uint64_t i) {
+    const uint64_t off = i << g.log2p;
+    return min((uint64_t)1 << g.log2p, (uint64_t)(g.bytes - off));
+}
+
 
 }  // namespace crum

@@ -41,65 +41,6 @@ __device__ __forceinline__ void st256(void *p, const uint32_t (&r)[8]) {
                  : "memory");
 }
 
-template <typename T>
-__device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Block-wide exclusive scan of one u64 per thread; returns the exclusive
-// prefix, *total = block sum.  blockDim.x must be a multiple of 32, <= 1024.
-__device__ uint64_t block_excl_scan(uint64_t v, uint64_t *total) {
-    __shared__ uint64_t warp_off[32];
-    __shared__ uint64_t block_tot;
-    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    uint64_t inc = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= (uint32_t)o) inc += t;
-    }
-    __syncthreads();  // previous call's readers are done with warp_off / block_tot
-    if (lane == 31) warp_off[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-        const uint64_t w = lane < nw ? warp_off[lane] : 0;
-        uint64_t wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint64_t t = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= (uint32_t)o) wi += t;
-        }
-        if (lane < nw) warp_off[lane] = wi - w;  // exclusive warp offsets
-        if (lane == 31) block_tot = wi;           // lanes >= nw add 0: lane 31 holds the sum
-    }
-    __syncthreads();
-    if (total) *total = block_tot;
-    return warp_off[wid] + inc - v;
-}
-
-__device__ __forceinline__ uint64_t block_sum(uint64_t v) {
-    uint64_t t;
-    block_excl_scan(v, &t);
-    return t;
-}
-
-// Largest r with regs[r].page_base <= g.
-__device__ __forceinline__ uint32_t region_of_page(const DevRegion *regs, uint32_t R, uint64_t g) {
-    uint32_t lo = 0, hi = R;
-    while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (regs[mid].page_base <= g) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
-__device__ __forceinline__ uint64_t page_len(const DevRegion &g, uint64_t i) {
-    const uint64_t off = i << g.log2p;
-    return min((uint64_t)1 << g.log2p, (uint64_t)(g.bytes - off));
-}
-
 // ---------------------------------------------------------------------------
 // A2 compaction
 // ---------------------------------------------------------------------------
@@ -1207,453 +1148,5 @@ void launch_fused_compare(const Launch &L, const FusedArgs &a, int blocks) {
     ++*L.counter;
 }
 
-
-// ===========================================================================
-// Compressed images (readings Z1-Z2).
-// A 4 KiB unit is 1024 LE u32 words; word j is predicted by word j-2 (0 for
-// j < 2).  Encoding: no mispredicted word -> 0 bytes; 128 + 4n < 4096 ->
-// 128-byte bitmap of the n mispredicted words + those words; else raw.
-// One warp per unit: lane l holds words 32i + l (i = 0..31), so the
-// prediction is a shfl_up by 2 (lanes 0/1 take lanes 30/31 of the previous
-// row) and the bitmap rows are 32 ballots.
-// ===========================================================================
-
-__device__ __forceinline__ uint32_t lanemask_lt() {
-    uint32_t m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
-
-// Row i (0..7) of a unit, as this lane sees it: the 16 bytes at 512 i + 16 lane
-// (words 128 i + 4 lane + t, t = 0..3); bytes at or beyond len read as zero.
-__device__ __forceinline__ uint4 z_row(const uint8_t *p, uint64_t len, uint32_t i, uint32_t lane) {
-    const uint64_t o = 512ull * i + 16ull * lane;
-    if (o + 16 <= len) return __ldg(reinterpret_cast<const uint4 *>(p + o));
-    uint32_t w[4] = {0, 0, 0, 0};
-    for (uint32_t k = 0; k < 16; ++k)
-        if (o + k < len) w[k >> 2] |= (uint32_t)p[o + k] << (8 * (k & 3));
-    return make_uint4(w[0], w[1], w[2], w[3]);
-}
-
-// Mispredicted-word nibble of this lane for row v (bit t <-> word 4 lane + t);
-// (cz, cw) carry words 128 i - 2, 128 i - 1 (lane 31's z, w of the previous row).
-__device__ __forceinline__ uint32_t z_nibble(const uint4 &v, uint32_t lane, uint32_t &cz, uint32_t &cw) {
-    uint32_t pz = __shfl_up_sync(0xffffffffu, v.z, 1), pw = __shfl_up_sync(0xffffffffu, v.w, 1);
-    if (lane == 0) {
-        pz = cz;
-        pw = cw;
-    }
-    cz = __shfl_sync(0xffffffffu, v.z, 31);
-    cw = __shfl_sync(0xffffffffu, v.w, 31);
-    return (uint32_t)(v.x != pz) | ((uint32_t)(v.y != pw) << 1) | ((uint32_t)(v.z != v.x) << 2) |
-           ((uint32_t)(v.w != v.y) << 3);
-}
-
-__device__ __forceinline__ uint32_t z_size_of(uint32_t n) {
-    return n == 0 ? 0u : (128u + 4u * n < kSegBytes ? 128u + 4u * n : (uint32_t)kSegBytes);
-}
-
-// Unit u of the gather -> (region, page, byte offset, logical length), walked
-// in tasks of kUnitsPerTask consecutive units: one binary search per task,
-// then the slot / region advance incrementally (as k_gather).
-struct ZUnit {
-    DevRegion g;
-    uint64_t gid, i, off, len, seg;
-};
-struct ZCursor {
-    const GatherArgs &a;
-    uint64_t k_hi, k, kbase, gid;
-    uint32_t r;
-    DevRegion g;
-    __device__ ZCursor(const GatherArgs &a_, uint64_t k_lo, uint64_t k_hi_, uint64_t u0) : a(a_), k_hi(k_hi_) {
-        k = a.u2s[u0];
-        gid = a.gids[k];
-        r = region_of_page(a.regs, a.R, gid);
-        g = a.regs[r];
-        kbase = a.sunit[k];
-    }
-    __device__ ZUnit at(uint64_t u) {  // u >= the previous call's u
-        const uint64_t nxt = (k + 1 < k_hi) ? a.sunit[k + 1] : ~0ull;
-        if (u >= nxt) {
-            k = a.u2s[u];
-            kbase = a.sunit[k];
-            gid = a.gids[k];
-            if (r + 1 < a.R && gid >= a.regs[r + 1].page_base) {
-                r = region_of_page(a.regs, a.R, gid);
-                g = a.regs[r];
-            }
-        }
-        ZUnit z;
-        z.g = g;
-        z.gid = gid;
-        z.seg = u - kbase;
-        z.i = gid - g.page_base;
-        z.off = (z.i << g.log2p) + (z.seg << kSegLog2);
-        z.len = g.bytes > z.off ? min((uint64_t)kSegBytes, g.bytes - z.off) : 0;
-        return z;
-    }
-};
-
-// Pass 1: encoded size of every unit of the gather (8 x 16 B per lane).
-__global__ void __launch_bounds__(256, 2) k_zsize(GatherArgs a, uint16_t *zsz) {
-    const DevStats *st = a.st;
-    if (st->status != kStOk) return;
-    const uint64_t k_lo = a.rb[0].k, k_hi = a.rb[1].k, U = a.rb[1].units;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t upt = max((uint64_t)1, min((uint64_t)kUnitsPerTask, (U + nwarps - 1) / nwarps));
-    const uint64_t ntask = (U + upt - 1) / upt;
-    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntask; t += nwarps) {
-        const uint64_t u0 = t * upt, u1 = min(u0 + upt, U);
-        ZCursor cur(a, k_lo, k_hi, u0);
-        for (uint64_t u = u0; u < u1; ++u) {
-            const ZUnit z = cur.at(u);
-            const uint8_t *p = z.g.base + z.off;
-            uint4 v[8];
-#pragma unroll
-            for (uint32_t i = 0; i < 8; ++i) v[i] = z_row(p, z.len, i, lane);
-            uint32_t cz = 0, cw = 0, n = 0;
-#pragma unroll
-            for (uint32_t i = 0; i < 8; ++i) n += __popc(z_nibble(v[i], lane, cz, cw));
-            n = __reduce_add_sync(0xffffffffu, n);
-            if (lane == 0) zsz[u] = (uint16_t)z_size_of(n);
-        }
-    }
-}
-
-// Local exclusive prefix of the sizes inside blocks of kZScanBlock units.
-// validate: a size other than 0, 4096 or 128 + 4n (1 <= n < 992) is CORRUPT.
-__global__ void __launch_bounds__(256) k_zscan_local(const uint16_t *zsz, DevStats *st, uint32_t *zloc,
-                                                    uint64_t *zblk, int validate) {
-    const uint64_t U = st->total_units;
-    const uint64_t base = (uint64_t)blockIdx.x * kZScanBlock;
-    if (base >= U) return;
-    constexpr uint32_t per = kZScanBlock / 256;
-    uint32_t v[per];
-    uint64_t sum = 0;
-    bool bad = false;
-#pragma unroll
-    for (uint32_t j = 0; j < per; ++j) {
-        const uint64_t u = base + threadIdx.x * per + j;
-        v[j] = u < U ? zsz[u] : 0u;
-        bad |= !(v[j] == 0 || v[j] == kSegBytes || (v[j] >= 132 && v[j] < kSegBytes && (v[j] & 3) == 0));
-        sum += v[j];
-    }
-    uint64_t tot;
-    uint64_t ex = block_excl_scan(sum, &tot);
-#pragma unroll
-    for (uint32_t j = 0; j < per; ++j) {
-        const uint64_t u = base + threadIdx.x * per + j;
-        if (u < U) zloc[u] = (uint32_t)ex;
-        ex += v[j];
-    }
-    if (threadIdx.x == 0) zblk[blockIdx.x] = tot;
-    if (validate && bad) st->status = kStCorrupt;
-}
-
-// Exclusive scan of the block totals (one block).  Gather: set the
-// compressed image's sizes, check capacity, zero the payload padding of img.
-// Restore: the sizes must sum to the header's payload length before padding,
-// and the size table's padding must be zero.
-__global__ void __launch_bounds__(1024) k_zscan_top(uint64_t *zblk, DevStats *st, int gather, uint8_t *img,
-                                                   uint64_t capacity, const uint16_t *zsz) {
-    const uint64_t U = st->total_units;
-    const uint64_t nblk = (U + kZScanBlock - 1) / kZScanBlock;
-    uint64_t carry = 0;
-    for (uint64_t b0 = 0; b0 < nblk; b0 += blockDim.x) {
-        const uint64_t b = b0 + threadIdx.x;
-        const uint64_t v = b < nblk ? zblk[b] : 0;
-        uint64_t tot;
-        const uint64_t ex = block_excl_scan(v, &tot);
-        if (b < nblk) zblk[b] = carry + ex;
-        carry += tot;
-    }
-    const uint64_t Z = carry;
-    const uint64_t zpay = round_up(Z, kSegBytes);
-    __syncthreads();
-    if (threadIdx.x == 0) zblk[nblk] = Z;  // the encoded length (chunk end of a host gather)
-    if (gather) {
-        if (st->status != kStOk) return;
-        const uint64_t K = st->K;
-        const uint64_t ids_off = st->poff + zpay;
-        const uint64_t image = ids_off + round_up(4 * K, 8) + ((st->img_flags & 2u) ? 8 * K : 0) + round_up(2 * U, 8);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            st->payload_bytes = zpay;
-            st->ids_off = ids_off;
-            st->image_bytes = image;
-            st->img_flags |= 4u;
-            if (image > capacity) st->status = kStCapacity;
-        }
-        if (img && image <= capacity)
-            for (uint64_t b = st->poff + Z + threadIdx.x; b < st->poff + zpay; b += blockDim.x) img[b] = 0;
-    } else if (threadIdx.x == 0) {
-        bool bad = zpay != st->payload_bytes;
-        for (uint64_t q = U; q < round_up(U, 4); ++q) bad |= zsz[q] != 0;
-        if (bad) st->status = kStCorrupt;
-    }
-}
-
-// Pass 2: encode units [u_lo, u_hi) and commit them (as k_gather).  Unit u
-// goes to dst + (add_poff ? poff : 0) + off(u) - off0, off(u) its offset in
-// the compressed payload (dst == nullptr: commit only).
-__global__ void __launch_bounds__(256, 2) k_zwrite(GatherArgs a, const uint32_t *zloc, const uint64_t *zblk,
-                                               uint8_t *dst, int add_poff, uint64_t u_lo, uint64_t u_hi,
-                                               uint64_t off0) {
-    const DevStats *st = a.st;
-    if (st->status != kStOk) return;
-    const uint64_t k_lo = a.rb[0].k, k_hi = a.rb[1].k, U = min(a.rb[1].units, u_hi);
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    uint8_t *payload = dst ? dst + (add_poff ? st->poff : 0) - off0 : nullptr;
-    const uint64_t nu = U > u_lo ? U - u_lo : 0;
-    const uint64_t upt = max((uint64_t)1, min((uint64_t)kUnitsPerTask, (nu + nwarps - 1) / nwarps));
-    const uint64_t ntask = (nu + upt - 1) / upt;
-    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntask; t += nwarps) {
-      const uint64_t u0 = u_lo + t * upt, u1 = min(u0 + upt, U);
-      ZCursor cur(a, k_lo, k_hi, u0);
-      for (uint64_t u = u0; u < u1; ++u) {
-        const ZUnit z = cur.at(u);
-        if (payload) {
-            const uint8_t *p = z.g.base + z.off;
-            uint4 v[8];
-#pragma unroll
-            for (uint32_t i = 0; i < 8; ++i) v[i] = z_row(p, z.len, i, lane);
-            uint32_t nib[8], cz = 0, cw = 0, n = 0;
-#pragma unroll
-            for (uint32_t i = 0; i < 8; ++i) {
-                nib[i] = z_nibble(v[i], lane, cz, cw);
-                n += __popc(nib[i]);
-            }
-            n = __reduce_add_sync(0xffffffffu, n);
-            const uint32_t cs = z_size_of(n);
-            uint32_t *out = reinterpret_cast<uint32_t *>(payload + zblk[u / kZScanBlock] + zloc[u]);
-            if (cs == kSegBytes) {
-#pragma unroll
-                for (uint32_t i = 0; i < 8; ++i) {
-                    uint32_t *o = out + 128 * i + 4 * lane;
-                    o[0] = v[i].x;
-                    o[1] = v[i].y;
-                    o[2] = v[i].z;
-                    o[3] = v[i].w;
-                }
-            } else if (cs) {
-                uint32_t base = 32;  // literals follow the 32 bitmap words
-#pragma unroll
-                for (uint32_t i = 0; i < 8; ++i) {
-                    // bitmap words 4i .. 4i+3: word 4i + m holds lanes 8m .. 8m+7, 4 bits each
-                    uint32_t x = nib[i] << (4 * (lane & 7));
-                    x |= __shfl_xor_sync(0xffffffffu, x, 1);
-                    x |= __shfl_xor_sync(0xffffffffu, x, 2);
-                    x |= __shfl_xor_sync(0xffffffffu, x, 4);
-                    if ((lane & 7) == 0) out[4 * i + (lane >> 3)] = x;
-                    // literal ranks: warp-exclusive prefix of the nibble populations
-                    const uint32_t c = __popc(nib[i]);
-                    uint32_t inc = c;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-                        if (lane >= (uint32_t)d) inc += y;
-                    }
-                    uint32_t pos = base + inc - c;
-                    if (nib[i] & 1u) out[pos++] = v[i].x;
-                    if (nib[i] & 2u) out[pos++] = v[i].y;
-                    if (nib[i] & 4u) out[pos++] = v[i].z;
-                    if (nib[i] & 8u) out[pos++] = v[i].w;
-                    base += __shfl_sync(0xffffffffu, inc, 31);
-                }
-            }
-        }
-        uint8_t *dst_mir = (z.g.mode == kModeCompare) ? z.g.mirror + z.off : nullptr;
-        if (dst_mir) copy_unit(z.g.base + z.off, z.len, z.g.aligned32 != 0, nullptr, dst_mir, lane);
-        if (z.seg == 0 && lane == 0) {
-            if (z.g.mode == kModeHash) z.g.table[z.i] = a.newhash[z.gid];
-            a.force[z.gid] = 0;
-        }
-      }
-    }
-}
-
-// Restore: decode every unit of the compressed payload at src into dst
-// (unit u at dst + 4096u).  A bitmap whose population disagrees with the
-// unit's size is CORRUPT.
-__global__ void __launch_bounds__(256) k_zdecode(const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
-                                                const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t u_lo,
-                                                uint64_t u_hi, int rebase) {
-    if (st->status != kStOk) return;
-    const uint64_t U = min(u_hi, st->total_units);
-    // rebase: src holds the payload from unit u_lo's encoding on (k_zfetch)
-    const uint64_t off0 = rebase ? zblk[u_lo / kZScanBlock] + zloc[u_lo] : 0;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t u = u_lo + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < U; u += nwarps) {
-        const uint32_t cs = zsz[u];
-        const uint32_t *in = reinterpret_cast<const uint32_t *>(src + (zblk[u / kZScanBlock] + zloc[u] - off0));
-        uint32_t *out = reinterpret_cast<uint32_t *>(dst + ((u - u_lo) << kSegLog2));
-        if (cs == kSegBytes) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) out[32 * i + lane] = in[32 * i + lane];
-            continue;
-        }
-        if (cs == 0) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) out[32 * i + lane] = 0u;
-            continue;
-        }
-        const uint32_t mine = in[lane];  // bitmap word `lane`
-        const uint32_t n = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mine));
-        if (128u + 4u * n != cs) {
-            if (lane == 0) st->status = kStCorrupt;
-            continue;
-        }
-        uint32_t base = 32, ce = 0, co = 0;  // literal cursor; carries of the even / odd word classes
-#pragma unroll
-        for (uint32_t i = 0; i < 8; ++i) {
-            const uint32_t nib = (__shfl_sync(0xffffffffu, mine, 4 * i + (lane >> 3)) >> (4 * (lane & 7))) & 15u;
-            const uint32_t c = __popc(nib);
-            uint32_t inc = c;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-                if (lane >= (uint32_t)d) inc += y;
-            }
-            uint32_t pos = base + inc - c;
-            uint32_t lx = 0, ly = 0, lz = 0, lw = 0;
-            if (nib & 1u) lx = in[pos++];
-            if (nib & 2u) ly = in[pos++];
-            if (nib & 4u) lz = in[pos++];
-            if (nib & 8u) lw = in[pos++];
-            base += __shfl_sync(0xffffffffu, inc, 31);
-            // even class: ... x_l, z_l, x_{l+1} ...; odd class: ... y_l, w_l ...
-            // last literal of this lane's pair, then an inclusive segmented scan over lanes
-            bool fe = (nib & 5u) != 0, fo = (nib & 10u) != 0;
-            uint32_t ve = (nib & 4u) ? lz : lx, vo = (nib & 8u) ? lw : ly;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t ve2 = __shfl_up_sync(0xffffffffu, ve, d);
-                const uint32_t vo2 = __shfl_up_sync(0xffffffffu, vo, d);
-                const bool fe2 = __shfl_up_sync(0xffffffffu, (uint32_t)fe, d) != 0;
-                const bool fo2 = __shfl_up_sync(0xffffffffu, (uint32_t)fo, d) != 0;
-                if (lane >= (uint32_t)d) {
-                    if (!fe) {
-                        ve = ve2;
-                        fe = fe2;
-                    }
-                    if (!fo) {
-                        vo = vo2;
-                        fo = fo2;
-                    }
-                }
-            }
-            // value flowing into this lane: the last literal of the lanes before it, else the row carry
-            uint32_t ie = __shfl_up_sync(0xffffffffu, ve, 1), io = __shfl_up_sync(0xffffffffu, vo, 1);
-            const bool ife = __shfl_up_sync(0xffffffffu, (uint32_t)fe, 1) != 0;
-            const bool ifo = __shfl_up_sync(0xffffffffu, (uint32_t)fo, 1) != 0;
-            if (lane == 0 || !ife) ie = ce;
-            if (lane == 0 || !ifo) io = co;
-            uint4 o;
-            o.x = (nib & 1u) ? lx : ie;
-            o.y = (nib & 2u) ? ly : io;
-            o.z = (nib & 4u) ? lz : o.x;
-            o.w = (nib & 8u) ? lw : o.y;
-            ce = __shfl_sync(0xffffffffu, o.z, 31);
-            co = __shfl_sync(0xffffffffu, o.w, 31);
-            *reinterpret_cast<uint4 *>(out + 128 * i + 4 * lane) = o;
-        }
-    }
-}
-
-static unsigned z_grid(const Launch &L, uint64_t units) {
-    uint64_t blocks = (units + 7) / 8;
-    const uint64_t cap = (uint64_t)L.sms * 8;
-    if (blocks > cap) blocks = cap;
-    return (unsigned)(blocks ? blocks : 1);
-}
-
-void launch_zsize(const Launch &L, const GatherArgs &a, uint16_t *zsz, uint64_t max_units) {
-    if (!max_units) return;
-    k_zsize<<<z_grid(L, max_units), 256, 0, L.stream>>>(a, zsz);
-    ++*L.counter;
-}
-
-void launch_zscan(const Launch &L, const uint16_t *zsz, DevStats *st, uint32_t *zloc, uint64_t *zblk,
-                  uint64_t max_units, int gather, uint8_t *img, uint64_t capacity) {
-    const uint64_t nblk = (max_units + kZScanBlock - 1) / kZScanBlock;
-    k_zscan_local<<<(unsigned)(nblk ? nblk : 1), 256, 0, L.stream>>>(zsz, st, zloc, zblk, gather ? 0 : 1);
-    k_zscan_top<<<1, 1024, 0, L.stream>>>(zblk, st, gather, img, capacity, zsz);
-    *L.counter += 2;
-}
-
-void launch_zwrite(const Launch &L, const GatherArgs &a, const uint32_t *zloc, const uint64_t *zblk, uint8_t *dst,
-                   int add_poff, uint64_t u_lo, uint64_t u_hi, uint64_t off0) {
-    if (u_hi <= u_lo) return;
-    k_zwrite<<<z_grid(L, u_hi - u_lo), 256, 0, L.stream>>>(a, zloc, zblk, dst, add_poff, u_lo, u_hi, off0);
-    ++*L.counter;
-}
-
-void launch_zdecode(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
-                    const uint64_t *zblk, DevStats *st, uint8_t *dst, uint64_t units, uint64_t u_lo, int rebase) {
-    if (!units) return;
-    k_zdecode<<<z_grid(L, units), 256, 0, L.stream>>>(src, zsz, zloc, zblk, st, dst, u_lo, u_lo + units, rebase);
-    ++*L.counter;
-}
-
-// Lazy restore of a compressed image: copy the encoded bytes of units
-// [u_lo, u_hi) -- one contiguous byte range of the payload -- from `src`
-// (e.g. a pinned image's mapped address) into `dst` with every thread (wide,
-// coalesced reads across the host link), so the decode then reads HBM.
-// dst receives payload bytes [off(u_lo), off(u_hi)) at dst[0..).
-__global__ void __launch_bounds__(256) k_zfetch(const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
-                                               const uint64_t *zblk, uint64_t u_lo, uint64_t u_hi, uint8_t *dst) {
-    if (u_hi <= u_lo) return;
-    const uint64_t b0 = zblk[u_lo / kZScanBlock] + zloc[u_lo];
-    const uint64_t b1 = zblk[(u_hi - 1) / kZScanBlock] + zloc[u_hi - 1] + zsz[u_hi - 1];
-    const uint64_t n4 = (b1 - b0) / 4;  // encodings are whole u32 words, offsets 4-aligned
-    const uint32_t *s4 = reinterpret_cast<const uint32_t *>(src + b0);
-    uint32_t *d4 = reinterpret_cast<uint32_t *>(dst);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; i + 3 * stride < n4; i += 4 * stride) {
-        const uint32_t a = s4[i], b = s4[i + stride], c = s4[i + 2 * stride], d = s4[i + 3 * stride];
-        d4[i] = a;
-        d4[i + stride] = b;
-        d4[i + 2 * stride] = c;
-        d4[i + 3 * stride] = d;
-    }
-    for (; i < n4; i += stride) d4[i] = s4[i];
-}
-
-void launch_zfetch(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
-                   const uint64_t *zblk, uint64_t u_lo, uint64_t u_hi, uint8_t *dst) {
-    if (u_hi <= u_lo) return;
-    uint64_t blocks = ((u_hi - u_lo) * 1024 + 255) / 256;  // <= one u32 per thread per unit word
-    if (blocks > (uint64_t)L.sms * 8) blocks = L.sms * 8;
-    k_zfetch<<<(unsigned)(blocks ? blocks : 1), 256, 0, L.stream>>>(src, zsz, zloc, zblk, u_lo, u_hi, dst);
-    ++*L.counter;
-}
-
-// Lazy restore of a compressed image: check every unit's bitmap population
-// against its size (the CORRUPT verdict a full decode would give) reading only
-// the 128-byte bitmaps, in place (e.g. through a pinned image's mapped address).
-__global__ void __launch_bounds__(256) k_zcheck(const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
-                                               const uint64_t *zblk, DevStats *st) {
-    const uint64_t U = st->total_units;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarps) {
-        const uint32_t cs = zsz[u];
-        if (cs == 0 || cs == kSegBytes) continue;
-        const uint32_t *in = reinterpret_cast<const uint32_t *>(src + zblk[u / kZScanBlock] + zloc[u]);
-        const uint32_t n = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(in[lane]));
-        if (128u + 4u * n != cs && lane == 0) st->status = kStCorrupt;
-    }
-}
-
-void launch_zcheck(const Launch &L, const uint8_t *src, const uint16_t *zsz, const uint32_t *zloc,
-                   const uint64_t *zblk, DevStats *st, uint64_t units) {
-    if (!units) return;
-    k_zcheck<<<z_grid(L, units), 256, 0, L.stream>>>(src, zsz, zloc, zblk, st);
-    ++*L.counter;
-}
 
 }  // namespace crum

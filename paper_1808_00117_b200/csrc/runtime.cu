@@ -302,7 +302,10 @@ struct crum_ctx {
     uint32_t *d_zloc = nullptr;
     uint64_t *d_zblk = nullptr;
     uint64_t z_cap = 0;            // units the three arrays hold
-    uint64_t *h_zblk = nullptr;    // pinned host copy of d_zblk (chunk offsets of a host gather)
+    uint64_t *d_zrun = nullptr;    // running encoded length of a compressed gather
+    uint64_t *h_zrun = nullptr;    // pinned, mapped: running length after each chunk ([0] = 0)
+    uint64_t *dh_zrun = nullptr;   // device address of h_zrun
+    uint8_t *d_zstage = nullptr;   // one chunk of encoded units (raw layout, kZChunkUnits x 4 KiB)
     // restore staging kept across calls (grow-only): decoded / verified payload, encoded payload
     uint8_t *d_rtmp = nullptr;
     uint64_t rtmp_cap = 0;
@@ -709,19 +712,26 @@ int ensure_z(crum_ctx *c, uint64_t units) {
     dev_free(c->d_zsz);
     dev_free(c->d_zloc);
     dev_free(c->d_zblk);
-    if (c->h_zblk) cudaFreeHost(c->h_zblk);
-    c->h_zblk = nullptr;
+    if (c->h_zrun) cudaFreeHost(c->h_zrun);
+    c->h_zrun = c->dh_zrun = nullptr;
     c->z_cap = 0;
     int st;
     if ((st = dev_alloc(c, &c->d_zsz, 2 * (units + 8))) || (st = dev_alloc(c, &c->d_zloc, 4 * (units + 8))) ||
         (st = dev_alloc(c, &c->d_zblk, 8 * (units / kZScanBlock + 2))))
         return st;
-    if (cudaHostAlloc(reinterpret_cast<void **>(&c->h_zblk), 8 * (units / kZScanBlock + 2), cudaHostAllocDefault) !=
-        cudaSuccess) {
-        c->h_zblk = nullptr;
+    if (!c->d_zrun && (st = dev_alloc(c, &c->d_zrun, 8))) return st;
+    if (!c->d_zstage && (st = dev_alloc(c, &c->d_zstage, (uint64_t)kZChunkUnits << kSegLog2))) return st;
+    const uint64_t nrun = units / kZChunkUnits + 2;
+    void *dp = nullptr;
+    if (cudaHostAlloc(reinterpret_cast<void **>(&c->h_zrun), 8 * nrun, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&dp, c->h_zrun, 0) != cudaSuccess) {
+        cudaGetLastError();
+        if (c->h_zrun) cudaFreeHost(c->h_zrun);
+        c->h_zrun = nullptr;
         set_detail("cudaHostAlloc of the compressed-chunk table failed");
         return CRUM_E_NOMEM;
     }
+    c->dh_zrun = static_cast<uint64_t *>(dp);
     c->z_cap = units;
     return CRUM_OK;
 }
@@ -1208,7 +1218,9 @@ int crum_destroy(crum_ctx *c) {
     dev_free(c->d_rtmp);
     dev_free(c->d_renc);
     dev_free(c->d_zblk);
-    if (c->h_zblk) cudaFreeHost(c->h_zblk);
+    if (c->h_zrun) cudaFreeHost(c->h_zrun);
+    dev_free(c->d_zrun);
+    dev_free(c->d_zstage);
     dev_free(c->d_st);
     dev_free(c->d_meta);
     for (int i = 0; i < kRing; ++i) dev_free(c->d_ring[i]);
@@ -1669,13 +1681,6 @@ int crum_image_load(crum_ctx *ctx, const char *path, crum_image **out) {
 // A7: sync shadow = detect + compact + commit (no image)
 // ---------------------------------------------------------------------------
 namespace {
-// CRUM_COMPRESS (readings Z1-Z2): detect, compact (+ table),
-// encoded size of every unit and their scan (+ the image's sizes, capacity
-// check), then the metadata CRC (+ tail incl. unit sizes, header) on the side
-// stream beside encode + commit.  `img` is a device buffer or the mapped
-// device address of a pinned host image (then the encoder's stores cross the
-// host link directly: only encoded bytes move).  Capacity failures commit
-// nothing (every later kernel checks the status).
 // A1-A3 into a device image (stream-ordered): detect, compact (+ table,
 // header fields), gather (+ commit), and on the side stream the metadata CRC
 // (+ tail, header).
@@ -1764,128 +1769,101 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
     return CRUM_OK;
 }
 
-int finish_gather_z(crum_ctx *c, cudaStream_t s, uint64_t capacity, crum_report *rep, DevStats *out);
-
-// Sizes: detect, compact (+ table into head), encoded sizes and their scan
-// (+ the image's size fields, capacity check, payload padding into head).
-int enqueue_z_sizes(crum_ctx *c, cudaStream_t s, uint8_t *head, uint64_t capacity, bool full, bool timing) {
+// Compressed gather (readings Z2-Z3).  Detect +
+// compact every page (one range; the host reads the unit count from mapped
+// memory: the one round trip), then per chunk of kZChunkUnits units on the
+// caller's stream: encode (k_zenc) -> chunk scan of the sizes (k_zscan_chunk,
+// running total mirrored into mapped memory) -> pack.  A device image gets
+// the packed bytes in place; a pinned image gets them through a ring slot and
+// one D2H copy per chunk on the copy stream, overlapping the next chunk's
+// encode.  Then the image fields (k_zfinal), the metadata CRC + tail +
+// header (stored through the pinned image's mapped address), and -- only once
+// the image is known to fit -- the commit of every listed page.
+int gather_z(crum_ctx *c, cudaStream_t s, uint8_t *dev_img, crum_image *himg, uint64_t capacity, bool full,
+             bool timing, crum_report *rep) {
     int st;
     if ((st = ensure_z(c, c->max_units))) return st;
-    if (timing) CK(cudaEventRecord(c->ev_t[0], s));
-    CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
-    enqueue_detect(c, s, c->all, full);
-    if (timing) CK(cudaEventRecord(c->ev_t[1], s));
-    enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, full, UINT64_MAX, head));
+    if (himg && (st = ensure_ring(c, (uint64_t)kZChunkUnits << kSegLog2))) return st;
+    uint8_t *img = dev_img;  // device address of the image (a pinned image: its mapped address)
+    if (himg) {
+        void *dp = nullptr;
+        CK(cudaHostGetDevicePointer(&dp, himg->host, 0));
+        img = static_cast<uint8_t *>(dp);
+    }
+    const uint64_t poff = payload_offset_for(c->regs.size());
+    uint8_t *head = capacity >= poff ? img : nullptr;
     Launch L = launch_of(c, s);
-    launch_zsize(L, gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX), c->d_zsz, c->max_units);
-    launch_zscan(L, c->d_zsz, c->d_st, c->d_zloc, c->d_zblk, c->max_units, 1, head, capacity);
+    CK(cudaEventRecord(c->ev_t[0], s));
+    CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
+    CK(cudaMemsetAsync(c->d_zrun, 0, 8, s));
+    enqueue_detect(c, s, c->all, full);
+    CK(cudaEventRecord(c->ev_t[1], s));
+    enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, full, UINT64_MAX, head));
     CK_LAUNCH();
-    if (timing) CK(cudaEventRecord(c->ev_t[2], s));
-    c->last_path = CRUM_PATH_COMPRESSED;
-    return CRUM_OK;
-}
-
-// Device image: the metadata CRC (+ tail incl. unit sizes, header) on the
-// side stream beside encode + commit of every unit.
-int enqueue_gather_z(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, bool full, bool timing) {
-    uint8_t *head = capacity >= payload_offset_for(c->regs.size()) ? img : nullptr;
-    int st = enqueue_z_sizes(c, s, head, capacity, full, timing);
-    if (st) return st;
-    CK(cudaEventRecord(c->ev_fork, s));
-    CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-    launch_crc_meta(launch_of(c, c->aux), crc_args(c, head, nullptr), crc_max_len(c));
-    CK(cudaEventRecord(c->ev_join, c->aux));
-    launch_zwrite(launch_of(c, s), gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX), c->d_zloc, c->d_zblk, head, 1,
-                  0, c->max_units, 0);
-    if (timing) CK(cudaEventRecord(c->ev_t[3], s));
-    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
-    CK_LAUNCH();
-    if (timing) CK(cudaEventRecord(c->ev_t[4], s));
-    CK(cudaEventRecord(c->ev_done, s));
-    c->last_kind = kLastDevGather;
-    c->last_timed = timing;
-    return CRUM_OK;
-}
-
-// Pinned host image: sizes first (the host waits for them: the encoded
-// offsets at every kZScanBlock-unit boundary become the copy boundaries),
-// then per chunk of whole scan blocks encode + commit into a ring slot on the
-// gather stream and copy the encoded bytes D2H on the copy stream; header,
-// table, tail and padding are stored through the image's mapped address.
-int gather_z_host(crum_ctx *c, crum_image *img, cudaStream_t s, bool full, crum_report *rep) {
-    void *dimg_v = nullptr;
-    CK(cudaHostGetDevicePointer(&dimg_v, img->host, 0));
-    uint8_t *dimg = static_cast<uint8_t *>(dimg_v);
-    uint8_t *head = img->cap >= payload_offset_for(c->regs.size()) ? dimg : nullptr;
-    int st = enqueue_z_sizes(c, s, head, img->cap, full, true);
-    if (st) return st;
-    CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(c->h_zblk, c->d_zblk, 8 * (c->max_units / kZScanBlock + 2), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const DevStats h0 = *c->h_st;
-    if (h0.status == kStCapacity) {
-        CK(cudaEventRecord(c->ev_t[3], s));
-        CK(cudaEventRecord(c->ev_t[4], s));
-        CK(cudaEventRecord(c->ev_t[5], s));
-        CK(cudaEventRecord(c->ev_done, s));
-        c->last_kind = kLastHostGather;
-        c->last_timed = true;
-        return finish_gather_z(c, s, img->cap, rep, nullptr);
-    }
-    CK(cudaEventRecord(c->ev_fork, s));
-    CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-    launch_crc_meta(launch_of(c, c->aux), crc_args(c, head, nullptr), crc_max_len(c));
-    CK(cudaEventRecord(c->ev_join, c->aux));
-    const uint64_t U = h0.total_units;
-    // chunks of whole scan blocks: h_zblk[b] = encoded offset of unit b * kZScanBlock,
-    // h_zblk[nblk] = encoded length (k_zscan_top)
-    const uint64_t upc = std::max<uint64_t>(kZScanBlock, (c->ring_cap >> kSegLog2) / kZScanBlock * kZScanBlock);
-    auto off_at = [&](uint64_t u) { return c->h_zblk[(u + kZScanBlock - 1) / kZScanBlock]; };
-    Launch G = launch_of(c, c->gstream);
+    CK(cudaEventRecord(c->ev_t[2], s));
+    CK(cudaEventSynchronize(c->ev_t[2]));  // h_rb[1] written by the compaction (mapped)
+    const uint64_t U = c->h_rb[1].units;
+    c->h_zrun[0] = 0;
     const GatherArgs ga = gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX);
-    CK(cudaEventRecord(c->ev_fork, s));
-    CK(cudaStreamWaitEvent(c->gstream, c->ev_fork, 0));
-    bool copy_started = false;
-    uint64_t chunk_idx = 0;
-    for (uint64_t u0 = 0; u0 < U; u0 += upc, ++chunk_idx) {
-        const uint64_t u1 = std::min(U, u0 + upc);
-        const int slot = (int)(chunk_idx % kRing);
-        if (chunk_idx >= (uint64_t)kRing) CK(cudaStreamWaitEvent(c->gstream, c->ev_copy[slot], 0));
-        const uint64_t o0 = off_at(u0);
-        launch_zwrite(G, ga, c->d_zloc, c->d_zblk, c->d_ring[slot], 0, u0, u1, o0);
-        CK_LAUNCH();
-        CK(cudaEventRecord(c->ev_gather[slot], c->gstream));
+    const uint64_t nch = (U + kZChunkUnits - 1) / kZChunkUnits;
+    bool overflow = false, copy_started = false;
+    auto copy_chunk = [&](uint64_t k) -> int {  // host image: chunk k's packed bytes -> the image
+        const int slot = (int)(k % kRing);
+        CK(cudaEventSynchronize(c->ev_gather[slot]));
+        const uint64_t o0 = c->h_zrun[k], o1 = c->h_zrun[k + 1];
+        if (poff + o1 > himg->cap) overflow = true;  // CAPACITY: stop copying, keep encoding for the size
         CK(cudaStreamWaitEvent(c->copy, c->ev_gather[slot], 0));
-        if (!copy_started) {
-            CK(cudaEventRecord(c->ev_t[4], c->copy));
-            copy_started = true;
+        if (!overflow && o1 > o0) {
+            if (!copy_started) {
+                CK(cudaEventRecord(c->ev_t[4], c->copy));
+                copy_started = true;
+            }
+            CK(cudaMemcpyAsync(himg->host + poff + o0, c->d_ring[slot], o1 - o0, cudaMemcpyDeviceToHost, c->copy));
         }
-        const uint64_t o1 = off_at(u1);  // u1 is a block boundary or U (-> the total)
-        if (o1 > o0)
-            CK(cudaMemcpyAsync(img->host + h0.poff + o0, c->d_ring[slot], o1 - o0, cudaMemcpyDeviceToHost, c->copy));
         CK(cudaEventRecord(c->ev_copy[slot], c->copy));
+        return CRUM_OK;
+    };
+    for (uint64_t k = 0; k < nch; ++k) {
+        const uint64_t u0 = k * kZChunkUnits, u1 = std::min(U, u0 + kZChunkUnits);
+        launch_zenc(L, ga, u0, u1, c->d_zstage, c->d_zsz);
+        launch_zscan_chunk(L, c->d_zsz, u0, u1, c->d_st, c->d_rb, c->d_zloc, c->d_zblk, c->d_zrun,
+                           c->dh_zrun + k + 1);
+        if (himg) {
+            const int slot = (int)(k % kRing);
+            if (k >= (uint64_t)kRing) CK(cudaStreamWaitEvent(s, c->ev_copy[slot], 0));
+            launch_zpack(L, c->d_zstage, c->d_zsz, c->d_zloc, c->d_zblk, u0, u1, c->d_st, c->d_rb, c->d_ring[slot], 1,
+                         0);
+            CK_LAUNCH();
+            CK(cudaEventRecord(c->ev_gather[slot], s));
+            if (k && (st = copy_chunk(k - 1))) return st;
+        } else {
+            launch_zpack(L, c->d_zstage, c->d_zsz, c->d_zloc, c->d_zblk, u0, u1, c->d_st, c->d_rb, img + poff, 0,
+                         capacity);
+            CK_LAUNCH();
+        }
     }
-    if (!copy_started) CK(cudaEventRecord(c->ev_t[4], c->copy));
-    CK(cudaEventRecord(c->ev_t[5], c->copy));
-    CK(cudaEventRecord(c->ev_t[3], c->gstream));
-    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
-    CK(cudaStreamSynchronize(c->gstream));
-    CK(cudaStreamSynchronize(c->copy));
+    if (himg && nch && (st = copy_chunk(nch - 1))) return st;
+    CK(cudaEventRecord(c->ev_t[3], s));
+    if (himg && !copy_started) CK(cudaEventRecord(c->ev_t[4], c->copy));
+    launch_zfinal(L, c->d_st, c->d_zrun, head, capacity);
+    launch_crc_meta(L, crc_args(c, head, nullptr), crc_max_len(c));
+    // commit every listed page (a no-op on the device when the image did not fit)
+    if (U) launch_gather(L, ga, U);
+    CK_LAUNCH();
+    if (himg) {
+        CK(cudaEventRecord(c->ev_t[5], c->copy));
+        CK(cudaStreamWaitEvent(s, c->ev_t[5], 0));
+    }
+    if (!himg) CK(cudaEventRecord(c->ev_t[4], s));  // device image: e4 = end of the call
     CK(cudaEventRecord(c->ev_done, s));
-    c->last_kind = kLastHostGather;
-    c->last_timed = true;
-    DevStats h;
-    st = finish_gather_z(c, s, img->cap, rep, &h);
-    if (st == CRUM_OK) img->len = h.image_bytes;
-    return st;
-}
-
-// Report + status of a finished compressed gather.
-int finish_gather_z(crum_ctx *c, cudaStream_t s, uint64_t capacity, crum_report *rep, DevStats *out) {
+    c->last_kind = himg ? kLastHostGather : kLastDevGather;
+    c->last_timed = timing;
+    c->last_path = CRUM_PATH_COMPRESSED;
+    if (!himg && !rep) return CRUM_OK;  // stream-asynchronous (capacity >= worst case)
     CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const DevStats h = *c->h_st;
-    if (out) *out = h;
+    if (himg && h.status == kStOk) himg->len = h.image_bytes;
     if (rep) {
         memset(rep, 0, sizeof *rep);
         fill_report(c, h, rep);
@@ -1961,10 +1939,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     uint64_t worst = 0;
     crum_image_required_bytes(c, UINT64_MAX, &worst);
     // The single-pass kernel is opt-in (CRUM_CFG_FUSED).
-        if (flags & CRUM_COMPRESS) {
-        if ((st = enqueue_gather_z(c, s, img, capacity, full, timing))) return st;
-        return rep ? finish_gather_z(c, s, capacity, rep, nullptr) : CRUM_OK;
-    }
+    if (flags & CRUM_COMPRESS) return gather_z(c, s, img, nullptr, capacity, full, timing, rep);
     if (c->fused_ok && c->fused_cfg && !full && capacity >= worst) {
         // single pass: detect + compact + gather + commit in one kernel, then
         // the metadata CRC / tail / header
@@ -2069,10 +2044,7 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool full = flags & CRUM_FULL;
-    if (flags & CRUM_COMPRESS) {
-        int st = ensure_ring(c, (uint64_t)kZScanBlock << kSegLog2);  // a slot holds >= one scan block
-        return st ? st : gather_z_host(c, img, s, full, rep);
-    }
+    if (flags & CRUM_COMPRESS) return gather_z(c, s, nullptr, img, img->cap, full, true, rep);
     c->last_path = 0;
     uint64_t worst;
     crum_image_required_bytes(c, UINT64_MAX, &worst);
@@ -2447,13 +2419,13 @@ int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img
     Launch L = launch_of(c, s);
     if (tab_len + tail_len) launch_crc_check(L, d_table, tab_len, d_tail, tail_len, c->d_st, crc_tables().x2n);
     launch_restore_validate(L, c->d_tregs, p.R, c->d_rs, d_ids, d_hashes, p.K, c->d_st);
-    // compressed: every unit size valid, sizes summing to the payload (readings Z1-Z2)
+    // compressed: every unit size <= 4096, sizes summing to the payload (readings Z2-Z3)
     const bool zimg = (p.flags & 4u) != 0;
     const uint64_t zunits = p.upayload >> kSegLog2;
     const uint16_t *d_zsz = reinterpret_cast<const uint16_t *>(d_tail + tail_bytes_for(p.K, hh));
     if (zimg) {
         if ((st = ensure_z(c, zunits))) return st;
-        launch_zscan(L, d_zsz, c->d_st, c->d_zloc, c->d_zblk, zunits, 0, nullptr, 0);
+        launch_zscan(L, d_zsz, c->d_st, c->d_zloc, c->d_zblk, zunits);
     }
     CK_LAUNCH();
     CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
@@ -2473,22 +2445,23 @@ int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img
     }
     uint8_t *d_payload_tmp = nullptr;
     const uint8_t *payload_dev = dev_img ? dev_img + p.poff : nullptr;
-    // compressed: decode every unit into device memory first (a bitmap that
-    // disagrees with its unit's size is CORRUPT); a pinned image's encoded
-    // payload crosses the link once (copy engine), then decodes from HBM
+    // compressed: decode every unit into device memory first (a unit that is
+    // not a valid encoding is CORRUPT); a pinned image's encoded payload
+    // crosses the link once (copy engine), then decodes from HBM
     if (zimg && lazy_z && host_img && !(flags & CRUM_VERIFY)) {
-        // lazy session: check every bitmap in place now (same CORRUPT verdict
-        // as a full decode), decode windows on demand later
+        // lazy session: validate every unit now by decoding it in place
+        // through the mapped address without storing the result (the same
+        // CORRUPT verdict as a full decode), decode windows on demand later
         void *dp = nullptr;
         CK(cudaHostGetDevicePointer(&dp, const_cast<uint8_t *>(host_img), 0));
         pr.zsrc = static_cast<const uint8_t *>(dp) + p.poff;
         pr.z_lazy = true;
-        launch_zcheck(L, pr.zsrc, d_zsz, c->d_zloc, c->d_zblk, c->d_st, zunits);
+        launch_zdecode(L, pr.zsrc, d_zsz, c->d_zloc, c->d_zblk, c->d_st, nullptr, zunits);
         CK_LAUNCH();
         CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (c->h_st->status != kStOk) {
-            set_detail("compressed unit whose bitmap disagrees with its size");
+            set_detail("compressed unit that is not a valid encoding");
             return CRUM_E_CORRUPT;
         }
     } else if (zimg) {
@@ -2505,7 +2478,7 @@ int prepare_restore(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img
         CK(cudaStreamSynchronize(s));
         if (c->h_st->status != kStOk) {
             tmp_free(d_payload_tmp);
-            set_detail("compressed unit whose bitmap disagrees with its size");
+            set_detail("compressed unit that is not a valid encoding");
             return CRUM_E_CORRUPT;
         }
         payload_dev = d_payload_tmp;
@@ -2705,7 +2678,7 @@ int session_scatter_slots(crum_restore_session *ss, uint32_t k, uint64_t klo, ui
         const uint64_t need = nu << kSegLog2;
         uint8_t *win = nullptr, *enc = nullptr;
         CK(cudaMallocAsync(reinterpret_cast<void **>(&win), need, s));
-        CK(cudaMallocAsync(reinterpret_cast<void **>(&enc), need, s));
+        CK(cudaMallocAsync(reinterpret_cast<void **>(&enc), need + 64, s));  // + word alignment slack
         const uint16_t *zsz = reinterpret_cast<const uint16_t *>(
             ss->d_tail + tail_bytes_for(ss->p.K, (ss->p.flags & 2u) != 0));
         const Launch L = launch_of(c, s);

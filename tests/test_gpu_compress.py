@@ -1,9 +1,11 @@
-"""GPU parity of compressed images (CRUM_COMPRESS; readings Z1-Z2):
-libcrum.so's encoder (host image through its mapped address, and device
-image) vs the CPU oracle byte for byte; restore (eager, VERIFY, lazy) of
-compressed images; corruption and capacity errors.  Region contents follow
-the paper's "50% random" shape plus fully random and
-sparse pages."""
+"""GPU parity of compressed images (CRUM_COMPRESS; readings Z2-Z3:
+per 4 KiB unit a greedy LZ77 parse in one fixed-Huffman DEFLATE block):
+libcrum.so's encoder (pinned image through the chunked pipeline, and device
+image) vs the CPU oracle byte for byte, every encoded unit inflated by zlib;
+restore (eager, VERIFY, lazy) of compressed images; the GPU decoder's verdict
+on damaged streams equal to the oracle's; capacity errors.  Region contents
+follow the paper's "50% random" shape, HPGMG-like fp64
+fields (smooth, constant, zero ghost zones) and fully random pages."""
 import numpy as np
 import pytest
 
@@ -33,24 +35,65 @@ def crum():
     return m
 
 
-def shaped_pair(seed_idx, shape="half"):
+def fill_structured(h: np.ndarray, seed: int):
+    """HPGMG-like content: per 32 KiB box, fp64 values of a smooth field, a
+    constant coefficient, or zero (ghost zones / cleared temporaries)."""
+    rng = np.random.default_rng(seed)
+    n = h.nbytes // 8 * 8
+    f = h[:n].view("<f8")
+    box = 4096
+    for b0 in range(0, f.size, box):
+        k = int(rng.integers(0, 4))
+        seg = f[b0:b0 + box]
+        if k == 0:
+            x = np.arange(seg.size) * rng.uniform(0.001, 0.05)
+            seg[:] = np.sin(x) * rng.uniform(0.5, 2)
+        elif k == 1:
+            seg[:] = rng.uniform(-1, 1)
+        elif k == 2:
+            seg[:] = 0
+        else:
+            seg[:] = np.round(rng.normal(size=seg.size), 3)
+    h[n:] = 0
+
+
+def shaped_pair(seed_idx, shape="half", specs=None):
     """Pair whose regions are random in their first half and constant after
-    (shape 'half'), or fully random ('random')."""
+    (shape 'half'), HPGMG-like ('structured'), or fully random ('random')."""
     from tests.gpu_pair import Pair
-    p = Pair(SPECS, synth.seed(seed_idx))
-    if shape == "half":
-        for h, d in zip(p.host, p.dev):
+    p = Pair(specs or SPECS, synth.seed(seed_idx))
+    if shape != "random":
+        for r, (h, d) in enumerate(zip(p.host, p.dev)):
             n = h.nbytes
-            h[n // 2:] = 0
-            h[n // 2 + 4096: n // 2 + 8192] = np.frombuffer(np.full(1024, 0.5, np.float32).tobytes(), np.uint8)
+            if shape == "half":
+                h[n // 2:] = 0
+                h[n // 2 + 4096: n // 2 + 8192] = np.frombuffer(np.full(1024, 0.5, np.float32).tobytes(), np.uint8)
+            else:
+                fill_structured(h, 1000 * seed_idx + r)
             d.copy_(torch.from_numpy(h))
         torch.cuda.synchronize()
     return p
 
 
-@pytest.mark.parametrize("shape", ["half", "random"])
+def check_units_inflate(img_bytes):
+    """Every encoded unit of a compressed image inflates (zlib, raw DEFLATE)
+    to 4096 bytes, ending exactly at its last byte (an independent decoder)."""
+    from tests import imgfmt
+    info = imgfmt.parse_image(np.frombuffer(img_bytes, dtype=np.uint8))
+    off = info["poff"]
+    n_deflate = 0
+    for cs in info["zsizes"]:
+        enc = img_bytes[off:off + cs]
+        if 0 < cs < 4096:
+            assert len(imgfmt.z_decode_unit(enc)) == 4096
+            n_deflate += 1
+        off += cs
+    return n_deflate
+
+
+@pytest.mark.parametrize("shape", ["half", "structured", "random"])
 def test_compressed_gather_bit_exact(crum, shape):
-    p = shaped_pair(90 if shape == "half" else 91, shape)
+    p = shaped_pair({"half": 90, "random": 91, "structured": 94}[shape], shape)
     img = p.g.new_image()
     cap = p.g.image_required_bytes()
     buf = torch.empty(cap + 256, dtype=torch.uint8, device="cuda")
@@ -68,6 +111,9 @@ def test_compressed_gather_bit_exact(crum, shape):
         assert rep["path"] & crum.PATH_COMPRESSED
         assert len(got) == len(want), epoch
         assert got == want.tobytes(), epoch
+        if epoch in (0, 3):
+            n_deflate = check_units_inflate(got)   # random pages: only the zero-padded tail units shrink
+            assert n_deflate > 0, epoch
         for k in ("dirty_pages", "dirty_bytes", "dirty_runs", "image_bytes"):
             assert rep[k] == rep_o[k], (epoch, k)
         assert p.shadows_equal(), epoch
@@ -153,16 +199,71 @@ def test_compressed_errors(crum):
     p.g.checkpoint_gather(img, flags=crum.COMPRESS)
     raw = img.view().copy()
     info = imgfmt.parse_image(raw)
-    u = next(i for i, cs in enumerate(info["zsizes"]) if 132 <= cs < 4096)
+    u = next(i for i, cs in enumerate(info["zsizes"]) if 0 < cs < 4096)
     coff = info["poff"] + sum(info["zsizes"][:u])
-    bm = np.unpackbits(raw[coff:coff + 128], bitorder="little")
-    j = int(np.flatnonzero(bm == 0)[0])
     bad = raw.copy()
-    bad[coff + j // 8] |= 1 << (j % 8)                                     # bitmap disagrees with size
+    bad[coff] ^= 1                                                        # BFINAL = 0: not this codec
     o, g, hz, dz = restart(crum, SPECS)
     assert o.restore_scatter(bad)[0] == crum.E_CORRUPT
     st, _ = g.restore_scatter(g.import_image(bad), raise_on_error=False)
     assert st == crum.E_CORRUPT
     torch.cuda.synchronize()
     assert all(int(d.count_nonzero()) == 0 for d in dz)                  # nothing written
+    with pytest.raises(crum.CrumError):                                   # lazy: validated at begin
+        g.restore_begin(g.import_image(bad))
     assert g.restore_scatter(g.import_image(raw))["dirty_pages"] == p.N
+
+
+def test_decoder_verdicts_match_oracle(crum):
+    """Damaged streams (the CRCs cover only the metadata): random bit flips
+    inside encoded units.  The GPU decoder and the oracle give the same
+    verdict, and when a damaged stream still decodes, the same bytes."""
+    from tests import imgfmt
+    p = shaped_pair(95, "structured")
+    img = p.g.new_image()
+    p.g.checkpoint_gather(img, flags=crum.COMPRESS)
+    raw = img.view().copy()
+    info = imgfmt.parse_image(raw)
+    offs, off = [], info["poff"]
+    for cs in info["zsizes"]:
+        if 0 < cs < 4096:
+            offs.append((off, cs))
+        off += cs
+    rng = np.random.default_rng(7)
+    outcomes = set()
+    for t in range(24):
+        o0, cs = offs[int(rng.integers(0, len(offs)))]
+        bad = raw.copy()
+        bit = int(rng.integers(0, 8 * cs))
+        bad[o0 + bit // 8] ^= 1 << (bit % 8)
+        o, g, hz, dz = restart(crum, SPECS)
+        st_o, _ = o.restore_scatter(bad)
+        st_g, _ = g.restore_scatter(g.import_image(bad), raise_on_error=False)
+        assert st_g == st_o, (t, bit)
+        outcomes.add(st_o)
+        if st_o == 0:
+            torch.cuda.synchronize()
+            for d, h in zip(dz, hz):
+                assert np.array_equal(d.cpu().numpy(), h), t
+    assert crum.E_CORRUPT in outcomes
+
+
+def test_compressed_multi_chunk(crum):
+    """Footprints of several 64 MiB encode chunks: the pinned pipeline's ring
+    and per-chunk copies, and a capacity failure part-way through them."""
+    specs = [(150 * MiB + 4096 * 3 + 5, 64 * KiB, C), (40 * MiB, 4 * KiB, H)]
+    p = shaped_pair(96, "structured", specs)
+    for epoch, d in ((0, 0), (1, 0.6)):
+        if epoch:
+            p.write(epoch, d)
+        st, want, rep_o = p.o.checkpoint_gather(flags=crum.COMPRESS)
+        short = p.g.new_image(len(want) // 2)
+        st, rep = p.g.checkpoint_gather(short, flags=crum.COMPRESS, raise_on_error=False)
+        assert st == crum.E_CAPACITY and rep["image_bytes"] == len(want)
+        short.destroy()
+        img = p.g.new_image(len(want))
+        rep = p.g.checkpoint_gather(img, flags=crum.COMPRESS)
+        assert img.tobytes() == want.tobytes(), epoch
+        assert rep["image_bytes"] == len(want) < rep["dirty_bytes"]
+        assert p.shadows_equal(), epoch
+        img.destroy()
