@@ -64,10 +64,13 @@ def parse():
     ap.add_argument("--dirty", type=float, default=None,
                     help="fraction of pages rewritten per step (default: 1%% for C1, 10%% otherwise, as BASELINE.json)")
     ap.add_argument("--region-gib", type=float, default=1.0)
-    ap.add_argument("--compress", action="store_true", help="CRUM_COMPRESS gathers (DESIGN.md Z1-Z2)")
-    ap.add_argument("--content", default="random", choices=["random", "half"],
+    ap.add_argument("--compress", action="store_true",
+                    help="CRUM_COMPRESS gathers: LZ77 + fixed-Huffman DEFLATE per 4 KiB unit (DESIGN.md Z2-Z3)")
+    ap.add_argument("--content", default="random", choices=["random", "half", "hpgmg"],
                     help="half: the paper's 50%%-random vectors (PAPER.md:907-912): second half of every "
-                         "region one repeated fp32 value; the writer then rewrites one word per dirty page")
+                         "region one repeated fp32 value; hpgmg: HPGMG-FV-like fp64 boxes (smooth fields, "
+                         "constant coefficients, zero temporaries and ghost zones; synth.hpgmg_box_kinds); "
+                         "for both the writer then rewrites one word per dirty page")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test the multi-rank path with several ranks sharing fewer GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -180,7 +183,8 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU oracle (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
-def oracle_steps(specs, S, dirty, seconds: float, max_steps: int, min_steps: int = 1):
+def oracle_steps(specs, S, dirty, seconds: float, max_steps: int, min_steps: int = 1, content: str = "random",
+                 flags: int = 0):
     """Time oracle checkpoint_gather on the same workload (host copies),
     writer outside the timing.  Returns (per-step seconds list, F, sample)."""
     from oracle import oracle
@@ -189,11 +193,15 @@ def oracle_steps(specs, S, dirty, seconds: float, max_steps: int, min_steps: int
     for r, (nb, P, mode) in enumerate(specs):
         h = oracle.aligned_empty(nb)
         synth.fill_region(h, S, r)
+        if content == "half":
+            h[nb // 2 // 4 * 4:].view(np.float32)[:] = 0.25
+        elif content == "hpgmg":
+            synth.hpgmg_fill(h, r)
         host.append(h)
         o.register(h, P, mode)
     cap = o.required_bytes()
     out = np.zeros(cap, dtype=np.uint8)  # reused: the timed step allocates nothing
-    o.checkpoint_gather(capacity=cap, out=out)   # initial full image (epoch 0), untimed
+    o.checkpoint_gather(flags=flags, capacity=cap, out=out)   # initial full image (epoch 0), untimed
     times = []
     t_start = time.perf_counter()
     epoch = 0
@@ -201,11 +209,11 @@ def oracle_steps(specs, S, dirty, seconds: float, max_steps: int, min_steps: int
         epoch += 1
         for r, (nb, P, mode) in enumerate(specs):
             pages = synth.choose_dirty(S, epoch, r, synth.n_pages(nb, P), dirty)
-            synth.apply_writer(host[r], P, pages, S, epoch, r)
+            synth.apply_writer(host[r], P, pages, S, epoch, r, touch=content != "random")
             if mode == 2:  # TRACKED: the writer marks what it writes
                 o.mark_pages(r + 1, pages)
         t0 = time.perf_counter()
-        st, img, rep = o.checkpoint_gather(capacity=cap, out=out)
+        st, img, rep = o.checkpoint_gather(flags=flags, capacity=cap, out=out)
         times.append(time.perf_counter() - t0)
         assert st == 0
     F = sum(nb for nb, _, _ in specs)
@@ -362,6 +370,34 @@ def config_for(args, specs, desc, world: int):
                    "written back there, untimed) and leaves it clean: every step starts cold")}
 
 
+def hpgmg_fill_device(t, r: int):
+    """HPGMG-FV-like content on the device (the paper's real-application image
+    compresses 113 MB -> 14-16 MB): every 32 KiB box of fp64
+    values is one of the kinds synth.hpgmg_box_kinds names -- a smooth field
+    (solution / right-hand side), a constant coefficient (alpha, beta, Dinv)
+    or zero (temporaries) -- with zero ghost layers at both ends of the box."""
+    import torch
+    n = t.numel() // 8
+    nbox = n // 4096
+    if nbox == 0:
+        return
+    kinds = synth.hpgmg_box_kinds(nbox, r)
+    F = t[:nbox * 4096 * 8].view(torch.float64).view(nbox, 4096)
+    x = torch.arange(4096, dtype=torch.float64, device=t.device)
+    step = max(1, (256 << 20) // (4096 * 8))   # 256 MiB of boxes at a time (bounded temporaries)
+    for b0 in range(0, nbox, step):
+        b1 = min(nbox, b0 + step)
+        k = torch.from_numpy(kinds[b0:b1]).to(t.device)
+        blk = F[b0:b1]
+        idx = torch.arange(b0, b1, dtype=torch.float64, device=t.device)
+        smooth = torch.sin(x[None, :] * (0.001 + 0.0005 * (idx[:, None] % 7)) + idx[:, None]) * (1 + (idx[:, None] % 3))
+        blk.copy_(torch.where((k <= 1)[:, None], smooth, blk))
+        for kind, val in ((2, 1.0), (3, 1.0), (4, 1.0), (5, 1.0), (6, 1.0 / 6.0), (7, 0.0)):
+            blk[k == kind] = val
+        blk[:, :256] = 0
+        blk[:, -256:] = 0
+
+
 def snapshot_to_host(tensors):
     """Host copies of device tensors at HBM-footprint scale: the destination
     pages are first touched by all host threads at once (a single-threaded
@@ -416,9 +452,10 @@ def parity_check(args, ctx, crum, regions, specs, rids, S, epoch, stream, img, d
     import torch
     from oracle import oracle
     from tests import fullparity
-    half = args.content == "half"
-    if gflags:
-        return {"checked": False, "why": "compressed images: tests/test_gpu_compress.py"}
+    half = args.content != "random"   # the touch writer
+    F = sum(nb for nb, _, _ in specs)
+    if gflags and F > 4 * GiB:
+        return {"checked": False, "why": "compressed images above 4 GiB: tests/test_gpu_compress.py"}
     torch.cuda.synchronize()
     ctx.sync_shadow(stream)
     torch.cuda.synchronize()
@@ -440,6 +477,25 @@ def parity_check(args, ctx, crum, regions, specs, rids, S, epoch, stream, img, d
     ctx.checkpoint_gather(img, stream=stream, flags=gflags)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
+    if gflags:
+        # compressed: the oracle gathers the same state with CRUM_COMPRESS (whole image)
+        o = oracle.Oracle()
+        for r, (nb, P, mode) in enumerate(specs):
+            o.register(host[r], P, mode)
+        o.sync_shadow()
+        for r, (nb, P, mode) in enumerate(specs):
+            pg = synth.choose_dirty(S, epoch, r, synth.n_pages(nb, P), args.dirty)
+            synth.apply_writer(host[r], P, pg, S, epoch, r, touch=half)
+            if mode == 2:
+                o.mark_pages(r + 1, pg)
+        st, want, _ = o.checkpoint_gather(flags=oracle.COMPRESS)
+        got = img.view()
+        ok = st == 0 and got.nbytes == want.nbytes and bool(np.array_equal(got, want))
+        o.close()
+        return {"checked": True, "ok": ok, "path": "crum_checkpoint_gather (pinned, compressed, as timed)",
+                "image_bytes": int(got.nbytes), "oracle_s": round(time.perf_counter() - t1, 2),
+                "what": "one more epoch after the timed steps: the GPU's compressed image vs the oracle's, byte "
+                        "for byte"}
     res = fullparity.regionwise_check(img.view(), specs, rids, lambda r: host[r], S, epoch, args.dirty,
                                       touch=half, threads=min(16, len(os.sched_getaffinity(0))))
     out = {"checked": True, "ok": bool(res["ok"]), "path": "crum_checkpoint_gather (pinned image, as timed)",
@@ -568,6 +624,8 @@ def main():
             crum.synth_fill(t, nb, S, r, stream=stream)
             if args.content == "half":
                 t[nb // 2 // 4 * 4:].view(torch.float32).fill_(0.25)
+            elif args.content == "hpgmg":
+                hpgmg_fill_device(t, r)
             regions.append(t)
     stream.synchronize()
     t_alloc = time.perf_counter() - t_setup
@@ -613,7 +671,7 @@ def main():
                 crum.synth_write_pages_tracked(regions[r], nb, P, pg, pg.numel(), S, e, r, trackers[r],
                                                stream=stream)
             else:
-                crum.synth_write_pages(regions[r], nb, P, pg, pg.numel(), S, e, r, args.content == "half",
+                crum.synth_write_pages(regions[r], nb, P, pg, pg.numel(), S, e, r, args.content != "random",
                                        stream=stream)
         crum.synth_scrub(scrub, scrub.numel(), stream=stream)
 
@@ -800,8 +858,12 @@ def main():
                             "hbm": hbm}
     if args.compress:
         line["compression"] = {"image_bytes": rep["image_bytes"], "dirty_bytes": rep["dirty_bytes"],
-                               "ratio": round(rep["dirty_bytes"] / max(rep["image_bytes"], 1), 3)}
-
+                               "ratio": round(rep["dirty_bytes"] / max(rep["image_bytes"], 1), 3),
+                               "detect_to_last_chunk_packed_ms": round(
+                                   statistics.median([g.local["t_gather_ms"] for g in greps]), 3),
+                               "codec": "per 4 KiB unit: greedy LZ77 (12-bit hash, every position inserted) in "
+                                        "one fixed-Huffman DEFLATE block, zero units empty, incompressible units "
+                                        "raw (DESIGN.md Z2-Z3)"}
     # ---- restore of the last timed step's image onto the live regions (H2D inside) ----
     torch.cuda.synchronize()
     r_ms = []
@@ -873,7 +935,8 @@ def main():
     # ---- cpu_baseline: the oracle on a bounded sample, rank 0 at N=1 only ----
     if not args.no_cpu_baseline and world == 1:
         sample, what = oracle_sample(specs)
-        times, Fo = oracle_steps(sample, synth.seed(1), args.dirty, seconds=args.cpu_seconds, max_steps=50)
+        times, Fo = oracle_steps(sample, synth.seed(1), args.dirty, seconds=args.cpu_seconds, max_steps=50,
+                                 content=args.content, flags=4 if args.compress else 0)
         v = Fo / statistics.median(times) / 1e9
         line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                                 "sample": f"{len(times)} oracle checkpoint_gather steps over {what} "

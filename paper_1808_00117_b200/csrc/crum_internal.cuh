@@ -230,27 +230,22 @@ void launch_scatter(const Launch &L, const ScatterArgs &a);
 
 // Compressed images (kernels_zip.cu; readings Z2-Z3): per 4 KiB
 // payload unit a greedy LZ77 parse coded as one fixed-Huffman DEFLATE block.
-// Offsets of the encoded units: zblk[u / kZScanBlock] + zloc[u] (bytes from
-// the payload start).  A gather encodes chunk by chunk (kZChunkUnits units,
-// a multiple of kZScanBlock): encode -> chunk scan -> pack.
+// A gather gathers the listed pages chunk by chunk into a raw staging buffer
+// (k_gather, no commit), then encode -> chunk scan -> pack.  Restore offsets
+// of encoded units: zblk[u / kZScanBlock] + zloc[u] (bytes from the payload).
 constexpr uint32_t kZScanBlock = 2048;
-constexpr uint32_t kZChunkUnits = 16384;   // 64 MiB of units per chunk
-// Encode units [u_lo, u_hi) of the gather (a: unit -> page map) into
-// stage + (u - u_lo) * 4096 (raw layout), sizes into zsz[u].
-void launch_zenc(const Launch &L, const GatherArgs &a, uint64_t u_lo, uint64_t u_hi, uint8_t *stage, uint16_t *zsz);
-// Offsets of units [u_lo, u_hi) (u_lo % kZScanBlock == 0): zloc / zblk from
-// the running total *zrun, which is advanced; *zrun_host (mapped, nullable)
-// receives the new running total.
-void launch_zscan_chunk(const Launch &L, const uint16_t *zsz, uint64_t u_lo, uint64_t u_hi, const DevStats *st,
-                        const RangeTotals *rb, uint32_t *zloc, uint64_t *zblk, uint64_t *zrun,
-                        uint64_t *zrun_host);
-// Move the encodings of units [u_lo, u_hi) from stage to their places:
-// dst + off(u) - (rel ? off(u_lo) : 0); with limit != 0 a unit is written
-// only if poff + off(u) + size <= limit (device image capacity).  rb: the
-// gather's totals (rb[1].units bounds the units).
-void launch_zpack(const Launch &L, const uint8_t *stage, const uint16_t *zsz, const uint32_t *zloc,
-                  const uint64_t *zblk, uint64_t u_lo, uint64_t u_hi, const DevStats *st, const RangeTotals *rb,
-                  uint8_t *dst, int rel, uint64_t limit);
+constexpr uint32_t kZChunkUnits = 4096;    // 16 MiB of units per compressed chunk
+// Encode the n units at raw (4 KiB each) into enc (same layout), sizes into zsz[0..n).
+void launch_zenc(const Launch &L, const uint8_t *raw, uint64_t n, uint8_t *enc, uint16_t *zsz, const DevStats *st);
+// Chunk-relative offsets zloc[0..n) of the n <= kZChunkUnits sizes; *zbase =
+// the running total *zrun before the chunk; *zrun (and *zrun_host, mapped,
+// nullable) advanced by the chunk's total.
+void launch_zscan_chunk(const Launch &L, const uint16_t *zsz, uint64_t n, uint32_t *zloc, uint64_t *zrun,
+                        uint64_t *zbase, uint64_t *zrun_host);
+// Move the n encodings from stage to dst + (base ? *base : 0) + zloc[i];
+// limit != 0: a unit is written only if poff + offset + size <= limit.
+void launch_zpack(const Launch &L, const uint8_t *stage, const uint16_t *zsz, const uint32_t *zloc, uint64_t n,
+                  const uint64_t *base, uint8_t *dst, uint64_t limit, const DevStats *st);
 // After the last chunk: the compressed image's sizes and capacity status
 // (total encoded length *zrun); zero the payload padding of img (nullable).
 void launch_zfinal(const Launch &L, DevStats *st, const uint64_t *zrun, uint8_t *img, uint64_t capacity);

@@ -11,19 +11,22 @@
 // capped at min(258, 4096 - p); a match iff len >= 4; the parse is greedy
 // from p = 0.
 //
-// One warp per unit.  The sequential parse is turned into parallel steps:
+// One warp per unit:
 //  1. hash candidates: 128 rounds of 32 consecutive positions; inside a round
 //     __match_any_sync resolves equal hashes (the nearest lower lane wins),
-//     across rounds a per-warp head table in shared memory;
-//  2. match lengths: lane l owns positions [128 l, 128 l + 128) and walks
-//     them backwards: len(x) = min(cap(x), 1 + len(x + 1)) when x + 1 has the
-//     same match distance (the same run, one byte shorter), else a direct
-//     compare;
-//  3. greedy parse: next(x) = x + (len >= 4 ? len : 1); each lane computes,
-//     backwards, where a parse entering its segment at x leaves it; lane 0
-//     chains the 32 segment entries; each lane then walks its own segment;
-//  4. bit offsets by a warp scan of each lane's token bits; tokens are OR-ed
-//     into a shared-memory bit buffer (a token is <= 31 bits, <= 2 words).
+//     across rounds a per-warp head table in shared memory.  A candidate whose
+//     4 bytes match is "verified": exactly the positions where len >= 4, i.e.
+//     where the greedy parse, if it stops there, emits a match.  Ballots give
+//     a verified-candidate bitmap and a ">= 144" byte bitmap (9-bit literals).
+//  2. greedy parse, warp-uniform: jump to the next verified candidate at or
+//     after x (bitmap search), measure its match with all 32 lanes (8 bytes
+//     each, first difference by a min-reduction), record it, x += len.  Match
+//     lengths are computed only where the parse stops.
+//  3. size: covered bitmap of the matches; literal bits = 8 per uncovered
+//     position + 1 per uncovered byte >= 144; + the matches' bits.
+//  4. emit, run by run: a literal run's bytes in parallel (bit offset of byte
+//     i = 8 i + the >= 144 count before it, from prefix counts), then the
+//     match; tokens are OR-ed into a shared-memory bit buffer (<= 2 words).
 // Decoding is one warp per unit: lane 0 reads the symbols, writing literals
 // and recording matches; the warp then expands the matches in order, each by
 // all lanes (byte j of a match of distance d copies byte pos - d + j mod d,
@@ -36,17 +39,25 @@ namespace {
 constexpr uint32_t kZHashShift = 20;        // 12-bit hash
 constexpr uint32_t kZMaxMatch = 258;
 constexpr uint32_t kZMinMatch = 4;
-constexpr uint32_t kZEncWarps = 4;          // warps per encoder CTA (2 CTAs / SM)
+constexpr uint32_t kZEncWarps = 2;          // warps per encoder CTA
+constexpr uint32_t kZEncCtasPerSm = 5;      // 10 warps / SM (22.5 KB of shared memory each)
 constexpr uint32_t kZSeg = kSegBytes / 32;  // positions per lane segment
 constexpr uint16_t kNone = 0xFFFF;
 
 // Per-warp shared memory of the encoder.
+constexpr uint32_t kZWords = kSegBytes / 32;  // 32-position bitmap words per unit
+
 struct alignas(16) ZEncSmem {
-    uint32_t data[kSegBytes / 4 + 4];  // the unit (+ 16 zero bytes for 4-byte reads at the end)
-    uint16_t a[kSegBytes];             // hash heads -> segment exits -> output bits (as u32 words)
-    uint16_t d[kSegBytes];             // match distance of each position (0: no match)
-    uint16_t r[kSegBytes];             // match length of each position (capped)
-    uint16_t entry[32];
+    uint32_t data[kSegBytes / 4 + 4];  // the unit (+ 16 zero bytes for reads past the end)
+    uint16_t head[kSegBytes];          // hash heads; then the output bits (as u32 words)
+    uint16_t d[kSegBytes];             // distance of each position's verified candidate (0: none);
+                                       // then the parse's matches, x | (len - 4) << 12 | (dist - 1) << 20,
+                                       // as u32 words: match k overwrites d[2k], d[2k+1], entries of
+                                       // positions the parse has passed (match k starts at >= 4k)
+    uint32_t mcand[kZWords];           // bit p: position p has a verified candidate (a match >= 4)
+    uint32_t m144[kZWords];            // bit p: byte p >= 144 (its literal code is 9 bits)
+    uint32_t cov[kZWords];             // bit p: position p lies inside a match of the parse
+    uint32_t p144[kZWords + 1];        // prefix counts of m144 words
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -128,80 +139,55 @@ __device__ __forceinline__ void put_bits(uint32_t *out, uint32_t pos, uint32_t v
     if (sh + n > 32) atomicOr(out + w + 1, v >> (32 - sh));
 }
 
-// Unit u of the gather -> (region, page, byte offset, logical length), walked
-// in increasing u: one binary search at the start, then the slot / region
-// advance incrementally (as k_gather).
-struct ZCursor {
-    const GatherArgs &a;
-    uint64_t k_hi, k, kbase, gid;
-    uint32_t r;
-    DevRegion g;
-    __device__ ZCursor(const GatherArgs &a_, uint64_t k_hi_, uint64_t u0) : a(a_), k_hi(k_hi_) {
-        k = a.u2s[u0];
-        gid = a.gids[k];
-        r = region_of_page(a.regs, a.R, gid);
-        g = a.regs[r];
-        kbase = a.sunit[k];
-    }
-    // byte offset of unit u in its region and its logical length
-    __device__ void at(uint64_t u, const uint8_t **src, uint64_t *len) {
-        const uint64_t nxt = (k + 1 < k_hi) ? a.sunit[k + 1] : ~0ull;
-        if (u >= nxt) {
-            k = a.u2s[u];
-            kbase = a.sunit[k];
-            gid = a.gids[k];
-            if (r + 1 < a.R && gid >= a.regs[r + 1].page_base) {
-                r = region_of_page(a.regs, a.R, gid);
-                g = a.regs[r];
-            }
+// >= 144 bytes at positions [0, x) (x <= 4096).
+__device__ __forceinline__ uint32_t pre144(const ZEncSmem &sm, uint32_t x) {
+    const uint32_t w = x >> 5, b = x & 31;
+    return sm.p144[w] + (b ? __popc(sm.m144[w] & ((1u << b) - 1)) : 0u);
+}
+
+// Length of the match at y (distance dist, the first 4 bytes known equal),
+// capped at cap: the first differing byte, found by all lanes (8 bytes each).
+__device__ __forceinline__ uint32_t warp_match_len(const uint32_t *data, uint32_t y, uint32_t dist, uint32_t cap,
+                                                   uint32_t lane) {
+    for (uint32_t base = 0; base < cap; base += 256) {
+        const uint32_t off = base + 8 * lane;
+        uint32_t first = cap;  // this lane's first difference (or cap)
+        if (off < cap) {
+            const uint32_t a0 = ld32u(data, y + off), b0 = ld32u(data, y - dist + off);
+            const uint32_t a1 = ld32u(data, y + off + 4), b1 = ld32u(data, y - dist + off + 4);
+            uint32_t i = 8;
+            if (a0 != b0) i = (__ffs(a0 ^ b0) - 1) >> 3;
+            else if (a1 != b1) i = 4 + ((__ffs(a1 ^ b1) - 1) >> 3);
+            first = min(cap, off + i);
+            if (i == 8 && off + 8 < cap) first = cap;  // no difference here: a later lane decides
         }
-        const uint64_t i = gid - g.page_base;
-        const uint64_t off = (i << g.log2p) + ((u - kbase) << kSegLog2);
-        *src = g.base + off;
-        *len = g.bytes > off ? min((uint64_t)kSegBytes, g.bytes - off) : 0;
+        const uint32_t m = __reduce_min_sync(0xffffffffu, first);
+        if (m < cap || base + 256 >= cap) return m;
     }
-};
+    return cap;
+}
 
 // ---------------------------------------------------------------------------
 // Encoder: one warp per unit.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(32 * kZEncWarps, 2) k_zenc(GatherArgs a, uint64_t u_lo, uint64_t u_hi,
-                                                             uint8_t *stage, uint16_t *zsz) {
+__global__ void __launch_bounds__(32 * kZEncWarps, kZEncCtasPerSm) k_zenc(const uint8_t *raw, uint64_t n,
+                                                                          uint8_t *enc, uint16_t *zsz,
+                                                                          const DevStats *st) {
     extern __shared__ __align__(16) uint8_t zsm_raw[];
-    const DevStats *st = a.st;
-    if (st->status != kStOk) return;
-    const uint64_t U = min(u_hi, a.rb[1].units);
-    if (U <= u_lo) return;
+    if (st->status == kStCorrupt) return;
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     ZEncSmem &sm = reinterpret_cast<ZEncSmem *>(zsm_raw)[wid];
     const uint64_t nwarps = (uint64_t)gridDim.x * kZEncWarps;
-    const uint64_t nu = U - u_lo;
-    // consecutive units per warp task: one cursor search per task
-    const uint64_t upt = max((uint64_t)1, min((uint64_t)8, (nu + nwarps - 1) / nwarps));
-    const uint64_t ntask = (nu + upt - 1) / upt;
-    for (uint64_t t = (uint64_t)blockIdx.x * kZEncWarps + wid; t < ntask; t += nwarps) {
-        const uint64_t t0 = u_lo + t * upt, t1 = min(t0 + upt, U);
-        ZCursor cur(a, a.rb[1].k, t0);
-        for (uint64_t u = t0; u < t1; ++u) {
-            const uint8_t *src;
-            uint64_t len;
-            cur.at(u, &src, &len);
+    for (uint64_t u = (uint64_t)blockIdx.x * kZEncWarps + wid; u < n; u += nwarps) {
+        {
             __syncwarp();  // the previous unit's readers of the shared buffers are done
-            uint8_t *out_g = stage + ((u - u_lo) << kSegLog2);
-            // ---- load the unit (bytes past its logical length read as zero) ----
+            const uint4 *src = reinterpret_cast<const uint4 *>(raw + (u << kSegLog2));
+            uint8_t *out_g = enc + (u << kSegLog2);
+            // ---- load the unit ----
             uint32_t any = 0;
 #pragma unroll
             for (uint32_t i = 0; i < 8; ++i) {
-                const uint64_t o = 512ull * i + 16ull * lane;
-                uint4 v;
-                if (o + 16 <= len) {
-                    v = __ldg(reinterpret_cast<const uint4 *>(src + o));
-                } else {
-                    uint32_t w[4] = {0, 0, 0, 0};
-                    for (uint32_t b = 0; b < 16; ++b)
-                        if (o + b < len) w[b >> 2] |= (uint32_t)src[o + b] << (8 * (b & 3));
-                    v = make_uint4(w[0], w[1], w[2], w[3]);
-                }
+                const uint4 v = __ldcs(src + 32 * i + lane);  // read once: streaming
                 reinterpret_cast<uint4 *>(sm.data)[32 * i + lane] = v;
                 any |= v.x | v.y | v.z | v.w;
             }
@@ -210,26 +196,49 @@ __global__ void __launch_bounds__(32 * kZEncWarps, 2) k_zenc(GatherArgs a, uint6
                 if (lane == 0) zsz[u] = 0;  // zero unit: nothing to store
                 continue;
             }
-            // ---- 1. hash candidates ----
-            for (uint32_t i = lane; i < kSegBytes / 2; i += 32) reinterpret_cast<uint32_t *>(sm.a)[i] = 0xFFFFFFFFu;
+            // ---- 1. hash candidates, verified-candidate and >= 144 bitmaps ----
+            for (uint32_t i = lane; i < kSegBytes / 2; i += 32) reinterpret_cast<uint32_t *>(sm.head)[i] = 0xFFFFFFFFu;
             __syncwarp();
             uint32_t found = 0;
-            for (uint32_t c = 0; c < kSegBytes / 32; ++c) {
-                const uint32_t p = 32 * c + lane;
-                const bool valid = p + 4 <= kSegBytes;
-                const uint32_t v = valid ? ld32u(sm.data, p) : 0u;
-                const uint32_t h = (v * 2654435761u) >> kZHashShift;
-                const uint32_t key = valid ? h : (0x10000u + lane);
-                const uint32_t peers = __match_any_sync(0xffffffffu, key);
-                const uint32_t lower = peers & lanemask_lt();
-                uint32_t q = kNone;
-                if (valid) q = lower ? 32 * c + (31 - __clz(lower)) : sm.a[h];
-                __syncwarp();
-                if (valid && (peers >> lane) == 1u) sm.a[h] = (uint16_t)p;  // highest lane of its group
-                uint32_t dist = 0;
-                if (q != kNone && ld32u(sm.data, q) == v) dist = p - q;  // the 4 bytes match: len >= 4
-                sm.d[p] = (uint16_t)dist;
-                found |= dist;
+            // rounds of 32 positions, four at a time: the match_any and hash work of
+            // the four rounds is independent (its latency overlaps); only the
+            // table reads / writes run round by round
+            constexpr uint32_t kUnroll = 4;
+            for (uint32_t c0 = 0; c0 < kZWords; c0 += kUnroll) {
+                uint32_t v[kUnroll], h[kUnroll], peers[kUnroll], q[kUnroll];
+#pragma unroll
+                for (uint32_t j = 0; j < kUnroll; ++j) {
+                    const uint32_t p = 32 * (c0 + j) + lane;
+                    const bool valid = p + 4 <= kSegBytes;
+                    v[j] = ld32u(sm.data, p);
+                    h[j] = (v[j] * 2654435761u) >> kZHashShift;
+                    peers[j] = __match_any_sync(0xffffffffu, valid ? h[j] : 0x10000u + lane);
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < kUnroll; ++j) {
+                    const uint32_t p = 32 * (c0 + j) + lane;
+                    const bool valid = p + 4 <= kSegBytes;
+                    const uint32_t lower = peers[j] & lanemask_lt();
+                    q[j] = kNone;
+                    if (valid) q[j] = lower ? 32 * (c0 + j) + (31 - __clz(lower)) : sm.head[h[j]];
+                    __syncwarp();
+                    if (valid && (peers[j] >> lane) == 1u) sm.head[h[j]] = (uint16_t)p;  // highest lane of its group
+                    __syncwarp();
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < kUnroll; ++j) {
+                    const uint32_t p = 32 * (c0 + j) + lane;
+                    uint32_t dist = 0;
+                    if (q[j] != kNone && ld32u(sm.data, q[j]) == v[j]) dist = p - q[j];  // 4 bytes match: len >= 4
+                    sm.d[p] = (uint16_t)dist;
+                    found |= dist;
+                    const uint32_t mc = __ballot_sync(0xffffffffu, dist != 0);
+                    const uint32_t mb = __ballot_sync(0xffffffffu, (v[j] & 0xffu) >= 144);
+                    if (lane == 0) {
+                        sm.mcand[c0 + j] = mc;
+                        sm.m144[c0 + j] = mb;
+                    }
+                }
                 __syncwarp();
             }
             if (!__any_sync(0xffffffffu, found != 0)) {
@@ -240,80 +249,62 @@ __global__ void __launch_bounds__(32 * kZEncWarps, 2) k_zenc(GatherArgs a, uint6
                 if (lane == 0) zsz[u] = (uint16_t)kSegBytes;
                 continue;
             }
-            // ---- 2. match lengths, backwards over this lane's segment ----
-            const uint32_t lo = kZSeg * lane, hi = lo + kZSeg;
-            {
-                uint32_t prev_d = 0, prev_r = 0;
-                for (uint32_t x = hi; x-- > lo;) {
-                    const uint32_t dd = sm.d[x];
-                    uint32_t rr = 0;
-                    if (dd) {
-                        const uint32_t cap = min(kZMaxMatch, kSegBytes - x);
-                        if (x + 1 < hi && prev_d == dd) {
-                            rr = min(cap, 1 + prev_r);
-                        } else {
-                            uint32_t i = 4;  // the first 4 bytes match (candidate check)
-                            bool diff = false;
-                            while (i + 4 <= cap) {
-                                const uint32_t w1 = ld32u(sm.data, x + i), w2 = ld32u(sm.data, x - dd + i);
-                                if (w1 != w2) {
-                                    i += (__ffs(w1 ^ w2) - 1) >> 3;  // first differing byte
-                                    diff = true;
-                                    break;
-                                }
-                                i += 4;
-                            }
-                            if (!diff)
-                                while (i < cap && byte_at(sm.data, x + i) == byte_at(sm.data, x - dd + i)) ++i;
-                            rr = min(i, cap);
+            // ---- 2. greedy parse (warp-uniform) ----
+            uint32_t *match = reinterpret_cast<uint32_t *>(sm.d);
+            uint32_t nm = 0;
+            for (uint32_t x = 0; x < kSegBytes;) {
+                uint32_t w = x >> 5;
+                uint32_t m = sm.mcand[w] & (0xFFFFFFFFu << (x & 31));
+                if (!m) {
+                    bool hit = false;
+                    for (uint32_t b = w + 1; b < kZWords; b += 32) {
+                        const uint32_t wi = b + lane;
+                        const uint32_t mm = wi < kZWords ? sm.mcand[wi] : 0u;
+                        const uint32_t bal = __ballot_sync(0xffffffffu, mm != 0);
+                        if (bal) {
+                            const uint32_t f = __ffs(bal) - 1;
+                            w = b + f;
+                            m = __shfl_sync(0xffffffffu, mm, f);
+                            hit = true;
+                            break;
                         }
                     }
-                    sm.r[x] = (uint16_t)rr;
-                    prev_d = dd;
-                    prev_r = rr;
+                    if (!hit) break;
                 }
-            }
-            // ---- 3. where a parse entering this segment at x leaves it ----
-            for (uint32_t x = hi; x-- > lo;) {
-                const uint32_t rr = sm.r[x];
-                const uint32_t n = x + (rr >= kZMinMatch ? rr : 1);
-                sm.a[x] = (uint16_t)(n >= hi ? n : sm.a[n]);
+                const uint32_t y = 32 * w + (__ffs(m) - 1);
+                const uint32_t dist = sm.d[y];
+                const uint32_t L = warp_match_len(sm.data, y, dist, min(kZMaxMatch, kSegBytes - y), lane);
+                if (lane == 0) match[nm] = y | ((L - kZMinMatch) << 12) | ((dist - 1) << 20);
+                ++nm;
+                x = y + L;
             }
             __syncwarp();
-            if (lane == 0) {
-                uint32_t pos = 0;
-                for (uint32_t s = 0; s < 32; ++s) {
-                    if (pos < kZSeg * (s + 1)) {
-                        sm.entry[s] = (uint16_t)pos;
-                        pos = sm.a[pos];
-                    } else {
-                        sm.entry[s] = kNone;
-                    }
+            // ---- 3. size: covered positions, literal and match bits ----
+            for (uint32_t i = lane; i < kZWords; i += 32) sm.cov[i] = 0;
+            __syncwarp();
+            uint32_t mbits = 0;
+            for (uint32_t i = lane; i < nm; i += 32) {
+                const uint32_t mr = match[i];
+                const uint32_t x0 = mr & 0xfffu, x1 = x0 + ((mr >> 12) & 0xffu) + kZMinMatch;
+                mbits += match_nbits(x1 - x0, (mr >> 20) + 1);
+                for (uint32_t wq = x0 >> 5; wq <= (x1 - 1) >> 5; ++wq) {
+                    const uint32_t lo = max(x0, 32 * wq) - 32 * wq, hi = min(x1, 32 * wq + 32) - 32 * wq;
+                    const uint32_t bits = (hi == 32 ? 0xFFFFFFFFu : ((1u << hi) - 1)) & ~((1u << lo) - 1);
+                    atomicOr(&sm.cov[wq], bits);
                 }
             }
             __syncwarp();
-            const uint32_t e0 = sm.entry[lane];
-            // ---- 4. token bits: count, scan, emit ----
-            uint32_t nbits = 0;
-            if (e0 != kNone) {
-                for (uint32_t x = e0; x < hi;) {
-                    const uint32_t rr = sm.r[x];
-                    if (rr >= kZMinMatch) {
-                        nbits += match_nbits(rr, sm.d[x]);
-                        x += rr;
-                    } else {
-                        nbits += byte_at(sm.data, x) <= 143 ? 8 : 9;
-                        x += 1;
-                    }
-                }
-            }
-            uint32_t incl = nbits;
+            uint32_t nlit = 0, n144 = 0, c144[kZWords / 32];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= (uint32_t)o) incl += y;
+            for (uint32_t k = 0; k < kZWords / 32; ++k) {
+                const uint32_t wq = 4 * lane + k;  // lane owns 4 consecutive words (prefix counts below)
+                const uint32_t lit = ~sm.cov[wq];
+                nlit += __popc(lit);
+                n144 += __popc(lit & sm.m144[wq]);
+                c144[k] = __popc(sm.m144[wq]);
             }
-            const uint32_t total = 3 + __shfl_sync(0xffffffffu, incl, 31) + 7;  // header .. end of block
+            const uint32_t total = 3 + 8 * __reduce_add_sync(0xffffffffu, nlit) + __reduce_add_sync(0xffffffffu, n144) +
+                                   __reduce_add_sync(0xffffffffu, mbits) + 7;
             const uint32_t nbytes = (total + 7) / 8;
             if (nbytes >= kSegBytes) {
 #pragma unroll
@@ -322,26 +313,51 @@ __global__ void __launch_bounds__(32 * kZEncWarps, 2) k_zenc(GatherArgs a, uint6
                 if (lane == 0) zsz[u] = (uint16_t)kSegBytes;
                 continue;
             }
-            uint32_t *obits = reinterpret_cast<uint32_t *>(sm.a);  // exits are no longer needed
-            __syncwarp();
-            const uint32_t nwords = (nbytes + 15) / 16 * 4;       // whole 16-byte rows
+            {   // prefix counts of the >= 144 bitmap (4 words per lane, warp scan)
+                const uint32_t own = c144[0] + c144[1] + c144[2] + c144[3];
+                uint32_t inc = own;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= (uint32_t)o) inc += y;
+                }
+                uint32_t run = inc - own;
+#pragma unroll
+                for (uint32_t k = 0; k < kZWords / 32; ++k) {
+                    sm.p144[4 * lane + k] = run;
+                    run += c144[k];
+                }
+                if (lane == 31) sm.p144[kZWords] = run;
+            }
+            // ---- 4. emit, run by run ----
+            uint32_t *obits = reinterpret_cast<uint32_t *>(sm.head);  // the hash heads are no longer needed
+            const uint32_t nwords = (nbytes + 15) / 16 * 4;         // whole 16-byte rows
             for (uint32_t i = lane; i < nwords + 1; i += 32) obits[i] = 0;
             __syncwarp();
             if (lane == 0) put_bits(obits, 0, 3u, 3);  // BFINAL = 1, BTYPE = 01
-            if (e0 != kNone) {
-                uint32_t pos = 3 + incl - nbits;
-                for (uint32_t x = e0; x < hi;) {
-                    const uint32_t rr = sm.r[x];
-                    uint32_t v, n;
-                    if (rr >= kZMinMatch) {
-                        v = match_bits(rr, sm.d[x], &n);
-                        x += rr;
-                    } else {
-                        v = litlen_bits(byte_at(sm.data, x), &n);
-                        x += 1;
-                    }
-                    put_bits(obits, pos, v, n);
+            uint32_t pos = 3, s0 = 0;
+            for (uint32_t mi = 0; mi <= nm; ++mi) {
+                uint32_t x1 = kSegBytes, L = 0, dist = 0;
+                if (mi < nm) {
+                    const uint32_t mr = match[mi];
+                    x1 = mr & 0xfffu;
+                    L = ((mr >> 12) & 0xffu) + kZMinMatch;
+                    dist = (mr >> 20) + 1;
+                }
+                const uint32_t b144 = pre144(sm, s0);
+                for (uint32_t i = lane; i < x1 - s0; i += 32) {
+                    const uint32_t xp = s0 + i;
+                    uint32_t n;
+                    const uint32_t v = litlen_bits(byte_at(sm.data, xp), &n);
+                    put_bits(obits, pos + 8 * i + (pre144(sm, xp) - b144), v, n);
+                }
+                pos += 8 * (x1 - s0) + (pre144(sm, x1) - b144);
+                if (mi < nm) {
+                    uint32_t n;
+                    const uint32_t v = match_bits(L, dist, &n);
+                    if (lane == 0) put_bits(obits, pos, v, n);
                     pos += n;
+                    s0 = x1 + L;
                 }
             }
             // end of block: code 256 is seven zero bits
@@ -349,7 +365,6 @@ __global__ void __launch_bounds__(32 * kZEncWarps, 2) k_zenc(GatherArgs a, uint6
             for (uint32_t i = lane; i < nwords / 4; i += 32)
                 reinterpret_cast<uint4 *>(out_g)[i] = reinterpret_cast<const uint4 *>(obits)[i];
             if (lane == 0) zsz[u] = (uint16_t)nbytes;
-            __syncwarp();
         }
     }
 }
@@ -359,75 +374,66 @@ __global__ void __launch_bounds__(32 * kZEncWarps, 2) k_zenc(GatherArgs a, uint6
 // ---------------------------------------------------------------------------
 constexpr uint32_t kZScanPer = kZChunkUnits / 1024;  // units per thread
 
-__global__ void __launch_bounds__(1024) k_zscan_chunk(const uint16_t *zsz, uint64_t u_lo, uint64_t u_hi,
-                                                      const DevStats *st, const RangeTotals *rb, uint32_t *zloc,
-                                                      uint64_t *zblk, uint64_t *zrun, uint64_t *zrun_host) {
-    const uint64_t U = min(u_hi, rb[1].units);
+// Exclusive offsets of the n (<= kZChunkUnits) sizes of one chunk (zloc,
+// chunk-relative); *zbase = the running total before the chunk, *zrun and
+// *zrun_host (mapped, nullable) = after it.
+__global__ void __launch_bounds__(1024) k_zscan_chunk(const uint16_t *zsz, uint64_t n, uint32_t *zloc,
+                                                      uint64_t *zrun, uint64_t *zbase, uint64_t *zrun_host) {
     const uint64_t run = *zrun;
     uint32_t v[kZScanPer];
     uint64_t sum = 0;
 #pragma unroll
     for (uint32_t j = 0; j < kZScanPer; ++j) {
-        const uint64_t u = u_lo + threadIdx.x * kZScanPer + j;
-        v[j] = (u < U && st->status == kStOk) ? zsz[u] : 0u;
+        const uint64_t i = threadIdx.x * kZScanPer + j;
+        v[j] = i < n ? zsz[i] : 0u;
         sum += v[j];
     }
     uint64_t tot;
-    const uint64_t ex = block_excl_scan(sum, &tot);
-    // block start (kZScanBlock units = kZScanBlock / kZScanPer threads): its chunk-relative prefix
-    __shared__ uint64_t s_blk[kZChunkUnits / kZScanBlock];
-    constexpr uint32_t tpb = kZScanBlock / kZScanPer;
-    if (threadIdx.x % tpb == 0) s_blk[threadIdx.x / tpb] = ex;
-    __syncthreads();
-    const uint64_t b0 = s_blk[threadIdx.x / tpb];
-    uint64_t o = ex;
+    uint64_t o = block_excl_scan(sum, &tot);
 #pragma unroll
     for (uint32_t j = 0; j < kZScanPer; ++j) {
-        const uint64_t u = u_lo + threadIdx.x * kZScanPer + j;
-        if (u < U) zloc[u] = (uint32_t)(o - b0);
+        const uint64_t i = threadIdx.x * kZScanPer + j;
+        if (i < n) zloc[i] = (uint32_t)o;
         o += v[j];
     }
-    if (threadIdx.x % tpb == 0 && u_lo + threadIdx.x * kZScanPer < U)
-        zblk[(u_lo + threadIdx.x * kZScanPer) / kZScanBlock] = run + ex;
-    __syncthreads();
     if (threadIdx.x == 0) {
+        *zbase = run;
         *zrun = run + tot;
         if (zrun_host) *reinterpret_cast<volatile uint64_t *>(zrun_host) = run + tot;
     }
 }
 
 // ---------------------------------------------------------------------------
-// Pack: one warp per unit, byte-exact destination.
+// Pack: one warp per unit, byte-exact destination:
+// dst + (base ? *base : 0) + zloc[i]; limit != 0: a unit is written only if
+// poff + that offset + its size <= limit (device image capacity).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_zpack(const uint8_t *stage, const uint16_t *zsz, const uint32_t *zloc,
-                                               const uint64_t *zblk, uint64_t u_lo, uint64_t u_hi,
-                                               const DevStats *st, const RangeTotals *rb, uint8_t *dst, int rel,
-                                               uint64_t limit) {
-    if (st->status != kStOk) return;
-    const uint64_t U = min(u_hi, rb[1].units);
-    if (U <= u_lo) return;
+                                               uint64_t n, const uint64_t *base, uint8_t *dst, uint64_t limit,
+                                               const DevStats *st) {
+    if (st->status == kStCorrupt) return;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t base = rel ? zblk[u_lo / kZScanBlock] : 0;
-    for (uint64_t u = u_lo + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < U; u += nwarps) {
-        const uint32_t n = zsz[u];
-        if (!n) continue;
-        const uint64_t off = zblk[u / kZScanBlock] + zloc[u];
-        if (limit && st->poff + off + n > limit) continue;  // does not fit: CAPACITY at the end
-        const uint32_t *s = reinterpret_cast<const uint32_t *>(stage + ((u - u_lo) << kSegLog2));
-        uint8_t *d = dst + (off - base);
+    const uint64_t b = base ? *base : 0;
+    for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nwarps) {
+        const uint32_t sz = zsz[u];
+        if (!sz) continue;
+        const uint64_t off = b + zloc[u];
+        if (limit && st->poff + off + sz > limit) continue;  // does not fit: CAPACITY at the end
+        const uint32_t *s = reinterpret_cast<const uint32_t *>(stage + (u << kSegLog2));
+        uint8_t *d = dst + off;
         // head bytes up to a 4-byte boundary of the destination, whole words, tail bytes
         const uint32_t head = (uint32_t)((4 - (reinterpret_cast<uintptr_t>(d) & 3)) & 3);
-        const uint32_t h = min(head, n);
+        const uint32_t h = min(head, sz);
         if (lane < h) d[lane] = (uint8_t)(s[lane >> 2] >> (8 * (lane & 3)));
-        const uint32_t nw = (n - h) / 4;
+        const uint32_t nw = (sz - h) / 4;
         uint32_t *dw = reinterpret_cast<uint32_t *>(d + h);
         for (uint32_t i = lane; i < nw; i += 32) {
             const uint32_t p = h + 4 * i;  // source byte offset
             dw[i] = __funnelshift_r(s[p >> 2], s[(p >> 2) + 1], 8 * (p & 3));
         }
         const uint32_t t0 = h + 4 * nw;
-        if (t0 + lane < n) {
+        if (t0 + lane < sz) {
             const uint32_t p = t0 + lane;
             d[p] = (uint8_t)(s[p >> 2] >> (8 * (p & 3)));
         }
@@ -688,27 +694,24 @@ unsigned z_grid(const Launch &L, uint64_t units, uint32_t warps_per_block, uint3
 
 }  // namespace
 
-void launch_zenc(const Launch &L, const GatherArgs &a, uint64_t u_lo, uint64_t u_hi, uint8_t *stage, uint16_t *zsz) {
-    if (u_hi <= u_lo) return;
+void launch_zenc(const Launch &L, const uint8_t *raw, uint64_t n, uint8_t *enc, uint16_t *zsz, const DevStats *st) {
+    if (!n) return;
     const size_t smem = sizeof(ZEncSmem) * kZEncWarps;
     cudaFuncSetAttribute(k_zenc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_zenc<<<z_grid(L, u_hi - u_lo, kZEncWarps, 2), 32 * kZEncWarps, smem, L.stream>>>(a, u_lo, u_hi, stage, zsz);
+    k_zenc<<<z_grid(L, n, kZEncWarps, kZEncCtasPerSm), 32 * kZEncWarps, smem, L.stream>>>(raw, n, enc, zsz, st);
     ++*L.counter;
 }
 
-void launch_zscan_chunk(const Launch &L, const uint16_t *zsz, uint64_t u_lo, uint64_t u_hi, const DevStats *st,
-                        const RangeTotals *rb, uint32_t *zloc, uint64_t *zblk, uint64_t *zrun,
-                        uint64_t *zrun_host) {
-    k_zscan_chunk<<<1, 1024, 0, L.stream>>>(zsz, u_lo, u_hi, st, rb, zloc, zblk, zrun, zrun_host);
+void launch_zscan_chunk(const Launch &L, const uint16_t *zsz, uint64_t n, uint32_t *zloc, uint64_t *zrun,
+                        uint64_t *zbase, uint64_t *zrun_host) {
+    k_zscan_chunk<<<1, 1024, 0, L.stream>>>(zsz, n, zloc, zrun, zbase, zrun_host);
     ++*L.counter;
 }
 
-void launch_zpack(const Launch &L, const uint8_t *stage, const uint16_t *zsz, const uint32_t *zloc,
-                  const uint64_t *zblk, uint64_t u_lo, uint64_t u_hi, const DevStats *st, const RangeTotals *rb,
-                  uint8_t *dst, int rel, uint64_t limit) {
-    if (u_hi <= u_lo) return;
-    k_zpack<<<z_grid(L, u_hi - u_lo, 8, 8), 256, 0, L.stream>>>(stage, zsz, zloc, zblk, u_lo, u_hi, st, rb, dst,
-                                                               rel, limit);
+void launch_zpack(const Launch &L, const uint8_t *stage, const uint16_t *zsz, const uint32_t *zloc, uint64_t n,
+                  const uint64_t *base, uint8_t *dst, uint64_t limit, const DevStats *st) {
+    if (!n) return;
+    k_zpack<<<z_grid(L, n, 8, 8), 256, 0, L.stream>>>(stage, zsz, zloc, n, base, dst, limit, st);
     ++*L.counter;
 }
 

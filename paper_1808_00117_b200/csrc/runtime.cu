@@ -306,6 +306,8 @@ struct crum_ctx {
     uint64_t *h_zrun = nullptr;    // pinned, mapped: running length after each chunk ([0] = 0)
     uint64_t *dh_zrun = nullptr;   // device address of h_zrun
     uint8_t *d_zstage = nullptr;   // one chunk of encoded units (raw layout, kZChunkUnits x 4 KiB)
+    uint8_t *d_zraw = nullptr;     // one chunk of gathered (not yet encoded) units
+    uint64_t *d_zbase = nullptr;   // running encoded length before the current chunk
     // restore staging kept across calls (grow-only): decoded / verified payload, encoded payload
     uint8_t *d_rtmp = nullptr;
     uint64_t rtmp_cap = 0;
@@ -720,8 +722,11 @@ int ensure_z(crum_ctx *c, uint64_t units) {
         (st = dev_alloc(c, &c->d_zblk, 8 * (units / kZScanBlock + 2))))
         return st;
     if (!c->d_zrun && (st = dev_alloc(c, &c->d_zrun, 8))) return st;
-    if (!c->d_zstage && (st = dev_alloc(c, &c->d_zstage, (uint64_t)kZChunkUnits << kSegLog2))) return st;
-    const uint64_t nrun = units / kZChunkUnits + 2;
+    if (!c->d_zbase && (st = dev_alloc(c, &c->d_zbase, 8))) return st;
+    // + slack: the pack kernel's funnel shift reads one word past a unit
+    if (!c->d_zstage && (st = dev_alloc(c, &c->d_zstage, ((uint64_t)kZChunkUnits << kSegLog2) + 256))) return st;
+    if (!c->d_zraw && (st = dev_alloc(c, &c->d_zraw, (uint64_t)kZChunkUnits << kSegLog2))) return st;
+    const uint64_t nrun = units / kZChunkUnits + kMaxRanges + 2;  // chunks: per range, then by size
     void *dp = nullptr;
     if (cudaHostAlloc(reinterpret_cast<void **>(&c->h_zrun), 8 * nrun, cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer(&dp, c->h_zrun, 0) != cudaSuccess) {
@@ -1220,7 +1225,9 @@ int crum_destroy(crum_ctx *c) {
     dev_free(c->d_zblk);
     if (c->h_zrun) cudaFreeHost(c->h_zrun);
     dev_free(c->d_zrun);
+    dev_free(c->d_zbase);
     dev_free(c->d_zstage);
+    dev_free(c->d_zraw);
     dev_free(c->d_st);
     dev_free(c->d_meta);
     for (int i = 0; i < kRing; ++i) dev_free(c->d_ring[i]);
@@ -1769,16 +1776,17 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
     return CRUM_OK;
 }
 
-// Compressed gather (readings Z2-Z3).  Detect +
-// compact every page (one range; the host reads the unit count from mapped
-// memory: the one round trip), then per chunk of kZChunkUnits units on the
-// caller's stream: encode (k_zenc) -> chunk scan of the sizes (k_zscan_chunk,
-// running total mirrored into mapped memory) -> pack.  A device image gets
-// the packed bytes in place; a pinned image gets them through a ring slot and
-// one D2H copy per chunk on the copy stream, overlapping the next chunk's
-// encode.  Then the image fields (k_zfinal), the metadata CRC + tail +
-// header (stored through the pinned image's mapped address), and -- only once
-// the image is known to fit -- the commit of every listed page.
+// Compressed gather (readings Z2-Z3).  Chunks of
+// <= kZChunkUnits units (16 MiB) run on the gather stream: k_gather of the
+// chunk's listed pages into a raw staging buffer (no commit), encode, chunk
+// scan of the sizes (running total mirrored into mapped memory), pack.  A
+// pinned image takes the range pipeline of the plain path (detect + compact
+// of range c on the caller's stream while chunks of range c - 1 encode and
+// copy); each chunk's packed bytes go through a ring slot and one D2H copy.
+// A device image compacts everything first and packs in place.  Then the
+// image fields (k_zfinal), the metadata CRC + tail + header (through the
+// pinned image's mapped address), and -- only once the image is known to
+// fit -- the commit of every listed page, range by range.
 int gather_z(crum_ctx *c, cudaStream_t s, uint8_t *dev_img, crum_image *himg, uint64_t capacity, bool full,
              bool timing, crum_report *rep) {
     int st;
@@ -1792,25 +1800,37 @@ int gather_z(crum_ctx *c, cudaStream_t s, uint8_t *dev_img, crum_image *himg, ui
     }
     const uint64_t poff = payload_offset_for(c->regs.size());
     uint8_t *head = capacity >= poff ? img : nullptr;
-    Launch L = launch_of(c, s);
+    // a host image streams range by range; a device image is one range
+    const uint32_t nr = himg ? (uint32_t)c->ranges.size() : 1;
+    auto range_of = [&](uint32_t ci) -> const Range & { return himg ? c->ranges[ci] : c->all; };
+    Launch G = launch_of(c, c->gstream);
     CK(cudaEventRecord(c->ev_t[0], s));
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
     CK(cudaMemsetAsync(c->d_zrun, 0, 8, s));
-    enqueue_detect(c, s, c->all, full);
-    CK(cudaEventRecord(c->ev_t[1], s));
-    enqueue_compact(c, s, compact_args(c, c->all, 0, true, true, full, UINT64_MAX, head));
-    CK_LAUNCH();
-    CK(cudaEventRecord(c->ev_t[2], s));
-    CK(cudaEventSynchronize(c->ev_t[2]));  // h_rb[1] written by the compaction (mapped)
-    const uint64_t U = c->h_rb[1].units;
+    uint32_t enq = 0;
+    auto enqueue_range = [&](uint32_t ci) -> int {
+        enqueue_detect(c, s, range_of(ci), full);
+        enqueue_compact(c, s, compact_args(c, range_of(ci), ci, ci == 0, ci + 1 == nr, full, UINT64_MAX, head));
+        CK_LAUNCH();
+        CK(cudaEventRecord(c->ev_range[ci], s));  // h_rb[ci + 1] written by the kernel (mapped)
+        if (ci + 1 == nr) {
+            CK(cudaEventRecord(c->ev_t[1], s));
+            if (!himg) CK(cudaEventRecord(c->ev_t[2], s));  // device image: encoding starts here
+        }
+        return CRUM_OK;
+    };
+    while (enq < nr && enq < 2)
+        if ((st = enqueue_range(enq++))) return st;
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(c->gstream, c->ev_fork, 0));  // the zrun / rb resets
     c->h_zrun[0] = 0;
-    const GatherArgs ga = gather_args(c, 0, nullptr, 0, false, 0, UINT64_MAX);
-    const uint64_t nch = (U + kZChunkUnits - 1) / kZChunkUnits;
+    c->h_rb[0] = RangeTotals{0, 0};
+    uint64_t k = 0;  // chunk index
     bool overflow = false, copy_started = false;
-    auto copy_chunk = [&](uint64_t k) -> int {  // host image: chunk k's packed bytes -> the image
-        const int slot = (int)(k % kRing);
+    auto copy_chunk = [&](uint64_t kk) -> int {  // host image: chunk kk's packed bytes -> the image
+        const int slot = (int)(kk % kRing);
         CK(cudaEventSynchronize(c->ev_gather[slot]));
-        const uint64_t o0 = c->h_zrun[k], o1 = c->h_zrun[k + 1];
+        const uint64_t o0 = c->h_zrun[kk], o1 = c->h_zrun[kk + 1];
         if (poff + o1 > himg->cap) overflow = true;  // CAPACITY: stop copying, keep encoding for the size
         CK(cudaStreamWaitEvent(c->copy, c->ev_gather[slot], 0));
         if (!overflow && o1 > o0) {
@@ -1823,45 +1843,59 @@ int gather_z(crum_ctx *c, cudaStream_t s, uint8_t *dev_img, crum_image *himg, ui
         CK(cudaEventRecord(c->ev_copy[slot], c->copy));
         return CRUM_OK;
     };
-    for (uint64_t k = 0; k < nch; ++k) {
-        const uint64_t u0 = k * kZChunkUnits, u1 = std::min(U, u0 + kZChunkUnits);
-        launch_zenc(L, ga, u0, u1, c->d_zstage, c->d_zsz);
-        launch_zscan_chunk(L, c->d_zsz, u0, u1, c->d_st, c->d_rb, c->d_zloc, c->d_zblk, c->d_zrun,
-                           c->dh_zrun + k + 1);
-        if (himg) {
+    for (uint32_t ci = 0; ci < nr; ++ci) {
+        while (enq < nr && enq <= ci + 2)
+            if ((st = enqueue_range(enq++))) return st;
+        CK(cudaEventSynchronize(c->ev_range[ci]));
+        const uint64_t U0 = c->h_rb[ci].units, U1 = c->h_rb[ci + 1].units;
+        if (U1 > U0) CK(cudaStreamWaitEvent(c->gstream, c->ev_range[ci], 0));
+        for (uint64_t u0 = U0; u0 < U1; u0 += kZChunkUnits, ++k) {
+            const uint64_t u1 = std::min(U1, u0 + kZChunkUnits), n = u1 - u0;
             const int slot = (int)(k % kRing);
-            if (k >= (uint64_t)kRing) CK(cudaStreamWaitEvent(s, c->ev_copy[slot], 0));
-            launch_zpack(L, c->d_zstage, c->d_zsz, c->d_zloc, c->d_zblk, u0, u1, c->d_st, c->d_rb, c->d_ring[slot], 1,
-                         0);
-            CK_LAUNCH();
-            CK(cudaEventRecord(c->ev_gather[slot], s));
-            if (k && (st = copy_chunk(k - 1))) return st;
-        } else {
-            launch_zpack(L, c->d_zstage, c->d_zsz, c->d_zloc, c->d_zblk, u0, u1, c->d_st, c->d_rb, img + poff, 0,
-                         capacity);
-            CK_LAUNCH();
+            GatherArgs ga = gather_args(c, ci, c->d_zraw, u0, false, u0, u1);
+            ga.no_commit = 1;
+            launch_gather(G, ga, n);
+            launch_zenc(G, c->d_zraw, n, c->d_zstage, c->d_zsz + u0, c->d_st);
+            launch_zscan_chunk(G, c->d_zsz + u0, n, c->d_zloc, c->d_zrun, c->d_zbase, c->dh_zrun + k + 1);
+            if (himg) {
+                if (k >= (uint64_t)kRing) CK(cudaStreamWaitEvent(c->gstream, c->ev_copy[slot], 0));
+                launch_zpack(G, c->d_zstage, c->d_zsz + u0, c->d_zloc, n, nullptr, c->d_ring[slot], 0, c->d_st);
+                CK_LAUNCH();
+                CK(cudaEventRecord(c->ev_gather[slot], c->gstream));
+                if (k && (st = copy_chunk(k - 1))) return st;
+            } else {
+                launch_zpack(G, c->d_zstage, c->d_zsz + u0, c->d_zloc, n, c->d_zbase, img + poff, capacity, c->d_st);
+                CK_LAUNCH();
+            }
         }
     }
-    if (himg && nch && (st = copy_chunk(nch - 1))) return st;
-    CK(cudaEventRecord(c->ev_t[3], s));
+    if (himg && k && (st = copy_chunk(k - 1))) return st;
+    CK(cudaEventRecord(c->ev_t[3], c->gstream));
     if (himg && !copy_started) CK(cudaEventRecord(c->ev_t[4], c->copy));
-    launch_zfinal(L, c->d_st, c->d_zrun, head, capacity);
-    launch_crc_meta(L, crc_args(c, head, nullptr), crc_max_len(c));
-    // commit every listed page (a no-op on the device when the image did not fit)
-    if (U) launch_gather(L, ga, U);
+    // image fields, CRC + tail + header, then the commit -- after the last range
+    CK(cudaStreamWaitEvent(c->gstream, c->ev_range[nr - 1], 0));
+    launch_zfinal(G, c->d_st, c->d_zrun, head, capacity);
+    launch_crc_meta(G, crc_args(c, head, nullptr), crc_max_len(c));
+    for (uint32_t ci = 0; ci < nr; ++ci) {
+        const uint64_t U0 = c->h_rb[ci].units, U1 = c->h_rb[ci + 1].units;
+        if (U1 > U0) launch_gather(G, gather_args(c, ci, nullptr, 0, false, U0, U1), U1 - U0);  // commit only
+    }
     CK_LAUNCH();
+    CK(cudaEventRecord(c->ev_join, c->gstream));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     if (himg) {
         CK(cudaEventRecord(c->ev_t[5], c->copy));
         CK(cudaStreamWaitEvent(s, c->ev_t[5], 0));
+    } else {
+        CK(cudaEventRecord(c->ev_t[4], s));  // device image: e4 = end of the call
     }
-    if (!himg) CK(cudaEventRecord(c->ev_t[4], s));  // device image: e4 = end of the call
     CK(cudaEventRecord(c->ev_done, s));
     c->last_kind = himg ? kLastHostGather : kLastDevGather;
     c->last_timed = timing;
     c->last_path = CRUM_PATH_COMPRESSED;
     if (!himg && !rep) return CRUM_OK;  // stream-asynchronous (capacity >= worst case)
-    CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpy(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost));
     const DevStats h = *c->h_st;
     if (himg && h.status == kStOk) himg->len = h.image_bytes;
     if (rep) {

@@ -137,3 +137,38 @@ def c4_region_sizes(S: int, n_box: int = 4096, levels: int = 7):
     small = np.exp(lo + u * (hi - lo))
     small = (np.ceil(small / 256) * 256).astype(np.int64).tolist()
     return big, small
+
+
+# --------------------------------------------------------------------------
+# Structured content (bench --content hpgmg; compressed-image measurements)
+HPGMG_KINDS = ("smooth u", "smooth f", "alpha", "beta_x", "beta_y", "beta_z", "Dinv", "temporary")
+
+
+def hpgmg_box_kinds(nbox: int, r: int) -> np.ndarray:
+    """Kind (index into HPGMG_KINDS) of every 32 KiB box of fp64 values of
+    region r: HPGMG-FV keeps 8 vectors per level -- two smooth fields, four
+    constant coefficients, the constant diagonal inverse, one cleared
+    temporary (PAPER.md:704-751 describes the application; the kinds are a
+    proposal, the paper prints no data).  Box b of region r has kind
+    (b + r) % 8, so every region holds every kind."""
+    return ((np.arange(nbox) + r) % 8).astype(np.int64)
+
+
+def hpgmg_fill(buf: np.ndarray, r: int) -> None:
+    """Host version of bench.hpgmg_fill_device (values agree up to the last
+    bits of sin(); used for the CPU baseline's sample only)."""
+    n = buf.nbytes // 8
+    nbox = n // 4096
+    if nbox == 0:
+        return
+    F = buf[:nbox * 4096 * 8].view(np.float64).reshape(nbox, 4096)
+    kinds = hpgmg_box_kinds(nbox, r)
+    x = np.arange(4096, dtype=np.float64)
+    for b in range(nbox):
+        k = kinds[b]
+        if k <= 1:
+            F[b] = np.sin(x * (0.001 + 0.0005 * (b % 7)) + b) * (1 + (b % 3))
+        else:
+            F[b] = {2: 1.0, 3: 1.0, 4: 1.0, 5: 1.0, 6: 1.0 / 6.0, 7: 0.0}[int(k)]
+        F[b, :256] = 0
+        F[b, -256:] = 0
