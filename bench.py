@@ -75,6 +75,9 @@ def parse():
                     help="gloo: test the multi-rank path with several ranks sharing fewer GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--restore-full", action="store_true",
+                    help="also time a FULL checkpoint (every page) into a pinned image and its restore onto the "
+                         "live regions (SURVEY.md 8(d) C3 (a): full checkpoint + full restore)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     a = ap.parse_args()
     if a.dirty is None:
@@ -878,6 +881,26 @@ def main():
                        "link_frac": round(rr["image_bytes"] / tr / 1e9 / link_peak, 4),
                        "note": "link_frac against the run's pinned D2H probe (H2D measured 55.6 vs D2H 55.2 GB/s "
                                "on the pool's boxes, profiles/r01/probe_box.json)"}
+    if args.restore_full:
+        # C3 (a): a FULL checkpoint (every page, CRUM_FULL) and its restore,
+        # both through the pinned image (host link in both directions)
+        fimg = ctx.new_image(ctx.image_required_bytes())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fr = ctx.checkpoint_gather(fimg, stream=stream, flags=crum.FULL)
+        tg = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rr2 = ctx.restore_scatter(fimg, stream=stream)
+        trf = time.perf_counter() - t0
+        line["restore_full"] = {"image_bytes": fr["image_bytes"], "checkpoint_GBs": round(F / tg / 1e9, 3),
+                                "checkpoint_ms": round(tg * 1e3, 3), "restore_GBs": round(F / trf / 1e9, 3),
+                                "restore_ms": round(trf * 1e3, 3),
+                                "checkpoint_link_frac": round(fr["image_bytes"] / tg / 1e9 / link_peak, 4),
+                                "restore_link_frac": round(rr2["image_bytes"] / trf / 1e9 / link_peak, 4),
+                                "note": "CRUM_FULL gather into a pinned image and crum_restore_scatter of it onto "
+                                        "the live regions, host wall clock, one call each"}
+        fimg.destroy()
     # lazy restore (sec. 4.2 read-fault heuristic): per-fault latency for
     # windows of 1, 2, 4, ... pages of region 1
     torch.cuda.synchronize()
@@ -906,6 +929,13 @@ def main():
         img2 = ctx.new_image(cap)
         tmpd = tempfile.mkdtemp(prefix="crum_bench_")
         pause_ms = []
+        # O_DIRECT + fsync (storage, not the page cache) where the filesystem allows it
+        direct = True
+        try:
+            img.persist(os.path.join(tmpd, "probe.crum"), fsync=True, direct=True)
+            img.persist_wait()
+        except crum.CrumError:
+            direct = False
         try:
             for i in range(4):
                 epoch += 1
@@ -916,11 +946,11 @@ def main():
                 t0 = time.perf_counter()
                 ctx.checkpoint_gather(im, stream=stream, flags=gflags)
                 pause_ms.append((time.perf_counter() - t0) * 1e3)
-                im.persist(os.path.join(tmpd, f"r{rank}_{i % 2}.crum"), fsync=True)
+                im.persist(os.path.join(tmpd, f"r{rank}_{i % 2}.crum"), fsync=True, direct=direct)
             img.persist_wait()
             img2.persist_wait()
             t0 = time.perf_counter()
-            img2.persist(os.path.join(tmpd, f"r{rank}_w.crum"), fsync=True)
+            img2.persist(os.path.join(tmpd, f"r{rank}_w.crum"), fsync=True, direct=direct)
             img2.persist_wait()
             w_ms = (time.perf_counter() - t0) * 1e3
         finally:
@@ -930,7 +960,9 @@ def main():
                           "image_bytes": img2.length,
                           "note": "gather wall time with the previous image's writer in flight (two alternating "
                                   "pinned images); persist = one image written and fsync'd to "
-                                  "tempfile.gettempdir()"}
+                                  "tempfile.gettempdir()" + (" with O_DIRECT (no page-cache copy)" if direct else
+                                                             " (buffered: the filesystem refused O_DIRECT)"),
+                          "o_direct": direct}
         img2.destroy()
     # ---- cpu_baseline: the oracle on a bounded sample, rank 0 at N=1 only ----
     if not args.no_cpu_baseline and world == 1:

@@ -301,7 +301,11 @@ CRUM_API int crum_device_numa_node(int device, int *node_out);
  * "ConcurrentCheckpoint"), so applications alternate two images; restoring
  * from it is allowed (the writer only reads it).
  *   crum_image_persist: start writing img[0, len) to path (created/truncated);
- *     flags: CRUM_PERSIST_FSYNC (fsync before completion).  Errors: INVAL, BUSY.
+ *     flags: CRUM_PERSIST_FSYNC (fsync before completion); CRUM_PERSIST_DIRECT
+ *     (O_DIRECT: the writer's bytes go from the pinned image to the device
+ *     without a page-cache copy -- whole 4 KiB blocks, the file then
+ *     truncated to the image length; a filesystem without O_DIRECT support
+ *     makes the writer fail with CRUM_E_IO).  Errors: INVAL, BUSY.
  *   crum_image_persist_wait: wait for the writer; returns its outcome (OK or
  *     CRUM_E_IO); OK if none is in flight.
  *   crum_image_persist_busy: *busy_out = 1 while the writer runs.
@@ -309,7 +313,7 @@ CRUM_API int crum_device_numa_node(int device, int *node_out);
  *     storage).  Errors: INVAL, IO, NOMEM.
  * crum_image_destroy waits for an in-flight writer first.
  * ------------------------------------------------------------------------- */
-enum { CRUM_PERSIST_FSYNC = 1u << 0 };
+enum { CRUM_PERSIST_FSYNC = 1u << 0, CRUM_PERSIST_DIRECT = 1u << 1 };
 CRUM_API int crum_image_persist(crum_image *img, const char *path, uint32_t flags);
 CRUM_API int crum_image_persist_wait(crum_image *img);
 CRUM_API int crum_image_persist_busy(const crum_image *img, int *busy_out);

@@ -33,7 +33,7 @@ MODE_TRACKED = 2
 CFG_TIMING, CFG_NO_GRAPH, CFG_FUSED, CFG_TRACE = 1, 2, 4, 8
 NUMA_AUTO, NUMA_DEFAULT = -1, -2
 PATH_FUSED, PATH_COMPRESSED = 1, 2
-PERSIST_FSYNC = 1
+PERSIST_FSYNC, PERSIST_DIRECT = 1, 2
 EXPORT_FORCE, EXPORT_HASHES, EXPORT_MIRROR = 0, 1, 2
 ALL_PAGES = (1 << 64) - 1
 
@@ -219,10 +219,11 @@ class Image:
         return self.view().tobytes()
 
     # -- forked checkpoint (sec. 3.3): persist on a writer thread
-    def persist(self, path: str, fsync: bool = False):
-        """Start writing the image to `path`; returns at once."""
-        _check(_L.crum_image_persist(self._h, os.fsencode(path), PERSIST_FSYNC if fsync else 0),
-               "crum_image_persist")
+    def persist(self, path: str, fsync: bool = False, direct: bool = False):
+        """Start writing the image to `path`; returns at once.  direct: O_DIRECT
+        (no page-cache copy); fsync: fsync before completion."""
+        _check(_L.crum_image_persist(self._h, os.fsencode(path), (PERSIST_FSYNC if fsync else 0) |
+                                     (PERSIST_DIRECT if direct else 0)), "crum_image_persist")
 
     def persist_wait(self):
         """Wait for the writer; raises CrumError(CRUM_E_IO) if it failed."""

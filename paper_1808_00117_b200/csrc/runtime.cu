@@ -238,6 +238,7 @@ struct crum_ctx {
         uint64_t cap = 0;
         uint32_t flags = 0;
         uint64_t used = 0;                    // LRU stamp
+        bool fused = false;                   // the captured sequence is the single-pass kernel
     };
     static constexpr int kGraphs = 4;         // e.g. two alternating images x {device, host}
     GraphEntry graphs[kGraphs];
@@ -779,17 +780,6 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // Detect marks changed pages with kFlagTag; compaction (and the debug export)
 // clear the marks they consume, so the flags are zero between calls.
 constexpr uint8_t kFlagTag = 1;
-
-// Next per-checkpoint tag of the single-pass kernel's look-back status words
-// (1..255); on wrap the status array is cleared.
-int next_tag(crum_ctx *c, cudaStream_t s) {
-    if (c->tag == 255 || c->tag == 0) {
-        if (c->d_status) CK(cudaMemsetAsync(c->d_status, 0, 8 * (c->n_tiles + 1), s));
-        c->tag = 0;
-    }
-    ++c->tag;
-    return CRUM_OK;
-}
 
 void enqueue_detect(crum_ctx *c, cudaStream_t s, const Range &rg, bool full) {
     Launch L = launch_of(c, s);
@@ -1604,7 +1594,7 @@ bool write_all(int fd, const uint8_t *p, uint64_t n) {
 }  // namespace
 
 int crum_image_persist(crum_image *img, const char *path, uint32_t flags) {
-    if (!img || !path || (flags & ~(uint32_t)CRUM_PERSIST_FSYNC)) {
+    if (!img || !path || (flags & ~(uint32_t)(CRUM_PERSIST_FSYNC | CRUM_PERSIST_DIRECT))) {
         set_detail("null image/path or bad flags");
         return CRUM_E_INVAL;
     }
@@ -1618,9 +1608,28 @@ int crum_image_persist(crum_image *img, const char *path, uint32_t flags) {
     img->error.clear();
     const std::string dst(path);
     img->writer = std::thread([img, dst, flags]() {
-        const int fd = ::open(dst.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+        const bool direct = flags & CRUM_PERSIST_DIRECT;
+        const int fd = ::open(dst.c_str(), O_WRONLY | O_CREAT | O_TRUNC | (direct ? O_DIRECT : 0), 0644);
         bool ok = fd >= 0;
-        if (ok) ok = write_all(fd, img->host, img->len);
+        if (ok && !direct) ok = write_all(fd, img->host, img->len);
+        if (ok && direct) {
+            // whole 4 KiB blocks straight from the (page-aligned) pinned image;
+            // the last partial block through an aligned bounce block
+            constexpr uint64_t kBlk = 4096;
+            const uint64_t whole = img->len / kBlk * kBlk, rest = img->len - whole;
+            ok = write_all(fd, img->host, whole);
+            if (ok && rest) {
+                void *b = nullptr;
+                ok = posix_memalign(&b, kBlk, kBlk) == 0;
+                if (ok) {
+                    memset(b, 0, kBlk);
+                    memcpy(b, img->host + whole, rest);
+                    ok = write_all(fd, static_cast<const uint8_t *>(b), kBlk);
+                    free(b);
+                }
+            }
+            if (ok) ok = ::ftruncate(fd, (off_t)img->len) == 0;
+        }
         if (ok && (flags & CRUM_PERSIST_FSYNC)) ok = ::fsync(fd) == 0;
         if (fd >= 0 && ::close(fd) != 0) ok = false;
         if (!ok) {
@@ -1693,6 +1702,58 @@ namespace {
 // (+ tail, header).
 // Timing / completion events are recorded as external event nodes so they
 // also fire when the sequence runs as a captured graph.
+// The single-pass kernel (detect + compaction + gather + commit, then the
+// metadata CRC) runs when the context asked for it (CRUM_CFG_FUSED) and, by
+// default, for footprints up to kFusedAutoBytes: there the multi-kernel
+// sequence is latency-bound (C1: detect -> compaction -> CRC, each a few
+// dependent round trips) and one launch removes two of them.  Eligible: all
+// regions COMPARE with pages <= 64 KiB, an incremental gather, and an image
+// that holds the worst case (no capacity failure can occur mid-kernel).
+constexpr uint64_t kFusedAutoBytes = 64ull << 20;
+
+bool use_fused(const crum_ctx *c, bool full, uint64_t capacity, uint64_t worst) {
+    return c->fused_ok && !full && capacity >= worst && (c->fused_cfg || c->F <= kFusedAutoBytes);
+}
+
+// Stream-ordered and graph-capturable: the scratch, per-region counts and
+// look-back status words are cleared before every launch (status words carry
+// a constant tag).
+int enqueue_fused(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, bool timing, bool capturing = false) {
+    const unsigned evf = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[0], s, evf));
+    CK(cudaMemsetAsync(c->d_fs, 0, sizeof(FusedScratch), s));
+    CK(cudaMemsetAsync(c->d_reg_nd, 0, 4 * c->regs.size(), s));
+    CK(cudaMemsetAsync(c->d_status, 0, 8 * (c->n_tiles + 1), s));
+    FusedArgs fa{};
+    fa.regs = c->d_regs;
+    fa.R = (uint32_t)c->regs.size();
+    fa.tag = 1;
+    fa.tile_base = c->d_tile_base;
+    fa.n_tiles = c->n_tiles;
+    fa.status = c->d_status;
+    fa.fs = c->d_fs;
+    fa.force = c->d_force;
+    fa.img = img;
+    fa.poff = payload_offset_for(c->regs.size());
+    fa.gids = c->d_gids;
+    fa.sunit = c->d_sunit;
+    fa.lids = c->d_lids;
+    fa.reg_nd = c->d_reg_nd;
+    fa.rs = c->d_rs;
+    fa.st = c->d_st;
+    fa.capacity = capacity;
+    Launch L = launch_of(c, s);
+    launch_fused_compare(L, fa, c->sms * c->fused_bps);
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[1], s, evf));
+    CrcArgs cra = crc_args(c, img, nullptr);
+    cra.st_host = nullptr;
+    launch_crc_meta(L, cra, crc_max_len(c));
+    CK_LAUNCH();
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[4], s, evf));
+    CK(cudaEventRecordWithFlags(c->ev_done, s, evf));
+    return CRUM_OK;
+}
+
 int enqueue_gather_dev(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, bool full, bool timing,
                        bool capturing = false) {
     const unsigned evf = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
@@ -1747,7 +1808,12 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
             cudaGetLastError();
             return CRUM_E_BUSY;
         }
-        const int st = enqueue_gather_dev(c, c->gcap, img, capacity, (flags & CRUM_FULL) != 0, timing, true);
+        uint64_t worst = 0;
+        crum_image_required_bytes(c, UINT64_MAX, &worst);
+        const bool fused = use_fused(c, (flags & CRUM_FULL) != 0, capacity, worst);
+        const int st = fused ? enqueue_fused(c, c->gcap, img, capacity, timing, true)
+                             : enqueue_gather_dev(c, c->gcap, img, capacity, (flags & CRUM_FULL) != 0, timing, true);
+        e->fused = fused;
         cudaGraph_t g = nullptr;
         const cudaError_t ce = cudaStreamEndCapture(c->gcap, &g);
         const uint64_t nk = c->launches - l0;
@@ -1773,6 +1839,7 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
     e->used = ++c->graph_clock;
     CK(cudaGraphLaunch(e->exec, s));
     c->launches += e->nk;
+    c->last_kind = e->fused ? kLastDevFused : kLastDevGather;
     return CRUM_OK;
 }
 
@@ -1974,40 +2041,12 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     crum_image_required_bytes(c, UINT64_MAX, &worst);
     // The single-pass kernel is opt-in (CRUM_CFG_FUSED).
     if (flags & CRUM_COMPRESS) return gather_z(c, s, img, nullptr, capacity, full, timing, rep);
-    if (c->fused_ok && c->fused_cfg && !full && capacity >= worst) {
+    if (use_fused(c, full, capacity, worst)) {
         // single pass: detect + compact + gather + commit in one kernel, then
-        // the metadata CRC / tail / header
-        if (timing) CK(cudaEventRecord(c->ev_t[0], s));
-        if ((st = next_tag(c, s))) return st;
-        CK(cudaMemsetAsync(c->d_fs, 0, sizeof(FusedScratch), s));
-        // per-region dirty counts start at zero (the multi-kernel path's
-        // compaction leaves its own counts there)
-        CK(cudaMemsetAsync(c->d_reg_nd, 0, 4 * c->regs.size(), s));
-        FusedArgs fa{};
-        fa.regs = c->d_regs;
-        fa.R = (uint32_t)c->regs.size();
-        fa.tag = c->tag;
-        fa.tile_base = c->d_tile_base;
-        fa.n_tiles = c->n_tiles;
-        fa.status = c->d_status;
-        fa.fs = c->d_fs;
-        fa.force = c->d_force;
-        fa.img = img;
-        fa.poff = payload_offset_for(c->regs.size());
-        fa.gids = c->d_gids;
-        fa.sunit = c->d_sunit;
-        fa.lids = c->d_lids;
-        fa.reg_nd = c->d_reg_nd;
-        fa.rs = c->d_rs;
-        fa.st = c->d_st;
-        fa.capacity = capacity;
-        Launch L = launch_of(c, s);
-        launch_fused_compare(L, fa, c->sms * c->fused_bps);
-        if (timing) CK(cudaEventRecord(c->ev_t[1], s));
-        launch_crc_meta(L, crc_args(c, img, nullptr), crc_max_len(c));
-        CK_LAUNCH();
-        if (timing) CK(cudaEventRecord(c->ev_t[4], s));
-        CK(cudaEventRecord(c->ev_done, s));
+        // the metadata CRC / tail / header (a replayed graph when asynchronous)
+        st = (!rep && c->graphs_on) ? gather_dev_graph(c, s, img, capacity, flags, timing) : CRUM_E_BUSY;
+        if (st == CRUM_E_BUSY) st = enqueue_fused(c, s, img, capacity, timing);
+        if (st) return st;
         c->last_kind = kLastDevFused;
         c->last_path = 0;
         c->last_timed = timing;
@@ -2091,9 +2130,13 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
         CK(cudaHostGetDevicePointer(&dimg, img->host, 0));
         uint8_t *d = static_cast<uint8_t *>(dimg);
         int st = graphs_on ? gather_dev_graph(c, s, d, img->cap, flags, true) : CRUM_E_BUSY;
-        if (st == CRUM_E_BUSY) st = enqueue_gather_dev(c, s, d, img->cap, full, true);
-        if (st) return st;
-        c->last_kind = kLastDevGather;
+        if (st == CRUM_E_BUSY) {
+            const bool fused = use_fused(c, full, img->cap, worst);
+            st = fused ? enqueue_fused(c, s, d, img->cap, true) : enqueue_gather_dev(c, s, d, img->cap, full, true);
+            c->last_kind = fused ? kLastDevFused : kLastDevGather;
+        }
+        if (st) return st;  // (gather_dev_graph set last_kind)
+        c->last_path = 0;
         c->last_timed = true;
         CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

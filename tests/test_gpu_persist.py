@@ -144,3 +144,25 @@ def test_persist_and_load_errors(crum, tmp_path):
     q = p.g.load_image(path)
     st, _ = p.g.restore_scatter(q, raise_on_error=False)
     assert st == crum.E_CORRUPT
+
+
+def test_persist_direct_io(crum, tmp_path):
+    """CRUM_PERSIST_DIRECT (O_DIRECT, whole blocks, truncated to the image
+    length) writes the image's exact bytes; a filesystem without O_DIRECT
+    (e.g. tmpfs) makes the writer report CRUM_E_IO instead of silently
+    buffering."""
+    import os
+    p = mkpair(43)
+    img = p.g.new_image()
+    st, want, _ = p.o.checkpoint_gather()
+    p.g.checkpoint_gather(img)
+    path = str(tmp_path / "direct.crum")
+    img.persist(path, fsync=True, direct=True)
+    try:
+        img.persist_wait()
+    except crum.CrumError as e:
+        assert e.status == crum.E_IO
+        pytest.skip(f"no O_DIRECT on {tmp_path}: {e}")
+    assert os.path.getsize(path) == img.length
+    with open(path, "rb") as f:
+        assert f.read() == want.tobytes()

@@ -24,6 +24,9 @@ FUSABLE = [
     (32 * MiB + 4096, 64 * KiB, C),         # several tiles, partial last page
     (12 * KiB + 256, 4 * KiB, C),
 ]
+# the same kind, above the default single-pass threshold (64 MiB): the
+# multi-kernel path unless CRUM_CFG_FUSED asks for the single pass
+FUSABLE_BIG = FUSABLE + [(40 * MiB + 12288, 64 * KiB, C)]
 MIXED = [
     (4 * MiB, 4 * KiB, C),
     (3 * 64 * KiB + 1234, 64 * KiB, H),
@@ -53,14 +56,15 @@ def variants():
             ("fused_no_graph", m.CFG_FUSED | m.CFG_NO_GRAPH)]
 
 
-@pytest.mark.parametrize("specs_name", ["fusable", "mixed"])
+@pytest.mark.parametrize("specs_name", ["fusable", "fusable_big", "mixed"])
 @pytest.mark.parametrize("variant", [v[0] for v in variants()])
 def test_every_path_bit_exact(crum, variant, specs_name):
     """Device image (asynchronous: graph replay unless NO_GRAPH; synchronous
     with a report), host image and sync, epoch by epoch, every dirty ratio and
     FULL: image bytes, reports and snapshots equal the oracle's."""
     flags = dict(variants())[variant]
-    specs = FUSABLE if specs_name == "fusable" else MIXED
+    specs = {"fusable": FUSABLE, "fusable_big": FUSABLE_BIG, "mixed": MIXED}[specs_name]
+    small = sum(nb for nb, _, _ in specs) <= 64 * MiB
     p = mkpair(specs, 40, flags=flags)
     cap = p.g.image_required_bytes()
     dbuf = torch.empty(cap + 4096, dtype=torch.uint8, device="cuda")
@@ -90,7 +94,11 @@ def test_every_path_bit_exact(crum, variant, specs_name):
         assert got == want.tobytes(), (variant, epoch, how)
         for k in ("dirty_pages", "dirty_bytes", "image_bytes"):
             assert rep[k] == rep_o[k], (epoch, k)
-        fused_eligible = specs_name == "fusable" and variant.startswith("fused") and how != "host" and not gflags
+        # single pass: compare-only, incremental, device image (the pinned
+        # path of these footprints is the range pipeline), and either asked
+        # for or a footprint <= 64 MiB (the default)
+        fused_eligible = (specs_name != "mixed" and how != "host" and not gflags and
+                          (variant.startswith("fused") or small))
         assert bool(rep["path"] & crum.PATH_FUSED) == fused_eligible, (variant, epoch, how, rep["path"])
         assert p.shadows_equal(), (variant, epoch)
 
