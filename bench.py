@@ -655,9 +655,12 @@ def main():
 
     scrub = torch.empty(256 * MiB, dtype=torch.uint8, device=dev)
     k_exp = sum(synth.dirty_count(args.dirty, synth.n_pages(nb, P)) for nb, P, _ in specs)
-    # the pinned image holds one step's image (the exact bound for this dirty
-    # ratio); the gather streams range by range and commits once it fits
-    cap = ctx.image_required_bytes(k_exp)
+    # the pinned image: a worst-case image when that is small (<= 2 GiB: the
+    # gather commits as it streams; C1 takes the one-launch small path), else
+    # the exact bound for this dirty ratio (the gather streams range by range
+    # and commits once the image is known to fit)
+    worst_img = ctx.image_required_bytes()
+    cap = worst_img if worst_img <= 2 * GiB else ctx.image_required_bytes(k_exp)
     img = ctx.new_image(cap)
     ctx.sync_shadow(stream)   # epoch 0: commit the whole footprint (every page starts force-dirty)
     torch.cuda.synchronize()
@@ -786,7 +789,11 @@ def main():
     # region + mirror (2F); hash reads region + table, writes new hashes
     # (F + 16N); tracked: the gather (reads + writes the listed pages).
     if fused:
-        kname, det_bytes = "fused_compare", 2 * F + 2 * slot_bytes
+        # a single-pass kernel (one launch: detect + compaction + gather + commit)
+        kname = "single_pass"
+        det_bytes = {"compare": 2 * F + 2 * slot_bytes, "tracked": n_pages + 2 * slot_bytes}.get(args.mode, 0)
+        det_ms = [r["t_detect_ms"] for r in dreps]
+        det_t = coord.max_over_ranks(sum(det_ms) / args.steps) / 1e3
     else:
         kname = "gather" if args.mode == "tracked" else f"detect_{args.mode}"
         det_bytes = {"compare": 2 * F, "hash": F + 16 * n_pages, "tracked": 2 * slot_bytes}[args.mode]

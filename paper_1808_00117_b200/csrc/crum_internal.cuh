@@ -175,16 +175,23 @@ struct ScatterArgs {
 // Single-pass checkpoint (all regions COMPARE, P <= 64 KiB): detect +
 // decoupled look-back compaction + gather + commit in one persistent kernel.
 constexpr uint32_t kFusedMaxLog2P = 16;
-constexpr uint32_t kFusedMinTileLog2 = 15;   // tile = max(P, 32 KiB)
+constexpr uint32_t kFusedMinTileLog2 = 15;   // tile = max(P, 32 KiB) (footprints above kFusedSmallBytes)
+constexpr uint64_t kFusedSmallBytes = 64ull << 20;  // at or below: tile = one page, metadata CRC in-kernel
+constexpr uint32_t kFusedInlineMeta = 16384;        // in-kernel CRC when table + ids can reach at most this
 struct FusedScratch {
     uint32_t ticket;          // next tile to claim
     uint32_t done;            // tiles finished
     uint64_t dirty_bytes;     // accumulated logical bytes of listed pages
 };
+// One contiguous scratch per context, cleared by ONE memset before every
+// launch: FusedScratch | per-region counts | look-back status words.
 struct FusedArgs {
     const DevRegion *regs;
     uint32_t R;
-    uint32_t tag;             // 1..255, also tags the look-back status words
+    uint32_t tag;             // tag of the look-back status words (constant: they are cleared per launch)
+    uint32_t tile_log2_min;   // tile = max(P, 2^tile_log2_min) bytes
+    int inline_meta;          // the finalising warp writes tail, runs, CRC and header (no k_crc_meta)
+    X2N x2n;                  // CRC shift tables (inline_meta)
     const uint64_t *tile_base;// per region: first tile (prefix, R + 1 entries)
     uint64_t n_tiles;
     uint64_t *status;         // per tile: tag | state | count | units
@@ -201,6 +208,31 @@ struct FusedArgs {
     uint64_t capacity;
 };
 void launch_fused_compare(const Launch &L, const FusedArgs &a, int blocks);
+
+// One-launch checkpoint of a small footprint (SURVEY.md sec. 7.3 hard part 6,
+// config C1): a cooperative grid detects (compare / tracked) into a page
+// bitmap, meets at one grid barrier, then every CTA derives the slot of
+// every dirty page from the bitmap in shared memory (no look-back): the
+// CTAs gather + commit, CTA 0 writes table, ids, CRC and header.  Eligible:
+// every region COMPARE or TRACKED with one page size, N <= kSmallPages,
+// image >= the worst case.
+constexpr uint32_t kSmallPages = 16384;
+struct SmallArgs {
+    const DevRegion *regs;
+    uint32_t R;
+    uint32_t log2p;           // the context's one page size
+    uint64_t N;               // pages
+    uint32_t *bitmap;         // 2 x kSmallPages bits: dirty pages (alternating, zero when a launch begins)
+    uint32_t *bar;            // [0] arrivals, [1] generation (grid barrier; persists across launches)
+    uint8_t *force;
+    uint8_t *img;             // image (payload at poff)
+    uint64_t poff;
+    uint64_t capacity;
+    DevStats *st;
+    X2N x2n;
+};
+void launch_small_ckpt(const Launch &L, const SmallArgs &a, int blocks);
+int small_blocks_per_sm();
 int fused_blocks_per_sm();
 
 // ---- detect (kernels_detect.cu) ----

@@ -926,6 +926,18 @@ __device__ __forceinline__ uint64_t ld_acquire(const uint64_t *p) {
     asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// A look-back status word is self-contained (tag, state, count, units in one
+// 64-bit word) and nothing else a predecessor wrote is read on the strength
+// of it (the finalising warp synchronises through the done counter), so
+// relaxed GPU-scope accesses suffice: no fence per load / store.
+__device__ __forceinline__ void st_relaxed(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void ld256(const void *p, uint32_t (&r)[8]) {
     asm volatile("ld.global.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
@@ -944,6 +956,63 @@ __device__ __forceinline__ uint64_t warp_excl_scan(uint64_t v, uint64_t *total) 
     }
     *total = __shfl_sync(0xffffffffu, inc, 31);
     return inc - v;
+}
+
+// Small footprints: the finalising warp also does k_crc_meta's work for
+// this image -- ids (+ pad) into the tail, runs, the zlib CRC-32 of table ||
+// ids (32 lane chunks, each a raw register shifted into place by
+// x^(8 * bytes after it)), and the header with its own CRC -- so the whole
+// checkpoint is one kernel.  Compare-only contexts: no hashes, no sizes.
+__device__ __noinline__ void fused_inline_meta(const FusedArgs &a, uint64_t K, uint64_t U, uint64_t poff,
+                                               uint32_t lane) {
+    __shared__ uint32_t T[256];  // byte-wise CRC-32 table (reflected polynomial)
+    for (uint32_t i = lane; i < 256; i += 32) {
+        uint32_t c = i;
+        for (int b = 0; b < 8; ++b) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+        T[i] = c;
+    }
+    DevStats *st = a.st;
+    const uint64_t payload = U << kSegLog2, ids_off = poff + payload;
+    const uint64_t idsw = round_up(4 * K, 8) / 4;
+    uint32_t *tids = reinterpret_cast<uint32_t *>(a.img + ids_off);
+    for (uint64_t k = lane; k < idsw; k += 32) tids[k] = k < K ? a.lids[k] : 0u;
+    uint64_t runs = 0;
+    for (uint64_t k = lane; k < K; k += 32) runs += (k == 0 || a.lids[k] == 0 || a.gids[k - 1] + 1 != a.gids[k]) ? 1 : 0;
+    runs = warp_sum(runs);
+    __syncwarp();
+    // CRC of table (12 R words at img + 64) || ids (idsw words, from lids)
+    const uint64_t tabw = 12ull * a.R, nw = tabw + idsw;
+    const uint64_t cw = (nw + 31) / 32;
+    const uint64_t w0 = min(nw, lane * cw), w1 = min(nw, w0 + cw);
+    const uint32_t *tab = reinterpret_cast<const uint32_t *>(a.img + 64);
+    uint32_t c = (w0 == 0 && w1 > 0) ? 0xffffffffu : 0u;
+    for (uint64_t w = w0; w < w1; ++w) {
+        const uint32_t v = w < tabw ? tab[w] : ((w - tabw) < K ? a.lids[w - tabw] : 0u);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) c = T[(c ^ (v >> (8 * b))) & 0xffu] ^ (c >> 8);
+    }
+    uint32_t term = (w1 > w0) ? gf2_mulmod(xpow8n(4 * (nw - w1), a.x2n.t), c) : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) term ^= __shfl_xor_sync(0xffffffffu, term, o);
+    if (lane != 0) return;
+    st->dirty_runs = runs;
+    const uint32_t meta_crc = nw == 0 ? 0u : (term ^ 0xffffffffu);
+    st->meta_crc = meta_crc;
+    uint8_t h[64];
+    h[0] = 'C'; h[1] = 'R'; h[2] = 'U'; h[3] = 'M';
+    put32(h + 4, 1);
+    put32(h + 8, 0);  // incremental, no hashes, not compressed
+    put32(h + 12, a.R);
+    put64(h + 16, K);
+    put64(h + 24, poff);
+    put64(h + 32, payload);
+    put64(h + 40, ids_off);
+    put64(h + 48, ids_off + 4 * idsw);
+    put32(h + 56, meta_crc);
+    uint32_t hc = 0xffffffffu;
+    for (int i = 0; i < 60; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
+    put32(h + 60, hc ^ 0xffffffffu);
+    for (int i = 0; i < 64; ++i) a.img[i] = h[i];
 }
 
 // Each WARP owns one tile at a time: no block barriers, so while one warp
@@ -967,7 +1036,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
             r = lo;
         }
         const DevRegion g = a.regs[r];
-        const uint32_t tlog = max(g.log2p, kFusedMinTileLog2);
+        const uint32_t tlog = max(g.log2p, a.tile_log2_min);
         const uint64_t off0 = (t - __ldg(a.tile_base + r)) << tlog;
         const uint64_t tlen = min((uint64_t)1 << tlog, g.bytes - off0);
         const uint64_t i0 = off0 >> g.log2p;  // first page of the tile
@@ -1009,29 +1078,55 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
         // ---- A2 compaction: aggregate, look-back, inclusive prefix ----
         const uint32_t cnt = __popc(dmask);
         const uint64_t ucnt = (uint64_t)cnt << spl;
-        if (lane == 0) st_release(a.status + t, pack_status(a.tag, kStAgg, cnt, ucnt));
+        if (lane == 0) st_relaxed(a.status + t, pack_status(a.tag, kStAgg, cnt, ucnt));
+        // look back kLB windows of 32 predecessors per step: the status loads
+        // of a step are independent, so a step costs one round trip however
+        // far the nearest inclusive prefix is (small footprints: when every
+        // tile starts at once, prefixes are rare and one-window steps made the
+        // last tiles wait ~n/32 round trips)
+        constexpr int kLB = 8;
         uint64_t ec = 0, eu = 0;
         int64_t top = (int64_t)t - 1;
         while (top >= 0) {
-            const int64_t idx = top - (int64_t)lane;
-            uint64_t v = pack_status(a.tag, kStPrefix, 0, 0);  // before tile 0: prefix 0
-            uint32_t stt = (uint32_t)kStPrefix;
-            if (idx >= 0) {
-                do {
-                    v = ld_acquire(a.status + idx);
-                    stt = ((v >> 56) == a.tag) ? (uint32_t)((v >> 54) & 3) : 0u;
-                } while (stt == 0);
+            uint64_t v[kLB];
+            uint32_t stt[kLB];
+#pragma unroll
+            for (int j = 0; j < kLB; ++j) {
+                const int64_t idx = top - (int64_t)lane - 32 * j;
+                v[j] = pack_status(a.tag, kStPrefix, 0, 0);  // before tile 0: prefix 0
+                stt[j] = (uint32_t)kStPrefix;
+                if (idx >= 0) {
+                    v[j] = ld_relaxed(a.status + idx);
+                    stt[j] = ((v[j] >> 56) == a.tag) ? (uint32_t)((v[j] >> 54) & 3) : 0u;
+                }
             }
-            const uint32_t pm = __ballot_sync(0xffffffffu, stt == kStPrefix);
-            const int first = pm ? __ffs(pm) - 1 : 32;
-            const uint64_t c = ((int)lane <= first) ? ((v >> 27) & 0x7ffffffull) : 0;
-            const uint64_t u = ((int)lane <= first) ? (v & 0x7ffffffull) : 0;
+#pragma unroll
+            for (int j = 0; j < kLB; ++j) {  // wait for the ones not yet published
+                const int64_t idx = top - (int64_t)lane - 32 * j;
+                while (stt[j] == 0) {
+                    v[j] = ld_relaxed(a.status + idx);
+                    stt[j] = ((v[j] >> 56) == a.tag) ? (uint32_t)((v[j] >> 54) & 3) : 0u;
+                }
+            }
+            // nearest inclusive prefix: smallest distance 32 j + lane
+            uint32_t mine = 0xffffffffu;
+#pragma unroll
+            for (int j = kLB - 1; j >= 0; --j)
+                if (stt[j] == kStPrefix) mine = 32 * j + lane;
+            const uint32_t first = __reduce_min_sync(0xffffffffu, mine);
+            uint64_t c = 0, u = 0;
+#pragma unroll
+            for (int j = 0; j < kLB; ++j)
+                if (32u * j + lane <= first) {
+                    c += (v[j] >> 27) & 0x7ffffffull;
+                    u += v[j] & 0x7ffffffull;
+                }
             ec += warp_sum(c);
             eu += warp_sum(u);
-            if (pm) break;
-            top -= 32;
+            if (first != 0xffffffffu) break;
+            top -= 32 * kLB;
         }
-        if (lane == 0) st_release(a.status + t, pack_status(a.tag, kStPrefix, ec + cnt, eu + ucnt));
+        if (lane == 0) st_relaxed(a.status + t, pack_status(a.tag, kStPrefix, ec + cnt, eu + ucnt));
         // ---- A3 gather + commit: the tile's dirty pages, ascending ----
         uint32_t m = dmask;
         for (uint32_t rank = 0; m; ++rank, m &= m - 1) {
@@ -1132,6 +1227,275 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
         // to its final claim must still see ticket >= n_tiles.  The host
         // zeroes the scratch stream-ordered before every launch.
     }
+    __syncwarp();  // the table, padding and stats written by the lanes above
+    if (a.inline_meta) fused_inline_meta(a, K, U, poff, lane);
+}
+
+// ---------------------------------------------------------------------------
+// One-launch small-footprint checkpoint (see SmallArgs).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kSmallThreads = 256;
+constexpr uint32_t kSmallWords = kSmallPages / 32;
+
+// Grid barrier of a cooperative launch (all CTAs co-resident): arrivals
+// counter + generation, sense by generation, state returns to 0 arrivals.
+__device__ __forceinline__ void grid_barrier(uint32_t *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile uint32_t *gen = bar + 1;
+        const uint32_t g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
+    __shared__ uint32_t s_bm[kSmallWords];    // dirty bitmap
+    __shared__ uint32_t s_pre[kSmallWords + 1];  // dirty pages before word w
+    __shared__ uint32_t T[256];                // CRC-32 byte table (CTA 0)
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t wid = ((uint64_t)blockIdx.x * kSmallThreads + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * kSmallThreads) >> 5;
+    const uint32_t spl = a.log2p - kSegLog2;   // log2 segments per page
+    const uint64_t P = 1ull << a.log2p;
+    // two bitmaps: this launch uses bitmap[gen & 1] (the barrier generation,
+    // the same for every CTA until the barrier), CTA 0 clears the other one
+    // for the next launch (a CTA may still read this launch's after CTA 0 is done)
+    const uint32_t par = *reinterpret_cast<volatile uint32_t *>(a.bar + 1) & 1u;
+    uint32_t *bitmap = a.bitmap + par * kSmallWords;
+    // ---- A1 detect: warp per 4 KiB segment; forced pages are dirty unread ----
+    uint32_t r = 0;
+    for (uint64_t g = wid; g < (a.N << spl); g += nwarps) {
+        const uint64_t pg = g >> spl;
+        while (r + 1 < a.R && a.regs[r + 1].page_base <= pg) ++r;
+        while (a.regs[r].page_base > pg) --r;
+        const DevRegion &R = a.regs[r];
+        bool dirty = a.force[pg] != 0;
+        if (!dirty && R.mode == kModeCompare) {
+            const uint64_t off = ((pg - R.page_base) << a.log2p) + ((g & ((1u << spl) - 1)) << kSegLog2);
+            uint32_t x = 0;
+            if (off < R.bytes) {
+                const uint64_t len = R.bytes - off;
+                const uint8_t *pa = R.base + off, *pb = R.mirror + off;
+                if (len >= kSegBytes) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const uint4 u = __ldcs(reinterpret_cast<const uint4 *>(pa + i * 512 + lane * 16));
+                        const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(pb + i * 512 + lane * 16));
+                        x |= (u.x ^ v.x) | (u.y ^ v.y) | (u.z ^ v.z) | (u.w ^ v.w);
+                    }
+                } else {
+                    for (uint32_t o = lane; o < len; o += 32) x |= (uint32_t)(pa[o] ^ pb[o]);
+                }
+            }
+            dirty = __any_sync(0xffffffffu, x != 0);
+        }
+        if (dirty && lane == 0) atomicOr(bitmap + (pg >> 5), 1u << (pg & 31));
+    }
+    grid_barrier(a.bar);
+    // ---- A2: every CTA: the bitmap and its word prefix in shared memory ----
+    const uint32_t nw = (uint32_t)((a.N + 31) >> 5);
+    for (uint32_t w = threadIdx.x; w < nw; w += kSmallThreads) s_bm[w] = __ldcg(bitmap + w);
+    __syncthreads();
+    {   // exclusive prefix of popc over the words: 256 threads x (nw / 256) words
+        const uint32_t per = (nw + kSmallThreads - 1) / kSmallThreads;
+        const uint32_t w0 = threadIdx.x * per;
+        uint64_t own = 0;
+        for (uint32_t w = w0; w < min(nw, w0 + per); ++w) own += __popc(s_bm[w]);
+        uint64_t tot;
+        uint64_t run = block_excl_scan(own, &tot);
+        for (uint32_t w = w0; w < min(nw, w0 + per); ++w) {
+            s_pre[w] = (uint32_t)run;
+            run += __popc(s_bm[w]);
+        }
+        if (threadIdx.x == 0) s_pre[nw] = (uint32_t)tot;
+    }
+    __syncthreads();
+    const uint64_t K = s_pre[nw];
+    // rank k -> page: the word by binary search over s_pre, the bit by select
+    auto page_of = [&](uint64_t k) -> uint64_t {
+        uint32_t lo = 0, hi = nw;  // largest w with s_pre[w] <= k
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_pre[mid] <= k) lo = mid; else hi = mid;
+        }
+        uint32_t m = s_bm[lo];
+        for (uint32_t j = (uint32_t)(k - s_pre[lo]); j; --j) m &= m - 1;
+        return 32ull * lo + (__ffs(m) - 1);
+    };
+    // ---- A3 gather + commit: warp per dirty page (CTA 0 does the metadata) ----
+    const uint64_t gw = blockIdx.x == 0 ? 0 : ((uint64_t)(blockIdx.x - 1) * kSmallThreads + threadIdx.x) >> 5;
+    const uint64_t gnw = ((uint64_t)(gridDim.x > 1 ? gridDim.x - 1 : 1) * kSmallThreads) >> 5;
+    if (blockIdx.x != 0 || gridDim.x == 1) {
+        uint32_t rr = 0;
+        for (uint64_t k = (gridDim.x == 1 ? (threadIdx.x >> 5) : gw); k < K; k += (gridDim.x == 1 ? kSmallThreads / 32 : gnw)) {
+            const uint64_t pg = page_of(k);
+            while (rr + 1 < a.R && a.regs[rr + 1].page_base <= pg) ++rr;
+            while (a.regs[rr].page_base > pg) --rr;
+            const DevRegion &R = a.regs[rr];
+            const uint64_t i = pg - R.page_base;
+            uint8_t *dst = a.img + a.poff + (k << a.log2p);
+            for (uint32_t sg = 0; sg < (1u << spl); ++sg) {
+                const uint64_t off = (i << a.log2p) + ((uint64_t)sg << kSegLog2);
+                const uint64_t len = R.bytes > off ? min((uint64_t)kSegBytes, R.bytes - off) : 0;
+                uint8_t *d = dst + ((uint64_t)sg << kSegLog2);
+                uint8_t *m = R.mode == kModeCompare ? R.mirror + off : nullptr;
+                if (len == kSegBytes) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const uint4 v = *reinterpret_cast<const uint4 *>(R.base + off + j * 512 + lane * 16);
+                        *reinterpret_cast<uint4 *>(d + j * 512 + lane * 16) = v;
+                        if (m) *reinterpret_cast<uint4 *>(m + j * 512 + lane * 16) = v;
+                    }
+                } else {
+                    for (uint32_t o = lane; o < kSegBytes; o += 32) {
+                        const uint8_t v = o < len ? R.base[off + o] : 0;
+                        d[o] = v;
+                        if (m && o < len) m[o] = v;
+                    }
+                }
+            }
+            if (lane == 0) a.force[pg] = 0;
+        }
+        if (blockIdx.x != 0) return;
+    }
+    // ---- CTA 0: bitmap cleared for the next launch, table, ids, CRC, header ----
+    __syncthreads();
+    uint32_t *other = a.bitmap + (par ^ 1u) * kSmallWords;
+    for (uint32_t w = threadIdx.x; w < nw; w += kSmallThreads) other[w] = 0;
+    for (uint32_t i = threadIdx.x; i < 256; i += kSmallThreads) {
+        uint32_t c = i;
+        for (int b = 0; b < 8; ++b) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+        T[i] = c;
+    }
+    const uint64_t poff = a.poff, payload = K << a.log2p, ids_off = poff + payload;
+    const uint64_t idsw = round_up(4 * K, 8) / 4;
+    uint8_t *img = a.img;
+    auto prefix_at = [&](uint64_t p) -> uint64_t {  // dirty pages before page p
+        const uint32_t w = (uint32_t)(p >> 5), b = (uint32_t)(p & 31);
+        return s_pre[w] + (b ? __popc(s_bm[w] & ((1u << b) - 1)) : 0u);
+    };
+    for (uint32_t rr = threadIdx.x; rr < a.R; rr += kSmallThreads) {
+        const DevRegion R = a.regs[rr];
+        const uint64_t first = prefix_at(R.page_base), nd = prefix_at(R.page_base + R.n_pages) - first;
+        uint8_t *e = img + 64 + 48ull * rr;
+        reinterpret_cast<uint32_t *>(e)[0] = R.id;
+        reinterpret_cast<uint32_t *>(e)[1] = R.mode;
+        reinterpret_cast<uint64_t *>(e)[1] = R.bytes;
+        reinterpret_cast<uint64_t *>(e)[2] = P;
+        reinterpret_cast<uint64_t *>(e)[3] = R.n_pages;
+        reinterpret_cast<uint64_t *>(e)[4] = nd;
+        reinterpret_cast<uint64_t *>(e)[5] = first;
+    }
+    for (uint64_t b = 64 + 48ull * a.R + threadIdx.x; b < poff; b += kSmallThreads) img[b] = 0;
+    // ids (region-local page indices), runs, logical bytes
+    uint32_t *tids = reinterpret_cast<uint32_t *>(img + ids_off);
+    uint64_t runs = 0, dbytes = 0;
+    {
+        uint32_t rr = 0;
+        for (uint64_t k = threadIdx.x; k < idsw; k += kSmallThreads) {
+            if (k >= K) {
+                tids[k] = 0;
+                continue;
+            }
+            const uint64_t pg = page_of(k);
+            while (rr + 1 < a.R && a.regs[rr + 1].page_base <= pg) ++rr;
+            while (a.regs[rr].page_base > pg) --rr;
+            const DevRegion &R = a.regs[rr];
+            const uint64_t i = pg - R.page_base;
+            tids[k] = (uint32_t)i;
+            runs += (i == 0 || !((s_bm[(pg - 1) >> 5] >> ((pg - 1) & 31)) & 1u)) ? 1 : 0;
+            dbytes += min(P, R.bytes - (i << a.log2p));
+        }
+    }
+    uint64_t tot_runs, tot_bytes;
+    block_excl_scan(runs, &tot_runs);
+    block_excl_scan(dbytes, &tot_bytes);
+    __syncthreads();  // table, ids and padding written
+    // CRC-32 of table (12 R words) || ids (idsw words): thread chunks, shifted into place
+    const uint64_t tabw = 12ull * a.R, nwords = tabw + idsw;
+    const uint64_t cw = (nwords + kSmallThreads - 1) / kSmallThreads;
+    const uint64_t w0 = min(nwords, threadIdx.x * cw), w1 = min(nwords, w0 + cw);
+    const uint32_t *tab = reinterpret_cast<const uint32_t *>(img + 64);
+    uint32_t c = (w0 == 0 && w1 > 0) ? 0xffffffffu : 0u;
+    for (uint64_t w = w0; w < w1; ++w) {
+        const uint32_t v = w < tabw ? tab[w] : tids[w - tabw];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) c = T[(c ^ (v >> (8 * b))) & 0xffu] ^ (c >> 8);
+    }
+    const uint32_t term = (w1 > w0) ? gf2_mulmod(xpow8n(4 * (nwords - w1), a.x2n.t), c) : 0u;
+    __shared__ uint32_t s_x[kSmallThreads / 32];
+    uint32_t x = term;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) s_x[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    uint32_t acc = 0;
+    for (uint32_t w = 0; w < kSmallThreads / 32; ++w) acc ^= s_x[w];
+    const uint32_t meta_crc = nwords == 0 ? 0u : (acc ^ 0xffffffffu);
+    DevStats *st = a.st;
+    st->K = K;
+    st->total_units = K << (a.log2p - kSegLog2);
+    st->poff = poff;
+    st->payload_bytes = payload;
+    st->ids_off = ids_off;
+    st->image_bytes = ids_off + 4 * idsw;
+    st->capacity = a.capacity;
+    st->status = st->image_bytes > a.capacity ? kStCapacity : kStOk;
+    st->img_flags = 0;
+    st->n_regions = a.R;
+    st->dirty_bytes = tot_bytes;
+    st->dirty_runs = tot_runs;
+    st->crc_acc = 0;
+    st->meta_crc = meta_crc;
+    uint8_t h[64];
+    h[0] = 'C'; h[1] = 'R'; h[2] = 'U'; h[3] = 'M';
+    put32(h + 4, 1);
+    put32(h + 8, 0);
+    put32(h + 12, a.R);
+    put64(h + 16, K);
+    put64(h + 24, poff);
+    put64(h + 32, payload);
+    put64(h + 40, ids_off);
+    put64(h + 48, ids_off + 4 * idsw);
+    put32(h + 56, meta_crc);
+    uint32_t hc = 0xffffffffu;
+    for (int i = 0; i < 60; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
+    put32(h + 60, hc ^ 0xffffffffu);
+    for (int i = 0; i < 64; ++i) img[i] = h[i];
+}
+
+int small_blocks_per_sm() {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_small_ckpt, kSmallThreads, 0) != cudaSuccess) {
+        cudaGetLastError();
+        n = 1;
+    }
+    return n > 0 ? n : 1;
+}
+
+void launch_small_ckpt(const Launch &L, const SmallArgs &a, int blocks) {
+    // every CTA must be resident at once (grid barrier): a cooperative launch
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(kSmallThreads);
+    cfg.stream = L.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_small_ckpt, a);
+    ++*L.counter;
 }
 
 int fused_blocks_per_sm() {
@@ -1144,6 +1508,9 @@ int fused_blocks_per_sm() {
 }
 
 void launch_fused_compare(const Launch &L, const FusedArgs &a, int blocks) {
+    // no more warps than tiles (every claim is an atomic on one counter)
+    const uint64_t need = (a.n_tiles + kFusedThreads / 32 - 1) / (kFusedThreads / 32);
+    if ((uint64_t)blocks > need) blocks = (int)(need ? need : 1);
     k_fused_compare<<<blocks, kFusedThreads, 0, L.stream>>>(a);
     ++*L.counter;
 }

@@ -117,6 +117,15 @@ inline uint32_t rd32(const uint8_t *p) {
 uint64_t payload_offset_for(uint64_t R) { return round_up(64 + 48 * R, 4096); }
 uint64_t tail_bytes_for(uint64_t K, bool has_hashes) { return round_up(4 * K, 8) + (has_hashes ? 8 * K : 0); }
 
+// The single-pass kernel's scratch, one allocation cleared by one memset per
+// launch: FusedScratch (256 B) | per-region counts (4 R, to 256 B) | status
+// words (8 per tile + 1).
+constexpr uint64_t kFsHead = 256;
+uint64_t fused_counts_bytes(uint64_t R) { return round_up(4 * R + 4, 256); }
+uint64_t fused_scratch_bytes(uint64_t R, uint64_t n_tiles) {
+    return kFsHead + fused_counts_bytes(R) + 8 * (n_tiles + 1);
+}
+
 struct HostRegion {
     uint32_t id;
     uint32_t mode;
@@ -271,8 +280,12 @@ struct crum_ctx {
     bool fused_ok = false;
     uint64_t *d_tile_base = nullptr;
     uint64_t n_tiles = 0;
-    uint64_t *d_status = nullptr;
-    FusedScratch *d_fs = nullptr;
+    uint32_t *d_small = nullptr;   // one-launch small path: 2 dirty bitmaps | grid barrier words
+    bool small_ok = false;         // every region COMPARE/TRACKED, one page size, N <= kSmallPages, F small
+    uint32_t small_log2p = 12;
+    int small_bps = 1;
+    uint64_t *d_status = nullptr;  // single-pass scratch: FusedScratch | per-region counts | status words
+    uint32_t fused_tile_min = 15;
     int fused_bps = 1;
     bool last_fused = false;
 
@@ -493,10 +506,13 @@ int rebuild(crum_ctx *c, std::vector<HostRegion> regs, const std::vector<uint64_
     }
     // single-pass eligibility and its tile map
     bool fused_ok = R > 0 && (units >> 27) == 0;
+    // small footprints: one page per tile (every warp's tile is one memory
+    // round trip); large ones: >= 32 KiB per tile
+    const uint32_t tile_min = F <= kFusedSmallBytes ? kSegLog2 : kFusedMinTileLog2;
     std::vector<uint64_t> tb{0};
     for (const HostRegion &h : regs) {
         fused_ok = fused_ok && h.mode == kModeCompare && h.log2p <= kFusedMaxLog2P;
-        const uint32_t tl = std::max(h.log2p, kFusedMinTileLog2);
+        const uint32_t tl = std::max(h.log2p, tile_min);
         tb.push_back(tb.back() + ((h.bytes + (1ull << tl) - 1) >> tl));
     }
     const uint64_t cap = pad_pages(N);
@@ -540,7 +556,7 @@ int rebuild(crum_ctx *c, std::vector<HostRegion> regs, const std::vector<uint64_
             return e;
         if (grow_u2s && (e = dev_alloc(c, &t.u2s, 4 * (units + 1)))) return e;
         if (fused_ok && ((e = dev_alloc(c, &t.tile_base, 8 * tb.size())) ||
-                         (e = dev_alloc(c, &t.status, 8 * (tb.back() + 1)))))
+                         (e = dev_alloc(c, &t.status, fused_scratch_bytes(R, tb.back())))))
             return e;
         if (grow_rs && (e = dev_alloc(c, &t.rs, sizeof(RegStat) * (R + 1)))) return e;
         if (grow_meta && (e = dev_alloc(c, &t.meta, meta_max))) return e;
@@ -598,7 +614,7 @@ int rebuild(crum_ctx *c, std::vector<HostRegion> regs, const std::vector<uint64_
             return e;
         if (fused_ok) {
             if ((e = upload(c, t.tile_base, tb.data(), 8 * tb.size()))) return e;
-            CK(cudaMemset(t.status, 0, 8 * (tb.back() + 1)));
+            CK(cudaMemset(t.status, 0, fused_scratch_bytes(R, tb.back())));
         }
         return CRUM_OK;
     };
@@ -640,6 +656,14 @@ int rebuild(crum_ctx *c, std::vector<HostRegion> regs, const std::vector<uint64_
     swap_in(c->d_status, t.status);
     c->fused_ok = fused_ok;
     c->n_tiles = fused_ok ? tb.back() : 0;
+    c->fused_tile_min = tile_min;
+    {
+        bool ok = R > 0 && N <= kSmallPages && F <= kFusedSmallBytes;
+        for (const HostRegion &h : regs)
+            ok = ok && (h.mode == kModeCompare || h.mode == kModeTracked) && h.log2p == regs[0].log2p;
+        c->small_ok = ok;
+        c->small_log2p = R ? regs[0].log2p : 12;
+    }
     if (grow_rs) {
         swap_in(c->d_rs, t.rs);
         c->rs_cap = R + 1;
@@ -1128,9 +1152,10 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     if (cudaMalloc(&c->d_st, sizeof(DevStats)) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaMalloc(&c->d_rb, sizeof(RangeTotals) * (kMaxRanges + 1)) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaMalloc(&c->d_done, 16) != cudaSuccess) return fail(CRUM_E_NOMEM);
-    if (cudaMalloc(&c->d_fs, sizeof(FusedScratch)) != cudaSuccess) return fail(CRUM_E_NOMEM);
-    cudaMemset(c->d_fs, 0, sizeof(FusedScratch));
     c->fused_bps = fused_blocks_per_sm();
+    c->small_bps = small_blocks_per_sm();
+    if (cudaMalloc(&c->d_small, 8 * kSmallPages / 32 + 64) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    cudaMemset(c->d_small, 0, 8 * kSmallPages / 32 + 64);
     if (cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocMapped) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaHostAlloc(&c->h_rb, sizeof(RangeTotals) * (kMaxRanges + 1), cudaHostAllocMapped) != cudaSuccess)
         return fail(CRUM_E_NOMEM);
@@ -1202,7 +1227,7 @@ int crum_destroy(crum_ctx *c) {
     dev_free(c->d_dbg);
     dev_free(c->d_tile_base);
     dev_free(c->d_status);
-    dev_free(c->d_fs);
+    dev_free(c->d_small);
     dev_free(c->d_reg_nd);
     dev_free(c->d_rs);
     dev_free(c->d_tregs);
@@ -1704,15 +1729,50 @@ namespace {
 // also fire when the sequence runs as a captured graph.
 // The single-pass kernel (detect + compaction + gather + commit, then the
 // metadata CRC) runs when the context asked for it (CRUM_CFG_FUSED) and, by
-// default, for footprints up to kFusedAutoBytes: there the multi-kernel
+// default, for footprints up to kFusedSmallBytes: there the multi-kernel
 // sequence is latency-bound (C1: detect -> compaction -> CRC, each a few
 // dependent round trips) and one launch removes two of them.  Eligible: all
 // regions COMPARE with pages <= 64 KiB, an incremental gather, and an image
 // that holds the worst case (no capacity failure can occur mid-kernel).
-constexpr uint64_t kFusedAutoBytes = 64ull << 20;
-
 bool use_fused(const crum_ctx *c, bool full, uint64_t capacity, uint64_t worst) {
-    return c->fused_ok && !full && capacity >= worst && (c->fused_cfg || c->F <= kFusedAutoBytes);
+    return c->fused_ok && !full && capacity >= worst && (c->fused_cfg || c->F <= kFusedSmallBytes);
+}
+
+// The one-launch small path (k_small_ckpt): preferred over the single-pass
+// kernel where it applies (one page size, COMPARE / TRACKED, N <= kSmallPages).
+bool use_small(const crum_ctx *c, bool full, uint64_t capacity, uint64_t worst) {
+    return c->small_ok && !full && capacity >= worst;
+}
+
+int enqueue_small(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, bool timing, bool capturing = false) {
+    const unsigned evf = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[0], s, evf));
+    SmallArgs sa{};
+    sa.regs = c->d_regs;
+    sa.R = (uint32_t)c->regs.size();
+    sa.log2p = c->small_log2p;
+    sa.N = c->N;
+    sa.bitmap = c->d_small;
+    sa.bar = c->d_small + 2 * (kSmallPages / 32);
+    sa.force = c->d_force;
+    sa.img = img;
+    sa.poff = payload_offset_for(c->regs.size());
+    sa.capacity = capacity;
+    sa.st = c->d_st;
+    sa.x2n = crc_tables().x2n;
+    const uint64_t warps = c->N << (c->small_log2p - kSegLog2);
+    uint64_t blocks = (warps + 7) / 8;
+    const uint64_t cap = (uint64_t)c->sms * c->small_bps;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 2) blocks = 2;  // CTA 0 writes the metadata beside the gathers of the others
+    if (blocks > cap) blocks = cap;
+    Launch L = launch_of(c, s);
+    launch_small_ckpt(L, sa, (int)blocks);
+    CK_LAUNCH();
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[1], s, evf));
+    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[4], s, evf));
+    CK(cudaEventRecordWithFlags(c->ev_done, s, evf));
+    return CRUM_OK;
 }
 
 // Stream-ordered and graph-capturable: the scratch, per-region counts and
@@ -1721,33 +1781,38 @@ bool use_fused(const crum_ctx *c, bool full, uint64_t capacity, uint64_t worst) 
 int enqueue_fused(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, bool timing, bool capturing = false) {
     const unsigned evf = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (timing) CK(cudaEventRecordWithFlags(c->ev_t[0], s, evf));
-    CK(cudaMemsetAsync(c->d_fs, 0, sizeof(FusedScratch), s));
-    CK(cudaMemsetAsync(c->d_reg_nd, 0, 4 * c->regs.size(), s));
-    CK(cudaMemsetAsync(c->d_status, 0, 8 * (c->n_tiles + 1), s));
+    const uint64_t R = c->regs.size();
+    CK(cudaMemsetAsync(c->d_status, 0, fused_scratch_bytes(R, c->n_tiles), s));
+    uint8_t *scr = reinterpret_cast<uint8_t *>(c->d_status);
     FusedArgs fa{};
     fa.regs = c->d_regs;
-    fa.R = (uint32_t)c->regs.size();
+    fa.R = (uint32_t)R;
     fa.tag = 1;
+    fa.tile_log2_min = c->fused_tile_min;
+    fa.inline_meta = c->F <= kFusedSmallBytes && 48 * R + 4 * c->N + 8 <= kFusedInlineMeta;
+    fa.x2n = crc_tables().x2n;
     fa.tile_base = c->d_tile_base;
     fa.n_tiles = c->n_tiles;
-    fa.status = c->d_status;
-    fa.fs = c->d_fs;
+    fa.fs = reinterpret_cast<FusedScratch *>(scr);
+    fa.reg_nd = reinterpret_cast<uint32_t *>(scr + kFsHead);
+    fa.status = reinterpret_cast<uint64_t *>(scr + kFsHead + fused_counts_bytes(R));
     fa.force = c->d_force;
     fa.img = img;
     fa.poff = payload_offset_for(c->regs.size());
     fa.gids = c->d_gids;
     fa.sunit = c->d_sunit;
     fa.lids = c->d_lids;
-    fa.reg_nd = c->d_reg_nd;
     fa.rs = c->d_rs;
     fa.st = c->d_st;
     fa.capacity = capacity;
     Launch L = launch_of(c, s);
     launch_fused_compare(L, fa, c->sms * c->fused_bps);
     if (timing) CK(cudaEventRecordWithFlags(c->ev_t[1], s, evf));
-    CrcArgs cra = crc_args(c, img, nullptr);
-    cra.st_host = nullptr;
-    launch_crc_meta(L, cra, crc_max_len(c));
+    if (!fa.inline_meta) {
+        CrcArgs cra = crc_args(c, img, nullptr);
+        cra.st_host = nullptr;
+        launch_crc_meta(L, cra, crc_max_len(c));
+    }
     CK_LAUNCH();
     if (timing) CK(cudaEventRecordWithFlags(c->ev_t[4], s, evf));
     CK(cudaEventRecordWithFlags(c->ev_done, s, evf));
@@ -1810,10 +1875,12 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
         }
         uint64_t worst = 0;
         crum_image_required_bytes(c, UINT64_MAX, &worst);
-        const bool fused = use_fused(c, (flags & CRUM_FULL) != 0, capacity, worst);
-        const int st = fused ? enqueue_fused(c, c->gcap, img, capacity, timing, true)
-                             : enqueue_gather_dev(c, c->gcap, img, capacity, (flags & CRUM_FULL) != 0, timing, true);
-        e->fused = fused;
+        const bool small = use_small(c, (flags & CRUM_FULL) != 0, capacity, worst);
+        const bool fused = !small && use_fused(c, (flags & CRUM_FULL) != 0, capacity, worst);
+        const int st = small ? enqueue_small(c, c->gcap, img, capacity, timing, true)
+                       : fused ? enqueue_fused(c, c->gcap, img, capacity, timing, true)
+                               : enqueue_gather_dev(c, c->gcap, img, capacity, (flags & CRUM_FULL) != 0, timing, true);
+        e->fused = small || fused;
         cudaGraph_t g = nullptr;
         const cudaError_t ce = cudaStreamEndCapture(c->gcap, &g);
         const uint64_t nk = c->launches - l0;
@@ -2041,11 +2108,15 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     crum_image_required_bytes(c, UINT64_MAX, &worst);
     // The single-pass kernel is opt-in (CRUM_CFG_FUSED).
     if (flags & CRUM_COMPRESS) return gather_z(c, s, img, nullptr, capacity, full, timing, rep);
-    if (use_fused(c, full, capacity, worst)) {
-        // single pass: detect + compact + gather + commit in one kernel, then
-        // the metadata CRC / tail / header (a replayed graph when asynchronous)
+    if (use_small(c, full, capacity, worst) || use_fused(c, full, capacity, worst)) {
+        // single pass: detect + compact + gather + commit in one kernel (the
+        // small path also writes the metadata; the single-pass kernel is
+        // followed by the metadata CRC / tail / header); a replayed graph
+        // when asynchronous
         st = (!rep && c->graphs_on) ? gather_dev_graph(c, s, img, capacity, flags, timing) : CRUM_E_BUSY;
-        if (st == CRUM_E_BUSY) st = enqueue_fused(c, s, img, capacity, timing);
+        if (st == CRUM_E_BUSY)
+            st = use_small(c, full, capacity, worst) ? enqueue_small(c, s, img, capacity, timing)
+                                                     : enqueue_fused(c, s, img, capacity, timing);
         if (st) return st;
         c->last_kind = kLastDevFused;
         c->last_path = 0;
@@ -2131,9 +2202,12 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
         uint8_t *d = static_cast<uint8_t *>(dimg);
         int st = graphs_on ? gather_dev_graph(c, s, d, img->cap, flags, true) : CRUM_E_BUSY;
         if (st == CRUM_E_BUSY) {
-            const bool fused = use_fused(c, full, img->cap, worst);
-            st = fused ? enqueue_fused(c, s, d, img->cap, true) : enqueue_gather_dev(c, s, d, img->cap, full, true);
-            c->last_kind = fused ? kLastDevFused : kLastDevGather;
+            const bool small = use_small(c, full, img->cap, worst);
+            const bool fused = !small && use_fused(c, full, img->cap, worst);
+            st = small ? enqueue_small(c, s, d, img->cap, true)
+                 : fused ? enqueue_fused(c, s, d, img->cap, true)
+                         : enqueue_gather_dev(c, s, d, img->cap, full, true);
+            c->last_kind = (small || fused) ? kLastDevFused : kLastDevGather;
         }
         if (st) return st;  // (gather_dev_graph set last_kind)
         c->last_path = 0;

@@ -500,3 +500,54 @@ def test_deferred_commit_streaming_gather(crum):
         assert rep["dirty_pages"] == rep_o["dirty_pages"] and rep["image_bytes"] == len(want)
         assert p.shadows_equal(), epoch
         img.destroy()
+
+
+def test_small_path_tracked_and_compare(crum):
+    """The one-launch small path (k_small_ckpt, C1-sized footprints with one
+    page size): tracked and compare regions together, device (async graph
+    replay and synchronous) and pinned images, byte for byte with the oracle
+    every epoch, shadows equal."""
+    from oracle import oracle
+    specs = [(4 * MiB, 4 * KiB, C), (256 * KiB + 100, 4 * KiB, 2), (64 * KiB, 4 * KiB, C)]
+    S = synth.seed(77)
+    o = oracle.Oracle()
+    ctx = crum.Context(0)
+    hs, ds = [], []
+    for r, (nb, P, mode) in enumerate(specs):
+        h = oracle.aligned_empty(nb)
+        synth.fill_region(h, S, r)
+        hs.append(h)
+        ds.append(torch.from_numpy(h.copy()).cuda())
+        o.register(h, P, mode)
+        ctx.register_region(ds[-1], nb, P, mode)
+    cap = ctx.image_required_bytes()
+    buf = torch.empty(cap + 256, dtype=torch.uint8, device="cuda")
+    img = ctx.new_image()
+    for epoch in range(8):
+        if epoch:
+            for r, (nb, P, mode) in enumerate(specs):
+                pg = synth.choose_dirty(S, epoch, r, synth.n_pages(nb, P), [0.01, 0.3, 0.0, 1.0][epoch % 4])
+                synth.apply_writer(hs[r], P, pg, S, epoch, r)
+                ds[r].copy_(torch.from_numpy(hs[r]))
+                if mode == 2:
+                    o.mark_pages(r + 1, pg)
+                    ctx.mark_dirty_pages(r + 1, torch.from_numpy(pg.astype(np.uint32)).cuda(), len(pg))
+        st, want, rep_o = o.checkpoint_gather()
+        assert st == 0
+        how = epoch % 3
+        if how == 0:
+            rep = ctx.checkpoint_gather(img)
+            got = img.tobytes()
+        else:
+            rep = ctx.checkpoint_gather_device(buf, cap, report=(how == 2))
+            rep = rep or ctx.last_report()
+            torch.cuda.synchronize()
+            got = buf[:len(want)].cpu().numpy().tobytes()
+        assert got == want.tobytes(), epoch
+        assert rep["path"] & crum.PATH_FUSED, epoch
+        for k in ("dirty_pages", "dirty_bytes", "dirty_runs", "image_bytes"):
+            assert rep[k] == rep_o[k], (epoch, k)
+    for r, (nb, P, mode) in enumerate(specs):
+        if mode == C:
+            assert np.array_equal(ctx.debug_export(r + 1, crum.EXPORT_MIRROR, nb), o.mirror(r + 1))
+        assert np.array_equal(ctx.debug_export(r + 1, crum.EXPORT_FORCE, synth.n_pages(nb, P)), o.force_bits(r + 1))

@@ -24,6 +24,8 @@ FUSABLE = [
     (32 * MiB + 4096, 64 * KiB, C),         # several tiles, partial last page
     (12 * KiB + 256, 4 * KiB, C),
 ]
+# one page size, compare only, 5.1 MiB: the one-launch small path (k_small_ckpt)
+SMALL = [(4 * MiB, 4 * KiB, C), (12 * KiB + 256, 4 * KiB, C), (1 * MiB + 4096 * 3 + 5, 4 * KiB, C)]
 # the same kind, above the default single-pass threshold (64 MiB): the
 # multi-kernel path unless CRUM_CFG_FUSED asks for the single pass
 FUSABLE_BIG = FUSABLE + [(40 * MiB + 12288, 64 * KiB, C)]
@@ -56,14 +58,14 @@ def variants():
             ("fused_no_graph", m.CFG_FUSED | m.CFG_NO_GRAPH)]
 
 
-@pytest.mark.parametrize("specs_name", ["fusable", "fusable_big", "mixed"])
+@pytest.mark.parametrize("specs_name", ["small", "fusable", "fusable_big", "mixed"])
 @pytest.mark.parametrize("variant", [v[0] for v in variants()])
 def test_every_path_bit_exact(crum, variant, specs_name):
     """Device image (asynchronous: graph replay unless NO_GRAPH; synchronous
     with a report), host image and sync, epoch by epoch, every dirty ratio and
     FULL: image bytes, reports and snapshots equal the oracle's."""
     flags = dict(variants())[variant]
-    specs = {"fusable": FUSABLE, "fusable_big": FUSABLE_BIG, "mixed": MIXED}[specs_name]
+    specs = {"small": SMALL, "fusable": FUSABLE, "fusable_big": FUSABLE_BIG, "mixed": MIXED}[specs_name]
     small = sum(nb for nb, _, _ in specs) <= 64 * MiB
     p = mkpair(specs, 40, flags=flags)
     cap = p.g.image_required_bytes()
@@ -97,7 +99,9 @@ def test_every_path_bit_exact(crum, variant, specs_name):
         # single pass: compare-only, incremental, device image (the pinned
         # path of these footprints is the range pipeline), and either asked
         # for or a footprint <= 64 MiB (the default)
-        fused_eligible = (specs_name != "mixed" and how != "host" and not gflags and
+        # (a pinned image of the small footprint takes the small path too)
+        fused_eligible = (specs_name != "mixed" and not gflags and
+                          (how != "host" or specs_name == "small") and
                           (variant.startswith("fused") or small))
         assert bool(rep["path"] & crum.PATH_FUSED) == fused_eligible, (variant, epoch, how, rep["path"])
         assert p.shadows_equal(), (variant, epoch)
