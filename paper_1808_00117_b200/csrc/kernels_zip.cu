@@ -430,7 +430,9 @@ __global__ void __launch_bounds__(256) k_zpack(const uint8_t *stage, const uint1
         uint32_t *dw = reinterpret_cast<uint32_t *>(d + h);
         for (uint32_t i = lane; i < nw; i += 32) {
             const uint32_t p = h + 4 * i;  // source byte offset
-            dw[i] = __funnelshift_r(s[p >> 2], s[(p >> 2) + 1], 8 * (p & 3));
+            // the next word only when the source is misaligned (then it holds
+            // bytes of this encoding; otherwise it may lie past what was written)
+            dw[i] = __funnelshift_r(s[p >> 2], (p & 3) ? s[(p >> 2) + 1] : 0u, 8 * (p & 3));
         }
         const uint32_t t0 = h + 4 * nw;
         if (t0 + lane < sz) {

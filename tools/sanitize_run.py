@@ -85,4 +85,58 @@ path = os.path.join(tempfile.mkdtemp(), "img.crum")
 fz.persist(path)
 fz.persist_wait()
 assert r.load_image(path).tobytes() == fz.tobytes()
+# round 2 kernels: the one-launch small path (one page size), the single-pass
+# kernel (compare-only, two page sizes, small footprint), batch registration,
+# and the LZ77 + DEFLATE codec on structured data across two encode chunks
+from oracle import oracle
+def fresh(specs, seed, structured=False, **kw):
+    q2 = Pair(specs, synth.seed(seed), **kw)
+    if structured:
+        rng = np.random.default_rng(seed)
+        for h, d in zip(q2.host, q2.dev):
+            f = h[:h.nbytes // 8 * 8].view("<f8")
+            for b0 in range(0, f.size, 4096):
+                k = int(rng.integers(0, 4))
+                f[b0:b0 + 4096] = (np.sin(np.arange(min(4096, f.size - b0)) * 0.01) if k == 0 else
+                                   [0.0, 1.0, 1.0 / 6.0][k - 1])
+            d.copy_(torch.from_numpy(h))
+        torch.cuda.synchronize()
+    return q2
+for specs, seed in (([(1 * MiB, 4 * KiB, 0), (64 * KiB + 5, 4 * KiB, 2)], 50),
+                    ([(1 * MiB, 4 * KiB, 0), (3 * 64 * KiB + 9, 64 * KiB, 0)], 51)):
+    q2 = fresh(specs, seed)
+    im2 = q2.g.new_image()
+    c2 = q2.g.image_required_bytes()
+    b2 = torch.zeros(c2 + 256, dtype=torch.uint8, device="cuda")
+    for e, d in ((1, 0.2), (2, 0.0), (3, 1.0)):
+        q2.write(e, d)
+        for r_, (nb, P, m) in enumerate(specs):
+            if m == 2:
+                pgs = synth.choose_dirty(q2.S, e, r_, synth.n_pages(nb, P), d)
+                q2.o.mark_pages(r_ + 1, pgs)
+                q2.g.mark_dirty_pages(r_ + 1, torch.from_numpy(pgs.astype(np.uint32)).cuda(), len(pgs))
+        st, want, _ = q2.o.checkpoint_gather()
+        if e == 2:
+            q2.g.checkpoint_gather_device(b2, c2, report=False)
+            torch.cuda.synchronize()
+            got = b2[:len(want)].cpu().numpy().tobytes()
+        else:
+            q2.g.checkpoint_gather(im2)
+            got = im2.tobytes()
+        assert got == want.tobytes(), (seed, e)
+bq = crum.Context(0)
+bt = [torch.zeros(n, dtype=torch.uint8, device="cuda") for n in (65536, 8192 + 5, 4096 * 3)]
+assert bq.register_regions([(x, x.numel(), 4096, 0) for x in bt]) == [1, 2, 3]
+zq = fresh([(20 * MiB + 4096 * 3 + 7, 64 * KiB, 0), (2 * MiB, 4 * KiB, 1)], 52, structured=True)
+zi = zq.g.new_image()
+st, want, _ = zq.o.checkpoint_gather(flags=crum.COMPRESS)
+zq.g.checkpoint_gather(zi, flags=crum.COMPRESS)
+assert zi.tobytes() == want.tobytes()
+zr2 = crum.Context(0)
+zz = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for nb, _, _ in zq.specs]
+for z, (nb, P, m) in zip(zz, zq.specs):
+    zr2.register_region(z, nb, P, m)
+zr2.restore_scatter(zi, flags=crum.VERIFY)
+torch.cuda.synchronize()
+assert all(np.array_equal(z.cpu().numpy(), h) for z, h in zip(zz, zq.host))
 print("sanitize workload ok; launches", p.g.launch_count + q.launch_count + r.launch_count + t.launch_count)
