@@ -74,6 +74,9 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test the multi-rank path with several ranks sharing fewer GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="CRUM_CFG_FUSED: the single-pass kernel for compare-only contexts of any size "
+                         "(default: only up to 64 MiB)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--restore-full", action="store_true",
                     help="also time a FULL checkpoint (every page) into a pinned image and its restore onto the "
@@ -616,7 +619,7 @@ def main():
     if args.compress or args.content != "random":
         desc += f", content {args.content}" + (", compressed images" if args.compress else "")
     t_setup = time.perf_counter()
-    ctx = crum.Context(local, timing=True)
+    ctx = crum.Context(local, timing=True, flags=crum.CFG_FUSED if args.fused else 0)
     regions = []
     with torch.cuda.stream(stream):
         for r, (nb, P, mode) in enumerate(specs):

@@ -1734,8 +1734,20 @@ namespace {
 // dependent round trips) and one launch removes two of them.  Eligible: all
 // regions COMPARE with pages <= 64 KiB, an incremental gather, and an image
 // that holds the worst case (no capacity failure can occur mid-kernel).
+// Above kFusedSmallBytes the single pass also runs when the previous
+// checkpoint listed at least kFusedDirtyFrac of the pages: it reads each dirty
+// page once (2F + 2KP) where the multi-kernel path re-reads it (2F + 3KP) --
+// measured on C2 compare, device image: d = 1: 1760 vs 1201 GB/s; d = 0.1:
+// 2473 vs 2667 GB/s (profiles/r02/sweep/).  The previous call's K is read
+// from the mapped copy of its stats (possibly one call older: a heuristic only;
+// both paths produce the same image).
+constexpr double kFusedDirtyFrac = 0.25;
+
 bool use_fused(const crum_ctx *c, bool full, uint64_t capacity, uint64_t worst) {
-    return c->fused_ok && !full && capacity >= worst && (c->fused_cfg || c->F <= kFusedSmallBytes);
+    if (!c->fused_ok || full || capacity < worst) return false;
+    if (c->fused_cfg || c->F <= kFusedSmallBytes) return true;
+    const uint64_t prev_k = *reinterpret_cast<volatile const uint64_t *>(&c->h_st->K);
+    return c->N && prev_k <= c->N && (double)prev_k >= kFusedDirtyFrac * (double)c->N;
 }
 
 // The one-launch small path (k_small_ckpt): preferred over the single-pass
@@ -1808,11 +1820,7 @@ int enqueue_fused(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, 
     Launch L = launch_of(c, s);
     launch_fused_compare(L, fa, c->sms * c->fused_bps);
     if (timing) CK(cudaEventRecordWithFlags(c->ev_t[1], s, evf));
-    if (!fa.inline_meta) {
-        CrcArgs cra = crc_args(c, img, nullptr);
-        cra.st_host = nullptr;
-        launch_crc_meta(L, cra, crc_max_len(c));
-    }
+    if (!fa.inline_meta) launch_crc_meta(L, crc_args(c, img, nullptr), crc_max_len(c));  // stats -> mapped (use_fused)
     CK_LAUNCH();
     if (timing) CK(cudaEventRecordWithFlags(c->ev_t[4], s, evf));
     CK(cudaEventRecordWithFlags(c->ev_done, s, evf));
@@ -1834,8 +1842,7 @@ int enqueue_gather_dev(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capac
     // metadata CRC (+ tail, header) on a side stream beside the payload gather
     CK(cudaEventRecord(c->ev_fork, s));
     CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-    CrcArgs cra = crc_args(c, img, nullptr);
-    cra.st_host = nullptr;
+    CrcArgs cra = crc_args(c, img, nullptr);  // st_host: the stats reach mapped memory (use_fused)
     launch_crc_meta(launch_of(c, c->aux), cra, crc_max_len(c));
     CK(cudaEventRecord(c->ev_join, c->aux));
     Launch L = launch_of(c, s);
@@ -1853,7 +1860,12 @@ int enqueue_gather_dev(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capac
 // generation, then replayed on `s`.  CRUM_E_BUSY: capture unavailable, the
 // caller enqueues directly.
 int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, uint32_t flags, bool timing) {
-    flags |= timing ? 0x80000000u : 0u;  // the key includes whether events are recorded
+    uint64_t worst = 0;
+    crum_image_required_bytes(c, UINT64_MAX, &worst);
+    const bool small = use_small(c, (flags & CRUM_FULL) != 0, capacity, worst);
+    const bool fused = !small && use_fused(c, (flags & CRUM_FULL) != 0, capacity, worst);
+    // the key includes whether events are recorded and which sequence runs
+    flags |= (timing ? 0x80000000u : 0u) | (fused ? 0x40000000u : 0u) | (small ? 0x20000000u : 0u);
     crum_ctx::GraphEntry *e = nullptr, *victim = &c->graphs[0];
     for (auto &g : c->graphs) {
         if (g.exec && g.epoch == c->graph_epoch && g.img == img && g.cap == capacity && g.flags == flags) {
@@ -1873,10 +1885,6 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
             cudaGetLastError();
             return CRUM_E_BUSY;
         }
-        uint64_t worst = 0;
-        crum_image_required_bytes(c, UINT64_MAX, &worst);
-        const bool small = use_small(c, (flags & CRUM_FULL) != 0, capacity, worst);
-        const bool fused = !small && use_fused(c, (flags & CRUM_FULL) != 0, capacity, worst);
         const int st = small ? enqueue_small(c, c->gcap, img, capacity, timing, true)
                        : fused ? enqueue_fused(c, c->gcap, img, capacity, timing, true)
                                : enqueue_gather_dev(c, c->gcap, img, capacity, (flags & CRUM_FULL) != 0, timing, true);
@@ -2106,17 +2114,26 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
     int st;
     uint64_t worst = 0;
     crum_image_required_bytes(c, UINT64_MAX, &worst);
-    // The single-pass kernel is opt-in (CRUM_CFG_FUSED).
     if (flags & CRUM_COMPRESS) return gather_z(c, s, img, nullptr, capacity, full, timing, rep);
-    if (use_small(c, full, capacity, worst) || use_fused(c, full, capacity, worst)) {
+    if (!rep && c->graphs_on) {
+        // asynchronous call: replay the captured sequence (the one-launch small
+        // path, the single pass, or the multi-kernel sequence: chosen and
+        // keyed inside; one launch instead of ~8 API calls)
+        if ((st = gather_dev_graph(c, s, img, capacity, flags, timing)) != CRUM_E_BUSY) {
+            if (st == CRUM_OK) {
+                c->last_timed = timing;
+                c->last_path = 0;
+            }
+            return st;
+        }
+        // capture not possible here: enqueue directly
+    }
+    const bool small = use_small(c, full, capacity, worst);
+    if (small || use_fused(c, full, capacity, worst)) {
         // single pass: detect + compact + gather + commit in one kernel (the
         // small path also writes the metadata; the single-pass kernel is
-        // followed by the metadata CRC / tail / header); a replayed graph
-        // when asynchronous
-        st = (!rep && c->graphs_on) ? gather_dev_graph(c, s, img, capacity, flags, timing) : CRUM_E_BUSY;
-        if (st == CRUM_E_BUSY)
-            st = use_small(c, full, capacity, worst) ? enqueue_small(c, s, img, capacity, timing)
-                                                     : enqueue_fused(c, s, img, capacity, timing);
+        // followed by the metadata CRC / tail / header)
+        st = small ? enqueue_small(c, s, img, capacity, timing) : enqueue_fused(c, s, img, capacity, timing);
         if (st) return st;
         c->last_kind = kLastDevFused;
         c->last_path = 0;
@@ -2129,20 +2146,6 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
             fill_times(c, rep);
         }
         return CRUM_OK;
-    }
-    const bool graphs_on = c->graphs_on;
-    if (!rep && graphs_on) {
-        // asynchronous call: replay the captured sequence (one launch instead of
-        // ~8 API calls; the small configurations are launch-bound)
-        if ((st = gather_dev_graph(c, s, img, capacity, flags, timing)) != CRUM_E_BUSY) {
-            if (st == CRUM_OK) {
-                c->last_kind = kLastDevGather;
-                c->last_timed = timing;
-                c->last_path = 0;
-            }
-            return st;
-        }
-        // capture not possible here: enqueue directly
     }
     if ((st = enqueue_gather_dev(c, s, img, capacity, full, timing))) return st;
     c->last_path = 0;

@@ -74,12 +74,15 @@ def test_every_path_bit_exact(crum, variant, specs_name):
     seq = [(0, 0.0, 0, "dev_async"), (1, 0.1, 0, "dev_async"), (2, 0.5, 0, "dev_sync"), (3, 0.0, 0, "dev_async"),
            (4, 1.0, 0, "host"), (5, 0.2, crum.FULL, "dev_async"), (6, 0.3, 0, "sync"), (7, 0.05, 0, "dev_async"),
            (8, 0.7, 0, "host"), (9, 0.0, 0, "dev_sync")]
+    prev_frac = 0.0  # dirty fraction of the previous call (the adaptive single-pass rule)
     for epoch, d, gflags, how in seq:
         if epoch:
             p.write(epoch, d)
         if how == "sync":
-            assert p.g.sync_shadow() == p.o.sync_shadow()
+            n = p.g.sync_shadow()
+            assert n == p.o.sync_shadow()
             assert p.shadows_equal()
+            prev_frac = n / p.N
             continue
         st, want, rep_o = p.o.checkpoint_gather(flags=gflags)
         assert st == 0
@@ -100,9 +103,12 @@ def test_every_path_bit_exact(crum, variant, specs_name):
         # path of these footprints is the range pipeline), and either asked
         # for or a footprint <= 64 MiB (the default)
         # (a pinned image of the small footprint takes the small path too)
+        # Above 64 MiB the single pass also runs when the previous call listed
+        # >= 25 % of the pages (adaptive rule)
         fused_eligible = (specs_name != "mixed" and not gflags and
                           (how != "host" or specs_name == "small") and
-                          (variant.startswith("fused") or small))
+                          (variant.startswith("fused") or small or prev_frac >= 0.25))
+        prev_frac = rep_o["dirty_pages"] / p.N
         assert bool(rep["path"] & crum.PATH_FUSED) == fused_eligible, (variant, epoch, how, rep["path"])
         assert p.shadows_equal(), (variant, epoch)
 
