@@ -66,7 +66,7 @@ def main():
 
     def demangle(n):
         r = subprocess.run(["c++filt", n], capture_output=True, text=True)
-        d = r.stdout.strip() or n
+        d = (r.stdout.strip() or n).replace("(anonymous namespace)::", "")
         return d.split("(")[0]
 
     cols = ["instructions"] + [p[0] for p in PATTERNS]
