@@ -205,6 +205,7 @@ struct FusedArgs {
     uint32_t *reg_nd;
     RegStat *rs;
     DevStats *st;
+    DevStats *st_host;        // inline_meta: mapped pinned copy of the final stats
     uint64_t capacity;
 };
 void launch_fused_compare(const Launch &L, const FusedArgs &a, int blocks);
@@ -229,6 +230,7 @@ struct SmallArgs {
     uint64_t poff;
     uint64_t capacity;
     DevStats *st;
+    DevStats *st_host;        // mapped pinned copy of the final stats (the host reads it after the kernel)
     X2N x2n;
 };
 void launch_small_ckpt(const Launch &L, const SmallArgs &a, int blocks);

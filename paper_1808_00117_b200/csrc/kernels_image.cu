@@ -1013,6 +1013,11 @@ __device__ __noinline__ void fused_inline_meta(const FusedArgs &a, uint64_t K, u
     for (int i = 0; i < 60; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
     put32(h + 60, hc ^ 0xffffffffu);
     for (int i = 0; i < 64; ++i) a.img[i] = h[i];
+    if (a.st_host) {  // the host reads the report without a copy
+        const uint64_t *src = reinterpret_cast<const uint64_t *>(st);
+        volatile uint64_t *dst = reinterpret_cast<volatile uint64_t *>(a.st_host);
+        for (uint32_t i = 0; i < sizeof(DevStats) / 8; ++i) dst[i] = src[i];
+    }
 }
 
 // Each WARP owns one tile at a time: no block barriers, so while one warp
@@ -1472,6 +1477,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     for (int i = 0; i < 60; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
     put32(h + 60, hc ^ 0xffffffffu);
     for (int i = 0; i < 64; ++i) img[i] = h[i];
+    if (a.st_host) {  // the host reads the report without a copy
+        const uint64_t *src = reinterpret_cast<const uint64_t *>(st);
+        volatile uint64_t *dst = reinterpret_cast<volatile uint64_t *>(a.st_host);
+        for (uint32_t i = 0; i < sizeof(DevStats) / 8; ++i) dst[i] = src[i];
+    }
 }
 
 int small_blocks_per_sm() {

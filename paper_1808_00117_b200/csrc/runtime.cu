@@ -1771,6 +1771,7 @@ int enqueue_small(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, 
     sa.poff = payload_offset_for(c->regs.size());
     sa.capacity = capacity;
     sa.st = c->d_st;
+    sa.st_host = c->dh_st;
     sa.x2n = crc_tables().x2n;
     const uint64_t warps = c->N << (c->small_log2p - kSegLog2);
     uint64_t blocks = (warps + 7) / 8;
@@ -1816,6 +1817,7 @@ int enqueue_fused(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, 
     fa.lids = c->d_lids;
     fa.rs = c->d_rs;
     fa.st = c->d_st;
+    fa.st_host = c->dh_st;
     fa.capacity = capacity;
     Launch L = launch_of(c, s);
     launch_fused_compare(L, fa, c->sms * c->fused_bps);
@@ -2215,7 +2217,8 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
         if (st) return st;  // (gather_dev_graph set last_kind)
         c->last_path = 0;
         c->last_timed = true;
-        CK(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+        // every small-footprint sequence's last kernel stores the final stats
+        // into the mapped h_st: no copy, only the wait
         CK(cudaStreamSynchronize(s));
         const DevStats h = *c->h_st;
         img->len = h.image_bytes;
