@@ -83,6 +83,8 @@ struct RangeTotals {
 struct X2N {
     uint32_t t[32];   // x^(2^k) mod P (reflected CRC-32 polynomial)
     uint32_t pw[32];  // x^(8 * 64 * j) mod P: shift by j 64-byte chunks
+    uint32_t lpw[32]; // x^(8 * 16 * j) mod P: shift by j 16-byte chunks
+    uint32_t wpw[8];  // x^(8 * 512 * w) mod P: shift by w warps of 16-byte chunks
 };
 
 struct Launch {

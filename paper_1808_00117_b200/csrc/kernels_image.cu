@@ -540,6 +540,45 @@ __device__ __forceinline__ uint32_t xpow8n(uint64_t n, const uint32_t *x2n) {
     return p;
 }
 
+// The same product in a fixed 32 steps without branches: for operands that
+// differ across the lanes of a warp, where the early exit above diverges.
+__device__ __forceinline__ uint32_t gf2_mulmod_bf(uint32_t a, uint32_t b) {
+    uint32_t p = 0;
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+        p ^= b & (0u - ((a >> i) & 1u));
+        b = (b >> 1) ^ (0xEDB88320u & (0u - (b & 1u)));
+    }
+    return p;
+}
+
+// Raw CRC registers of 16-byte chunks counted from the END of a word stream
+// (chunk q is followed by 16 q bytes, so it is placed by x^(128 q)).  Thread
+// t of n takes chunks t, t + n, ... and folds them by Horner with
+// rpw = x^(128 n); the result still needs x^(128 t).  The (possibly short)
+// chunk holding word 0 carries zlib's ~0 initial register.
+template <class WordFn>
+__device__ __forceinline__ uint32_t crc_chunks_from_end(const WordFn &word, uint64_t nw, uint32_t t, uint32_t n,
+                                                        uint32_t rpw, const uint32_t *T) {
+    const uint64_t nchunks = (nw + 3) / 4;
+    uint32_t acc = 0;
+    for (uint64_t r = (nchunks + n - 1) / n; r-- > 0;) {
+        if (acc) acc = gf2_mulmod_bf(rpw, acc);
+        const uint64_t q = r * n + t;
+        if (q < nchunks) {
+            const uint64_t wend = nw - 4 * q, wbeg = wend > 4 ? wend - 4 : 0;
+            uint32_t c = wbeg == 0 ? 0xffffffffu : 0u;
+            for (uint64_t w = wbeg; w < wend; ++w) {
+                const uint32_t v = word(w);
+#pragma unroll
+                for (int b = 0; b < 4; ++b) c = T[(c ^ (v >> (8 * b))) & 0xffu] ^ (c >> 8);
+            }
+            acc ^= c;
+        }
+    }
+    return acc;
+}
+
 __device__ __forceinline__ void put32(uint8_t *p, uint32_t v) {
     for (int i = 0; i < 4; ++i) p[i] = (uint8_t)(v >> (8 * i));
 }
@@ -980,18 +1019,15 @@ __device__ __noinline__ void fused_inline_meta(const FusedArgs &a, uint64_t K, u
     for (uint64_t k = lane; k < K; k += 32) runs += (k == 0 || a.lids[k] == 0 || a.gids[k - 1] + 1 != a.gids[k]) ? 1 : 0;
     runs = warp_sum(runs);
     __syncwarp();
-    // CRC of table (12 R words at img + 64) || ids (idsw words, from lids)
+    // CRC of table (12 R words at img + 64) || ids (idsw words, from lids):
+    // 16-byte chunks from the end, lane j's placed by x^(128 j)
     const uint64_t tabw = 12ull * a.R, nw = tabw + idsw;
-    const uint64_t cw = (nw + 31) / 32;
-    const uint64_t w0 = min(nw, lane * cw), w1 = min(nw, w0 + cw);
     const uint32_t *tab = reinterpret_cast<const uint32_t *>(a.img + 64);
-    uint32_t c = (w0 == 0 && w1 > 0) ? 0xffffffffu : 0u;
-    for (uint64_t w = w0; w < w1; ++w) {
-        const uint32_t v = w < tabw ? tab[w] : ((w - tabw) < K ? a.lids[w - tabw] : 0u);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) c = T[(c ^ (v >> (8 * b))) & 0xffu] ^ (c >> 8);
-    }
-    uint32_t term = (w1 > w0) ? gf2_mulmod(xpow8n(4 * (nw - w1), a.x2n.t), c) : 0u;
+    auto word = [&](uint64_t w) -> uint32_t {
+        return w < tabw ? tab[w] : ((w - tabw) < K ? a.lids[w - tabw] : 0u);
+    };
+    uint32_t term = crc_chunks_from_end(word, nw, lane, 32, a.x2n.t[12], T);
+    term = gf2_mulmod_bf(a.x2n.lpw[lane], term);
 #pragma unroll
     for (int o = 16; o; o >>= 1) term ^= __shfl_xor_sync(0xffffffffu, term, o);
     if (lane != 0) return;
@@ -1266,6 +1302,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     __shared__ uint32_t s_bm[kSmallWords];    // dirty bitmap
     __shared__ uint32_t s_pre[kSmallWords + 1];  // dirty pages before word w
     __shared__ uint32_t T[256];                // CRC-32 byte table (CTA 0)
+    __shared__ uint32_t s_lpw[32];             // x^(128 j) mod P (CTA 0)
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t wid = ((uint64_t)blockIdx.x * kSmallThreads + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * kSmallThreads) >> 5;
@@ -1376,6 +1413,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     __syncthreads();
     uint32_t *other = a.bitmap + (par ^ 1u) * kSmallWords;
     for (uint32_t w = threadIdx.x; w < nw; w += kSmallThreads) other[w] = 0;
+    if (threadIdx.x < 32) s_lpw[threadIdx.x] = a.x2n.lpw[threadIdx.x];
     for (uint32_t i = threadIdx.x; i < 256; i += kSmallThreads) {
         uint32_t c = i;
         for (int b = 0; b < 8; ++b) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
@@ -1400,7 +1438,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         reinterpret_cast<uint64_t *>(e)[4] = nd;
         reinterpret_cast<uint64_t *>(e)[5] = first;
     }
-    for (uint64_t b = 64 + 48ull * a.R + threadIdx.x; b < poff; b += kSmallThreads) img[b] = 0;
+    // zero padding to the payload: 16-byte stores (64 + 48 R and poff are multiples of 16)
+    for (uint64_t b = 64 + 48ull * a.R + 16ull * threadIdx.x; b < poff; b += 16ull * kSmallThreads)
+        *reinterpret_cast<uint4 *>(img + b) = make_uint4(0, 0, 0, 0);
     // ids (region-local page indices), runs, logical bytes
     uint32_t *tids = reinterpret_cast<uint32_t *>(img + ids_off);
     uint64_t runs = 0, dbytes = 0;
@@ -1425,23 +1465,55 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     block_excl_scan(runs, &tot_runs);
     block_excl_scan(dbytes, &tot_bytes);
     __syncthreads();  // table, ids and padding written
-    // CRC-32 of table (12 R words) || ids (idsw words): thread chunks, shifted into place
+    // CRC-32 of table (12 R words) || ids (idsw words), 16-byte chunks from
+    // the end.  The words are recomputed here, not read back from the image
+    // (which may be a pinned image behind the host link).
     const uint64_t tabw = 12ull * a.R, nwords = tabw + idsw;
-    const uint64_t cw = (nwords + kSmallThreads - 1) / kSmallThreads;
-    const uint64_t w0 = min(nwords, threadIdx.x * cw), w1 = min(nwords, w0 + cw);
-    const uint32_t *tab = reinterpret_cast<const uint32_t *>(img + 64);
-    uint32_t c = (w0 == 0 && w1 > 0) ? 0xffffffffu : 0u;
-    for (uint64_t w = w0; w < w1; ++w) {
-        const uint32_t v = w < tabw ? tab[w] : tids[w - tabw];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) c = T[(c ^ (v >> (8 * b))) & 0xffu] ^ (c >> 8);
-    }
-    const uint32_t term = (w1 > w0) ? gf2_mulmod(xpow8n(4 * (nwords - w1), a.x2n.t), c) : 0u;
-    __shared__ uint32_t s_x[kSmallThreads / 32];
-    uint32_t x = term;
+    uint32_t cr = 0;  // region cursor for the ids
+    auto word = [&](uint64_t w) -> uint32_t {
+        if (w < tabw) {
+            const DevRegion &R = a.regs[w / 12];
+            uint64_t f = 0;
+            switch ((uint32_t)(w % 12) >> 1) {
+                case 0: f = ((uint64_t)R.mode << 32) | R.id; break;
+                case 1: f = R.bytes; break;
+                case 2: f = P; break;
+                case 3: f = R.n_pages; break;
+                case 4: f = prefix_at(R.page_base + R.n_pages) - prefix_at(R.page_base); break;
+                default: f = prefix_at(R.page_base); break;
+            }
+            return (uint32_t)(f >> (32 * (w & 1)));
+        }
+        if (w - tabw >= K) return 0u;
+        const uint64_t pg = page_of(w - tabw);
+        while (cr + 1 < a.R && a.regs[cr + 1].page_base <= pg) ++cr;
+        while (a.regs[cr].page_base > pg) --cr;
+        return (uint32_t)(pg - a.regs[cr].page_base);
+    };
+    // thread t = 32 w + lane is placed by x^(128 t) = x^(128 lane) x^(4096 w)
+    uint32_t x = crc_chunks_from_end(word, nwords, threadIdx.x, kSmallThreads, a.x2n.t[15], T);
+    x = gf2_mulmod_bf(s_lpw[lane], x);
 #pragma unroll
     for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) s_x[threadIdx.x >> 5] = x;
+    __shared__ uint32_t s_x[kSmallThreads / 32];
+    __shared__ uint32_t s_hc;
+    if (lane == 0) s_x[threadIdx.x >> 5] = gf2_mulmod_bf(a.x2n.wpw[threadIdx.x >> 5], x);
+    // the header's first 56 bytes are known already: their CRC beside the others
+    alignas(16) uint8_t h[64];
+    h[0] = 'C'; h[1] = 'R'; h[2] = 'U'; h[3] = 'M';
+    put32(h + 4, 1);
+    put32(h + 8, 0);
+    put32(h + 12, a.R);
+    put64(h + 16, K);
+    put64(h + 24, poff);
+    put64(h + 32, payload);
+    put64(h + 40, ids_off);
+    put64(h + 48, ids_off + 4 * idsw);
+    if (threadIdx.x == 32) {
+        uint32_t hc = 0xffffffffu;
+        for (int i = 0; i < 56; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
+        s_hc = hc;
+    }
     __syncthreads();
     if (threadIdx.x != 0) return;
     uint32_t acc = 0;
@@ -1462,21 +1534,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     st->dirty_runs = tot_runs;
     st->crc_acc = 0;
     st->meta_crc = meta_crc;
-    uint8_t h[64];
-    h[0] = 'C'; h[1] = 'R'; h[2] = 'U'; h[3] = 'M';
-    put32(h + 4, 1);
-    put32(h + 8, 0);
-    put32(h + 12, a.R);
-    put64(h + 16, K);
-    put64(h + 24, poff);
-    put64(h + 32, payload);
-    put64(h + 40, ids_off);
-    put64(h + 48, ids_off + 4 * idsw);
     put32(h + 56, meta_crc);
-    uint32_t hc = 0xffffffffu;
-    for (int i = 0; i < 60; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
+    uint32_t hc = s_hc;
+    for (int i = 56; i < 60; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
     put32(h + 60, hc ^ 0xffffffffu);
-    for (int i = 0; i < 64; ++i) img[i] = h[i];
+    for (int i = 0; i < 64; i += 16) *reinterpret_cast<uint4 *>(img + i) = *reinterpret_cast<const uint4 *>(h + i);
     if (a.st_host) {  // the host reads the report without a copy
         const uint64_t *src = reinterpret_cast<const uint64_t *>(st);
         volatile uint64_t *dst = reinterpret_cast<volatile uint64_t *>(a.st_host);

@@ -90,6 +90,11 @@ const CrcTables &crc_tables() {
         // pw[j] = x^(512 j): x^512 = x^(2^9)
         c.x2n.pw[0] = 0x80000000u;  // x^0
         for (int j = 1; j < 32; ++j) c.x2n.pw[j] = gf2_mulmod_host(c.x2n.t[9], c.x2n.pw[j - 1]);
+        // lpw[j] = x^(128 j) (x^128 = x^(2^7)), wpw[w] = x^(4096 w) (x^(2^12))
+        c.x2n.lpw[0] = 0x80000000u;
+        for (int j = 1; j < 32; ++j) c.x2n.lpw[j] = gf2_mulmod_host(c.x2n.t[7], c.x2n.lpw[j - 1]);
+        c.x2n.wpw[0] = 0x80000000u;
+        for (int w = 1; w < 8; ++w) c.x2n.wpw[w] = gf2_mulmod_host(c.x2n.t[12], c.x2n.wpw[w - 1]);
         return c;
     }();
     return t;

@@ -1,0 +1,32 @@
+# Temporary phase timestamps in k_small_ckpt (CTA 0, thread 0 prints) -- a
+# profiling aid applied on the GPU box only (tools/gpu_r02x.sh)
+p='paper_1808_00117_b200/csrc/kernels_image.cu'
+s=open(p).read()
+s='#include <cstdio>\n'+s
+def ins(anchor, text, after=False):
+    global s
+    assert anchor in s, anchor
+    s=s.replace(anchor, (anchor+text) if after else (text+anchor), 1)
+ins('__global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {',
+    '__device__ __forceinline__ uint64_t gtimer() { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }\n')
+ins('__global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {', '\n    const uint64_t T0 = gtimer();', after=True)
+ins('    grid_barrier(a.bar);\n', '    const uint64_t T1 = gtimer();\n')
+ins('    grid_barrier(a.bar);\n', '    const uint64_t T2 = gtimer();\n', after=True)
+ins('    const uint64_t K = s_pre[nw];\n', '    const uint64_t T3 = gtimer();\n', after=True)
+ins('    // ids (region-local page indices), runs, logical bytes\n', '    const uint64_t T4 = gtimer();\n')
+ins('    uint64_t tot_runs, tot_bytes;\n', '    const uint64_t T5 = gtimer();\n')
+ins('    // thread t = 32 w + lane is placed by', '    const uint64_t T6 = gtimer();\n')
+ins('    if (threadIdx.x != 0) return;\n    uint32_t acc = 0;', '    const uint64_t T7 = gtimer();\n')
+ins('''    if (a.st_host) {  // the host reads the report without a copy
+        const uint64_t *src = reinterpret_cast<const uint64_t *>(st);
+        volatile uint64_t *dst = reinterpret_cast<volatile uint64_t *>(a.st_host);
+        for (uint32_t i = 0; i < sizeof(DevStats) / 8; ++i) dst[i] = src[i];
+    }
+}
+
+int small_blocks_per_sm''', '''    printf("small: detect %llu barrier %llu prefix %llu table+pad %llu ids %llu scans %llu crc %llu hdr %llu ns K=%llu\\n",
+           (unsigned long long)(T1 - T0), (unsigned long long)(T2 - T1), (unsigned long long)(T3 - T2),
+           (unsigned long long)(T4 - T3), (unsigned long long)(T5 - T4), (unsigned long long)(T6 - T5),
+           (unsigned long long)(T7 - T6), (unsigned long long)(gtimer() - T7), (unsigned long long)K);
+''')
+open(p,'w').write(s)
