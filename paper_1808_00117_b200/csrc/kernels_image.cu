@@ -1277,6 +1277,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
 // ---------------------------------------------------------------------------
 constexpr uint32_t kSmallThreads = 256;
 constexpr uint32_t kSmallWords = kSmallPages / 32;
+constexpr uint32_t kSmallStageWords = 2048;  // metadata words CTA 0 keeps in shared memory
 
 // Grid barrier of a cooperative launch (all CTAs co-resident): arrivals
 // counter + generation, sense by generation, state returns to 0 arrivals.
@@ -1303,6 +1304,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     __shared__ uint32_t s_pre[kSmallWords + 1];  // dirty pages before word w
     __shared__ uint32_t T[256];                // CRC-32 byte table (CTA 0)
     __shared__ uint32_t s_lpw[32];             // x^(128 j) mod P (CTA 0)
+    __shared__ uint32_t s_w[kSmallStageWords]; // table || ids words for the CRC (CTA 0)
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t wid = ((uint64_t)blockIdx.x * kSmallThreads + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * kSmallThreads) >> 5;
@@ -1437,6 +1439,16 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         reinterpret_cast<uint64_t *>(e)[3] = R.n_pages;
         reinterpret_cast<uint64_t *>(e)[4] = nd;
         reinterpret_cast<uint64_t *>(e)[5] = first;
+        if (12 * rr + 12 <= kSmallStageWords) {
+            uint32_t *sw = s_w + 12 * rr;
+            sw[0] = R.id;
+            sw[1] = R.mode;
+            sw[2] = (uint32_t)R.bytes;   sw[3] = (uint32_t)(R.bytes >> 32);
+            sw[4] = (uint32_t)P;         sw[5] = (uint32_t)(P >> 32);
+            sw[6] = (uint32_t)R.n_pages; sw[7] = (uint32_t)(R.n_pages >> 32);
+            sw[8] = (uint32_t)nd;        sw[9] = (uint32_t)(nd >> 32);
+            sw[10] = (uint32_t)first;    sw[11] = (uint32_t)(first >> 32);
+        }
     }
     // zero padding to the payload: 16-byte stores (64 + 48 R and poff are multiples of 16)
     for (uint64_t b = 64 + 48ull * a.R + 16ull * threadIdx.x; b < poff; b += 16ull * kSmallThreads)
@@ -1449,6 +1461,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         for (uint64_t k = threadIdx.x; k < idsw; k += kSmallThreads) {
             if (k >= K) {
                 tids[k] = 0;
+                if (12ull * a.R + k < kSmallStageWords) s_w[12 * a.R + k] = 0;
                 continue;
             }
             const uint64_t pg = page_of(k);
@@ -1457,6 +1470,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
             const DevRegion &R = a.regs[rr];
             const uint64_t i = pg - R.page_base;
             tids[k] = (uint32_t)i;
+            if (12ull * a.R + k < kSmallStageWords) s_w[12 * a.R + k] = (uint32_t)i;
             runs += (i == 0 || !((s_bm[(pg - 1) >> 5] >> ((pg - 1) & 31)) & 1u)) ? 1 : 0;
             dbytes += min(P, R.bytes - (i << a.log2p));
         }
@@ -1466,11 +1480,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     block_excl_scan(dbytes, &tot_bytes);
     __syncthreads();  // table, ids and padding written
     // CRC-32 of table (12 R words) || ids (idsw words), 16-byte chunks from
-    // the end.  The words are recomputed here, not read back from the image
-    // (which may be a pinned image behind the host link).
+    // the end.  The words come from the shared-memory stage, beyond it they
+    // are recomputed -- never read back from the image (which may be a pinned
+    // image behind the host link).
     const uint64_t tabw = 12ull * a.R, nwords = tabw + idsw;
     uint32_t cr = 0;  // region cursor for the ids
     auto word = [&](uint64_t w) -> uint32_t {
+        if (w < kSmallStageWords && (w >= tabw || 12 * (w / 12) + 12 <= kSmallStageWords)) return s_w[w];
         if (w < tabw) {
             const DevRegion &R = a.regs[w / 12];
             uint64_t f = 0;

@@ -17,6 +17,9 @@ ins('    // ids (region-local page indices), runs, logical bytes\n', '    const 
 ins('    uint64_t tot_runs, tot_bytes;\n', '    const uint64_t T5 = gtimer();\n')
 ins('    // thread t = 32 w + lane is placed by', '    const uint64_t T6 = gtimer();\n')
 ins('    if (threadIdx.x != 0) return;\n    uint32_t acc = 0;', '    const uint64_t T7 = gtimer();\n')
+ins('    x = gf2_mulmod_bf(s_lpw[lane], x);\n', '    asm volatile("" :: "r"(x));\n    const uint64_t T6a = gtimer();\n')
+ins('    // the header\'s first 56 bytes are known already', '    asm volatile("" :: "r"(x));\n    const uint64_t T6b = gtimer();\n')
+ins('    __syncthreads();\n    const uint64_t T7', '    const uint64_t T6c = gtimer();\n')
 ins('''    if (a.st_host) {  // the host reads the report without a copy
         const uint64_t *src = reinterpret_cast<const uint64_t *>(st);
         volatile uint64_t *dst = reinterpret_cast<volatile uint64_t *>(a.st_host);
@@ -24,7 +27,7 @@ ins('''    if (a.st_host) {  // the host reads the report without a copy
     }
 }
 
-int small_blocks_per_sm''', '''    printf("small: detect %llu barrier %llu prefix %llu table+pad %llu ids %llu scans %llu crc %llu hdr %llu ns K=%llu\\n",
+int small_blocks_per_sm''', '''    printf("small: chunks %llu place %llu hdr56 %llu sync %llu | detect %llu barrier %llu prefix %llu table+pad %llu ids %llu scans %llu crc %llu hdr %llu ns K=%llu\\n", (unsigned long long)(T6a - T6), (unsigned long long)(T6b - T6a), (unsigned long long)(T6c - T6b), (unsigned long long)(T7 - T6c),
            (unsigned long long)(T1 - T0), (unsigned long long)(T2 - T1), (unsigned long long)(T3 - T2),
            (unsigned long long)(T4 - T3), (unsigned long long)(T5 - T4), (unsigned long long)(T6 - T5),
            (unsigned long long)(T7 - T6), (unsigned long long)(gtimer() - T7), (unsigned long long)K);
