@@ -130,7 +130,11 @@ CRUM_API int crum_config_init(crum_config *cfg);
 /* crum_config.flags.
  *   CRUM_CFG_TIMING   record CUDA events around the phases of EVERY call (also
  *                     asynchronous ones), so crum_last_report can return phase
- *                     times without the call itself waiting.
+ *                     times without the call itself waiting.  The one-launch
+ *                     small-footprint kernel times itself instead (globaltimer
+ *                     stamps, see CRUM_PATH_SMALL).  Calls that return a report
+ *                     (pinned-image gathers, synchronous device gathers) time
+ *                     themselves with or without this flag.
  *   CRUM_CFG_NO_GRAPH never replay a captured CUDA graph for asynchronous device
  *                     gathers (every launch is enqueued directly).
  *   CRUM_CFG_FUSED    device-image gathers of a context whose regions are all
@@ -162,11 +166,16 @@ typedef struct {
                                 (t_detect_ms then covers all three, t_gather_ms is 0);
                                 bit1 CRUM_PATH_COMPRESSED: compressed gather (t_compact_ms includes
                                 the encoded-size pass, t_gather_ms is encode + commit, including
-                                the host-link stores for a pinned image; t_copy_ms is 0) */
+                                the host-link stores for a pinned image; t_copy_ms is 0);
+                                bit2 CRUM_PATH_SMALL (with bit0): the one-launch small-footprint
+                                kernel, which also writes the metadata; with CRUM_CFG_TIMING it
+                                times itself (globaltimer, first CTA in -> last CTA out), so
+                                t_detect_ms = t_total_ms = the kernel, and no events are recorded
+                                around it */
     uint32_t reserved;
 } crum_report;
 
-enum { CRUM_PATH_FUSED = 1u << 0, CRUM_PATH_COMPRESSED = 1u << 1 };
+enum { CRUM_PATH_FUSED = 1u << 0, CRUM_PATH_COMPRESSED = 1u << 1, CRUM_PATH_SMALL = 1u << 2 };
 
 /* ---------------------------------------------------------------------------
  * Context.  crum_create binds to CUDA device `device` (cudaSetDevice is

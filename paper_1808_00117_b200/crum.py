@@ -32,7 +32,7 @@ FULL, VERIFY, COMPRESS = 1, 2, 4
 MODE_TRACKED = 2
 CFG_TIMING, CFG_NO_GRAPH, CFG_FUSED, CFG_TRACE = 1, 2, 4, 8
 NUMA_AUTO, NUMA_DEFAULT = -1, -2
-PATH_FUSED, PATH_COMPRESSED = 1, 2
+PATH_FUSED, PATH_COMPRESSED, PATH_SMALL = 1, 2, 4
 PERSIST_FSYNC, PERSIST_DIRECT = 1, 2
 EXPORT_FORCE, EXPORT_HASHES, EXPORT_MIRROR = 0, 1, 2
 ALL_PAGES = (1 << 64) - 1

@@ -72,6 +72,7 @@ struct DevStats {
     uint32_t n_regions;
     uint32_t meta_crc;       // final zlib CRC-32 of table || ids || hashes
     uint32_t pad0;
+    uint64_t t_ns;           // small path, timed: first CTA in -> last CTA out (globaltimer ns)
 };
 
 // Running totals of the compaction before range c (rb[c]); rb[0] = {0, 0}.
@@ -226,7 +227,8 @@ struct SmallArgs {
     uint32_t log2p;           // the context's one page size
     uint64_t N;               // pages
     uint32_t *bitmap;         // 2 x kSmallPages bits: dirty pages (alternating, zero when a launch begins)
-    uint32_t *bar;            // [0] arrivals, [1] generation (grid barrier; persists across launches)
+    uint32_t *bar;            // [0] arrivals, [1] generation (grid barrier; persists across launches),
+                              // [2] CTAs out, [4..5] ~(earliest CTA entry, ns) when timed; [0], [2], [4..5] end at 0
     uint8_t *force;
     uint8_t *img;             // image (payload at poff)
     uint64_t poff;
@@ -234,6 +236,7 @@ struct SmallArgs {
     DevStats *st;
     DevStats *st_host;        // mapped pinned copy of the final stats (the host reads it after the kernel)
     X2N x2n;
+    uint32_t timing;          // record t_ns (the kernel's own duration) in the stats
 };
 void launch_small_ckpt(const Launch &L, const SmallArgs &a, int blocks);
 int small_blocks_per_sm();

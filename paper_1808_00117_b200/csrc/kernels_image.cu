@@ -1299,6 +1299,31 @@ __device__ __forceinline__ void grid_barrier(uint32_t *bar) {
     __syncthreads();
 }
 
+__device__ __forceinline__ uint64_t gtime_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Every CTA leaves through here (thread 0, after its CTA's work): the last one
+// out publishes the stats to the host -- with the kernel's own duration when
+// timed -- and returns the scratch words to 0 for the next launch.
+__device__ __forceinline__ void small_leave(const SmallArgs &a) {
+    __threadfence();
+    if (atomicAdd(a.bar + 2, 1u) != gridDim.x - 1) return;
+    __threadfence();
+    volatile unsigned long long *t0 = reinterpret_cast<volatile unsigned long long *>(a.bar + 4);
+    DevStats *st = a.st;
+    st->t_ns = a.timing ? gtime_ns() - ~*t0 : 0;
+    *t0 = 0;
+    a.bar[2] = 0;
+    if (a.st_host) {  // the host reads the report without a copy
+        const volatile uint64_t *src = reinterpret_cast<const volatile uint64_t *>(st);
+        volatile uint64_t *dst = reinterpret_cast<volatile uint64_t *>(a.st_host);
+        for (uint32_t i = 0; i < sizeof(DevStats) / 8; ++i) dst[i] = src[i];
+    }
+}
+
 __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     __shared__ uint32_t s_bm[kSmallWords];    // dirty bitmap
     __shared__ uint32_t s_pre[kSmallWords + 1];  // dirty pages before word w
@@ -1313,6 +1338,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     // two bitmaps: this launch uses bitmap[gen & 1] (the barrier generation,
     // the same for every CTA until the barrier), CTA 0 clears the other one
     // for the next launch (a CTA may still read this launch's after CTA 0 is done)
+    if (a.timing && threadIdx.x == 0)  // the max of ~t is the earliest entry
+        atomicMax(reinterpret_cast<unsigned long long *>(a.bar + 4), ~(unsigned long long)gtime_ns());
     const uint32_t par = *reinterpret_cast<volatile uint32_t *>(a.bar + 1) & 1u;
     uint32_t *bitmap = a.bitmap + par * kSmallWords;
     // ---- A1 detect: warp per 4 KiB segment; forced pages are dirty unread ----
@@ -1409,7 +1436,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
             }
             if (lane == 0) a.force[pg] = 0;
         }
-        if (blockIdx.x != 0) return;
+        if (blockIdx.x != 0) {
+            __syncthreads();
+            if (threadIdx.x == 0) small_leave(a);
+            return;
+        }
     }
     // ---- CTA 0: bitmap cleared for the next launch, table, ids, CRC, header ----
     __syncthreads();
@@ -1555,11 +1586,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     for (int i = 56; i < 60; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
     put32(h + 60, hc ^ 0xffffffffu);
     for (int i = 0; i < 64; i += 16) *reinterpret_cast<uint4 *>(img + i) = *reinterpret_cast<const uint4 *>(h + i);
-    if (a.st_host) {  // the host reads the report without a copy
-        const uint64_t *src = reinterpret_cast<const uint64_t *>(st);
-        volatile uint64_t *dst = reinterpret_cast<volatile uint64_t *>(a.st_host);
-        for (uint32_t i = 0; i < sizeof(DevStats) / 8; ++i) dst[i] = src[i];
-    }
+    small_leave(a);
 }
 
 int small_blocks_per_sm() {

@@ -253,6 +253,7 @@ struct crum_ctx {
         uint32_t flags = 0;
         uint64_t used = 0;                    // LRU stamp
         bool fused = false;                   // the captured sequence is the single-pass kernel
+        bool small = false;                   // ... the one-launch small-footprint kernel
     };
     static constexpr int kGraphs = 4;         // e.g. two alternating images x {device, host}
     GraphEntry graphs[kGraphs];
@@ -357,6 +358,7 @@ struct crum_ctx {
     // CRUM_CFG_TIMING and the most recent call (crum_last_report)
     bool timing_cfg = false;
     int last_kind = 0;      // 0 none, 1 sync, 2 device gather, 3 host gather, 4 restore
+    bool last_small = false;  // with kLastDevFused: the one-launch small kernel (two events)
     bool last_timed = false;
     cudaEvent_t ev_done = nullptr;
 };
@@ -911,7 +913,7 @@ enum { kLastNone = 0, kLastSync = 1, kLastDevGather = 2, kLastHostGather = 3, kL
 
 // Phase times of the most recent call from its events (see each call for
 // which events delimit which phase).
-void fill_times(crum_ctx *c, crum_report *rep) {
+void fill_times(crum_ctx *c, const DevStats &h, crum_report *rep) {
     cudaEvent_t *e = c->ev_t;
     switch (c->last_kind) {
         case kLastSync:
@@ -921,6 +923,11 @@ void fill_times(crum_ctx *c, crum_report *rep) {
             rep->t_total_ms = ev_ms(e[0], e[4]);
             break;
         case kLastDevFused:
+            if (c->last_small) {  // one kernel, timed by itself (first CTA in -> last CTA out)
+                rep->t_detect_ms = rep->t_total_ms = h.t_ns * 1e-6;
+                rep->path = CRUM_PATH_FUSED | CRUM_PATH_SMALL;
+                break;
+            }
             rep->t_detect_ms = ev_ms(e[0], e[1]);   // detect + compact + gather (one kernel)
             rep->t_compact_ms = ev_ms(e[1], e[4]);  // metadata CRC + header
             rep->t_total_ms = ev_ms(e[0], e[4]);
@@ -1766,8 +1773,8 @@ bool use_small(const crum_ctx *c, bool full, uint64_t capacity, uint64_t worst) 
 
 int enqueue_small(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, bool timing, bool capturing = false) {
     const unsigned evf = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
-    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[0], s, evf));
     SmallArgs sa{};
+    sa.timing = timing;  // the kernel times itself: no events around it
     sa.regs = c->d_regs;
     sa.R = (uint32_t)c->regs.size();
     sa.log2p = c->small_log2p;
@@ -1790,8 +1797,6 @@ int enqueue_small(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, 
     Launch L = launch_of(c, s);
     launch_small_ckpt(L, sa, (int)blocks);
     CK_LAUNCH();
-    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[1], s, evf));
-    if (timing) CK(cudaEventRecordWithFlags(c->ev_t[4], s, evf));
     CK(cudaEventRecordWithFlags(c->ev_done, s, evf));
     return CRUM_OK;
 }
@@ -1899,6 +1904,7 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
                        : fused ? enqueue_fused(c, c->gcap, img, capacity, timing, true)
                                : enqueue_gather_dev(c, c->gcap, img, capacity, (flags & CRUM_FULL) != 0, timing, true);
         e->fused = small || fused;
+        e->small = small;
         cudaGraph_t g = nullptr;
         const cudaError_t ce = cudaStreamEndCapture(c->gcap, &g);
         const uint64_t nk = c->launches - l0;
@@ -1925,6 +1931,7 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
     CK(cudaGraphLaunch(e->exec, s));
     c->launches += e->nk;
     c->last_kind = e->fused ? kLastDevFused : kLastDevGather;
+    c->last_small = e->small;
     return CRUM_OK;
 }
 
@@ -2053,7 +2060,7 @@ int gather_z(crum_ctx *c, cudaStream_t s, uint8_t *dev_img, crum_image *himg, ui
     if (rep) {
         memset(rep, 0, sizeof *rep);
         fill_report(c, h, rep);
-        fill_times(c, rep);
+        fill_times(c, h, rep);
         rep->path |= CRUM_PATH_COMPRESSED;
     }
     if (h.status == kStCapacity) {
@@ -2146,6 +2153,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
         st = small ? enqueue_small(c, s, img, capacity, timing) : enqueue_fused(c, s, img, capacity, timing);
         if (st) return st;
         c->last_kind = kLastDevFused;
+        c->last_small = small;
         c->last_path = 0;
         c->last_timed = timing;
         if (rep) {
@@ -2153,7 +2161,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
             CK(cudaStreamSynchronize(s));
             memset(rep, 0, sizeof *rep);
             fill_report(c, *c->h_st, rep);
-            fill_times(c, rep);
+            fill_times(c, *c->h_st, rep);
         }
         return CRUM_OK;
     }
@@ -2167,7 +2175,7 @@ int crum_checkpoint_gather_device(crum_ctx *ctx, void *dev_image, uint64_t capac
         const DevStats h = *c->h_st;
         memset(rep, 0, sizeof *rep);
         fill_report(c, h, rep);
-        fill_times(c, rep);
+        fill_times(c, h, rep);
         if (h.status == kStCapacity) {
             set_detail("image needs %llu bytes, capacity %llu", (unsigned long long)h.image_bytes,
                        (unsigned long long)capacity);
@@ -2221,6 +2229,7 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
                  : fused ? enqueue_fused(c, s, d, img->cap, true)
                          : enqueue_gather_dev(c, s, d, img->cap, full, true);
             c->last_kind = (small || fused) ? kLastDevFused : kLastDevGather;
+            c->last_small = small;
         }
         if (st) return st;  // (gather_dev_graph set last_kind)
         c->last_path = 0;
@@ -2233,7 +2242,7 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
         if (rep) {
             memset(rep, 0, sizeof *rep);
             fill_report(c, h, rep);
-            fill_times(c, rep);
+            fill_times(c, h, rep);
         }
         return CRUM_OK;
     }
@@ -2381,7 +2390,7 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     if (rep) {
         memset(rep, 0, sizeof *rep);
         fill_report(c, h, rep);
-        fill_times(c, rep);
+        fill_times(c, h, rep);
     }
     return CRUM_OK;
 }
@@ -2752,7 +2761,7 @@ int restore_common(crum_ctx *c, const uint8_t *host_img, const uint8_t *dev_img,
         memset(rep, 0, sizeof *rep);
         fill_report(c, *c->h_st, rep);
         rep->image_bytes = p.image;
-        fill_times(c, rep);
+        fill_times(c, *c->h_st, rep);
     }
     return CRUM_OK;
 }
@@ -3078,8 +3087,9 @@ int crum_last_report(crum_ctx *ctx, crum_report *rep) {
     CK(cudaMemcpy(c->h_st, c->d_st, sizeof(DevStats), cudaMemcpyDeviceToHost));
     memset(rep, 0, sizeof *rep);
     fill_report(c, *c->h_st, rep);
-    if (c->last_timed) fill_times(c, rep);
-    else rep->path = (c->last_kind == kLastDevFused ? CRUM_PATH_FUSED : 0u) | c->last_path;  // no times
+    if (c->last_timed) fill_times(c, *c->h_st, rep);
+    else rep->path = (c->last_kind == kLastDevFused ? CRUM_PATH_FUSED : 0u) |
+                     (c->last_kind == kLastDevFused && c->last_small ? CRUM_PATH_SMALL : 0u) | c->last_path;  // no times
     return CRUM_OK;
 }
 

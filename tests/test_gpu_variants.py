@@ -110,6 +110,9 @@ def test_every_path_bit_exact(crum, variant, specs_name):
                           (variant.startswith("fused") or small or prev_frac >= 0.25))
         prev_frac = rep_o["dirty_pages"] / p.N
         assert bool(rep["path"] & crum.PATH_FUSED) == fused_eligible, (variant, epoch, how, rep["path"])
+        # the one-launch kernel: one page size, compare-only, <= 16384 pages
+        assert bool(rep["path"] & crum.PATH_SMALL) == (fused_eligible and specs_name == "small"), \
+            (variant, epoch, how, rep["path"])
         assert p.shadows_equal(), (variant, epoch)
 
 
@@ -206,3 +209,41 @@ def test_register_rollback_on_nomem(crum):
     rid = p.g.register_region(region, nb, 4096, H)
     assert rid == 3
     p.g.unregister_region(rid)
+
+
+@pytest.mark.parametrize("specs_name", ["small", "fusable_big"])
+def test_phase_times_reported(crum, specs_name):
+    """CRUM_CFG_TIMING: the small kernel times itself (t_detect = t_total =
+    its own duration, no events around it); the multi-kernel path reports its
+    phases from events.  Without the flag an asynchronous device-image call
+    reports no times (a pinned-image gather and a synchronous report always
+    time their call).  Images stay bit-exact
+    either way."""
+    specs = {"small": SMALL, "fusable_big": FUSABLE_BIG}[specs_name]
+    for timing in (True, False):
+        p = mkpair(specs, 41, timing=timing)
+        img = p.g.new_image()
+        for epoch, d in ((0, 0.0), (1, 0.1), (2, 0.02)):
+            if epoch:
+                p.write(epoch, d)
+            st, want, _ = p.o.checkpoint_gather()
+            rep = p.g.checkpoint_gather(img)
+            assert img.tobytes() == want.tobytes()
+            if not timing:  # (a pinned-image gather times itself regardless)
+                continue
+            assert 0 < rep["t_detect_ms"] <= rep["t_total_ms"] < 1e3, rep
+            if specs_name == "small":
+                assert rep["path"] & crum.PATH_SMALL
+                assert rep["t_detect_ms"] == rep["t_total_ms"] and rep["t_compact_ms"] == 0
+            else:
+                assert not rep["path"] & crum.PATH_SMALL
+        # the device image path: asynchronous (timed only under the flag; a
+        # synchronous report always times its call)
+        dbuf = torch.empty(p.g.image_required_bytes() + 256, dtype=torch.uint8, device="cuda")
+        p.write(3, 0.05)
+        st, want, _ = p.o.checkpoint_gather()
+        assert p.g.checkpoint_gather_device(dbuf, p.g.image_required_bytes(), report=False) is None
+        rep = p.g.last_report()
+        assert dbuf[:len(want)].cpu().numpy().tobytes() == want.tobytes()
+        assert (rep["t_total_ms"] > 0) == timing, rep
+        assert bool(rep["path"] & crum.PATH_SMALL) == (specs_name == "small")

@@ -20,11 +20,7 @@ ins('    if (threadIdx.x != 0) return;\n    uint32_t acc = 0;', '    const uint6
 ins('    x = gf2_mulmod_bf(s_lpw[lane], x);\n', '    asm volatile("" :: "r"(x));\n    const uint64_t T6a = gtimer();\n')
 ins('    // the header\'s first 56 bytes are known already', '    asm volatile("" :: "r"(x));\n    const uint64_t T6b = gtimer();\n')
 ins('    __syncthreads();\n    const uint64_t T7', '    const uint64_t T6c = gtimer();\n')
-ins('''    if (a.st_host) {  // the host reads the report without a copy
-        const uint64_t *src = reinterpret_cast<const uint64_t *>(st);
-        volatile uint64_t *dst = reinterpret_cast<volatile uint64_t *>(a.st_host);
-        for (uint32_t i = 0; i < sizeof(DevStats) / 8; ++i) dst[i] = src[i];
-    }
+ins('''    small_leave(a);
 }
 
 int small_blocks_per_sm''', '''    printf("small: chunks %llu place %llu hdr56 %llu sync %llu | detect %llu barrier %llu prefix %llu table+pad %llu ids %llu scans %llu crc %llu hdr %llu ns K=%llu\\n", (unsigned long long)(T6a - T6), (unsigned long long)(T6b - T6a), (unsigned long long)(T6c - T6b), (unsigned long long)(T7 - T6c),
