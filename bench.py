@@ -707,6 +707,9 @@ def main():
     for i in range(args.steps):
         epoch += 1
         app_epoch(epoch)
+        # the application's writes + L2 scrub finish before the call: the host
+        # clock (e2e) then times the call alone, as the events do
+        stream.synchronize()
         ev0[i].record(stream)
         t0 = time.perf_counter()
         greps.append(pinned_step())

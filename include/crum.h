@@ -140,12 +140,16 @@ CRUM_API int crum_config_init(crum_config *cfg);
  *   CRUM_CFG_FUSED    device-image gathers of a context whose regions are all
  *                     COMPARE with pages <= 64 KiB run the single-pass kernel
  *                     (detect + compaction + gather + commit in one launch).
- *   CRUM_CFG_TRACE    print the host pipeline's per-range times to stderr. */
+ *   CRUM_CFG_TRACE    print the host pipeline's per-range times to stderr.
+ *   CRUM_CFG_NO_MAPPED pinned-image gathers never take the mapped-store range
+ *                     pipeline (CRUM_PATH_MAPPED); every payload goes through the
+ *                     device ring and D2H copies. */
 enum {
     CRUM_CFG_TIMING = 1u << 0,
     CRUM_CFG_NO_GRAPH = 1u << 1,
     CRUM_CFG_FUSED = 1u << 2,
-    CRUM_CFG_TRACE = 1u << 3
+    CRUM_CFG_TRACE = 1u << 3,
+    CRUM_CFG_NO_MAPPED = 1u << 4
 };
 
 /* Outcome of a sync / gather / restore.  Times are CUDA-event milliseconds
@@ -171,11 +175,15 @@ typedef struct {
                                 kernel, which also writes the metadata; with CRUM_CFG_TIMING it
                                 times itself (globaltimer, first CTA in -> last CTA out), so
                                 t_detect_ms = t_total_ms = the kernel, and no events are recorded
-                                around it */
+                                around it;
+                                bit3 CRUM_PATH_MAPPED: pinned gather whose kernels stored the
+                                payload and metadata straight into the image through its mapped
+                                address, range by range with no host wait between ranges (small
+                                payloads); t_copy_ms is then the span of those stores */
     uint32_t reserved;
 } crum_report;
 
-enum { CRUM_PATH_FUSED = 1u << 0, CRUM_PATH_COMPRESSED = 1u << 1, CRUM_PATH_SMALL = 1u << 2 };
+enum { CRUM_PATH_FUSED = 1u << 0, CRUM_PATH_COMPRESSED = 1u << 1, CRUM_PATH_SMALL = 1u << 2, CRUM_PATH_MAPPED = 1u << 3 };
 
 /* ---------------------------------------------------------------------------
  * Context.  crum_create binds to CUDA device `device` (cudaSetDevice is

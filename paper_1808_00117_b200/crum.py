@@ -30,9 +30,9 @@ E_CAPACITY, E_CORRUPT, E_MISMATCH, E_BUSY, E_DEVICE, E_CUDA, E_IO = -6, -7, -8, 
 MODE_COMPARE, MODE_HASH = 0, 1
 FULL, VERIFY, COMPRESS = 1, 2, 4
 MODE_TRACKED = 2
-CFG_TIMING, CFG_NO_GRAPH, CFG_FUSED, CFG_TRACE = 1, 2, 4, 8
+CFG_TIMING, CFG_NO_GRAPH, CFG_FUSED, CFG_TRACE, CFG_NO_MAPPED = 1, 2, 4, 8, 16
 NUMA_AUTO, NUMA_DEFAULT = -1, -2
-PATH_FUSED, PATH_COMPRESSED, PATH_SMALL = 1, 2, 4
+PATH_FUSED, PATH_COMPRESSED, PATH_SMALL, PATH_MAPPED = 1, 2, 4, 8
 PERSIST_FSYNC, PERSIST_DIRECT = 1, 2
 EXPORT_FORCE, EXPORT_HASHES, EXPORT_MIRROR = 0, 1, 2
 ALL_PAGES = (1 << 64) - 1

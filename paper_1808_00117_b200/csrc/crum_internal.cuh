@@ -156,6 +156,8 @@ struct CrcArgs {
     uint32_t *done;
     X2N x2n;
     const uint16_t *zsz;    // compressed image: per-unit encoded sizes (tail after the hashes)
+    uint8_t *out;           // nullptr, or the image's mapped address: the table + padding
+                            // [64, poff) are copied there from head, the tail and header go there
 };
 
 // A6: scatter units [u_lo, u_hi); unit u read from src + (u - src_unit0)*4096.
@@ -201,6 +203,8 @@ struct FusedArgs {
     FusedScratch *fs;
     uint8_t *force;
     uint8_t *img;             // device image (payload at poff)
+    uint8_t *meta;            // nullptr, or where the region table + padding go instead of img
+                              // (img is a pinned image's mapped address; k_crc_meta copies them)
     uint64_t poff;
     uint32_t *gids;
     uint64_t *sunit;
@@ -282,7 +286,7 @@ void launch_zenc(const Launch &L, const uint8_t *raw, uint64_t n, uint8_t *enc, 
 void launch_zscan_chunk(const Launch &L, const uint16_t *zsz, uint64_t n, uint32_t *zloc, uint64_t *zrun,
                         uint64_t *zbase, uint64_t *zrun_host);
 // Move the n encodings from stage to dst + (base ? *base : 0) + zloc[i];
-// limit != 0: a unit is written only if poff + offset + size <= limit.
+// limit != 0: a unit is written only if offset + size <= limit (payload bytes that fit).
 void launch_zpack(const Launch &L, const uint8_t *stage, const uint16_t *zsz, const uint32_t *zloc, uint64_t n,
                   const uint64_t *base, uint8_t *dst, uint64_t limit, const DevStats *st);
 // After the last chunk: the compressed image's sizes and capacity status

@@ -669,9 +669,14 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
     const uint64_t zw = zz ? round_up(2 * U, 8) / 4 : 0;
     const uint64_t tabw = 12 * R, idsw = round_up(4 * K, 8) / 4, hw = hh ? 2 * K : 0;
     const uint64_t nwords = tabw + idsw + hw + zw;
-    uint8_t *tail = a.tail ? a.tail : a.head + st->ids_off;
+    uint8_t *tail = a.tail ? a.tail : (a.out ? a.out : a.head) + st->ids_off;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    if (a.out) {  // table + padding into the mapped image (64 + 48 R and poff are multiples of 16)
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.head + 64);
+        uint4 *dst = reinterpret_cast<uint4 *>(a.out + 64);
+        for (uint64_t q = tid; q < (st->poff - 64) / 16; q += nth) dst[q] = src[q];
+    }
     // copy ids (+pad) and hashes into the image tail
     uint32_t *tids = reinterpret_cast<uint32_t *>(tail);
     for (uint64_t k = tid; k < idsw; k += nth) tids[k] = k < K ? a.lids[k] : 0u;
@@ -731,7 +736,7 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
     // empty stream: zlib crc32("") == 0
     const uint32_t meta_crc = (nwords == 0) ? 0u : (total ^ 0xffffffffu);
     st->meta_crc = meta_crc;
-    uint8_t h[64];
+    alignas(16) uint8_t h[64];
     h[0] = 'C'; h[1] = 'R'; h[2] = 'U'; h[3] = 'M';
     put32(h + 4, 1);
     put32(h + 8, st->img_flags);
@@ -748,6 +753,8 @@ __global__ void __launch_bounds__(256) k_crc_meta(CrcArgs a) {
                                (uint32_t)h[i + 3] << 24));
     put32(h + 60, c ^ 0xffffffffu);
     for (int i = 0; i < 64; ++i) a.head[i] = h[i];
+    if (a.out)
+        for (int i = 0; i < 64; i += 16) *reinterpret_cast<uint4 *>(a.out + i) = *reinterpret_cast<const uint4 *>(h + i);
     if (a.st_host) {
         const uint64_t *src = reinterpret_cast<const uint64_t *>(st);
         volatile uint64_t *dst = reinterpret_cast<volatile uint64_t *>(a.st_host);
@@ -1233,7 +1240,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
             s.payload_base = s.unit_base << kSegLog2;
             a.rs[r] = s;
             a.reg_nd[r] = 0;  // ready for the next checkpoint
-            uint8_t *e = a.img + 64 + 48ull * r;
+            uint8_t *e = (a.meta ? a.meta : a.img) + 64 + 48ull * r;
             reinterpret_cast<uint32_t *>(e)[0] = g.id;
             reinterpret_cast<uint32_t *>(e)[1] = g.mode;
             reinterpret_cast<uint64_t *>(e)[1] = g.bytes;
@@ -1246,7 +1253,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
         carry_units += tun;
     }
     const uint64_t poff = a.poff;
-    for (uint64_t b = 64 + 48ull * a.R + lane; b < poff; b += 32) a.img[b] = 0;
+    for (uint64_t b = 64 + 48ull * a.R + lane; b < poff; b += 32) (a.meta ? a.meta : a.img)[b] = 0;
     if (lane == 0) {
         DevStats *st = a.st;
         const uint64_t payload = U << kSegLog2;

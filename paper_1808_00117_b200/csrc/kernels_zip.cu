@@ -200,29 +200,42 @@ __global__ void __launch_bounds__(32 * kZEncWarps, kZEncCtasPerSm) k_zenc(const 
             for (uint32_t i = lane; i < kSegBytes / 2; i += 32) reinterpret_cast<uint32_t *>(sm.head)[i] = 0xFFFFFFFFu;
             __syncwarp();
             uint32_t found = 0;
-            // rounds of 32 positions, four at a time: the match_any and hash work of
-            // the four rounds is independent (its latency overlaps); only the
-            // table reads / writes run round by round
+            // rounds of 32 positions, four at a time: the hash work of the four
+            // rounds is independent (its latency overlaps); only the table
+            // reads / writes run round by round.  A round first assumes its 32
+            // hashes are distinct: every lane takes the head entry as its
+            // candidate and stores its position there, then reads the entry
+            // back -- a lane that finds another lane's position shares its hash
+            // with a lane of this round, and only then does the round resolve
+            // its groups with __match_any_sync (the nearest lower lane of the
+            // group is the candidate, the group's highest lane the new head).
+            // MATCH.ANY costs hundreds of cycles; random data has a shared hash
+            // in ~11 % of rounds (32 lanes, 4096 buckets).
             constexpr uint32_t kUnroll = 4;
             for (uint32_t c0 = 0; c0 < kZWords; c0 += kUnroll) {
-                uint32_t v[kUnroll], h[kUnroll], peers[kUnroll], q[kUnroll];
+                uint32_t v[kUnroll], h[kUnroll], q[kUnroll];
 #pragma unroll
                 for (uint32_t j = 0; j < kUnroll; ++j) {
                     const uint32_t p = 32 * (c0 + j) + lane;
-                    const bool valid = p + 4 <= kSegBytes;
                     v[j] = ld32u(sm.data, p);
                     h[j] = (v[j] * 2654435761u) >> kZHashShift;
-                    peers[j] = __match_any_sync(0xffffffffu, valid ? h[j] : 0x10000u + lane);
                 }
 #pragma unroll
                 for (uint32_t j = 0; j < kUnroll; ++j) {
                     const uint32_t p = 32 * (c0 + j) + lane;
                     const bool valid = p + 4 <= kSegBytes;
-                    const uint32_t lower = peers[j] & lanemask_lt();
-                    q[j] = kNone;
-                    if (valid) q[j] = lower ? 32 * (c0 + j) + (31 - __clz(lower)) : sm.head[h[j]];
+                    q[j] = valid ? sm.head[h[j]] : kNone;
                     __syncwarp();
-                    if (valid && (peers[j] >> lane) == 1u) sm.head[h[j]] = (uint16_t)p;  // highest lane of its group
+                    if (valid) sm.head[h[j]] = (uint16_t)p;
+                    __syncwarp();
+                    const bool shared = valid && sm.head[h[j]] != (uint16_t)p;
+                    if (__any_sync(0xffffffffu, shared)) {
+                        const uint32_t peers = __match_any_sync(0xffffffffu, valid ? h[j] : 0x10000u + lane);
+                        const uint32_t lower = peers & lanemask_lt();
+                        if (valid && lower) q[j] = 32 * (c0 + j) + (31 - __clz(lower));
+                        __syncwarp();
+                        if (valid && (peers >> lane) == 1u) sm.head[h[j]] = (uint16_t)p;  // highest lane of its group
+                    }
                     __syncwarp();
                 }
 #pragma unroll
@@ -406,7 +419,7 @@ __global__ void __launch_bounds__(1024) k_zscan_chunk(const uint16_t *zsz, uint6
 // ---------------------------------------------------------------------------
 // Pack: one warp per unit, byte-exact destination:
 // dst + (base ? *base : 0) + zloc[i]; limit != 0: a unit is written only if
-// poff + that offset + its size <= limit (device image capacity).
+// that payload offset + its size <= limit (the payload bytes that fit).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_zpack(const uint8_t *stage, const uint16_t *zsz, const uint32_t *zloc,
                                                uint64_t n, const uint64_t *base, uint8_t *dst, uint64_t limit,
@@ -419,7 +432,7 @@ __global__ void __launch_bounds__(256) k_zpack(const uint8_t *stage, const uint1
         const uint32_t sz = zsz[u];
         if (!sz) continue;
         const uint64_t off = b + zloc[u];
-        if (limit && st->poff + off + sz > limit) continue;  // does not fit: CAPACITY at the end
+        if (limit && off + sz > limit) continue;  // does not fit: CAPACITY at the end
         const uint32_t *s = reinterpret_cast<const uint32_t *>(stage + (u << kSegLog2));
         uint8_t *d = dst + off;
         // head bytes up to a 4-byte boundary of the destination, whole words, tail bytes
@@ -428,11 +441,25 @@ __global__ void __launch_bounds__(256) k_zpack(const uint8_t *stage, const uint1
         if (lane < h) d[lane] = (uint8_t)(s[lane >> 2] >> (8 * (lane & 3)));
         const uint32_t nw = (sz - h) / 4;
         uint32_t *dw = reinterpret_cast<uint32_t *>(d + h);
-        for (uint32_t i = lane; i < nw; i += 32) {
-            const uint32_t p = h + 4 * i;  // source byte offset
-            // the next word only when the source is misaligned (then it holds
-            // bytes of this encoding; otherwise it may lie past what was written)
-            dw[i] = __funnelshift_r(s[p >> 2], (p & 3) ? s[(p >> 2) + 1] : 0u, 8 * (p & 3));
+        // destination word i holds source bytes h + 4 i ..: words h / 4 + i
+        // (h <= 3, so word i) and i + 1 shifted by 8 h; the next word only when
+        // h != 0 (then it holds bytes of this encoding; otherwise it may lie
+        // past what was written).  Eight loads in flight per lane before the
+        // stores: a 4 KiB unit is 4 round trips to L2, not 32.
+        const uint32_t sh = 8 * (h & 3);
+        for (uint32_t i0 = 0; i0 < nw; i0 += 32 * 8) {
+            uint32_t lo[8], hi[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t i = i0 + 32 * k + lane;
+                lo[k] = i < nw ? s[i] : 0u;
+                hi[k] = (i < nw && sh) ? s[i + 1] : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t i = i0 + 32 * k + lane;
+                if (i < nw) dw[i] = __funnelshift_r(lo[k], hi[k], sh);
+            }
         }
         const uint32_t t0 = h + 4 * nw;
         if (t0 + lane < sz) {

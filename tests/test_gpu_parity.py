@@ -551,3 +551,47 @@ def test_small_path_tracked_and_compare(crum):
         if mode == C:
             assert np.array_equal(ctx.debug_export(r + 1, crum.EXPORT_MIRROR, nb), o.mirror(r + 1))
         assert np.array_equal(ctx.debug_export(r + 1, crum.EXPORT_FORCE, synth.n_pages(nb, P)), o.force_bits(r + 1))
+
+
+@pytest.mark.parametrize("kind", ["mixed", "compare"])
+@pytest.mark.parametrize("no_mapped", [False, True])
+def test_mapped_store_gather(crum, kind, no_mapped):
+    """Pinned gathers above the small-footprint size whose previous payload
+    was small store straight into the pinned image through its mapped address
+    (CRUM_PATH_MAPPED, previous payload <= 16 MiB: the single-pass kernel
+    above 2 MiB when every region is COMPARE with pages <= 64 KiB, else the
+    detect -> compact -> gather sequence in halving ranges above 1 MiB, in
+    one range below); a larger
+    previous payload, the first gather after registration, or
+    CRUM_CFG_NO_MAPPED take the ring + D2H pipeline.  Image bytes, reports
+    and shadows equal the oracle's every epoch, on every path, with ragged
+    tails (and hash regions in the mixed set)."""
+    if kind == "mixed":
+        specs = [(40 * MiB + 4096 * 3 + 5, 4 * KiB, C), (72 * MiB, 64 * KiB, H), (24 * MiB, 64 * KiB, C),
+                 (8 * MiB + 300, 2 * MiB, H)]
+        limit = 16 * MiB
+    else:
+        specs = [(40 * MiB + 4096 * 3 + 5, 4 * KiB, C), (72 * MiB, 64 * KiB, C), (8 * MiB + 300, 64 * KiB, C)]
+        limit = 16 * MiB
+    p = mkpair(specs, 23, flags=crum.CFG_NO_MAPPED if no_mapped else 0)
+    img = p.g.new_image()
+    assert img.capacity == p.g.image_required_bytes()
+    prev_payload = None
+    for epoch, d in [(0, 0.0), (1, 0.01), (2, 0.0), (3, 0.3), (4, 0.02), (5, 0.005), (6, 0.1), (7, 0.0)]:
+        if epoch:
+            p.write(epoch, d)
+        st, want, rep_o = p.o.checkpoint_gather()
+        assert st == 0
+        rep = p.g.checkpoint_gather(img)
+        assert img.length == len(want)
+        assert img.tobytes() == want.tobytes(), epoch
+        for k in ("dirty_pages", "dirty_bytes", "dirty_runs", "image_bytes"):
+            assert rep[k] == rep_o[k], (epoch, k)
+        assert p.shadows_equal(), epoch
+        mapped = bool(rep["path"] & crum.PATH_MAPPED)
+        # epoch 0: the first gather after registration (every page force-dirty)
+        expect = not no_mapped and prev_payload is not None and prev_payload <= limit
+        assert mapped == expect, (epoch, prev_payload)
+        if mapped:  # the single pass above 2 MiB; below it, halving ranges above 1 MiB, else one range
+            assert bool(rep["path"] & crum.PATH_FUSED) == (kind == "compare" and prev_payload > 2 * MiB)
+        prev_payload = int.from_bytes(want.tobytes()[32:40], "little")

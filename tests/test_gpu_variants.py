@@ -1,7 +1,8 @@
 """GPU parity of every kernel path the library ships, selected per context by
 crum_config (include/crum.h): the captured-graph replay vs direct launches
 (CRUM_CFG_NO_GRAPH) and the single-pass detect+compact+gather kernel
-(CRUM_CFG_FUSED) vs the multi-kernel path, each bit-exact with the oracle on
+(CRUM_CFG_FUSED) vs the multi-kernel path, the mapped-store pinned gathers vs
+the ring + D2H pipeline (CRUM_CFG_NO_MAPPED), each bit-exact with the oracle on
 the same seeded inputs; the pinned pool (crum_config.pinned_pool_bytes) and
 the transactional register / unregister (a failed rebuild changes nothing)."""
 import numpy as np
@@ -55,7 +56,7 @@ def mkpair(specs, seed_idx, **kw):
 def variants():
     from paper_1808_00117_b200 import crum as m
     return [("default", 0), ("no_graph", m.CFG_NO_GRAPH), ("fused", m.CFG_FUSED),
-            ("fused_no_graph", m.CFG_FUSED | m.CFG_NO_GRAPH)]
+            ("fused_no_graph", m.CFG_FUSED | m.CFG_NO_GRAPH), ("no_mapped", m.CFG_NO_MAPPED)]
 
 
 @pytest.mark.parametrize("specs_name", ["small", "fusable", "fusable_big", "mixed"])
@@ -75,6 +76,8 @@ def test_every_path_bit_exact(crum, variant, specs_name):
            (4, 1.0, 0, "host"), (5, 0.2, crum.FULL, "dev_async"), (6, 0.3, 0, "sync"), (7, 0.05, 0, "dev_async"),
            (8, 0.7, 0, "host"), (9, 0.0, 0, "dev_sync")]
     prev_frac = 0.0  # dirty fraction of the previous call (the adaptive single-pass rule)
+    prev_payload = None  # payload of the previous gather (the mapped-store rule)
+    host_gathers = 0
     for epoch, d, gflags, how in seq:
         if epoch:
             p.write(epoch, d)
@@ -108,7 +111,18 @@ def test_every_path_bit_exact(crum, variant, specs_name):
         fused_eligible = (specs_name != "mixed" and not gflags and
                           (how != "host" or specs_name == "small") and
                           (variant.startswith("fused") or small or prev_frac >= 0.25))
+        # a pinned gather above the small-footprint size (worst case > 16 MiB:
+        # FUSABLE, FUSABLE_BIG) whose previous payload was <= 16 MiB (not the
+        # first since registration) stores through the image's mapped address;
+        # the single pass there above 2 MiB (these sets are compare-only)
+        mapped = (how == "host" and specs_name in ("fusable", "fusable_big") and not gflags and host_gathers > 0 and
+                  variant != "no_mapped" and prev_payload is not None and prev_payload <= 16 * MiB)
+        assert bool(rep["path"] & crum.PATH_MAPPED) == mapped, (variant, epoch, how, rep["path"])
+        if mapped:
+            fused_eligible = prev_payload > 2 * MiB
         prev_frac = rep_o["dirty_pages"] / p.N
+        prev_payload = int.from_bytes(want.tobytes()[32:40], "little")
+        host_gathers += how == "host"
         assert bool(rep["path"] & crum.PATH_FUSED) == fused_eligible, (variant, epoch, how, rep["path"])
         # the one-launch kernel: one page size, compare-only, <= 16384 pages
         assert bool(rep["path"] & crum.PATH_SMALL) == (fused_eligible and specs_name == "small"), \
