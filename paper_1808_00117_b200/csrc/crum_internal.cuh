@@ -230,7 +230,7 @@ struct SmallArgs {
     uint32_t R;
     uint32_t log2p;           // the context's one page size
     uint64_t N;               // pages
-    uint32_t *bitmap;         // 2 x kSmallPages bits: dirty pages (alternating, zero when a launch begins)
+    uint32_t *bitmap;         // kSmallPages bits: dirty pages (zero when a launch begins; the last CTA out clears it)
     uint32_t *bar;            // [0] arrivals, [1] generation (grid barrier; persists across launches),
                               // [2] CTAs out, [4..5] ~(earliest CTA entry, ns) when timed; [0], [2], [4..5] end at 0
     uint8_t *force;

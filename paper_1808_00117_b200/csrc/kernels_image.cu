@@ -1286,6 +1286,11 @@ constexpr uint32_t kSmallThreads = 256;
 constexpr uint32_t kSmallWords = kSmallPages / 32;
 constexpr uint32_t kSmallStageWords = 2048;  // metadata words CTA 0 keeps in shared memory
 
+// A GPU-scope acquire-release fence: with the relaxed atomics around it, the
+// release / acquire pattern a barrier or a "last one out" election needs --
+// lighter than __threadfence() (fence.sc).
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // Grid barrier of a cooperative launch (all CTAs co-resident): arrivals
 // counter + generation, sense by generation, state returns to 0 arrivals.
 __device__ __forceinline__ void grid_barrier(uint32_t *bar) {
@@ -1293,15 +1298,15 @@ __device__ __forceinline__ void grid_barrier(uint32_t *bar) {
     if (threadIdx.x == 0) {
         volatile uint32_t *gen = bar + 1;
         const uint32_t g = *gen;
-        __threadfence();
+        fence_acq_rel_gpu();  // release this CTA's writes (bitmap atomics) before its arrival
         if (atomicAdd(bar, 1u) == gridDim.x - 1) {
             bar[0] = 0;
-            __threadfence();
+            fence_acq_rel_gpu();
             atomicAdd(bar + 1, 1u);
         } else {
             while (*gen == g) __nanosleep(32);
         }
-        __threadfence();
+        fence_acq_rel_gpu();  // acquire every CTA's writes
     }
     __syncthreads();
 }
@@ -1312,13 +1317,25 @@ __device__ __forceinline__ uint64_t gtime_ns() {
     return t;
 }
 
-// Every CTA leaves through here (thread 0, after its CTA's work): the last one
-// out publishes the stats to the host -- with the kernel's own duration when
-// timed -- and returns the scratch words to 0 for the next launch.
-__device__ __forceinline__ void small_leave(const SmallArgs &a) {
-    __threadfence();
-    if (atomicAdd(a.bar + 2, 1u) != gridDim.x - 1) return;
-    __threadfence();
+// Every CTA leaves through here (all threads, after the CTA's work -- which
+// includes its last read of the global bitmap): the last one out clears the
+// bitmap's nw words for the next launch, publishes the stats to the host --
+// with the kernel's own duration when timed -- and returns the scratch words
+// to 0.  (One bitmap, cleared on the way out: a launch needs no generation
+// read before its first load, which stalled every warp's first instructions
+// ~1 us when two bitmaps alternated by the barrier generation.)
+__device__ __forceinline__ void small_leave(const SmallArgs &a, uint32_t nw) {
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fence_acq_rel_gpu();  // release (CTA 0: the stats) before counting out
+        s_last = atomicAdd(a.bar + 2, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) a.bitmap[w] = 0;
+    if (threadIdx.x != 0) return;
+    fence_acq_rel_gpu();  // acquire CTA 0's stats
     volatile unsigned long long *t0 = reinterpret_cast<volatile unsigned long long *>(a.bar + 4);
     DevStats *st = a.st;
     st->t_ns = a.timing ? gtime_ns() - ~*t0 : 0;
@@ -1342,22 +1359,22 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     const uint64_t nwarps = ((uint64_t)gridDim.x * kSmallThreads) >> 5;
     const uint32_t spl = a.log2p - kSegLog2;   // log2 segments per page
     const uint64_t P = 1ull << a.log2p;
-    // two bitmaps: this launch uses bitmap[gen & 1] (the barrier generation,
-    // the same for every CTA until the barrier), CTA 0 clears the other one
-    // for the next launch (a CTA may still read this launch's after CTA 0 is done)
     if (a.timing && threadIdx.x == 0)  // the max of ~t is the earliest entry
         atomicMax(reinterpret_cast<unsigned long long *>(a.bar + 4), ~(unsigned long long)gtime_ns());
-    const uint32_t par = *reinterpret_cast<volatile uint32_t *>(a.bar + 1) & 1u;
-    uint32_t *bitmap = a.bitmap + par * kSmallWords;
-    // ---- A1 detect: warp per 4 KiB segment; forced pages are dirty unread ----
+    uint32_t *bitmap = a.bitmap;  // zero when the launch begins (small_leave)
+    // ---- A1 detect: warp per 4 KiB segment; a forced page is dirty ----
     uint32_t r = 0;
     for (uint64_t g = wid; g < (a.N << spl); g += nwarps) {
         const uint64_t pg = g >> spl;
         while (r + 1 < a.R && a.regs[r + 1].page_base <= pg) ++r;
         while (a.regs[r].page_base > pg) --r;
         const DevRegion &R = a.regs[r];
-        bool dirty = a.force[pg] != 0;
-        if (!dirty && R.mode == kModeCompare) {
+        // the force byte is loaded before, and consumed after, the segment's
+        // loads (a forced page's compare is wasted, but the loads overlap
+        // instead of chaining two cold HBM round trips)
+        const uint8_t forced = a.force[pg];
+        bool dirty = false;
+        if (R.mode == kModeCompare) {
             const uint64_t off = ((pg - R.page_base) << a.log2p) + ((g & ((1u << spl) - 1)) << kSegLog2);
             uint32_t x = 0;
             if (off < R.bytes) {
@@ -1376,6 +1393,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
             }
             dirty = __any_sync(0xffffffffu, x != 0);
         }
+        dirty = dirty || forced != 0;
         if (dirty && lane == 0) atomicOr(bitmap + (pg >> 5), 1u << (pg & 31));
     }
     grid_barrier(a.bar);
@@ -1444,15 +1462,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
             if (lane == 0) a.force[pg] = 0;
         }
         if (blockIdx.x != 0) {
-            __syncthreads();
-            if (threadIdx.x == 0) small_leave(a);
+            small_leave(a, nw);
             return;
         }
     }
-    // ---- CTA 0: bitmap cleared for the next launch, table, ids, CRC, header ----
+    // ---- CTA 0: table, ids, CRC, header ----
     __syncthreads();
-    uint32_t *other = a.bitmap + (par ^ 1u) * kSmallWords;
-    for (uint32_t w = threadIdx.x; w < nw; w += kSmallThreads) other[w] = 0;
     if (threadIdx.x < 32) s_lpw[threadIdx.x] = a.x2n.lpw[threadIdx.x];
     for (uint32_t i = threadIdx.x; i < 256; i += kSmallThreads) {
         uint32_t c = i;
@@ -1569,31 +1584,32 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         s_hc = hc;
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    uint32_t acc = 0;
-    for (uint32_t w = 0; w < kSmallThreads / 32; ++w) acc ^= s_x[w];
-    const uint32_t meta_crc = nwords == 0 ? 0u : (acc ^ 0xffffffffu);
-    DevStats *st = a.st;
-    st->K = K;
-    st->total_units = K << (a.log2p - kSegLog2);
-    st->poff = poff;
-    st->payload_bytes = payload;
-    st->ids_off = ids_off;
-    st->image_bytes = ids_off + 4 * idsw;
-    st->capacity = a.capacity;
-    st->status = st->image_bytes > a.capacity ? kStCapacity : kStOk;
-    st->img_flags = 0;
-    st->n_regions = a.R;
-    st->dirty_bytes = tot_bytes;
-    st->dirty_runs = tot_runs;
-    st->crc_acc = 0;
-    st->meta_crc = meta_crc;
-    put32(h + 56, meta_crc);
-    uint32_t hc = s_hc;
-    for (int i = 56; i < 60; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
-    put32(h + 60, hc ^ 0xffffffffu);
-    for (int i = 0; i < 64; i += 16) *reinterpret_cast<uint4 *>(img + i) = *reinterpret_cast<const uint4 *>(h + i);
-    small_leave(a);
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (uint32_t w = 0; w < kSmallThreads / 32; ++w) acc ^= s_x[w];
+        const uint32_t meta_crc = nwords == 0 ? 0u : (acc ^ 0xffffffffu);
+        DevStats *st = a.st;
+        st->K = K;
+        st->total_units = K << (a.log2p - kSegLog2);
+        st->poff = poff;
+        st->payload_bytes = payload;
+        st->ids_off = ids_off;
+        st->image_bytes = ids_off + 4 * idsw;
+        st->capacity = a.capacity;
+        st->status = st->image_bytes > a.capacity ? kStCapacity : kStOk;
+        st->img_flags = 0;
+        st->n_regions = a.R;
+        st->dirty_bytes = tot_bytes;
+        st->dirty_runs = tot_runs;
+        st->crc_acc = 0;
+        st->meta_crc = meta_crc;
+        put32(h + 56, meta_crc);
+        uint32_t hc = s_hc;
+        for (int i = 56; i < 60; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
+        put32(h + 60, hc ^ 0xffffffffu);
+        for (int i = 0; i < 64; i += 16) *reinterpret_cast<uint4 *>(img + i) = *reinterpret_cast<const uint4 *>(h + i);
+    }
+    small_leave(a, nw);
 }
 
 int small_blocks_per_sm() {

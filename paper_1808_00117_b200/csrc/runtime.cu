@@ -288,7 +288,7 @@ struct crum_ctx {
     bool fused_ok = false;
     uint64_t *d_tile_base = nullptr;
     uint64_t n_tiles = 0;
-    uint32_t *d_small = nullptr;   // one-launch small path: 2 dirty bitmaps | grid barrier words
+    uint32_t *d_small = nullptr;   // one-launch small path: dirty bitmap | grid barrier words
     bool small_ok = false;         // every region COMPARE/TRACKED, one page size, N <= kSmallPages, F small
     uint32_t small_log2p = 12;
     int small_bps = 1;
@@ -1197,8 +1197,8 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     if (cudaMalloc(&c->d_done, 16) != cudaSuccess) return fail(CRUM_E_NOMEM);
     c->fused_bps = fused_blocks_per_sm();
     c->small_bps = small_blocks_per_sm();
-    if (cudaMalloc(&c->d_small, 8 * kSmallPages / 32 + 64) != cudaSuccess) return fail(CRUM_E_NOMEM);
-    cudaMemset(c->d_small, 0, 8 * kSmallPages / 32 + 64);
+    if (cudaMalloc(&c->d_small, 4 * kSmallPages / 32 + 64) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    cudaMemset(c->d_small, 0, 4 * kSmallPages / 32 + 64);
     if (cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocMapped) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaHostAlloc(&c->h_rb, sizeof(RangeTotals) * (kMaxRanges + 1), cudaHostAllocMapped) != cudaSuccess)
         return fail(CRUM_E_NOMEM);
@@ -1808,7 +1808,7 @@ int enqueue_small(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, 
     sa.log2p = c->small_log2p;
     sa.N = c->N;
     sa.bitmap = c->d_small;
-    sa.bar = c->d_small + 2 * (kSmallPages / 32);
+    sa.bar = c->d_small + kSmallPages / 32;
     sa.force = c->d_force;
     sa.img = img;
     sa.poff = payload_offset_for(c->regs.size());
