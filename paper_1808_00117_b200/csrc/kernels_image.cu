@@ -1317,6 +1317,41 @@ __device__ __forceinline__ uint64_t gtime_ns() {
     return t;
 }
 
+// Profiling aid (off in every shipped build): -DCRUM_SMALL_STAMPS records
+// globaltimer stamps per CTA and phase (after the barrier words) and the last
+// CTA out prints, per phase, the earliest and latest CTA relative to the first
+// entry (tools/gpu_r02_c1_stamps.sh).
+#ifdef CRUM_SMALL_STAMPS
+}  // namespace crum
+#include <cstdio>
+namespace crum {
+constexpr int kStampN = 8;
+#define SMALL_STAMP(k)                                                                              \
+    do {                                                                                            \
+        if (threadIdx.x == 0)                                                                       \
+            reinterpret_cast<uint64_t *>(a.bar + 16)[blockIdx.x * kStampN + (k)] = gtime_ns();     \
+    } while (0)
+__device__ void small_stamps_print(const SmallArgs &a) {
+    const uint64_t *t = reinterpret_cast<const uint64_t *>(a.bar + 16);
+    uint64_t t0 = ~0ull;
+    for (uint32_t b = 0; b < gridDim.x; ++b) t0 = min(t0, t[b * kStampN]);
+    for (int k = 0; k < kStampN; ++k) {
+        uint64_t lo = ~0ull, hi = 0;
+        for (uint32_t b = 0; b < gridDim.x; ++b) {
+            const uint64_t v = t[b * kStampN + k];
+            if (!v) continue;
+            lo = min(lo, v - t0);
+            hi = max(hi, v - t0);
+        }
+        if (hi) printf("[small stamps] phase %d: first %llu ns, last %llu ns\n", k, (unsigned long long)lo,
+                       (unsigned long long)hi);
+    }
+    for (uint32_t i = 0; i < gridDim.x * kStampN; ++i) const_cast<uint64_t *>(t)[i] = 0;
+}
+#else
+#define SMALL_STAMP(k) do {} while (0)
+#endif
+
 // Every CTA leaves through here (all threads, after the CTA's work -- which
 // includes its last read of the global bitmap): the last one out clears the
 // bitmap's nw words for the next launch, publishes the stats to the host --
@@ -1327,6 +1362,7 @@ __device__ __forceinline__ uint64_t gtime_ns() {
 __device__ __forceinline__ void small_leave(const SmallArgs &a, uint32_t nw) {
     __shared__ bool s_last;
     __syncthreads();
+    SMALL_STAMP(7);
     if (threadIdx.x == 0) {
         fence_acq_rel_gpu();  // release (CTA 0: the stats) before counting out
         s_last = atomicAdd(a.bar + 2, 1u) == gridDim.x - 1;
@@ -1336,6 +1372,9 @@ __device__ __forceinline__ void small_leave(const SmallArgs &a, uint32_t nw) {
     for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) a.bitmap[w] = 0;
     if (threadIdx.x != 0) return;
     fence_acq_rel_gpu();  // acquire CTA 0's stats
+#ifdef CRUM_SMALL_STAMPS
+    small_stamps_print(a);
+#endif
     volatile unsigned long long *t0 = reinterpret_cast<volatile unsigned long long *>(a.bar + 4);
     DevStats *st = a.st;
     st->t_ns = a.timing ? gtime_ns() - ~*t0 : 0;
@@ -1362,6 +1401,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     if (a.timing && threadIdx.x == 0)  // the max of ~t is the earliest entry
         atomicMax(reinterpret_cast<unsigned long long *>(a.bar + 4), ~(unsigned long long)gtime_ns());
     uint32_t *bitmap = a.bitmap;  // zero when the launch begins (small_leave)
+    SMALL_STAMP(0);
     // ---- A1 detect: warp per 4 KiB segment; a forced page is dirty ----
     uint32_t r = 0;
     for (uint64_t g = wid; g < (a.N << spl); g += nwarps) {
@@ -1396,7 +1436,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         dirty = dirty || forced != 0;
         if (dirty && lane == 0) atomicOr(bitmap + (pg >> 5), 1u << (pg & 31));
     }
+#ifdef CRUM_SMALL_STAMPS
+    __syncthreads();
+#endif
+    SMALL_STAMP(1);
     grid_barrier(a.bar);
+    SMALL_STAMP(2);
     // ---- A2: every CTA: the bitmap and its word prefix in shared memory ----
     const uint32_t nw = (uint32_t)((a.N + 31) >> 5);
     for (uint32_t w = threadIdx.x; w < nw; w += kSmallThreads) s_bm[w] = __ldcg(bitmap + w);
@@ -1415,6 +1460,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         if (threadIdx.x == 0) s_pre[nw] = (uint32_t)tot;
     }
     __syncthreads();
+    SMALL_STAMP(3);
     const uint64_t K = s_pre[nw];
     // rank k -> page: the word by binary search over s_pre, the bit by select
     auto page_of = [&](uint64_t k) -> uint64_t {
@@ -1468,6 +1514,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     }
     // ---- CTA 0: table, ids, CRC, header ----
     __syncthreads();
+    SMALL_STAMP(4);
     if (threadIdx.x < 32) s_lpw[threadIdx.x] = a.x2n.lpw[threadIdx.x];
     for (uint32_t i = threadIdx.x; i < 256; i += kSmallThreads) {
         uint32_t c = i;
@@ -1532,6 +1579,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     block_excl_scan(runs, &tot_runs);
     block_excl_scan(dbytes, &tot_bytes);
     __syncthreads();  // table, ids and padding written
+    SMALL_STAMP(5);
     // CRC-32 of table (12 R words) || ids (idsw words), 16-byte chunks from
     // the end.  The words come from the shared-memory stage, beyond it they
     // are recomputed -- never read back from the image (which may be a pinned
@@ -1584,6 +1632,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         s_hc = hc;
     }
     __syncthreads();
+    SMALL_STAMP(6);
     if (threadIdx.x == 0) {
         uint32_t acc = 0;
         for (uint32_t w = 0; w < kSmallThreads / 32; ++w) acc ^= s_x[w];

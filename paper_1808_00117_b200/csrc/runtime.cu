@@ -1197,8 +1197,9 @@ int crum_create(int device, const crum_config *cfg, crum_ctx **out) {
     if (cudaMalloc(&c->d_done, 16) != cudaSuccess) return fail(CRUM_E_NOMEM);
     c->fused_bps = fused_blocks_per_sm();
     c->small_bps = small_blocks_per_sm();
-    if (cudaMalloc(&c->d_small, 4 * kSmallPages / 32 + 64) != cudaSuccess) return fail(CRUM_E_NOMEM);
-    cudaMemset(c->d_small, 0, 4 * kSmallPages / 32 + 64);
+    // bitmap | 64 B of barrier words (+ the CRUM_SMALL_STAMPS profiling stamps)
+    if (cudaMalloc(&c->d_small, 4 * kSmallPages / 32 + 64 + 8 * 8 * 2048) != cudaSuccess) return fail(CRUM_E_NOMEM);
+    cudaMemset(c->d_small, 0, 4 * kSmallPages / 32 + 64 + 8 * 8 * 2048);
     if (cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocMapped) != cudaSuccess) return fail(CRUM_E_NOMEM);
     if (cudaHostAlloc(&c->h_rb, sizeof(RangeTotals) * (kMaxRanges + 1), cudaHostAllocMapped) != cudaSuccess)
         return fail(CRUM_E_NOMEM);
@@ -2219,7 +2220,6 @@ int crum_sync_shadow(crum_ctx *ctx, void *stream, uint64_t *dirty_out) {
     NOT_IN_SESSION(c);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool timing = c->timing_cfg;
-    int st;
     if (timing) CK(cudaEventRecord(c->ev_t[0], s));
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
     enqueue_detect(c, s, c->all, false);
@@ -3251,7 +3251,6 @@ int crum_debug_detect(crum_ctx *ctx, void *stream, uint8_t *host_flags, uint64_t
         return CRUM_E_INVAL;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    int st;
     enqueue_detect(c, s, c->all, false);
     launch_export_flags(launch_of(c, s), c->d_flags, c->d_force, c->N, kFlagTag, c->d_dbg);
     CK_LAUNCH();
