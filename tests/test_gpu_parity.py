@@ -553,7 +553,7 @@ def test_small_path_tracked_and_compare(crum):
         assert np.array_equal(ctx.debug_export(r + 1, crum.EXPORT_FORCE, synth.n_pages(nb, P)), o.force_bits(r + 1))
 
 
-@pytest.mark.parametrize("kind", ["mixed", "compare"])
+@pytest.mark.parametrize("kind", ["mixed", "compare", "tracked"])
 @pytest.mark.parametrize("no_mapped", [False, True])
 def test_mapped_store_gather(crum, kind, no_mapped):
     """Pinned gathers above the small-footprint size whose previous payload
@@ -566,9 +566,13 @@ def test_mapped_store_gather(crum, kind, no_mapped):
     CRUM_CFG_NO_MAPPED take the ring + D2H pipeline.  Image bytes, reports
     and shadows equal the oracle's every epoch, on every path, with ragged
     tails (and hash regions in the mixed set)."""
+    T = 2
     if kind == "mixed":
         specs = [(40 * MiB + 4096 * 3 + 5, 4 * KiB, C), (72 * MiB, 64 * KiB, H), (24 * MiB, 64 * KiB, C),
                  (8 * MiB + 300, 2 * MiB, H)]
+        limit = 16 * MiB
+    elif kind == "tracked":  # TRACKED regions: the writer marks what it writes
+        specs = [(24 * MiB + 4096 + 9, 4 * KiB, T), (16 * MiB, 64 * KiB, C), (8 * MiB, 64 * KiB, T)]
         limit = 16 * MiB
     else:
         specs = [(40 * MiB + 4096 * 3 + 5, 4 * KiB, C), (72 * MiB, 64 * KiB, C), (8 * MiB + 300, 64 * KiB, C)]
@@ -580,6 +584,12 @@ def test_mapped_store_gather(crum, kind, no_mapped):
     for epoch, d in [(0, 0.0), (1, 0.01), (2, 0.0), (3, 0.3), (4, 0.02), (5, 0.005), (6, 0.1), (7, 0.0)]:
         if epoch:
             p.write(epoch, d)
+            for r, (nb, P, mode) in enumerate(specs):
+                if mode == T:
+                    pages = synth.choose_dirty(p.S, epoch, r, synth.n_pages(nb, P), d)
+                    p.o.mark_pages(p.rid_o[r], pages)
+                    p.g.mark_dirty_pages(p.rid_g[r], torch.from_numpy(pages.astype(np.uint32)).cuda(), len(pages))
+            torch.cuda.synchronize()
         st, want, rep_o = p.o.checkpoint_gather()
         assert st == 0
         rep = p.g.checkpoint_gather(img)

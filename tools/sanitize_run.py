@@ -139,4 +139,19 @@ for z, (nb, P, m) in zip(zz, zq.specs):
 zr2.restore_scatter(zi, flags=crum.VERIFY)
 torch.cuda.synchronize()
 assert all(np.array_equal(z.cpu().numpy(), h) for z, h in zip(zz, zq.host))
+# mapped-store pinned gathers (footprints above the small-footprint size): one
+# range, halving ranges (mixed modes) and the single pass (compare only), each
+# after a gather whose payload selects it
+for specs, seed in (([(20 * MiB + 4096 * 3 + 7, 4 * KiB, 0), (8 * MiB, 64 * KiB, 1)], 53),
+                    ([(20 * MiB + 4096 * 3 + 7, 4 * KiB, 0), (8 * MiB + 100, 64 * KiB, 0)], 54)):
+    mq = fresh(specs, seed)
+    mi = mq.g.new_image()
+    paths = []
+    for e, d in ((1, 0.002), (2, 0.002), (3, 0.15), (4, 0.05), (5, 0.0)):
+        mq.write(e, d)
+        st, want, _ = mq.o.checkpoint_gather()
+        rep = mq.g.checkpoint_gather(mi)
+        paths.append(rep["path"])
+        assert mi.tobytes() == want.tobytes(), (seed, e)
+    assert any(x & crum.PATH_MAPPED for x in paths), paths
 print("sanitize workload ok; launches", p.g.launch_count + q.launch_count + r.launch_count + t.launch_count)
