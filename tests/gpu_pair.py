@@ -67,6 +67,8 @@ class Pair:
             if mode == crum.MODE_HASH:
                 if not np.array_equal(self.o.hashes(ro), self.g.debug_export(rg, crum.EXPORT_HASHES, n)):
                     return False
+            elif mode == crum.MODE_TRACKED:
+                continue  # no snapshot: the force bits are the whole state
             else:
                 if not np.array_equal(self.o.mirror(ro), self.g.debug_export(rg, crum.EXPORT_MIRROR, nb)):
                     return False
