@@ -44,6 +44,26 @@ CRUM_API int crum_synth_write_pages_tracked(void *dev_ptr, uint64_t bytes, uint6
                                            uint64_t epoch, uint64_t region_index, int touch,
                                            const void *tracker /* const crum_tracker* */, void *stream);
 
+/* Many regions in one launch (a footprint of thousands of regions -- config 4
+ * -- would otherwise cost one launch per region per epoch).  `regions` is a
+ * HOST array of n descriptors (copied before the call returns); region i gets
+ * exactly what crum_synth_fill(dev_ptr, bytes, seed, region_index, 0) /
+ * crum_synth_write_pages(dev_ptr, bytes, page_size, dev_pages, n_pages, seed,
+ * epoch, region_index, touch) give it (dev_pages: device u32 page list, may be
+ * NULL when n_pages == 0).  Errors: INVAL (a null or unaligned pointer, a page
+ * size that is 0 or not a multiple of 8), NOMEM, CUDA. */
+typedef struct crum_synth_region {
+    void *dev_ptr;
+    uint64_t bytes;
+    uint64_t page_size;        /* writer only */
+    uint64_t region_index;
+    const uint32_t *dev_pages; /* writer only */
+    uint64_t n_pages;          /* writer only */
+} crum_synth_region;
+CRUM_API int crum_synth_fill_regions(const crum_synth_region *regions, uint64_t n, uint64_t seed, void *stream);
+CRUM_API int crum_synth_write_regions(const crum_synth_region *regions, uint64_t n, uint64_t seed, uint64_t epoch,
+                                      int touch, void *stream);
+
 /* Streaming read of `bytes` (device buffer) between timed repetitions: evicts
  * L2 (writing dirty lines back outside the timed region), leaves it clean. */
 CRUM_API int crum_synth_scrub(void *dev_ptr, uint64_t bytes, void *stream);

@@ -45,12 +45,19 @@ EXPORTED = (
     "crum_restore_scatter", "crum_restore_scatter_device", "crum_status_string", "crum_last_error_detail",
     "crum_debug_detect", "crum_debug_export", "crum_launch_count", "crum_last_report",
     "crum_synth_fill", "crum_synth_write_pages", "crum_synth_scrub", "crum_probe_copy",
+    "crum_synth_fill_regions", "crum_synth_write_regions",
     "crum_synth_alloc_managed", "crum_synth_free_managed", "crum_synth_write_pages_tracked",
     "crum_mark_dirty_pages", "crum_region_tracker",
     "crum_image_persist", "crum_image_persist_wait", "crum_image_persist_busy", "crum_image_load",
     "crum_restore_begin", "crum_restore_fetch", "crum_restore_end",
     "crum_image_numa_node", "crum_device_numa_node", "crum_config_init", "crum_pinned_pool_info",
 )
+
+
+class SynthRegion(C.Structure):
+    """crum_synth_region (include/crum_synth.h): one region of a batched synth call."""
+    _fields_ = [("dev_ptr", C.c_void_p), ("bytes", C.c_uint64), ("page_size", C.c_uint64),
+                ("region_index", C.c_uint64), ("dev_pages", C.c_void_p), ("n_pages", C.c_uint64)]
 
 
 class Tracker(C.Structure):
@@ -112,6 +119,8 @@ _sig = {
     "crum_synth_fill": (_i, [_vp, _u64, _u64, _u64, _u64, _vp]),
     "crum_synth_write_pages": (_i, [_vp, _u64, _u64, _vp, _u64, _u64, _u64, _u64, _i, _vp]),
     "crum_synth_scrub": (_i, [_vp, _u64, _vp]),
+    "crum_synth_fill_regions": (_i, [C.POINTER(SynthRegion), _u64, _u64, _vp]),
+    "crum_synth_write_regions": (_i, [C.POINTER(SynthRegion), _u64, _u64, _u64, _i, _vp]),
     "crum_probe_copy": (_i, [_vp, _vp, _u64, _i, _vp]),
     "crum_synth_alloc_managed": (_i, [C.POINTER(_vp), _u64, _i, _u64]),
     "crum_synth_free_managed": (_i, [_vp]),
@@ -495,6 +504,20 @@ def synth_write_pages_tracked(dev_ptr, nbytes: int, page_size: int, dev_pages, n
     _check(_L.crum_synth_write_pages_tracked(_addr(dev_ptr), nbytes, page_size, _addr(dev_pages) if n_pages else None,
                                              n_pages, seed, epoch, region_index, int(touch), C.byref(tracker),
                                              _stream(stream)), "crum_synth_write_pages_tracked")
+
+
+def synth_fill_regions(regions, seed: int, stream=None):
+    """regions: [(dev_ptr, nbytes, region_index)], one launch for all of them."""
+    arr = (SynthRegion * len(regions))(*[SynthRegion(_addr(p), nb, 0, r, None, 0) for p, nb, r in regions])
+    _check(_L.crum_synth_fill_regions(arr, len(regions), seed, _stream(stream)), "crum_synth_fill_regions")
+
+
+def synth_write_regions(regions, seed: int, epoch: int, touch: bool = False, stream=None):
+    """regions: [(dev_ptr, nbytes, page_size, region_index, dev_pages, n_pages)], one launch."""
+    arr = (SynthRegion * len(regions))(*[SynthRegion(_addr(p), nb, P, r, _addr(pg) if n else None, n)
+                                         for p, nb, P, r, pg, n in regions])
+    _check(_L.crum_synth_write_regions(arr, len(regions), seed, epoch, int(touch), _stream(stream)),
+           "crum_synth_write_regions")
 
 
 def synth_scrub(dev_ptr, nbytes: int, stream=None):

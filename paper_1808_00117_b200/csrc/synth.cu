@@ -1,5 +1,8 @@
 // synth.cu -- device implementation of the seeded input recipe of
 // synth/__init__.py (bench/test inputs only; holds none of the method).
+#include <algorithm>
+#include <vector>
+
 #include "crum_internal.cuh"
 #include "../../include/crum.h"
 #include "../../include/crum_synth.h"
@@ -37,6 +40,72 @@ __global__ void k_synth_write(uint8_t *p, uint64_t bytes, uint64_t page_size, co
     const uint64_t lo = i * page_size;
     const uint64_t hi = min(lo + page_size, bytes);
     const uint64_t nfull = (hi - lo) / 8;
+    uint64_t *w = reinterpret_cast<uint64_t *>(p + lo);
+    if (touch) {
+        if (threadIdx.x == 0) {
+            const uint64_t wlo = lo + ((hi - lo - 1) / 8) * 8;
+            for (uint64_t b = wlo; b < hi; ++b) p[b] ^= (uint8_t)(m >> (8 * (b - wlo)));
+        }
+        return;
+    }
+    for (uint64_t j = threadIdx.x; j < nfull; j += blockDim.x) w[j] ^= m;
+    if (threadIdx.x == 0)
+        for (uint64_t b = lo + nfull * 8; b < hi; ++b) p[b] ^= (uint8_t)(m >> (8 * (b - lo - nfull * 8)));
+}
+
+// Batched forms: descriptor d covers words [w0, w0 + words) of the batch
+// (fill) or listed pages [q0, q0 + n) (writer); a thread / block finds its
+// descriptor by binary search over the prefix.
+struct SynthDesc {
+    uint8_t *p;
+    uint64_t bytes, page_size, r;
+    const uint32_t *pages;
+    uint64_t n;        // listed pages
+    uint64_t w0, q0;   // prefix of whole words / listed pages before this descriptor
+};
+
+__device__ __forceinline__ uint32_t synth_desc_of(const SynthDesc *d, uint32_t nd, uint64_t x, bool pages) {
+    uint32_t lo = 0, hi = nd;  // largest i with prefix(i) <= x
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((pages ? d[mid].q0 : d[mid].w0) <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_synth_fill_regions(const SynthDesc *d, uint32_t nd, uint64_t total_words, uint64_t seed) {
+    uint32_t i = 0;
+    uint64_t lo = 1, hi = 0;  // word range of descriptor i (cached)
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total_words;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        if (j < lo || j >= hi) {
+            i = synth_desc_of(d, nd, j, false);
+            lo = d[i].w0;
+            hi = lo + d[i].bytes / 8;
+        }
+        reinterpret_cast<uint64_t *>(d[i].p)[j - lo] = splitmix64((seed ^ (d[i].r << 40)) ^ (j - lo));
+    }
+    // ragged tails: one thread per descriptor
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nd; k += (uint64_t)gridDim.x * blockDim.x) {
+        const SynthDesc &e = d[k];
+        const uint64_t nw = e.bytes / 8;
+        if (!(e.bytes & 7)) continue;
+        const uint64_t v = splitmix64((seed ^ (e.r << 40)) ^ nw);
+        for (uint64_t b = nw * 8; b < e.bytes; ++b) e.p[b] = (uint8_t)(v >> (8 * (b - nw * 8)));
+    }
+}
+
+// One block per listed page of the batch (k_synth_write's body).
+__global__ void k_synth_write_regions(const SynthDesc *d, uint32_t nd, uint64_t q_base, uint64_t seed,
+                                      uint64_t epoch, int touch) {
+    const uint64_t q = q_base + blockIdx.x;
+    const SynthDesc &e = d[synth_desc_of(d, nd, q, true)];
+    const uint64_t i = e.pages[q - e.q0];
+    const uint64_t m = splitmix64((seed + 2) ^ (epoch << 56) ^ (e.r << 40) ^ i) | 1ull;
+    const uint64_t lo = i * e.page_size;
+    const uint64_t hi = min(lo + e.page_size, e.bytes);
+    const uint64_t nfull = (hi - lo) / 8;
+    uint8_t *p = e.p;
     uint64_t *w = reinterpret_cast<uint64_t *>(p + lo);
     if (touch) {
         if (threadIdx.x == 0) {
@@ -130,6 +199,63 @@ extern "C" int crum_synth_write_pages_tracked(void *dev_ptr, uint64_t bytes, uin
     if (!dev_pages) return CRUM_E_INVAL;
     crum::launch_synth_write((cudaStream_t)stream, (uint8_t *)dev_ptr, bytes, page_size, dev_pages, n_pages,
                              seed, epoch, region_index, touch, static_cast<const crum_tracker *>(tracker));
+    return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
+}
+
+namespace {
+// Descriptors -> a stream-ordered device copy (freed stream-ordered after use).
+int synth_descs(const crum_synth_region *regions, uint64_t n, bool writer, cudaStream_t s,
+                crum::SynthDesc **out, uint64_t *words, uint64_t *listed) {
+    std::vector<crum::SynthDesc> h(n);
+    uint64_t w = 0, q = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const crum_synth_region &r = regions[i];
+        if (!r.dev_ptr || (reinterpret_cast<uintptr_t>(r.dev_ptr) & 7)) return CRUM_E_INVAL;
+        if (writer && (!r.page_size || (r.page_size & 7) || (r.n_pages && !r.dev_pages))) return CRUM_E_INVAL;
+        h[i] = crum::SynthDesc{static_cast<uint8_t *>(r.dev_ptr), r.bytes, r.page_size, r.region_index,
+                               r.dev_pages, writer ? r.n_pages : 0, w, q};
+        w += r.bytes / 8;
+        q += writer ? r.n_pages : 0;
+    }
+    *words = w;
+    *listed = q;
+    if (cudaMallocAsync(reinterpret_cast<void **>(out), n * sizeof(crum::SynthDesc), s) != cudaSuccess) {
+        cudaGetLastError();
+        return CRUM_E_NOMEM;
+    }
+    // pageable source: the copy is complete (staged) when the call returns
+    if (cudaMemcpyAsync(*out, h.data(), n * sizeof(crum::SynthDesc), cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return CRUM_E_CUDA;
+    return CRUM_OK;
+}
+}  // namespace
+
+extern "C" int crum_synth_fill_regions(const crum_synth_region *regions, uint64_t n, uint64_t seed, void *stream) {
+    if (!n) return CRUM_OK;
+    if (!regions || n > 0xffffffffull) return CRUM_E_INVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    crum::SynthDesc *d = nullptr;
+    uint64_t words = 0, listed = 0;
+    int st = synth_descs(regions, n, false, s, &d, &words, &listed);
+    if (st) return st;
+    crum::k_synth_fill_regions<<<148 * 8, 256, 0, s>>>(d, (uint32_t)n, words, seed);
+    cudaFreeAsync(d, s);
+    return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
+}
+
+extern "C" int crum_synth_write_regions(const crum_synth_region *regions, uint64_t n, uint64_t seed, uint64_t epoch,
+                                        int touch, void *stream) {
+    if (!n) return CRUM_OK;
+    if (!regions || n > 0xffffffffull) return CRUM_E_INVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    crum::SynthDesc *d = nullptr;
+    uint64_t words = 0, listed = 0;
+    int st = synth_descs(regions, n, true, s, &d, &words, &listed);
+    if (st) return st;
+    for (uint64_t b0 = 0; b0 < listed; b0 += (1u << 30))
+        crum::k_synth_write_regions<<<(unsigned)std::min<uint64_t>(listed - b0, 1ull << 30), 256, 0, s>>>(
+            d, (uint32_t)n, b0, seed, epoch, touch);
+    cudaFreeAsync(d, s);
     return cudaGetLastError() == cudaSuccess ? CRUM_OK : CRUM_E_CUDA;
 }
 

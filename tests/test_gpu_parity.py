@@ -67,6 +67,32 @@ def test_detect_parity_mixed(crum, misalign):
     assert np.array_equal(p.g.debug_detect(p.N), p.oracle_flags())
 
 
+def test_synth_batched_matches_single(crum):
+    """crum_synth_fill_regions / crum_synth_write_regions (one launch for many
+    regions, bench.py's C4 setup and writer) give every region exactly what
+    the per-region calls give it: ragged sizes (one below a word), empty
+    page lists, both writer forms."""
+    sizes = [4 * 4096 + 13, 5, 64 * KiB, 3 * 4096, 9 * 4096 + 8]
+    P = 4096
+    S = synth.seed(9)
+    a = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for nb in sizes]
+    b = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for nb in sizes]
+    crum.synth_fill_regions([(t, nb, r + 3) for r, (t, nb) in enumerate(zip(a, sizes))], S)
+    for r, (t, nb) in enumerate(zip(b, sizes)):
+        crum.synth_fill(t, nb, S, r + 3)
+    torch.cuda.synchronize()
+    assert all(torch.equal(x, y) for x, y in zip(a, b))
+    for touch in (False, True):
+        pages = [torch.tensor(sorted({0, synth.n_pages(nb, P) - 1}) if r != 1 else [], dtype=torch.int32,
+                              device="cuda") for r, nb in enumerate(sizes)]
+        crum.synth_write_regions([(t, nb, P, r + 3, pg, pg.numel()) for r, (t, nb, pg) in enumerate(zip(a, sizes, pages))],
+                                 S, 7, touch)
+        for r, (t, nb, pg) in enumerate(zip(b, sizes, pages)):
+            crum.synth_write_pages(t, nb, P, pg, pg.numel(), S, 7, r + 3, touch)
+        torch.cuda.synchronize()
+        assert all(torch.equal(x, y) for x, y in zip(a, b)), touch
+
+
 def test_exhaustive_single_byte_flips(crum):
     for mode in (C, H):
         p = mkpair([(2 * 4096, 4096, mode)], 11)
