@@ -1,5 +1,5 @@
 # Temporary phase timestamps in k_small_ckpt (CTA 0, thread 0 prints) -- a
-# profiling aid applied on the GPU box only (tools/gpu_r02x.sh)
+# profiling aid applied on the GPU box only (tools/calls/gpu_r02x.sh)
 p='paper_1808_00117_b200/csrc/kernels_image.cu'
 s=open(p).read()
 s='#include <cstdio>\n'+s
