@@ -2173,6 +2173,7 @@ int gather_mapped(crum_ctx *c, cudaStream_t s, crum_image *img, bool fused, bool
         uint8_t *payload = d + payload_offset_for(c->regs.size());
         Launch L = launch_of(c, s), G = launch_of(c, c->gstream);
         CK(cudaEventRecord(c->ev_t[0], s));
+        CK(cudaEventRecord(c->ev_t[4], s));  // the stores start with the first range's gather
         CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
         for (uint32_t ci = 0; ci < nr; ++ci) {
             enqueue_detect(c, s, rs[ci], false);
