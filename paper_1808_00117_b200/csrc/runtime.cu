@@ -2025,7 +2025,11 @@ int gather_z(crum_ctx *c, cudaStream_t s, uint8_t *dev_img, crum_image *himg, ui
         }
         return CRUM_OK;
     };
-    while (enq < nr && enq < 2)
+    // one range ahead of the chunk loop: a detect grid holds the SMs the
+    // encoder needs (C2, profiles/r02/compress/lookahead/: two ahead random
+    // 465 / half 602 / hpgmg 549 GB/s, one ahead 466 / 618 / 553, all ahead
+    // 404 / 521 / 485)
+    while (enq < nr && enq < 1)
         if ((st = enqueue_range(enq++))) return st;
     CK(cudaEventRecord(c->ev_fork, s));
     CK(cudaStreamWaitEvent(c->gstream, c->ev_fork, 0));  // the zrun / rb resets
@@ -2051,7 +2055,7 @@ int gather_z(crum_ctx *c, cudaStream_t s, uint8_t *dev_img, crum_image *himg, ui
         return CRUM_OK;
     };
     for (uint32_t ci = 0; ci < nr; ++ci) {
-        while (enq < nr && enq <= ci + 2)
+        while (enq < nr && enq <= ci + 1)
             if ((st = enqueue_range(enq++))) return st;
         CK(cudaEventSynchronize(c->ev_range[ci]));
         const uint64_t U0 = c->h_rb[ci].units, U1 = c->h_rb[ci + 1].units;
