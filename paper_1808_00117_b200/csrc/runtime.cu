@@ -2418,6 +2418,9 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     const uint32_t nr = one_range ? 1u : (uint32_t)c->ranges.size();
     auto range_at = [&](uint32_t ci) -> const Range & { return one_range ? c->all : c->ranges[ci]; };
     const uint64_t poff = payload_offset_for(c->regs.size());
+    void *dp = nullptr;
+    CK(cudaHostGetDevicePointer(&dp, img->host, 0));
+    uint8_t *dimg = static_cast<uint8_t *>(dp);  // the image's mapped address (metadata)
     CK(cudaEventRecord(c->ev_t[0], s));
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
     // detect + compact of range ci on the caller's stream; after the last range
@@ -2426,15 +2429,22 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     auto enqueue_range = [&](uint32_t ci) -> int {
         const Range &rg = range_at(ci);
         enqueue_detect(c, s, rg, full);
-        enqueue_compact(c, s, compact_args(c, rg, ci, ci == 0, ci + 1 == nr, full, UINT64_MAX, c->d_meta));
+        // the final compaction checks the image's capacity: a CAPACITY status
+        // stops the CRC kernel before it writes anything into the image
+        enqueue_compact(c, s, compact_args(c, rg, ci, ci == 0, ci + 1 == nr, full, img->cap, c->d_meta));
         CK_LAUNCH();
         CK(cudaEventRecord(c->ev_range[ci], s));  // h_rb[ci + 1] written by the kernel (mapped)
         if (c->trace) CK(cudaEventRecord(c->ev_trace[3 * ci], s));
         if (ci + 1 == nr) {
             CK(cudaEventRecord(c->ev_t[1], s));
-            launch_crc_meta(launch_of(c, s), crc_args(c, c->d_meta, c->d_meta + poff), crc_max_len(c));
+            // header, table, padding and tail straight into the pinned image
+            // through its mapped address (no metadata copies, no host wait at
+            // the end); the final stats into mapped memory
+            CrcArgs cra = crc_args(c, c->d_meta, nullptr);
+            cra.out = dimg;
+            launch_crc_meta(launch_of(c, s), cra, crc_max_len(c));
             CK_LAUNCH();
-            CK(cudaEventRecord(c->ev_meta, s));  // h_st written by the CRC kernel's last block (mapped)
+            CK(cudaEventRecord(c->ev_meta, s));  // h_st written by the CRC kernel (mapped)
         }
         return CRUM_OK;
     };
@@ -2509,20 +2519,15 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
             }
         }
     }
-    // header + table, then ids/hashes
-    CK(cudaEventSynchronize(c->ev_meta));
-    const DevStats h = *c->h_st;
-    CK(cudaStreamWaitEvent(c->copy, c->ev_meta, 0));
+    // the metadata went in through the mapped address (CRC kernel on s)
     if (!copy_started) CK(cudaEventRecord(c->ev_t[4], c->copy));
-    CK(cudaMemcpyAsync(img->host, c->d_meta, poff, cudaMemcpyDeviceToHost, c->copy));
-    if (h.image_bytes > h.ids_off)
-        CK(cudaMemcpyAsync(img->host + h.ids_off, c->d_meta + poff, h.image_bytes - h.ids_off,
-                           cudaMemcpyDeviceToHost, c->copy));
+    CK(cudaStreamWaitEvent(c->copy, c->ev_meta, 0));
     CK(cudaEventRecord(c->ev_t[5], c->copy));
     CK(cudaEventRecord(c->ev_t[3], c->gstream));
     CK(cudaStreamSynchronize(c->gstream));
     CK(cudaStreamSynchronize(c->copy));
     CK(cudaStreamSynchronize(s));
+    const DevStats h = *c->h_st;
     CK(cudaEventRecord(c->ev_done, s));
     ++c->gathers_since_rebuild;
     c->last_kind = kLastHostGather;
