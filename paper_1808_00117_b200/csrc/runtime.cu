@@ -264,6 +264,7 @@ struct crum_ctx {
     std::vector<HostRegion> regs;
     std::vector<Range> ranges;
     std::vector<Range> mranges;  // the mapped-store path's ranges (halving: 1/2, 1/4, 1/4)
+    std::vector<Range> zranges;  // compressed pinned gathers: as ranges, from 64 MiB
     Range all{};
     uint32_t next_id = 1;
     uint64_t N = 0, F = 0, max_units = 0;
@@ -707,29 +708,37 @@ int rebuild(crum_ctx *c, std::vector<HostRegion> regs, const std::vector<uint64_
     // delayed the first copy more than it saved: C2 hash 2 MiB e2e 482 vs 502.)
     const uint64_t min_big = (uint64_t)std::max(c->sms, 1);
     const uint64_t target_max = std::max(kMinRangeBytes, F / 8);
-    uint64_t target = std::max<uint64_t>(16ull << 20, F / 128);
-    uint64_t lo = 0, acc = 0, nbig = 0;
-    for (uint32_t r = 0; r < R; ++r) {
-        const HostRegion &h = c->regs[r];
-        const bool big_hash = h.mode == kModeHash && h.log2p >= 16;
-        for (uint64_t i = 0; i < h.n_pages; ++i) {
-            const uint64_t g = h.page_base + i;
-            if (acc >= target && (nbig == 0 || nbig >= min_big) && g % 16 == 0 &&
-                (int)c->ranges.size() < kMaxRanges - 1) {
-                c->ranges.push_back(make_range(c, lo, g));
-                lo = g;
-                acc = 0;
-                nbig = 0;
-                target = std::min(target_max, 2 * target);
+    auto build_ranges = [&](std::vector<Range> &out, uint64_t target) {
+        out.clear();
+        uint64_t lo = 0, acc = 0, nbig = 0;
+        for (uint32_t r = 0; r < R; ++r) {
+            const HostRegion &h = c->regs[r];
+            const bool big_hash = h.mode == kModeHash && h.log2p >= 16;
+            for (uint64_t i = 0; i < h.n_pages; ++i) {
+                const uint64_t g = h.page_base + i;
+                if (acc >= target && (nbig == 0 || nbig >= min_big) && g % 16 == 0 &&
+                    (int)out.size() < kMaxRanges - 1) {
+                    out.push_back(make_range(c, lo, g));
+                    lo = g;
+                    acc = 0;
+                    nbig = 0;
+                    target = std::min(target_max, 2 * target);
+                }
+                // whole pages at a time is fine for large regions; skip ahead in big steps
+                const uint64_t step = std::min<uint64_t>(h.n_pages - i, 16 - (g % 16));
+                acc += step * h.page_size;
+                if (big_hash) nbig += step;
+                i += step - 1;
             }
-            // whole pages at a time is fine for large regions; skip ahead in big steps
-            const uint64_t step = std::min<uint64_t>(h.n_pages - i, 16 - (g % 16));
-            acc += step * h.page_size;
-            if (big_hash) nbig += step;
-            i += step - 1;
         }
-    }
-    c->ranges.push_back(make_range(c, lo, N));
+        out.push_back(make_range(c, lo, N));
+    };
+    build_ranges(c->ranges, std::max<uint64_t>(16ull << 20, F / 128));
+    // Compressed gathers start from 64 MiB ranges: a chunk's way to the link
+    // (detect, compact, host wake, gather, encode ~30 us, scan, pack, host
+    // wake) is ~100 us, which the first ranges' short copies did not cover
+    build_ranges(c->zranges, std::max<uint64_t>(64ull << 20, F / 32));
+    uint64_t lo = 0;
     // The mapped-store path's ranges: the stores of range c overlap the
     // detection of range c + 1 and every boundary costs a kernel drain, so a
     // few ranges of decreasing size -- the first half, a quarter, the rest --
@@ -737,7 +746,6 @@ int rebuild(crum_ctx *c, std::vector<HostRegion> regs, const std::vector<uint64_
     // serial chains want every page of the footprint in one launch (C2 hash
     // 2 MiB at 1 %: two ranges of 256 pages 0.465 ms, one range 0.435 ms).
     c->mranges.clear();
-    lo = 0;
     if (big_at(c, N) == 0)
         for (const uint64_t want : {N / 2, (3 * N) / 4}) {
             const uint64_t g = want / 16 * 16;
@@ -2007,8 +2015,8 @@ int gather_z(crum_ctx *c, cudaStream_t s, uint8_t *dev_img, crum_image *himg, ui
     uint8_t *head = himg ? c->d_meta : (capacity >= poff ? img : nullptr);
     const uint64_t plimit = capacity > poff ? capacity - poff : 1;  // payload bytes that fit
     // a host image streams range by range; a device image is one range
-    const uint32_t nr = himg ? (uint32_t)c->ranges.size() : 1;
-    auto range_of = [&](uint32_t ci) -> const Range & { return himg ? c->ranges[ci] : c->all; };
+    const uint32_t nr = himg ? (uint32_t)c->zranges.size() : 1;
+    auto range_of = [&](uint32_t ci) -> const Range & { return himg ? c->zranges[ci] : c->all; };
     Launch G = launch_of(c, c->gstream);
     CK(cudaEventRecord(c->ev_t[0], s));
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
