@@ -631,3 +631,27 @@ def test_mapped_store_gather(crum, kind, no_mapped):
         if mapped:  # the single pass above 2 MiB; below it, halving ranges above 1 MiB, else one range
             assert bool(rep["path"] & crum.PATH_FUSED) == (kind == "compare" and prev_payload > 2 * MiB)
         prev_payload = int.from_bytes(want.tobytes()[32:40], "little")
+
+
+@pytest.mark.parametrize("where", ["pool", "numa"])
+def test_mapped_store_pool_and_numa_images(crum, where):
+    """The mapped-store paths write through the image's device-mapped
+    address: images carved from the context's pinned pool
+    (crum_config.pinned_pool_bytes) and NUMA-bound images (mmap + mbind +
+    registration) take them too, bit-exact with the oracle."""
+    specs = [(40 * MiB + 4096 * 3 + 5, 4 * KiB, C), (24 * MiB, 64 * KiB, C)]
+    kw = {"pinned_pool_bytes": 256 * MiB} if where == "pool" else {"numa_node": 0}
+    p = mkpair(specs, 29, **kw)
+    img = p.g.new_image()
+    paths = []
+    for epoch, d in [(0, 0.0), (1, 0.005), (2, 0.0), (3, 0.1), (4, 0.001)]:
+        if epoch:
+            p.write(epoch, d)
+        st, want, _ = p.o.checkpoint_gather()
+        assert st == 0
+        rep = p.g.checkpoint_gather(img)
+        assert img.tobytes() == want.tobytes(), epoch
+        assert p.shadows_equal(), epoch
+        paths.append(rep["path"])
+    assert sum(bool(x & crum.PATH_MAPPED) for x in paths) >= 3, paths
+    assert any(x & crum.PATH_FUSED for x in paths), paths   # epoch 4: after the 10 % epoch

@@ -264,7 +264,6 @@ struct crum_ctx {
     std::vector<HostRegion> regs;
     std::vector<Range> ranges;
     std::vector<Range> mranges;  // the mapped-store path's ranges (halving: 1/2, 1/4, 1/4)
-    std::vector<Range> zranges;  // compressed pinned gathers: as ranges, from 64 MiB
     Range all{};
     uint32_t next_id = 1;
     uint64_t N = 0, F = 0, max_units = 0;
@@ -708,37 +707,29 @@ int rebuild(crum_ctx *c, std::vector<HostRegion> regs, const std::vector<uint64_
     // delayed the first copy more than it saved: C2 hash 2 MiB e2e 482 vs 502.)
     const uint64_t min_big = (uint64_t)std::max(c->sms, 1);
     const uint64_t target_max = std::max(kMinRangeBytes, F / 8);
-    auto build_ranges = [&](std::vector<Range> &out, uint64_t target) {
-        out.clear();
-        uint64_t lo = 0, acc = 0, nbig = 0;
-        for (uint32_t r = 0; r < R; ++r) {
-            const HostRegion &h = c->regs[r];
-            const bool big_hash = h.mode == kModeHash && h.log2p >= 16;
-            for (uint64_t i = 0; i < h.n_pages; ++i) {
-                const uint64_t g = h.page_base + i;
-                if (acc >= target && (nbig == 0 || nbig >= min_big) && g % 16 == 0 &&
-                    (int)out.size() < kMaxRanges - 1) {
-                    out.push_back(make_range(c, lo, g));
-                    lo = g;
-                    acc = 0;
-                    nbig = 0;
-                    target = std::min(target_max, 2 * target);
-                }
-                // whole pages at a time is fine for large regions; skip ahead in big steps
-                const uint64_t step = std::min<uint64_t>(h.n_pages - i, 16 - (g % 16));
-                acc += step * h.page_size;
-                if (big_hash) nbig += step;
-                i += step - 1;
+    uint64_t target = std::max<uint64_t>(16ull << 20, F / 128);
+    uint64_t lo = 0, acc = 0, nbig = 0;
+    for (uint32_t r = 0; r < R; ++r) {
+        const HostRegion &h = c->regs[r];
+        const bool big_hash = h.mode == kModeHash && h.log2p >= 16;
+        for (uint64_t i = 0; i < h.n_pages; ++i) {
+            const uint64_t g = h.page_base + i;
+            if (acc >= target && (nbig == 0 || nbig >= min_big) && g % 16 == 0 &&
+                (int)c->ranges.size() < kMaxRanges - 1) {
+                c->ranges.push_back(make_range(c, lo, g));
+                lo = g;
+                acc = 0;
+                nbig = 0;
+                target = std::min(target_max, 2 * target);
             }
+            // whole pages at a time is fine for large regions; skip ahead in big steps
+            const uint64_t step = std::min<uint64_t>(h.n_pages - i, 16 - (g % 16));
+            acc += step * h.page_size;
+            if (big_hash) nbig += step;
+            i += step - 1;
         }
-        out.push_back(make_range(c, lo, N));
-    };
-    build_ranges(c->ranges, std::max<uint64_t>(16ull << 20, F / 128));
-    // Compressed gathers start from 64 MiB ranges: a chunk's way to the link
-    // (detect, compact, host wake, gather, encode ~30 us, scan, pack, host
-    // wake) is ~100 us, which the first ranges' short copies did not cover
-    build_ranges(c->zranges, std::max<uint64_t>(64ull << 20, F / 32));
-    uint64_t lo = 0;
+    }
+    c->ranges.push_back(make_range(c, lo, N));
     // The mapped-store path's ranges: the stores of range c overlap the
     // detection of range c + 1 and every boundary costs a kernel drain, so a
     // few ranges of decreasing size -- the first half, a quarter, the rest --
@@ -746,6 +737,7 @@ int rebuild(crum_ctx *c, std::vector<HostRegion> regs, const std::vector<uint64_
     // serial chains want every page of the footprint in one launch (C2 hash
     // 2 MiB at 1 %: two ranges of 256 pages 0.465 ms, one range 0.435 ms).
     c->mranges.clear();
+    lo = 0;
     if (big_at(c, N) == 0)
         for (const uint64_t want : {N / 2, (3 * N) / 4}) {
             const uint64_t g = want / 16 * 16;
@@ -1985,10 +1977,9 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
 // <= kZChunkUnits units (16 MiB) run on the gather stream: k_gather of the
 // chunk's listed pages into a raw staging buffer (no commit), encode, chunk
 // scan of the sizes (running total mirrored into mapped memory), pack.  A
-// pinned image takes a range pipeline like the plain path's, on coarser
-// ranges (c->zranges, from 64 MiB) and one range of detection ahead (detect +
-// compact of range c on the caller's stream while chunks of range c - 1
-// encode and copy); each chunk's packed bytes go through a ring slot and one D2H copy
+// pinned image takes the range pipeline of the plain path (detect + compact
+// of range c on the caller's stream while chunks of range c - 1 encode and
+// copy); each chunk's packed bytes go through a ring slot and one D2H copy
 // (the host reads the chunk's end offset once its pack is done, behind the
 // next chunk's encode).  Measured alternatives (profiles/r02/compress/):
 // short first chunks doubling up to 16 MiB (the link starts after a small
@@ -2016,8 +2007,8 @@ int gather_z(crum_ctx *c, cudaStream_t s, uint8_t *dev_img, crum_image *himg, ui
     uint8_t *head = himg ? c->d_meta : (capacity >= poff ? img : nullptr);
     const uint64_t plimit = capacity > poff ? capacity - poff : 1;  // payload bytes that fit
     // a host image streams range by range; a device image is one range
-    const uint32_t nr = himg ? (uint32_t)c->zranges.size() : 1;
-    auto range_of = [&](uint32_t ci) -> const Range & { return himg ? c->zranges[ci] : c->all; };
+    const uint32_t nr = himg ? (uint32_t)c->ranges.size() : 1;
+    auto range_of = [&](uint32_t ci) -> const Range & { return himg ? c->ranges[ci] : c->all; };
     Launch G = launch_of(c, c->gstream);
     CK(cudaEventRecord(c->ev_t[0], s));
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
@@ -2427,9 +2418,6 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     const uint32_t nr = one_range ? 1u : (uint32_t)c->ranges.size();
     auto range_at = [&](uint32_t ci) -> const Range & { return one_range ? c->all : c->ranges[ci]; };
     const uint64_t poff = payload_offset_for(c->regs.size());
-    void *dp = nullptr;
-    CK(cudaHostGetDevicePointer(&dp, img->host, 0));
-    uint8_t *dimg = static_cast<uint8_t *>(dp);  // the image's mapped address (metadata)
     CK(cudaEventRecord(c->ev_t[0], s));
     CK(cudaMemsetAsync(c->d_rb, 0, sizeof(RangeTotals), s));
     // detect + compact of range ci on the caller's stream; after the last range
@@ -2438,22 +2426,15 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     auto enqueue_range = [&](uint32_t ci) -> int {
         const Range &rg = range_at(ci);
         enqueue_detect(c, s, rg, full);
-        // the final compaction checks the image's capacity: a CAPACITY status
-        // stops the CRC kernel before it writes anything into the image
-        enqueue_compact(c, s, compact_args(c, rg, ci, ci == 0, ci + 1 == nr, full, img->cap, c->d_meta));
+        enqueue_compact(c, s, compact_args(c, rg, ci, ci == 0, ci + 1 == nr, full, UINT64_MAX, c->d_meta));
         CK_LAUNCH();
         CK(cudaEventRecord(c->ev_range[ci], s));  // h_rb[ci + 1] written by the kernel (mapped)
         if (c->trace) CK(cudaEventRecord(c->ev_trace[3 * ci], s));
         if (ci + 1 == nr) {
             CK(cudaEventRecord(c->ev_t[1], s));
-            // header, table, padding and tail straight into the pinned image
-            // through its mapped address (no metadata copies, no host wait at
-            // the end); the final stats into mapped memory
-            CrcArgs cra = crc_args(c, c->d_meta, nullptr);
-            cra.out = dimg;
-            launch_crc_meta(launch_of(c, s), cra, crc_max_len(c));
+            launch_crc_meta(launch_of(c, s), crc_args(c, c->d_meta, c->d_meta + poff), crc_max_len(c));
             CK_LAUNCH();
-            CK(cudaEventRecord(c->ev_meta, s));  // h_st written by the CRC kernel (mapped)
+            CK(cudaEventRecord(c->ev_meta, s));  // h_st written by the CRC kernel's last block (mapped)
         }
         return CRUM_OK;
     };
@@ -2528,15 +2509,20 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
             }
         }
     }
-    // the metadata went in through the mapped address (CRC kernel on s)
-    if (!copy_started) CK(cudaEventRecord(c->ev_t[4], c->copy));
+    // header + table, then ids/hashes
+    CK(cudaEventSynchronize(c->ev_meta));
+    const DevStats h = *c->h_st;
     CK(cudaStreamWaitEvent(c->copy, c->ev_meta, 0));
+    if (!copy_started) CK(cudaEventRecord(c->ev_t[4], c->copy));
+    CK(cudaMemcpyAsync(img->host, c->d_meta, poff, cudaMemcpyDeviceToHost, c->copy));
+    if (h.image_bytes > h.ids_off)
+        CK(cudaMemcpyAsync(img->host + h.ids_off, c->d_meta + poff, h.image_bytes - h.ids_off,
+                           cudaMemcpyDeviceToHost, c->copy));
     CK(cudaEventRecord(c->ev_t[5], c->copy));
     CK(cudaEventRecord(c->ev_t[3], c->gstream));
     CK(cudaStreamSynchronize(c->gstream));
     CK(cudaStreamSynchronize(c->copy));
     CK(cudaStreamSynchronize(s));
-    const DevStats h = *c->h_st;
     CK(cudaEventRecord(c->ev_done, s));
     ++c->gathers_since_rebuild;
     c->last_kind = kLastHostGather;
