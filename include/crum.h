@@ -341,8 +341,11 @@ CRUM_API int crum_image_load(crum_ctx *ctx, const char *path, crum_image **out);
  * readings Q5/Q12): detect (A1), compact the dirty ids in (region id, page
  * index) order (A2), gather those pages into the v1 image (A3; DESIGN.md
  * "Image format") and commit them, copying the image into `img` in pinned host
- * memory over the host link (A4).  flags: 0 or CRUM_FULL.  Returns when the
- * image is complete in host memory and the commit is done.
+ * memory over the host link (A4): range by range through a device ring and
+ * D2H copies, or -- small expected payloads, an image that holds a worst-case
+ * image -- stored by the kernels through the image's device-mapped address
+ * (CRUM_PATH_MAPPED).  flags: 0, CRUM_FULL, CRUM_COMPRESS.
+ * Returns when the image is complete in host memory and the commit is done.
  * Errors: INVAL; CAPACITY (nothing committed; report->image_bytes = needed);
  * CUDA.  report may be NULL.
  * ------------------------------------------------------------------------- */
