@@ -1300,20 +1300,25 @@ __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_re
 
 // Grid barrier of a cooperative launch (all CTAs co-resident): arrivals
 // counter + generation, sense by generation, state returns to 0 arrivals.
+// The arrival is one acq_rel atomic (it releases this CTA's bitmap atomics
+// and, for the last arrival, acquires everyone's); the last one resets the
+// count and publishes the next generation with a release store; the others
+// spin on an acquire load of the generation -- no separate fences.
 __device__ __forceinline__ void grid_barrier(uint32_t *bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile uint32_t *gen = bar + 1;
-        const uint32_t g = *gen;
-        fence_acq_rel_gpu();  // release this CTA's writes (bitmap atomics) before its arrival
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0;
-            fence_acq_rel_gpu();
-            atomicAdd(bar + 1, 1u);
+        uint32_t g, old;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        if (old == gridDim.x - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(g + 1) : "memory");
         } else {
-            while (*gen == g) __nanosleep(32);
+            uint32_t cur;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+            } while (cur == g);
         }
-        fence_acq_rel_gpu();  // acquire every CTA's writes
     }
     __syncthreads();
 }
