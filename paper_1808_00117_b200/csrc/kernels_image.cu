@@ -1402,7 +1402,8 @@ __device__ __forceinline__ void small_leave(const SmallArgs &a, uint32_t nw) {
 __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     __shared__ uint32_t s_bm[kSmallWords];    // dirty bitmap
     __shared__ uint32_t s_pre[kSmallWords + 1];  // dirty pages before word w
-    __shared__ uint32_t T[256];                // CRC-32 byte table (CTA 0)
+    __shared__ uint32_t T4[4][256];            // CRC-32 tables (CTA 0): T4[k][i] = byte i then k zero bytes
+    uint32_t *T = T4[0];                       // the byte-wise table
     __shared__ uint32_t s_lpw[32];             // x^(128 j) mod P (CTA 0)
     __shared__ uint32_t s_w[kSmallStageWords]; // table || ids words for the CRC (CTA 0)
     const uint32_t lane = threadIdx.x & 31;
@@ -1530,8 +1531,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     if (threadIdx.x < 32) s_lpw[threadIdx.x] = a.x2n.lpw[threadIdx.x];
     for (uint32_t i = threadIdx.x; i < 256; i += kSmallThreads) {
         uint32_t c = i;
-        for (int b = 0; b < 8; ++b) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
-        T[i] = c;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            for (int b = 0; b < 8; ++b) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+            T4[k][i] = c;
+        }
     }
     const uint64_t poff = a.poff, payload = K << a.log2p, ids_off = poff + payload;
     const uint64_t idsw = round_up(4 * K, 8) / 4;
@@ -1627,20 +1631,22 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     __shared__ uint32_t s_x[kSmallThreads / 32];
     __shared__ uint32_t s_hc;
     if (lane == 0) s_x[threadIdx.x >> 5] = gf2_mulmod_bf(a.x2n.wpw[threadIdx.x >> 5], x);
-    // the header's first 56 bytes are known already: their CRC beside the others
-    alignas(16) uint8_t h[64];
-    h[0] = 'C'; h[1] = 'R'; h[2] = 'U'; h[3] = 'M';
-    put32(h + 4, 1);
-    put32(h + 8, 0);
-    put32(h + 12, a.R);
-    put64(h + 16, K);
-    put64(h + 24, poff);
-    put64(h + 32, payload);
-    put64(h + 40, ids_off);
-    put64(h + 48, ids_off + 4 * idsw);
+    // the header's first 56 bytes (14 words, in registers) are known already:
+    // their CRC register beside the others, a word per step (slicing by 4)
+    auto crc_w4 = [&](uint32_t c, uint32_t w) -> uint32_t {
+        c ^= w;
+        return T4[3][c & 0xffu] ^ T4[2][(c >> 8) & 0xffu] ^ T4[1][(c >> 16) & 0xffu] ^ T4[0][c >> 24];
+    };
+    const uint64_t iend = ids_off + 4 * idsw;
+    const uint32_t hw0 = 0x4D555243u /* "CRUM" */, hw1 = 1u, hw2 = 0u, hw3 = a.R;
     if (threadIdx.x == 32) {
         uint32_t hc = 0xffffffffu;
-        for (int i = 0; i < 56; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
+        hc = crc_w4(hc, hw0); hc = crc_w4(hc, hw1); hc = crc_w4(hc, hw2); hc = crc_w4(hc, hw3);
+        hc = crc_w4(hc, (uint32_t)K); hc = crc_w4(hc, (uint32_t)(K >> 32));
+        hc = crc_w4(hc, (uint32_t)poff); hc = crc_w4(hc, (uint32_t)(poff >> 32));
+        hc = crc_w4(hc, (uint32_t)payload); hc = crc_w4(hc, (uint32_t)(payload >> 32));
+        hc = crc_w4(hc, (uint32_t)ids_off); hc = crc_w4(hc, (uint32_t)(ids_off >> 32));
+        hc = crc_w4(hc, (uint32_t)iend); hc = crc_w4(hc, (uint32_t)(iend >> 32));
         s_hc = hc;
     }
     __syncthreads();
@@ -1664,11 +1670,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         st->dirty_runs = tot_runs;
         st->crc_acc = 0;
         st->meta_crc = meta_crc;
-        put32(h + 56, meta_crc);
-        uint32_t hc = s_hc;
-        for (int i = 56; i < 60; ++i) hc = T[(hc ^ h[i]) & 0xffu] ^ (hc >> 8);
-        put32(h + 60, hc ^ 0xffffffffu);
-        for (int i = 0; i < 64; i += 16) *reinterpret_cast<uint4 *>(img + i) = *reinterpret_cast<const uint4 *>(h + i);
+        const uint32_t hcrc = crc_w4(s_hc, meta_crc) ^ 0xffffffffu;
+        uint4 *hd = reinterpret_cast<uint4 *>(img);
+        hd[0] = make_uint4(hw0, hw1, hw2, hw3);
+        hd[1] = make_uint4((uint32_t)K, (uint32_t)(K >> 32), (uint32_t)poff, (uint32_t)(poff >> 32));
+        hd[2] = make_uint4((uint32_t)payload, (uint32_t)(payload >> 32), (uint32_t)ids_off, (uint32_t)(ids_off >> 32));
+        hd[3] = make_uint4((uint32_t)iend, (uint32_t)(iend >> 32), meta_crc, hcrc);
     }
     small_leave(a, nw);
 }
