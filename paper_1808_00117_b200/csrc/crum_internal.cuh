@@ -225,6 +225,7 @@ void launch_fused_compare(const Launch &L, const FusedArgs &a, int blocks);
 // every region COMPARE or TRACKED with one page size, N <= kSmallPages,
 // image >= the worst case.
 constexpr uint32_t kSmallPages = 16384;
+constexpr uint32_t kSmallItemsLog2 = 2;  // k_small_ckpt detect: 2^this warp work items per 4 KiB segment
 struct SmallArgs {
     const DevRegion *regs;
     uint32_t R;

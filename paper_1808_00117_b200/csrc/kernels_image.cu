@@ -1415,11 +1415,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         atomicMax(reinterpret_cast<unsigned long long *>(a.bar + 4), ~(unsigned long long)gtime_ns());
     uint32_t *bitmap = a.bitmap;  // zero when the launch begins (small_leave)
     SMALL_STAMP(0);
-    // ---- A1 detect: warp per 2 KiB half segment (twice the warps of one per
-    // 4 KiB: more SMs issue the cold loads at once); a forced page is dirty ----
+    // ---- A1 detect: a warp per 4 KiB >> kSmallItemsLog2 of a segment (more
+    // warps than one per 4 KiB: more SMs issue the cold loads at once); a
+    // forced page is dirty ----
+    constexpr uint32_t kSmallItems = 1u << kSmallItemsLog2;
     uint32_t r = 0;
-    for (uint64_t g = wid; g < (a.N << spl) * 2; g += nwarps) {
-        const uint64_t pg = g >> (spl + 1);
+    for (uint64_t g = wid; g < (a.N << spl) * kSmallItems; g += nwarps) {
+        const uint64_t pg = g >> (spl + kSmallItemsLog2);
         while (r + 1 < a.R && a.regs[r + 1].page_base <= pg) ++r;
         while (a.regs[r].page_base > pg) --r;
         const DevRegion &R = a.regs[r];
@@ -1429,14 +1431,15 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         const uint8_t forced = a.force[pg];
         bool dirty = false;
         if (R.mode == kModeCompare) {
-            const uint64_t off = ((pg - R.page_base) << a.log2p) + ((g & ((2u << spl) - 1)) << (kSegLog2 - 1));
+            const uint64_t off = ((pg - R.page_base) << a.log2p) +
+                                 ((g & ((kSmallItems << spl) - 1)) << (kSegLog2 - kSmallItemsLog2));
             uint32_t x = 0;
             if (off < R.bytes) {
                 const uint64_t len = R.bytes - off;
                 const uint8_t *pa = R.base + off, *pb = R.mirror + off;
-                if (len >= kSegBytes / 2) {
+                if (len >= (kSegBytes >> kSmallItemsLog2)) {
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
+                    for (int i = 0; i < (8 >> kSmallItemsLog2); ++i) {
                         const uint4 u = __ldcs(reinterpret_cast<const uint4 *>(pa + i * 512 + lane * 16));
                         const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(pb + i * 512 + lane * 16));
                         x |= (u.x ^ v.x) | (u.y ^ v.y) | (u.z ^ v.z) | (u.w ^ v.w);

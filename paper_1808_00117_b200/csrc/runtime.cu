@@ -1825,7 +1825,7 @@ int enqueue_small(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, 
     sa.st = c->d_st;
     sa.st_host = c->dh_st;
     sa.x2n = crc_tables().x2n;
-    const uint64_t warps = (c->N << (c->small_log2p - kSegLog2)) * 2;  // one per 2 KiB
+    const uint64_t warps = (c->N << (c->small_log2p - kSegLog2)) << kSmallItemsLog2;  // a detect item each
     uint64_t blocks = (warps + 7) / 8;
     const uint64_t cap = (uint64_t)c->sms * c->small_bps;
     if (blocks > cap) blocks = cap;
