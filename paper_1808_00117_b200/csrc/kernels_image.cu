@@ -1303,7 +1303,9 @@ __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_re
 // The arrival is one acq_rel atomic (it releases this CTA's bitmap atomics
 // and, for the last arrival, acquires everyone's); the last one resets the
 // count and publishes the next generation with a release store; the others
-// spin on an acquire load of the generation -- no separate fences.
+// poll an acquire load of the generation, backing off between polls (~500
+// CTAs polling one address back to back slowed the release by ~1 us; a
+// two-level arrival tree was slower still).
 __device__ __forceinline__ void grid_barrier(uint32_t *bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1315,9 +1317,11 @@ __device__ __forceinline__ void grid_barrier(uint32_t *bar) {
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(g + 1) : "memory");
         } else {
             uint32_t cur;
-            do {
+            for (;;) {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
-            } while (cur == g);
+                if (cur != g) break;
+                __nanosleep(64);
+            }
         }
     }
     __syncthreads();
@@ -1337,7 +1341,7 @@ __device__ __forceinline__ uint64_t gtime_ns() {
 }  // namespace crum
 #include <cstdio>
 namespace crum {
-constexpr int kStampN = 8;
+constexpr int kStampN = 16;
 #define SMALL_STAMP(k)                                                                              \
     do {                                                                                            \
         if (threadIdx.x == 0)                                                                       \
@@ -1365,25 +1369,33 @@ __device__ void small_stamps_print(const SmallArgs &a) {
 #endif
 
 // Every CTA leaves through here (all threads, after the CTA's work -- which
-// includes its last read of the global bitmap): the last one out clears the
-// bitmap's nw words for the next launch, publishes the stats to the host --
-// with the kernel's own duration when timed -- and returns the scratch words
-// to 0.  (One bitmap, cleared on the way out: a launch needs no generation
-// read before its first load, which stalled every warp's first instructions
-// ~1 us when two bitmaps alternated by the barrier generation.)
+// includes its last read of the global bitmap).  CTAs 1.. count themselves
+// out; CTA 0 (the metadata CTA, the last to finish) waits until they all
+// have, then clears the bitmap's nw words for the next launch, publishes the
+// stats to the host -- with the kernel's own duration when timed -- and
+// returns the scratch words to 0.  CTA 0 itself needs no fence: nobody else
+// reads what it wrote during the launch (a fence after its header's stores
+// to a pinned image waited ~1.5 us for the host link).  (One bitmap, cleared
+// on the way out: a launch needs no generation read before its first load.)
 __device__ __forceinline__ void small_leave(const SmallArgs &a, uint32_t nw) {
-    __shared__ bool s_last;
     __syncthreads();
     SMALL_STAMP(7);
+    if (blockIdx.x != 0) {
+        if (threadIdx.x == 0) {
+            fence_acq_rel_gpu();  // this CTA's bitmap reads and commits before it counts out
+            atomicAdd(a.bar + 2, 1u);
+        }
+        return;
+    }
     if (threadIdx.x == 0) {
-        fence_acq_rel_gpu();  // release (CTA 0: the stats) before counting out
-        s_last = atomicAdd(a.bar + 2, 1u) == gridDim.x - 1;
+        uint32_t out;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(out) : "l"(a.bar + 2) : "memory");
+        } while (out != gridDim.x - 1);
     }
     __syncthreads();
-    if (!s_last) return;
     for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) a.bitmap[w] = 0;
     if (threadIdx.x != 0) return;
-    fence_acq_rel_gpu();  // acquire CTA 0's stats
 #ifdef CRUM_SMALL_STAMPS
     small_stamps_print(a);
 #endif
@@ -1407,8 +1419,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     __shared__ uint32_t s_lpw[32];             // x^(128 j) mod P (CTA 0)
     __shared__ uint32_t s_w[kSmallStageWords]; // table || ids words for the CRC (CTA 0)
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t wid = ((uint64_t)blockIdx.x * kSmallThreads + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * kSmallThreads) >> 5;
+    // detect runs on CTAs 1.. (CTA 0, the metadata CTA, builds its CRC tables
+    // meanwhile and reaches the barrier early); a one-CTA grid detects itself
+    const uint32_t dcta = gridDim.x > 1 ? 1u : 0u;
+    const uint64_t wid = ((uint64_t)(blockIdx.x - dcta) * kSmallThreads + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)(gridDim.x - dcta) * kSmallThreads) >> 5;
     const uint32_t spl = a.log2p - kSegLog2;   // log2 segments per page
     const uint64_t P = 1ull << a.log2p;
     if (a.timing && threadIdx.x == 0)  // the max of ~t is the earliest entry
@@ -1420,7 +1435,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     // forced page is dirty ----
     constexpr uint32_t kSmallItems = 1u << kSmallItemsLog2;
     uint32_t r = 0;
-    for (uint64_t g = wid; g < (a.N << spl) * kSmallItems; g += nwarps) {
+    for (uint64_t g = wid; blockIdx.x >= dcta && g < (a.N << spl) * kSmallItems; g += nwarps) {
         const uint64_t pg = g >> (spl + kSmallItemsLog2);
         while (r + 1 < a.R && a.regs[r + 1].page_base <= pg) ++r;
         while (a.regs[r].page_base > pg) --r;
@@ -1457,6 +1472,17 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     __syncthreads();
 #endif
     SMALL_STAMP(1);
+    if (blockIdx.x == 0) {  // CTA 0's CRC tables, while the barrier waits for the last CTA
+        if (threadIdx.x < 32) s_lpw[threadIdx.x] = a.x2n.lpw[threadIdx.x];
+        for (uint32_t i = threadIdx.x; i < 256; i += kSmallThreads) {
+            uint32_t c = i;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                for (int b = 0; b < 8; ++b) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+                T4[k][i] = c;
+            }
+        }
+    }
     grid_barrier(a.bar);
     SMALL_STAMP(2);
     // ---- A2: every CTA: the bitmap and its word prefix in shared memory ----
@@ -1532,15 +1558,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     // ---- CTA 0: table, ids, CRC, header ----
     __syncthreads();
     SMALL_STAMP(4);
-    if (threadIdx.x < 32) s_lpw[threadIdx.x] = a.x2n.lpw[threadIdx.x];
-    for (uint32_t i = threadIdx.x; i < 256; i += kSmallThreads) {
-        uint32_t c = i;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            for (int b = 0; b < 8; ++b) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
-            T4[k][i] = c;
-        }
-    }
+    SMALL_STAMP(8);
     const uint64_t poff = a.poff, payload = K << a.log2p, ids_off = poff + payload;
     const uint64_t idsw = round_up(4 * K, 8) / 4;
     uint8_t *img = a.img;
@@ -1573,6 +1591,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     // zero padding to the payload: 16-byte stores (64 + 48 R and poff are multiples of 16)
     for (uint64_t b = 64 + 48ull * a.R + 16ull * threadIdx.x; b < poff; b += 16ull * kSmallThreads)
         *reinterpret_cast<uint4 *>(img + b) = make_uint4(0, 0, 0, 0);
+    SMALL_STAMP(9);
     // ids (region-local page indices), runs, logical bytes
     uint32_t *tids = reinterpret_cast<uint32_t *>(img + ids_off);
     uint64_t runs = 0, dbytes = 0;
@@ -1595,6 +1614,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
             dbytes += min(P, R.bytes - (i << a.log2p));
         }
     }
+    SMALL_STAMP(10);
     uint64_t tot_runs, tot_bytes;
     block_excl_scan(runs, &tot_runs);
     block_excl_scan(dbytes, &tot_bytes);
@@ -1627,8 +1647,28 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
         while (a.regs[cr].page_base > pg) --cr;
         return (uint32_t)(pg - a.regs[cr].page_base);
     };
-    // thread t = 32 w + lane is placed by x^(128 t) = x^(128 lane) x^(4096 w)
-    uint32_t x = crc_chunks_from_end(word, nwords, threadIdx.x, kSmallThreads, a.x2n.t[15], T);
+    // thread t = 32 w + lane is placed by x^(128 t) = x^(128 lane) x^(4096 w);
+    // a chunk's four words a word per step (slicing by 4: four independent
+    // table loads per step instead of a chain of sixteen)
+    auto crc_w4 = [&](uint32_t c, uint32_t w) -> uint32_t {
+        c ^= w;
+        return T4[3][c & 0xffu] ^ T4[2][(c >> 8) & 0xffu] ^ T4[1][(c >> 16) & 0xffu] ^ T4[0][c >> 24];
+    };
+    uint32_t x = 0;
+    {
+        const uint64_t nchunks = (nwords + 3) / 4;
+        for (uint64_t r = (nchunks + kSmallThreads - 1) / kSmallThreads; r-- > 0;) {
+            if (x) x = gf2_mulmod_bf(a.x2n.t[15], x);
+            const uint64_t q = r * kSmallThreads + threadIdx.x;
+            if (q < nchunks) {
+                const uint64_t wend = nwords - 4 * q, wbeg = wend > 4 ? wend - 4 : 0;
+                uint32_t c = wbeg == 0 ? 0xffffffffu : 0u;
+                for (uint64_t w = wbeg; w < wend; ++w) c = crc_w4(c, word(w));
+                x ^= c;
+            }
+        }
+    }
+    SMALL_STAMP(11);
     x = gf2_mulmod_bf(s_lpw[lane], x);
 #pragma unroll
     for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
@@ -1637,10 +1677,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_ckpt(SmallArgs a) {
     if (lane == 0) s_x[threadIdx.x >> 5] = gf2_mulmod_bf(a.x2n.wpw[threadIdx.x >> 5], x);
     // the header's first 56 bytes (14 words, in registers) are known already:
     // their CRC register beside the others, a word per step (slicing by 4)
-    auto crc_w4 = [&](uint32_t c, uint32_t w) -> uint32_t {
-        c ^= w;
-        return T4[3][c & 0xffu] ^ T4[2][(c >> 8) & 0xffu] ^ T4[1][(c >> 16) & 0xffu] ^ T4[0][c >> 24];
-    };
     const uint64_t iend = ids_off + 4 * idsw;
     const uint32_t hw0 = 0x4D555243u /* "CRUM" */, hw1 = 1u, hw2 = 0u, hw3 = a.R;
     if (threadIdx.x == 32) {

@@ -1826,8 +1826,8 @@ int enqueue_small(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacity, 
     sa.st_host = c->dh_st;
     sa.x2n = crc_tables().x2n;
     const uint64_t warps = (c->N << (c->small_log2p - kSegLog2)) << kSmallItemsLog2;  // a detect item each
-    uint64_t blocks = (warps + 7) / 8;
-    const uint64_t cap = (uint64_t)c->sms * c->small_bps;
+    uint64_t blocks = (warps + 7) / 8 + 1;  // + CTA 0 (metadata; it detects nothing)
+    const uint64_t cap = (uint64_t)c->sms * c->small_bps;  // co-resident (cooperative launch)
     if (blocks > cap) blocks = cap;
     if (blocks < 2) blocks = 2;  // CTA 0 writes the metadata beside the gathers of the others
     if (blocks > cap) blocks = cap;
