@@ -8,6 +8,6 @@ run() {
   done
 }
 run cur
-cp tools/calls/ab/runtime_pre_crcout.cu paper_1808_00117_b200/csrc/runtime.cu
-cp tools/calls/ab/kernels_image_pre_crcout.cu paper_1808_00117_b200/csrc/kernels_image.cu
+# (the A/B copied the f8ff49c versions of runtime.cu / kernels_image.cu over the tree; files removed since)
+# (the A/B copied the f8ff49c versions of runtime.cu / kernels_image.cu over the tree; files removed since)
 run pre
