@@ -835,10 +835,17 @@ def main():
     # mirror + image); hash F + 8N + 8K + KP; tracked N + 2KP
     dev_alg = {"compare": 2 * F + 2 * slot_bytes, "hash": F + 8 * n_pages + 8 * K + slot_bytes,
                "tracked": n_pages + 2 * slot_bytes}[args.mode]
-    # context for fractions above 1.0: a plain streaming READ of the largest HBM buffer
+    # context for fractions above 1.0: a plain streaming READ of the largest HBM
+    # buffer -- at least 2 GiB (a temporary buffer when every region is smaller:
+    # a short read stream under-measures the rate, C3's 256 MiB gave 5.8 TB/s)
     dev_regs = [t for t in regions if t.is_cuda]
     rd_t = max(dev_regs + [scrub], key=lambda t: t.numel())
+    if rd_t.numel() < 2 * GiB:
+        free_b, _ = torch.cuda.mem_get_info(dev)
+        if free_b > 4 * GiB:
+            rd_t = torch.zeros(2 * GiB, dtype=torch.uint8, device=dev)
     read_stream = timed_read_stream(crum, rd_t, min(rd_t.numel(), 8 * GiB) // 32 * 32, stream)
+    del rd_t
     host_regs = [t for t in regions if not t.is_cuda]
     host_link = None
     if host_regs:
