@@ -1107,6 +1107,13 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused_compare(FusedArgs a) {
             const uint64_t off = off0 + ((uint64_t)sg << kSegLog2);
             const uint64_t len = g.bytes - off;
             const uint8_t *pa = g.base + off, *pb = g.mirror + off;
+            // the next segment's lines into L2 while this one is compared: a
+            // warp walks its tile serially, so one segment of loads in flight
+            // per warp (plus the prefetch) instead of one
+            if (a.prefetch && sg + 1 < nseg && len >= 2 * kSegBytes) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + kSegBytes + lane * 128));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + kSegBytes + lane * 128));
+            }
             uint32_t x = 0;
             if (len >= kSegBytes && g.aligned32) {
                 uint32_t va[4][8], vb[4][8];

@@ -1,0 +1,8 @@
+# single pass with the prefetch heuristic: parity, C2 lines at 1 / 10 / 100 %
+python -c "import __graft_entry__ as g; g.build()"
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_variants.py -q -k "mapped or every_path or full_size or small" 2>&1 | tail -1
+O=gpurun_out/r04d; mkdir -p $O
+for d in 0.01 0.02 0.1 1.0; do
+  timeout 400 python bench.py --config c2 --dirty $d --no-cpu-baseline --no-e2e > $O/c2_$d.json 2> $O/c2_$d.err
+  python -c "import json; d=json.load(open('$O/c2_$d.json')); r=d['roofline']; print('c2 $d', d['value'], d['ms_per_step'], d['step']['frac'], r['kernel'], r['frac'], d['device_phase']['frac'], d['parity']['ok'])"
+done
