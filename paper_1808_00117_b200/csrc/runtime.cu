@@ -810,6 +810,9 @@ constexpr uint64_t kOneRangePayload = 16ull << 20;
 // (stores overlapping the next range's detection), at most it in one range.
 constexpr uint64_t kMappedSerialPayload = 2ull << 20;
 constexpr uint64_t kMappedOneRange = 1ull << 20;
+// (C2, profiles/r02/mapped/fused_32m_ab/: d = 2 % 0.57 ms mapped single pass vs
+// 0.72 ms ring; 5 % 1.17 vs 1.14; 7 % 1.49 vs 1.50)
+constexpr uint64_t kMappedFusedPayload = 32ull << 20;
 
 // Host images whose worst case is at most this (and at most one pipeline
 // chunk) take the zero-copy path.
@@ -2432,9 +2435,14 @@ int crum_checkpoint_gather(crum_ctx *ctx, crum_image *img, void *stream, uint32_
     // ... and where nothing can overflow, mapped stores with no host wait at
     // all (a one-range kernel sequence stores after the detection, so only
     // very small payloads take it; the single pass overlaps the two)
-    if (!deferred && !full && c->gathers_since_rebuild > 0 && c->mapped_cfg && one_range)
+    const bool mapped_ok = !deferred && !full && c->gathers_since_rebuild > 0 && c->mapped_cfg;
+    if (mapped_ok && one_range)
         return gather_mapped(c, s, img, c->fused_ok && prev_payload > kMappedSerialPayload,
                              prev_payload > kMappedOneRange, rep);
+    // the single pass also up to kMappedFusedPayload: its stores overlap the
+    // detection, where the ring pipeline pays a host wait per range
+    if (mapped_ok && c->fused_ok && prev_payload <= kMappedFusedPayload)
+        return gather_mapped(c, s, img, true, false, rep);
     const uint32_t nr = one_range ? 1u : (uint32_t)c->ranges.size();
     auto range_at = [&](uint32_t ci) -> const Range & { return one_range ? c->all : c->ranges[ci]; };
     const uint64_t poff = payload_offset_for(c->regs.size());

@@ -584,8 +584,9 @@ def test_small_path_tracked_and_compare(crum):
 def test_mapped_store_gather(crum, kind, no_mapped):
     """Pinned gathers above the small-footprint size whose previous payload
     was small store straight into the pinned image through its mapped address
-    (CRUM_PATH_MAPPED, previous payload <= 16 MiB: the single-pass kernel
-    above 2 MiB when every region is COMPARE with pages <= 64 KiB, else the
+    (CRUM_PATH_MAPPED, previous payload <= 16 MiB -- 32 MiB in compare-only
+    contexts: the single-pass kernel above 2 MiB when every region is COMPARE
+    with pages <= 64 KiB, else the
     detect -> compact -> gather sequence in halving ranges above 1 MiB, in
     one range below); a larger
     previous payload, the first gather after registration, or
@@ -600,9 +601,9 @@ def test_mapped_store_gather(crum, kind, no_mapped):
     elif kind == "tracked":  # TRACKED regions: the writer marks what it writes
         specs = [(24 * MiB + 4096 + 9, 4 * KiB, T), (16 * MiB, 64 * KiB, C), (8 * MiB, 64 * KiB, T)]
         limit = 16 * MiB
-    else:
+    else:  # compare-only: the single pass takes payloads up to 32 MiB
         specs = [(40 * MiB + 4096 * 3 + 5, 4 * KiB, C), (72 * MiB, 64 * KiB, C), (8 * MiB + 300, 64 * KiB, C)]
-        limit = 16 * MiB
+        limit = 32 * MiB
     p = mkpair(specs, 23, flags=crum.CFG_NO_MAPPED if no_mapped else 0)
     img = p.g.new_image()
     assert img.capacity == p.g.image_required_bytes()

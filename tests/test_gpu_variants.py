@@ -112,11 +112,11 @@ def test_every_path_bit_exact(crum, variant, specs_name):
                           (how != "host" or specs_name == "small") and
                           (variant.startswith("fused") or small or prev_frac >= 0.25))
         # a pinned gather above the small-footprint size (worst case > 16 MiB:
-        # FUSABLE, FUSABLE_BIG) whose previous payload was <= 16 MiB (not the
+        # FUSABLE, FUSABLE_BIG) whose previous payload was <= 32 MiB (not the
         # first since registration) stores through the image's mapped address;
         # the single pass there above 2 MiB (these sets are compare-only)
         mapped = (how == "host" and specs_name in ("fusable", "fusable_big") and not gflags and host_gathers > 0 and
-                  variant != "no_mapped" and prev_payload is not None and prev_payload <= 16 * MiB)
+                  variant != "no_mapped" and prev_payload is not None and prev_payload <= 32 * MiB)
         assert bool(rep["path"] & crum.PATH_MAPPED) == mapped, (variant, epoch, how, rep["path"])
         if mapped:
             fused_eligible = prev_payload > 2 * MiB
