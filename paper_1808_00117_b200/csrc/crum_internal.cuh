@@ -280,7 +280,7 @@ void launch_scatter(const Launch &L, const ScatterArgs &a);
 // (k_gather, no commit), then encode -> chunk scan -> pack.  Restore offsets
 // of encoded units: zblk[u / kZScanBlock] + zloc[u] (bytes from the payload).
 constexpr uint32_t kZScanBlock = 2048;
-constexpr uint32_t kZChunkUnits = 16384;   // at most 64 MiB of units per compressed chunk ...
+constexpr uint32_t kZChunkUnits = 32768;   // at most 128 MiB of units per compressed chunk ...
 constexpr uint32_t kZMinChunkUnits = 4096;  // ... at least 16 MiB (a quarter of the range's units in between)
 // Encode the n units at raw (4 KiB each) into enc (same layout), sizes into zsz[0..n).
 void launch_zenc(const Launch &L, const uint8_t *raw, uint64_t n, uint8_t *enc, uint16_t *zsz, const DevStats *st);

@@ -1996,7 +1996,7 @@ int gather_dev_graph(crum_ctx *c, cudaStream_t s, uint8_t *img, uint64_t capacit
 }
 
 // Compressed gather (readings Z2-Z3).  Chunks of
-// of 16-64 MiB of units (a quarter of a range) run on the gather stream: k_gather of the
+// of 16-128 MiB of units (a quarter of a range) run on the gather stream: k_gather of the
 // chunk's listed pages into a raw staging buffer (no commit), encode, chunk
 // scan of the sizes (running total mirrored into mapped memory), pack.  A
 // pinned image takes a range pipeline like the plain path's, on coarser
@@ -2083,10 +2083,11 @@ int gather_z(crum_ctx *c, cudaStream_t s, uint8_t *dev_img, crum_image *himg, ui
         CK(cudaEventSynchronize(c->ev_range[ci]));
         const uint64_t U0 = c->h_rb[ci].units, U1 = c->h_rb[ci + 1].units;
         if (U1 > U0) CK(cudaStreamWaitEvent(c->gstream, c->ev_range[ci], 0));
-        // chunks of a quarter of the range's units, 16-64 MiB: per-chunk costs
-        // (host wait, kernel drains) amortise over large payloads, small ones
-        // keep a few chunks in flight (C4 HPGMG-like compressed: 16 MiB chunks
-        // 730 GB/s, 32 MiB 794-798, 64 MiB 868; C2 hpgmg 601 / 597-600 / 583)
+        // chunks of a quarter of the range's units, 16-128 MiB: per-chunk costs
+        // (kernel drains, the single-block scan, host wait) amortise over large
+        // payloads, small ones keep a few chunks in flight (C4 HPGMG-like
+        // compressed: 16 MiB chunks 730 GB/s, 32 MiB 794-798, 64 MiB 868,
+        // 128 MiB 908; C2 hpgmg at a fixed 64 MiB 583 vs 601 at 16 MiB)
         const uint64_t cu = std::min<uint64_t>(kZChunkUnits, std::max<uint64_t>(kZMinChunkUnits, (U1 - U0) / 4));
         for (uint64_t u0 = U0; u0 < U1; u0 += cu, ++k) {
             const uint64_t u1 = std::min(U1, u0 + cu), n = u1 - u0;
