@@ -85,6 +85,13 @@ def test_cpu_side_argument_checks(crum):
     assert L.crum_image_numa_node(None, C.byref(node)) == crum.E_INVAL
     assert L.crum_device_numa_node(0, None) == crum.E_INVAL
     assert L.crum_device_numa_node(-1, C.byref(node)) == crum.E_DEVICE
+    # batched synth calls: argument checks happen before any CUDA work
+    assert L.crum_synth_fill_regions(None, 0, 1, None) == crum.OK
+    assert L.crum_synth_fill_regions(None, 2, 1, None) == crum.E_INVAL
+    bad = (crum.SynthRegion * 1)(crum.SynthRegion(0x1003, 64, 0, 0, None, 0))   # unaligned pointer
+    assert L.crum_synth_fill_regions(bad, 1, 1, None) == crum.E_INVAL
+    bad = (crum.SynthRegion * 1)(crum.SynthRegion(0x1000, 64, 12, 0, None, 1))  # page size % 8, no pages
+    assert L.crum_synth_write_regions(bad, 1, 1, 0, 0, None) == crum.E_INVAL
     try:
         import torch
         has_gpu = torch.cuda.is_available()
