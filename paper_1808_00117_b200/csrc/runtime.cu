@@ -804,10 +804,11 @@ int ensure_z(crum_ctx *c, uint64_t units) {
 
 // A pinned gather whose previous payload was at most this runs as one range.
 constexpr uint64_t kOneRangePayload = 16ull << 20;
-// Mapped-store gathers (gather_mapped, previous payload <= kOneRangePayload):
-// above kMappedSerialPayload a compare-only context runs the single pass;
-// otherwise above kMappedOneRange the kernel sequence runs in c->mranges
-// (stores overlapping the next range's detection), at most it in one range.
+// Mapped-store gathers (gather_mapped, previous payload <= kOneRangePayload,
+// or <= kMappedFusedPayload in a compare-only context): above
+// kMappedSerialPayload a compare-only context runs the single pass; otherwise
+// above kMappedOneRange the kernel sequence runs in c->mranges (stores
+// overlapping the next range's detection), at most it in one range.
 constexpr uint64_t kMappedSerialPayload = 2ull << 20;
 constexpr uint64_t kMappedOneRange = 1ull << 20;
 // (C2, profiles/r02/mapped/fused_32m_ab/: d = 2 % 0.57 ms mapped single pass vs
